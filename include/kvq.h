@@ -1,0 +1,184 @@
+/*
+ * kvq.h -- C ABI of the B200-native KVQuant decode hot path (arXiv 2401.18079).
+ *
+ * One handle = one layer's compressed KV cache (per-layer codebooks, PAPER.md P:303,
+ * P:322).  Keys are stored per channel and pre-RoPE, Values
+ * per token, as b-bit codes (b in {2,3,4}) indexing a non-uniform
+ * codebook, with a per-vector dense-and-sparse split of about f = 1%
+ * fp16 outliers kept compressed along the token axis so an append only
+ * touches array tails.  Decode attention runs directly on that cache:
+ * codebook dequantization with the affine fold, RoPE applied on the fly
+ * to the dequantized pre-RoPE Keys, the sparse outlier terms in the
+ * same launch.  See DESIGN.md for the readings of the paper (R1..R22) that
+ * fix every detail the paper leaves open, and for the GPU data layout.
+ *
+ * Conventions for every call:
+ *   - No exception crosses the ABI.  Every call returns a kvq_status; on failure the
+ *     thread-local kvq_last_error() holds a message.
+ *   - Validation runs synchronously before anything is enqueued; a failed call changes
+ *     nothing and leaves outputs untouched.
+ *   - Problems detected on the device (Key-outlier capacity overflow, asynchronous CUDA
+ *     faults) are STICKY: the next call on that cache (or kvq_sync) returns them.
+ *   - "device or host" buffers: the library detects host memory (pinned or pageable)
+ *     with cudaPointerGetAttributes and stages it through device scratch on the call's
+ *     stream (H2D before, D2H after, all stream ordered; pageable host memory makes the
+ *     call synchronous).  Device buffers must live on cfg.device (else KVQ_EDEVICE).
+ *     With KVQ_FLAG_TRUST_DEVICE_PTRS the check is skipped and pointers are assumed
+ *     to be device pointers on cfg.device.
+ *   - Borrowed buffers must stay valid until the stream reaches the call.
+ *   - Threading: one writer per cache (append / prefill); attend calls may run
+ *     concurrently with each other but not with a writer on another stream.  Distinct
+ *     caches are independent.
+ *   - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ */
+#ifndef KVQ_H_
+#define KVQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KVQ_OK = 0,
+    KVQ_EINVAL = 1,     /* bad bits/ppm/codebook/thresholds/argument */
+    KVQ_ESHAPE = 2,     /* unsupported or inconsistent head shape */
+    KVQ_EEMPTY = 3,     /* attend on an empty cache */
+    KVQ_ECAPACITY = 4,  /* token capacity exceeded, or (sticky) Key-outlier capacity */
+    KVQ_EDEVICE = 5,    /* pointer or stream on the wrong device */
+    KVQ_ECUDA = 6       /* CUDA runtime error (sticky when asynchronous) */
+} kvq_status;
+
+typedef struct kvq_cache kvq_cache;
+
+#define KVQ_FLAG_TRUST_DEVICE_PTRS 1u
+
+typedef struct {
+    int32_t n_q_heads;          /* H_q >= 1 */
+    int32_t n_kv_heads;         /* H_kv >= 1, H_q % H_kv == 0 (GQA group G = H_q/H_kv) */
+    int32_t head_dim;           /* d; this build supports d == 128 */
+    int32_t bits;               /* b in {2, 3, 4} */
+    int32_t outlier_ppm;        /* f in parts per million, 0 <= ppm < 500000;
+                                   per-token Value outliers k = ceil(ppm*D/1e6) (R2) */
+    int64_t capacity_tokens;    /* preallocated tokens; the cache never reallocates
+                                   (fixes the copy-on-append of P:686-687) */
+    int64_t k_outlier_capacity; /* Key-outlier records; 0 = auto (2*k + 64 per token) */
+    int64_t pos_base;           /* RoPE position of cached token 0 (sequence shards) */
+    double rope_theta;          /* RoPE base, 10000 for LLaMA/Mistral */
+    int32_t device;             /* CUDA device ordinal */
+    uint32_t flags;             /* KVQ_FLAG_* */
+} kvq_config;
+
+typedef struct {
+    /* Host pointers, copied at creation.  Codebooks: 2^bits fp32, strictly ascending
+     * (encode).  Decode codebooks may differ (Q-Norm; reading R9);
+     * NULL means "same as encode". */
+    const float *key_cb_enc, *key_cb_dec;
+    const float *val_cb_enc, *val_cb_dec;
+    /* Per-channel Key thresholds [D] (offline calibrated).  s_c and z_c
+     * are derived as fp32((hi-lo)/2), fp32((hi+lo)/2) in fp64 (reading R6). */
+    const float *key_lo, *key_hi;
+} kvq_params;
+
+/* Create a layer cache.  Validates: bits, ppm, D = H_kv*d, d == 128, H_q % H_kv,
+ * strictly ascending finite codebooks, finite lo <= hi, k < D, capacity > 0.
+ * Allocates every device buffer up front.  Returns KVQ_EINVAL / KVQ_ESHAPE /
+ * KVQ_ECUDA (allocation) on failure with *out untouched. */
+kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *params, kvq_cache **out);
+
+/* Free every device buffer.  NULL is a no-op. */
+void kvq_cache_destroy(kvq_cache *cache);
+
+/* Quantize-on-append of one decode token.
+ * k_prerope_f16: [D] fp16 pre-RoPE Key;  v_f16: [D] fp16 Value (device or host).
+ * Keys: outlier iff x < lo_c or x > hi_c; code = ENC(clamp(x)) (R4, R5, R8).
+ * Values: two-sided top-k split with ties to the lower index (R2, R3), (s,z) from
+ * the kept range, code = ENC(clamp(v)).  Codes, outliers, (s,z) are appended at the
+ * tails.  KVQ_ECAPACITY when the token capacity is full. */
+kvq_status kvq_append(kvq_cache *cache, const void *k_prerope_f16, const void *v_f16,
+                      void *stream);
+
+/* Block quantization of T prompt tokens (a9; "future work" in the paper).
+ * K_f16, V_f16: [T][D] fp16, row major.  Result is identical to T kvq_append calls. */
+kvq_status kvq_prefill_quantize(kvq_cache *cache, const void *K_f16, const void *V_f16,
+                                int64_t T, void *stream);
+
+/* Single-token decode attention over all cached tokens (a1-a7):
+ *   o_g = softmax_n( RoPE(q_g,pos) . RoPE(K^_{n,h(g)}, pos_base+n) / sqrt(d) ) V^_{n,h(g)}
+ * q_f16: [H_q][d] fp16 PRE-RoPE queries; o: [H_q][d] fp32.  One fused launch (query
+ * prologue + split-T tile loop + split merge).  KVQ_EEMPTY on an empty cache. */
+kvq_status kvq_decode_attend(kvq_cache *cache, const void *q_f16, int64_t pos, float *o,
+                             void *stream);
+
+/* Same as kvq_decode_attend but returns this cache's un-normalized partial
+ *   part: [H_q][d+2] fp32 = (sum_n p_n V^_n [d], m, l)
+ * with p_n = 2^(s'_n - m), s'_n the score in log2 units (s_n * log2 e), l = sum p_n.
+ * An empty cache yields (0, -inf, 0).  Used for sequence sharding. */
+kvq_status kvq_decode_attend_partial(kvq_cache *cache, const void *q_f16, int64_t pos,
+                                     float *part, void *stream);
+
+/* Exact log-sum-exp merge of P partials (fixed order 0..P-1):
+ *   parts: [P][H_q][d+2] fp32 (device or host); o: [H_q][d] fp32.
+ * device: the CUDA device to run on. */
+kvq_status kvq_merge_partials(const float *parts, int32_t P, int32_t H_q, int32_t d,
+                              float *o, int32_t device, void *stream);
+
+/* Number of cached tokens (host shadow; no sync). */
+int64_t kvq_num_tokens(const kvq_cache *cache);
+
+/* Drop every cached token (capacity kept).  Stream ordered after prior work on
+ * `stream`. */
+kvq_status kvq_reset(kvq_cache *cache, void *stream);
+
+/* Synchronize the cache's device and surface sticky errors. */
+kvq_status kvq_sync(kvq_cache *cache);
+
+/* Canonical export of tokens [t0, t1) (synchronizes).  Host buffers, caller owned:
+ *   kcodes, vcodes : uint8 [t1-t0][D]        (codes in channel order)
+ *   kptr           : int64 [t1-t0+1]         (absolute CSC offsets into the Key
+ *                                             outlier array; kptr[0] = start)
+ *   kidx, kval     : uint16 [kptr[last]-kptr[0]]  channel, fp16 bits
+ *   vidx, vval     : uint16 [t1-t0][k]       channel (ascending), fp16 bits
+ *   vs, vz         : float  [t1-t0]
+ * Any pointer may be NULL to skip that array (kidx/kval need kptr).  Use
+ * kvq_key_outlier_span first to size kidx/kval. */
+typedef struct {
+    uint8_t *kcodes;
+    int64_t *kptr;
+    uint16_t *kidx, *kval;
+    uint8_t *vcodes;
+    uint16_t *vidx, *vval;
+    float *vs, *vz;
+} kvq_export_buf;
+
+kvq_status kvq_key_outlier_span(kvq_cache *cache, int64_t t0, int64_t t1, int64_t *begin,
+                                int64_t *end);
+kvq_status kvq_export(kvq_cache *cache, int64_t t0, int64_t t1, kvq_export_buf *buf);
+
+/* Introspection for benchmarks and tests. */
+typedef struct {
+    int32_t heads_per_cta;      /* query heads per attend CTA (HG) */
+    int32_t splits;             /* token splits per head group of the last attend */
+    int32_t value_outliers;     /* k per token */
+    int32_t words_per_token;    /* packed 32-bit code words per token per K or V */
+    int64_t capacity_tokens;
+    int64_t k_outlier_capacity;
+    int64_t device_bytes;       /* bytes of device memory owned */
+} kvq_info;
+kvq_status kvq_get_info(const kvq_cache *cache, kvq_info *info);
+
+/* Force the number of token splits per head group for attend (0 = auto). */
+kvq_status kvq_set_splits(kvq_cache *cache, int32_t splits);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char *kvq_last_error(void);
+
+/* Library version (major*10000 + minor*100 + patch). */
+int32_t kvq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVQ_H_ */

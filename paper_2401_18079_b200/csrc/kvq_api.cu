@@ -1,0 +1,477 @@
+// kvq_api.cu -- C ABI of libkvq: validation, the cache object, staging, export.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/kvq.h"
+#include "kvq_internal.cuh"
+
+using namespace kvq;
+
+struct kvq_cache {
+    kvq_config cfg;
+    DevCache dc;
+    int64_t T = 0;             // host shadow of the token count
+    int hg = 0;                // query heads per attend CTA
+    int splits_forced = 0;
+    int last_splits = 0;
+    float *parts = nullptr;    // [max_splits][H_q][d+2]
+    int max_splits = 0;
+    unsigned *tickets = nullptr;
+    int *err_host = nullptr;   // host-mapped sticky error word
+    void *stage = nullptr;     // device staging for host buffers
+    size_t stage_bytes = 0;
+    int64_t device_bytes = 0;
+    std::vector<void *> allocs;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+kvq_status fail(kvq_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+kvq_status fail(kvq_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+kvq_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(KVQ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(expr)                                                     \
+    do {                                                             \
+        cudaError_t e__ = (expr);                                    \
+        if (e__ != cudaSuccess) return cuda_fail(e__, #expr);        \
+    } while (0)
+
+bool finite_f(float x) { return std::isfinite(x); }
+
+kvq_status check_sticky(kvq_cache *c) {
+    if (c->err_host && *(volatile int *)c->err_host) {
+        int e = *(volatile int *)c->err_host;
+        if (e & kErrKeyCapacity)
+            return fail(KVQ_ECAPACITY, "key-outlier capacity (%lld records) exceeded on device",
+                        (long long)c->dc.kcap);
+        return fail(KVQ_ECUDA, "sticky device error %d", e);
+    }
+    return KVQ_OK;
+}
+
+template <typename T>
+kvq_status dev_alloc(kvq_cache *c, T **p, size_t bytes) {
+    void *q = nullptr;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(&q, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    e = cudaMemset(q, 0, bytes);
+    if (e != cudaSuccess) { cudaFree(q); return cuda_fail(e, "cudaMemset"); }
+    c->allocs.push_back(q);
+    c->device_bytes += (int64_t)bytes;
+    *p = reinterpret_cast<T *>(q);
+    return KVQ_OK;
+}
+
+// Classify a user pointer: 0 = device on `dev`, 1 = host, -1 = device elsewhere.
+int classify(const void *p, int dev, uint32_t flags) {
+    if (flags & KVQ_FLAG_TRUST_DEVICE_PTRS) return 0;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) { cudaGetLastError(); return 1; }
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged)
+        return at.device == dev ? 0 : -1;
+    return 1;
+}
+
+kvq_status ensure_stage(kvq_cache *c, size_t bytes) {
+    if (c->stage_bytes >= bytes) return KVQ_OK;
+    if (c->stage) { cudaFree(c->stage); c->device_bytes -= (int64_t)c->stage_bytes; c->stage = nullptr; }
+    void *p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    c->stage = p;
+    c->stage_bytes = bytes;
+    c->device_bytes += (int64_t)bytes;
+    return KVQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t kvq_version(void) { return 100; }
+
+const char *kvq_last_error(void) { return g_last_error.c_str(); }
+
+kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_cache **out) {
+    if (!cfg || !prm || !out) return fail(KVQ_EINVAL, "null argument");
+    const kvq_config &C = *cfg;
+    if (C.bits < 2 || C.bits > 4) return fail(KVQ_EINVAL, "bits must be 2, 3 or 4 (got %d)", C.bits);
+    if (C.outlier_ppm < 0 || C.outlier_ppm >= 500000)
+        return fail(KVQ_EINVAL, "outlier_ppm must be in [0, 500000) (got %d)", C.outlier_ppm);
+    if (C.n_q_heads < 1 || C.n_kv_heads < 1) return fail(KVQ_ESHAPE, "head counts must be >= 1");
+    if (C.n_q_heads % C.n_kv_heads) return fail(KVQ_ESHAPE, "n_q_heads %% n_kv_heads != 0");
+    if (C.head_dim != kHeadDim) return fail(KVQ_ESHAPE, "this build supports head_dim == 128 (got %d)", C.head_dim);
+    const int G = C.n_q_heads / C.n_kv_heads;
+    if (G != 1 && G != 2 && G != 4 && G != 8) return fail(KVQ_ESHAPE, "GQA group must be 1, 2, 4 or 8");
+    const int64_t D = (int64_t)C.n_kv_heads * C.head_dim;
+    if (D > 65535) return fail(KVQ_ESHAPE, "D = H_kv*d must fit a 16-bit channel index");
+    if (C.capacity_tokens < 1) return fail(KVQ_EINVAL, "capacity_tokens must be >= 1");
+    if (!(C.rope_theta > 0) || !std::isfinite(C.rope_theta)) return fail(KVQ_EINVAL, "rope_theta must be > 0");
+    if (C.pos_base < 0) return fail(KVQ_EINVAL, "pos_base must be >= 0");
+    const int hg = attend_heads_per_cta(C.bits, C.n_q_heads, G);
+    if (hg == 0) return fail(KVQ_ESHAPE, "no attend tiling for bits=%d H_q=%d G=%d", C.bits, C.n_q_heads, G);
+    const int64_t kv = ((int64_t)C.outlier_ppm * D + 999999) / 1000000;
+    if (kv >= D) return fail(KVQ_EINVAL, "value outliers per token (%lld) must be < D", (long long)kv);
+    const int nlev = 1 << C.bits;
+    const float *cbs[4] = {prm->key_cb_enc, prm->key_cb_dec ? prm->key_cb_dec : prm->key_cb_enc,
+                           prm->val_cb_enc, prm->val_cb_dec ? prm->val_cb_dec : prm->val_cb_enc};
+    for (int k = 0; k < 4; ++k) {
+        if (!cbs[k]) return fail(KVQ_EINVAL, "codebook %d is NULL", k);
+        for (int j = 0; j < nlev; ++j) {
+            if (!finite_f(cbs[k][j])) return fail(KVQ_EINVAL, "codebook %d has a non-finite entry", k);
+            if ((k == 0 || k == 2) && j > 0 && !(cbs[k][j] > cbs[k][j - 1]))
+                return fail(KVQ_EINVAL, "encode codebook %d is not strictly ascending", k);
+        }
+    }
+    if (!prm->key_lo || !prm->key_hi) return fail(KVQ_EINVAL, "key thresholds are NULL");
+    for (int64_t ch = 0; ch < D; ++ch) {
+        float lo = prm->key_lo[ch], hi = prm->key_hi[ch];
+        if (!finite_f(lo) || !finite_f(hi) || lo > hi)
+            return fail(KVQ_EINVAL, "key thresholds of channel %lld invalid", (long long)ch);
+    }
+
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (C.device < 0 || C.device >= ndev) return fail(KVQ_EDEVICE, "device %d not present", C.device);
+    CK(cudaSetDevice(C.device));
+
+    kvq_cache *c = new (std::nothrow) kvq_cache();
+    if (!c) return fail(KVQ_EINVAL, "out of host memory");
+    c->cfg = C;
+    c->hg = hg;
+    DevCache &d = c->dc;
+    d.H_q = C.n_q_heads; d.H_kv = C.n_kv_heads; d.d = C.head_dim; d.D = (int)D;
+    d.bits = C.bits; d.nlev = nlev; d.kv = (int)kv; d.G = G;
+    d.QW = C.n_kv_heads * 4 * C.bits;
+    d.VW = (int)(D * C.bits / 32);
+    d.cap = (C.capacity_tokens + 31) / 32 * 32;
+    // default Key-outlier headroom: 2*ceil(f*D) per token (at least 8) + slack (R21)
+    d.kcap = C.k_outlier_capacity > 0 ? C.k_outlier_capacity
+                                      : d.cap * (2 * kv > 8 ? 2 * kv : 8) + 4096;
+    if (d.kcap > 0xFFFFFFF0LL) d.kcap = 0xFFFFFFF0LL;
+    d.pos_base = C.pos_base;
+    d.theta = C.rope_theta;
+
+    kvq_status st = KVQ_OK;
+    auto A = [&](auto **p, size_t bytes) { if (st == KVQ_OK) st = dev_alloc(c, p, bytes); };
+    A(&d.kcodes, (size_t)(d.cap / 32) * d.QW * 32 * 4);
+    A(&d.vcodes, (size_t)d.cap * d.VW * 4 + 16);
+    A(&d.vsz, (size_t)d.cap * sizeof(float2));
+    A(&d.vout, (size_t)d.cap * (kv > 0 ? kv : 1) * 4);
+    A(&d.kptr, (size_t)(d.cap + 1) * 4);
+    A(&d.kout, (size_t)d.kcap * 4 + 16);
+    A(&d.kpar, (size_t)4 * D * 4);
+    A(&d.cb, 64 * 4);
+    A(&d.mids, 32 * 8);
+    A(&d.counts, (size_t)d.cap * 4);
+    c->max_splits = 4 * 148;
+    A(&c->parts, (size_t)c->max_splits * d.H_q * (kHeadDim + 2) * 4);
+    A(&c->tickets, 64 * 4);
+    if (st != KVQ_OK) { kvq_cache_destroy(c); return st; }
+    {
+        cudaError_t e = cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped);
+        if (e != cudaSuccess) { kvq_cache_destroy(c); return cuda_fail(e, "cudaHostAlloc"); }
+        memset(c->err_host, 0, 64);
+        e = cudaHostGetDevicePointer((void **)&d.err, c->err_host, 0);
+        if (e != cudaSuccess) { kvq_cache_destroy(c); return cuda_fail(e, "cudaHostGetDevicePointer"); }
+    }
+    // per-channel Key params: s = fp32((hi-lo)/2), z = fp32((hi+lo)/2) in fp64 (R6)
+    std::vector<float> kpar(4 * D);
+    for (int64_t ch = 0; ch < D; ++ch) {
+        const double lo = prm->key_lo[ch], hi = prm->key_hi[ch];
+        kpar[ch] = (float)((hi - lo) / 2.0);
+        kpar[D + ch] = (float)((hi + lo) / 2.0);
+        kpar[2 * D + ch] = prm->key_lo[ch];
+        kpar[3 * D + ch] = prm->key_hi[ch];
+    }
+    float cb[64] = {0};
+    double mids[32] = {0};
+    for (int k = 0; k < 4; ++k)
+        for (int j = 0; j < nlev; ++j) cb[16 * k + j] = cbs[k][j];
+    for (int j = 0; j + 1 < nlev; ++j) {
+        mids[j] = (double)cbs[0][j] + (double)cbs[0][j + 1];
+        mids[16 + j] = (double)cbs[2][j] + (double)cbs[2][j + 1];
+    }
+    cudaError_t e = cudaMemcpy(d.kpar, kpar.data(), kpar.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d.cb, cb, sizeof cb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d.mids, mids, sizeof mids, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { kvq_cache_destroy(c); return cuda_fail(e, "upload parameters"); }
+    *out = c;
+    return KVQ_OK;
+}
+
+void kvq_cache_destroy(kvq_cache *c) {
+    if (!c) return;
+    cudaSetDevice(c->cfg.device);
+    cudaDeviceSynchronize();
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->stage) cudaFree(c->stage);
+    if (c->err_host) cudaFreeHost(c->err_host);
+    delete c;
+}
+
+int64_t kvq_num_tokens(const kvq_cache *c) { return c ? c->T : 0; }
+
+kvq_status kvq_get_info(const kvq_cache *c, kvq_info *info) {
+    if (!c || !info) return fail(KVQ_EINVAL, "null argument");
+    info->heads_per_cta = c->hg;
+    info->splits = c->last_splits;
+    info->value_outliers = c->dc.kv;
+    info->words_per_token = c->dc.VW;
+    info->capacity_tokens = c->dc.cap;
+    info->k_outlier_capacity = c->dc.kcap;
+    info->device_bytes = c->device_bytes;
+    return KVQ_OK;
+}
+
+kvq_status kvq_set_splits(kvq_cache *c, int32_t splits) {
+    if (!c) return fail(KVQ_EINVAL, "null cache");
+    if (splits < 0 || splits > c->max_splits) return fail(KVQ_EINVAL, "splits out of range [0, %d]", c->max_splits);
+    c->splits_forced = splits;
+    return KVQ_OK;
+}
+
+kvq_status kvq_sync(kvq_cache *c) {
+    if (!c) return fail(KVQ_EINVAL, "null cache");
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaDeviceSynchronize());
+    return check_sticky(c);
+}
+
+kvq_status kvq_reset(kvq_cache *c, void *stream) {
+    if (!c) return fail(KVQ_EINVAL, "null cache");
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaMemsetAsync(c->dc.kptr, 0, 4, (cudaStream_t)stream));
+    c->T = 0;
+    return KVQ_OK;
+}
+
+static kvq_status append_tokens(kvq_cache *c, const void *K, const void *V, int64_t T, void *stream) {
+    if (!c) return fail(KVQ_EINVAL, "null cache");
+    if (T < 0) return fail(KVQ_EINVAL, "negative token count");
+    if (T == 0) return KVQ_OK;
+    if (!K || !V) return fail(KVQ_EINVAL, "null K or V");
+    kvq_status st = check_sticky(c);
+    if (st != KVQ_OK) return st;
+    if (c->T + T > c->cfg.capacity_tokens)
+        return fail(KVQ_ECAPACITY, "token capacity %lld exceeded (have %lld, adding %lld)",
+                    (long long)c->cfg.capacity_tokens, (long long)c->T, (long long)T);
+    CK(cudaSetDevice(c->cfg.device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)T * c->dc.D * 2;
+    const int ck = classify(K, c->cfg.device, c->cfg.flags), cv = classify(V, c->cfg.device, c->cfg.flags);
+    if (ck < 0 || cv < 0) return fail(KVQ_EDEVICE, "K/V device pointer is not on device %d", c->cfg.device);
+    const __half *Kd = (const __half *)K, *Vd = (const __half *)V;
+    if (ck == 1 || cv == 1) {
+        st = ensure_stage(c, 2 * bytes);
+        if (st != KVQ_OK) return st;
+        char *sb = (char *)c->stage;
+        if (ck == 1) { CK(cudaMemcpyAsync(sb, K, bytes, cudaMemcpyHostToDevice, s)); Kd = (const __half *)sb; }
+        if (cv == 1) { CK(cudaMemcpyAsync(sb + bytes, V, bytes, cudaMemcpyHostToDevice, s)); Vd = (const __half *)(sb + bytes); }
+    }
+    cudaError_t e = launch_quantize(c->dc, Kd, Vd, c->T, T, s);
+    if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
+    c->T += T;
+    return KVQ_OK;
+}
+
+kvq_status kvq_append(kvq_cache *c, const void *k, const void *v, void *stream) {
+    return append_tokens(c, k, v, 1, stream);
+}
+
+kvq_status kvq_prefill_quantize(kvq_cache *c, const void *K, const void *V, int64_t T, void *stream) {
+    return append_tokens(c, K, V, T, stream);
+}
+
+static kvq_status attend_impl(kvq_cache *c, const void *q, int64_t pos, float *out, int partial,
+                              void *stream) {
+    if (!c) return fail(KVQ_EINVAL, "null cache");
+    if (!q || !out) return fail(KVQ_EINVAL, "null q or output");
+    if (pos < 0) return fail(KVQ_EINVAL, "negative position");
+    kvq_status st = check_sticky(c);
+    if (st != KVQ_OK) return st;
+    CK(cudaSetDevice(c->cfg.device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int H = c->dc.H_q;
+    const size_t qbytes = (size_t)H * kHeadDim * 2;
+    const size_t obytes = (size_t)H * (kHeadDim + (partial ? 2 : 0)) * 4;
+    if (c->T == 0) {
+        if (!partial) return fail(KVQ_EEMPTY, "attend on an empty cache");
+        // empty partial: (0, -inf, 0)
+        std::vector<float> h((size_t)H * (kHeadDim + 2), 0.f);
+        for (int g = 0; g < H; ++g) h[(size_t)g * (kHeadDim + 2) + kHeadDim] = -INFINITY;
+        const int co = classify(out, c->cfg.device, c->cfg.flags);
+        if (co < 0) return fail(KVQ_EDEVICE, "output pointer not on device %d", c->cfg.device);
+        if (co == 1) { memcpy(out, h.data(), obytes); return KVQ_OK; }
+        CK(cudaMemcpyAsync(out, h.data(), obytes, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        return KVQ_OK;
+    }
+    const int cq = classify(q, c->cfg.device, c->cfg.flags), co = classify(out, c->cfg.device, c->cfg.flags);
+    if (cq < 0 || co < 0) return fail(KVQ_EDEVICE, "q/output pointer not on device %d", c->cfg.device);
+    const __half *qd = (const __half *)q;
+    float *od = out;
+    if (cq == 1 || co == 1) {
+        st = ensure_stage(c, qbytes + obytes + 256);
+        if (st != KVQ_OK) return st;
+        char *sb = (char *)c->stage;
+        if (cq == 1) { CK(cudaMemcpyAsync(sb, q, qbytes, cudaMemcpyHostToDevice, s)); qd = (const __half *)sb; }
+        if (co == 1) od = (float *)(sb + ((qbytes + 255) / 256) * 256);
+    }
+    AttendArgs a;
+    a.q = qd; a.pos = pos; a.T = c->T; a.out = od; a.write_partial = partial;
+    a.parts = c->parts; a.tickets = c->tickets; a.splits = c->splits_forced;
+    cudaError_t e = launch_attend(c->dc, a, &c->last_splits, s);
+    if (e != cudaSuccess) return cuda_fail(e, "attend launch");
+    if (co == 1) {
+        CK(cudaMemcpyAsync(out, od, obytes, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    return KVQ_OK;
+}
+
+kvq_status kvq_decode_attend(kvq_cache *c, const void *q, int64_t pos, float *o, void *stream) {
+    return attend_impl(c, q, pos, o, 0, stream);
+}
+
+kvq_status kvq_decode_attend_partial(kvq_cache *c, const void *q, int64_t pos, float *part, void *stream) {
+    return attend_impl(c, q, pos, part, 1, stream);
+}
+
+kvq_status kvq_merge_partials(const float *parts, int32_t P, int32_t H, int32_t d, float *o,
+                              int32_t device, void *stream) {
+    if (!parts || !o) return fail(KVQ_EINVAL, "null argument");
+    if (P < 1 || H < 1 || d < 1) return fail(KVQ_EINVAL, "P, H_q, d must be >= 1");
+    CK(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int cp = classify(parts, device, 0), co = classify(o, device, 0);
+    if (cp < 0 || co < 0) return fail(KVQ_EDEVICE, "pointer not on device %d", device);
+    const size_t pb = (size_t)P * H * (d + 2) * 4, ob = (size_t)H * d * 4;
+    const float *pd = parts;
+    float *od = o;
+    void *tmp = nullptr;
+    if (cp == 1 || co == 1) {
+        CK(cudaMallocAsync(&tmp, pb + ob, s));
+        if (cp == 1) { CK(cudaMemcpyAsync(tmp, parts, pb, cudaMemcpyHostToDevice, s)); pd = (const float *)tmp; }
+        if (co == 1) od = (float *)((char *)tmp + pb);
+    }
+    cudaError_t e = launch_merge(pd, P, H, d, od, s);
+    if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+    if (co == 1) { CK(cudaMemcpyAsync(o, od, ob, cudaMemcpyDeviceToHost, s)); }
+    if (tmp) { CK(cudaFreeAsync(tmp, s)); }
+    if (co == 1) CK(cudaStreamSynchronize(s));
+    return KVQ_OK;
+}
+
+kvq_status kvq_key_outlier_span(kvq_cache *c, int64_t t0, int64_t t1, int64_t *begin, int64_t *end) {
+    if (!c || !begin || !end) return fail(KVQ_EINVAL, "null argument");
+    if (t0 < 0 || t1 < t0 || t1 > c->T) return fail(KVQ_EINVAL, "bad token range");
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaDeviceSynchronize());
+    uint32_t a = 0, b = 0;
+    CK(cudaMemcpy(&a, c->dc.kptr + t0, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&b, c->dc.kptr + t1, 4, cudaMemcpyDeviceToHost));
+    *begin = a;
+    *end = b;
+    return check_sticky(c);
+}
+
+kvq_status kvq_export(kvq_cache *c, int64_t t0, int64_t t1, kvq_export_buf *buf) {
+    if (!c || !buf) return fail(KVQ_EINVAL, "null argument");
+    if (t0 < 0 || t1 < t0 || t1 > c->T) return fail(KVQ_EINVAL, "bad token range");
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaDeviceSynchronize());
+    kvq_status st = check_sticky(c);
+    if (st != KVQ_OK) return st;
+    const DevCache &d = c->dc;
+    const int64_t n = t1 - t0;
+    const int b = d.bits, D = d.D;
+    if (n == 0) { if (buf->kptr) { uint32_t a; CK(cudaMemcpy(&a, d.kptr + t0, 4, cudaMemcpyDeviceToHost)); buf->kptr[0] = a; } return KVQ_OK; }
+    if (buf->kcodes) {
+        const int64_t tile0 = t0 / 32, tile1 = (t1 + 31) / 32;
+        std::vector<uint32_t> kc((size_t)(tile1 - tile0) * d.QW * 32);
+        CK(cudaMemcpy(kc.data(), d.kcodes + tile0 * d.QW * 32, kc.size() * 4, cudaMemcpyDeviceToHost));
+        for (int64_t t = t0; t < t1; ++t) {
+            const int64_t tl = t / 32 - tile0;
+            const int j = (int)(t % 32);
+            uint8_t *row = buf->kcodes + (t - t0) * D;
+            for (int h = 0; h < d.H_kv; ++h) {
+                for (int p = 0; p < kPairs; ++p) {
+                    const int bit = 2 * b * p;
+                    const int q = h * 4 * b + bit / 32;
+                    uint64_t w = kc[((size_t)tl * d.QW + q) * 32 + j];
+                    if (bit % 32 + 2 * b > 32) w |= (uint64_t)kc[((size_t)tl * d.QW + q + 1) * 32 + j] << 32;
+                    const unsigned pc = (unsigned)(w >> (bit % 32)) & ((1u << (2 * b)) - 1);
+                    row[h * kHeadDim + p] = (uint8_t)(pc & ((1u << b) - 1));
+                    row[h * kHeadDim + p + kPairs] = (uint8_t)(pc >> b);
+                }
+            }
+        }
+    }
+    if (buf->vcodes) {
+        std::vector<uint32_t> vc((size_t)n * d.VW + 1);
+        CK(cudaMemcpy(vc.data(), d.vcodes + t0 * d.VW, (size_t)n * d.VW * 4, cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < n; ++t)
+            for (int ch = 0; ch < D; ++ch) {
+                const int64_t bit = (int64_t)b * ch;
+                uint64_t w = vc[t * d.VW + bit / 32];
+                if (bit % 32 + b > 32) w |= (uint64_t)vc[t * d.VW + bit / 32 + 1] << 32;
+                buf->vcodes[t * D + ch] = (uint8_t)((w >> (bit % 32)) & ((1u << b) - 1));
+            }
+    }
+    if (buf->vs || buf->vz) {
+        std::vector<float2> sz((size_t)n);
+        CK(cudaMemcpy(sz.data(), d.vsz + t0, (size_t)n * sizeof(float2), cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < n; ++t) {
+            if (buf->vs) buf->vs[t] = sz[t].x;
+            if (buf->vz) buf->vz[t] = sz[t].y;
+        }
+    }
+    if ((buf->vidx || buf->vval) && d.kv > 0) {
+        std::vector<uint32_t> vo((size_t)n * d.kv);
+        CK(cudaMemcpy(vo.data(), d.vout + t0 * d.kv, vo.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t r = 0; r < vo.size(); ++r) {
+            if (buf->vidx) buf->vidx[r] = (uint16_t)(vo[r] & 0xffffu);
+            if (buf->vval) buf->vval[r] = (uint16_t)(vo[r] >> 16);
+        }
+    }
+    if (buf->kptr) {
+        std::vector<uint32_t> kp((size_t)n + 1);
+        CK(cudaMemcpy(kp.data(), d.kptr + t0, kp.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t r = 0; r < kp.size(); ++r) buf->kptr[r] = kp[r];
+        if (buf->kidx || buf->kval) {
+            const int64_t nnz = (int64_t)kp[n] - kp[0];
+            if (nnz > 0) {
+                std::vector<uint32_t> ko((size_t)nnz);
+                CK(cudaMemcpy(ko.data(), d.kout + kp[0], ko.size() * 4, cudaMemcpyDeviceToHost));
+                for (size_t r = 0; r < ko.size(); ++r) {
+                    if (buf->kidx) buf->kidx[r] = (uint16_t)(ko[r] & 0xffffu);
+                    if (buf->kval) buf->kval[r] = (uint16_t)(ko[r] >> 16);
+                }
+            }
+        }
+    }
+    return KVQ_OK;
+}
+
+}  // extern "C"

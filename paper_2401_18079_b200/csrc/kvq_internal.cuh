@@ -1,0 +1,72 @@
+// kvq_internal.cuh -- device data layout and launch interfaces of libkvq (sm_100a).
+//
+// GPU layout of one layer cache:
+//
+//   kcodes  u32 [ntiles][QW][32]      Key codes, token tiles of 32 tokens.  For token
+//           n = 32*t + j and KV head h, the head's pair stream (64 pairs, pair p packs
+//           code(h, p) | code(h, p+64) << b in 2b bits at bit offset 2b*p, RoPE partners
+//           adjacent) occupies words q = h*4b .. h*4b+4b-1, stored at [t][q][j] so a
+//           warp with lane = token reads 128 contiguous bytes per word slot.
+//   vcodes  u32 [cap][VW]             Value codes: the canonical little-endian bitstream
+//           of the token (code c at bit b*c), VW = D*b/32 words per token.
+//   vsz     float2 [cap]              per-token Value (s_n, z_n), fp32 (reading R6).
+//   vout    u32 [cap][kv]             Value outliers, exactly kv = ceil(f*D) per token
+//           (implicit CSR row pointer n*kv), ascending channel; record =
+//           channel | fp16(value) << 16  (16-bit index + 16-bit value).
+//   kptr    u32 [cap+1]               Key-outlier CSC column pointers (32-bit per token,
+//           P:1151), kout u32 [kcap] records as above.
+//   kpar    float [4][D]              s_c, z_c, lo_c, hi_c of the Keys.
+//   cb      float [4][16]             Key enc, Key dec, Value enc, Value dec codebooks.
+//   mids    double [2][16]            encode midpoints c_j + c_{j+1} (fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace kvq {
+
+constexpr int kTileTokens = 32;
+constexpr int kHeadDim = 128;
+constexpr int kPairs = kHeadDim / 2;
+
+struct DevCache {
+    int H_q, H_kv, d, D, bits, nlev, kv;   // kv = value outliers per token
+    int G;                                 // GQA group size
+    int QW;                                // Key words per token (= H_kv * 4b)
+    int VW;                                // Value words per token (= D*b/32)
+    int64_t cap, kcap, pos_base;
+    double theta;
+    uint32_t *kcodes, *vcodes, *vout, *kptr, *kout;
+    float2 *vsz;
+    float *kpar;    // [4][D]
+    float *cb;      // [4][16]
+    double *mids;   // [2][16]
+    int *err;       // device view of the sticky error word (host mapped)
+    int *counts;    // prefill scratch [cap]
+};
+
+enum ErrBits { kErrKeyCapacity = 1 };
+
+// ---- quantization (kvq_quant.cu) ----
+cudaError_t launch_quantize(const DevCache &c, const __half *K, const __half *V, int64_t n0,
+                            int64_t T, cudaStream_t s);
+
+// ---- attention (kvq_attend.cu) ----
+struct AttendArgs {
+    const __half *q;
+    int64_t pos;
+    int64_t T;
+    float *out;          // o [H_q][d] or merged partial [H_q][d+2]
+    int write_partial;   // 0: normalized o; 1: partial
+    float *parts;        // scratch [splits][H_q][d+2]
+    unsigned *tickets;   // [n_head_groups], zero between launches
+    int splits;          // 0 = auto
+};
+int attend_heads_per_cta(int bits, int H_q, int G);
+int attend_auto_splits(const DevCache &c, int64_t T, int hg);
+cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_used,
+                          cudaStream_t s);
+cudaError_t launch_merge(const float *parts, int P, int H, int d, float *o, cudaStream_t s);
+size_t attend_smem_bytes(int bits, int hg);
+
+}  // namespace kvq

@@ -1,0 +1,389 @@
+// kvq_quant.cu -- QZ: quantize-on-append (decode) and block prefill quantization.
+//
+// One CTA per token (256 threads).  Per token:
+//   Keys: outlier iff x < lo_c || x > hi_c (R4); code =
+//         ENC(clamp(x); s_c, z_c) (R5, R8); outliers appended to the CSC tail in
+//         ascending channel order.
+//   Values (topk P:1028-1031): two-sided top-k with
+//         k = ceil(f*D): ceil(k/2) largest then floor(k/2) smallest of the rest,
+//         ties to the lower index, -0 == +0 (R2, R3), done as a CTA radix select on
+//         order-preserving 16-bit keys; (s, z) from the kept [lo, hi] in fp64 rounded
+//         once to fp32 (R6, R7); code = ENC(clamp(v)).
+//   ENC: code = #{j : 2(y - z) > s (c_j + c_{j+1})} in fp64 with explicit round-to-
+//         nearest intrinsics (no contraction), evaluated as a binary search since the
+//         predicate is monotone in j for an ascending codebook (R8).  Taking this
+//         integer decision in fp64 on both sides is what makes codes bit-exact.
+//   Packing: Key tile layout / Value canonical rows (kvq_internal.cuh).
+// Modes: 0 = single decode append (count, CTA scan, tail append, kptr[n+1]);
+//        1 = prefill pass 1 (Key-outlier counts only);
+//        2 = prefill pass 3 (everything, Key-outlier base from the scanned kptr).
+#include "kvq_internal.cuh"
+
+namespace kvq {
+namespace {
+
+constexpr int QZ_THREADS = 256;
+constexpr int QZ_WARPS = QZ_THREADS / 32;
+
+__device__ __forceinline__ uint16_t f16_order_key(uint16_t h) {
+    if (h == 0x8000u) h = 0;                         // -0 == +0 (R3)
+    return (h & 0x8000u) ? (uint16_t)(~h) : (uint16_t)(h | 0x8000u);
+}
+
+__device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+
+// Exact ENC (R8): count of midpoints with 2(y-z) > s*m_j.
+template <int NM>
+__device__ __forceinline__ int enc_fp64(double y, double s, double z, const double *mids) {
+    const double lhs = 2.0 * __dsub_rn(y, z);
+    int lo = 0, hi = NM;
+#pragma unroll
+    for (int it = 0; it < 5; ++it) {
+        if (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (lhs > __dmul_rn(s, mids[mid])) lo = mid + 1; else hi = mid;
+        }
+    }
+    return lo;
+}
+
+// Block-wide exclusive scan of one int per thread; returns exclusive prefix, *total.
+__device__ __forceinline__ int block_excl_scan(int v, int *total, int *sbuf /*[QZ_WARPS+1]*/) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) sbuf[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int w = 0; w < QZ_WARPS; ++w) { int t = sbuf[w]; sbuf[w] = acc; acc += t; }
+        sbuf[QZ_WARPS] = acc;
+    }
+    __syncthreads();
+    int res = sbuf[warp] + x - v;
+    *total = sbuf[QZ_WARPS];
+    return res;
+}
+
+// Radix select over 16-bit keys of the "candidate" elements: returns tau such that
+// #(cand with key' > tau) < need <= #(cand with key' >= tau), where key' = key (desc=1)
+// or 0xffff - key (desc=0, i.e. ascending order).  Also returns #(key' > tau).
+__device__ void radix_select16(const uint16_t *keys, const uint8_t *flags, int D, int c_begin,
+                               int c_end, int need, bool desc, int *hist /*[256]*/,
+                               int *shared_out /*[4]*/, int *tau_out, int *gt_out) {
+    int prefix_hi = -1;   // selected high byte
+    int gt = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int b = threadIdx.x; b < 256; b += QZ_THREADS) hist[b] = 0;
+        __syncthreads();
+        for (int c = c_begin; c < c_end; ++c) {
+            if (flags[c]) continue;
+            int kk = desc ? keys[c] : (0xffff - keys[c]);
+            if (pass == 0) atomicAdd(&hist[kk >> 8], 1);
+            else if ((kk >> 8) == prefix_hi) atomicAdd(&hist[kk & 0xff], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // walk from the top bin down
+            int cum = 0, sel = 0;
+            for (int b = 255; b >= 0; --b) {
+                int h = hist[b];
+                if (cum + h >= need - gt) { sel = b; break; }
+                cum += h;
+            }
+            shared_out[0] = sel;
+            shared_out[1] = cum;
+        }
+        __syncthreads();
+        int sel = shared_out[0];
+        gt += shared_out[1];
+        if (pass == 0) prefix_hi = sel;
+        else *tau_out = (prefix_hi << 8) | sel;
+        __syncthreads();
+    }
+    *gt_out = gt;
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(QZ_THREADS)
+qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__ Vin, int64_t n0,
+          int mode) {
+    constexpr int NLEV = 1 << BITS;
+    constexpr int NM = NLEV - 1;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int D = c.D;
+    uint16_t *xk = reinterpret_cast<uint16_t *>(smem);          // [D]
+    uint16_t *xv = xk + D;                                        // [D]
+    uint16_t *vkey = xv + D;                                      // [D]
+    uint8_t *kc = reinterpret_cast<uint8_t *>(vkey + D);          // [D]
+    uint8_t *vc = kc + D;                                         // [D]
+    uint8_t *vflag = vc + D;                                      // [D]
+    int *hist = reinterpret_cast<int *>(vflag + ((D + 15) & ~15));// [256]
+    int *sbuf = hist + 256;                                       // [16]
+    int *sout = sbuf + 16;                                        // [8]
+    float *fred = reinterpret_cast<float *>(sout + 8);            // [16]
+    __shared__ double s_mk[16], s_mv[16];
+
+    const int64_t t = blockIdx.x;
+    const int64_t n = n0 + t;
+    const int tid = threadIdx.x;
+    const __half *krow = Kin + t * (int64_t)D;
+    const __half *vrow = Vin + t * (int64_t)D;
+    const uint16_t *kr16 = reinterpret_cast<const uint16_t *>(krow);
+    const uint16_t *vr16 = reinterpret_cast<const uint16_t *>(vrow);
+
+    if (tid < NM) { s_mk[tid] = c.mids[tid]; s_mv[tid] = c.mids[16 + tid]; }
+    for (int i = tid; i < D; i += QZ_THREADS) {
+        xk[i] = kr16[i];
+        if (mode != 1) { uint16_t v = vr16[i]; xv[i] = v; vkey[i] = f16_order_key(v); vflag[i] = 0; }
+    }
+    __syncthreads();
+
+    const float *ks = c.kpar, *kz = c.kpar + D, *klo = c.kpar + 2 * D, *khi = c.kpar + 3 * D;
+    // thread-contiguous channel ownership keeps ranks in ascending channel order
+    const int E = (D + QZ_THREADS - 1) / QZ_THREADS;
+    const int cb0 = min(D, tid * E), cb1 = min(D, cb0 + E);
+
+    // ------------------------------------------------------------------ Keys
+    int kcnt = 0;
+    for (int ch = cb0; ch < cb1; ++ch) {
+        float x = h2f(xk[ch]);
+        float lo = klo[ch], hi = khi[ch];
+        bool out = (x < lo) || (x > hi);
+        kcnt += out;
+        if (mode != 1) {
+            float y = x < lo ? lo : (x > hi ? hi : x);
+            kc[ch] = (uint8_t)enc_fp64<NM>((double)y, (double)ks[ch], (double)kz[ch], s_mk);
+        }
+    }
+    int ktotal;
+    int krank = block_excl_scan(kcnt, &ktotal, sbuf);
+    if (mode == 1) {
+        if (tid == 0) c.counts[t] = ktotal;
+        return;
+    }
+    {
+        __shared__ uint32_t s_base;
+        __shared__ int s_ok;
+        if (tid == 0) {
+            uint32_t base = c.kptr[n];
+            uint32_t end;
+            if (mode == 0) {
+                end = base + (uint32_t)ktotal;
+                bool ok = (int64_t)end <= c.kcap;
+                if (!ok) { end = base; *(volatile int *)c.err |= kErrKeyCapacity; }
+                c.kptr[n + 1] = end;
+                s_ok = ok;
+            } else {
+                end = c.kptr[n + 1];
+                bool ok = (int64_t)end <= c.kcap;
+                if (!ok) *(volatile int *)c.err |= kErrKeyCapacity;
+                s_ok = ok;
+            }
+            s_base = base;
+        }
+        __syncthreads();
+        if (s_ok) {
+            uint32_t pos = s_base + (uint32_t)krank;
+            for (int ch = cb0; ch < cb1; ++ch) {
+                float x = h2f(xk[ch]);
+                if ((x < klo[ch]) || (x > khi[ch]))
+                    c.kout[pos++] = (uint32_t)ch | ((uint32_t)xk[ch] << 16);
+            }
+        }
+    }
+
+    // ----------------------------------------------------------------- Values
+    const int k = c.kv;
+    const int ku = (k + 1) / 2, kl = k / 2;
+    for (int sel = 0; sel < 2; ++sel) {
+        const int need = sel == 0 ? ku : kl;
+        if (need == 0) continue;
+        const bool desc = (sel == 0);
+        int tau, gt;
+        radix_select16(vkey, vflag, D, cb0, cb1, need, desc, hist, sout, &tau, &gt);
+        // ties at tau: lowest channel index first
+        int ties = 0;
+        for (int ch = cb0; ch < cb1; ++ch) {
+            if (vflag[ch]) continue;
+            int kk = desc ? vkey[ch] : (0xffff - vkey[ch]);
+            ties += (kk == tau);
+        }
+        int tt;
+        int trank = block_excl_scan(ties, &tt, sbuf);
+        const int take = need - gt;
+        for (int ch = cb0; ch < cb1; ++ch) {
+            if (vflag[ch]) continue;
+            int kk = desc ? vkey[ch] : (0xffff - vkey[ch]);
+            if (kk > tau) vflag[ch] = 1 + sel;
+            else if (kk == tau) { if (trank < take) vflag[ch] = 1 + sel; ++trank; }
+        }
+        __syncthreads();
+    }
+
+    // kept range: value min/max, then the lowest-index element attaining it
+    float vmin = INFINITY, vmax = -INFINITY;
+    for (int ch = cb0; ch < cb1; ++ch) {
+        if (vflag[ch]) continue;
+        float x = h2f(xv[ch]);
+        vmin = fminf(vmin, x);
+        vmax = fmaxf(vmax, x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    if ((tid & 31) == 0) { fred[tid >> 5] = vmin; fred[8 + (tid >> 5)] = vmax; }
+    __syncthreads();
+    if (tid == 0) {
+        float a = fred[0], b = fred[8];
+        for (int w = 1; w < QZ_WARPS; ++w) { a = fminf(a, fred[w]); b = fmaxf(b, fred[8 + w]); }
+        fred[0] = a; fred[8] = b;
+    }
+    __syncthreads();
+    vmin = fred[0]; vmax = fred[8];
+    int imin = 0x7fffffff, imax = 0x7fffffff;
+    for (int ch = cb0; ch < cb1; ++ch) {
+        if (vflag[ch]) continue;
+        float x = h2f(xv[ch]);
+        if (x == vmin && imin == 0x7fffffff) imin = ch;
+        if (x == vmax && imax == 0x7fffffff) imax = ch;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        imin = min(imin, __shfl_xor_sync(0xffffffffu, imin, o));
+        imax = min(imax, __shfl_xor_sync(0xffffffffu, imax, o));
+    }
+    __syncthreads();
+    if ((tid & 31) == 0) { sbuf[tid >> 5] = imin; sout[tid >> 5] = imax; }
+    __syncthreads();
+    __shared__ double s_lo, s_hi, s_s, s_z;
+    if (tid == 0) {
+        int a = sbuf[0], b = sout[0];
+        for (int w = 1; w < QZ_WARPS; ++w) { a = min(a, sbuf[w]); b = min(b, sout[w]); }
+        double lo = (double)h2f(xv[a]), hi = (double)h2f(xv[b]);
+        float s = __double2float_rn(__dsub_rn(hi, lo) / 2.0);
+        float z = __double2float_rn(__dadd_rn(hi, lo) / 2.0);
+        s_lo = lo; s_hi = hi; s_s = (double)s; s_z = (double)z;
+        c.vsz[n] = make_float2(s, z);
+    }
+    __syncthreads();
+    {
+        const double lo = s_lo, hi = s_hi, s = s_s, z = s_z;
+        int vcnt = 0;
+        for (int ch = cb0; ch < cb1; ++ch) {
+            double x = (double)h2f(xv[ch]);
+            double y = x < lo ? lo : (x > hi ? hi : x);
+            vc[ch] = (uint8_t)enc_fp64<NM>(y, s, z, s_mv);
+            vcnt += vflag[ch] != 0;
+        }
+        int vtot;
+        int vr = block_excl_scan(vcnt, &vtot, sbuf);
+        uint32_t *vo = c.vout + n * (int64_t)k;
+        for (int ch = cb0; ch < cb1; ++ch)
+            if (vflag[ch]) vo[vr++] = (uint32_t)ch | ((uint32_t)xv[ch] << 16);
+    }
+    __syncthreads();
+
+    // --------------------------------------------------------------- packing
+    constexpr int PB = 2 * BITS;                 // bits per Key pair code
+    const int tile = (int)(n >> 5), jj = (int)(n & 31);
+    for (int q = tid; q < c.QW; q += QZ_THREADS) {
+        const int h = q / (4 * BITS), w = q % (4 * BITS);
+        const int bit0 = 32 * w;
+        const int p0 = bit0 / PB, off = bit0 - p0 * PB;
+        unsigned long long acc = 0;
+        for (int p = p0, sh = 0; sh < 32 + off && p < kPairs; ++p, sh += PB) {
+            unsigned pc = (unsigned)kc[h * kHeadDim + p] | ((unsigned)kc[h * kHeadDim + p + kPairs] << BITS);
+            acc |= (unsigned long long)pc << sh;
+        }
+        c.kcodes[((int64_t)tile * c.QW + q) * 32 + jj] = (uint32_t)(acc >> off);
+    }
+    for (int w = tid; w < c.VW; w += QZ_THREADS) {
+        const int bit0 = 32 * w;
+        const int c0 = bit0 / BITS, off = bit0 - c0 * BITS;
+        unsigned long long acc = 0;
+        for (int ch = c0, sh = 0; sh < 32 + off && ch < D; ++ch, sh += BITS)
+            acc |= (unsigned long long)vc[ch] << sh;
+        c.vcodes[n * (int64_t)c.VW + w] = (uint32_t)(acc >> off);
+    }
+}
+
+// Prefill pass 2: kptr[n0+1+t] = kptr[n0] + inclusive_scan(counts)[t]  (one CTA).
+__global__ void __launch_bounds__(1024) scan_counts_kernel(DevCache c, int64_t n0, int64_t T) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) carry = c.kptr[n0];
+    __syncthreads();
+    for (int64_t b = 0; b < T; b += 1024) {
+        int64_t i = b + tid;
+        uint32_t v = i < T ? (uint32_t)c.counts[i] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t s = wsum[lane], t2 = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, t2, o);
+                if (lane >= o) t2 += y;
+            }
+            wsum[lane] = t2 - s;   // exclusive warp offsets
+        }
+        __syncthreads();
+        uint32_t incl = carry + wsum[warp] + x;
+        if (i < T) c.kptr[n0 + 1 + i] = incl;
+        __syncthreads();
+        if (tid == 1023) carry = incl;
+        __syncthreads();
+    }
+}
+
+size_t qz_smem(int D) {
+    size_t b = (size_t)D * 2 * 3 + (size_t)D * 3;
+    b = (b + 15) & ~size_t(15);
+    b += (256 + 16 + 8 + 16) * 4;
+    return b;
+}
+
+template <int BITS>
+cudaError_t launch_qz_bits(const DevCache &c, const __half *K, const __half *V, int64_t n0,
+                           int64_t T, cudaStream_t s) {
+    size_t smem = qz_smem(c.D);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(qz_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (T == 1) {
+        qz_kernel<BITS><<<1, QZ_THREADS, smem, s>>>(c, K, V, n0, 0);
+        return cudaGetLastError();
+    }
+    qz_kernel<BITS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 1);
+    scan_counts_kernel<<<1, 1024, 0, s>>>(c, n0, T);
+    qz_kernel<BITS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 2);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_quantize(const DevCache &c, const __half *K, const __half *V, int64_t n0,
+                            int64_t T, cudaStream_t s) {
+    switch (c.bits) {
+        case 2: return launch_qz_bits<2>(c, K, V, n0, T, s);
+        case 3: return launch_qz_bits<3>(c, K, V, n0, T, s);
+        case 4: return launch_qz_bits<4>(c, K, V, n0, T, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace kvq

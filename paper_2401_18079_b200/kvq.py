@@ -1,0 +1,255 @@
+"""Thin Python binding of libkvq (ctypes).  Argument marshalling only.
+
+Every call goes to the C ABI declared in include/kvq.h; every step of the hot path runs
+in the sm_100a kernels of libkvq.so.  There is no CPU fallback: if the shared library
+is missing or fails to load, importing the binding raises.
+
+Buffers may be torch CUDA tensors (device pointers on the cache's device), torch CPU
+tensors or numpy arrays (host memory: the library stages them on the call's stream).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkvq.so")
+
+KVQ_OK, KVQ_EINVAL, KVQ_ESHAPE, KVQ_EEMPTY, KVQ_ECAPACITY, KVQ_EDEVICE, KVQ_ECUDA = range(7)
+_STATUS = {0: "KVQ_OK", 1: "KVQ_EINVAL", 2: "KVQ_ESHAPE", 3: "KVQ_EEMPTY",
+           4: "KVQ_ECAPACITY", 5: "KVQ_EDEVICE", 6: "KVQ_ECUDA"}
+KVQ_FLAG_TRUST_DEVICE_PTRS = 1
+
+# Every symbol include/kvq.h declares (checked by tests/test_abi.py).
+EXPORTED = ["kvq_cache_create", "kvq_cache_destroy", "kvq_append", "kvq_prefill_quantize",
+            "kvq_decode_attend", "kvq_decode_attend_partial", "kvq_merge_partials",
+            "kvq_num_tokens", "kvq_reset", "kvq_sync", "kvq_key_outlier_span", "kvq_export",
+            "kvq_get_info", "kvq_set_splits", "kvq_last_error", "kvq_version"]
+
+
+class KVQError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class kvq_config(ctypes.Structure):
+    _fields_ = [("n_q_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("bits", ctypes.c_int32),
+                ("outlier_ppm", ctypes.c_int32), ("capacity_tokens", ctypes.c_int64),
+                ("k_outlier_capacity", ctypes.c_int64), ("pos_base", ctypes.c_int64),
+                ("rope_theta", ctypes.c_double), ("device", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+_PF = ctypes.POINTER(ctypes.c_float)
+
+
+class kvq_params(ctypes.Structure):
+    _fields_ = [("key_cb_enc", _PF), ("key_cb_dec", _PF), ("val_cb_enc", _PF),
+                ("val_cb_dec", _PF), ("key_lo", _PF), ("key_hi", _PF)]
+
+
+class kvq_export_buf(ctypes.Structure):
+    _fields_ = [("kcodes", ctypes.c_void_p), ("kptr", ctypes.c_void_p), ("kidx", ctypes.c_void_p),
+                ("kval", ctypes.c_void_p), ("vcodes", ctypes.c_void_p), ("vidx", ctypes.c_void_p),
+                ("vval", ctypes.c_void_p), ("vs", ctypes.c_void_p), ("vz", ctypes.c_void_p)]
+
+
+class kvq_info(ctypes.Structure):
+    _fields_ = [("heads_per_cta", ctypes.c_int32), ("splits", ctypes.c_int32),
+                ("value_outliers", ctypes.c_int32), ("words_per_token", ctypes.c_int32),
+                ("capacity_tokens", ctypes.c_int64), ("k_outlier_capacity", ctypes.c_int64),
+                ("device_bytes", ctypes.c_int64)]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libkvq.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "kvq_cache_create": (i32, [ctypes.POINTER(kvq_config), ctypes.POINTER(kvq_params), ctypes.POINTER(vp)]),
+        "kvq_cache_destroy": (None, [vp]),
+        "kvq_append": (i32, [vp, vp, vp, vp]),
+        "kvq_prefill_quantize": (i32, [vp, vp, vp, i64, vp]),
+        "kvq_decode_attend": (i32, [vp, vp, i64, vp, vp]),
+        "kvq_decode_attend_partial": (i32, [vp, vp, i64, vp, vp]),
+        "kvq_merge_partials": (i32, [vp, i32, i32, i32, vp, i32, vp]),
+        "kvq_num_tokens": (i64, [vp]),
+        "kvq_reset": (i32, [vp, vp]),
+        "kvq_sync": (i32, [vp]),
+        "kvq_key_outlier_span": (i32, [vp, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "kvq_export": (i32, [vp, i64, i64, ctypes.POINTER(kvq_export_buf)]),
+        "kvq_get_info": (i32, [vp, ctypes.POINTER(kvq_info)]),
+        "kvq_set_splits": (i32, [vp, i32]),
+        "kvq_last_error": (ctypes.c_char_p, []),
+        "kvq_version": (i32, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def _check(status: int):
+    if status != KVQ_OK:
+        raise KVQError(status, _lib.kvq_last_error().decode(errors="replace"))
+
+
+def _ptr(x):
+    """Raw pointer of a torch tensor (device or host) or numpy array (host)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(x.data_ptr())
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return ctypes.c_void_p(x.ctypes.data)
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def _stream(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except ImportError:
+            pass
+        return None
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+def version() -> int:
+    return _lib.kvq_version()
+
+
+class KVQCache:
+    """One layer's compressed KV cache (wraps a kvq_cache handle)."""
+
+    def __init__(self, *, n_q_heads: int, n_kv_heads: int, head_dim: int = 128, bits: int,
+                 outlier_ppm: int, capacity_tokens: int, key_cb, val_cb, key_lo, key_hi,
+                 key_cb_dec=None, val_cb_dec=None, k_outlier_capacity: int = 0,
+                 pos_base: int = 0, rope_theta: float = 10000.0, device: int = 0,
+                 trust_device_ptrs: bool = False):
+        cfg = kvq_config(n_q_heads, n_kv_heads, head_dim, bits, outlier_ppm, capacity_tokens,
+                         k_outlier_capacity, pos_base, rope_theta, device,
+                         KVQ_FLAG_TRUST_DEVICE_PTRS if trust_device_ptrs else 0)
+        keep = [_f32(key_cb), None if key_cb_dec is None else _f32(key_cb_dec), _f32(val_cb),
+                None if val_cb_dec is None else _f32(val_cb_dec), _f32(key_lo), _f32(key_hi)]
+
+        def fp(a):
+            return None if a is None else a.ctypes.data_as(_PF)
+
+        prm = kvq_params(*[fp(a) for a in keep])
+        h = ctypes.c_void_p()
+        _check(_lib.kvq_cache_create(ctypes.byref(cfg), ctypes.byref(prm), ctypes.byref(h)))
+        self._h = h
+        self.cfg = cfg
+        self.D = n_kv_heads * head_dim
+        self.H_q, self.H_kv, self.d, self.bits = n_q_heads, n_kv_heads, head_dim, bits
+
+    # -- lifecycle -------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.kvq_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- hot path --------------------------------------------------------------------
+    def append(self, k, v, stream=None):
+        _check(_lib.kvq_append(self._h, _ptr(k), _ptr(v), _stream(stream)))
+
+    def prefill(self, K, V, stream=None):
+        T = int(K.shape[0])
+        _check(_lib.kvq_prefill_quantize(self._h, _ptr(K), _ptr(V), T, _stream(stream)))
+
+    def attend(self, q, pos: int, out, stream=None):
+        _check(_lib.kvq_decode_attend(self._h, _ptr(q), int(pos), _ptr(out), _stream(stream)))
+        return out
+
+    def attend_partial(self, q, pos: int, out, stream=None):
+        _check(_lib.kvq_decode_attend_partial(self._h, _ptr(q), int(pos), _ptr(out), _stream(stream)))
+        return out
+
+    # -- utilities -------------------------------------------------------------------
+    @property
+    def num_tokens(self) -> int:
+        return int(_lib.kvq_num_tokens(self._h))
+
+    def reset(self, stream=None):
+        _check(_lib.kvq_reset(self._h, _stream(stream)))
+
+    def sync(self):
+        _check(_lib.kvq_sync(self._h))
+
+    def set_splits(self, splits: int):
+        _check(_lib.kvq_set_splits(self._h, int(splits)))
+
+    def info(self) -> dict:
+        inf = kvq_info()
+        _check(_lib.kvq_get_info(self._h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in kvq_info._fields_}
+
+    def key_outlier_span(self, t0: int, t1: int):
+        b, e = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.kvq_key_outlier_span(self._h, t0, t1, ctypes.byref(b), ctypes.byref(e)))
+        return b.value, e.value
+
+    def export(self, t0: int = 0, t1: Optional[int] = None) -> dict:
+        """Canonical cache contents of tokens [t0, t1) as numpy arrays."""
+        if t1 is None:
+            t1 = self.num_tokens
+        n = t1 - t0
+        kb, ke = self.key_outlier_span(t0, t1)
+        kv = self.info()["value_outliers"]
+        out = dict(kcodes=np.zeros((n, self.D), np.uint8), vcodes=np.zeros((n, self.D), np.uint8),
+                   kptr=np.zeros(n + 1, np.int64), kidx=np.zeros(max(ke - kb, 1), np.uint16),
+                   kval=np.zeros(max(ke - kb, 1), np.uint16), vidx=np.zeros((n, max(kv, 1)), np.uint16),
+                   vval=np.zeros((n, max(kv, 1)), np.uint16), vs=np.zeros(n, np.float32),
+                   vz=np.zeros(n, np.float32))
+        buf = kvq_export_buf(*[out[k].ctypes.data for k in
+                               ("kcodes", "kptr", "kidx", "kval", "vcodes", "vidx", "vval", "vs", "vz")])
+        _check(_lib.kvq_export(self._h, t0, t1, ctypes.byref(buf)))
+        out["kidx"] = out["kidx"][: ke - kb]
+        out["kval"] = out["kval"][: ke - kb]
+        out["vidx"] = out["vidx"][:, :kv]
+        out["vval"] = out["vval"][:, :kv]
+        return out
+
+
+def merge_partials(parts, out, device: int = 0, stream=None):
+    """Log-sum-exp merge of [P, H_q, d+2] partials (m in log2 units) into o [H_q, d]."""
+    P, H, d2 = (int(s) for s in parts.shape)
+    _check(_lib.kvq_merge_partials(_ptr(parts), P, H, d2 - 2, _ptr(out), int(device), _stream(stream)))
+    return out

@@ -1,0 +1,237 @@
+"""GPU parity: CUDA path (through the C ABI) vs the CPU oracle, same seeded inputs.
+
+Bars (north_star):
+  * packed codes, outlier indices / values, CSC pointers, per-token (s, z): bit-exact
+    (the integer decisions are taken in fp64 on both sides, reading R8);
+  * attention output: per query head ||o_gpu - o_ref||_inf / ||o_ref||_inf <= 2e-3
+    (fp16 products with fp32 accumulation, derived in DESIGN.md).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from kvq_synth import gen
+
+from .gpu_common import (assert_cache_equal, make_cache, merged_partial_to_natural,
+                         rel_err_per_head, setup_layer)
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def kvq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2401_18079_b200 import kvq as m
+    return m
+
+
+def oracle_cache(cal, K, V, ppm):
+    return O.prefill(K, V, cal["key_lo"], cal["key_hi"], cal["cbK"], cal["cbV"], ppm)
+
+
+def oracle_attend(cal, cache, q, pos, H_q, H_kv, pos_base=0):
+    return O.attend(cache, q, pos, H_q=H_q, H_kv=H_kv, d=128, key_lo=cal["key_lo"],
+                    key_hi=cal["key_hi"], cbK_dec=cal["cbK_dec"], cbV_dec=cal["cbV_dec"],
+                    pos_base=pos_base, nthreads=0)
+
+
+# -------------------------------------------------------------- quantization (T1) --
+@pytest.mark.parametrize("H,bits,ppm,T", [(1, 4, 10_000, 77), (2, 3, 10_000, 100),
+                                          (2, 2, 10_000, 65), (8, 3, 10_000, 96),
+                                          (4, 4, 1_000, 33), (1, 3, 0, 40)])
+def test_prefill_quantization_bit_exact(kvq, H, bits, ppm, T):
+    cal, K, V = setup_layer(1, 0, H, H, bits, ppm, T)
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=T + 5)
+    c.prefill(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    c.sync()
+    assert_cache_equal(c.export(), ref)
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4])
+def test_append_then_prefill_mixed(kvq, bits):
+    H, ppm, T = 2, 10_000, 70
+    cal, K, V = setup_layer(2, 1, H, H, bits, ppm, T)
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=T)
+    Kt, Vt = torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda()
+    for n in range(5):
+        c.append(Kt[n], Vt[n])
+    c.prefill(Kt[5:50], Vt[5:50])
+    for n in range(50, T):
+        c.append(Kt[n], Vt[n])
+    c.sync()
+    assert c.num_tokens == T
+    assert_cache_equal(c.export(), ref)
+    assert_cache_equal(c.export(31, 66), ref, 31, 66)
+
+
+def test_adversarial_quantization_inputs(kvq):
+    """ties, -0/+0, all-equal tokens, values on midpoints and on thresholds."""
+    H, bits, ppm = 1, 3, 20_000
+    D = 128
+    cb = np.array([-1.0, -0.5, -0.25, 0.0, 0.25, 0.5, 0.75, 1.0], np.float32)
+    lo = np.full(D, -2.0, np.float32)
+    hi = np.full(D, 2.0, np.float32)
+    cal = dict(cbK=cb, cbV=cb, cbK_dec=cb, cbV_dec=cb, key_lo=lo, key_hi=hi)
+    rows_k, rows_v = [], []
+    rng = np.random.default_rng(5)
+    rows_k.append(np.zeros(D)); rows_v.append(np.zeros(D))                       # all zero
+    z = np.zeros(D); z[::2] = -0.0; rows_k.append(z); rows_v.append(z.copy())    # -0 / +0
+    rows_k.append(np.full(D, 2.0)); rows_v.append(np.full(D, 3.5))               # == hi, all equal
+    mids = np.repeat([-0.75, -0.375, -0.125, 0.125, 0.375, 0.625, 0.875], 19)[:D] * 2.0
+    rows_k.append(mids); rows_v.append(np.concatenate([mids[:-2], [7.0, -7.0]]))  # midpoints
+    t = rng.choice([-1.0, 0.0, 1.0, 2.0], D); rows_k.append(t); rows_v.append(t)  # heavy ties
+    rows_k.append(np.linspace(-3, 3, D)); rows_v.append(np.linspace(-3, 3, D)[::-1].copy())
+    K = np.stack(rows_k).astype(np.float16)
+    V = np.stack(rows_v).astype(np.float16)
+    K[1, ::2] = np.float16(-0.0)
+    V[1, ::2] = np.float16(-0.0)
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=16)
+    Kt, Vt = torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda()
+    c.prefill(Kt[:3], Vt[:3])
+    for n in range(3, K.shape[0]):
+        c.append(Kt[n], Vt[n])
+    c.sync()
+    assert_cache_equal(c.export(), ref)
+
+
+def test_host_buffers_are_staged(kvq):
+    H, bits, ppm, T = 2, 3, 10_000, 40
+    cal, K, V = setup_layer(3, 0, H, H, bits, ppm, T)
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=T)
+    c.prefill(K[:30], V[:30])                      # numpy (pageable host)
+    for n in range(30, T):
+        c.append(np.ascontiguousarray(K[n]), np.ascontiguousarray(V[n]))
+    c.sync()
+    assert_cache_equal(c.export(), ref)
+    q = gen.gen_queries(3, 0, H, H, 128)[0]
+    o = np.zeros((H, 128), np.float32)
+    c.attend(q, T - 1, o)
+    assert rel_err_per_head(o, oracle_attend(cal, ref, q, T - 1, H, H)).max() < TOL
+
+
+# ----------------------------------------------------------------- attention (T2) --
+@pytest.mark.parametrize("H_q,H_kv,bits,T", [(1, 1, 4, 4096), (8, 8, 3, 1000), (2, 2, 4, 333),
+                                             (8, 8, 2, 517), (8, 2, 3, 300), (4, 1, 3, 129),
+                                             (16, 16, 3, 700), (32, 8, 3, 257)])
+def test_attend_matches_oracle(kvq, H_q, H_kv, bits, T):
+    ppm = 10_000
+    cal, K, V = setup_layer(4, 0, H_q, H_kv, bits, ppm, T)
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H_q, H_kv, bits, ppm, capacity=T + 64)
+    c.prefill(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    qs = gen.gen_queries(4, 0, H_q, H_kv, 128, n=2)
+    for pos, q in zip((T - 1, T + 1000), qs):
+        o = torch.zeros((H_q, 128), dtype=torch.float32, device="cuda")
+        c.attend(torch.from_numpy(q).cuda(), pos, o)
+        torch.cuda.synchronize()
+        err = rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, pos, H_q, H_kv))
+        assert err.max() < TOL, err
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 7, 40])
+def test_attend_independent_of_split_count(kvq, splits):
+    H, bits, ppm, T = 8, 3, 10_000, 1234
+    cal, K, V = setup_layer(5, 0, H, H, bits, ppm, T)
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=T)
+    c.prefill(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    c.set_splits(splits)
+    q = gen.gen_queries(5, 0, H, H, 128)[0]
+    o = torch.zeros((H, 128), dtype=torch.float32, device="cuda")
+    c.attend(torch.from_numpy(q).cuda(), T, o)
+    torch.cuda.synchronize()
+    assert rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, T, H, H)).max() < TOL
+
+
+def test_long_positions_exact_angles(kvq):
+    """pos_base near 10M: RoPE angles must be reduced exactly (reading R12)."""
+    H, bits, ppm, T = 2, 3, 10_000, 200
+    base = 9_999_000
+    cal, K, V = setup_layer(6, 0, H, H, bits, ppm, T)
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=T, pos_base=base)
+    c.prefill(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    q = gen.gen_queries(6, 0, H, H, 128)[0]
+    o = torch.zeros((H, 128), dtype=torch.float32, device="cuda")
+    c.attend(torch.from_numpy(q).cuda(), base + T, o)
+    torch.cuda.synchronize()
+    err = rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, base + T, H, H, pos_base=base))
+    assert err.max() < TOL, err
+
+
+def test_sharded_partials_merge_to_unsharded(kvq):
+    """Sequence sharding on one GPU: P shards with pos_base, merged."""
+    H, bits, ppm, T = 8, 3, 10_000, 999
+    cal, K, V = setup_layer(7, 0, H, H, bits, ppm, T)
+    ref = oracle_cache(cal, K, V, ppm)
+    q = gen.gen_queries(7, 0, H, H, 128)[0]
+    qt = torch.from_numpy(q).cuda()
+    cuts = [0, 250, 600, 601, 999]
+    parts = torch.zeros((len(cuts) - 1, H, 130), dtype=torch.float32, device="cuda")
+    caches = []
+    for r, (a, b) in enumerate(zip(cuts[:-1], cuts[1:])):
+        c = make_cache(kvq, cal, H, H, bits, ppm, capacity=b - a, pos_base=a)
+        c.prefill(torch.from_numpy(K[a:b]).cuda(), torch.from_numpy(V[a:b]).cuda())
+        c.attend_partial(qt, T, parts[r])
+        caches.append(c)
+    o = torch.zeros((H, 128), dtype=torch.float32, device="cuda")
+    kvq.merge_partials(parts, o)
+    torch.cuda.synchronize()
+    exp = oracle_attend(cal, ref, q, T, H, H)
+    assert rel_err_per_head(o.cpu().numpy(), exp).max() < TOL
+    # each shard's partial against the oracle's partial on the same shard
+    for r, (a, b) in enumerate(zip(cuts[:-1], cuts[1:])):
+        sub = oracle_cache(cal, K[a:b], V[a:b], ppm)
+        pref = O.attend_partial(sub, q, T, H_q=H, H_kv=H, d=128, key_lo=cal["key_lo"],
+                                key_hi=cal["key_hi"], cbK_dec=cal["cbK_dec"],
+                                cbV_dec=cal["cbV_dec"], pos_base=a)
+        pg = merged_partial_to_natural(parts[r].cpu().numpy())
+        np.testing.assert_allclose(pg[:, -2], pref[:, -2], rtol=1e-3, atol=1e-3)
+        og = pg[:, :128] / pg[:, -1:]
+        orr = pref[:, :128] / pref[:, -1:]
+        assert rel_err_per_head(og, orr).max() < TOL
+
+
+def test_empty_cache_and_capacity_errors(kvq):
+    H, bits, ppm = 1, 3, 10_000
+    cal, K, V = setup_layer(8, 0, H, H, bits, ppm, 40)
+    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=32)
+    q = torch.zeros((H, 128), dtype=torch.float16, device="cuda")
+    o = torch.zeros((H, 128), dtype=torch.float32, device="cuda")
+    with pytest.raises(kvq.KVQError) as e:
+        c.attend(q, 0, o)
+    assert e.value.status == kvq.KVQ_EEMPTY
+    p = torch.zeros((H, 130), dtype=torch.float32, device="cuda")
+    c.attend_partial(q, 0, p)
+    assert float(p[0, 129]) == 0.0 and float(p[0, 128]) == float("-inf")
+    Kt, Vt = torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda()
+    c.prefill(Kt[:32], Vt[:32])
+    with pytest.raises(kvq.KVQError) as e:
+        c.append(Kt[32], Vt[32])
+    assert e.value.status == kvq.KVQ_ECAPACITY
+    assert c.num_tokens == 32
+    c.reset()
+    c.prefill(Kt[:7], Vt[:7])
+    c.sync()
+    assert_cache_equal(c.export(), oracle_cache(cal, K[:7], V[:7], ppm))
+
+
+def test_key_outlier_capacity_is_sticky(kvq):
+    H, bits, ppm, T = 1, 3, 10_000, 64
+    cal, K, V = setup_layer(9, 0, H, H, bits, ppm, T)
+    cal = dict(cal)
+    cal["key_lo"] = np.full(128, -0.01, np.float32)      # nearly everything is an outlier
+    cal["key_hi"] = np.full(128, 0.01, np.float32)
+    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=T, k_outlier_capacity=100)
+    c.prefill(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    with pytest.raises(kvq.KVQError) as e:
+        c.sync()
+    assert e.value.status == kvq.KVQ_ECAPACITY
