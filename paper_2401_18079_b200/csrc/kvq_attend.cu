@@ -29,8 +29,6 @@ namespace {
 constexpr int ATT_THREADS = 256;
 constexpr int ATT_WARPS = 8;
 
-__device__ __forceinline__ float fma_f16(uint32_t ab, uint32_t cd, float acc_lo_unused);
-
 // acc += lo(x)*lo(y) ; acc2 += hi(x)*hi(y)   (fp16 products, fp32 accumulation)
 __device__ __forceinline__ void fma2_f16_f32(uint32_t x, uint32_t y, float &acc, float &acc2) {
     asm("{\n\t.reg .b16 x0, x1, y0, y1;\n\t"
@@ -82,8 +80,11 @@ struct Params {
 template <int BITS, int HG>
 struct Smem {
     static constexpr int NE = 1 << (2 * BITS);
+    static constexpr int HMAX = BITS == 4 ? 4 : 8;   // fp32 "heavy" pairs per head
     static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
     static constexpr size_t vlut = (size_t)NE * 32 * 4;
+    static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
+    static constexpr size_t cis = (size_t)kPairs * 32 * 8;
     static constexpr size_t fixed =
         HG * kHeadDim * 4              /* qs */
         + ATT_WARPS * HG * 32 * 4      /* red */
@@ -94,8 +95,10 @@ struct Smem {
         + 64 * 4                       /* theta32 */
         + 40 * 4 + 32 * 8              /* kptr slice, vsz slice */
         + HG * 4 * 8                   /* per-head scalars */
+        + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
+        + HG * 16 * 4                  /* heavy pair list + counts */
         + 64;
-    static constexpr size_t total = klut + vlut + fixed + 128;
+    static constexpr size_t total = klut + vlut + hlut + cis + fixed + 128;
 };
 
 template <int BITS, int HG, int G>
@@ -107,12 +110,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     constexpr int LPT = 4 * HG;                     // V lanes per token
     constexpr int SLOTS = ATT_THREADS / LPT;        // tokens per V step
     constexpr int VSTEPS = (32 + SLOTS - 1) / SLOTS;
-    constexpr float LOG2E = 1.4426950408889634f;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned char *sp = smem_raw;
     uint32_t *klut = reinterpret_cast<uint32_t *>(sp); sp += Smem<BITS, HG>::klut;
     uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += Smem<BITS, HG>::vlut;
+    float2 *hlut = reinterpret_cast<float2 *>(sp); sp += Smem<BITS, HG>::hlut;
+    float2 *cis_s = reinterpret_cast<float2 *>(sp); sp += Smem<BITS, HG>::cis;
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *red = reinterpret_cast<float *>(sp); sp += ATT_WARPS * HG * 32 * 4;
     float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
@@ -132,6 +136,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *z_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
     uint16_t *w16 = reinterpret_cast<uint16_t *>(sp); sp += HG * 32 * 2;
     int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
+    float *bound_s = reinterpret_cast<float *>(sp); sp += HG * 64 * 4;
+    uint8_t *heavy_s = reinterpret_cast<uint8_t *>(sp); sp += HG * 64;
+    int *hv_pair = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
+    int *hv_n = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
+    constexpr int HMAX = Smem<BITS, HG>::HMAX;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
@@ -176,8 +185,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         qs[g * kHeadDim + i + 64] = (float)((b * cs.x + a * cs.y) * qscale);
     }
     __syncthreads();
-    // K LUT scale: per head bound of |A|,|B|
-    __shared__ float bound_s[HG * 64];
+    // K LUT: per (head, pair) bound of |A|,|B|.  The few pairs carrying a heavy Key
+    // channel (bound > 1/4 of the head max, at most HMAX per head) get fp32 tables and
+    // are accumulated exactly in fp32 (a3'); the rest use fp16 tables whose scale is set
+    // by the largest remaining bound.
     for (int x = tid; x < HG * 64; x += ATT_THREADS) {
         const int g = x >> 6, i = x & 63;
         const int kvh = (g0 + g) / G;
@@ -189,12 +200,27 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     }
     __syncthreads();
     if (warp < HG) {
-        float b = fmaxf(bound_s[warp * 64 + lane], bound_s[warp * 64 + 32 + lane]);
-        b = warp_max(b);
+        const float b0 = bound_s[warp * 64 + lane], b1 = bound_s[warp * 64 + 32 + lane];
+        const float M = warp_max(fmaxf(b0, b1));
+        float tau = 0.25f * M;
+        unsigned m0 = __ballot_sync(0xffffffffu, b0 > tau), m1 = __ballot_sync(0xffffffffu, b1 > tau);
+        while (__popc(m0) + __popc(m1) > HMAX) {
+            tau *= 1.25f;
+            m0 = __ballot_sync(0xffffffffu, b0 > tau);
+            m1 = __ballot_sync(0xffffffffu, b1 > tau);
+        }
+        const unsigned lt = (1u << lane) - 1u;
+        const int n0c = __popc(m0);
+        if ((m0 >> lane) & 1u) hv_pair[warp * 8 + __popc(m0 & lt)] = lane;
+        if ((m1 >> lane) & 1u) hv_pair[warp * 8 + n0c + __popc(m1 & lt)] = lane + 32;
+        heavy_s[warp * 64 + lane] = (m0 >> lane) & 1u;
+        heavy_s[warp * 64 + 32 + lane] = (m1 >> lane) & 1u;
+        const float rest = warp_max(fmaxf(((m0 >> lane) & 1u) ? 0.f : b0, ((m1 >> lane) & 1u) ? 0.f : b1));
         if (lane == 0) {
+            hv_n[warp] = n0c + __popc(m1);
             // scale so that |entry| <= 2^14 (fp16 max 65504)
             int e = 0;
-            if (b > 0.f && isfinite(b)) e = 14 - ilogbf(b) - 1;
+            if (rest > 0.f && isfinite(rest)) e = 14 - ilogbf(rest) - 1;
             e = max(-100, min(100, e));
             alpha_s[warp] = ldexpf(1.f, e);      // temp: LUT scale
             lut_inv[warp] = ldexpf(1.f, -e);
@@ -215,15 +241,25 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             Y[a] = cbK[a] * ks[cj] + kz[cj];
         }
         uint32_t *dst = klut + (size_t)(g * 64 + i) * NE;
+        const bool heavy = heavy_s[x] != 0;
+        int hslot = -1;
+        if (heavy)
+            for (int u = 0; u < hv_n[g]; ++u) hslot = hv_pair[g * 8 + u] == i ? u : hslot;
+        const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
         for (int e0 = 0; e0 < NE; ++e0) {
             const int e = (e0 + lane) & (NE - 1);
             const int a = e & CM, bb = e >> BITS;
             float xa = 0.f, yb = 0.f;
 #pragma unroll
             for (int u = 0; u <= CM; ++u) { xa = (u == a) ? X[u] : xa; yb = (u == bb) ? Y[u] : yb; }
-            const float A = qa * xa + qb * yb;
-            const float B = qb * xa - qa * yb;
-            dst[e] = pack_half2(A, B);
+            if (heavy) {
+                dst[e] = 0u;
+                hlut[(g * HMAX + hslot) * NE + e] = make_float2(qa1 * xa + qb1 * yb, qb1 * xa - qa1 * yb);
+            } else {
+                const float A = qa * xa + qb * yb;
+                const float B = qb * xa - qa * yb;
+                dst[e] = pack_half2(A, B);
+            }
         }
     }
     // V LUT: lane-private copies (entry e for lane slot l at word e*32 + l)
@@ -322,6 +358,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const float cc = an.x * t1c[k] - an.y * t1s[k];
                 const float ss = an.x * t1s[k] + an.y * t1c[k];
                 const uint32_t cs = pack_half2(cc, ss);
+                cis_s[i * 32 + lane] = make_float2(cc, ss);
 #pragma unroll
                 for (int h = 0; h < HKV; ++h) {
                     const int pc = (int)((win[h] >> (2 * BITS * k)) & (NE - 1));
@@ -360,10 +397,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const int code = (pc >> (up * BITS)) & CM;
                 const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
                 const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
-                float sj, cj;
-                sincosf((float)j * theta32[i], &sj, &cj);
-                const float2 an = anc32[i];
-                const float co = an.x * cj - an.y * sj, si = an.x * sj + an.y * cj;
+                const float2 cs = cis_s[i * 32 + j];
+                const float co = cs.x, si = cs.y;
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
                     const int g = (kvh - h0) * G + gg;
@@ -371,6 +406,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     const float d = up ? (qb * co - qa * si) : (qa * co + qb * si);
                     atomicAdd(&kcorr[g * 32 + j], delta * d);
                 }
+            }
+            // a2': heavy RoPE pairs in fp32 (tables hlut; cis of the tile from the K phase)
+            for (int x = tid; x < HG * 8 * 32; x += ATT_THREADS) {
+                const int g = x >> 8, slot = (x >> 5) & 7, j = x & 31;
+                if (slot >= hv_n[g] || j >= ntok) continue;
+                const int i = hv_pair[g * 8 + slot];
+                const int kvh = (g0 + g) / G;
+                const int bit = 2 * BITS * i;
+                const uint32_t *kb = c.kcodes + (int64_t)t * c.QW * 32;
+                const int wq = kvh * 4 * BITS + (bit >> 5);
+                unsigned long long w64 = __ldg(kb + wq * 32 + j);
+                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)__ldg(kb + (wq + 1) * 32 + j) << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                const float2 ab = hlut[(g * HMAX + slot) * NE + pc];
+                const float2 cs = cis_s[i * 32 + j];
+                atomicAdd(&kcorr[g * 32 + j], cs.x * ab.x + cs.y * ab.y);
             }
         }
         __syncthreads();
@@ -427,7 +478,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             const int j = slot + st * SLOTS;
             if (j < 32) {
                 const uint16_t w = w16[vh * 32 + j];
-                unsigned long long lo64 = vw[st][0] | ((unsigned long long)(BITS > 1 ? vw[st][1] : 0u) << 32);
 #pragma unroll
                 for (int pp = 0; pp < 16; ++pp) {
                     const int bit = 2 * BITS * pp;
@@ -441,7 +491,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                         if (sh + 6 <= 32) pc = (vw[st][wi] >> sh) & 63u;
                         else pc = (uint32_t)((((unsigned long long)vw[st][wi + 1] << 32) | vw[st][wi]) >> sh) & 63u;
                     }
-                    (void)lo64;
                     const uint32_t cv = vlut[pc * 32 + lane];
                     fma_w_f16x2(w, cv, acc[2 * pp], acc[2 * pp + 1]);
                 }
@@ -500,13 +549,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // ------------------------------------------------------------ write partial
     if (warp < HG && lane == 0) { m_fin[warp] = m_run; l_fin[warp] = l_run; z_fin[warp] = z_run; }
     {
+        // dense P.V accumulators are in units of 2^-E_cur; threads whose slot had no
+        // token (HG == 1) hold zeros.
         const float sc = ldexpf(1.f, E_cur);
-        if (slot < 32 || VSTEPS > 1) {
-            float *dst = osp + vh * kHeadDim + qq * 32;
-            if (slot * 1 < 32)
+        float *dst = osp + vh * kHeadDim + qq * 32;
 #pragma unroll
-                for (int x = 0; x < 32; ++x) atomicAdd(&dst[x], acc[x] * sc);
-        }
+        for (int x = 0; x < 32; ++x) atomicAdd(&dst[x], acc[x] * sc);
     }
     __syncthreads();
     float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
