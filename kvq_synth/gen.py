@@ -86,11 +86,14 @@ def gen_queries(seed: int, layer: int, H_q: int, H_kv: int, d: int, n: int = 1) 
 
 
 # ---------------------------------------------------------------- GPU generator ---
-def gen_layer_torch(seed: int, layer: int, T: int, D: int, device, which: str):
-    """Large-config generator on the GPU (bench only).  Same recipe, torch RNG."""
+def gen_layer_torch(seed: int, layer: int, T: int, D: int, device, which: str,
+                    param_seed: int = 0, param_layer: int = 0):
+    """Large-config generator on the GPU (bench only).  Same recipe, torch RNG; the
+    per-channel Key statistics come from (param_seed, param_layer) so they match the
+    calibration tokens of that layer."""
     import torch
 
-    mu, sigma = key_channel_params(seed, layer, D)
+    mu, sigma = key_channel_params(param_seed, param_layer, D)
     gen = torch.Generator(device=device)
     gen.manual_seed((seed * 1000003 + layer * 7919 + (1 if which == "K" else 2)) & 0x7FFFFFFFFFFF)
     out = torch.empty((T, D), dtype=torch.float16, device=device)

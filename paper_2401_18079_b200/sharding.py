@@ -51,9 +51,10 @@ def gather_partials(part, group=None):
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    out = torch.empty((world,) + tuple(part.shape), dtype=part.dtype, device=part.device)
+    out = torch.empty((world * part.shape[0],) + tuple(part.shape[1:]), dtype=part.dtype,
+                      device=part.device)
     dist.all_gather_into_tensor(out, part.contiguous(), group=group)
-    return out
+    return out.view((world,) + tuple(part.shape))
 
 
 def gather_merge(part, out, group=None, stream=None):
