@@ -177,7 +177,7 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     A(&d.vcodes, (size_t)d.cap * d.VW * 4 + 16);
     A(&d.vsz, (size_t)d.cap * sizeof(float2));
     A(&d.vout, (size_t)d.cap * (kv > 0 ? kv : 1) * 4);
-    A(&d.kptr, (size_t)(d.cap + 1) * 4);
+    A(&d.kptr, (size_t)(d.cap + 64) * 4);   // +63: attend stages 48-word CSC slices
     A(&d.kout, (size_t)d.kcap * 4 + 16);
     A(&d.kpar, (size_t)4 * D * 4);
     A(&d.cb, 64 * 4);

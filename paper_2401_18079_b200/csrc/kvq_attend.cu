@@ -2,6 +2,11 @@
 //
 // One launch per attend:
 //   grid  = n_head_groups x splits (head group fastest), 256 threads, 1 CTA / SM.
+//   Staging: every 32-token tile of the CTA's head group (K code words, V code words,
+//          per-token (s,z), CSC pointers, Value and Key outlier records) is moved
+//          global -> shared by TMA bulk copies (cp.async.bulk + mbarrier complete_tx)
+//          into a STAGES-deep ring, issued STAGES-1 tiles ahead by warp 0, so the compute
+//          phases never wait on HBM latency.
 //   a1 QP  each CTA rotates its HG query heads with exact fp64 angles (R11, R12) and
 //          folds 1/sqrt(d) * log2(e) into q~.
 //   LUTs   K: per (query head g, RoPE pair i) a 2^{2b}-entry table of fp16 pairs
@@ -10,13 +15,13 @@
 //          taken one step further: the query and the per-channel affine are folded in, so
 //          one lookup + 2 FMAs per RoPE pair yields  cos(n'th_i) A + sin(n'th_i) B, which
 //          is exactly the pair's contribution to q~ . RoPE(K^_n, n').
-//          V: the shared codebook, lane-private copies (conflict-free).
-//   a2 KS  lane = token of a 32-token tile, warp w = RoPE pairs 8w..8w+7 for all heads;
-//          fp32 accumulation of fp16 products (fma.rn.f32.f16).
-//   a3     Key outliers of the tile add  (x - K^(code)) * dscore/dK  (same launch).
+//          Pairs carrying a heavy Key channel get fp32 tables (precision, DESIGN 9).
+//          V: the shared codebook as a pair table, lane-private copies (conflict-free).
+//   a2 KS  lane = token of the tile, warp w = RoPE pairs 8w..8w+7 for all heads;
+//          fp16 x fp16 -> fp32 FMAs (fma.rn.f32.f16).
+//   a3     Key outliers of the tile add (x - K^(code)) * dscore/dK (same launch).
 //   a4     exact online softmax in base 2 (running max, rescale on change).
-//   a5 PV  lane = 32 channels, V^ = s_n Chat_V[code] + z_n folded as
-//          sum_n (p_n s_n) Chat_V[code] + sum_n p_n z_n  (affine fold).
+//   a5 PV  lane = CPL channels:  sum_n (p_n s_n) Chat_V[code] + sum_n p_n z_n  (affine fold).
 //   a6     Value outliers add p_n (v - V^(code)).
 //   a7 MRG the last CTA of each head group merges the split partials (log-sum-exp).
 #include "kvq_internal.cuh"
@@ -28,6 +33,42 @@ namespace {
 
 constexpr int ATT_THREADS = 256;
 constexpr int ATT_WARPS = 8;
+
+// ------------------------------------------------------------------ PTX helpers --
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 
 // acc += lo(x)*lo(y) ; acc2 += hi(x)*hi(y)   (fp16 products, fp32 accumulation)
 __device__ __forceinline__ void fma2_f16_f32(uint32_t x, uint32_t y, float &acc, float &acc2) {
@@ -66,6 +107,39 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// ---------------------------------------------------------------- configuration --
+constexpr int cpl_for(int bits, int hg) {
+    // channels per lane in the V phase: smallest of {8,16,32} with whole words per lane
+    // and at most 32 lanes per token
+    return (bits == 4 && hg * 128 / 8 <= 32) ? 8
+           : ((bits == 4 || bits == 2) && hg * 128 / 16 <= 32) ? 16
+                                                                : 32;
+}
+
+template <int BITS, int HG>
+struct Cfg {
+    static constexpr int NE = 1 << (2 * BITS);
+    static constexpr int HMAX = BITS == 4 ? 4 : 8;   // fp32 "heavy" pairs per head
+    static constexpr int CPL = cpl_for(BITS, HG);
+    static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
+    static constexpr size_t vlut = (size_t)NE * 32 * 4;
+    static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
+    static constexpr size_t cis = (size_t)kPairs * 32 * 8;
+    static constexpr size_t small =
+        HG * kHeadDim * 4              /* qs */
+        + ATT_WARPS * HG * 32 * 4      /* red */
+        + HG * 32 * 4 * 2              /* p, kcorr */
+        + HG * 32 * 2                  /* w16 */
+        + HG * kHeadDim * 4            /* osp */
+        + 64 * 16 * 3 + 64 * 8         /* anc64, rot64, qcis, anc32 */
+        + 64 * 4                       /* theta32 */
+        + HG * 4 * 8                   /* per-head scalars */
+        + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
+        + HG * 16 * 4                  /* heavy pair list + counts */
+        + 256;
+    static constexpr size_t fixed = klut + vlut + hlut + cis + small;
+};
+
 struct Params {
     const __half *q;
     int64_t pos, T;
@@ -75,48 +149,33 @@ struct Params {
     float *parts;
     unsigned *tickets;
     int write_partial;
-};
-
-template <int BITS, int HG>
-struct Smem {
-    static constexpr int NE = 1 << (2 * BITS);
-    static constexpr int HMAX = BITS == 4 ? 4 : 8;   // fp32 "heavy" pairs per head
-    static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
-    static constexpr size_t vlut = (size_t)NE * 32 * 4;
-    static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
-    static constexpr size_t cis = (size_t)kPairs * 32 * 8;
-    static constexpr size_t fixed =
-        HG * kHeadDim * 4              /* qs */
-        + ATT_WARPS * HG * 32 * 4      /* red */
-        + HG * 32 * 4 * 2              /* p, kcorr */
-        + HG * 32 * 2                  /* w16 */
-        + HG * kHeadDim * 4            /* osp */
-        + 64 * 16 + 64 * 8 + 64 * 16   /* anc64, anc32, rot64 */
-        + 64 * 4                       /* theta32 */
-        + 40 * 4 + 32 * 8              /* kptr slice, vsz slice */
-        + HG * 4 * 8                   /* per-head scalars */
-        + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
-        + HG * 16 * 4                  /* heavy pair list + counts */
-        + 64;
-    static constexpr size_t total = klut + vlut + hlut + cis + fixed + 128;
+    // stage ring layout (bytes), computed on the host
+    int stages;
+    int krec_cap;        // u32 records per stage buffer (multiple of 4)
+    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kptr, so_vrec, so_krec;
 };
 
 template <int BITS, int HG, int G>
 __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params P) {
-    constexpr int NE = 1 << (2 * BITS);
+    using C = Cfg<BITS, HG>;
+    constexpr int NE = C::NE;
     constexpr int CM = (1 << BITS) - 1;
     constexpr int HKV = HG / G;
-    constexpr int NWW = (BITS == 2) ? 1 : 2;      // K words per (lane, kv head, warp)
-    constexpr int LPT = 4 * HG;                     // V lanes per token
+    constexpr int QWC = HKV * 4 * BITS;             // K (and V) words per token in the CTA
+    constexpr int NWW = (BITS == 2) ? 1 : 2;        // K words per (lane, kv head, warp)
+    constexpr int CPL = C::CPL;                     // V channels per lane
+    constexpr int VWL = CPL * BITS / 32;            // V words per lane per token
+    constexpr int LPT = HG * kHeadDim / CPL;        // V lanes per token
     constexpr int SLOTS = ATT_THREADS / LPT;        // tokens per V step
     constexpr int VSTEPS = (32 + SLOTS - 1) / SLOTS;
+    constexpr int HMAX = C::HMAX;
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sp = smem_raw;
-    uint32_t *klut = reinterpret_cast<uint32_t *>(sp); sp += Smem<BITS, HG>::klut;
-    uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += Smem<BITS, HG>::vlut;
-    float2 *hlut = reinterpret_cast<float2 *>(sp); sp += Smem<BITS, HG>::hlut;
-    float2 *cis_s = reinterpret_cast<float2 *>(sp); sp += Smem<BITS, HG>::cis;
+    uint32_t *klut = reinterpret_cast<uint32_t *>(sp); sp += C::klut;
+    uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
+    float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
+    float2 *cis_s = reinterpret_cast<float2 *>(sp); sp += C::cis;
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *red = reinterpret_cast<float *>(sp); sp += ATT_WARPS * HG * 32 * 4;
     float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
@@ -124,10 +183,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *osp = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
     double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
     float2 *anc32 = reinterpret_cast<float2 *>(sp); sp += 64 * 8;
     float *theta32 = reinterpret_cast<float *>(sp); sp += 64 * 4;
-    float2 *vsz_s = reinterpret_cast<float2 *>(sp); sp += 32 * 8;
-    uint32_t *kptr_s = reinterpret_cast<uint32_t *>(sp); sp += 40 * 4;
     float *lut_inv = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *alpha_s = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *beta_s = reinterpret_cast<float *>(sp); sp += HG * 4;
@@ -135,12 +193,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *l_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *z_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
     uint16_t *w16 = reinterpret_cast<uint16_t *>(sp); sp += HG * 32 * 2;
-    int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
     float *bound_s = reinterpret_cast<float *>(sp); sp += HG * 64 * 4;
     uint8_t *heavy_s = reinterpret_cast<uint8_t *>(sp); sp += HG * 64;
     int *hv_pair = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
     int *hv_n = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
-    constexpr int HMAX = Smem<BITS, HG>::HMAX;
+    int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 64);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
@@ -151,11 +209,62 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     const int t_begin = (int)((int64_t)split * P.ntiles / P.S);
     const int t_end = (int)((int64_t)(split + 1) * P.ntiles / P.S);
     const int D = c.D;
+    const int kv = c.kv;
     const float *ks = c.kpar, *kz = c.kpar + D;
     const float *cbK = c.cb + 16, *cbV = c.cb + 48;   // decode codebooks
 
+    auto stage_ptr = [&](int st) -> unsigned char * { return smem_raw + P.st_base + (size_t)st * P.st_bytes; };
+
+    // ----------------------------------------------------------- TMA producer
+    // kp_lo/kp_hi: CSC pointers of the next tile to issue (prefetched one issue ahead)
+    uint32_t kp_lo = 0, kp_hi = 0;
+    auto kptr_at = [&](int t, uint32_t &lo, uint32_t &hi) {
+        const int64_t n0 = (int64_t)t * 32;
+        const int64_t n1 = n0 + 32 < P.T ? n0 + 32 : P.T;
+        lo = __ldg(c.kptr + n0);
+        hi = __ldg(c.kptr + n1);
+    };
+    auto issue = [&](int t, int st) {   // warp 0 only
+        if (t >= t_end) return;
+        unsigned char *sb = stage_ptr(st);
+        uint64_t *bar = bars + st;
+        const uint32_t klo = __shfl_sync(0xffffffffu, kp_lo, 0);
+        const uint32_t khi = __shfl_sync(0xffffffffu, kp_hi, 0);
+        const uint32_t ka = klo & ~3u;
+        uint32_t kn = ((khi + 3u) & ~3u) - ka;
+        if (kn > (uint32_t)P.krec_cap) kn = (uint32_t)P.krec_cap;
+        const unsigned b_kw = 32u * QWC * 4u;
+        const unsigned b_row = QWC * 4u;
+        const unsigned b_vrec = 32u * (unsigned)kv * 4u;
+        const unsigned total = b_kw + 32u * b_row + 256u + 192u + b_vrec + kn * 4u;
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(bar, total);
+        }
+        __syncwarp();
+        const int64_t n0 = (int64_t)t * 32;
+        if (lane == 0)
+            bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)t * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
+        if (lane == 1) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
+        if (lane == 2) bulk_g2s(sb + P.so_kptr, c.kptr + n0, 192u, bar);
+        if (lane == 3 && b_vrec) bulk_g2s(sb + P.so_vrec, c.vout + n0 * kv, b_vrec, bar);
+        if (lane == 4 && kn) bulk_g2s(sb + P.so_krec, c.kout + ka, kn * 4u, bar);
+        bulk_g2s(sb + P.so_vw + lane * b_row, c.vcodes + (n0 + lane) * c.VW + h0 * 4 * BITS, b_row, bar);
+        // prefetch the CSC range of the tile after this one
+        if (lane == 0 && t + 1 < t_end) kptr_at(t + 1, kp_lo, kp_hi);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < P.stages; ++s) mbar_init(bars + s, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0 && t_begin < t_end) kptr_at(t_begin, kp_lo, kp_hi);
+        for (int s = 0; s < P.stages - 1; ++s) issue(t_begin + s, s);
+    }
+
     // ---------------------------------------------------------------- prologue
-    __shared__ double2 qcis[64];
     if (tid < 64) {
         const int i = tid;
         const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
@@ -185,10 +294,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         qs[g * kHeadDim + i + 64] = (float)((b * cs.x + a * cs.y) * qscale);
     }
     __syncthreads();
-    // K LUT: per (head, pair) bound of |A|,|B|.  The few pairs carrying a heavy Key
+    // K tables: per (head, pair) bound of |A|,|B|.  The few pairs carrying a heavy Key
     // channel (bound > 1/4 of the head max, at most HMAX per head) get fp32 tables and
-    // are accumulated exactly in fp32 (a3'); the rest use fp16 tables whose scale is set
-    // by the largest remaining bound.
+    // are accumulated in fp32; the rest use fp16 tables scaled by the largest remaining
+    // bound.
     for (int x = tid; x < HG * 64; x += ATT_THREADS) {
         const int g = x >> 6, i = x & 63;
         const int kvh = (g0 + g) / G;
@@ -199,8 +308,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         bound_s[x] = fmaxf(qa * mx + qb * my, qb * mx + qa * my);
     }
     __syncthreads();
-    if (warp < HG) {
-        const float b0 = bound_s[warp * 64 + lane], b1 = bound_s[warp * 64 + 32 + lane];
+    for (int g = warp; g < HG; g += ATT_WARPS) {
+        const float b0 = bound_s[g * 64 + lane], b1 = bound_s[g * 64 + 32 + lane];
         const float M = warp_max(fmaxf(b0, b1));
         float tau = 0.25f * M;
         unsigned m0 = __ballot_sync(0xffffffffu, b0 > tau), m1 = __ballot_sync(0xffffffffu, b1 > tau);
@@ -211,29 +320,29 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         }
         const unsigned lt = (1u << lane) - 1u;
         const int n0c = __popc(m0);
-        if ((m0 >> lane) & 1u) hv_pair[warp * 8 + __popc(m0 & lt)] = lane;
-        if ((m1 >> lane) & 1u) hv_pair[warp * 8 + n0c + __popc(m1 & lt)] = lane + 32;
-        heavy_s[warp * 64 + lane] = (m0 >> lane) & 1u;
-        heavy_s[warp * 64 + 32 + lane] = (m1 >> lane) & 1u;
+        if ((m0 >> lane) & 1u) hv_pair[g * 8 + __popc(m0 & lt)] = lane;
+        if ((m1 >> lane) & 1u) hv_pair[g * 8 + n0c + __popc(m1 & lt)] = lane + 32;
+        heavy_s[g * 64 + lane] = (m0 >> lane) & 1u;
+        heavy_s[g * 64 + 32 + lane] = (m1 >> lane) & 1u;
         const float rest = warp_max(fmaxf(((m0 >> lane) & 1u) ? 0.f : b0, ((m1 >> lane) & 1u) ? 0.f : b1));
         if (lane == 0) {
-            hv_n[warp] = n0c + __popc(m1);
-            // scale so that |entry| <= 2^14 (fp16 max 65504)
-            int e = 0;
+            hv_n[g] = n0c + __popc(m1);
+            int e = 0;     // scale so that |entry| <= 2^14 (fp16 max 65504)
             if (rest > 0.f && isfinite(rest)) e = 14 - ilogbf(rest) - 1;
             e = max(-100, min(100, e));
-            alpha_s[warp] = ldexpf(1.f, e);      // temp: LUT scale
-            lut_inv[warp] = ldexpf(1.f, -e);
+            alpha_s[g] = ldexpf(1.f, e);      // temp: table scale
+            lut_inv[g] = ldexpf(1.f, -e);
         }
     }
     __syncthreads();
-    // K LUT entries
+    // K table entries
     for (int x = tid; x < HG * 64; x += ATT_THREADS) {
         const int g = x >> 6, i = x & 63;
         const int kvh = (g0 + g) / G;
         const int ci = kvh * kHeadDim + i, cj = ci + 64;
         const float sc = alpha_s[g];
-        const float qa = qs[g * kHeadDim + i] * sc, qb = qs[g * kHeadDim + i + 64] * sc;
+        const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
+        const float qa = qa1 * sc, qb = qb1 * sc;
         float X[1 << BITS], Y[1 << BITS];
 #pragma unroll
         for (int a = 0; a <= CM; ++a) {
@@ -242,27 +351,27 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         }
         uint32_t *dst = klut + (size_t)(g * 64 + i) * NE;
         const bool heavy = heavy_s[x] != 0;
-        int hslot = -1;
+        int hslot = 0;
         if (heavy)
             for (int u = 0; u < hv_n[g]; ++u) hslot = hv_pair[g * 8 + u] == i ? u : hslot;
-        const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
-        for (int e0 = 0; e0 < NE; ++e0) {
-            const int e = (e0 + lane) & (NE - 1);
-            const int a = e & CM, bb = e >> BITS;
-            float xa = 0.f, yb = 0.f;
+#pragma unroll 1
+        for (int bb = 0; bb <= CM; ++bb) {
+            float yb = 0.f;
 #pragma unroll
-            for (int u = 0; u <= CM; ++u) { xa = (u == a) ? X[u] : xa; yb = (u == bb) ? Y[u] : yb; }
-            if (heavy) {
-                dst[e] = 0u;
-                hlut[(g * HMAX + hslot) * NE + e] = make_float2(qa1 * xa + qb1 * yb, qb1 * xa - qa1 * yb);
-            } else {
-                const float A = qa * xa + qb * yb;
-                const float B = qb * xa - qa * yb;
-                dst[e] = pack_half2(A, B);
+            for (int u = 0; u <= CM; ++u) yb = (u == bb) ? Y[u] : yb;
+#pragma unroll
+            for (int a = 0; a <= CM; ++a) {
+                const int e = a | (bb << BITS);
+                if (heavy) {
+                    dst[e] = 0u;
+                    hlut[(g * HMAX + hslot) * NE + e] = make_float2(qa1 * X[a] + qb1 * yb, qb1 * X[a] - qa1 * yb);
+                } else {
+                    dst[e] = pack_half2(qa * X[a] + qb * yb, qb * X[a] - qa * yb);
+                }
             }
         }
     }
-    // V LUT: lane-private copies (entry e for lane slot l at word e*32 + l)
+    // V table: lane-private copies (entry e for lane slot l at word e*32 + l)
     for (int x = tid; x < NE * 32; x += ATT_THREADS) {
         const int e = x >> 5;
         vlut[x] = pack_half2(cbV[e & CM], cbV[e >> BITS]);
@@ -282,62 +391,35 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 
     // V-phase mapping
     const int cg = tid % LPT, slot = tid / LPT;
-    const int vh = cg >> 2, qq = cg & 3;             // local query head, quarter
-    const int vkvh = (g0 + vh) / G;                  // global kv head for V
-    const int vword0 = (vkvh * 4 + qq) * BITS;       // first word of the lane's 32 channels
-    float acc[32];
+    const int vh = cg / (kHeadDim / CPL);                    // local query head
+    const int vq = cg % (kHeadDim / CPL);                    // CPL-channel group in the head
+    const int vw0 = ((vh / G) * kHeadDim + vq * CPL) * BITS / 32;   // first word within a row
+    float acc[CPL];
 #pragma unroll
-    for (int x = 0; x < 32; ++x) acc[x] = 0.f;
+    for (int x = 0; x < CPL; ++x) acc[x] = 0.f;
 
     // running softmax state (S-phase warps: warp g <-> head g)
     float m_run = -CUDART_INF_F, l_run = 0.f, z_run = 0.f;
     int E_cur = -126;     // dense V accumulator units: 2^E_cur
 
-    // K-phase word window
     const int kbit0 = 16 * BITS * warp;
     const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
-
-    uint32_t kw[HKV][NWW], vw[VSTEPS][BITS];
-    uint32_t kptr_next = 0;
-    float2 vsz_next = make_float2(0.f, 0.f);
-
-    auto load_tile = [&](int t, uint32_t (&kwo)[HKV][NWW], uint32_t (&vwo)[VSTEPS][BITS]) {
-        const uint32_t *kb = c.kcodes + (int64_t)t * c.QW * 32;
-#pragma unroll
-        for (int h = 0; h < HKV; ++h)
-#pragma unroll
-            for (int x = 0; x < NWW; ++x)
-                kwo[h][x] = __ldg(kb + ((h0 + h) * 4 * BITS + kq0 + x) * 32 + lane);
-#pragma unroll
-        for (int st = 0; st < VSTEPS; ++st) {
-            const int j = slot + st * SLOTS;
-            const int64_t n = (int64_t)t * 32 + (j < 32 ? j : 0);
-            const uint32_t *vb = c.vcodes + n * c.VW + vword0;
-#pragma unroll
-            for (int x = 0; x < BITS; ++x) vwo[st][x] = (j < 32) ? __ldg(vb + x) : 0u;
-        }
-        if (tid < 33) {
-            int64_t n = (int64_t)t * 32 + tid;
-            if (n > P.T) n = P.T;
-            kptr_next = __ldg(c.kptr + n);
-        }
-        if (tid >= 64 && tid < 96) {
-            int64_t n = (int64_t)t * 32 + (tid - 64);
-            vsz_next = n < P.T ? __ldg(c.vsz + n) : make_float2(0.f, 0.f);
-        }
-    };
-
-    if (t_begin < t_end) load_tile(t_begin, kw, vw);
     __syncthreads();
 
     for (int t = t_begin; t < t_end; ++t) {
+        const int it = t - t_begin;
+        const int st = it % P.stages;
+        if (warp == 0) issue(t + P.stages - 1, (it + P.stages - 1) % P.stages);
+        mbar_wait(bars + st, (unsigned)((it / P.stages) & 1));
+        unsigned char *sb = stage_ptr(st);
+        const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
+        const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
+        const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
+        const uint32_t *kptr_s = reinterpret_cast<const uint32_t *>(sb + P.so_kptr);
+        const uint32_t *vrec_s = reinterpret_cast<const uint32_t *>(sb + P.so_vrec);
+        const uint32_t *krec_s = reinterpret_cast<const uint32_t *>(sb + P.so_krec);
         const int64_t n0 = (int64_t)t * 32;
         const int ntok = (int)min((int64_t)32, P.T - n0);
-        // publish this tile's small arrays, then prefetch the next tile
-        if (tid < 33) kptr_s[tid] = kptr_next;
-        if (tid >= 64 && tid < 96) vsz_s[tid - 64] = vsz_next;
-        uint32_t kwn[HKV][NWW], vwn[VSTEPS][BITS];
-        if (t + 1 < t_end) load_tile(t + 1, kwn, vwn);
 
         // ------------------------------------------------------------ a2: K dense
         {
@@ -347,8 +429,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             unsigned long long win[HKV];
 #pragma unroll
             for (int h = 0; h < HKV; ++h) {
-                unsigned long long w64 = kw[h][0];
-                if (NWW == 2) w64 |= (unsigned long long)kw[h][NWW - 1] << 32;
+                unsigned long long w64 = kw_s[(h * 4 * BITS + kq0) * 32 + lane];
+                if (NWW == 2) w64 |= (unsigned long long)kw_s[(h * 4 * BITS + kq0 + 1) * 32 + lane] << 32;
                 win[h] = w64 >> kshift;
             }
 #pragma unroll
@@ -375,51 +457,48 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         }
         __syncthreads();
 
-        // ----------------------------------------------------- a3: K outliers
+        // ------------------------------------------- a3: K outliers, heavy pairs
         {
-            const uint32_t r0 = kptr_s[0], r1 = kptr_s[ntok];
-            for (uint32_t r = r0 + tid; r < r1; r += ATT_THREADS) {
-                // token of record r: largest j with kptr_s[j] <= r
-                int lo = 0, hi = ntok - 1;
-                while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (kptr_s[mid] <= r) lo = mid; else hi = mid - 1; }
-                const int j = lo;
-                const uint32_t rec = __ldg(c.kout + r);
-                const int ch = (int)(rec & 0xffffu);
-                const int kvh = ch >> 7;
-                if (kvh < h0 || kvh >= h0 + HKV) continue;
-                const int cc = ch & 127, i = cc & 63, up = cc >> 6;
-                const int bit = 2 * BITS * i;
-                const uint32_t *kb = c.kcodes + (int64_t)t * c.QW * 32;
-                const int wq = kvh * 4 * BITS + (bit >> 5);
-                unsigned long long w64 = __ldg(kb + wq * 32 + j);
-                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)__ldg(kb + (wq + 1) * 32 + j) << 32;
-                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                const int code = (pc >> (up * BITS)) & CM;
-                const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
-                const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
-                const float2 cs = cis_s[i * 32 + j];
-                const float co = cs.x, si = cs.y;
+            const uint32_t kbase = kptr_s[0];
+            const uint32_t ka = kbase & ~3u;
+            for (int j = warp; j < ntok; j += ATT_WARPS) {
+                const uint32_t r0 = kptr_s[j], r1 = kptr_s[j + 1];
+                for (uint32_t r = r0 + lane; r < r1; r += 32) {
+                    const uint32_t off = r - ka;
+                    const uint32_t rec = off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
+                    const int ch = (int)(rec & 0xffffu);
+                    const int kvh = ch >> 7;
+                    if (kvh < h0 || kvh >= h0 + HKV) continue;
+                    const int cc = ch & 127, i = cc & 63, up = cc >> 6;
+                    const int bit = 2 * BITS * i;
+                    const int wq = (kvh - h0) * 4 * BITS + (bit >> 5);
+                    unsigned long long w64 = kw_s[wq * 32 + j];
+                    if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                    const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                    const int code = (pc >> (up * BITS)) & CM;
+                    const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
+                    const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
+                    const float2 cs = cis_s[i * 32 + j];
 #pragma unroll
-                for (int gg = 0; gg < G; ++gg) {
-                    const int g = (kvh - h0) * G + gg;
-                    const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
-                    const float d = up ? (qb * co - qa * si) : (qa * co + qb * si);
-                    atomicAdd(&kcorr[g * 32 + j], delta * d);
+                    for (int gg = 0; gg < G; ++gg) {
+                        const int g = (kvh - h0) * G + gg;
+                        const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
+                        const float d = up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y);
+                        atomicAdd(&kcorr[g * 32 + j], delta * d);
+                    }
                 }
             }
-            // a2': heavy RoPE pairs in fp32 (tables hlut; cis of the tile from the K phase)
+            // heavy RoPE pairs in fp32 (tables hlut; cis of the tile from the K phase)
             for (int x = tid; x < HG * 8 * 32; x += ATT_THREADS) {
-                const int g = x >> 8, slot = (x >> 5) & 7, j = x & 31;
-                if (slot >= hv_n[g] || j >= ntok) continue;
-                const int i = hv_pair[g * 8 + slot];
-                const int kvh = (g0 + g) / G;
+                const int g = x >> 8, hs = (x >> 5) & 7, j = x & 31;
+                if (hs >= hv_n[g] || j >= ntok) continue;
+                const int i = hv_pair[g * 8 + hs];
                 const int bit = 2 * BITS * i;
-                const uint32_t *kb = c.kcodes + (int64_t)t * c.QW * 32;
-                const int wq = kvh * 4 * BITS + (bit >> 5);
-                unsigned long long w64 = __ldg(kb + wq * 32 + j);
-                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)__ldg(kb + (wq + 1) * 32 + j) << 32;
+                const int wq = (g / G) * 4 * BITS + (bit >> 5);
+                unsigned long long w64 = kw_s[wq * 32 + j];
+                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
                 const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                const float2 ab = hlut[(g * HMAX + slot) * NE + pc];
+                const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
                 const float2 cs = cis_s[i * 32 + j];
                 atomicAdd(&kcorr[g * 32 + j], cs.x * ab.x + cs.y * ab.y);
             }
@@ -433,8 +512,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             smax = warp_max(smax);
             int E_new = E_cur;
             if (smax > 0.f) E_new = max(E_cur, ilogbf(smax) + 1);
-            if (warp < HG) {
-                const int g = warp;
+            for (int g = warp; g < HG; g += ATT_WARPS) {
                 float s = 0.f;
 #pragma unroll
                 for (int w = 0; w < ATT_WARPS; ++w) s += red[(w * HG + g) * 32 + lane];
@@ -446,7 +524,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const float m_new = fmaxf(m_run, mt);
                 const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
                 const float p = valid ? exp2f(s - m_new) : 0.f;
-                const float2 sz = vsz_s[lane];
+                const float2 sz = valid ? vsz_s[lane] : make_float2(0.f, 0.f);
                 l_run = l_run * alpha + warp_sum(p);
                 z_run = z_run * alpha + warp_sum(p * sz.y);
                 m_run = m_new;
@@ -469,28 +547,25 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             const float b = beta_s[vh];
             if (b != 1.f) {
 #pragma unroll
-                for (int x = 0; x < 32; ++x) acc[x] *= b;
+                for (int x = 0; x < CPL; ++x) acc[x] *= b;
             }
             for (int x = tid; x < HG * kHeadDim; x += ATT_THREADS) osp[x] *= alpha_s[x >> 7];
         }
 #pragma unroll
-        for (int st = 0; st < VSTEPS; ++st) {
-            const int j = slot + st * SLOTS;
+        for (int vs = 0; vs < VSTEPS; ++vs) {
+            const int j = slot + vs * SLOTS;
             if (j < 32) {
                 const uint16_t w = w16[vh * 32 + j];
+                uint32_t vw[VWL];
 #pragma unroll
-                for (int pp = 0; pp < 16; ++pp) {
+                for (int x = 0; x < VWL; ++x) vw[x] = vw_s[j * QWC + vw0 + x];
+#pragma unroll
+                for (int pp = 0; pp < CPL / 2; ++pp) {
                     const int bit = 2 * BITS * pp;
+                    const int wi = bit >> 5, sh = bit & 31;
                     uint32_t pc;
-                    if (BITS == 2) {
-                        pc = (vw[st][bit >> 5] >> (bit & 31)) & (NE - 1);
-                    } else if (BITS == 4) {
-                        pc = (vw[st][bit >> 5] >> (bit & 31)) & (NE - 1);
-                    } else {  // 3 bits: 96-bit group, pairs straddle word boundaries
-                        const int wi = bit >> 5, sh = bit & 31;
-                        if (sh + 6 <= 32) pc = (vw[st][wi] >> sh) & 63u;
-                        else pc = (uint32_t)((((unsigned long long)vw[st][wi + 1] << 32) | vw[st][wi]) >> sh) & 63u;
-                    }
+                    if (sh + 2 * BITS <= 32) pc = (vw[wi] >> sh) & (NE - 1);
+                    else pc = (uint32_t)((((unsigned long long)vw[wi + 1] << 32) | vw[wi]) >> sh) & (NE - 1);
                     const uint32_t cv = vlut[pc * 32 + lane];
                     fma_w_f16x2(w, cv, acc[2 * pp], acc[2 * pp + 1]);
                 }
@@ -502,20 +577,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         }
 
         // ---------------------------------------------------- a6: V outliers
-        {
-            const int kv = c.kv;
-            const int nrec = ntok * kv;
-            const uint32_t *vo = c.vout + n0 * kv;
-            for (int r = tid; r < nrec; r += ATT_THREADS) {
-                const uint32_t rec = __ldg(vo + r);
+        for (int j = warp; j < ntok; j += ATT_WARPS) {
+            for (int r = lane; r < kv; r += 32) {
+                const uint32_t rec = vrec_s[j * kv + r];
                 const int ch = (int)(rec & 0xffffu);
                 const int kvh = ch >> 7;
                 if (kvh < h0 || kvh >= h0 + HKV) continue;
-                const int j = r / kv;
-                const int bit = BITS * ch;
-                const uint32_t *vrow = c.vcodes + (n0 + j) * c.VW;
-                unsigned long long w64 = __ldg(vrow + (bit >> 5));
-                if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)__ldg(vrow + (bit >> 5) + 1) << 32;
+                const int bit = BITS * (ch - h0 * kHeadDim);
+                const uint32_t *vrow = vw_s + j * QWC;
+                unsigned long long w64 = vrow[bit >> 5];
+                if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vrow[(bit >> 5) + 1] << 32;
                 const int code = (int)((w64 >> (bit & 31)) & CM);
                 const float2 sz = vsz_s[j];
                 const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
@@ -535,26 +606,17 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             anc64[tid] = b;
             anc32[tid] = make_float2((float)b.x, (float)b.y);
         }
-#pragma unroll
-        for (int h = 0; h < HKV; ++h)
-#pragma unroll
-            for (int x = 0; x < NWW; ++x) kw[h][x] = kwn[h][x];
-#pragma unroll
-        for (int st = 0; st < VSTEPS; ++st)
-#pragma unroll
-            for (int x = 0; x < BITS; ++x) vw[st][x] = vwn[st][x];
         __syncthreads();
     }
 
     // ------------------------------------------------------------ write partial
-    if (warp < HG && lane == 0) { m_fin[warp] = m_run; l_fin[warp] = l_run; z_fin[warp] = z_run; }
+    for (int g = warp; g < HG; g += ATT_WARPS)
+        if (lane == 0) { m_fin[g] = m_run; l_fin[g] = l_run; z_fin[g] = z_run; }
     {
-        // dense P.V accumulators are in units of 2^-E_cur; threads whose slot had no
-        // token (HG == 1) hold zeros.
         const float sc = ldexpf(1.f, E_cur);
-        float *dst = osp + vh * kHeadDim + qq * 32;
+        float *dst = osp + vh * kHeadDim + vq * CPL;
 #pragma unroll
-        for (int x = 0; x < 32; ++x) atomicAdd(&dst[x], acc[x] * sc);
+        for (int x = 0; x < CPL; ++x) atomicAdd(&dst[x], acc[x] * sc);
     }
     __syncthreads();
     float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
@@ -569,13 +631,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // ------------------------------------------------------- a7: split merge
     __threadfence();
     __syncthreads();
-    __shared__ int s_last;
+    int *s_last = flag_s + 1;
     if (tid == 0) {
         const unsigned prev = atomicAdd(&P.tickets[hg], 1u);
-        s_last = (prev == (unsigned)(P.S - 1));
+        *s_last = (prev == (unsigned)(P.S - 1));
     }
     __syncthreads();
-    if (!s_last) return;
+    if (!*s_last) return;
     __threadfence();
     for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
         const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
@@ -593,7 +655,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             if (ch < kHeadDim) o += wgt * __ldcg(ps + ch);
         }
         if (P.write_partial) {
-            float v = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
+            const float v = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
             P.out[gq * (kHeadDim + 2) + ch] = v;
         } else if (ch < kHeadDim) {
             P.out[gq * kHeadDim + ch] = o / l;
@@ -619,9 +681,42 @@ __global__ void merge_kernel(const float *__restrict__ parts, int Pn, int H, int
     o[x] = acc / l;
 }
 
+constexpr size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
+
+template <int BITS, int HG>
+size_t layout(const DevCache &c, Params &P) {
+    using C = Cfg<BITS, HG>;
+    const int HKV = HG / c.G;
+    const size_t qwc = (size_t)HKV * 4 * BITS;
+    size_t off = 0;
+    P.so_kw = (unsigned)off; off = align128(off + 32 * qwc * 4);
+    P.so_vw = (unsigned)off; off = align128(off + 32 * qwc * 4);
+    P.so_vsz = (unsigned)off; off = align128(off + 256);
+    P.so_kptr = (unsigned)off; off = align128(off + 192);
+    P.so_vrec = (unsigned)off; off = align128(off + (size_t)32 * c.kv * 4);
+    P.so_krec = (unsigned)off;
+    const size_t limit = 227 * 1024;
+    const size_t base = align128(C::fixed + 64);
+    P.st_base = (unsigned)base;
+    for (int stages = 3; stages >= 2; --stages) {
+        for (int krec = 2048; krec >= 256; krec -= 256) {
+            const size_t stb = align128(off + (size_t)krec * 4);
+            const size_t total = base + stages * stb;
+            if (total <= limit) {
+                P.stages = stages;
+                P.krec_cap = krec;
+                P.st_bytes = (unsigned)stb;
+                return total;
+            }
+        }
+    }
+    return 0;
+}
+
 template <int BITS, int HG, int G>
-cudaError_t launch_t(const DevCache &c, const Params &P, int grid, cudaStream_t s) {
-    const size_t smem = Smem<BITS, HG>::total;
+cudaError_t launch_t(const DevCache &c, Params &P, int grid, cudaStream_t s) {
+    const size_t smem = layout<BITS, HG>(c, P);
+    if (smem == 0) return cudaErrorInvalidConfiguration;
     cudaError_t e = cudaFuncSetAttribute(att_kernel<BITS, HG, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -630,7 +725,7 @@ cudaError_t launch_t(const DevCache &c, const Params &P, int grid, cudaStream_t 
 }
 
 template <int BITS, int HG>
-cudaError_t launch_g(const DevCache &c, const Params &P, int grid, cudaStream_t s) {
+cudaError_t launch_g(const DevCache &c, Params &P, int grid, cudaStream_t s) {
     switch (c.G) {
         case 1: return launch_t<BITS, HG, 1>(c, P, grid, s);
         case 2: if constexpr (HG >= 2) return launch_t<BITS, HG, 2>(c, P, grid, s); break;
@@ -641,12 +736,12 @@ cudaError_t launch_g(const DevCache &c, const Params &P, int grid, cudaStream_t 
 }
 
 template <int BITS>
-cudaError_t launch_b(const DevCache &c, const Params &P, int hg, int grid, cudaStream_t s) {
+cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_t s) {
     switch (hg) {
         case 1: return launch_g<BITS, 1>(c, P, grid, s);
-        case 2: return launch_g<BITS, 2>(c, P, grid, s);
+        case 2: if constexpr (BITS <= 3) return launch_g<BITS, 2>(c, P, grid, s); break;
         case 4: if constexpr (BITS <= 3) return launch_g<BITS, 4>(c, P, grid, s); break;
-        case 8: if constexpr (BITS <= 3) return launch_g<BITS, 8>(c, P, grid, s); break;
+        case 8: if constexpr (BITS <= 2) return launch_g<BITS, 8>(c, P, grid, s); break;
     }
     return cudaErrorInvalidValue;
 }
@@ -654,7 +749,7 @@ cudaError_t launch_b(const DevCache &c, const Params &P, int hg, int grid, cudaS
 }  // namespace
 
 int attend_heads_per_cta(int bits, int H_q, int G) {
-    const int cap = bits == 4 ? 2 : 8;
+    const int cap = bits == 4 ? 1 : (bits == 3 ? 4 : 8);
     for (int hg = cap; hg >= 1; hg >>= 1)
         if (H_q % hg == 0 && hg % G == 0) return hg;
     return 0;
@@ -662,16 +757,14 @@ int attend_heads_per_cta(int bits, int H_q, int G) {
 
 size_t attend_smem_bytes(int bits, int hg) {
     switch (bits * 100 + hg) {
-        case 201: return Smem<2, 1>::total;
-        case 202: return Smem<2, 2>::total;
-        case 204: return Smem<2, 4>::total;
-        case 208: return Smem<2, 8>::total;
-        case 301: return Smem<3, 1>::total;
-        case 302: return Smem<3, 2>::total;
-        case 304: return Smem<3, 4>::total;
-        case 308: return Smem<3, 8>::total;
-        case 401: return Smem<4, 1>::total;
-        case 402: return Smem<4, 2>::total;
+        case 201: return Cfg<2, 1>::fixed;
+        case 202: return Cfg<2, 2>::fixed;
+        case 204: return Cfg<2, 4>::fixed;
+        case 208: return Cfg<2, 8>::fixed;
+        case 301: return Cfg<3, 1>::fixed;
+        case 302: return Cfg<3, 2>::fixed;
+        case 304: return Cfg<3, 4>::fixed;
+        case 401: return Cfg<4, 1>::fixed;
     }
     return 0;
 }
@@ -695,7 +788,7 @@ cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_us
     int S = a.splits > 0 ? a.splits : attend_auto_splits(c, a.T, hg);
     if (S > ntiles) S = ntiles;
     if (S < 1) S = 1;
-    Params P;
+    Params P{};
     P.q = a.q; P.pos = a.pos; P.T = a.T; P.S = S; P.ntiles = ntiles;
     P.out = a.out; P.parts = a.parts; P.tickets = a.tickets; P.write_partial = a.write_partial;
     const int grid = (c.H_q / hg) * S;
