@@ -31,8 +31,9 @@
 namespace kvq {
 namespace {
 
-constexpr int ATT_THREADS = 256;
-constexpr int ATT_WARPS = 8;
+constexpr int ATT_THREADS = 512;
+constexpr int ATT_WARPS = 16;
+constexpr int KPW = kPairs / ATT_WARPS;   // RoPE pairs per warp in the K phase
 
 // ------------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -128,7 +129,7 @@ struct Cfg {
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
         + ATT_WARPS * HG * 32 * 4      /* red */
-        + HG * 32 * 4 * 2              /* p, kcorr */
+        + HG * 32 * 4 * 3              /* p, kcorr, hcorr */
         + HG * 32 * 2                  /* w16 */
         + HG * kHeadDim * 4            /* osp */
         + 64 * 16 * 3 + 64 * 8         /* anc64, rot64, qcis, anc32 */
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *red = reinterpret_cast<float *>(sp); sp += ATT_WARPS * HG * 32 * 4;
     float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
     float *kcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
+    float *hcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
     float *osp = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
     double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
@@ -377,11 +379,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         vlut[x] = pack_half2(cbV[e & CM], cbV[e >> BITS]);
     }
 
-    // per-lane constants for the K phase: cis(j * theta_i) for this warp's 8 pairs
-    float t1c[8], t1s[8];
+    // per-lane constants for the K phase: cis(j * theta_i) for this warp's KPW pairs
+    float t1c[KPW], t1s[KPW];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int i = warp * 8 + k;
+    for (int k = 0; k < KPW; ++k) {
+        const int i = warp * KPW + k;
         const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
         float s, co;
         sincosf((float)((double)lane * th), &s, &co);
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float m_run = -CUDART_INF_F, l_run = 0.f, z_run = 0.f;
     int E_cur = -126;     // dense V accumulator units: 2^E_cur
 
-    const int kbit0 = 16 * BITS * warp;
+    const int kbit0 = 2 * BITS * KPW * warp;
     const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
     __syncthreads();
 
@@ -430,12 +432,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
             for (int h = 0; h < HKV; ++h) {
                 unsigned long long w64 = kw_s[(h * 4 * BITS + kq0) * 32 + lane];
-                if (NWW == 2) w64 |= (unsigned long long)kw_s[(h * 4 * BITS + kq0 + 1) * 32 + lane] << 32;
+                if (kshift + 2 * BITS * KPW > 32)
+                    w64 |= (unsigned long long)kw_s[(h * 4 * BITS + kq0 + 1) * 32 + lane] << 32;
                 win[h] = w64 >> kshift;
             }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int i = warp * 8 + k;
+            for (int k = 0; k < KPW; ++k) {
+                const int i = warp * KPW + k;
                 const float2 an = anc32[i];
                 const float cc = an.x * t1c[k] - an.y * t1s[k];
                 const float ss = an.x * t1s[k] + an.y * t1c[k];
@@ -455,52 +458,75 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
             for (int g = 0; g < HG; ++g) red[(warp * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
         }
-        __syncthreads();
+        __syncwarp();   // this warp's cis_s rows are read by other warps after the barrier
 
-        // ------------------------------------------- a3: K outliers, heavy pairs
+        // ---------------------- a3: K outliers (warp per token, no atomics), heavy pairs
+        // Heavy pairs first (head g <-> warp g, lane = token): reads cis_s rows written by
+        // other warps, so it runs after the barrier below; the outliers need cis_s too.
+        __syncthreads();
         {
-            const uint32_t kbase = kptr_s[0];
-            const uint32_t ka = kbase & ~3u;
+            const uint32_t ka = kptr_s[0] & ~3u;
+            const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
             for (int j = warp; j < ntok; j += ATT_WARPS) {
                 const uint32_t r0 = kptr_s[j], r1 = kptr_s[j + 1];
-                for (uint32_t r = r0 + lane; r < r1; r += 32) {
-                    const uint32_t off = r - ka;
-                    const uint32_t rec = off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
+                float corr[HG];
+#pragma unroll
+                for (int g = 0; g < HG; ++g) corr[g] = 0.f;
+                for (uint32_t rb = r0; rb < r1; rb += 32) {
+                    const uint32_t r = rb + lane;
+                    uint32_t rec = 0xffffu;
+                    if (r < r1) {
+                        const uint32_t off = r - ka;
+                        rec = off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
+                    }
                     const int ch = (int)(rec & 0xffffu);
-                    const int kvh = ch >> 7;
-                    if (kvh < h0 || kvh >= h0 + HKV) continue;
-                    const int cc = ch & 127, i = cc & 63, up = cc >> 6;
+                    const bool in = (r < r1) && ch >= c_lo && ch < c_hi;
+                    if (!__any_sync(0xffffffffu, in)) continue;
+                    if (in) {
+                        const int kvh = ch >> 7;
+                        const int cc = ch & 127, i = cc & 63, up = cc >> 6;
+                        const int bit = 2 * BITS * i;
+                        const int wq = (kvh - h0) * 4 * BITS + (bit >> 5);
+                        unsigned long long w64 = kw_s[wq * 32 + j];
+                        if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                        const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                        const int code = (pc >> (up * BITS)) & CM;
+                        const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
+                        const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
+                        const float2 cs = cis_s[i * 32 + j];
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) {
+                            const int gl = (kvh - h0) * G + gg;
+                            const float qa = qs[gl * kHeadDim + i], qb = qs[gl * kHeadDim + i + 64];
+                            const float d = up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y);
+#pragma unroll
+                            for (int g = 0; g < HG; ++g) corr[g] += (g == gl) ? delta * d : 0.f;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < HG; ++g) {
+                    const float v = warp_sum(corr[g]);
+                    if (lane == 0) kcorr[g * 32 + j] = v;
+                }
+            }
+            if (warp < HG) {
+                // heavy RoPE pairs of head g = warp in fp32 (tables hlut), lane = token
+                const int g = warp, j = lane;
+                float hc = 0.f;
+                const int nh = hv_n[g];
+                for (int hs = 0; hs < nh; ++hs) {
+                    const int i = hv_pair[g * 8 + hs];
                     const int bit = 2 * BITS * i;
-                    const int wq = (kvh - h0) * 4 * BITS + (bit >> 5);
+                    const int wq = (g / G) * 4 * BITS + (bit >> 5);
                     unsigned long long w64 = kw_s[wq * 32 + j];
                     if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
                     const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                    const int code = (pc >> (up * BITS)) & CM;
-                    const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
-                    const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
+                    const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
                     const float2 cs = cis_s[i * 32 + j];
-#pragma unroll
-                    for (int gg = 0; gg < G; ++gg) {
-                        const int g = (kvh - h0) * G + gg;
-                        const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
-                        const float d = up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y);
-                        atomicAdd(&kcorr[g * 32 + j], delta * d);
-                    }
+                    hc += cs.x * ab.x + cs.y * ab.y;
                 }
-            }
-            // heavy RoPE pairs in fp32 (tables hlut; cis of the tile from the K phase)
-            for (int x = tid; x < HG * 8 * 32; x += ATT_THREADS) {
-                const int g = x >> 8, hs = (x >> 5) & 7, j = x & 31;
-                if (hs >= hv_n[g] || j >= ntok) continue;
-                const int i = hv_pair[g * 8 + hs];
-                const int bit = 2 * BITS * i;
-                const int wq = (g / G) * 4 * BITS + (bit >> 5);
-                unsigned long long w64 = kw_s[wq * 32 + j];
-                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
-                const float2 cs = cis_s[i * 32 + j];
-                atomicAdd(&kcorr[g * 32 + j], cs.x * ab.x + cs.y * ab.y);
+                hcorr[g * 32 + j] = hc;
             }
         }
         __syncthreads();
@@ -516,8 +542,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 float s = 0.f;
 #pragma unroll
                 for (int w = 0; w < ATT_WARPS; ++w) s += red[(w * HG + g) * 32 + lane];
-                s = s * lut_inv[g] + kcorr[g * 32 + lane];
-                kcorr[g * 32 + lane] = 0.f;
+                s = s * lut_inv[g] + kcorr[g * 32 + lane] + hcorr[g * 32 + lane];
                 const bool valid = lane < ntok;
                 if (!valid) s = -CUDART_INF_F;
                 const float mt = warp_max(s);
