@@ -130,6 +130,7 @@ struct Cfg {
         HG * kHeadDim * 4              /* qs */
         + ATT_WARPS * HG * 32 * 4      /* red */
         + HG * 32 * 4 * 3              /* p, kcorr, hcorr */
+        + 4 * 33 * 4                   /* per-token record sub-ranges + prefix */
         + HG * 32 * 2                  /* w16 */
         + HG * kHeadDim * 4            /* osp */
         + 64 * 16 * 3 + 64 * 8         /* anc64, rot64, qcis, anc32 */
@@ -163,7 +164,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     constexpr int CM = (1 << BITS) - 1;
     constexpr int HKV = HG / G;
     constexpr int QWC = HKV * 4 * BITS;             // K (and V) words per token in the CTA
-    constexpr int NWW = (BITS == 2) ? 1 : 2;        // K words per (lane, kv head, warp)
     constexpr int CPL = C::CPL;                     // V channels per lane
     constexpr int VWL = CPL * BITS / 32;            // V words per lane per token
     constexpr int LPT = HG * kHeadDim / CPL;        // V lanes per token
@@ -182,6 +182,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
     float *kcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
     float *hcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
+    int *rk_beg = reinterpret_cast<int *>(sp); sp += 33 * 4;   // K records of this head group
+    int *rk_len = reinterpret_cast<int *>(sp); sp += 33 * 4;
+    int *rv_beg = reinterpret_cast<int *>(sp); sp += 33 * 4;   // V records of this head group
+    int *rv_len = reinterpret_cast<int *>(sp); sp += 33 * 4;
     float *osp = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
     double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
@@ -423,6 +427,49 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const int64_t n0 = (int64_t)t * 32;
         const int ntok = (int)min((int64_t)32, P.T - n0);
 
+        // ---- per-token record sub-ranges of this head group (records are channel-sorted)
+        {
+            const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
+            const uint32_t ka = kptr_s[0] & ~3u;
+            for (int j = warp; j < 32; j += ATT_WARPS) {
+                int kb = 0, kl = 0, vb = 0, vl = 0;
+                if (j < ntok) {
+                    const uint32_t r0 = kptr_s[j], r1 = kptr_s[j + 1];
+                    int first = -1, cnt = 0;
+                    for (uint32_t rb = r0; rb < r1; rb += 32) {
+                        const uint32_t r = rb + lane;
+                        bool in = false;
+                        if (r < r1) {
+                            const uint32_t off = r - ka;
+                            const uint32_t rec = off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
+                            const int ch = (int)(rec & 0xffffu);
+                            in = ch >= c_lo && ch < c_hi;
+                        }
+                        const unsigned m = __ballot_sync(0xffffffffu, in);
+                        if (m && first < 0) first = (int)(rb - r0) + __ffs(m) - 1;
+                        cnt += __popc(m);
+                    }
+                    kb = first < 0 ? 0 : (int)r0 + first;
+                    kl = cnt;
+                    first = -1; cnt = 0;
+                    for (int rb = 0; rb < kv; rb += 32) {
+                        const int r = rb + lane;
+                        bool in = false;
+                        if (r < kv) {
+                            const int ch = (int)(vrec_s[j * kv + r] & 0xffffu);
+                            in = ch >= c_lo && ch < c_hi;
+                        }
+                        const unsigned m = __ballot_sync(0xffffffffu, in);
+                        if (m && first < 0) first = rb + __ffs(m) - 1;
+                        cnt += __popc(m);
+                    }
+                    vb = first < 0 ? 0 : j * kv + first;
+                    vl = cnt;
+                }
+                if (lane == 0) { rk_beg[j] = kb; rk_len[j] = kl; rv_beg[j] = vb; rv_len[j] = vl; }
+            }
+        }
+
         // ------------------------------------------------------------ a2: K dense
         {
             float acc_c[HG], acc_s[HG];
@@ -458,56 +505,51 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
             for (int g = 0; g < HG; ++g) red[(warp * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
         }
-        __syncwarp();   // this warp's cis_s rows are read by other warps after the barrier
 
-        // ---------------------- a3: K outliers (warp per token, no atomics), heavy pairs
-        // Heavy pairs first (head g <-> warp g, lane = token): reads cis_s rows written by
-        // other warps, so it runs after the barrier below; the outliers need cis_s too.
+        // ----------------------------- a3: K outliers (flat over relevant records), heavy
         __syncthreads();
         {
+            // inclusive prefix of the per-token counts (every warp, registers)
+            int kl = rk_len[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, kl, o);
+                if (lane >= o) kl += y;
+            }
+            const int ktot = __shfl_sync(0xffffffffu, kl, 31);
             const uint32_t ka = kptr_s[0] & ~3u;
-            const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
-            for (int j = warp; j < ntok; j += ATT_WARPS) {
-                const uint32_t r0 = kptr_s[j], r1 = kptr_s[j + 1];
-                float corr[HG];
+            for (int xb = warp * 32; xb < ktot; xb += ATT_THREADS) {
+                const int x = xb + lane;
+                // token j = number of tokens whose inclusive prefix is <= x (warp-wide search)
+                int j = 0;
 #pragma unroll
-                for (int g = 0; g < HG; ++g) corr[g] = 0.f;
-                for (uint32_t rb = r0; rb < r1; rb += 32) {
-                    const uint32_t r = rb + lane;
-                    uint32_t rec = 0xffffu;
-                    if (r < r1) {
-                        const uint32_t off = r - ka;
-                        rec = off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
-                    }
-                    const int ch = (int)(rec & 0xffffu);
-                    const bool in = (r < r1) && ch >= c_lo && ch < c_hi;
-                    if (!__any_sync(0xffffffffu, in)) continue;
-                    if (in) {
-                        const int kvh = ch >> 7;
-                        const int cc = ch & 127, i = cc & 63, up = cc >> 6;
-                        const int bit = 2 * BITS * i;
-                        const int wq = (kvh - h0) * 4 * BITS + (bit >> 5);
-                        unsigned long long w64 = kw_s[wq * 32 + j];
-                        if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                        const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                        const int code = (pc >> (up * BITS)) & CM;
-                        const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
-                        const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
-                        const float2 cs = cis_s[i * 32 + j];
-#pragma unroll
-                        for (int gg = 0; gg < G; ++gg) {
-                            const int gl = (kvh - h0) * G + gg;
-                            const float qa = qs[gl * kHeadDim + i], qb = qs[gl * kHeadDim + i + 64];
-                            const float d = up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y);
-#pragma unroll
-                            for (int g = 0; g < HG; ++g) corr[g] += (g == gl) ? delta * d : 0.f;
-                        }
-                    }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const int v = __shfl_sync(0xffffffffu, kl, j + o - 1);
+                    if (v <= x) j += o;
                 }
+                const int excl = __shfl_sync(0xffffffffu, kl, (j + 31) & 31);
+                if (x >= ktot) continue;
+                const uint32_t r = (uint32_t)rk_beg[j] + (uint32_t)(x - (j ? excl : 0));
+                const uint32_t off = r - ka;
+                const uint32_t rec = off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
+                const int ch = (int)(rec & 0xffffu);
+                const int kvh = ch >> 7;
+                const int cc = ch & 127, i = cc & 63, up = cc >> 6;
+                const int bit = 2 * BITS * i;
+                const int wq = (kvh - h0) * 4 * BITS + (bit >> 5);
+                unsigned long long w64 = kw_s[wq * 32 + j];
+                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                const int code = (pc >> (up * BITS)) & CM;
+                const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
+                const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
+                const float2 cs = cis_s[i * 32 + j];
 #pragma unroll
-                for (int g = 0; g < HG; ++g) {
-                    const float v = warp_sum(corr[g]);
-                    if (lane == 0) kcorr[g * 32 + j] = v;
+                for (int gg = 0; gg < G; ++gg) {
+                    const int gl = (kvh - h0) * G + gg;
+                    const float qa = qs[gl * kHeadDim + i], qb = qs[gl * kHeadDim + i + 64];
+                    const float d = up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y);
+                    atomicAdd(&kcorr[gl * 32 + j], delta * d);
                 }
             }
             if (warp < HG) {
@@ -543,6 +585,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
                 for (int w = 0; w < ATT_WARPS; ++w) s += red[(w * HG + g) * 32 + lane];
                 s = s * lut_inv[g] + kcorr[g * 32 + lane] + hcorr[g * 32 + lane];
+                kcorr[g * 32 + lane] = 0.f;
                 const bool valid = lane < ntok;
                 if (!valid) s = -CUDART_INF_F;
                 const float mt = warp_max(s);
@@ -601,13 +644,28 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             if (tid == 0) flag_s[0] = 0;
         }
 
-        // ---------------------------------------------------- a6: V outliers
-        for (int j = warp; j < ntok; j += ATT_WARPS) {
-            for (int r = lane; r < kv; r += 32) {
-                const uint32_t rec = vrec_s[j * kv + r];
+        // ------------------------------- a6: V outliers (flat over relevant records)
+        {
+            int vl = rv_len[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, vl, o);
+                if (lane >= o) vl += y;
+            }
+            const int vtot = __shfl_sync(0xffffffffu, vl, 31);
+            for (int xb = warp * 32; xb < vtot; xb += ATT_THREADS) {
+                const int x = xb + lane;
+                int j = 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const int v = __shfl_sync(0xffffffffu, vl, j + o - 1);
+                    if (v <= x) j += o;
+                }
+                const int excl = __shfl_sync(0xffffffffu, vl, (j + 31) & 31);
+                if (x >= vtot) continue;
+                const uint32_t rec = vrec_s[rv_beg[j] + (x - (j ? excl : 0))];
                 const int ch = (int)(rec & 0xffffu);
                 const int kvh = ch >> 7;
-                if (kvh < h0 || kvh >= h0 + HKV) continue;
                 const int bit = BITS * (ch - h0 * kHeadDim);
                 const uint32_t *vrow = vw_s + j * QWC;
                 unsigned long long w64 = vrow[bit >> 5];
