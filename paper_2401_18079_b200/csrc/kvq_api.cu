@@ -174,7 +174,7 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     kvq_status st = KVQ_OK;
     auto A = [&](auto **p, size_t bytes) { if (st == KVQ_OK) st = dev_alloc(c, p, bytes); };
     A(&d.kcodes, (size_t)(d.cap / 32) * d.QW * 32 * 4);
-    A(&d.vcodes, (size_t)d.cap * d.VW * 4 + 16);
+    A(&d.vcodes, (size_t)d.cap * d.VW * 4 + 16);   // [cap/32][H_kv][32][4b]
     A(&d.vsz, (size_t)d.cap * sizeof(float2));
     A(&d.vout, (size_t)d.cap * (kv > 0 ? kv : 1) * 4);
     A(&d.kptr, (size_t)(d.cap + 64) * 4);   // +63: attend stages 48-word CSC slices
@@ -429,15 +429,22 @@ kvq_status kvq_export(kvq_cache *c, int64_t t0, int64_t t1, kvq_export_buf *buf)
         }
     }
     if (buf->vcodes) {
-        std::vector<uint32_t> vc((size_t)n * d.VW + 1);
-        CK(cudaMemcpy(vc.data(), d.vcodes + t0 * d.VW, (size_t)n * d.VW * 4, cudaMemcpyDeviceToHost));
-        for (int64_t t = 0; t < n; ++t)
+        const int64_t tile0 = t0 / 32, tile1 = (t1 + 31) / 32;
+        const int hw = 4 * b;   // words per (token, kv head)
+        std::vector<uint32_t> vc((size_t)(tile1 - tile0) * d.H_kv * 32 * hw);
+        CK(cudaMemcpy(vc.data(), d.vcodes + tile0 * d.H_kv * 32 * hw, vc.size() * 4, cudaMemcpyDeviceToHost));
+        for (int64_t t = t0; t < t1; ++t) {
+            const int64_t tl = t / 32 - tile0;
+            const int j = (int)(t % 32);
             for (int ch = 0; ch < D; ++ch) {
-                const int64_t bit = (int64_t)b * ch;
-                uint64_t w = vc[t * d.VW + bit / 32];
-                if (bit % 32 + b > 32) w |= (uint64_t)vc[t * d.VW + bit / 32 + 1] << 32;
-                buf->vcodes[t * D + ch] = (uint8_t)((w >> (bit % 32)) & ((1u << b) - 1));
+                const int h = ch / kHeadDim, cc = ch % kHeadDim;
+                const uint32_t *row = vc.data() + ((tl * d.H_kv + h) * 32 + j) * hw;
+                const int bit = b * cc;
+                uint64_t w = row[bit / 32];
+                if (bit % 32 + b > 32) w |= (uint64_t)row[bit / 32 + 1] << 32;
+                buf->vcodes[(t - t0) * D + ch] = (uint8_t)((w >> (bit % 32)) & ((1u << b) - 1));
             }
+        }
     }
     if (buf->vs || buf->vz) {
         std::vector<float2> sz((size_t)n);

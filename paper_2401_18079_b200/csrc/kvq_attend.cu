@@ -109,12 +109,10 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // ---------------------------------------------------------------- configuration --
-constexpr int cpl_for(int bits, int hg) {
-    // channels per lane in the V phase: smallest of {8,16,32} with whole words per lane
-    // and at most 32 lanes per token
-    return (bits == 4 && hg * 128 / 8 <= 32) ? 8
-           : ((bits == 4 || bits == 2) && hg * 128 / 16 <= 32) ? 16
-                                                                : 32;
+constexpr int cpl_for(int bits, int /*hg*/) {
+    // V channels per lane: whole 32-bit words of codes per lane (b=4: 8, b=2/3: 32);
+    // one (head, token-group) task per warp needs HG * 128/CPL <= 16 (see caps below)
+    return bits == 4 ? 8 : 32;
 }
 
 template <int BITS, int HG>
@@ -129,7 +127,7 @@ struct Cfg {
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
         + ATT_WARPS * HG * 32 * 4      /* red */
-        + HG * 32 * 4 * 3              /* p, kcorr, hcorr */
+        + HG * 32 * 4 * 2              /* p, kcorr */
         + 4 * 33 * 4                   /* per-token record sub-ranges + prefix */
         + HG * 32 * 2                  /* w16 */
         + HG * kHeadDim * 4            /* osp */
@@ -166,9 +164,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     constexpr int QWC = HKV * 4 * BITS;             // K (and V) words per token in the CTA
     constexpr int CPL = C::CPL;                     // V channels per lane
     constexpr int VWL = CPL * BITS / 32;            // V words per lane per token
-    constexpr int LPT = HG * kHeadDim / CPL;        // V lanes per token
-    constexpr int SLOTS = ATT_THREADS / LPT;        // tokens per V step
-    constexpr int VSTEPS = (32 + SLOTS - 1) / SLOTS;
     constexpr int HMAX = C::HMAX;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -181,7 +176,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *red = reinterpret_cast<float *>(sp); sp += ATT_WARPS * HG * 32 * 4;
     float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
     float *kcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
-    float *hcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
     int *rk_beg = reinterpret_cast<int *>(sp); sp += 33 * 4;   // K records of this head group
     int *rk_len = reinterpret_cast<int *>(sp); sp += 33 * 4;
     int *rv_beg = reinterpret_cast<int *>(sp); sp += 33 * 4;   // V records of this head group
@@ -240,9 +234,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         uint32_t kn = ((khi + 3u) & ~3u) - ka;
         if (kn > (uint32_t)P.krec_cap) kn = (uint32_t)P.krec_cap;
         const unsigned b_kw = 32u * QWC * 4u;
-        const unsigned b_row = QWC * 4u;
         const unsigned b_vrec = 32u * (unsigned)kv * 4u;
-        const unsigned total = b_kw + 32u * b_row + 256u + 192u + b_vrec + kn * 4u;
+        const unsigned total = 2u * b_kw + 256u + 192u + b_vrec + kn * 4u;
         if (lane == 0) {
             fence_proxy_async();
             mbar_expect_tx(bar, total);
@@ -255,7 +248,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         if (lane == 2) bulk_g2s(sb + P.so_kptr, c.kptr + n0, 192u, bar);
         if (lane == 3 && b_vrec) bulk_g2s(sb + P.so_vrec, c.vout + n0 * kv, b_vrec, bar);
         if (lane == 4 && kn) bulk_g2s(sb + P.so_krec, c.kout + ka, kn * 4u, bar);
-        bulk_g2s(sb + P.so_vw + lane * b_row, c.vcodes + (n0 + lane) * c.VW + h0 * 4 * BITS, b_row, bar);
+        if (lane == 5)
+            bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)t * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
         // prefetch the CSC range of the tile after this one
         if (lane == 0 && t + 1 < t_end) kptr_at(t + 1, kp_lo, kp_hi);
     };
@@ -395,21 +389,27 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         t1s[k] = s;
     }
 
-    // V-phase mapping
-    const int cg = tid % LPT, slot = tid / LPT;
-    const int vh = cg / (kHeadDim / CPL);                    // local query head
-    const int vq = cg % (kHeadDim / CPL);                    // CPL-channel group in the head
-    const int vw0 = ((vh / G) * kHeadDim + vq * CPL) * BITS / 32;   // first word within a row
+    // V-phase task mapping: one (query head, token group) task per warp
+    constexpr int LH = kHeadDim / CPL;          // lanes per token per head
+    constexpr int TPW = 32 / LH;                // tokens per warp task
+    constexpr int NTASK = HG * (32 / TPW);      // tasks per tile
+    static_assert(NTASK <= ATT_WARPS, "V tasks must fit the CTA's warps");
+    const bool vtask = warp < NTASK;
+    const int vh = vtask ? warp / (32 / TPW) : 0;            // local query head
+    const int vj = (warp % (32 / TPW)) * TPW + lane / LH;    // token in the tile
+    const int vq = lane % LH;                                // channel group in the head
+    const int vkv = vh / G;                                  // local kv head
     float acc[CPL];
 #pragma unroll
     for (int x = 0; x < CPL; ++x) acc[x] = 0.f;
 
     // running softmax state (S-phase warps: warp g <-> head g)
     float m_run = -CUDART_INF_F, l_run = 0.f, z_run = 0.f;
-    int E_cur = -126;     // dense V accumulator units: 2^E_cur
+    int E_cur = -126;     // dense V accumulator units: 2^E_cur (CTA uniform)
 
     const int kbit0 = 2 * BITS * KPW * warp;
     const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
+    const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
     __syncthreads();
 
     for (int t = t_begin; t < t_end; ++t) {
@@ -426,48 +426,33 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const uint32_t *krec_s = reinterpret_cast<const uint32_t *>(sb + P.so_krec);
         const int64_t n0 = (int64_t)t * 32;
         const int ntok = (int)min((int64_t)32, P.T - n0);
+        const uint32_t ka = kptr_s[0] & ~3u;
+        auto krec = [&](uint32_t r) -> uint32_t {
+            const uint32_t off = r - ka;
+            return off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
+        };
 
-        // ---- per-token record sub-ranges of this head group (records are channel-sorted)
-        {
-            const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
-            const uint32_t ka = kptr_s[0] & ~3u;
-            for (int j = warp; j < 32; j += ATT_WARPS) {
-                int kb = 0, kl = 0, vb = 0, vl = 0;
-                if (j < ntok) {
-                    const uint32_t r0 = kptr_s[j], r1 = kptr_s[j + 1];
-                    int first = -1, cnt = 0;
-                    for (uint32_t rb = r0; rb < r1; rb += 32) {
-                        const uint32_t r = rb + lane;
-                        bool in = false;
-                        if (r < r1) {
-                            const uint32_t off = r - ka;
-                            const uint32_t rec = off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
-                            const int ch = (int)(rec & 0xffffu);
-                            in = ch >= c_lo && ch < c_hi;
-                        }
-                        const unsigned m = __ballot_sync(0xffffffffu, in);
-                        if (m && first < 0) first = (int)(rb - r0) + __ffs(m) - 1;
-                        cnt += __popc(m);
-                    }
-                    kb = first < 0 ? 0 : (int)r0 + first;
-                    kl = cnt;
-                    first = -1; cnt = 0;
-                    for (int rb = 0; rb < kv; rb += 32) {
-                        const int r = rb + lane;
-                        bool in = false;
-                        if (r < kv) {
-                            const int ch = (int)(vrec_s[j * kv + r] & 0xffffu);
-                            in = ch >= c_lo && ch < c_hi;
-                        }
-                        const unsigned m = __ballot_sync(0xffffffffu, in);
-                        if (m && first < 0) first = rb + __ffs(m) - 1;
-                        cnt += __popc(m);
-                    }
-                    vb = first < 0 ? 0 : j * kv + first;
-                    vl = cnt;
-                }
-                if (lane == 0) { rk_beg[j] = kb; rk_len[j] = kl; rv_beg[j] = vb; rv_len[j] = vl; }
+        // ---- per-token record sub-ranges of this head group: records are channel-sorted,
+        //      so lane j of the last warp binary-searches [c_lo, c_hi) in token j's list
+        if (warp == ATT_WARPS - 1) {
+            const int j = lane;
+            int kb = 0, ke = 0, vb = 0, ve = 0;
+            if (j < ntok) {
+                uint32_t lo = kptr_s[j], hi = kptr_s[j + 1];
+                uint32_t a = lo, e = hi;
+                while (a < e) { const uint32_t m = (a + e) >> 1; if ((int)(krec(m) & 0xffffu) < c_lo) a = m + 1; else e = m; }
+                kb = (int)a;
+                e = hi;
+                while (a < e) { const uint32_t m = (a + e) >> 1; if ((int)(krec(m) & 0xffffu) < c_hi) a = m + 1; else e = m; }
+                ke = (int)a;
+                int va = j * kv, vee = (j + 1) * kv;
+                while (va < vee) { const int m = (va + vee) >> 1; if ((int)(vrec_s[m] & 0xffffu) < c_lo) va = m + 1; else vee = m; }
+                vb = va;
+                vee = (j + 1) * kv;
+                while (va < vee) { const int m = (va + vee) >> 1; if ((int)(vrec_s[m] & 0xffffu) < c_hi) va = m + 1; else vee = m; }
+                ve = va;
             }
+            rk_beg[j] = kb; rk_len[j] = ke - kb; rv_beg[j] = vb; rv_len[j] = ve - vb;
         }
 
         // ------------------------------------------------------------ a2: K dense
@@ -505,143 +490,100 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
             for (int g = 0; g < HG; ++g) red[(warp * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
         }
-
-        // ----------------------------- a3: K outliers (flat over relevant records), heavy
-        __syncthreads();
-        {
-            // inclusive prefix of the per-token counts (every warp, registers)
-            int kl = rk_len[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, kl, o);
-                if (lane >= o) kl += y;
-            }
-            const int ktot = __shfl_sync(0xffffffffu, kl, 31);
-            const uint32_t ka = kptr_s[0] & ~3u;
-            for (int xb = warp * 32; xb < ktot; xb += ATT_THREADS) {
-                const int x = xb + lane;
-                // token j = number of tokens whose inclusive prefix is <= x (warp-wide search)
-                int j = 0;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const int v = __shfl_sync(0xffffffffu, kl, j + o - 1);
-                    if (v <= x) j += o;
-                }
-                const int excl = __shfl_sync(0xffffffffu, kl, (j + 31) & 31);
-                if (x >= ktot) continue;
-                const uint32_t r = (uint32_t)rk_beg[j] + (uint32_t)(x - (j ? excl : 0));
-                const uint32_t off = r - ka;
-                const uint32_t rec = off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
-                const int ch = (int)(rec & 0xffffu);
-                const int kvh = ch >> 7;
-                const int cc = ch & 127, i = cc & 63, up = cc >> 6;
-                const int bit = 2 * BITS * i;
-                const int wq = (kvh - h0) * 4 * BITS + (bit >> 5);
-                unsigned long long w64 = kw_s[wq * 32 + j];
-                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                const int code = (pc >> (up * BITS)) & CM;
-                const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
-                const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
-                const float2 cs = cis_s[i * 32 + j];
-#pragma unroll
-                for (int gg = 0; gg < G; ++gg) {
-                    const int gl = (kvh - h0) * G + gg;
-                    const float qa = qs[gl * kHeadDim + i], qb = qs[gl * kHeadDim + i + 64];
-                    const float d = up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y);
-                    atomicAdd(&kcorr[gl * 32 + j], delta * d);
-                }
-            }
-            if (warp < HG) {
-                // heavy RoPE pairs of head g = warp in fp32 (tables hlut), lane = token
-                const int g = warp, j = lane;
-                float hc = 0.f;
-                const int nh = hv_n[g];
-                for (int hs = 0; hs < nh; ++hs) {
-                    const int i = hv_pair[g * 8 + hs];
-                    const int bit = 2 * BITS * i;
-                    const int wq = (g / G) * 4 * BITS + (bit >> 5);
-                    unsigned long long w64 = kw_s[wq * 32 + j];
-                    if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                    const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                    const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
-                    const float2 cs = cis_s[i * 32 + j];
-                    hc += cs.x * ab.x + cs.y * ab.y;
-                }
-                hcorr[g * 32 + j] = hc;
-            }
-        }
         __syncthreads();
 
-        // ------------------------------------------------------- a4: softmax
+        // ------------- a3 + a4: K outliers, heavy pairs, online softmax (warp g, lane j)
         {
-            // CTA-uniform V scale exponent from the tile's max s_n
             float smax = lane < ntok ? vsz_s[lane].x : 0.f;
             smax = warp_max(smax);
             int E_new = E_cur;
             if (smax > 0.f) E_new = max(E_cur, ilogbf(smax) + 1);
             for (int g = warp; g < HG; g += ATT_WARPS) {
+                const int j = lane;
+                const bool valid = j < ntok;
                 float s = 0.f;
 #pragma unroll
-                for (int w = 0; w < ATT_WARPS; ++w) s += red[(w * HG + g) * 32 + lane];
-                s = s * lut_inv[g] + kcorr[g * 32 + lane] + hcorr[g * 32 + lane];
-                kcorr[g * 32 + lane] = 0.f;
-                const bool valid = lane < ntok;
-                if (!valid) s = -CUDART_INF_F;
+                for (int w = 0; w < ATT_WARPS; ++w) s += red[(w * HG + g) * 32 + j];
+                s *= lut_inv[g];
+                const int gkv = h0 + g / G;             // global kv head of query head g
+                if (valid) {
+                    // Key outliers of (token j, kv head of g): x - K^(code) times dscore/dK
+                    const int rb = rk_beg[j], re = rb + rk_len[j];
+                    for (int r = rb; r < re; ++r) {
+                        const uint32_t rec = krec((uint32_t)r);
+                        const int ch = (int)(rec & 0xffffu);
+                        if ((ch >> 7) != gkv) continue;
+                        const int cc = ch & 127, i = cc & 63, up = cc >> 6;
+                        const int bit = 2 * BITS * i;
+                        const int wq = (g / G) * 4 * BITS + (bit >> 5);
+                        unsigned long long w64 = kw_s[wq * 32 + j];
+                        if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                        const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                        const int code = (pc >> (up * BITS)) & CM;
+                        const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
+                        const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
+                        const float2 cs = cis_s[i * 32 + j];
+                        const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
+                        s += delta * (up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y));
+                    }
+                    // heavy RoPE pairs of head g in fp32 (tables hlut)
+                    const int nh = hv_n[g];
+                    for (int hs = 0; hs < nh; ++hs) {
+                        const int i = hv_pair[g * 8 + hs];
+                        const int bit = 2 * BITS * i;
+                        const int wq = (g / G) * 4 * BITS + (bit >> 5);
+                        unsigned long long w64 = kw_s[wq * 32 + j];
+                        if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                        const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                        const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
+                        const float2 cs = cis_s[i * 32 + j];
+                        s += cs.x * ab.x + cs.y * ab.y;
+                    }
+                } else {
+                    s = -CUDART_INF_F;
+                }
                 const float mt = warp_max(s);
                 const float m_new = fmaxf(m_run, mt);
                 const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
                 const float p = valid ? exp2f(s - m_new) : 0.f;
-                const float2 sz = valid ? vsz_s[lane] : make_float2(0.f, 0.f);
+                const float2 sz = valid ? vsz_s[j] : make_float2(0.f, 0.f);
                 l_run = l_run * alpha + warp_sum(p);
                 z_run = z_run * alpha + warp_sum(p * sz.y);
                 m_run = m_new;
-                p_s[g * 32 + lane] = p;
-                const float wv = p * ldexpf(sz.x, -E_new);
-                w16[g * 32 + lane] = __half_as_ushort(__float2half_rn(wv));
-                if (lane == 0) {
-                    alpha_s[g] = alpha;
-                    beta_s[g] = alpha * ldexpf(1.f, E_cur - E_new);
-                    if (alpha != 1.f || E_new != E_cur) flag_s[0] = 1;
+                p_s[g * 32 + j] = p;
+                w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * ldexpf(sz.x, -E_new)));
+                if (alpha != 1.f) {
+#pragma unroll
+                    for (int x = 0; x < kHeadDim / 32; ++x) osp[g * kHeadDim + x * 32 + lane] *= alpha;
                 }
+                if (lane == 0) beta_s[g] = alpha * ldexpf(1.f, E_cur - E_new);
             }
             E_cur = E_new;
         }
         __syncthreads();
 
         // -------------------------------------------------------- a5: P.V dense
-        const bool rescale = flag_s[0] != 0;
-        if (rescale) {
+        if (vtask) {
             const float b = beta_s[vh];
             if (b != 1.f) {
 #pragma unroll
                 for (int x = 0; x < CPL; ++x) acc[x] *= b;
             }
-            for (int x = tid; x < HG * kHeadDim; x += ATT_THREADS) osp[x] *= alpha_s[x >> 7];
-        }
+            const uint16_t w = w16[vh * 32 + vj];
+            uint32_t vw[VWL];
+            const uint32_t *src = vw_s + (vkv * 32 + vj) * (4 * BITS) + vq * VWL;
 #pragma unroll
-        for (int vs = 0; vs < VSTEPS; ++vs) {
-            const int j = slot + vs * SLOTS;
-            if (j < 32) {
-                const uint16_t w = w16[vh * 32 + j];
-                uint32_t vw[VWL];
+            for (int x = 0; x < VWL; ++x) vw[x] = src[x];
 #pragma unroll
-                for (int x = 0; x < VWL; ++x) vw[x] = vw_s[j * QWC + vw0 + x];
-#pragma unroll
-                for (int pp = 0; pp < CPL / 2; ++pp) {
-                    const int bit = 2 * BITS * pp;
-                    const int wi = bit >> 5, sh = bit & 31;
-                    uint32_t pc;
-                    if (sh + 2 * BITS <= 32) pc = (vw[wi] >> sh) & (NE - 1);
-                    else pc = (uint32_t)((((unsigned long long)vw[wi + 1] << 32) | vw[wi]) >> sh) & (NE - 1);
-                    const uint32_t cv = vlut[pc * 32 + lane];
-                    fma_w_f16x2(w, cv, acc[2 * pp], acc[2 * pp + 1]);
-                }
+            for (int pp = 0; pp < CPL / 2; ++pp) {
+                const int bit = 2 * BITS * pp;
+                const int wi = bit >> 5, sh = bit & 31;
+                uint32_t pc;
+                if (sh + 2 * BITS <= 32) pc = (vw[wi] >> sh) & (NE - 1);
+                else pc = (uint32_t)((((unsigned long long)vw[wi + 1] << 32) | vw[wi]) >> sh) & (NE - 1);
+                const uint32_t cv = vlut[pc * 32 + lane];
+                fma_w_f16x2(w, cv, acc[2 * pp], acc[2 * pp + 1]);
             }
-        }
-        if (rescale) {
-            __syncthreads();
-            if (tid == 0) flag_s[0] = 0;
         }
 
         // ------------------------------- a6: V outliers (flat over relevant records)
@@ -665,9 +607,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 if (x >= vtot) continue;
                 const uint32_t rec = vrec_s[rv_beg[j] + (x - (j ? excl : 0))];
                 const int ch = (int)(rec & 0xffffu);
-                const int kvh = ch >> 7;
-                const int bit = BITS * (ch - h0 * kHeadDim);
-                const uint32_t *vrow = vw_s + j * QWC;
+                const int kvl = (ch >> 7) - h0;
+                const int bit = BITS * (ch & 127);
+                const uint32_t *vrow = vw_s + (kvl * 32 + j) * (4 * BITS);
                 unsigned long long w64 = vrow[bit >> 5];
                 if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vrow[(bit >> 5) + 1] << 32;
                 const int code = (int)((w64 >> (bit & 31)) & CM);
@@ -676,7 +618,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const float delta = xval - (cbV[code] * sz.x + sz.y);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
-                    const int g = (kvh - h0) * G + gg;
+                    const int g = kvl * G + gg;
                     atomicAdd(&osp[g * kHeadDim + (ch & 127)], p_s[g * 32 + j] * delta);
                 }
             }
@@ -698,8 +640,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     {
         const float sc = ldexpf(1.f, E_cur);
         float *dst = osp + vh * kHeadDim + vq * CPL;
+        if (vtask) {
 #pragma unroll
-        for (int x = 0; x < CPL; ++x) atomicAdd(&dst[x], acc[x] * sc);
+            for (int x = 0; x < CPL; ++x) atomicAdd(&dst[x], acc[x] * sc);
+        }
     }
     __syncthreads();
     float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
@@ -824,7 +768,6 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
         case 1: return launch_g<BITS, 1>(c, P, grid, s);
         case 2: if constexpr (BITS <= 3) return launch_g<BITS, 2>(c, P, grid, s); break;
         case 4: if constexpr (BITS <= 3) return launch_g<BITS, 4>(c, P, grid, s); break;
-        case 8: if constexpr (BITS <= 2) return launch_g<BITS, 8>(c, P, grid, s); break;
     }
     return cudaErrorInvalidValue;
 }
@@ -832,7 +775,7 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
 }  // namespace
 
 int attend_heads_per_cta(int bits, int H_q, int G) {
-    const int cap = bits == 4 ? 1 : (bits == 3 ? 4 : 8);
+    const int cap = bits == 4 ? 1 : 4;   // V tasks: HG * 128/CPL <= 16 warps
     for (int hg = cap; hg >= 1; hg >>= 1)
         if (H_q % hg == 0 && hg % G == 0) return hg;
     return 0;
@@ -843,7 +786,6 @@ size_t attend_smem_bytes(int bits, int hg) {
         case 201: return Cfg<2, 1>::fixed;
         case 202: return Cfg<2, 2>::fixed;
         case 204: return Cfg<2, 4>::fixed;
-        case 208: return Cfg<2, 8>::fixed;
         case 301: return Cfg<3, 1>::fixed;
         case 302: return Cfg<3, 2>::fixed;
         case 304: return Cfg<3, 4>::fixed;

@@ -7,8 +7,10 @@
 //           code(h, p) | code(h, p+64) << b in 2b bits at bit offset 2b*p, RoPE partners
 //           adjacent) occupies words q = h*4b .. h*4b+4b-1, stored at [t][q][j] so a
 //           warp with lane = token reads 128 contiguous bytes per word slot.
-//   vcodes  u32 [cap][VW]             Value codes: the canonical little-endian bitstream
-//           of the token (code c at bit b*c), VW = D*b/32 words per token.
+//   vcodes  u32 [ntiles][H_kv][32][4b] Value codes: for token n = 32t+j and KV head h, the
+//           head's 128 codes as the canonical little-endian bitstream (code c at bit b*c,
+//           4b words), stored at [t][h][j] so one head group's slice of a tile is one
+//           contiguous block (a single TMA bulk copy).
 //   vsz     float2 [cap]              per-token Value (s_n, z_n), fp32 (reading R6).
 //   vout    u32 [cap][kv]             Value outliers, exactly kv = ceil(f*D) per token
 //           (implicit CSR row pointer n*kv), ascending channel; record =

@@ -70,37 +70,65 @@ __device__ __forceinline__ int block_excl_scan(int v, int *total, int *sbuf /*[Q
     return res;
 }
 
+// Histogram add with warp aggregation: lanes hitting the same bin are merged with
+// match.any, so a concentrated value distribution does not serialize on one bank.
+__device__ __forceinline__ void hist_add(int *hist, int bin, bool valid) {
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+        const unsigned peers = __match_any_sync(act, bin);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+    }
+}
+
+// Warp 0 finds, walking bins from 255 down, the bin `sel` where the running count reaches
+// `need`, and the count strictly above it (`above`).  Parallel: 8 bins per lane + a
+// warp scan, no serial 256-step walk.
+__device__ __forceinline__ void select_bin(const int *hist, int need, int *out /*[2]*/) {
+    const int lane = threadIdx.x & 31;
+    int c[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { c[k] = hist[255 - (8 * lane + k)]; sum += c[k]; }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int excl = incl - sum;
+    if (excl < need && need <= incl) {
+        int cum = excl;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (cum + c[k] >= need) { out[0] = 255 - (8 * lane + k); out[1] = cum; break; }
+            cum += c[k];
+        }
+    }
+}
+
 // Radix select over 16-bit keys of the "candidate" elements: returns tau such that
 // #(cand with key' > tau) < need <= #(cand with key' >= tau), where key' = key (desc=1)
 // or 0xffff - key (desc=0, i.e. ascending order).  Also returns #(key' > tau).
+// Loop trip counts are uniform across the CTA (E elements per thread).
 __device__ void radix_select16(const uint16_t *keys, const uint8_t *flags, int D, int c_begin,
-                               int c_end, int need, bool desc, int *hist /*[256]*/,
+                               int E, int need, bool desc, int *hist /*[256]*/,
                                int *shared_out /*[4]*/, int *tau_out, int *gt_out) {
     int prefix_hi = -1;   // selected high byte
     int gt = 0;
     for (int pass = 0; pass < 2; ++pass) {
         for (int b = threadIdx.x; b < 256; b += QZ_THREADS) hist[b] = 0;
         __syncthreads();
-        for (int c = c_begin; c < c_end; ++c) {
-            if (flags[c]) continue;
-            int kk = desc ? keys[c] : (0xffff - keys[c]);
-            if (pass == 0) atomicAdd(&hist[kk >> 8], 1);
-            else if ((kk >> 8) == prefix_hi) atomicAdd(&hist[kk & 0xff], 1);
+        for (int e = 0; e < E; ++e) {
+            const int c = c_begin + e;
+            bool valid = c < D && !flags[c];
+            int kk = 0;
+            if (valid) kk = desc ? keys[c] : (0xffff - keys[c]);
+            if (pass == 1) valid = valid && ((kk >> 8) == prefix_hi);
+            hist_add(hist, pass == 0 ? (kk >> 8) : (kk & 0xff), valid);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            // walk from the top bin down
-            int cum = 0, sel = 0;
-            for (int b = 255; b >= 0; --b) {
-                int h = hist[b];
-                if (cum + h >= need - gt) { sel = b; break; }
-                cum += h;
-            }
-            shared_out[0] = sel;
-            shared_out[1] = cum;
-        }
+        if (threadIdx.x < 32) select_bin(hist, need - gt, shared_out);
         __syncthreads();
-        int sel = shared_out[0];
+        const int sel = shared_out[0];
         gt += shared_out[1];
         if (pass == 0) prefix_hi = sel;
         else *tau_out = (prefix_hi << 8) | sel;
@@ -206,7 +234,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         if (need == 0) continue;
         const bool desc = (sel == 0);
         int tau, gt;
-        radix_select16(vkey, vflag, D, cb0, cb1, need, desc, hist, sout, &tau, &gt);
+        radix_select16(vkey, vflag, D, tid * E, E, need, desc, hist, sout, &tau, &gt);
         // ties at tau: lowest channel index first
         int ties = 0;
         for (int ch = cb0; ch < cb1; ++ch) {
@@ -311,7 +339,9 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         unsigned long long acc = 0;
         for (int ch = c0, sh = 0; sh < 32 + off && ch < D; ++ch, sh += BITS)
             acc |= (unsigned long long)vc[ch] << sh;
-        c.vcodes[n * (int64_t)c.VW + w] = (uint32_t)(acc >> off);
+        // tile layout: [tile][kv head][32 tokens][4b words] (kvq_internal.cuh)
+        const int hh = w / (4 * BITS), wi = w % (4 * BITS);
+        c.vcodes[(((int64_t)tile * c.H_kv + hh) * 32 + jj) * (4 * BITS) + wi] = (uint32_t)(acc >> off);
     }
 }
 
