@@ -172,6 +172,11 @@ kvq_status kvq_get_info(const kvq_cache *cache, kvq_info *info);
 /* Force the number of token splits per head group for attend (0 = auto). */
 kvq_status kvq_set_splits(kvq_cache *cache, int32_t splits);
 
+/* Diagnostics: per-phase cycle sums of the attend kernel since the last call
+ * (out[0..4]: issue, TMA wait, K phase, softmax phase, V phase; out[5]: tiles), summed
+ * over CTAs.  Only when the process was started with KVQ_PHASE_TIMERS=1. */
+kvq_status kvq_phase_timers(kvq_cache *cache, uint64_t *out /* host [8] */);
+
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char *kvq_last_error(void);
 

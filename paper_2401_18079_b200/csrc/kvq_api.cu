@@ -2,6 +2,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -22,6 +23,7 @@ struct kvq_cache {
     float *parts = nullptr;    // [max_splits][H_q][d+2]
     int max_splits = 0;
     unsigned *tickets = nullptr;
+    unsigned long long *timers = nullptr;   // diagnostics (KVQ_PHASE_TIMERS=1)
     int *err_host = nullptr;   // host-mapped sticky error word
     void *stage = nullptr;     // device staging for host buffers
     size_t stage_bytes = 0;
@@ -186,6 +188,7 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     c->max_splits = 4 * 148;
     A(&c->parts, (size_t)c->max_splits * d.H_q * (kHeadDim + 2) * 4);
     A(&c->tickets, 64 * 4);
+    if (getenv("KVQ_PHASE_TIMERS")) A(&c->timers, 8 * 8);
     if (st != KVQ_OK) { kvq_cache_destroy(c); return st; }
     {
         cudaError_t e = cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped);
@@ -241,6 +244,16 @@ kvq_status kvq_get_info(const kvq_cache *c, kvq_info *info) {
     info->capacity_tokens = c->dc.cap;
     info->k_outlier_capacity = c->dc.kcap;
     info->device_bytes = c->device_bytes;
+    return KVQ_OK;
+}
+
+kvq_status kvq_phase_timers(kvq_cache *c, uint64_t *out) {
+    if (!c || !out) return fail(KVQ_EINVAL, "null argument");
+    if (!c->timers) return fail(KVQ_EINVAL, "phase timers disabled (set KVQ_PHASE_TIMERS=1)");
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, c->timers, 8 * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(c->timers, 0, 8 * 8));
     return KVQ_OK;
 }
 
@@ -341,6 +354,7 @@ static kvq_status attend_impl(kvq_cache *c, const void *q, int64_t pos, float *o
     AttendArgs a;
     a.q = qd; a.pos = pos; a.T = c->T; a.out = od; a.write_partial = partial;
     a.parts = c->parts; a.tickets = c->tickets; a.splits = c->splits_forced;
+    a.timers = c->timers;
     cudaError_t e = launch_attend(c->dc, a, &c->last_splits, s);
     if (e != cudaSuccess) return cuda_fail(e, "attend launch");
     if (co == 1) {

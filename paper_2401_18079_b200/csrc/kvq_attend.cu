@@ -153,6 +153,7 @@ struct Params {
     int stages;
     int krec_cap;        // u32 records per stage buffer (multiple of 4)
     unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kptr, so_vrec, so_krec;
+    unsigned long long *timers;   // optional [8] phase cycle sums (diagnostics), may be null
 };
 
 template <int BITS, int HG, int G>
@@ -412,11 +413,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
     __syncthreads();
 
+    unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
+    long long tc0 = clock64(), tc1;
     for (int t = t_begin; t < t_end; ++t) {
         const int it = t - t_begin;
         const int st = it % P.stages;
         if (warp == 0) issue(t + P.stages - 1, (it + P.stages - 1) % P.stages);
+        tc1 = clock64(); tm[0] += tc1 - tc0; tc0 = tc1;
         mbar_wait(bars + st, (unsigned)((it / P.stages) & 1));
+        tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
         unsigned char *sb = stage_ptr(st);
         const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
         const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
@@ -491,6 +496,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             for (int g = 0; g < HG; ++g) red[(warp * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
         }
         __syncthreads();
+        tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
 
         // ------------- a3 + a4: K outliers, heavy pairs, online softmax (warp g, lane j)
         {
@@ -561,6 +567,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             E_cur = E_new;
         }
         __syncthreads();
+        tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
 
         // -------------------------------------------------------- a5: P.V dense
         if (vtask) {
@@ -632,6 +639,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             anc32[tid] = make_float2((float)b.x, (float)b.y);
         }
         __syncthreads();
+        tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
+    }
+    if (P.timers && tid == 0) {
+#pragma unroll
+        for (int x = 0; x < 5; ++x) atomicAdd(P.timers + x, tm[x]);
+        atomicAdd(P.timers + 5, (unsigned long long)(t_end - t_begin));
     }
 
     // ------------------------------------------------------------ write partial
@@ -816,6 +829,7 @@ cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_us
     Params P{};
     P.q = a.q; P.pos = a.pos; P.T = a.T; P.S = S; P.ntiles = ntiles;
     P.out = a.out; P.parts = a.parts; P.tickets = a.tickets; P.write_partial = a.write_partial;
+    P.timers = a.timers;
     const int grid = (c.H_q / hg) * S;
     if (splits_used) *splits_used = S;
     switch (c.bits) {

@@ -63,6 +63,7 @@ struct AttendArgs {
     float *parts;        // scratch [splits][H_q][d+2]
     unsigned *tickets;   // [n_head_groups], zero between launches
     int splits;          // 0 = auto
+    unsigned long long *timers;   // diagnostics: phase cycle sums, or null
 };
 int attend_heads_per_cta(int bits, int H_q, int G);
 int attend_auto_splits(const DevCache &c, int64_t T, int hg);

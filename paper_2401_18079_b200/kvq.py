@@ -27,7 +27,7 @@ KVQ_FLAG_TRUST_DEVICE_PTRS = 1
 EXPORTED = ["kvq_cache_create", "kvq_cache_destroy", "kvq_append", "kvq_prefill_quantize",
             "kvq_decode_attend", "kvq_decode_attend_partial", "kvq_merge_partials",
             "kvq_num_tokens", "kvq_reset", "kvq_sync", "kvq_key_outlier_span", "kvq_export",
-            "kvq_get_info", "kvq_set_splits", "kvq_last_error", "kvq_version"]
+            "kvq_get_info", "kvq_set_splits", "kvq_phase_timers", "kvq_last_error", "kvq_version"]
 
 
 class KVQError(RuntimeError):
@@ -86,6 +86,7 @@ def _load() -> ctypes.CDLL:
         "kvq_export": (i32, [vp, i64, i64, ctypes.POINTER(kvq_export_buf)]),
         "kvq_get_info": (i32, [vp, ctypes.POINTER(kvq_info)]),
         "kvq_set_splits": (i32, [vp, i32]),
+        "kvq_phase_timers": (i32, [vp, ctypes.POINTER(ctypes.c_uint64)]),
         "kvq_last_error": (ctypes.c_char_p, []),
         "kvq_version": (i32, []),
     }
@@ -215,6 +216,11 @@ class KVQCache:
 
     def set_splits(self, splits: int):
         _check(_lib.kvq_set_splits(self._h, int(splits)))
+
+    def phase_timers(self) -> list:
+        out = (ctypes.c_uint64 * 8)()
+        _check(_lib.kvq_phase_timers(self._h, out))
+        return list(out)
 
     def info(self) -> dict:
         inf = kvq_info()
