@@ -129,6 +129,7 @@ struct Cfg {
         + ATT_WARPS * HG * 32 * 4      /* red */
         + HG * 32 * 4 * 2              /* p, kcorr */
         + 4 * 33 * 4                   /* per-token record sub-ranges + prefix */
+        + HG * kHeadDim * 4 * 2 + 64 * 4 /* staged s_c, z_c of the group, codebooks */
         + HG * 32 * 2                  /* w16 */
         + HG * kHeadDim * 4            /* osp */
         + 64 * 16 * 3 + 64 * 8         /* anc64, rot64, qcis, anc32 */
@@ -181,6 +182,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     int *rk_len = reinterpret_cast<int *>(sp); sp += 33 * 4;
     int *rv_beg = reinterpret_cast<int *>(sp); sp += 33 * 4;   // V records of this head group
     int *rv_len = reinterpret_cast<int *>(sp); sp += 33 * 4;
+    float *ks_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;   // s_c of the group's channels
+    float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
+    float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
     float *osp = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
     double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         lo = __ldg(c.kptr + n0);
         hi = __ldg(c.kptr + n1);
     };
-    auto issue = [&](int t, int st) {   // warp 0 only
+    auto issue = [&](int t, int st) {   // producer warp only
         if (t >= t_end) return;
         unsigned char *sb = stage_ptr(st);
         uint64_t *bar = bars + st;
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         mbar_fence_init();
     }
     __syncthreads();
-    if (warp == 0) {
+    if (warp == ATT_WARPS - 1) {   // the producer warp (also issues inside the tile loop)
         if (lane == 0 && t_begin < t_end) kptr_at(t_begin, kp_lo, kp_hi);
         for (int s = 0; s < P.stages - 1; ++s) issue(t_begin + s, s);
     }
@@ -281,6 +285,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         rot64[i] = make_double2(co, s);
     }
     for (int x = tid; x < HG * kHeadDim; x += ATT_THREADS) osp[x] = 0.f;
+    for (int x = tid; x < HKV * kHeadDim; x += ATT_THREADS) {
+        ks_s[x] = ks[h0 * kHeadDim + x];
+        kz_s[x] = kz[h0 * kHeadDim + x];
+    }
+    if (tid < 64) cb_s[tid] = c.cb[tid];
     for (int x = tid; x < HG * 32; x += ATT_THREADS) kcorr[x] = 0.f;
     if (tid < 16) flag_s[tid] = 0;
     __syncthreads();
@@ -415,11 +424,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 
     unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
     long long tc0 = clock64(), tc1;
+    const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
     for (int t = t_begin; t < t_end; ++t) {
         const int it = t - t_begin;
         const int st = it % P.stages;
-        if (warp == 0) issue(t + P.stages - 1, (it + P.stages - 1) % P.stages);
-        tc1 = clock64(); tm[0] += tc1 - tc0; tc0 = tc1;
         mbar_wait(bars + st, (unsigned)((it / P.stages) & 1));
         tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
         unsigned char *sb = stage_ptr(st);
@@ -434,30 +442,36 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const uint32_t ka = kptr_s[0] & ~3u;
         auto krec = [&](uint32_t r) -> uint32_t {
             const uint32_t off = r - ka;
-            return off < (uint32_t)P.krec_cap ? krec_s[off] : __ldg(c.kout + r);
+            if (off < (uint32_t)P.krec_cap) return krec_s[off];
+            return __ldcg(c.kout + r);    // beyond the staged window (very dense tiles)
         };
 
         // ---- per-token record sub-ranges of this head group: records are channel-sorted,
-        //      so lane j of the last warp binary-searches [c_lo, c_hi) in token j's list
-        if (warp == ATT_WARPS - 1) {
-            const int j = lane;
-            int kb = 0, ke = 0, vb = 0, ve = 0;
+        //      so the first record >= c is popc(ballot(ch < c)) past the token's start
+        for (int j = warp; j < 32; j += ATT_WARPS) {
+            int kb = 0, kn = 0, vb = 0, vn = 0;
             if (j < ntok) {
-                uint32_t lo = kptr_s[j], hi = kptr_s[j + 1];
-                uint32_t a = lo, e = hi;
-                while (a < e) { const uint32_t m = (a + e) >> 1; if ((int)(krec(m) & 0xffffu) < c_lo) a = m + 1; else e = m; }
-                kb = (int)a;
-                e = hi;
-                while (a < e) { const uint32_t m = (a + e) >> 1; if ((int)(krec(m) & 0xffffu) < c_hi) a = m + 1; else e = m; }
-                ke = (int)a;
-                int va = j * kv, vee = (j + 1) * kv;
-                while (va < vee) { const int m = (va + vee) >> 1; if ((int)(vrec_s[m] & 0xffffu) < c_lo) va = m + 1; else vee = m; }
-                vb = va;
-                vee = (j + 1) * kv;
-                while (va < vee) { const int m = (va + vee) >> 1; if ((int)(vrec_s[m] & 0xffffu) < c_hi) va = m + 1; else vee = m; }
-                ve = va;
+                const uint32_t r0 = kptr_s[j], r1 = kptr_s[j + 1];
+                int below_lo = 0, below_hi = 0;
+                for (uint32_t rb = r0; rb < r1; rb += 32) {
+                    const uint32_t r = rb + lane;
+                    const int ch = r < r1 ? (int)(krec(r) & 0xffffu) : 0x7fffffff;
+                    below_lo += __popc(__ballot_sync(0xffffffffu, ch < c_lo));
+                    below_hi += __popc(__ballot_sync(0xffffffffu, ch < c_hi));
+                }
+                kb = (int)r0 + below_lo;
+                kn = below_hi - below_lo;
+                below_lo = below_hi = 0;
+                for (int rb = 0; rb < kv; rb += 32) {
+                    const int r = rb + lane;
+                    const int ch = r < kv ? (int)(vrec_s[j * kv + r] & 0xffffu) : 0x7fffffff;
+                    below_lo += __popc(__ballot_sync(0xffffffffu, ch < c_lo));
+                    below_hi += __popc(__ballot_sync(0xffffffffu, ch < c_hi));
+                }
+                vb = j * kv + below_lo;
+                vn = below_hi - below_lo;
             }
-            rk_beg[j] = kb; rk_len[j] = ke - kb; rv_beg[j] = vb; rv_len[j] = ve - vb;
+            if (lane == 0) { rk_beg[j] = kb; rk_len[j] = kn; rv_beg[j] = vb; rv_len[j] = vn; }
         }
 
         // ------------------------------------------------------------ a2: K dense
@@ -498,7 +512,68 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         __syncthreads();
         tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
 
-        // ------------- a3 + a4: K outliers, heavy pairs, online softmax (warp g, lane j)
+        // --------------------- a3: K outliers + heavy pairs, flat over the CTA's threads
+        {
+            int kl = rk_len[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, kl, o);
+                if (lane >= o) kl += y;
+            }
+            const int ktot = __shfl_sync(0xffffffffu, kl, 31);
+            for (int xb = warp * 32; xb < ktot; xb += ATT_THREADS) {
+                const int x = xb + lane;
+                int j = 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const int v = __shfl_sync(0xffffffffu, kl, j + o - 1);
+                    if (v <= x) j += o;
+                }
+                const int excl = __shfl_sync(0xffffffffu, kl, (j + 31) & 31);
+                if (x >= ktot) continue;
+                const uint32_t rec = krec((uint32_t)(rk_beg[j] + (x - (j ? excl : 0))));
+                const int ch = (int)(rec & 0xffffu);
+                const int kvl = (ch >> 7) - h0;
+                const int cc = ch & 127, i = cc & 63, up = cc >> 6;
+                const int bit = 2 * BITS * i;
+                const int wq = kvl * 4 * BITS + (bit >> 5);
+                unsigned long long w64 = kw_s[wq * 32 + j];
+                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                const int code = (pc >> (up * BITS)) & CM;
+                const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
+                const int cl = kvl * kHeadDim + cc;
+                const float delta = xval - (cbKs[code] * ks_s[cl] + kz_s[cl]);
+                const float2 cs = cis_s[i * 32 + j];
+#pragma unroll
+                for (int gg = 0; gg < G; ++gg) {
+                    const int g = kvl * G + gg;
+                    const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
+                    atomicAdd(&kcorr[g * 32 + j], delta * (up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y)));
+                }
+            }
+            // heavy RoPE pairs in fp32: items (head g, heavy slot, token j)
+            for (int x = tid; x < HG * HMAX * 32; x += ATT_THREADS) {
+                const int g = x / (HMAX * 32), hs = (x / 32) % HMAX, j = x & 31;
+                if (hs >= hv_n[g] || j >= ntok) continue;
+                const int i = hv_pair[g * 8 + hs];
+                const int bit = 2 * BITS * i;
+                const int wq = (g / G) * 4 * BITS + (bit >> 5);
+                unsigned long long w64 = kw_s[wq * 32 + j];
+                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
+                const float2 cs = cis_s[i * 32 + j];
+                atomicAdd(&kcorr[g * 32 + j], cs.x * ab.x + cs.y * ab.y);
+            }
+            // TMA producer for tile t + STAGES - 1 (the buffer of tile t-1 is free): the last
+            // warp issues here so that no warp's K phase waits on it
+            if (warp == ATT_WARPS - 1) issue(t + P.stages - 1, (it + P.stages - 1) % P.stages);
+        }
+        __syncthreads();
+        tc1 = clock64(); tm[0] += tc1 - tc0; tc0 = tc1;
+
+        // ------------------------------------------------------- a4: online softmax
         {
             float smax = lane < ntok ? vsz_s[lane].x : 0.f;
             smax = warp_max(smax);
@@ -510,44 +585,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 float s = 0.f;
 #pragma unroll
                 for (int w = 0; w < ATT_WARPS; ++w) s += red[(w * HG + g) * 32 + j];
-                s *= lut_inv[g];
-                const int gkv = h0 + g / G;             // global kv head of query head g
-                if (valid) {
-                    // Key outliers of (token j, kv head of g): x - K^(code) times dscore/dK
-                    const int rb = rk_beg[j], re = rb + rk_len[j];
-                    for (int r = rb; r < re; ++r) {
-                        const uint32_t rec = krec((uint32_t)r);
-                        const int ch = (int)(rec & 0xffffu);
-                        if ((ch >> 7) != gkv) continue;
-                        const int cc = ch & 127, i = cc & 63, up = cc >> 6;
-                        const int bit = 2 * BITS * i;
-                        const int wq = (g / G) * 4 * BITS + (bit >> 5);
-                        unsigned long long w64 = kw_s[wq * 32 + j];
-                        if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                        const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                        const int code = (pc >> (up * BITS)) & CM;
-                        const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
-                        const float delta = xval - (cbK[code] * ks[ch] + kz[ch]);
-                        const float2 cs = cis_s[i * 32 + j];
-                        const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
-                        s += delta * (up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y));
-                    }
-                    // heavy RoPE pairs of head g in fp32 (tables hlut)
-                    const int nh = hv_n[g];
-                    for (int hs = 0; hs < nh; ++hs) {
-                        const int i = hv_pair[g * 8 + hs];
-                        const int bit = 2 * BITS * i;
-                        const int wq = (g / G) * 4 * BITS + (bit >> 5);
-                        unsigned long long w64 = kw_s[wq * 32 + j];
-                        if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                        const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                        const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
-                        const float2 cs = cis_s[i * 32 + j];
-                        s += cs.x * ab.x + cs.y * ab.y;
-                    }
-                } else {
-                    s = -CUDART_INF_F;
-                }
+                s = valid ? s * lut_inv[g] + kcorr[g * 32 + j] : -CUDART_INF_F;
+                kcorr[g * 32 + j] = 0.f;
                 const float mt = warp_max(s);
                 const float m_new = fmaxf(m_run, mt);
                 const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
@@ -622,7 +661,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const int code = (int)((w64 >> (bit & 31)) & CM);
                 const float2 sz = vsz_s[j];
                 const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
-                const float delta = xval - (cbV[code] * sz.x + sz.y);
+                const float delta = xval - (cbVs[code] * sz.x + sz.y);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
                     const int g = kvl * G + gg;
