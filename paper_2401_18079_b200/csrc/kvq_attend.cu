@@ -1,29 +1,29 @@
 // kvq_attend.cu -- ATT: fused single-token decode attention over the compressed cache.
 //
-// One launch per attend:
-//   grid  = n_head_groups x splits (head group fastest), 256 threads, 1 CTA / SM.
-//   Staging: every 32-token tile of the CTA's head group (K code words, V code words,
-//          per-token (s,z), CSC pointers, Value and Key outlier records) is moved
-//          global -> shared by TMA bulk copies (cp.async.bulk + mbarrier complete_tx)
-//          into a STAGES-deep ring, issued STAGES-1 tiles ahead by warp 0, so the compute
-//          phases never wait on HBM latency.
-//   a1 QP  each CTA rotates its HG query heads with exact fp64 angles (R11, R12) and
-//          folds 1/sqrt(d) * log2(e) into q~.
-//   LUTs   K: per (query head g, RoPE pair i) a 2^{2b}-entry table of fp16 pairs
-//          (A, B) with  A = q~_i K^_i(a) + q~_i' K^_i'(b),  B = q~_i' K^_i(a) - q~_i K^_i'(b)
-//          for K^_c(a) = Chat_K[a] s_c + z_c -- the paper's per-channel LUT
-//          taken one step further: the query and the per-channel affine are folded in, so
-//          one lookup + 2 FMAs per RoPE pair yields  cos(n'th_i) A + sin(n'th_i) B, which
-//          is exactly the pair's contribution to q~ . RoPE(K^_n, n').
-//          Pairs carrying a heavy Key channel get fp32 tables (precision, DESIGN 9).
-//          V: the shared codebook as a pair table, lane-private copies (conflict-free).
-//   a2 KS  lane = token of the tile, warp w = RoPE pairs 8w..8w+7 for all heads;
-//          fp16 x fp16 -> fp32 FMAs (fma.rn.f32.f16).
-//   a3     Key outliers of the tile add (x - K^(code)) * dscore/dK (same launch).
-//   a4     exact online softmax in base 2 (running max, rescale on change).
-//   a5 PV  lane = CPL channels:  sum_n (p_n s_n) Chat_V[code] + sum_n p_n z_n  (affine fold).
-//   a6     Value outliers add p_n (v - V^(code)).
-//   a7 MRG the last CTA of each head group merges the split partials (log-sum-exp).
+// One launch per attend.  grid = n_head_groups x splits (head group
+// fastest), one CTA per SM, warp specialized:
+//   warp 16 (producer)  TMA bulk copies (cp.async.bulk + mbarrier complete_tx) of every
+//                       32-token tile of the CTA's head group -- K code words, V code words,
+//                       per-token (s,z), CSC pointers, Value and Key outlier records -- into a
+//                       STAGES-deep shared-memory ring; then compacts the tile's Key-outlier
+//                       records of this head group into a self-contained item list.
+//   warp 17 (producer)  compacts the tile's Value-outlier records of this head group.
+//   warps 0..15         compute, synchronized among themselves with a named barrier:
+//     a2+a3  K phase: RoPE-pair table lookups (lane = token, warp = 4 RoPE pairs, all
+//            heads of the group; fp16 x fp16 -> fp32 FMAs), Key-outlier and heavy-pair
+//            corrections in fp32 (flat over the item list, shared atomics);
+//     a4     online softmax in base 2 (warp g = head g; per-lane deferred sums);
+//     a5+a6  P.V: lane = CPL channels, sum_n (p_n s_n) Chat_V[code] + sum_n p_n z_n
+//            (affine fold), Value-outlier corrections flat over the item list;
+//     a7     the last CTA of each head group merges the split partials (log-sum-exp).
+//   Tables (built per CTA, a1): q~ = RoPE(q, pos) with exact fp64 angles (R11, R12) times
+//   log2(e)/sqrt(d); per (query head g, RoPE pair i) a 2^{2b}-entry table of fp16 pairs
+//   (A, B), A = q~_i K^_i(a) + q~_i' K^_i'(b), B = q~_i' K^_i(a) - q~_i K^_i'(b) with
+//   K^_c(a) = Chat_K[a] s_c + z_c: the paper's per-channel LUT with the query
+//   and the affine folded in, so one lookup + 2 FMAs give cos(n' th_i) A + sin(n' th_i) B,
+//   exactly the pair's share of q~ . RoPE(K^_n, n') (RoPE after dequantization, P:379,
+//   P:730).  Pairs carrying a heavy Key channel use fp32 tables.  V: the
+//   shared codebook as a pair table, one private copy per lane (conflict free).
 #include "kvq_internal.cuh"
 
 #include <math_constants.h>
@@ -31,9 +31,13 @@
 namespace kvq {
 namespace {
 
-constexpr int ATT_THREADS = 512;
-constexpr int ATT_WARPS = 16;
-constexpr int KPW = kPairs / ATT_WARPS;   // RoPE pairs per warp in the K phase
+constexpr int NCW = 16;                       // compute warps
+constexpr int NCT = NCW * 32;                 // compute threads
+constexpr int ATT_THREADS = NCT + 64;         // + 2 producer warps
+constexpr int PW_K = NCW;                     // producer warp ids: NCW (TMA + K), NCW+1 (V)
+constexpr int KPW = kPairs / NCW;             // RoPE pairs per compute warp in the K phase
+constexpr int KITEM_CAP = 512;                // compacted records per tile and stage
+constexpr int VITEM_CAP = 512;
 
 // ------------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -49,6 +53,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
     asm volatile(
@@ -69,6 +76,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+// named barrier among the compute warps only (the producer warps never join it)
+__device__ __forceinline__ void compute_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
 }
 
 // acc += lo(x)*lo(y) ; acc2 += hi(x)*hi(y)   (fp16 products, fp32 accumulation)
@@ -107,29 +118,31 @@ __device__ __forceinline__ float warp_sum(float v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+// warp max of floats with one REDUX via an order-preserving integer map
+__device__ __forceinline__ float warp_max_redux(float v) {
+    unsigned u = __float_as_uint(v);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    u = __reduce_max_sync(0xffffffffu, u);
+    u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+    return __uint_as_float(u);
+}
 
 // ---------------------------------------------------------------- configuration --
-constexpr int cpl_for(int bits, int /*hg*/) {
-    // V channels per lane: whole 32-bit words of codes per lane (b=4: 8, b=2/3: 32);
-    // one (head, token-group) task per warp needs HG * 128/CPL <= 16 (see caps below)
-    return bits == 4 ? 8 : 32;
-}
+constexpr int cpl_for(int bits) { return bits == 4 ? 8 : 32; }   // whole code words per lane
 
 template <int BITS, int HG>
 struct Cfg {
     static constexpr int NE = 1 << (2 * BITS);
     static constexpr int HMAX = BITS == 4 ? 4 : 8;   // fp32 "heavy" pairs per head
-    static constexpr int CPL = cpl_for(BITS, HG);
+    static constexpr int CPL = cpl_for(BITS);
     static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
     static constexpr size_t vlut = (size_t)NE * 32 * 4;
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
-    static constexpr size_t cis = (size_t)kPairs * 32 * 8;
+    static constexpr size_t t1 = (size_t)kPairs * 32 * 8;
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
-        + ATT_WARPS * HG * 32 * 4      /* red */
+        + NCW * HG * 32 * 4            /* red */
         + HG * 32 * 4 * 2              /* p, kcorr */
-        + 4 * 33 * 4                   /* per-token record sub-ranges + prefix */
-        + HG * kHeadDim * 4 * 2 + 64 * 4 /* staged s_c, z_c of the group, codebooks */
         + HG * 32 * 2                  /* w16 */
         + HG * kHeadDim * 4            /* osp */
         + 64 * 16 * 3 + 64 * 8         /* anc64, rot64, qcis, anc32 */
@@ -137,8 +150,9 @@ struct Cfg {
         + HG * 4 * 8                   /* per-head scalars */
         + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
         + HG * 16 * 4                  /* heavy pair list + counts */
+        + HG * kHeadDim * 4 * 2 + 64 * 4 /* staged s_c, z_c of the group, codebooks */
         + 256;
-    static constexpr size_t fixed = klut + vlut + hlut + cis + small;
+    static constexpr size_t fixed = klut + vlut + hlut + t1 + small;
 };
 
 struct Params {
@@ -153,9 +167,15 @@ struct Params {
     // stage ring layout (bytes), computed on the host
     int stages;
     int krec_cap;        // u32 records per stage buffer (multiple of 4)
-    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kptr, so_vrec, so_krec;
+    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kptr, so_vrec, so_krec, so_kit, so_vit,
+        so_hdr;
     unsigned long long *timers;   // optional [8] phase cycle sums (diagnostics), may be null
 };
+
+// compacted outlier item: fp16 value << 16 | token (5 bits) << 11 | channel in group (11 bits)
+__device__ __forceinline__ uint32_t make_item(uint32_t rec, int j, int c_lo) {
+    return (rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)((int)(rec & 0xffffu) - c_lo);
+}
 
 template <int BITS, int HG, int G>
 __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params P) {
@@ -173,18 +193,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     uint32_t *klut = reinterpret_cast<uint32_t *>(sp); sp += C::klut;
     uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
     float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
-    float2 *cis_s = reinterpret_cast<float2 *>(sp); sp += C::cis;
+    float2 *t1tab = reinterpret_cast<float2 *>(sp); sp += C::t1;   // cis(j theta_i) [i][j]
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
-    float *red = reinterpret_cast<float *>(sp); sp += ATT_WARPS * HG * 32 * 4;
+    float *red = reinterpret_cast<float *>(sp); sp += NCW * HG * 32 * 4;
     float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
     float *kcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
-    int *rk_beg = reinterpret_cast<int *>(sp); sp += 33 * 4;   // K records of this head group
-    int *rk_len = reinterpret_cast<int *>(sp); sp += 33 * 4;
-    int *rv_beg = reinterpret_cast<int *>(sp); sp += 33 * 4;   // V records of this head group
-    int *rv_len = reinterpret_cast<int *>(sp); sp += 33 * 4;
-    float *ks_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;   // s_c of the group's channels
-    float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
-    float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
     float *osp = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
     double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
@@ -192,7 +205,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float2 *anc32 = reinterpret_cast<float2 *>(sp); sp += 64 * 8;
     float *theta32 = reinterpret_cast<float *>(sp); sp += 64 * 4;
     float *lut_inv = reinterpret_cast<float *>(sp); sp += HG * 4;
-    float *alpha_s = reinterpret_cast<float *>(sp); sp += HG * 4;
+    float *lut_sc = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *beta_s = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *m_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *l_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
@@ -202,8 +215,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     uint8_t *heavy_s = reinterpret_cast<uint8_t *>(sp); sp += HG * 64;
     int *hv_pair = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
     int *hv_n = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
+    float *ks_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;   // s_c of the group
+    float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
+    float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
     int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 64);
+    // barriers just below the stage ring: full[S], ready[S], empty[S]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
+    uint64_t *full_b = bars, *ready_b = bars + 4, *empty_b = bars + 8;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
@@ -213,60 +231,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     const int h0 = g0 / G;           // first KV head
     const int t_begin = (int)((int64_t)split * P.ntiles / P.S);
     const int t_end = (int)((int64_t)(split + 1) * P.ntiles / P.S);
+    const int ntl = t_end - t_begin;
     const int D = c.D;
     const int kv = c.kv;
     const float *ks = c.kpar, *kz = c.kpar + D;
     const float *cbK = c.cb + 16, *cbV = c.cb + 48;   // decode codebooks
+    const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
 
     auto stage_ptr = [&](int st) -> unsigned char * { return smem_raw + P.st_base + (size_t)st * P.st_bytes; };
 
-    // ----------------------------------------------------------- TMA producer
-    // kp_lo/kp_hi: CSC pointers of the next tile to issue (prefetched one issue ahead)
-    uint32_t kp_lo = 0, kp_hi = 0;
-    auto kptr_at = [&](int t, uint32_t &lo, uint32_t &hi) {
-        const int64_t n0 = (int64_t)t * 32;
-        const int64_t n1 = n0 + 32 < P.T ? n0 + 32 : P.T;
-        lo = __ldg(c.kptr + n0);
-        hi = __ldg(c.kptr + n1);
-    };
-    auto issue = [&](int t, int st) {   // producer warp only
-        if (t >= t_end) return;
-        unsigned char *sb = stage_ptr(st);
-        uint64_t *bar = bars + st;
-        const uint32_t klo = __shfl_sync(0xffffffffu, kp_lo, 0);
-        const uint32_t khi = __shfl_sync(0xffffffffu, kp_hi, 0);
-        const uint32_t ka = klo & ~3u;
-        uint32_t kn = ((khi + 3u) & ~3u) - ka;
-        if (kn > (uint32_t)P.krec_cap) kn = (uint32_t)P.krec_cap;
-        const unsigned b_kw = 32u * QWC * 4u;
-        const unsigned b_vrec = 32u * (unsigned)kv * 4u;
-        const unsigned total = 2u * b_kw + 256u + 192u + b_vrec + kn * 4u;
-        if (lane == 0) {
-            fence_proxy_async();
-            mbar_expect_tx(bar, total);
-        }
-        __syncwarp();
-        const int64_t n0 = (int64_t)t * 32;
-        if (lane == 0)
-            bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)t * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
-        if (lane == 1) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
-        if (lane == 2) bulk_g2s(sb + P.so_kptr, c.kptr + n0, 192u, bar);
-        if (lane == 3 && b_vrec) bulk_g2s(sb + P.so_vrec, c.vout + n0 * kv, b_vrec, bar);
-        if (lane == 4 && kn) bulk_g2s(sb + P.so_krec, c.kout + ka, kn * 4u, bar);
-        if (lane == 5)
-            bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)t * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
-        // prefetch the CSC range of the tile after this one
-        if (lane == 0 && t + 1 < t_end) kptr_at(t + 1, kp_lo, kp_hi);
-    };
-
     if (tid == 0) {
-        for (int s = 0; s < P.stages; ++s) mbar_init(bars + s, 1);
+        for (int s = 0; s < P.stages; ++s) {
+            mbar_init(full_b + s, 1);
+            mbar_init(ready_b + s, 2);
+            mbar_init(empty_b + s, 1);
+        }
         mbar_fence_init();
-    }
-    __syncthreads();
-    if (warp == ATT_WARPS - 1) {   // the producer warp (also issues inside the tile loop)
-        if (lane == 0 && t_begin < t_end) kptr_at(t_begin, kp_lo, kp_hi);
-        for (int s = 0; s < P.stages - 1; ++s) issue(t_begin + s, s);
     }
 
     // ---------------------------------------------------------------- prologue
@@ -284,10 +264,17 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         sincos(32.0 * th, &s, &co);
         rot64[i] = make_double2(co, s);
     }
+    for (int x = tid; x < kPairs * 32; x += ATT_THREADS) {
+        const int i = x >> 5, j = x & 31;
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)j * th, &s, &co);
+        t1tab[x] = make_float2((float)co, (float)s);
+    }
     for (int x = tid; x < HG * kHeadDim; x += ATT_THREADS) osp[x] = 0.f;
     for (int x = tid; x < HKV * kHeadDim; x += ATT_THREADS) {
-        ks_s[x] = ks[h0 * kHeadDim + x];
-        kz_s[x] = kz[h0 * kHeadDim + x];
+        ks_s[x] = ks[c_lo + x];
+        kz_s[x] = kz[c_lo + x];
     }
     if (tid < 64) cb_s[tid] = c.cb[tid];
     for (int x = tid; x < HG * 32; x += ATT_THREADS) kcorr[x] = 0.f;
@@ -310,15 +297,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // bound.
     for (int x = tid; x < HG * 64; x += ATT_THREADS) {
         const int g = x >> 6, i = x & 63;
-        const int kvh = (g0 + g) / G;
-        const int ci = kvh * kHeadDim + i, cj = ci + 64;
-        const float mx = fmaxf(fabsf(cbK[0] * ks[ci] + kz[ci]), fabsf(cbK[CM] * ks[ci] + kz[ci]));
-        const float my = fmaxf(fabsf(cbK[0] * ks[cj] + kz[cj]), fabsf(cbK[CM] * ks[cj] + kz[cj]));
+        const int ci = (g / G) * kHeadDim + i, cj = ci + 64;
+        const float mx = fmaxf(fabsf(cbK[0] * ks_s[ci] + kz_s[ci]), fabsf(cbK[CM] * ks_s[ci] + kz_s[ci]));
+        const float my = fmaxf(fabsf(cbK[0] * ks_s[cj] + kz_s[cj]), fabsf(cbK[CM] * ks_s[cj] + kz_s[cj]));
         const float qa = fabsf(qs[g * kHeadDim + i]), qb = fabsf(qs[g * kHeadDim + i + 64]);
         bound_s[x] = fmaxf(qa * mx + qb * my, qb * mx + qa * my);
     }
     __syncthreads();
-    for (int g = warp; g < HG; g += ATT_WARPS) {
+    for (int g = warp; g < HG; g += ATT_THREADS / 32) {
         const float b0 = bound_s[g * 64 + lane], b1 = bound_s[g * 64 + 32 + lane];
         const float M = warp_max(fmaxf(b0, b1));
         float tau = 0.25f * M;
@@ -340,44 +326,34 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             int e = 0;     // scale so that |entry| <= 2^14 (fp16 max 65504)
             if (rest > 0.f && isfinite(rest)) e = 14 - ilogbf(rest) - 1;
             e = max(-100, min(100, e));
-            alpha_s[g] = ldexpf(1.f, e);      // temp: table scale
+            lut_sc[g] = ldexpf(1.f, e);
             lut_inv[g] = ldexpf(1.f, -e);
         }
     }
     __syncthreads();
-    // K table entries
-    for (int x = tid; x < HG * 64; x += ATT_THREADS) {
-        const int g = x >> 6, i = x & 63;
-        const int kvh = (g0 + g) / G;
-        const int ci = kvh * kHeadDim + i, cj = ci + 64;
-        const float sc = alpha_s[g];
+    // K table entries: one (head, pair, second code) row of 2^b entries per work item
+    for (int x = tid; x < HG * 64 * (CM + 1); x += ATT_THREADS) {
+        const int bb = x % (CM + 1), gi = x / (CM + 1);
+        const int g = gi >> 6, i = gi & 63;
+        const int ci = (g / G) * kHeadDim + i, cj = ci + 64;
+        const float sc = lut_sc[g];
         const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
         const float qa = qa1 * sc, qb = qb1 * sc;
-        float X[1 << BITS], Y[1 << BITS];
-#pragma unroll
-        for (int a = 0; a <= CM; ++a) {
-            X[a] = cbK[a] * ks[ci] + kz[ci];
-            Y[a] = cbK[a] * ks[cj] + kz[cj];
-        }
-        uint32_t *dst = klut + (size_t)(g * 64 + i) * NE;
-        const bool heavy = heavy_s[x] != 0;
+        const float yb = cbK[bb] * ks_s[cj] + kz_s[cj];
+        uint32_t *dst = klut + (size_t)(g * 64 + i) * NE + (bb << BITS);
+        const bool heavy = heavy_s[gi] != 0;
         int hslot = 0;
         if (heavy)
             for (int u = 0; u < hv_n[g]; ++u) hslot = hv_pair[g * 8 + u] == i ? u : hslot;
-#pragma unroll 1
-        for (int bb = 0; bb <= CM; ++bb) {
-            float yb = 0.f;
 #pragma unroll
-            for (int u = 0; u <= CM; ++u) yb = (u == bb) ? Y[u] : yb;
-#pragma unroll
-            for (int a = 0; a <= CM; ++a) {
-                const int e = a | (bb << BITS);
-                if (heavy) {
-                    dst[e] = 0u;
-                    hlut[(g * HMAX + hslot) * NE + e] = make_float2(qa1 * X[a] + qb1 * yb, qb1 * X[a] - qa1 * yb);
-                } else {
-                    dst[e] = pack_half2(qa * X[a] + qb * yb, qb * X[a] - qa * yb);
-                }
+        for (int a = 0; a <= CM; ++a) {
+            const float xa = cbK[a] * ks_s[ci] + kz_s[ci];
+            if (heavy) {
+                dst[a] = 0u;
+                hlut[(g * HMAX + hslot) * NE + (bb << BITS) + a] =
+                    make_float2(qa1 * xa + qb1 * yb, qb1 * xa - qa1 * yb);
+            } else {
+                dst[a] = pack_half2(qa * xa + qb * yb, qb * xa - qa * yb);
             }
         }
     }
@@ -386,24 +362,133 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const int e = x >> 5;
         vlut[x] = pack_half2(cbV[e & CM], cbV[e >> BITS]);
     }
+    __syncthreads();
 
-    // per-lane constants for the K phase: cis(j * theta_i) for this warp's KPW pairs
-    float t1c[KPW], t1s[KPW];
+    // ================================================================= producers
+    if (warp >= NCW) {
+        const bool kwarp = warp == PW_K;
+        uint32_t kp_lo = 0, kp_hi = 0;      // CSC range of the next tile to issue (lane 0)
+        auto kptr_at = [&](int t) {
+            const int64_t n0 = (int64_t)t * 32;
+            const int64_t n1 = n0 + 32 < P.T ? n0 + 32 : P.T;
+            kp_lo = __ldg(c.kptr + n0);
+            kp_hi = __ldg(c.kptr + n1);
+        };
+        if (kwarp && lane == 0 && ntl > 0) kptr_at(t_begin);
+        const int Sg = P.stages;
+        for (int it = 0; it < ntl + Sg - 1; ++it) {
+            // ---- compact the outliers of tile tc (its data landed S-1 issues ago)
+            const int ic = it - (Sg - 1);
+            if (ic >= 0) {
+                const int sc = ic % Sg;
+                const int tcur = t_begin + ic;
+                mbar_wait(full_b + sc, (unsigned)((ic / Sg) & 1));
+                unsigned char *sb = stage_ptr(sc);
+                const uint32_t *kptr_s = reinterpret_cast<const uint32_t *>(sb + P.so_kptr);
+                int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
+                const int ntok = (int)min((int64_t)32, P.T - (int64_t)tcur * 32);
+                const int j = lane;
+                if (kwarp) {
+                    const uint32_t *krec_s = reinterpret_cast<const uint32_t *>(sb + P.so_krec);
+                    uint32_t *kit = reinterpret_cast<uint32_t *>(sb + P.so_kit);
+                    const uint32_t ka = kptr_s[0] & ~3u;
+                    auto krec = [&](uint32_t r) -> uint32_t {
+                        const uint32_t off = r - ka;
+                        if (off < (uint32_t)P.krec_cap) return krec_s[off];
+                        return __ldcg(c.kout + r);
+                    };
+                    uint32_t a = 0, e = 0;
+                    if (j < ntok) {
+                        const uint32_t r0 = kptr_s[j], r1 = kptr_s[j + 1];
+                        a = r0; e = r1;
+                        while (a < e) { const uint32_t m = (a + e) >> 1; if ((int)(krec(m) & 0xffffu) < c_lo) a = m + 1; else e = m; }
+                        uint32_t b = a; e = r1;
+                        while (b < e) { const uint32_t m = (b + e) >> 1; if ((int)(krec(m) & 0xffffu) < c_hi) b = m + 1; else e = m; }
+                        e = b;
+                    }
+                    const int cnt = (int)(e - a);
+                    int incl = cnt;
 #pragma unroll
-    for (int k = 0; k < KPW; ++k) {
-        const int i = warp * KPW + k;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
-        float s, co;
-        sincosf((float)((double)lane * th), &s, &co);
-        t1c[k] = co;
-        t1s[k] = s;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                    int pos = incl - cnt;
+                    for (uint32_t r = a; r < e && pos < KITEM_CAP; ++r, ++pos) kit[pos] = make_item(krec(r), j, c_lo);
+                    if (lane == 0) { hdr[0] = min(tot, KITEM_CAP); hdr[2] = tot > KITEM_CAP; }
+                    // overflow (pathological tiles): the rest of the records are handled by
+                    // the compute warps from the per-token ranges
+                    hdr[8 + j] = (int)a;
+                    hdr[8 + 32 + j] = (int)e;
+                } else {
+                    const uint32_t *vrec_s = reinterpret_cast<const uint32_t *>(sb + P.so_vrec);
+                    uint32_t *vit = reinterpret_cast<uint32_t *>(sb + P.so_vit);
+                    int a = 0, e = 0;
+                    if (j < ntok && kv > 0) {
+                        a = j * kv; e = (j + 1) * kv;
+                        while (a < e) { const int m = (a + e) >> 1; if ((int)(vrec_s[m] & 0xffffu) < c_lo) a = m + 1; else e = m; }
+                        int b = a; e = (j + 1) * kv;
+                        while (b < e) { const int m = (b + e) >> 1; if ((int)(vrec_s[m] & 0xffffu) < c_hi) b = m + 1; else e = m; }
+                        e = b;
+                    }
+                    const int cnt = e - a;
+                    int incl = cnt;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                    int pos = incl - cnt;
+                    for (int r = a; r < e && pos < VITEM_CAP; ++r, ++pos) vit[pos] = make_item(vrec_s[r], j, c_lo);
+                    if (lane == 0) { hdr[1] = min(tot, VITEM_CAP); hdr[3] = tot > VITEM_CAP; }
+                    hdr[8 + 64 + j] = a;
+                    hdr[8 + 96 + j] = e;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(ready_b + sc);
+            }
+            // ---- issue tile ti into its stage once the compute warps released it
+            const int ti = t_begin + it;
+            if (kwarp && ti < t_end) {
+                const int si = it % Sg;
+                if (it >= Sg) mbar_wait(empty_b + si, (unsigned)(((it / Sg) - 1) & 1));
+                unsigned char *sb = stage_ptr(si);
+                uint64_t *bar = full_b + si;
+                const uint32_t klo = __shfl_sync(0xffffffffu, kp_lo, 0);
+                const uint32_t khi = __shfl_sync(0xffffffffu, kp_hi, 0);
+                const uint32_t ka = klo & ~3u;
+                uint32_t kn = ((khi + 3u) & ~3u) - ka;
+                if (kn > (uint32_t)P.krec_cap) kn = (uint32_t)P.krec_cap;
+                const unsigned b_kw = 32u * QWC * 4u;
+                const unsigned b_vrec = 32u * (unsigned)kv * 4u;
+                const unsigned total = 2u * b_kw + 256u + 192u + b_vrec + kn * 4u;
+                if (lane == 0) {
+                    fence_proxy_async();
+                    mbar_expect_tx(bar, total);
+                }
+                __syncwarp();
+                const int64_t n0 = (int64_t)ti * 32;
+                if (lane == 0)
+                    bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
+                if (lane == 1)
+                    bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
+                if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
+                if (lane == 3) bulk_g2s(sb + P.so_kptr, c.kptr + n0, 192u, bar);
+                if (lane == 4 && b_vrec) bulk_g2s(sb + P.so_vrec, c.vout + n0 * kv, b_vrec, bar);
+                if (lane == 5 && kn) bulk_g2s(sb + P.so_krec, c.kout + ka, kn * 4u, bar);
+                if (lane == 0 && ti + 1 < t_end) kptr_at(ti + 1);
+            }
+        }
     }
 
+    // =========================================================== compute warps
     // V-phase task mapping: one (query head, token group) task per warp
     constexpr int LH = kHeadDim / CPL;          // lanes per token per head
     constexpr int TPW = 32 / LH;                // tokens per warp task
     constexpr int NTASK = HG * (32 / TPW);      // tasks per tile
-    static_assert(NTASK <= ATT_WARPS, "V tasks must fit the CTA's warps");
+    static_assert(NTASK <= NCW, "V tasks must fit the compute warps");
     const bool vtask = warp < NTASK;
     const int vh = vtask ? warp / (32 / TPW) : 0;            // local query head
     const int vj = (warp % (32 / TPW)) * TPW + lane / LH;    // token in the tile
@@ -412,300 +497,258 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float acc[CPL];
 #pragma unroll
     for (int x = 0; x < CPL; ++x) acc[x] = 0.f;
-
-    // running softmax state (S-phase warps: warp g <-> head g)
-    float m_run = -CUDART_INF_F, l_run = 0.f, z_run = 0.f;
+    // running softmax state (warp g <-> head g): max per warp, deferred per-lane sums
+    float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;
     int E_cur = -126;     // dense V accumulator units: 2^E_cur (CTA uniform)
-
-    const int kbit0 = 2 * BITS * KPW * warp;
-    const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
-    const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
-    __syncthreads();
-
     unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
-    long long tc0 = clock64(), tc1;
-    const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
-    for (int t = t_begin; t < t_end; ++t) {
-        const int it = t - t_begin;
-        const int st = it % P.stages;
-        mbar_wait(bars + st, (unsigned)((it / P.stages) & 1));
-        tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
-        unsigned char *sb = stage_ptr(st);
-        const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
-        const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
-        const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
-        const uint32_t *kptr_s = reinterpret_cast<const uint32_t *>(sb + P.so_kptr);
-        const uint32_t *vrec_s = reinterpret_cast<const uint32_t *>(sb + P.so_vrec);
-        const uint32_t *krec_s = reinterpret_cast<const uint32_t *>(sb + P.so_krec);
-        const int64_t n0 = (int64_t)t * 32;
-        const int ntok = (int)min((int64_t)32, P.T - n0);
-        const uint32_t ka = kptr_s[0] & ~3u;
-        auto krec = [&](uint32_t r) -> uint32_t {
-            const uint32_t off = r - ka;
-            if (off < (uint32_t)P.krec_cap) return krec_s[off];
-            return __ldcg(c.kout + r);    // beyond the staged window (very dense tiles)
-        };
 
-        // ---- per-token record sub-ranges of this head group: records are channel-sorted,
-        //      so the first record >= c is popc(ballot(ch < c)) past the token's start
-        for (int j = warp; j < 32; j += ATT_WARPS) {
-            int kb = 0, kn = 0, vb = 0, vn = 0;
-            if (j < ntok) {
-                const uint32_t r0 = kptr_s[j], r1 = kptr_s[j + 1];
-                int below_lo = 0, below_hi = 0;
-                for (uint32_t rb = r0; rb < r1; rb += 32) {
-                    const uint32_t r = rb + lane;
-                    const int ch = r < r1 ? (int)(krec(r) & 0xffffu) : 0x7fffffff;
-                    below_lo += __popc(__ballot_sync(0xffffffffu, ch < c_lo));
-                    below_hi += __popc(__ballot_sync(0xffffffffu, ch < c_hi));
-                }
-                kb = (int)r0 + below_lo;
-                kn = below_hi - below_lo;
-                below_lo = below_hi = 0;
-                for (int rb = 0; rb < kv; rb += 32) {
-                    const int r = rb + lane;
-                    const int ch = r < kv ? (int)(vrec_s[j * kv + r] & 0xffffu) : 0x7fffffff;
-                    below_lo += __popc(__ballot_sync(0xffffffffu, ch < c_lo));
-                    below_hi += __popc(__ballot_sync(0xffffffffu, ch < c_hi));
-                }
-                vb = j * kv + below_lo;
-                vn = below_hi - below_lo;
-            }
-            if (lane == 0) { rk_beg[j] = kb; rk_len[j] = kn; rv_beg[j] = vb; rv_len[j] = vn; }
+    if (warp < NCW) {
+        // per-lane constants for the K phase: cis(j * theta_i) for this warp's KPW pairs
+        float t1c[KPW], t1s[KPW];
+#pragma unroll
+        for (int k = 0; k < KPW; ++k) {
+            const float2 v = t1tab[(warp * KPW + k) * 32 + lane];
+            t1c[k] = v.x;
+            t1s[k] = v.y;
         }
+        const int kbit0 = 2 * BITS * KPW * warp;
+        const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
+        const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
+        long long tc0 = clock64(), tc1;
 
-        // ------------------------------------------------------------ a2: K dense
-        {
-            float acc_c[HG], acc_s[HG];
-#pragma unroll
-            for (int g = 0; g < HG; ++g) { acc_c[g] = 0.f; acc_s[g] = 0.f; }
-            unsigned long long win[HKV];
-#pragma unroll
-            for (int h = 0; h < HKV; ++h) {
-                unsigned long long w64 = kw_s[(h * 4 * BITS + kq0) * 32 + lane];
-                if (kshift + 2 * BITS * KPW > 32)
-                    w64 |= (unsigned long long)kw_s[(h * 4 * BITS + kq0 + 1) * 32 + lane] << 32;
-                win[h] = w64 >> kshift;
-            }
-#pragma unroll
-            for (int k = 0; k < KPW; ++k) {
-                const int i = warp * KPW + k;
-                const float2 an = anc32[i];
-                const float cc = an.x * t1c[k] - an.y * t1s[k];
-                const float ss = an.x * t1s[k] + an.y * t1c[k];
-                const uint32_t cs = pack_half2(cc, ss);
-                cis_s[i * 32 + lane] = make_float2(cc, ss);
-#pragma unroll
-                for (int h = 0; h < HKV; ++h) {
-                    const int pc = (int)((win[h] >> (2 * BITS * k)) & (NE - 1));
-#pragma unroll
-                    for (int gg = 0; gg < G; ++gg) {
-                        const int g = h * G + gg;
-                        const uint32_t ab = klut[(g * 64 + i) * NE + pc];
-                        fma2_f16_f32(ab, cs, acc_c[g], acc_s[g]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int g = 0; g < HG; ++g) red[(warp * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
-        }
-        __syncthreads();
-        tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
+        for (int t = t_begin; t < t_end; ++t) {
+            const int it = t - t_begin;
+            const int st = it % P.stages;
+            mbar_wait(ready_b + st, (unsigned)((it / P.stages) & 1));
+            mbar_wait(full_b + st, (unsigned)((it / P.stages) & 1));
+            tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
+            unsigned char *sb = stage_ptr(st);
+            const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
+            const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
+            const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
+            const uint32_t *kit = reinterpret_cast<const uint32_t *>(sb + P.so_kit);
+            const uint32_t *vit = reinterpret_cast<const uint32_t *>(sb + P.so_vit);
+            const int *hdr = reinterpret_cast<const int *>(sb + P.so_hdr);
+            const int64_t n0 = (int64_t)t * 32;
+            const int ntok = (int)min((int64_t)32, P.T - n0);
 
-        // --------------------- a3: K outliers + heavy pairs, flat over the CTA's threads
-        {
-            int kl = rk_len[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, kl, o);
-                if (lane >= o) kl += y;
-            }
-            const int ktot = __shfl_sync(0xffffffffu, kl, 31);
-            for (int xb = warp * 32; xb < ktot; xb += ATT_THREADS) {
-                const int x = xb + lane;
-                int j = 0;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const int v = __shfl_sync(0xffffffffu, kl, j + o - 1);
-                    if (v <= x) j += o;
-                }
-                const int excl = __shfl_sync(0xffffffffu, kl, (j + 31) & 31);
-                if (x >= ktot) continue;
-                const uint32_t rec = krec((uint32_t)(rk_beg[j] + (x - (j ? excl : 0))));
-                const int ch = (int)(rec & 0xffffu);
-                const int kvl = (ch >> 7) - h0;
-                const int cc = ch & 127, i = cc & 63, up = cc >> 6;
+            // K-outlier correction of one compacted item (fp32, shared atomics)
+            auto k_item = [&](uint32_t itm) {
+                const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                const int kvl = chl >> 7, cc = chl & 127, i = cc & 63, up = cc >> 6;
                 const int bit = 2 * BITS * i;
                 const int wq = kvl * 4 * BITS + (bit >> 5);
                 unsigned long long w64 = kw_s[wq * 32 + j];
                 if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
                 const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
                 const int code = (pc >> (up * BITS)) & CM;
-                const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
-                const int cl = kvl * kHeadDim + cc;
-                const float delta = xval - (cbKs[code] * ks_s[cl] + kz_s[cl]);
-                const float2 cs = cis_s[i * 32 + j];
+                const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+                const float delta = xval - (cbKs[code] * ks_s[chl] + kz_s[chl]);
+                const float2 an = anc32[i], tt = t1tab[i * 32 + j];
+                const float co = an.x * tt.x - an.y * tt.y, si = an.x * tt.y + an.y * tt.x;
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
                     const int g = kvl * G + gg;
                     const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
-                    atomicAdd(&kcorr[g * 32 + j], delta * (up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y)));
+                    atomicAdd(&kcorr[g * 32 + j], delta * (up ? (qb * co - qa * si) : (qa * co + qb * si)));
+                }
+            };
+
+            // ------------------------------------------ a3: K outliers, heavy pairs
+            {
+                const int nk = hdr[0];
+                for (int x = tid; x < nk; x += NCT) k_item(kit[x]);
+                if (hdr[2]) {
+                    // overflowed item list: remaining records straight from the CSC arrays
+                    int skip = KITEM_CAP;
+                    for (int j = 0; j < ntok; ++j) {
+                        const int b = hdr[8 + j], e = hdr[8 + 32 + j];
+                        const int s0 = min(e - b, skip);
+                        skip -= s0;
+                        for (int r = b + s0 + tid; r < e; r += NCT)
+                            k_item(make_item(__ldcg(c.kout + r), j, c_lo));
+                    }
+                }
+                for (int x = tid; x < HG * HMAX * 32; x += NCT) {
+                    const int g = x / (HMAX * 32), hs = (x / 32) % HMAX, j = x & 31;
+                    if (hs >= hv_n[g] || j >= ntok) continue;
+                    const int i = hv_pair[g * 8 + hs];
+                    const int bit = 2 * BITS * i;
+                    const int wq = (g / G) * 4 * BITS + (bit >> 5);
+                    unsigned long long w64 = kw_s[wq * 32 + j];
+                    if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                    const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                    const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
+                    const float2 an = anc32[i], tt = t1tab[i * 32 + j];
+                    const float co = an.x * tt.x - an.y * tt.y, si = an.x * tt.y + an.y * tt.x;
+                    atomicAdd(&kcorr[g * 32 + j], co * ab.x + si * ab.y);
                 }
             }
-            // heavy RoPE pairs in fp32: items (head g, heavy slot, token j)
-            for (int x = tid; x < HG * HMAX * 32; x += ATT_THREADS) {
-                const int g = x / (HMAX * 32), hs = (x / 32) % HMAX, j = x & 31;
-                if (hs >= hv_n[g] || j >= ntok) continue;
-                const int i = hv_pair[g * 8 + hs];
-                const int bit = 2 * BITS * i;
-                const int wq = (g / G) * 4 * BITS + (bit >> 5);
-                unsigned long long w64 = kw_s[wq * 32 + j];
-                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
-                const float2 cs = cis_s[i * 32 + j];
-                atomicAdd(&kcorr[g * 32 + j], cs.x * ab.x + cs.y * ab.y);
-            }
-            // TMA producer for tile t + STAGES - 1 (the buffer of tile t-1 is free): the last
-            // warp issues here so that no warp's K phase waits on it
-            if (warp == ATT_WARPS - 1) issue(t + P.stages - 1, (it + P.stages - 1) % P.stages);
-        }
-        __syncthreads();
-        tc1 = clock64(); tm[0] += tc1 - tc0; tc0 = tc1;
-
-        // ------------------------------------------------------- a4: online softmax
-        {
-            float smax = lane < ntok ? vsz_s[lane].x : 0.f;
-            smax = warp_max(smax);
-            int E_new = E_cur;
-            if (smax > 0.f) E_new = max(E_cur, ilogbf(smax) + 1);
-            for (int g = warp; g < HG; g += ATT_WARPS) {
-                const int j = lane;
-                const bool valid = j < ntok;
-                float s = 0.f;
+            // ------------------------------------------------------------ a2: K dense
+            {
+                float acc_c[HG], acc_s[HG];
 #pragma unroll
-                for (int w = 0; w < ATT_WARPS; ++w) s += red[(w * HG + g) * 32 + j];
-                s = valid ? s * lut_inv[g] + kcorr[g * 32 + j] : -CUDART_INF_F;
-                kcorr[g * 32 + j] = 0.f;
-                const float mt = warp_max(s);
-                const float m_new = fmaxf(m_run, mt);
-                const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
-                const float p = valid ? exp2f(s - m_new) : 0.f;
-                const float2 sz = valid ? vsz_s[j] : make_float2(0.f, 0.f);
-                l_run = l_run * alpha + warp_sum(p);
-                z_run = z_run * alpha + warp_sum(p * sz.y);
-                m_run = m_new;
-                p_s[g * 32 + j] = p;
-                w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * ldexpf(sz.x, -E_new)));
-                if (alpha != 1.f) {
+                for (int g = 0; g < HG; ++g) { acc_c[g] = 0.f; acc_s[g] = 0.f; }
+                unsigned long long win[HKV];
 #pragma unroll
-                    for (int x = 0; x < kHeadDim / 32; ++x) osp[g * kHeadDim + x * 32 + lane] *= alpha;
+                for (int h = 0; h < HKV; ++h) {
+                    unsigned long long w64 = kw_s[(h * 4 * BITS + kq0) * 32 + lane];
+                    if (kshift + 2 * BITS * KPW > 32)
+                        w64 |= (unsigned long long)kw_s[(h * 4 * BITS + kq0 + 1) * 32 + lane] << 32;
+                    win[h] = w64 >> kshift;
                 }
-                if (lane == 0) beta_s[g] = alpha * ldexpf(1.f, E_cur - E_new);
+#pragma unroll
+                for (int k = 0; k < KPW; ++k) {
+                    const int i = warp * KPW + k;
+                    const float2 an = anc32[i];
+                    const float cc = an.x * t1c[k] - an.y * t1s[k];
+                    const float ss = an.x * t1s[k] + an.y * t1c[k];
+                    const uint32_t cs = pack_half2(cc, ss);
+#pragma unroll
+                    for (int h = 0; h < HKV; ++h) {
+                        const int pc = (int)((win[h] >> (2 * BITS * k)) & (NE - 1));
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) {
+                            const int g = h * G + gg;
+                            const uint32_t ab = klut[(g * 64 + i) * NE + pc];
+                            fma2_f16_f32(ab, cs, acc_c[g], acc_s[g]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < HG; ++g) red[(warp * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
             }
-            E_cur = E_new;
-        }
-        __syncthreads();
-        tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
+            compute_sync();
+            tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
 
-        // -------------------------------------------------------- a5: P.V dense
+            // ------------------------------------------------------- a4: online softmax
+            {
+                float smax = lane < ntok ? vsz_s[lane].x : 0.f;
+                smax = warp_max_redux(smax);
+                int E_new = E_cur;
+                if (smax > 0.f) E_new = max(E_cur, ilogbf(smax) + 1);
+                if (warp < HG) {
+                    const int g = warp, j = lane;
+                    const bool valid = j < ntok;
+                    float s = 0.f;
+#pragma unroll
+                    for (int w = 0; w < NCW; ++w) s += red[(w * HG + g) * 32 + j];
+                    s = valid ? s * lut_inv[g] + kcorr[g * 32 + j] : -CUDART_INF_F;
+                    kcorr[g * 32 + j] = 0.f;
+                    const float m_new = fmaxf(m_run, warp_max_redux(s));
+                    const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
+                    const float p = valid ? exp2f(s - m_new) : 0.f;
+                    const float2 sz = valid ? vsz_s[j] : make_float2(0.f, 0.f);
+                    l_lane = l_lane * alpha + p;
+                    z_lane = z_lane * alpha + p * sz.y;
+                    m_run = m_new;
+                    p_s[g * 32 + j] = p;
+                    w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * ldexpf(sz.x, -E_new)));
+                    if (alpha != 1.f) {
+#pragma unroll
+                        for (int x = 0; x < kHeadDim / 32; ++x) osp[g * kHeadDim + x * 32 + lane] *= alpha;
+                    }
+                    if (lane == 0) beta_s[g] = alpha * ldexpf(1.f, E_cur - E_new);
+                }
+                E_cur = E_new;
+            }
+            compute_sync();
+            tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
+
+            // -------------------------------------------------------- a5: P.V dense
+            if (vtask) {
+                const float b = beta_s[vh];
+                if (b != 1.f) {
+#pragma unroll
+                    for (int x = 0; x < CPL; ++x) acc[x] *= b;
+                }
+                const uint16_t w = w16[vh * 32 + vj];
+                uint32_t vw[VWL];
+                const uint32_t *src = vw_s + (vkv * 32 + vj) * (4 * BITS) + vq * VWL;
+#pragma unroll
+                for (int x = 0; x < VWL; ++x) vw[x] = src[x];
+#pragma unroll
+                for (int pp = 0; pp < CPL / 2; ++pp) {
+                    const int bit = 2 * BITS * pp;
+                    const int wi = bit >> 5, sh = bit & 31;
+                    uint32_t pc;
+                    if (sh + 2 * BITS <= 32) pc = (vw[wi] >> sh) & (NE - 1);
+                    else pc = (uint32_t)((((unsigned long long)vw[wi + 1] << 32) | vw[wi]) >> sh) & (NE - 1);
+                    const uint32_t cv = vlut[pc * 32 + lane];
+                    fma_w_f16x2(w, cv, acc[2 * pp], acc[2 * pp + 1]);
+                }
+            }
+            // ---------------------------------------------------- a6: V outliers
+            {
+                auto v_item = [&](uint32_t itm) {
+                    const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                    const int kvl = chl >> 7, cc = chl & 127;
+                    const int bit = BITS * cc;
+                    const uint32_t *vrow = vw_s + (kvl * 32 + j) * (4 * BITS);
+                    unsigned long long w64 = vrow[bit >> 5];
+                    if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vrow[(bit >> 5) + 1] << 32;
+                    const int code = (int)((w64 >> (bit & 31)) & CM);
+                    const float2 sz = vsz_s[j];
+                    const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+                    const float delta = xval - (cbVs[code] * sz.x + sz.y);
+#pragma unroll
+                    for (int gg = 0; gg < G; ++gg) {
+                        const int g = kvl * G + gg;
+                        atomicAdd(&osp[g * kHeadDim + cc], p_s[g * 32 + j] * delta);
+                    }
+                };
+                const int nvi = hdr[1];
+                for (int x = tid; x < nvi; x += NCT) v_item(vit[x]);
+                if (hdr[3]) {
+                    const uint32_t *vrec_s = reinterpret_cast<const uint32_t *>(sb + P.so_vrec);
+                    int skip = VITEM_CAP;
+                    for (int j = 0; j < ntok; ++j) {
+                        const int b = hdr[8 + 64 + j], e = hdr[8 + 96 + j];
+                        const int s0 = min(e - b, skip);
+                        skip -= s0;
+                        for (int r = b + s0 + tid; r < e; r += NCT) v_item(make_item(vrec_s[r], j, c_lo));
+                    }
+                }
+            }
+            // advance anchors to the next tile (fp64 complex rotation by 32 theta_i)
+            if (tid < 64) {
+                const double2 a = anc64[tid], r = rot64[tid];
+                const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
+                anc64[tid] = b;
+                anc32[tid] = make_float2((float)b.x, (float)b.y);
+            }
+            compute_sync();
+            if (tid == 0) mbar_arrive(empty_b + st);
+            tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
+        }
+        if (warp < HG) {
+            const float l = warp_sum(l_lane), z = warp_sum(z_lane);
+            if (lane == 0) { m_fin[warp] = m_run; l_fin[warp] = l; z_fin[warp] = z; }
+        }
         if (vtask) {
-            const float b = beta_s[vh];
-            if (b != 1.f) {
-#pragma unroll
-                for (int x = 0; x < CPL; ++x) acc[x] *= b;
-            }
-            const uint16_t w = w16[vh * 32 + vj];
-            uint32_t vw[VWL];
-            const uint32_t *src = vw_s + (vkv * 32 + vj) * (4 * BITS) + vq * VWL;
-#pragma unroll
-            for (int x = 0; x < VWL; ++x) vw[x] = src[x];
-#pragma unroll
-            for (int pp = 0; pp < CPL / 2; ++pp) {
-                const int bit = 2 * BITS * pp;
-                const int wi = bit >> 5, sh = bit & 31;
-                uint32_t pc;
-                if (sh + 2 * BITS <= 32) pc = (vw[wi] >> sh) & (NE - 1);
-                else pc = (uint32_t)((((unsigned long long)vw[wi + 1] << 32) | vw[wi]) >> sh) & (NE - 1);
-                const uint32_t cv = vlut[pc * 32 + lane];
-                fma_w_f16x2(w, cv, acc[2 * pp], acc[2 * pp + 1]);
-            }
-        }
-
-        // ------------------------------- a6: V outliers (flat over relevant records)
-        {
-            int vl = rv_len[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, vl, o);
-                if (lane >= o) vl += y;
-            }
-            const int vtot = __shfl_sync(0xffffffffu, vl, 31);
-            for (int xb = warp * 32; xb < vtot; xb += ATT_THREADS) {
-                const int x = xb + lane;
-                int j = 0;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const int v = __shfl_sync(0xffffffffu, vl, j + o - 1);
-                    if (v <= x) j += o;
-                }
-                const int excl = __shfl_sync(0xffffffffu, vl, (j + 31) & 31);
-                if (x >= vtot) continue;
-                const uint32_t rec = vrec_s[rv_beg[j] + (x - (j ? excl : 0))];
-                const int ch = (int)(rec & 0xffffu);
-                const int kvl = (ch >> 7) - h0;
-                const int bit = BITS * (ch & 127);
-                const uint32_t *vrow = vw_s + (kvl * 32 + j) * (4 * BITS);
-                unsigned long long w64 = vrow[bit >> 5];
-                if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vrow[(bit >> 5) + 1] << 32;
-                const int code = (int)((w64 >> (bit & 31)) & CM);
-                const float2 sz = vsz_s[j];
-                const float xval = __half2float(__ushort_as_half((uint16_t)(rec >> 16)));
-                const float delta = xval - (cbVs[code] * sz.x + sz.y);
-#pragma unroll
-                for (int gg = 0; gg < G; ++gg) {
-                    const int g = kvl * G + gg;
-                    atomicAdd(&osp[g * kHeadDim + (ch & 127)], p_s[g * 32 + j] * delta);
-                }
-            }
-        }
-
-        // advance anchors to the next tile (fp64 complex rotation by 32 theta_i)
-        if (tid < 64) {
-            const double2 a = anc64[tid], r = rot64[tid];
-            const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
-            anc64[tid] = b;
-            anc32[tid] = make_float2((float)b.x, (float)b.y);
-        }
-        __syncthreads();
-        tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
-    }
-    if (P.timers && tid == 0) {
-#pragma unroll
-        for (int x = 0; x < 5; ++x) atomicAdd(P.timers + x, tm[x]);
-        atomicAdd(P.timers + 5, (unsigned long long)(t_end - t_begin));
-    }
-
-    // ------------------------------------------------------------ write partial
-    for (int g = warp; g < HG; g += ATT_WARPS)
-        if (lane == 0) { m_fin[g] = m_run; l_fin[g] = l_run; z_fin[g] = z_run; }
-    {
-        const float sc = ldexpf(1.f, E_cur);
-        float *dst = osp + vh * kHeadDim + vq * CPL;
-        if (vtask) {
+            // dense P.V accumulators are in units of 2^-E_cur
+            const float sc = ldexpf(1.f, E_cur);
+            float *dst = osp + vh * kHeadDim + vq * CPL;
 #pragma unroll
             for (int x = 0; x < CPL; ++x) atomicAdd(&dst[x], acc[x] * sc);
         }
+        if (P.timers && tid == 0) {
+#pragma unroll
+            for (int x = 0; x < 5; ++x) atomicAdd(P.timers + x, tm[x]);
+            atomicAdd(P.timers + 5, (unsigned long long)ntl);
+        }
     }
     __syncthreads();
+
+    // ------------------------------------------------------------ write partial
     float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
     for (int x = tid; x < HG * kHeadDim; x += ATT_THREADS) {
         const int g = x >> 7, ch = x & 127;
-        part[(g0 + g) * (kHeadDim + 2) + ch] = osp[x] + z_fin[g];
+        part[(g0 + g) * (kHeadDim + 2) + ch] = ntl > 0 ? osp[x] + z_fin[g] : 0.f;
     }
     if (tid < HG) {
-        part[(g0 + tid) * (kHeadDim + 2) + kHeadDim] = m_fin[tid];
-        part[(g0 + tid) * (kHeadDim + 2) + kHeadDim + 1] = l_fin[tid];
+        part[(g0 + tid) * (kHeadDim + 2) + kHeadDim] = ntl > 0 ? m_fin[tid] : -CUDART_INF_F;
+        part[(g0 + tid) * (kHeadDim + 2) + kHeadDim + 1] = ntl > 0 ? l_fin[tid] : 0.f;
     }
     // ------------------------------------------------------- a7: split merge
     __threadfence();
@@ -772,10 +815,13 @@ size_t layout(const DevCache &c, Params &P) {
     P.so_vw = (unsigned)off; off = align128(off + 32 * qwc * 4);
     P.so_vsz = (unsigned)off; off = align128(off + 256);
     P.so_kptr = (unsigned)off; off = align128(off + 192);
+    P.so_hdr = (unsigned)off; off = align128(off + (8 + 128) * 4);
+    P.so_kit = (unsigned)off; off = align128(off + KITEM_CAP * 4);
+    P.so_vit = (unsigned)off; off = align128(off + VITEM_CAP * 4);
     P.so_vrec = (unsigned)off; off = align128(off + (size_t)32 * c.kv * 4);
     P.so_krec = (unsigned)off;
     const size_t limit = 227 * 1024;
-    const size_t base = align128(C::fixed + 64);
+    const size_t base = align128(C::fixed + 128);
     P.st_base = (unsigned)base;
     for (int stages = 3; stages >= 2; --stages) {
         for (int krec = 2048; krec >= 256; krec -= 256) {
@@ -809,7 +855,6 @@ cudaError_t launch_g(const DevCache &c, Params &P, int grid, cudaStream_t s) {
         case 1: return launch_t<BITS, HG, 1>(c, P, grid, s);
         case 2: if constexpr (HG >= 2) return launch_t<BITS, HG, 2>(c, P, grid, s); break;
         case 4: if constexpr (HG >= 4) return launch_t<BITS, HG, 4>(c, P, grid, s); break;
-        case 8: if constexpr (HG >= 8) return launch_t<BITS, HG, 8>(c, P, grid, s); break;
     }
     return cudaErrorInvalidValue;
 }
@@ -827,7 +872,7 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
 }  // namespace
 
 int attend_heads_per_cta(int bits, int H_q, int G) {
-    const int cap = bits == 4 ? 1 : 4;   // V tasks: HG * 128/CPL <= 16 warps
+    const int cap = bits == 4 ? 1 : 4;   // V tasks: HG * 128/CPL <= 16 compute warps
     for (int hg = cap; hg >= 1; hg >>= 1)
         if (H_q % hg == 0 && hg % G == 0) return hg;
     return 0;
