@@ -173,9 +173,10 @@ kvq_status kvq_get_info(const kvq_cache *cache, kvq_info *info);
 kvq_status kvq_set_splits(kvq_cache *cache, int32_t splits);
 
 /* Diagnostics: per-phase cycle sums of the attend kernel since the last call
- * (out[0..4]: issue, TMA wait, K phase, softmax phase, V phase; out[5]: tiles), summed
+ * (out[0..4]: -, ready wait, K phase, softmax phase, V phase; out[5]: tiles;
+ * out[6..8] / out[9..11]: wait / compaction / TMA issue of the two producer warps), summed
  * over CTAs.  Only when the process was started with KVQ_PHASE_TIMERS=1. */
-kvq_status kvq_phase_timers(kvq_cache *cache, uint64_t *out /* host [8] */);
+kvq_status kvq_phase_timers(kvq_cache *cache, uint64_t *out /* host [16] */);
 
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char *kvq_last_error(void);

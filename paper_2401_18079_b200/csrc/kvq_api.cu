@@ -188,7 +188,7 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     c->max_splits = 4 * 148;
     A(&c->parts, (size_t)c->max_splits * d.H_q * (kHeadDim + 2) * 4);
     A(&c->tickets, 64 * 4);
-    if (getenv("KVQ_PHASE_TIMERS")) A(&c->timers, 8 * 8);
+    if (getenv("KVQ_PHASE_TIMERS")) A(&c->timers, 16 * 8);
     if (st != KVQ_OK) { kvq_cache_destroy(c); return st; }
     {
         cudaError_t e = cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped);
@@ -252,8 +252,8 @@ kvq_status kvq_phase_timers(kvq_cache *c, uint64_t *out) {
     if (!c->timers) return fail(KVQ_EINVAL, "phase timers disabled (set KVQ_PHASE_TIMERS=1)");
     CK(cudaSetDevice(c->cfg.device));
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(out, c->timers, 8 * 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemset(c->timers, 0, 8 * 8));
+    CK(cudaMemcpy(out, c->timers, 16 * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(c->timers, 0, 16 * 8));
     return KVQ_OK;
 }
 

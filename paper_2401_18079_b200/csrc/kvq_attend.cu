@@ -376,6 +376,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         };
         if (kwarp && lane == 0 && ntl > 0) kptr_at(t_begin);
         const int Sg = P.stages;
+        unsigned long long ptm[3] = {0, 0, 0};   // wait, compact, issue cycles
+        long long pc0 = clock64(), pc1;
         for (int it = 0; it < ntl + Sg - 1; ++it) {
             // ---- compact the outliers of tile tc (its data landed S-1 issues ago)
             const int ic = it - (Sg - 1);
@@ -383,6 +385,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const int sc = ic % Sg;
                 const int tcur = t_begin + ic;
                 mbar_wait(full_b + sc, (unsigned)((ic / Sg) & 1));
+                pc1 = clock64(); ptm[0] += pc1 - pc0; pc0 = pc1;
                 unsigned char *sb = stage_ptr(sc);
                 const uint32_t *kptr_s = reinterpret_cast<const uint32_t *>(sb + P.so_kptr);
                 int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
@@ -448,6 +451,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(ready_b + sc);
+                pc1 = clock64(); ptm[1] += pc1 - pc0; pc0 = pc1;
             }
             // ---- issue tile ti into its stage once the compute warps released it
             const int ti = t_begin + it;
@@ -479,7 +483,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 if (lane == 4 && b_vrec) bulk_g2s(sb + P.so_vrec, c.vout + n0 * kv, b_vrec, bar);
                 if (lane == 5 && kn) bulk_g2s(sb + P.so_krec, c.kout + ka, kn * 4u, bar);
                 if (lane == 0 && ti + 1 < t_end) kptr_at(ti + 1);
+                pc1 = clock64(); ptm[2] += pc1 - pc0; pc0 = pc1;
             }
+        }
+        if (P.timers && lane == 0) {
+            atomicAdd(P.timers + (kwarp ? 6 : 9), ptm[0]);
+            atomicAdd(P.timers + (kwarp ? 7 : 10), ptm[1]);
+            atomicAdd(P.timers + (kwarp ? 8 : 11), ptm[2]);
         }
     }
 

@@ -218,7 +218,7 @@ class KVQCache:
         _check(_lib.kvq_set_splits(self._h, int(splits)))
 
     def phase_timers(self) -> list:
-        out = (ctypes.c_uint64 * 8)()
+        out = (ctypes.c_uint64 * 16)()
         _check(_lib.kvq_phase_timers(self._h, out))
         return list(out)
 

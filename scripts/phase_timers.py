@@ -39,5 +39,7 @@ tm = c.phase_timers()
 tiles = tm[5]
 names = ["issue", "tma_wait", "K_phase", "softmax", "V_phase"]
 print(f"{wname} T={T} attend {e0.elapsed_time(e1) / 5 * 1e3:.1f} us, info {c.info()}")
-print("cycles per tile per CTA:", {n: round(tm[i] / tiles, 1) for i, n in enumerate(names)},
-      "total", round(sum(tm[:5]) / tiles, 1))
+print("compute cycles per tile per CTA:", {n: round(tm[i] / tiles, 1) for i, n in enumerate(names)},
+      "total", round(sum(tm[1:5]) / tiles, 1))
+print("producer K (wait/compact/issue):", [round(tm[i] / tiles, 1) for i in (6, 7, 8)],
+      " producer V (wait/compact/-):", [round(tm[i] / tiles, 1) for i in (9, 10, 11)])
