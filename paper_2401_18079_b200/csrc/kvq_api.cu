@@ -185,6 +185,24 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     A(&d.cb, 64 * 4);
     A(&d.mids, 32 * 8);
     A(&d.counts, (size_t)d.cap * 4);
+    // outlier buckets per (tile, attend head group); capacity ~3x the expected count
+    {
+        const int hkv_g = hg / G;
+        d.GW = hkv_g * kHeadDim;
+        d.NG = C.n_kv_heads / hkv_g;
+        const double f = C.outlier_ppm / 1e6;
+        int kc = (int)std::ceil(3.0 * f * d.GW);
+        kc = kc < 8 ? 8 : kc;
+        int vc = (int)std::ceil(3.0 * (double)kv * d.GW / (double)D);
+        vc = vc < 8 ? 8 : vc;
+        if (vc > kv) vc = (int)kv;
+        d.kcap_g = ((32 * kc) + 3) & ~3;
+        d.vcap_g = ((32 * (vc > 0 ? vc : 1)) + 3) & ~3;
+        const size_t ntiles = (size_t)(d.cap / 32);
+        A(&d.kit, ntiles * d.NG * d.kcap_g * 4);
+        A(&d.vit, ntiles * d.NG * d.vcap_g * 4);
+        A(&d.gcnt, ntiles * d.NG * 2 * 4 + 16);
+    }
     c->max_splits = 4 * 148;
     A(&c->parts, (size_t)c->max_splits * d.H_q * (kHeadDim + 2) * 4);
     A(&c->tickets, 64 * 4);
@@ -275,6 +293,7 @@ kvq_status kvq_reset(kvq_cache *c, void *stream) {
     if (!c) return fail(KVQ_EINVAL, "null cache");
     CK(cudaSetDevice(c->cfg.device));
     CK(cudaMemsetAsync(c->dc.kptr, 0, 4, (cudaStream_t)stream));
+    CK(cudaMemsetAsync(c->dc.gcnt, 0, (size_t)(c->dc.cap / 32) * c->dc.NG * 2 * 4, (cudaStream_t)stream));
     c->T = 0;
     return KVQ_OK;
 }

@@ -33,11 +33,9 @@ namespace {
 
 constexpr int NCW = 16;                       // compute warps
 constexpr int NCT = NCW * 32;                 // compute threads
-constexpr int ATT_THREADS = NCT + 64;         // + 2 producer warps
-constexpr int PW_K = NCW;                     // producer warp ids: NCW (TMA + K), NCW+1 (V)
+constexpr int ATT_THREADS = NCT + 32;         // + 1 producer warp
+constexpr int PW_K = NCW;                     // producer (TMA) warp id
 constexpr int KPW = kPairs / NCW;             // RoPE pairs per compute warp in the K phase
-constexpr int KITEM_CAP = 512;                // compacted records per tile and stage
-constexpr int VITEM_CAP = 512;
 
 // ------------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -142,7 +140,8 @@ struct Cfg {
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
         + NCW * HG * 32 * 4            /* red */
-        + HG * 32 * 4 * 2              /* p, kcorr */
+        + HG * 32 * 4 * 3              /* p, kcorr, hcorr */
+        + 64 * 4                       /* kbeg, kend */
         + HG * 32 * 2                  /* w16 */
         + HG * kHeadDim * 4            /* osp */
         + 64 * 16 * 3 + 64 * 8         /* anc64, rot64, qcis, anc32 */
@@ -167,15 +166,9 @@ struct Params {
     // stage ring layout (bytes), computed on the host
     int stages;
     int krec_cap;        // u32 records per stage buffer (multiple of 4)
-    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kptr, so_vrec, so_krec, so_kit, so_vit,
-        so_hdr;
+    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit, so_hdr, so_kcon;
     unsigned long long *timers;   // optional [8] phase cycle sums (diagnostics), may be null
 };
-
-// compacted outlier item: fp16 value << 16 | token (5 bits) << 11 | channel in group (11 bits)
-__device__ __forceinline__ uint32_t make_item(uint32_t rec, int j, int c_lo) {
-    return (rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)((int)(rec & 0xffffu) - c_lo);
-}
 
 template <int BITS, int HG, int G>
 __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params P) {
@@ -197,7 +190,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *red = reinterpret_cast<float *>(sp); sp += NCW * HG * 32 * 4;
     float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
-    float *kcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
+    float *kcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;   // overflow fallback only
+    float *hcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
+    int *kbeg = reinterpret_cast<int *>(sp); sp += 32 * 4;
+    int *kend = reinterpret_cast<int *>(sp); sp += 32 * 4;
     float *osp = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
     double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
@@ -219,9 +215,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
     int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
-    // barriers just below the stage ring: full[S], ready[S], empty[S]
+    float *kcon = reinterpret_cast<float *>(smem_raw + P.so_kcon);   // [kcap_g][G]
+    // barriers just below the stage ring: full[S], empty[S]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
-    uint64_t *full_b = bars, *ready_b = bars + 4, *empty_b = bars + 8;
+    uint64_t *full_b = bars, *empty_b = bars + 8;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
@@ -243,7 +240,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     if (tid == 0) {
         for (int s = 0; s < P.stages; ++s) {
             mbar_init(full_b + s, 1);
-            mbar_init(ready_b + s, 2);
             mbar_init(empty_b + s, 1);
         }
         mbar_fence_init();
@@ -278,6 +274,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     }
     if (tid < 64) cb_s[tid] = c.cb[tid];
     for (int x = tid; x < HG * 32; x += ATT_THREADS) kcorr[x] = 0.f;
+    if (tid < 32) { kbeg[tid] = 0; kend[tid] = 0; }
     if (tid < 16) flag_s[tid] = 0;
     __syncthreads();
     // a1: q~ = RoPE(q, pos) * log2(e)/sqrt(d)
@@ -364,132 +361,50 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     }
     __syncthreads();
 
-    // ================================================================= producers
-    if (warp >= NCW) {
-        const bool kwarp = warp == PW_K;
-        uint32_t kp_lo = 0, kp_hi = 0;      // CSC range of the next tile to issue (lane 0)
-        auto kptr_at = [&](int t) {
-            const int64_t n0 = (int64_t)t * 32;
-            const int64_t n1 = n0 + 32 < P.T ? n0 + 32 : P.T;
-            kp_lo = __ldg(c.kptr + n0);
-            kp_hi = __ldg(c.kptr + n1);
+    // ================================================================== producer
+    if (warp == PW_K) {
+        // counts of the (tile, group) outlier buckets of the next tile to issue (lane 0)
+        uint32_t nk_next = 0, nv_next = 0;
+        auto counts_at = [&](int t) {
+            const uint32_t *gc = c.gcnt + ((int64_t)t * c.NG + hg) * 2;
+            nk_next = __ldg(gc);
+            nv_next = __ldg(gc + 1);
         };
-        if (kwarp && lane == 0 && ntl > 0) kptr_at(t_begin);
+        if (lane == 0 && ntl > 0) counts_at(t_begin);
         const int Sg = P.stages;
-        unsigned long long ptm[3] = {0, 0, 0};   // wait, compact, issue cycles
-        long long pc0 = clock64(), pc1;
-        for (int it = 0; it < ntl + Sg - 1; ++it) {
-            // ---- compact the outliers of tile tc (its data landed S-1 issues ago)
-            const int ic = it - (Sg - 1);
-            if (ic >= 0) {
-                const int sc = ic % Sg;
-                const int tcur = t_begin + ic;
-                mbar_wait(full_b + sc, (unsigned)((ic / Sg) & 1));
-                pc1 = clock64(); ptm[0] += pc1 - pc0; pc0 = pc1;
-                unsigned char *sb = stage_ptr(sc);
-                const uint32_t *kptr_s = reinterpret_cast<const uint32_t *>(sb + P.so_kptr);
-                int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
-                const int ntok = (int)min((int64_t)32, P.T - (int64_t)tcur * 32);
-                const int j = lane;
-                if (kwarp) {
-                    const uint32_t *krec_s = reinterpret_cast<const uint32_t *>(sb + P.so_krec);
-                    uint32_t *kit = reinterpret_cast<uint32_t *>(sb + P.so_kit);
-                    const uint32_t ka = kptr_s[0] & ~3u;
-                    auto krec = [&](uint32_t r) -> uint32_t {
-                        const uint32_t off = r - ka;
-                        if (off < (uint32_t)P.krec_cap) return krec_s[off];
-                        return __ldcg(c.kout + r);
-                    };
-                    uint32_t a = 0, e = 0;
-                    if (j < ntok) {
-                        const uint32_t r0 = kptr_s[j], r1 = kptr_s[j + 1];
-                        a = r0; e = r1;
-                        while (a < e) { const uint32_t m = (a + e) >> 1; if ((int)(krec(m) & 0xffffu) < c_lo) a = m + 1; else e = m; }
-                        uint32_t b = a; e = r1;
-                        while (b < e) { const uint32_t m = (b + e) >> 1; if ((int)(krec(m) & 0xffffu) < c_hi) b = m + 1; else e = m; }
-                        e = b;
-                    }
-                    const int cnt = (int)(e - a);
-                    int incl = cnt;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += y;
-                    }
-                    const int tot = __shfl_sync(0xffffffffu, incl, 31);
-                    int pos = incl - cnt;
-                    for (uint32_t r = a; r < e && pos < KITEM_CAP; ++r, ++pos) kit[pos] = make_item(krec(r), j, c_lo);
-                    if (lane == 0) { hdr[0] = min(tot, KITEM_CAP); hdr[2] = tot > KITEM_CAP; }
-                    // overflow (pathological tiles): the rest of the records are handled by
-                    // the compute warps from the per-token ranges
-                    hdr[8 + j] = (int)a;
-                    hdr[8 + 32 + j] = (int)e;
-                } else {
-                    const uint32_t *vrec_s = reinterpret_cast<const uint32_t *>(sb + P.so_vrec);
-                    uint32_t *vit = reinterpret_cast<uint32_t *>(sb + P.so_vit);
-                    int a = 0, e = 0;
-                    if (j < ntok && kv > 0) {
-                        a = j * kv; e = (j + 1) * kv;
-                        while (a < e) { const int m = (a + e) >> 1; if ((int)(vrec_s[m] & 0xffffu) < c_lo) a = m + 1; else e = m; }
-                        int b = a; e = (j + 1) * kv;
-                        while (b < e) { const int m = (b + e) >> 1; if ((int)(vrec_s[m] & 0xffffu) < c_hi) b = m + 1; else e = m; }
-                        e = b;
-                    }
-                    const int cnt = e - a;
-                    int incl = cnt;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += y;
-                    }
-                    const int tot = __shfl_sync(0xffffffffu, incl, 31);
-                    int pos = incl - cnt;
-                    for (int r = a; r < e && pos < VITEM_CAP; ++r, ++pos) vit[pos] = make_item(vrec_s[r], j, c_lo);
-                    if (lane == 0) { hdr[1] = min(tot, VITEM_CAP); hdr[3] = tot > VITEM_CAP; }
-                    hdr[8 + 64 + j] = a;
-                    hdr[8 + 96 + j] = e;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(ready_b + sc);
-                pc1 = clock64(); ptm[1] += pc1 - pc0; pc0 = pc1;
-            }
-            // ---- issue tile ti into its stage once the compute warps released it
+        for (int it = 0; it < ntl; ++it) {
             const int ti = t_begin + it;
-            if (kwarp && ti < t_end) {
-                const int si = it % Sg;
-                if (it >= Sg) mbar_wait(empty_b + si, (unsigned)(((it / Sg) - 1) & 1));
-                unsigned char *sb = stage_ptr(si);
-                uint64_t *bar = full_b + si;
-                const uint32_t klo = __shfl_sync(0xffffffffu, kp_lo, 0);
-                const uint32_t khi = __shfl_sync(0xffffffffu, kp_hi, 0);
-                const uint32_t ka = klo & ~3u;
-                uint32_t kn = ((khi + 3u) & ~3u) - ka;
-                if (kn > (uint32_t)P.krec_cap) kn = (uint32_t)P.krec_cap;
-                const unsigned b_kw = 32u * QWC * 4u;
-                const unsigned b_vrec = 32u * (unsigned)kv * 4u;
-                const unsigned total = 2u * b_kw + 256u + 192u + b_vrec + kn * 4u;
-                if (lane == 0) {
-                    fence_proxy_async();
-                    mbar_expect_tx(bar, total);
-                }
-                __syncwarp();
-                const int64_t n0 = (int64_t)ti * 32;
-                if (lane == 0)
-                    bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
-                if (lane == 1)
-                    bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
-                if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
-                if (lane == 3) bulk_g2s(sb + P.so_kptr, c.kptr + n0, 192u, bar);
-                if (lane == 4 && b_vrec) bulk_g2s(sb + P.so_vrec, c.vout + n0 * kv, b_vrec, bar);
-                if (lane == 5 && kn) bulk_g2s(sb + P.so_krec, c.kout + ka, kn * 4u, bar);
-                if (lane == 0 && ti + 1 < t_end) kptr_at(ti + 1);
-                pc1 = clock64(); ptm[2] += pc1 - pc0; pc0 = pc1;
+            const int si = it % Sg;
+            if (it >= Sg) mbar_wait(empty_b + si, (unsigned)(((it / Sg) - 1) & 1));
+            unsigned char *sb = stage_ptr(si);
+            uint64_t *bar = full_b + si;
+            const uint32_t nk = __shfl_sync(0xffffffffu, nk_next, 0);
+            const uint32_t nv = __shfl_sync(0xffffffffu, nv_next, 0);
+            const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
+            const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
+            const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
+            const unsigned b_kw = 32u * QWC * 4u;
+            const unsigned total = 2u * b_kw + 256u + bk + bv;
+            if (lane == 0) {
+                int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
+                hdr[0] = kov ? 0 : (int)nk;
+                hdr[1] = vov ? 0 : (int)nv;
+                hdr[2] = kov;
+                hdr[3] = vov;
+                fence_proxy_async();
+                mbar_expect_tx(bar, total);
             }
-        }
-        if (P.timers && lane == 0) {
-            atomicAdd(P.timers + (kwarp ? 6 : 9), ptm[0]);
-            atomicAdd(P.timers + (kwarp ? 7 : 10), ptm[1]);
-            atomicAdd(P.timers + (kwarp ? 8 : 11), ptm[2]);
+            __syncwarp();
+            const int64_t n0 = (int64_t)ti * 32;
+            const int64_t bucket = (int64_t)ti * c.NG + hg;
+            if (lane == 0)
+                bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
+            if (lane == 1)
+                bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
+            if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
+            if (lane == 3 && bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
+            if (lane == 4 && bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
+            if (lane == 0 && ti + 1 < t_end) counts_at(ti + 1);
         }
     }
 
@@ -529,7 +444,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         for (int t = t_begin; t < t_end; ++t) {
             const int it = t - t_begin;
             const int st = it % P.stages;
-            mbar_wait(ready_b + st, (unsigned)((it / P.stages) & 1));
             mbar_wait(full_b + st, (unsigned)((it / P.stages) & 1));
             tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
             unsigned char *sb = stage_ptr(st);
@@ -542,8 +456,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             const int64_t n0 = (int64_t)t * 32;
             const int ntok = (int)min((int64_t)32, P.T - n0);
 
-            // K-outlier correction of one compacted item (fp32, shared atomics)
-            auto k_item = [&](uint32_t itm) {
+            // K-outlier correction of one item: (x - K^(code)) * dscore/dK for the G query
+            // heads of its kv head, in fp32
+            auto k_corr = [&](uint32_t itm, int gg, int &j_out, int &g_out) -> float {
                 const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
                 const int kvl = chl >> 7, cc = chl & 127, i = cc & 63, up = cc >> 6;
                 const int bit = 2 * BITS * i;
@@ -556,42 +471,63 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const float delta = xval - (cbKs[code] * ks_s[chl] + kz_s[chl]);
                 const float2 an = anc32[i], tt = t1tab[i * 32 + j];
                 const float co = an.x * tt.x - an.y * tt.y, si = an.x * tt.y + an.y * tt.x;
-#pragma unroll
-                for (int gg = 0; gg < G; ++gg) {
-                    const int g = kvl * G + gg;
-                    const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
-                    atomicAdd(&kcorr[g * 32 + j], delta * (up ? (qb * co - qa * si) : (qa * co + qb * si)));
-                }
+                const int g = kvl * G + gg;
+                const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
+                j_out = j;
+                g_out = g;
+                return delta * (up ? (qb * co - qa * si) : (qa * co + qb * si));
             };
 
             // ------------------------------------------ a3: K outliers, heavy pairs
             {
                 const int nk = hdr[0];
-                for (int x = tid; x < nk; x += NCT) k_item(kit[x]);
+                // items are in (token, channel) order: contributions go to kcon[item][gg],
+                // token boundaries to kbeg/kend; the softmax lane (g, j) gathers them
+                for (int x = tid; x < nk; x += NCT) {
+                    const uint32_t itm = kit[x];
+                    int j = 0, g = 0;
+#pragma unroll
+                    for (int gg = 0; gg < G; ++gg) kcon[x * G + gg] = k_corr(itm, gg, j, g);
+                    const int jp = x > 0 ? (int)((kit[x - 1] >> 11) & 31u) : -1;
+                    const int jn = x + 1 < nk ? (int)((kit[x + 1] >> 11) & 31u) : 32;
+                    if (jp != j) kbeg[j] = x;
+                    if (jn != j) kend[j] = x + 1;
+                }
                 if (hdr[2]) {
-                    // overflowed item list: remaining records straight from the CSC arrays
-                    int skip = KITEM_CAP;
+                    // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
                     for (int j = 0; j < ntok; ++j) {
-                        const int b = hdr[8 + j], e = hdr[8 + 32 + j];
-                        const int s0 = min(e - b, skip);
-                        skip -= s0;
-                        for (int r = b + s0 + tid; r < e; r += NCT)
-                            k_item(make_item(__ldcg(c.kout + r), j, c_lo));
+                        const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
+                        for (uint32_t r = r0 + tid; r < r1; r += NCT) {
+                            const uint32_t rec = __ldcg(c.kout + r);
+                            const int ch = (int)(rec & 0xffffu);
+                            if (ch < c_lo || ch >= c_hi) continue;
+                            const uint32_t itm = (rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - c_lo);
+#pragma unroll
+                            for (int gg = 0; gg < G; ++gg) {
+                                int jj, g;
+                                const float v = k_corr(itm, gg, jj, g);
+                                atomicAdd(&kcorr[g * 32 + jj], v);
+                            }
+                        }
                     }
                 }
-                for (int x = tid; x < HG * HMAX * 32; x += NCT) {
-                    const int g = x / (HMAX * 32), hs = (x / 32) % HMAX, j = x & 31;
-                    if (hs >= hv_n[g] || j >= ntok) continue;
-                    const int i = hv_pair[g * 8 + hs];
-                    const int bit = 2 * BITS * i;
-                    const int wq = (g / G) * 4 * BITS + (bit >> 5);
-                    unsigned long long w64 = kw_s[wq * 32 + j];
-                    if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                    const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                    const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
-                    const float2 an = anc32[i], tt = t1tab[i * 32 + j];
-                    const float co = an.x * tt.x - an.y * tt.y, si = an.x * tt.y + an.y * tt.x;
-                    atomicAdd(&kcorr[g * 32 + j], co * ab.x + si * ab.y);
+                if (tid < HG * 32) {
+                    // heavy RoPE pairs of head g in fp32 (tables hlut), one thread per (g, j)
+                    const int g = tid >> 5, j = tid & 31;
+                    float hc = 0.f;
+                    const int nh = hv_n[g];
+                    for (int hs = 0; hs < nh; ++hs) {
+                        const int i = hv_pair[g * 8 + hs];
+                        const int bit = 2 * BITS * i;
+                        const int wq = (g / G) * 4 * BITS + (bit >> 5);
+                        unsigned long long w64 = kw_s[wq * 32 + j];
+                        if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                        const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                        const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
+                        const float2 an = anc32[i], tt = t1tab[i * 32 + j];
+                        hc += (an.x * tt.x - an.y * tt.y) * ab.x + (an.x * tt.y + an.y * tt.x) * ab.y;
+                    }
+                    hcorr[g * 32 + j] = hc;
                 }
             }
             // ------------------------------------------------------------ a2: K dense
@@ -643,8 +579,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     float s = 0.f;
 #pragma unroll
                     for (int w = 0; w < NCW; ++w) s += red[(w * HG + g) * 32 + j];
-                    s = valid ? s * lut_inv[g] + kcorr[g * 32 + j] : -CUDART_INF_F;
+                    s = s * lut_inv[g] + kcorr[g * 32 + j] + hcorr[g * 32 + j];
                     kcorr[g * 32 + j] = 0.f;
+                    {
+                        // gather this (head, token)'s Key-outlier corrections
+                        const int xb = kbeg[j], xe = kend[j];
+                        const int gkv = g / G;
+                        for (int x = xb; x < xe; ++x)
+                            if ((int)((kit[x] & 0x7ffu) >> 7) == gkv) s += kcon[x * G + (g % G)];
+                    }
+                    s = valid ? s : -CUDART_INF_F;
                     const float m_new = fmaxf(m_run, warp_max_redux(s));
                     const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
                     const float p = valid ? exp2f(s - m_new) : 0.f;
@@ -710,13 +654,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const int nvi = hdr[1];
                 for (int x = tid; x < nvi; x += NCT) v_item(vit[x]);
                 if (hdr[3]) {
-                    const uint32_t *vrec_s = reinterpret_cast<const uint32_t *>(sb + P.so_vrec);
-                    int skip = VITEM_CAP;
-                    for (int j = 0; j < ntok; ++j) {
-                        const int b = hdr[8 + 64 + j], e = hdr[8 + 96 + j];
-                        const int s0 = min(e - b, skip);
-                        skip -= s0;
-                        for (int r = b + s0 + tid; r < e; r += NCT) v_item(make_item(vrec_s[r], j, c_lo));
+                    // overflowed bucket: this tile's Value outliers from the CSR rows (rare)
+                    for (int r = tid; r < ntok * kv; r += NCT) {
+                        const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
+                        const int ch = (int)(rec & 0xffffu);
+                        if (ch < c_lo || ch >= c_hi) continue;
+                        v_item((rec & 0xffff0000u) | ((uint32_t)(r / kv) << 11) | (uint32_t)(ch - c_lo));
                     }
                 }
             }
@@ -727,6 +670,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 anc64[tid] = b;
                 anc32[tid] = make_float2((float)b.x, (float)b.y);
             }
+            if (tid < 32) { kbeg[tid] = 0; kend[tid] = 0; }
             compute_sync();
             if (tid == 0) mbar_arrive(empty_b + st);
             tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
@@ -824,25 +768,22 @@ size_t layout(const DevCache &c, Params &P) {
     P.so_kw = (unsigned)off; off = align128(off + 32 * qwc * 4);
     P.so_vw = (unsigned)off; off = align128(off + 32 * qwc * 4);
     P.so_vsz = (unsigned)off; off = align128(off + 256);
-    P.so_kptr = (unsigned)off; off = align128(off + 192);
-    P.so_hdr = (unsigned)off; off = align128(off + (8 + 128) * 4);
-    P.so_kit = (unsigned)off; off = align128(off + KITEM_CAP * 4);
-    P.so_vit = (unsigned)off; off = align128(off + VITEM_CAP * 4);
-    P.so_vrec = (unsigned)off; off = align128(off + (size_t)32 * c.kv * 4);
-    P.so_krec = (unsigned)off;
-    const size_t limit = 227 * 1024;
-    const size_t base = align128(C::fixed + 128);
+    P.so_hdr = (unsigned)off; off = align128(off + 16);
+    P.so_kit = (unsigned)off; off = align128(off + (size_t)c.kcap_g * 4);
+    P.so_vit = (unsigned)off; off = align128(off + (size_t)c.vcap_g * 4);
+    const size_t stb = off;
+    // per-item Key-outlier contributions (one tile at a time), then the stage ring
+    const size_t kcon = align128((size_t)c.kcap_g * c.G * 4);
+    P.so_kcon = (unsigned)align128(C::fixed);
+    const size_t base = align128(P.so_kcon + kcon + 128);
     P.st_base = (unsigned)base;
-    for (int stages = 3; stages >= 2; --stages) {
-        for (int krec = 2048; krec >= 256; krec -= 256) {
-            const size_t stb = align128(off + (size_t)krec * 4);
-            const size_t total = base + stages * stb;
-            if (total <= limit) {
-                P.stages = stages;
-                P.krec_cap = krec;
-                P.st_bytes = (unsigned)stb;
-                return total;
-            }
+    const size_t limit = 227 * 1024;
+    for (int stages = 4; stages >= 2; --stages) {
+        const size_t total = base + stages * stb;
+        if (total <= limit) {
+            P.stages = stages;
+            P.st_bytes = (unsigned)stb;
+            return total;
         }
     }
     return 0;

@@ -17,6 +17,8 @@
 //           channel | fp16(value) << 16  (16-bit index + 16-bit value).
 //   kptr    u32 [cap+1]               Key-outlier CSC column pointers (32-bit per token,
 //           P:1151), kout u32 [kcap] records as above.
+//   kit/vit u32 [ntiles][NG][cap]     Key / Value outliers again, bucketed per (tile, attend
+//           head group) as self-contained items (value, token, channel); gcnt counts.
 //   kpar    float [4][D]              s_c, z_c, lo_c, hi_c of the Keys.
 //   cb      float [4][16]             Key enc, Key dec, Value enc, Value dec codebooks.
 //   mids    double [2][16]            encode midpoints c_j + c_{j+1} (fp64).
@@ -45,6 +47,16 @@ struct DevCache {
     double *mids;   // [2][16]
     int *err;       // device view of the sticky error word (host mapped)
     int *counts;    // prefill scratch [cap]
+    // Outliers bucketed per (32-token tile, attend head group) for the attend kernel:
+    // item = fp16 value << 16 | token-in-tile << 11 | channel - group_start (11 bits),
+    // in token order.  Written by the quantizer next to the token-major CSC/CSR arrays
+    // (which stay the canonical form for export and the overflow fallback).
+    int NG, GW;             // head groups, channels per group
+    int kcap_g, vcap_g;     // items per (tile, group)
+    uint32_t *kit, *vit;    // [ntiles][NG][cap]
+    uint32_t *gcnt;         // [ntiles][NG][2] counts; bit 31 = overflowed (use CSC/CSR)
+    uint16_t *gtmp;         // prefill scratch [cap][NG][2] per-token group counts
+    uint32_t *gbase;        // prefill scratch [NG][2] counts of the first tile before
 };
 
 enum ErrBits { kErrKeyCapacity = 1 };

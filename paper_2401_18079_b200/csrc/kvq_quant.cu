@@ -225,6 +225,46 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
             }
         }
     }
+    // ---- Key outliers bucketed per (tile, attend head group): each thread's channel chunk
+    //      lies in one group (GW % E == 0); slots are reserved per group with one atomic
+    //      (prefill: arbitrary order, sorted afterwards by sort_buckets_kernel; append:
+    //      a single CTA, so slots are in token order already).  count > cap = overflow.
+    {
+        __shared__ int gk[64], gbk[64];
+        if (tid < 64) gk[tid] = 0;
+        __syncthreads();
+        const int myg = cb0 < D ? cb0 / c.GW : 0;
+        int myoff = 0;
+        if (kcnt) myoff = atomicAdd(&gk[myg], kcnt);   // offset of this thread inside the group
+        __syncthreads();
+        // thread order inside a group must be channel order: recompute offsets by a
+        // group-local prefix of the per-thread counts (threads of a group are contiguous)
+        (void)myoff;
+        if (tid < c.NG) {
+            const int tile0 = (int)(n >> 5);
+            gbk[tid] = gk[tid] ? (int)atomicAdd(&c.gcnt[((int64_t)tile0 * c.NG + tid) * 2], (uint32_t)gk[tid]) : 0;
+        }
+        __syncthreads();
+        // group-local exclusive prefix = krank - (rank of the group's first record)
+        __shared__ int gfirst[64];
+        if (tid < 64) gfirst[tid] = 0x7fffffff;
+        __syncthreads();
+        if (kcnt) atomicMin(&gfirst[myg], krank);
+        __syncthreads();
+        if (kcnt) {
+            const int tile0 = (int)(n >> 5), jj0 = (int)(n & 31);
+            int pos = gbk[myg] + (krank - gfirst[myg]);
+            uint32_t *dst = c.kit + ((int64_t)tile0 * c.NG + myg) * c.kcap_g;
+            for (int ch = cb0; ch < cb1; ++ch) {
+                float x = h2f(xk[ch]);
+                if ((x < klo[ch]) || (x > khi[ch])) {
+                    if (pos < c.kcap_g)
+                        dst[pos] = ((uint32_t)xk[ch] << 16) | ((uint32_t)jj0 << 11) | (uint32_t)(ch - myg * c.GW);
+                    ++pos;
+                }
+            }
+        }
+    }
 
     // ----------------------------------------------------------------- Values
     const int k = c.kv;
@@ -314,8 +354,25 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         int vtot;
         int vr = block_excl_scan(vcnt, &vtot, sbuf);
         uint32_t *vo = c.vout + n * (int64_t)k;
+        // Value outliers bucketed per (tile, group) as for the Keys
+        __shared__ int gvc[64], gbv[64], gvf[64];
+        if (tid < 64) { gvc[tid] = 0; gvf[tid] = 0x7fffffff; }
+        __syncthreads();
+        const int myg = cb0 < D ? cb0 / c.GW : 0;
+        if (vcnt) { atomicAdd(&gvc[myg], vcnt); atomicMin(&gvf[myg], vr); }
+        __syncthreads();
+        if (tid < c.NG)
+            gbv[tid] = gvc[tid] ? (int)atomicAdd(&c.gcnt[((int64_t)(n >> 5) * c.NG + tid) * 2 + 1], (uint32_t)gvc[tid]) : 0;
+        __syncthreads();
+        int vpos = vcnt ? gbv[myg] + (vr - gvf[myg]) : 0;
+        uint32_t *vdst = c.vit + ((int64_t)(n >> 5) * c.NG + myg) * c.vcap_g;
         for (int ch = cb0; ch < cb1; ++ch)
-            if (vflag[ch]) vo[vr++] = (uint32_t)ch | ((uint32_t)xv[ch] << 16);
+            if (vflag[ch]) {
+                vo[vr++] = (uint32_t)ch | ((uint32_t)xv[ch] << 16);
+                if (vpos < c.vcap_g)
+                    vdst[vpos] = ((uint32_t)xv[ch] << 16) | ((uint32_t)(n & 31) << 11) | (uint32_t)(ch - myg * c.GW);
+                ++vpos;
+            }
     }
     __syncthreads();
 
@@ -381,6 +438,38 @@ __global__ void __launch_bounds__(1024) scan_counts_kernel(DevCache c, int64_t n
     }
 }
 
+// Sort the bucketed items of (tile, group) lists touched by a prefill into (token, channel)
+// order (the low 16 bits), i.e. the order T successive appends produce.  One CTA per list.
+__global__ void __launch_bounds__(256) sort_buckets_kernel(DevCache c, int64_t tile0, int which) {
+    const int64_t tile = tile0 + blockIdx.x / c.NG;
+    const int g = blockIdx.x % c.NG;
+    const int cap = which ? c.vcap_g : c.kcap_g;
+    uint32_t *lst = (which ? c.vit : c.kit) + (tile * c.NG + g) * cap;
+    const uint32_t cnt = c.gcnt[(tile * c.NG + g) * 2 + which];
+    if (cnt > (uint32_t)cap || cnt < 2) return;   // overflowed lists are not used by attend
+    extern __shared__ uint32_t sitem[];
+    int n2 = 1;
+    while (n2 < (int)cnt) n2 <<= 1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) sitem[i] = i < (int)cnt ? lst[i] : 0xffffffffu;
+    __syncthreads();
+    // bitonic sort on the low 16 bits (token << 11 | channel); keys are unique per list
+    for (int k = 2; k <= n2; k <<= 1)
+        for (int jv = k >> 1; jv > 0; jv >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int ixj = i ^ jv;
+                if (ixj > i) {
+                    const uint32_t a = sitem[i], b = sitem[ixj];
+                    const uint32_t ka = a == 0xffffffffu ? 0xffffffffu : (a & 0xffffu);
+                    const uint32_t kb = b == 0xffffffffu ? 0xffffffffu : (b & 0xffffu);
+                    const bool up = (i & k) == 0;
+                    if ((ka > kb) == up) { sitem[i] = b; sitem[ixj] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < (int)cnt; i += blockDim.x) lst[i] = sitem[i];
+}
+
 size_t qz_smem(int D) {
     size_t b = (size_t)D * 2 * 3 + (size_t)D * 3;
     b = (b + 15) & ~size_t(15);
@@ -401,6 +490,13 @@ cudaError_t launch_qz_bits(const DevCache &c, const __half *K, const __half *V, 
     qz_kernel<BITS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 1);
     scan_counts_kernel<<<1, 1024, 0, s>>>(c, n0, T);
     qz_kernel<BITS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 2);
+    const int64_t tile0 = n0 / 32, tile1 = (n0 + T - 1) / 32;
+    const unsigned nl = (unsigned)((tile1 - tile0 + 1) * c.NG);
+    int pk = 1, pv = 1;
+    while (pk < c.kcap_g) pk <<= 1;
+    while (pv < c.vcap_g) pv <<= 1;
+    sort_buckets_kernel<<<nl, 256, pk * 4, s>>>(c, tile0, 0);
+    sort_buckets_kernel<<<nl, 256, pv * 4, s>>>(c, tile0, 1);
     return cudaGetLastError();
 }
 
