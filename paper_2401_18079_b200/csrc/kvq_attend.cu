@@ -31,11 +31,14 @@
 namespace kvq {
 namespace {
 
-constexpr int NCW = 16;                       // compute warps
+constexpr int NHALF = 2;                      // independent compute halves (alternate tiles)
+constexpr int HW = 8;                         // warps per half
+constexpr int HT = HW * 32;                   // threads per half
+constexpr int NCW = NHALF * HW;               // compute warps
 constexpr int NCT = NCW * 32;                 // compute threads
 constexpr int ATT_THREADS = NCT + 32;         // + 1 producer warp
 constexpr int PW_K = NCW;                     // producer (TMA) warp id
-constexpr int KPW = kPairs / NCW;             // RoPE pairs per compute warp in the K phase
+constexpr int KPW = kPairs / HW;              // RoPE pairs per warp in the K phase
 
 // ------------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -75,9 +78,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-// named barrier among the compute warps only (the producer warps never join it)
-__device__ __forceinline__ void compute_sync() {
-    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
+// named barrier among the warps of one compute half (ids 1, 2; the producer never joins)
+__device__ __forceinline__ void half_sync(int half) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "n"(HT) : "memory");
 }
 
 // acc += lo(x)*lo(y) ; acc2 += hi(x)*hi(y)   (fp16 products, fp32 accumulation)
@@ -137,14 +140,14 @@ struct Cfg {
     static constexpr size_t vlut = (size_t)NE * 32 * 4;
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
     static constexpr size_t t1 = (size_t)kPairs * 32 * 8;
+    // per compute half: red, p, kcorr, hcorr, kbeg/kend, w16, osp, anchors, scalars
+    static constexpr size_t half_bytes =
+        HW * HG * 32 * 4 + HG * 32 * 4 * 3 + 64 * 4 + HG * 32 * 2 + HG * kHeadDim * 4
+        + 64 * 16 + 64 * 8 + HG * 4 * 4 + 64;
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
-        + NCW * HG * 32 * 4            /* red */
-        + HG * 32 * 4 * 3              /* p, kcorr, hcorr */
-        + 64 * 4                       /* kbeg, kend */
-        + HG * 32 * 2                  /* w16 */
-        + HG * kHeadDim * 4            /* osp */
-        + 64 * 16 * 3 + 64 * 8         /* anc64, rot64, qcis, anc32 */
+        + NHALF * half_bytes
+        + 64 * 16 * 2                  /* rot64, qcis */
         + 64 * 4                       /* theta32 */
         + HG * 4 * 8                   /* per-head scalars */
         + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
@@ -188,25 +191,42 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
     float2 *t1tab = reinterpret_cast<float2 *>(sp); sp += C::t1;   // cis(j theta_i) [i][j]
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
-    float *red = reinterpret_cast<float *>(sp); sp += NCW * HG * 32 * 4;
-    float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
-    float *kcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;   // overflow fallback only
-    float *hcorr = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
-    int *kbeg = reinterpret_cast<int *>(sp); sp += 32 * 4;
-    int *kend = reinterpret_cast<int *>(sp); sp += 32 * 4;
-    float *osp = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
-    double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
-    double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    // per compute half h (alternate tiles): scratch of its own tile
+    struct Half {
+        float *red, *p_s, *kcorr, *hcorr, *osp, *beta_s, *m_fin, *l_fin, *z_fin;
+        int *kbeg, *kend;
+        uint16_t *w16;
+        double2 *anc64;
+        float2 *anc32;
+        float *kcon;
+    };
+    Half hs_[NHALF];
+    for (int h = 0; h < NHALF; ++h) {
+        unsigned char *q = sp + h * C::half_bytes;
+        Half &H = hs_[h];
+        H.red = reinterpret_cast<float *>(q); q += HW * HG * 32 * 4;
+        H.p_s = reinterpret_cast<float *>(q); q += HG * 32 * 4;
+        H.kcorr = reinterpret_cast<float *>(q); q += HG * 32 * 4;   // overflow fallback only
+        H.hcorr = reinterpret_cast<float *>(q); q += HG * 32 * 4;
+        H.kbeg = reinterpret_cast<int *>(q); q += 32 * 4;
+        H.kend = reinterpret_cast<int *>(q); q += 32 * 4;
+        H.w16 = reinterpret_cast<uint16_t *>(q); q += HG * 32 * 2;
+        H.osp = reinterpret_cast<float *>(q); q += HG * kHeadDim * 4;
+        q = reinterpret_cast<unsigned char *>(((uintptr_t)q + 15) & ~(uintptr_t)15);
+        H.anc64 = reinterpret_cast<double2 *>(q); q += 64 * 16;
+        H.anc32 = reinterpret_cast<float2 *>(q); q += 64 * 8;
+        H.beta_s = reinterpret_cast<float *>(q); q += HG * 4;
+        H.m_fin = reinterpret_cast<float *>(q); q += HG * 4;
+        H.l_fin = reinterpret_cast<float *>(q); q += HG * 4;
+        H.z_fin = reinterpret_cast<float *>(q); q += HG * 4;
+        H.kcon = reinterpret_cast<float *>(smem_raw + P.so_kcon) + h * c.kcap_g * G;
+    }
+    sp += NHALF * C::half_bytes;
+    double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;   // rotation by 64 theta
     double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
-    float2 *anc32 = reinterpret_cast<float2 *>(sp); sp += 64 * 8;
     float *theta32 = reinterpret_cast<float *>(sp); sp += 64 * 4;
     float *lut_inv = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *lut_sc = reinterpret_cast<float *>(sp); sp += HG * 4;
-    float *beta_s = reinterpret_cast<float *>(sp); sp += HG * 4;
-    float *m_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
-    float *l_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
-    float *z_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
-    uint16_t *w16 = reinterpret_cast<uint16_t *>(sp); sp += HG * 32 * 2;
     float *bound_s = reinterpret_cast<float *>(sp); sp += HG * 64 * 4;
     uint8_t *heavy_s = reinterpret_cast<uint8_t *>(sp); sp += HG * 64;
     int *hv_pair = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
@@ -215,7 +235,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
     int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
-    float *kcon = reinterpret_cast<float *>(smem_raw + P.so_kcon);   // [kcap_g][G]
     // barriers just below the stage ring: full[S], empty[S]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
     uint64_t *full_b = bars, *empty_b = bars + 8;
@@ -253,11 +272,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         double s, co;
         sincos((double)P.pos * th, &s, &co);
         qcis[i] = make_double2(co, s);
-        const double a0 = (double)(c.pos_base + (int64_t)t_begin * kTileTokens) * th;
-        sincos(a0, &s, &co);
-        anc64[i] = make_double2(co, s);
-        anc32[i] = make_float2((float)co, (float)s);
-        sincos(32.0 * th, &s, &co);
+        for (int h = 0; h < NHALF; ++h) {   // half h starts at tile t_begin + h
+            const double a0 = (double)(c.pos_base + (int64_t)(t_begin + h) * kTileTokens) * th;
+            sincos(a0, &s, &co);
+            hs_[h].anc64[i] = make_double2(co, s);
+            hs_[h].anc32[i] = make_float2((float)co, (float)s);
+        }
+        sincos((double)(NHALF * kTileTokens) * th, &s, &co);
         rot64[i] = make_double2(co, s);
     }
     for (int x = tid; x < kPairs * 32; x += ATT_THREADS) {
@@ -267,14 +288,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         sincos((double)j * th, &s, &co);
         t1tab[x] = make_float2((float)co, (float)s);
     }
-    for (int x = tid; x < HG * kHeadDim; x += ATT_THREADS) osp[x] = 0.f;
+    for (int x = tid; x < NHALF * HG * kHeadDim; x += ATT_THREADS) hs_[x / (HG * kHeadDim)].osp[x % (HG * kHeadDim)] = 0.f;
     for (int x = tid; x < HKV * kHeadDim; x += ATT_THREADS) {
         ks_s[x] = ks[c_lo + x];
         kz_s[x] = kz[c_lo + x];
     }
     if (tid < 64) cb_s[tid] = c.cb[tid];
-    for (int x = tid; x < HG * 32; x += ATT_THREADS) kcorr[x] = 0.f;
-    if (tid < 32) { kbeg[tid] = 0; kend[tid] = 0; }
+    for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) hs_[x / (HG * 32)].kcorr[x % (HG * 32)] = 0.f;
+    if (tid < NHALF * 32) { hs_[tid >> 5].kbeg[tid & 31] = 0; hs_[tid >> 5].kend[tid & 31] = 0; }
     if (tid < 16) flag_s[tid] = 0;
     __syncthreads();
     // a1: q~ = RoPE(q, pos) * log2(e)/sqrt(d)
@@ -409,22 +430,27 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     }
 
     // =========================================================== compute warps
-    // V-phase task mapping: one (query head, token group) task per warp
+    // Two independent halves of 8 warps process alternate tiles with their own scratch,
+    // softmax state and named barrier; they share the read-only tables and hide each
+    // other's latency.  Their partials are merged at the end.
+    const int half = warp / HW, hw = warp % HW, htid = tid % HT;
+    Half &H = hs_[half < NHALF ? half : 0];
+    // V-phase task mapping inside a half: warp -> (query head, token groups)
     constexpr int LH = kHeadDim / CPL;          // lanes per token per head
-    constexpr int TPW = 32 / LH;                // tokens per warp task
-    constexpr int NTASK = HG * (32 / TPW);      // tasks per tile
-    static_assert(NTASK <= NCW, "V tasks must fit the compute warps");
-    const bool vtask = warp < NTASK;
-    const int vh = vtask ? warp / (32 / TPW) : 0;            // local query head
-    const int vj = (warp % (32 / TPW)) * TPW + lane / LH;    // token in the tile
+    constexpr int TPW = 32 / LH;                // tokens per task
+    constexpr int TG = 32 / TPW;                // token groups per head
+    constexpr int WPH = HW / HG;                // warps per head
+    constexpr int VT = (TG + WPH - 1) / WPH;    // token groups per warp
+    static_assert(HG <= HW && HW % HG == 0, "head group must divide the half's warps");
+    const int vh = hw / WPH;                                 // local query head
     const int vq = lane % LH;                                // channel group in the head
     const int vkv = vh / G;                                  // local kv head
     float acc[CPL];
 #pragma unroll
     for (int x = 0; x < CPL; ++x) acc[x] = 0.f;
-    // running softmax state (warp g <-> head g): max per warp, deferred per-lane sums
+    // running softmax state (warp g of a half <-> head g): max, deferred per-lane sums
     float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;
-    int E_cur = -126;     // dense V accumulator units: 2^E_cur (CTA uniform)
+    int E_cur = -126;     // dense V accumulator units: 2^E_cur (uniform in a half)
     unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
 
     if (warp < NCW) {
@@ -432,16 +458,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         float t1c[KPW], t1s[KPW];
 #pragma unroll
         for (int k = 0; k < KPW; ++k) {
-            const float2 v = t1tab[(warp * KPW + k) * 32 + lane];
+            const float2 v = t1tab[(hw * KPW + k) * 32 + lane];
             t1c[k] = v.x;
             t1s[k] = v.y;
         }
-        const int kbit0 = 2 * BITS * KPW * warp;
+        const int kbit0 = 2 * BITS * KPW * hw;
         const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
         const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
         long long tc0 = clock64(), tc1;
 
-        for (int t = t_begin; t < t_end; ++t) {
+        for (int t = t_begin + half; t < t_end; t += NHALF) {
             const int it = t - t_begin;
             const int st = it % P.stages;
             mbar_wait(full_b + st, (unsigned)((it / P.stages) & 1));
@@ -455,9 +481,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             const int *hdr = reinterpret_cast<const int *>(sb + P.so_hdr);
             const int64_t n0 = (int64_t)t * 32;
             const int ntok = (int)min((int64_t)32, P.T - n0);
+            const float2 *anc32 = H.anc32;
 
-            // K-outlier correction of one item: (x - K^(code)) * dscore/dK for the G query
-            // heads of its kv head, in fp32
+            // K-outlier correction of one item: (x - K^(code)) * dscore/dK for query head
+            // kvl*G + gg, in fp32
             auto k_corr = [&](uint32_t itm, int gg, int &j_out, int &g_out) -> float {
                 const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
                 const int kvl = chl >> 7, cc = chl & 127, i = cc & 63, up = cc >> 6;
@@ -483,21 +510,21 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const int nk = hdr[0];
                 // items are in (token, channel) order: contributions go to kcon[item][gg],
                 // token boundaries to kbeg/kend; the softmax lane (g, j) gathers them
-                for (int x = tid; x < nk; x += NCT) {
+                for (int x = htid; x < nk; x += HT) {
                     const uint32_t itm = kit[x];
                     int j = 0, g = 0;
 #pragma unroll
-                    for (int gg = 0; gg < G; ++gg) kcon[x * G + gg] = k_corr(itm, gg, j, g);
+                    for (int gg = 0; gg < G; ++gg) H.kcon[x * G + gg] = k_corr(itm, gg, j, g);
                     const int jp = x > 0 ? (int)((kit[x - 1] >> 11) & 31u) : -1;
                     const int jn = x + 1 < nk ? (int)((kit[x + 1] >> 11) & 31u) : 32;
-                    if (jp != j) kbeg[j] = x;
-                    if (jn != j) kend[j] = x + 1;
+                    if (jp != j) H.kbeg[j] = x;
+                    if (jn != j) H.kend[j] = x + 1;
                 }
                 if (hdr[2]) {
                     // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
                     for (int j = 0; j < ntok; ++j) {
                         const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
-                        for (uint32_t r = r0 + tid; r < r1; r += NCT) {
+                        for (uint32_t r = r0 + htid; r < r1; r += HT) {
                             const uint32_t rec = __ldcg(c.kout + r);
                             const int ch = (int)(rec & 0xffffu);
                             if (ch < c_lo || ch >= c_hi) continue;
@@ -506,28 +533,28 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                             for (int gg = 0; gg < G; ++gg) {
                                 int jj, g;
                                 const float v = k_corr(itm, gg, jj, g);
-                                atomicAdd(&kcorr[g * 32 + jj], v);
+                                atomicAdd(&H.kcorr[g * 32 + jj], v);
                             }
                         }
                     }
                 }
-                if (tid < HG * 32) {
+                if (htid < HG * 32) {
                     // heavy RoPE pairs of head g in fp32 (tables hlut), one thread per (g, j)
-                    const int g = tid >> 5, j = tid & 31;
+                    const int g = htid >> 5, j = htid & 31;
                     float hc = 0.f;
                     const int nh = hv_n[g];
-                    for (int hs = 0; hs < nh; ++hs) {
-                        const int i = hv_pair[g * 8 + hs];
+                    for (int hsl = 0; hsl < nh; ++hsl) {
+                        const int i = hv_pair[g * 8 + hsl];
                         const int bit = 2 * BITS * i;
                         const int wq = (g / G) * 4 * BITS + (bit >> 5);
                         unsigned long long w64 = kw_s[wq * 32 + j];
                         if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
                         const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                        const float2 ab = hlut[(g * HMAX + hs) * NE + pc];
+                        const float2 ab = hlut[(g * HMAX + hsl) * NE + pc];
                         const float2 an = anc32[i], tt = t1tab[i * 32 + j];
                         hc += (an.x * tt.x - an.y * tt.y) * ab.x + (an.x * tt.y + an.y * tt.x) * ab.y;
                     }
-                    hcorr[g * 32 + j] = hc;
+                    H.hcorr[g * 32 + j] = hc;
                 }
             }
             // ------------------------------------------------------------ a2: K dense
@@ -545,7 +572,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 }
 #pragma unroll
                 for (int k = 0; k < KPW; ++k) {
-                    const int i = warp * KPW + k;
+                    const int i = hw * KPW + k;
                     const float2 an = anc32[i];
                     const float cc = an.x * t1c[k] - an.y * t1s[k];
                     const float ss = an.x * t1s[k] + an.y * t1c[k];
@@ -562,9 +589,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     }
                 }
 #pragma unroll
-                for (int g = 0; g < HG; ++g) red[(warp * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
+                for (int g = 0; g < HG; ++g) H.red[(hw * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
             }
-            compute_sync();
+            half_sync(half);
             tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
 
             // ------------------------------------------------------- a4: online softmax
@@ -573,20 +600,20 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 smax = warp_max_redux(smax);
                 int E_new = E_cur;
                 if (smax > 0.f) E_new = max(E_cur, ilogbf(smax) + 1);
-                if (warp < HG) {
-                    const int g = warp, j = lane;
+                if (hw < HG) {
+                    const int g = hw, j = lane;
                     const bool valid = j < ntok;
                     float s = 0.f;
 #pragma unroll
-                    for (int w = 0; w < NCW; ++w) s += red[(w * HG + g) * 32 + j];
-                    s = s * lut_inv[g] + kcorr[g * 32 + j] + hcorr[g * 32 + j];
-                    kcorr[g * 32 + j] = 0.f;
+                    for (int w = 0; w < HW; ++w) s += H.red[(w * HG + g) * 32 + j];
+                    s = s * lut_inv[g] + H.kcorr[g * 32 + j] + H.hcorr[g * 32 + j];
+                    H.kcorr[g * 32 + j] = 0.f;
                     {
                         // gather this (head, token)'s Key-outlier corrections
-                        const int xb = kbeg[j], xe = kend[j];
+                        const int xb = H.kbeg[j], xe = H.kend[j];
                         const int gkv = g / G;
                         for (int x = xb; x < xe; ++x)
-                            if ((int)((kit[x] & 0x7ffu) >> 7) == gkv) s += kcon[x * G + (g % G)];
+                            if ((int)((kit[x] & 0x7ffu) >> 7) == gkv) s += H.kcon[x * G + (g % G)];
                     }
                     s = valid ? s : -CUDART_INF_F;
                     const float m_new = fmaxf(m_run, warp_max_redux(s));
@@ -596,40 +623,47 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     l_lane = l_lane * alpha + p;
                     z_lane = z_lane * alpha + p * sz.y;
                     m_run = m_new;
-                    p_s[g * 32 + j] = p;
-                    w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * ldexpf(sz.x, -E_new)));
+                    H.p_s[g * 32 + j] = p;
+                    H.w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * ldexpf(sz.x, -E_new)));
                     if (alpha != 1.f) {
 #pragma unroll
-                        for (int x = 0; x < kHeadDim / 32; ++x) osp[g * kHeadDim + x * 32 + lane] *= alpha;
+                        for (int x = 0; x < kHeadDim / 32; ++x) H.osp[g * kHeadDim + x * 32 + lane] *= alpha;
                     }
-                    if (lane == 0) beta_s[g] = alpha * ldexpf(1.f, E_cur - E_new);
+                    if (lane == 0) H.beta_s[g] = alpha * ldexpf(1.f, E_cur - E_new);
                 }
                 E_cur = E_new;
             }
-            compute_sync();
+            half_sync(half);
             tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
 
             // -------------------------------------------------------- a5: P.V dense
-            if (vtask) {
-                const float b = beta_s[vh];
+            {
+                const float b = H.beta_s[vh];
                 if (b != 1.f) {
 #pragma unroll
                     for (int x = 0; x < CPL; ++x) acc[x] *= b;
                 }
-                const uint16_t w = w16[vh * 32 + vj];
-                uint32_t vw[VWL];
-                const uint32_t *src = vw_s + (vkv * 32 + vj) * (4 * BITS) + vq * VWL;
 #pragma unroll
-                for (int x = 0; x < VWL; ++x) vw[x] = src[x];
+                for (int v = 0; v < VT; ++v) {
+                    const int tg = (hw % WPH) * VT + v;
+                    if (tg < TG) {
+                        const int vj = tg * TPW + lane / LH;
+                        const uint16_t w = H.w16[vh * 32 + vj];
+                        uint32_t vw[VWL];
+                        const uint32_t *src = vw_s + (vkv * 32 + vj) * (4 * BITS) + vq * VWL;
 #pragma unroll
-                for (int pp = 0; pp < CPL / 2; ++pp) {
-                    const int bit = 2 * BITS * pp;
-                    const int wi = bit >> 5, sh = bit & 31;
-                    uint32_t pc;
-                    if (sh + 2 * BITS <= 32) pc = (vw[wi] >> sh) & (NE - 1);
-                    else pc = (uint32_t)((((unsigned long long)vw[wi + 1] << 32) | vw[wi]) >> sh) & (NE - 1);
-                    const uint32_t cv = vlut[pc * 32 + lane];
-                    fma_w_f16x2(w, cv, acc[2 * pp], acc[2 * pp + 1]);
+                        for (int x = 0; x < VWL; ++x) vw[x] = src[x];
+#pragma unroll
+                        for (int pp = 0; pp < CPL / 2; ++pp) {
+                            const int bit = 2 * BITS * pp;
+                            const int wi = bit >> 5, sh = bit & 31;
+                            uint32_t pc;
+                            if (sh + 2 * BITS <= 32) pc = (vw[wi] >> sh) & (NE - 1);
+                            else pc = (uint32_t)((((unsigned long long)vw[wi + 1] << 32) | vw[wi]) >> sh) & (NE - 1);
+                            const uint32_t cv = vlut[pc * 32 + lane];
+                            fma_w_f16x2(w, cv, acc[2 * pp], acc[2 * pp + 1]);
+                        }
+                    }
                 }
             }
             // ---------------------------------------------------- a6: V outliers
@@ -648,14 +682,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
                         const int g = kvl * G + gg;
-                        atomicAdd(&osp[g * kHeadDim + cc], p_s[g * 32 + j] * delta);
+                        atomicAdd(&H.osp[g * kHeadDim + cc], H.p_s[g * 32 + j] * delta);
                     }
                 };
                 const int nvi = hdr[1];
-                for (int x = tid; x < nvi; x += NCT) v_item(vit[x]);
+                for (int x = htid; x < nvi; x += HT) v_item(vit[x]);
                 if (hdr[3]) {
                     // overflowed bucket: this tile's Value outliers from the CSR rows (rare)
-                    for (int r = tid; r < ntok * kv; r += NCT) {
+                    for (int r = htid; r < ntok * kv; r += HT) {
                         const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
                         const int ch = (int)(rec & 0xffffu);
                         if (ch < c_lo || ch >= c_hi) continue;
@@ -663,26 +697,26 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     }
                 }
             }
-            // advance anchors to the next tile (fp64 complex rotation by 32 theta_i)
-            if (tid < 64) {
-                const double2 a = anc64[tid], r = rot64[tid];
+            // advance this half's anchors by two tiles (fp64 complex rotation by 64 theta_i)
+            if (htid < 64) {
+                const double2 a = H.anc64[htid], r = rot64[htid];
                 const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
-                anc64[tid] = b;
-                anc32[tid] = make_float2((float)b.x, (float)b.y);
+                H.anc64[htid] = b;
+                H.anc32[htid] = make_float2((float)b.x, (float)b.y);
             }
-            if (tid < 32) { kbeg[tid] = 0; kend[tid] = 0; }
-            compute_sync();
-            if (tid == 0) mbar_arrive(empty_b + st);
+            if (htid < 32) { H.kbeg[htid] = 0; H.kend[htid] = 0; }
+            half_sync(half);
+            if (htid == 0) mbar_arrive(empty_b + st);
             tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
         }
-        if (warp < HG) {
+        if (hw < HG) {
             const float l = warp_sum(l_lane), z = warp_sum(z_lane);
-            if (lane == 0) { m_fin[warp] = m_run; l_fin[warp] = l; z_fin[warp] = z; }
+            if (lane == 0) { H.m_fin[hw] = m_run; H.l_fin[hw] = l; H.z_fin[hw] = z; }
         }
-        if (vtask) {
+        {
             // dense P.V accumulators are in units of 2^-E_cur
             const float sc = ldexpf(1.f, E_cur);
-            float *dst = osp + vh * kHeadDim + vq * CPL;
+            float *dst = H.osp + vh * kHeadDim + vq * CPL;
 #pragma unroll
             for (int x = 0; x < CPL; ++x) atomicAdd(&dst[x], acc[x] * sc);
         }
@@ -694,15 +728,21 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     }
     __syncthreads();
 
-    // ------------------------------------------------------------ write partial
+    // ------------------------------------------------ write partial (merge halves)
     float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
-    for (int x = tid; x < HG * kHeadDim; x += ATT_THREADS) {
-        const int g = x >> 7, ch = x & 127;
-        part[(g0 + g) * (kHeadDim + 2) + ch] = ntl > 0 ? osp[x] + z_fin[g] : 0.f;
-    }
-    if (tid < HG) {
-        part[(g0 + tid) * (kHeadDim + 2) + kHeadDim] = ntl > 0 ? m_fin[tid] : -CUDART_INF_F;
-        part[(g0 + tid) * (kHeadDim + 2) + kHeadDim + 1] = ntl > 0 ? l_fin[tid] : 0.f;
+    for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
+        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+        float m = -CUDART_INF_F;
+        for (int h = 0; h < NHALF; ++h)
+            if (ntl > h) m = fmaxf(m, hs_[h].m_fin[g]);
+        float l = 0.f, o = 0.f;
+        for (int h = 0; h < NHALF; ++h) {
+            if (ntl <= h || hs_[h].l_fin[g] == 0.f) continue;
+            const float w = exp2f(hs_[h].m_fin[g] - m);
+            l += w * hs_[h].l_fin[g];
+            if (ch < kHeadDim) o += w * (hs_[h].osp[g * kHeadDim + ch] + hs_[h].z_fin[g]);
+        }
+        part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
     }
     // ------------------------------------------------------- a7: split merge
     __threadfence();
@@ -773,7 +813,7 @@ size_t layout(const DevCache &c, Params &P) {
     P.so_vit = (unsigned)off; off = align128(off + (size_t)c.vcap_g * 4);
     const size_t stb = off;
     // per-item Key-outlier contributions (one tile at a time), then the stage ring
-    const size_t kcon = align128((size_t)c.kcap_g * c.G * 4);
+    const size_t kcon = align128((size_t)NHALF * c.kcap_g * c.G * 4);
     P.so_kcon = (unsigned)align128(C::fixed);
     const size_t base = align128(P.so_kcon + kcon + 128);
     P.st_base = (unsigned)base;
