@@ -174,7 +174,7 @@ struct Params {
 };
 
 template <int BITS, int HG, int G>
-__global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params P) {
+__global__ void __maxnreg__(120) att_kernel(DevCache c, Params P) {
     using C = Cfg<BITS, HG>;
     constexpr int NE = C::NE;
     constexpr int CM = (1 << BITS) - 1;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
     float2 *t1tab = reinterpret_cast<float2 *>(sp); sp += C::t1;   // cis(j theta_i) [i][j]
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
-    // per compute half h (alternate tiles): scratch of its own tile
+    // per compute half h (alternate tiles): scratch of its own tile, at sp + h*half_bytes
     struct Half {
         float *red, *p_s, *kcorr, *hcorr, *osp, *beta_s, *m_fin, *l_fin, *z_fin;
         int *kbeg, *kend;
@@ -200,10 +200,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         float2 *anc32;
         float *kcon;
     };
-    Half hs_[NHALF];
-    for (int h = 0; h < NHALF; ++h) {
+    auto half_at = [&](int h) -> Half {
+        Half H;
         unsigned char *q = sp + h * C::half_bytes;
-        Half &H = hs_[h];
         H.red = reinterpret_cast<float *>(q); q += HW * HG * 32 * 4;
         H.p_s = reinterpret_cast<float *>(q); q += HG * 32 * 4;
         H.kcorr = reinterpret_cast<float *>(q); q += HG * 32 * 4;   // overflow fallback only
@@ -212,7 +211,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         H.kend = reinterpret_cast<int *>(q); q += 32 * 4;
         H.w16 = reinterpret_cast<uint16_t *>(q); q += HG * 32 * 2;
         H.osp = reinterpret_cast<float *>(q); q += HG * kHeadDim * 4;
-        q = reinterpret_cast<unsigned char *>(((uintptr_t)q + 15) & ~(uintptr_t)15);
+        q += (16 - ((HG * 32 * 2) % 16)) % 16;
         H.anc64 = reinterpret_cast<double2 *>(q); q += 64 * 16;
         H.anc32 = reinterpret_cast<float2 *>(q); q += 64 * 8;
         H.beta_s = reinterpret_cast<float *>(q); q += HG * 4;
@@ -220,7 +219,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         H.l_fin = reinterpret_cast<float *>(q); q += HG * 4;
         H.z_fin = reinterpret_cast<float *>(q); q += HG * 4;
         H.kcon = reinterpret_cast<float *>(smem_raw + P.so_kcon) + h * c.kcap_g * G;
-    }
+        return H;
+    };
     sp += NHALF * C::half_bytes;
     double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;   // rotation by 64 theta
     double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
@@ -275,8 +275,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         for (int h = 0; h < NHALF; ++h) {   // half h starts at tile t_begin + h
             const double a0 = (double)(c.pos_base + (int64_t)(t_begin + h) * kTileTokens) * th;
             sincos(a0, &s, &co);
-            hs_[h].anc64[i] = make_double2(co, s);
-            hs_[h].anc32[i] = make_float2((float)co, (float)s);
+            half_at(h).anc64[i] = make_double2(co, s);
+            half_at(h).anc32[i] = make_float2((float)co, (float)s);
         }
         sincos((double)(NHALF * kTileTokens) * th, &s, &co);
         rot64[i] = make_double2(co, s);
@@ -288,14 +288,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         sincos((double)j * th, &s, &co);
         t1tab[x] = make_float2((float)co, (float)s);
     }
-    for (int x = tid; x < NHALF * HG * kHeadDim; x += ATT_THREADS) hs_[x / (HG * kHeadDim)].osp[x % (HG * kHeadDim)] = 0.f;
+    for (int x = tid; x < NHALF * HG * kHeadDim; x += ATT_THREADS) half_at(x / (HG * kHeadDim)).osp[x % (HG * kHeadDim)] = 0.f;
     for (int x = tid; x < HKV * kHeadDim; x += ATT_THREADS) {
         ks_s[x] = ks[c_lo + x];
         kz_s[x] = kz[c_lo + x];
     }
     if (tid < 64) cb_s[tid] = c.cb[tid];
-    for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) hs_[x / (HG * 32)].kcorr[x % (HG * 32)] = 0.f;
-    if (tid < NHALF * 32) { hs_[tid >> 5].kbeg[tid & 31] = 0; hs_[tid >> 5].kend[tid & 31] = 0; }
+    for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) half_at(x / (HG * 32)).kcorr[x % (HG * 32)] = 0.f;
+    if (tid < NHALF * 32) { half_at(tid >> 5).kbeg[tid & 31] = 0; half_at(tid >> 5).kend[tid & 31] = 0; }
     if (tid < 16) flag_s[tid] = 0;
     __syncthreads();
     // a1: q~ = RoPE(q, pos) * log2(e)/sqrt(d)
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // softmax state and named barrier; they share the read-only tables and hide each
     // other's latency.  Their partials are merged at the end.
     const int half = warp / HW, hw = warp % HW, htid = tid % HT;
-    Half &H = hs_[half < NHALF ? half : 0];
+    const Half H = half_at(half < NHALF ? half : 0);
     // V-phase task mapping inside a half: warp -> (query head, token groups)
     constexpr int LH = kHeadDim / CPL;          // lanes per token per head
     constexpr int TPW = 32 / LH;                // tokens per task
@@ -730,19 +730,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 
     // ------------------------------------------------ write partial (merge halves)
     float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
-    for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
-        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
-        float m = -CUDART_INF_F;
-        for (int h = 0; h < NHALF; ++h)
-            if (ntl > h) m = fmaxf(m, hs_[h].m_fin[g]);
-        float l = 0.f, o = 0.f;
-        for (int h = 0; h < NHALF; ++h) {
-            if (ntl <= h || hs_[h].l_fin[g] == 0.f) continue;
-            const float w = exp2f(hs_[h].m_fin[g] - m);
-            l += w * hs_[h].l_fin[g];
-            if (ch < kHeadDim) o += w * (hs_[h].osp[g * kHeadDim + ch] + hs_[h].z_fin[g]);
+    {
+        const Half H0 = half_at(0), H1 = half_at(1);
+        for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
+            const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+            const bool u0 = ntl > 0 && H0.l_fin[g] != 0.f, u1 = ntl > 1 && H1.l_fin[g] != 0.f;
+            const float m0 = u0 ? H0.m_fin[g] : -CUDART_INF_F, m1 = u1 ? H1.m_fin[g] : -CUDART_INF_F;
+            const float m = fmaxf(m0, m1);
+            const float w0 = u0 ? exp2f(m0 - m) : 0.f, w1 = u1 ? exp2f(m1 - m) : 0.f;
+            const float l = w0 * (u0 ? H0.l_fin[g] : 0.f) + w1 * (u1 ? H1.l_fin[g] : 0.f);
+            float o = 0.f;
+            if (ch < kHeadDim) {
+                if (u0) o += w0 * (H0.osp[g * kHeadDim + ch] + H0.z_fin[g]);
+                if (u1) o += w1 * (H1.osp[g * kHeadDim + ch] + H1.z_fin[g]);
+            }
+            part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
         }
-        part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
     }
     // ------------------------------------------------------- a7: split merge
     __threadfence();
