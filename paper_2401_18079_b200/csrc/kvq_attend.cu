@@ -174,7 +174,7 @@ struct Params {
 };
 
 template <int BITS, int HG, int G>
-__global__ void __maxnreg__(120) att_kernel(DevCache c, Params P) {
+__global__ void __maxnreg__(112) att_kernel(DevCache c, Params P) {
     using C = Cfg<BITS, HG>;
     constexpr int NE = C::NE;
     constexpr int CM = (1 << BITS) - 1;
