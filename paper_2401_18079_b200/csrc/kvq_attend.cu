@@ -36,8 +36,7 @@ constexpr int HW = 8;                         // warps per half
 constexpr int HT = HW * 32;                   // threads per half
 constexpr int NCW = NHALF * HW;               // compute warps
 constexpr int NCT = NCW * 32;                 // compute threads
-constexpr int ATT_THREADS = NCT + 32;         // + 1 producer warp
-constexpr int PW_K = NCW;                     // producer (TMA) warp id
+constexpr int ATT_THREADS = NCT;              // 16 warps: 4 per SM sub-partition
 constexpr int KPW = kPairs / HW;              // RoPE pairs per warp in the K phase
 
 // ------------------------------------------------------------------ PTX helpers --
@@ -174,7 +173,7 @@ struct Params {
 };
 
 template <int BITS, int HG, int G>
-__global__ void __maxnreg__(112) att_kernel(DevCache c, Params P) {
+__global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params P) {
     using C = Cfg<BITS, HG>;
     constexpr int NE = C::NE;
     constexpr int CM = (1 << BITS) - 1;
@@ -237,7 +236,7 @@ __global__ void __maxnreg__(112) att_kernel(DevCache c, Params P) {
     int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
     // barriers just below the stage ring: full[S], empty[S]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
-    uint64_t *full_b = bars, *empty_b = bars + 8;
+    uint64_t *full_b = bars;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
@@ -259,7 +258,6 @@ __global__ void __maxnreg__(112) att_kernel(DevCache c, Params P) {
     if (tid == 0) {
         for (int s = 0; s < P.stages; ++s) {
             mbar_init(full_b + s, 1);
-            mbar_init(empty_b + s, 1);
         }
         mbar_fence_init();
     }
@@ -382,52 +380,50 @@ __global__ void __maxnreg__(112) att_kernel(DevCache c, Params P) {
     }
     __syncthreads();
 
-    // ================================================================== producer
-    if (warp == PW_K) {
-        // counts of the (tile, group) outlier buckets of the next tile to issue (lane 0)
-        uint32_t nk_next = 0, nv_next = 0;
-        auto counts_at = [&](int t) {
-            const uint32_t *gc = c.gcnt + ((int64_t)t * c.NG + hg) * 2;
-            nk_next = __ldg(gc);
-            nv_next = __ldg(gc + 1);
-        };
-        if (lane == 0 && ntl > 0) counts_at(t_begin);
-        const int Sg = P.stages;
-        for (int it = 0; it < ntl; ++it) {
-            const int ti = t_begin + it;
-            const int si = it % Sg;
-            if (it >= Sg) mbar_wait(empty_b + si, (unsigned)(((it / Sg) - 1) & 1));
-            unsigned char *sb = stage_ptr(si);
-            uint64_t *bar = full_b + si;
-            const uint32_t nk = __shfl_sync(0xffffffffu, nk_next, 0);
-            const uint32_t nv = __shfl_sync(0xffffffffu, nv_next, 0);
-            const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
-            const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
-            const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
-            const unsigned b_kw = 32u * QWC * 4u;
-            const unsigned total = 2u * b_kw + 256u + bk + bv;
-            if (lane == 0) {
-                int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
-                hdr[0] = kov ? 0 : (int)nk;
-                hdr[1] = vov ? 0 : (int)nv;
-                hdr[2] = kov;
-                hdr[3] = vov;
-                fence_proxy_async();
-                mbar_expect_tx(bar, total);
-            }
-            __syncwarp();
-            const int64_t n0 = (int64_t)ti * 32;
-            const int64_t bucket = (int64_t)ti * c.NG + hg;
-            if (lane == 0)
-                bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
-            if (lane == 1)
-                bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
-            if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
-            if (lane == 3 && bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
-            if (lane == 4 && bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
-            if (lane == 0 && ti + 1 < t_end) counts_at(ti + 1);
+    // ====================================================== TMA issue (per half)
+    // Each half owns SH = stages/2 ring slots and issues its own tiles: tiles of half h are
+    // t_k = t_begin + h + 2k, slot k % SH.  The last warp of the half issues tile t_{k+SH-1}
+    // at the top of iteration k, into the slot its half released at the end of k-1.
+    auto issue = [&](int hh, int k) {   // called by one full warp
+        const int SH = P.stages / NHALF;
+        const int ti = t_begin + hh + NHALF * k;
+        if (ti >= t_end) return;
+        const int si = hh * SH + (k % SH);
+        unsigned char *sb = stage_ptr(si);
+        uint64_t *bar = full_b + si;
+        uint32_t nk = 0, nv = 0;
+        if (lane == 0) {
+            const uint32_t *gc = c.gcnt + ((int64_t)ti * c.NG + hg) * 2;
+            nk = __ldg(gc);
+            nv = __ldg(gc + 1);
         }
-    }
+        nk = __shfl_sync(0xffffffffu, nk, 0);
+        nv = __shfl_sync(0xffffffffu, nv, 0);
+        const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
+        const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
+        const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
+        const unsigned b_kw = 32u * QWC * 4u;
+        const unsigned total = 2u * b_kw + 256u + bk + bv;
+        if (lane == 0) {
+            int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
+            hdr[0] = kov ? 0 : (int)nk;
+            hdr[1] = vov ? 0 : (int)nv;
+            hdr[2] = kov;
+            hdr[3] = vov;
+            fence_proxy_async();
+            mbar_expect_tx(bar, total);
+        }
+        __syncwarp();
+        const int64_t n0 = (int64_t)ti * 32;
+        const int64_t bucket = (int64_t)ti * c.NG + hg;
+        if (lane == 0)
+            bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
+        if (lane == 1)
+            bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
+        if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
+        if (lane == 3 && bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
+        if (lane == 4 && bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
+    };
 
     // =========================================================== compute warps
     // Two independent halves of 8 warps process alternate tiles with their own scratch,
@@ -467,10 +463,14 @@ __global__ void __maxnreg__(112) att_kernel(DevCache c, Params P) {
         const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
         long long tc0 = clock64(), tc1;
 
+        const int SH = P.stages / NHALF;
+        if (hw == HW - 1)
+            for (int k = 0; k < SH - 1; ++k) issue(half, k);
         for (int t = t_begin + half; t < t_end; t += NHALF) {
-            const int it = t - t_begin;
-            const int st = it % P.stages;
-            mbar_wait(full_b + st, (unsigned)((it / P.stages) & 1));
+            const int kk = (t - t_begin) / NHALF;       // this half's k-th tile
+            const int st = half * SH + (kk % SH);
+            if (hw == HW - 1) issue(half, kk + SH - 1);
+            mbar_wait(full_b + st, (unsigned)((kk / SH) & 1));
             tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
             unsigned char *sb = stage_ptr(st);
             const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
@@ -706,7 +706,6 @@ __global__ void __maxnreg__(112) att_kernel(DevCache c, Params P) {
             }
             if (htid < 32) { H.kbeg[htid] = 0; H.kend[htid] = 0; }
             half_sync(half);
-            if (htid == 0) mbar_arrive(empty_b + st);
             tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
         }
         if (hw < HG) {
@@ -821,7 +820,7 @@ size_t layout(const DevCache &c, Params &P) {
     const size_t base = align128(P.so_kcon + kcon + 128);
     P.st_base = (unsigned)base;
     const size_t limit = 227 * 1024;
-    for (int stages = 4; stages >= 2; --stages) {
+    for (int stages = 4; stages >= 2; stages -= 2) {
         const size_t total = base + stages * stb;
         if (total <= limit) {
             P.stages = stages;
