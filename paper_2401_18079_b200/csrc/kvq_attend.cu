@@ -199,9 +199,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         float2 *anc32;
         float *kcon;
     };
+    unsigned char *const half_base = sp;
     auto half_at = [&](int h) -> Half {
         Half H;
-        unsigned char *q = sp + h * C::half_bytes;
+        unsigned char *q = half_base + h * C::half_bytes;
         H.red = reinterpret_cast<float *>(q); q += HW * HG * 32 * 4;
         H.p_s = reinterpret_cast<float *>(q); q += HG * 32 * 4;
         H.kcorr = reinterpret_cast<float *>(q); q += HG * 32 * 4;   // overflow fallback only
