@@ -891,7 +891,8 @@ int attend_auto_splits(const DevCache &c, int64_t T, int hg) {
     int sms = 148;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int S = (sms + n_hg - 1) / n_hg;
+    // one wave: every CTA needs a whole SM (launch_bounds(.., 1), ~200 KB smem)
+    int S = sms / n_hg;
     if (S > ntiles) S = ntiles;
     if (S < 1) S = 1;
     return S;
