@@ -176,7 +176,7 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     kvq_status st = KVQ_OK;
     auto A = [&](auto **p, size_t bytes) { if (st == KVQ_OK) st = dev_alloc(c, p, bytes); };
     A(&d.kcodes, (size_t)(d.cap / 32) * d.QW * 32 * 4);
-    A(&d.vcodes, (size_t)d.cap * d.VW * 4 + 16);   // [cap/32][H_kv][32][4b]
+    A(&d.vcodes, (size_t)d.cap * d.VW * 4 + 16);   // [cap/32][H_kv][4b][32]
     A(&d.vsz, (size_t)d.cap * sizeof(float2));
     A(&d.vout, (size_t)d.cap * (kv > 0 ? kv : 1) * 4);
     A(&d.kptr, (size_t)(d.cap + 64) * 4);   // +63: attend stages 48-word CSC slices
@@ -294,6 +294,8 @@ kvq_status kvq_reset(kvq_cache *c, void *stream) {
     CK(cudaSetDevice(c->cfg.device));
     CK(cudaMemsetAsync(c->dc.kptr, 0, 4, (cudaStream_t)stream));
     CK(cudaMemsetAsync(c->dc.gcnt, 0, (size_t)(c->dc.cap / 32) * c->dc.NG * 2 * 4, (cudaStream_t)stream));
+    // Value code words are OR-ed into by the quantizer (fragment layout)
+    CK(cudaMemsetAsync(c->dc.vcodes, 0, (size_t)((c->T + 31) / 32) * 32 * c->dc.VW * 4, (cudaStream_t)stream));
     c->T = 0;
     return KVQ_OK;
 }
@@ -471,10 +473,10 @@ kvq_status kvq_export(kvq_cache *c, int64_t t0, int64_t t1, kvq_export_buf *buf)
             const int j = (int)(t % 32);
             for (int ch = 0; ch < D; ++ch) {
                 const int h = ch / kHeadDim, cc = ch % kHeadDim;
-                const uint32_t *row = vc.data() + ((tl * d.H_kv + h) * 32 + j) * hw;
-                const int bit = b * cc;
-                uint64_t w = row[bit / 32];
-                if (bit % 32 + b > 32) w |= (uint64_t)row[bit / 32 + 1] << 32;
+                const int bit = vf_bit(j, cc, b), lane = vf_lane(j, cc);
+                const uint32_t *wp = vc.data() + vf_word(tl, d.H_kv, h, bit / 32, lane, b);
+                uint64_t w = wp[0];
+                if (bit % 32 + b > 32) w |= (uint64_t)wp[32] << 32;
                 buf->vcodes[(t - t0) * D + ch] = (uint8_t)((w >> (bit % 32)) & ((1u << b) - 1));
             }
         }

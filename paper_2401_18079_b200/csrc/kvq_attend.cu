@@ -93,14 +93,13 @@ __device__ __forceinline__ void fma2_f16_f32(uint32_t x, uint32_t y, float &acc,
         : "r"(x), "r"(y));
 }
 
-// acc_a += w*lo(v) ; acc_b += w*hi(v)   with w a scalar fp16
-__device__ __forceinline__ void fma_w_f16x2(uint16_t w, uint32_t v, float &acc_a, float &acc_b) {
-    asm("{\n\t.reg .b16 v0, v1;\n\t"
-        "mov.b32 {v0, v1}, %3;\n\t"
-        "fma.rn.f32.f16 %0, %2, v0, %0;\n\t"
-        "fma.rn.f32.f16 %1, %2, v1, %1;\n\t}"
-        : "+f"(acc_a), "+f"(acc_b)
-        : "h"(w), "r"(v));
+// d += A * B on the tensor cores: mma.m16n8k16, fp16 operands, fp32 accumulation
+__device__ __forceinline__ void mma_f16_f32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
@@ -128,13 +127,11 @@ __device__ __forceinline__ float warp_max_redux(float v) {
 }
 
 // ---------------------------------------------------------------- configuration --
-constexpr int cpl_for(int bits) { return bits == 4 ? 8 : 32; }   // whole code words per lane
 
 template <int BITS, int HG>
 struct Cfg {
     static constexpr int NE = 1 << (2 * BITS);
     static constexpr int HMAX = BITS == 4 ? 4 : 8;   // fp32 "heavy" pairs per head
-    static constexpr int CPL = cpl_for(BITS);
     static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
     static constexpr size_t vlut = (size_t)NE * 32 * 4;
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
@@ -179,8 +176,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     constexpr int CM = (1 << BITS) - 1;
     constexpr int HKV = HG / G;
     constexpr int QWC = HKV * 4 * BITS;             // K (and V) words per token in the CTA
-    constexpr int CPL = C::CPL;                     // V channels per lane
-    constexpr int VWL = CPL * BITS / 32;            // V words per lane per token
     constexpr int HMAX = C::HMAX;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -432,20 +427,24 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // other's latency.  Their partials are merged at the end.
     const int half = warp / HW, hw = warp % HW, htid = tid % HT;
     const Half H = half_at(half < NHALF ? half : 0);
-    // V-phase task mapping inside a half: warp -> (query head, token groups)
-    constexpr int LH = kHeadDim / CPL;          // lanes per token per head
-    constexpr int TPW = 32 / LH;                // tokens per task
-    constexpr int TG = 32 / TPW;                // token groups per head
-    constexpr int WPH = HW / HG;                // warps per head
-    constexpr int VT = (TG + WPH - 1) / WPH;    // token groups per warp
-    static_assert(HG <= HW && HW % HG == 0, "head group must divide the half's warps");
-    const int vh = hw / WPH;                                 // local query head
-    const int vq = lane % LH;                                // channel group in the head
-    const int vkv = vh / G;                                  // local kv head
-    float acc[CPL];
+    // V-phase task mapping inside a half (tensor cores, mma.m16n8k16): warp -> (local KV
+    // head vkv, m-tiles [mt0, mt0 + MTW) of 16 channels); A = V codes (rows = channels,
+    // k = tokens) through the pair table, B = fp16 weights (columns = the G query heads of
+    // vkv), D = fp32 P.V accumulators (columns >= G unused).
+    constexpr int WPK = HW / HKV;               // warps per KV head
+    constexpr int MTW = 8 / WPK;                // m-tiles per warp
+    constexpr int FB = 2 * BITS;                // bits per A field (2 tokens x 1 channel)
+    constexpr int NWV = (MTW * 16 * BITS + 31) / 32;   // code words per lane per tile
+    static_assert(HKV <= HW && HW % HKV == 0 && G <= 8, "V task mapping");
+    const int vkv = hw / WPK;                                // local KV head
+    const int mt0 = (hw % WPK) * MTW;
+    const int vbit0 = mt0 * 16 * BITS;
+    const int vw0 = vbit0 >> 5, voff = vbit0 & 31;           // voff = 16 only for b=3, MTW=1
+    const int vg = lane >> 2, vt = lane & 3;
+    const int vq_lo = vkv * G + min(2 * vt, G - 1), vq_hi = vkv * G + min(2 * vt + 1, G - 1);
+    float dacc[MTW][4];
 #pragma unroll
-    for (int x = 0; x < CPL; ++x) acc[x] = 0.f;
-    // running softmax state (warp g of a half <-> head g): max, deferred per-lane sums
+    for (int x = 0; x < MTW; ++x) dacc[x][0] = dacc[x][1] = dacc[x][2] = dacc[x][3] = 0.f;
     float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;
     int E_cur = -126;     // dense V accumulator units: 2^E_cur (uniform in a half)
     unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
@@ -639,31 +638,42 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 
             // -------------------------------------------------------- a5: P.V dense
             {
-                const float b = H.beta_s[vh];
-                if (b != 1.f) {
+                const float b_lo = H.beta_s[vq_lo], b_hi = H.beta_s[vq_hi];
+                if (b_lo != 1.f || b_hi != 1.f) {
 #pragma unroll
-                    for (int x = 0; x < CPL; ++x) acc[x] *= b;
+                    for (int x = 0; x < MTW; ++x) {
+                        dacc[x][0] *= b_lo; dacc[x][1] *= b_hi;
+                        dacc[x][2] *= b_lo; dacc[x][3] *= b_hi;
+                    }
+                }
+                uint32_t vr[NWV + 1];
+#pragma unroll
+                for (int x = 0; x < NWV; ++x) vr[x] = vw_s[(vkv * 4 * BITS + vw0 + x) * 32 + lane];
+                vr[NWV] = 0u;
+                if (BITS == 3 && MTW == 1 && voff) { vr[0] = __funnelshift_r(vr[0], vr[1], 16); vr[1] >>= 16; }
+                // B fragments (weights of query head vkv*G + g for tokens 16s + 2t.. / +8..)
+                uint32_t bw[2][2];
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    const uint32_t *w32 = reinterpret_cast<const uint32_t *>(H.w16 + (vkv * G + (vg < G ? vg : 0)) * 32 + 16 * s2 + 2 * vt);
+                    bw[s2][0] = vg < G ? w32[0] : 0u;
+                    bw[s2][1] = vg < G ? w32[4] : 0u;
                 }
 #pragma unroll
-                for (int v = 0; v < VT; ++v) {
-                    const int tg = (hw % WPH) * VT + v;
-                    if (tg < TG) {
-                        const int vj = tg * TPW + lane / LH;
-                        const uint16_t w = H.w16[vh * 32 + vj];
-                        uint32_t vw[VWL];
-                        const uint32_t *src = vw_s + (vkv * 32 + vj) * (4 * BITS) + vq * VWL;
+                for (int ml = 0; ml < MTW; ++ml) {
 #pragma unroll
-                        for (int x = 0; x < VWL; ++x) vw[x] = src[x];
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        uint32_t a[4];
 #pragma unroll
-                        for (int pp = 0; pp < CPL / 2; ++pp) {
-                            const int bit = 2 * BITS * pp;
+                        for (int r = 0; r < 4; ++r) {
+                            const int bit = ((ml * 2 + s2) * 4 + r) * FB;
                             const int wi = bit >> 5, sh = bit & 31;
                             uint32_t pc;
-                            if (sh + 2 * BITS <= 32) pc = (vw[wi] >> sh) & (NE - 1);
-                            else pc = (uint32_t)((((unsigned long long)vw[wi + 1] << 32) | vw[wi]) >> sh) & (NE - 1);
-                            const uint32_t cv = vlut[pc * 32 + lane];
-                            fma_w_f16x2(w, cv, acc[2 * pp], acc[2 * pp + 1]);
+                            if (sh + FB <= 32) pc = (vr[wi] >> sh) & (NE - 1);
+                            else pc = __funnelshift_r(vr[wi], vr[wi + 1], sh) & (NE - 1);
+                            a[r] = vlut[pc * 32 + lane];
                         }
+                        mma_f16_f32(dacc[ml], a, bw[s2]);
                     }
                 }
             }
@@ -672,10 +682,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 auto v_item = [&](uint32_t itm) {
                     const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
                     const int kvl = chl >> 7, cc = chl & 127;
-                    const int bit = BITS * cc;
-                    const uint32_t *vrow = vw_s + (kvl * 32 + j) * (4 * BITS);
-                    unsigned long long w64 = vrow[bit >> 5];
-                    if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vrow[(bit >> 5) + 1] << 32;
+                    const int bit = vf_bit(j, cc, BITS);
+                    const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
+                    unsigned long long w64 = vwp[0];
+                    if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vwp[32] << 32;
                     const int code = (int)((w64 >> (bit & 31)) & CM);
                     const float2 sz = vsz_s[j];
                     const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
@@ -714,11 +724,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             if (lane == 0) { H.m_fin[hw] = m_run; H.l_fin[hw] = l; H.z_fin[hw] = z; }
         }
         {
-            // dense P.V accumulators are in units of 2^-E_cur
+            // dense P.V accumulators (units of 2^-E_cur): row g / g+8 = channel, column = head
             const float sc = ldexpf(1.f, E_cur);
-            float *dst = H.osp + vh * kHeadDim + vq * CPL;
 #pragma unroll
-            for (int x = 0; x < CPL; ++x) atomicAdd(&dst[x], acc[x] * sc);
+            for (int ml = 0; ml < MTW; ++ml) {
+                const int ch = (mt0 + ml) * 16 + vg;
+                if (2 * vt < G) {
+                    float *o = H.osp + (vkv * G + 2 * vt) * kHeadDim + ch;
+                    o[0] += dacc[ml][0] * sc;
+                    o[8] += dacc[ml][2] * sc;
+                }
+                if (2 * vt + 1 < G) {
+                    float *o = H.osp + (vkv * G + 2 * vt + 1) * kHeadDim + ch;
+                    o[0] += dacc[ml][1] * sc;
+                    o[8] += dacc[ml][3] * sc;
+                }
+            }
         }
         if (P.timers && tid == 0) {
 #pragma unroll
@@ -866,7 +887,7 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
 }  // namespace
 
 int attend_heads_per_cta(int bits, int H_q, int G) {
-    const int cap = bits == 4 ? 1 : 4;   // V tasks: HG * 128/CPL <= 16 compute warps
+    const int cap = bits == 4 ? 1 : 4;   // K tables: HG * 64 * 4^b * 4 bytes of shared memory
     for (int hg = cap; hg >= 1; hg >>= 1)
         if (H_q % hg == 0 && hg % G == 0) return hg;
     return 0;

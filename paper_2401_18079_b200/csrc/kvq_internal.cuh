@@ -7,10 +7,12 @@
 //           code(h, p) | code(h, p+64) << b in 2b bits at bit offset 2b*p, RoPE partners
 //           adjacent) occupies words q = h*4b .. h*4b+4b-1, stored at [t][q][j] so a
 //           warp with lane = token reads 128 contiguous bytes per word slot.
-//   vcodes  u32 [ntiles][H_kv][32][4b] Value codes: for token n = 32t+j and KV head h, the
-//           head's 128 codes as the canonical little-endian bitstream (code c at bit b*c,
-//           4b words), stored at [t][h][j] so one head group's slice of a tile is one
-//           contiguous block (a single TMA bulk copy).
+//   vcodes  u32 [ntiles][H_kv][4b][32] Value codes of a (tile, KV head) in the order of the
+//           A operand of mma.m16n8k16 (rows = channels, k = tokens; see vf_lane/vf_bit):
+//           lane l of word w holds bits 32w..32w+31 of lane l's 128b-bit string, which is
+//           64 fields of 2b bits, field = (code of token 2u, code of token 2u+1) for one
+//           channel -- exactly one f16x2 A register after the pair-table lookup.  One head
+//           group's slice of a tile is one contiguous block (a single TMA bulk copy).
 //   vsz     float2 [cap]              per-token Value (s_n, z_n), fp32 (reading R6).
 //   vout    u32 [cap][kv]             Value outliers, exactly kv = ceil(f*D) per token
 //           (implicit CSR row pointer n*kv), ascending channel; record =
@@ -60,6 +62,20 @@ struct DevCache {
 };
 
 enum ErrBits { kErrKeyCapacity = 1 };
+
+// Value-code fragment layout.  Token j (0..31) of a tile, channel cc (0..127) of a head:
+// m-tile mt = cc/16, k-step s = j/16, and the mma.m16n8k16 A-fragment coordinates
+// (groupID g = cc%8, thread-in-group t = (j%8)/2, register a = 2*(j%16/8) + cc%16/8,
+// half = j%2) give lane 4g+t and field f = (2mt+s)*4 + a of that lane's string.
+__host__ __device__ inline int vf_lane(int j, int cc) { return (cc & 7) * 4 + ((j & 7) >> 1); }
+__host__ __device__ inline int vf_bit(int j, int cc, int bits) {
+    const int f = ((cc >> 4) * 2 + (j >> 4)) * 4 + ((j >> 3) & 1) * 2 + ((cc >> 3) & 1);
+    return f * 2 * bits + (j & 1) * bits;
+}
+// word (tile, KV head h, word w, lane l) of vcodes
+__host__ __device__ inline int64_t vf_word(int64_t tile, int H_kv, int h, int w, int lane, int bits) {
+    return ((tile * H_kv + h) * (4 * bits) + w) * 32 + lane;
+}
 
 // ---- quantization (kvq_quant.cu) ----
 cudaError_t launch_quantize(const DevCache &c, const __half *K, const __half *V, int64_t n0,

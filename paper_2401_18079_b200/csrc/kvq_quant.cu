@@ -390,15 +390,18 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         }
         c.kcodes[((int64_t)tile * c.QW + q) * 32 + jj] = (uint32_t)(acc >> off);
     }
-    for (int w = tid; w < c.VW; w += QZ_THREADS) {
-        const int bit0 = 32 * w;
-        const int c0 = bit0 / BITS, off = bit0 - c0 * BITS;
-        unsigned long long acc = 0;
-        for (int ch = c0, sh = 0; sh < 32 + off && ch < D; ++ch, sh += BITS)
-            acc |= (unsigned long long)vc[ch] << sh;
-        // tile layout: [tile][kv head][32 tokens][4b words] (kvq_internal.cuh)
-        const int hh = w / (4 * BITS), wi = w % (4 * BITS);
-        c.vcodes[(((int64_t)tile * c.H_kv + hh) * 32 + jj) * (4 * BITS) + wi] = (uint32_t)(acc >> off);
+    // Value codes into the fragment layout (kvq_internal.cuh): the two channels 16mt+g and
+    // 16mt+g+8 of a head share a lane and sit 2b bits apart, so one OR per pair of codes.
+    // Words are shared with the tile's other tokens (zeroed at create/reset).
+    for (int x = tid; x < c.H_kv * 64; x += QZ_THREADS) {
+        const int hh = x >> 6, mt = (x >> 3) & 7, g = x & 7;
+        const int cc = mt * 16 + g;
+        const int bit = vf_bit(jj, cc, BITS);
+        const uint32_t v = (uint32_t)vc[hh * kHeadDim + cc] | ((uint32_t)vc[hh * kHeadDim + cc + 8] << (2 * BITS));
+        const int lane = vf_lane(jj, cc), w = bit >> 5, off = bit & 31;
+        uint32_t *dst = c.vcodes + vf_word(tile, c.H_kv, hh, w, lane, BITS);
+        atomicOr(dst, v << off);
+        if (off + 3 * BITS > 32) atomicOr(dst + 32, v >> (32 - off));
     }
 }
 
