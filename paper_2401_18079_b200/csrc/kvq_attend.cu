@@ -138,8 +138,8 @@ struct Cfg {
     static constexpr size_t t1 = (size_t)kPairs * 32 * 8;
     // per compute half: red, p, kcorr, hcorr, kbeg/kend, w16, osp, anchors, scalars
     static constexpr size_t half_bytes =
-        HW * HG * 32 * 4 + HG * 32 * 4 * 3 + 64 * 4 + HG * 32 * 2 + HG * kHeadDim * 4
-        + 64 * 16 + 64 * 8 + HG * 4 * 4 + 64;
+        HW * HG * 32 * 4 + HG * 32 * 4 * 3 + HG * 64 * 4 + HG * 32 * 2 + HG * kHeadDim * 4 * 2
+        + 64 * 16 + 64 * 8 + HG * 4 * 4 + 16 + 64;
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
         + NHALF * half_bytes
@@ -165,7 +165,7 @@ struct Params {
     // stage ring layout (bytes), computed on the host
     int stages;
     int krec_cap;        // u32 records per stage buffer (multiple of 4)
-    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit, so_hdr, so_kcon;
+    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit, so_hdr, so_kcon, so_vdel;
     unsigned long long *timers;   // optional [8] phase cycle sums (diagnostics), may be null
 };
 
@@ -188,7 +188,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // per compute half h (alternate tiles): scratch of its own tile, at sp + h*half_bytes
     struct Half {
         float *red, *p_s, *kcorr, *hcorr, *osp, *beta_s, *m_fin, *l_fin, *z_fin;
-        int *kbeg, *kend;
+        int *kbeg, *kend;       // [HKV][32] Key-item segment of (local KV head, token)
+        int *vfix;              // [HG][128] Value-outlier sums of the tile, fixed point
+        int *vmax;              // [0] max |delta| of the tile's Value items (float bits)
+        float *vscale;          // [0] fixed-point scale of the tile's V items
+        float *vdel;            // [vcap_g] delta of each Value item of the tile
         uint16_t *w16;
         double2 *anc64;
         float2 *anc32;
@@ -202,10 +206,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         H.p_s = reinterpret_cast<float *>(q); q += HG * 32 * 4;
         H.kcorr = reinterpret_cast<float *>(q); q += HG * 32 * 4;   // overflow fallback only
         H.hcorr = reinterpret_cast<float *>(q); q += HG * 32 * 4;
-        H.kbeg = reinterpret_cast<int *>(q); q += 32 * 4;
-        H.kend = reinterpret_cast<int *>(q); q += 32 * 4;
+        H.kbeg = reinterpret_cast<int *>(q); q += HG * 32 * 4;
+        H.kend = reinterpret_cast<int *>(q); q += HG * 32 * 4;
         H.w16 = reinterpret_cast<uint16_t *>(q); q += HG * 32 * 2;
         H.osp = reinterpret_cast<float *>(q); q += HG * kHeadDim * 4;
+        H.vfix = reinterpret_cast<int *>(q); q += HG * kHeadDim * 4;
         q += (16 - ((HG * 32 * 2) % 16)) % 16;
         H.anc64 = reinterpret_cast<double2 *>(q); q += 64 * 16;
         H.anc32 = reinterpret_cast<float2 *>(q); q += 64 * 8;
@@ -213,7 +218,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         H.m_fin = reinterpret_cast<float *>(q); q += HG * 4;
         H.l_fin = reinterpret_cast<float *>(q); q += HG * 4;
         H.z_fin = reinterpret_cast<float *>(q); q += HG * 4;
+        H.vmax = reinterpret_cast<int *>(q); q += 4;
+        H.vscale = reinterpret_cast<float *>(q); q += 4;
         H.kcon = reinterpret_cast<float *>(smem_raw + P.so_kcon) + h * c.kcap_g * G;
+        H.vdel = reinterpret_cast<float *>(smem_raw + P.so_vdel) + h * c.vcap_g;
         return H;
     };
     sp += NHALF * C::half_bytes;
@@ -234,6 +242,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
     uint64_t *full_b = bars;
 
+    const long long t_kernel0 = clock64();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
     const int hg = blockIdx.x % n_hg;
@@ -282,14 +291,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         sincos((double)j * th, &s, &co);
         t1tab[x] = make_float2((float)co, (float)s);
     }
-    for (int x = tid; x < NHALF * HG * kHeadDim; x += ATT_THREADS) half_at(x / (HG * kHeadDim)).osp[x % (HG * kHeadDim)] = 0.f;
+    for (int x = tid; x < NHALF * HG * kHeadDim; x += ATT_THREADS) {
+        const Half Hx = half_at(x / (HG * kHeadDim));
+        Hx.osp[x % (HG * kHeadDim)] = 0.f;
+        Hx.vfix[x % (HG * kHeadDim)] = 0;
+    }
+    if (tid < NHALF) { half_at(tid).vmax[0] = 0; half_at(tid).vscale[0] = 1.f; }
     for (int x = tid; x < HKV * kHeadDim; x += ATT_THREADS) {
         ks_s[x] = ks[c_lo + x];
         kz_s[x] = kz[c_lo + x];
     }
     if (tid < 64) cb_s[tid] = c.cb[tid];
     for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) half_at(x / (HG * 32)).kcorr[x % (HG * 32)] = 0.f;
-    if (tid < NHALF * 32) { half_at(tid >> 5).kbeg[tid & 31] = 0; half_at(tid >> 5).kend[tid & 31] = 0; }
+    for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) {
+        half_at(x / (HG * 32)).kbeg[x % (HG * 32)] = 0;
+        half_at(x / (HG * 32)).kend[x % (HG * 32)] = 0;
+    }
     if (tid < 16) flag_s[tid] = 0;
     __syncthreads();
     // a1: q~ = RoPE(q, pos) * log2(e)/sqrt(d)
@@ -462,6 +479,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
         const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
         long long tc0 = clock64(), tc1;
+        tm[0] = tc0 - t_kernel0;   // prologue
 
         const int SH = P.stages / NHALF;
         if (hw == HW - 1)
@@ -508,17 +526,30 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             // ------------------------------------------ a3: K outliers, heavy pairs
             {
                 const int nk = hdr[0];
-                // items are in (token, channel) order: contributions go to kcon[item][gg],
-                // token boundaries to kbeg/kend; the softmax lane (g, j) gathers them
+                // items are in (token, channel) order, so each (token, local KV head) is one
+                // segment: contributions go to kcon[item][gg], segment bounds to kbeg/kend;
+                // the softmax lane (g, j) gathers its segment
+                auto seg = [](uint32_t it) { return (int)((it >> 11) & 31u) * 16 + (int)((it & 0x7ffu) >> 7); };
                 for (int x = htid; x < nk; x += HT) {
                     const uint32_t itm = kit[x];
                     int j = 0, g = 0;
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) H.kcon[x * G + gg] = k_corr(itm, gg, j, g);
-                    const int jp = x > 0 ? (int)((kit[x - 1] >> 11) & 31u) : -1;
-                    const int jn = x + 1 < nk ? (int)((kit[x + 1] >> 11) & 31u) : 32;
-                    if (jp != j) H.kbeg[j] = x;
-                    if (jn != j) H.kend[j] = x + 1;
+                    const int sg = seg(itm);
+                    const int sp = x > 0 ? seg(kit[x - 1]) : -1;
+                    const int sn = x + 1 < nk ? seg(kit[x + 1]) : -1;
+                    const int kvl = (int)((itm & 0x7ffu) >> 7);
+                    if (sp != sg) H.kbeg[kvl * 32 + j] = x;
+                    if (sn != sg) H.kend[kvl * 32 + j] = x + 1;
+                }
+                // Value-outlier sums of this half's previous tile (fixed point) -> osp
+                {
+                    const float inv = 1.f / H.vscale[0];
+                    for (int x = htid; x < HG * kHeadDim; x += HT) {
+                        const int v = H.vfix[x];
+                        if (v) { H.osp[x] += (float)v * inv; H.vfix[x] = 0; }
+                    }
+                    if (htid == 0) H.vmax[0] = 0;
                 }
                 if (hdr[2]) {
                     // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
@@ -610,10 +641,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     H.kcorr[g * 32 + j] = 0.f;
                     {
                         // gather this (head, token)'s Key-outlier corrections
-                        const int xb = H.kbeg[j], xe = H.kend[j];
-                        const int gkv = g / G;
-                        for (int x = xb; x < xe; ++x)
-                            if ((int)((kit[x] & 0x7ffu) >> 7) == gkv) s += H.kcon[x * G + (g % G)];
+                        const int kvl = g / G;
+                        const int xb = H.kbeg[kvl * 32 + j], xe = H.kend[kvl * 32 + j];
+                        for (int x = xb; x < xe; ++x) s += H.kcon[x * G + (g % G)];
                     }
                     s = valid ? s : -CUDART_INF_F;
                     const float m_new = fmaxf(m_run, warp_max_redux(s));
@@ -630,6 +660,28 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                         for (int x = 0; x < kHeadDim / 32; ++x) H.osp[g * kHeadDim + x * 32 + lane] *= alpha;
                     }
                     if (lane == 0) H.beta_s[g] = alpha * ldexpf(1.f, E_cur - E_new);
+                } else {
+                    // meanwhile the other warps compute the Value-outlier deltas
+                    // x - (Chat_V[code] s_n + z_n) of the tile's items and their max |delta|
+                    const int nvi = hdr[1];
+                    float mx = 0.f;
+                    for (int x = htid - HG * 32; x < nvi; x += HT - HG * 32) {
+                        const uint32_t itm = vit[x];
+                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                        const int kvl = chl >> 7, cc = chl & 127;
+                        const int bit = vf_bit(j, cc, BITS);
+                        const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
+                        unsigned long long w64 = vwp[0];
+                        if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vwp[32] << 32;
+                        const int code = (int)((w64 >> (bit & 31)) & CM);
+                        const float2 sz = vsz_s[j];
+                        const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+                        const float delta = xval - (cbVs[code] * sz.x + sz.y);
+                        H.vdel[x] = delta;
+                        mx = fmaxf(mx, fabsf(delta));
+                    }
+                    mx = warp_max_redux(mx);
+                    if (lane == 0 && mx > 0.f) atomicMax(H.vmax, __float_as_int(mx));
                 }
                 E_cur = E_new;
             }
@@ -697,7 +749,24 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     }
                 };
                 const int nvi = hdr[1];
-                for (int x = htid; x < nvi; x += HT) v_item(vit[x]);
+                if (nvi) {
+                    // sum_n p_n delta_{n,c} in fixed point: |p delta| 2^(24-e) < 2^25 with
+                    // 2^e <= max|delta| < 2^(e+1); <= 32 items per (head, channel) and tile
+                    const float mx = __int_as_float(H.vmax[0]);
+                    const float S = mx > 0.f ? ldexpf(1.f, 24 - ilogbf(mx)) : 1.f;
+                    if (htid == 0) H.vscale[0] = S;
+                    for (int x = htid; x < nvi; x += HT) {
+                        const uint32_t itm = vit[x];
+                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                        const int kvl = chl >> 7, cc = chl & 127;
+                        const float dS = H.vdel[x] * S;
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) {
+                            const int g = kvl * G + gg;
+                            atomicAdd(&H.vfix[g * kHeadDim + cc], __float2int_rn(H.p_s[g * 32 + j] * dS));
+                        }
+                    }
+                }
                 if (hdr[3]) {
                     // overflowed bucket: this tile's Value outliers from the CSR rows (rare)
                     for (int r = htid; r < ntok * kv; r += HT) {
@@ -715,10 +784,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 H.anc64[htid] = b;
                 H.anc32[htid] = make_float2((float)b.x, (float)b.y);
             }
-            if (htid < 32) { H.kbeg[htid] = 0; H.kend[htid] = 0; }
+            for (int x = htid; x < HKV * 32; x += HT) { H.kbeg[x] = 0; H.kend[x] = 0; }
             half_sync(half);
             tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
         }
+        {
+            const float inv = 1.f / H.vscale[0];
+            for (int x = htid; x < HG * kHeadDim; x += HT) {
+                const int v = H.vfix[x];
+                if (v) H.osp[x] += (float)v * inv;
+            }
+        }
+        half_sync(half);   // osp entries are updated by other threads below
         if (hw < HG) {
             const float l = warp_sum(l_lane), z = warp_sum(z_lane);
             if (lane == 0) { H.m_fin[hw] = m_run; H.l_fin[hw] = l; H.z_fin[hw] = z; }
@@ -838,8 +915,10 @@ size_t layout(const DevCache &c, Params &P) {
     const size_t stb = off;
     // per-item Key-outlier contributions (one tile at a time), then the stage ring
     const size_t kcon = align128((size_t)NHALF * c.kcap_g * c.G * 4);
+    const size_t vdel = align128((size_t)NHALF * c.vcap_g * 4);
     P.so_kcon = (unsigned)align128(C::fixed);
-    const size_t base = align128(P.so_kcon + kcon + 128);
+    P.so_vdel = (unsigned)(P.so_kcon + kcon);
+    const size_t base = align128(P.so_vdel + vdel + 128);
     P.st_base = (unsigned)base;
     const size_t limit = 227 * 1024;
     for (int stages = 4; stages >= 2; stages -= 2) {

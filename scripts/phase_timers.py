@@ -37,9 +37,9 @@ e1.record()
 torch.cuda.synchronize()
 tm = c.phase_timers()
 tiles = tm[5]
-names = ["issue", "tma_wait", "K_phase", "softmax", "V_phase"]
+names = ["prologue", "tma_wait", "K_phase", "softmax", "V_phase"]
+ctas = info_splits = c.info()["splits"] * (w.H_q // c.info()["heads_per_cta"])
 print(f"{wname} T={T} attend {e0.elapsed_time(e1) / 5 * 1e3:.1f} us, info {c.info()}")
 print("compute cycles per tile per CTA:", {n: round(tm[i] / tiles, 1) for i, n in enumerate(names)},
       "total", round(sum(tm[1:5]) / tiles, 1))
-print("producer K (wait/compact/issue):", [round(tm[i] / tiles, 1) for i in (6, 7, 8)],
-      " producer V (wait/compact/-):", [round(tm[i] / tiles, 1) for i in (9, 10, 11)])
+print(f"prologue cycles per CTA: {tm[0] / (5 * ctas):.0f}  loop cycles per CTA: {sum(tm[1:5]) / (5 * ctas):.0f}")
