@@ -117,6 +117,20 @@ __device__ __forceinline__ float warp_sum(float v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+// 2^k as a float for k in [-126, 127] (clamped); exact, no libm call
+__device__ __forceinline__ float pow2i(int k) {
+    k = max(-126, min(127, k));
+    return __int_as_float((k + 127) << 23);
+}
+// floor(log2(x)) of a positive normal float (x = 0 or subnormal gives -127)
+__device__ __forceinline__ int ilog2f(float x) { return ((__float_as_int(x) >> 23) & 255) - 127; }
+// 32-bit shared-window load
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 // warp max of floats with one REDUX via an order-preserving integer map
 __device__ __forceinline__ float warp_max_redux(float v) {
     unsigned u = __float_as_uint(v);
@@ -462,6 +476,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float dacc[MTW][4];
 #pragma unroll
     for (int x = 0; x < MTW; ++x) dacc[x][0] = dacc[x][1] = dacc[x][2] = dacc[x][3] = 0.f;
+    // lookup address = vlut + ((code << 7) | (lane << 2)): the OR is exact, the base add
+    // folds into the load (uniform base register)
+    const uint32_t vlut_base = smem_u32(vlut), vlane4 = 4u * lane;
     float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;
     int E_cur = -126;     // dense V accumulator units: 2^E_cur (uniform in a half)
     unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
@@ -475,6 +492,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             t1c[k] = v.x;
             t1s[k] = v.y;
         }
+        // this warp's K tables: base | (pair code << 2), + a constant per (head, pair); the
+        // base is a multiple of NE*4 bytes (dynamic shared memory is 1 KB aligned)
+        const uint32_t klut_w = smem_u32(klut) + (uint32_t)(hw * KPW * NE * 4);
+        if (klut_w & (NE * 4u - 1u)) __trap();
         const int kbit0 = 2 * BITS * KPW * hw;
         const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
         const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
@@ -484,11 +505,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const int SH = P.stages / NHALF;
         if (hw == HW - 1)
             for (int k = 0; k < SH - 1; ++k) issue(half, k);
-        for (int t = t_begin + half; t < t_end; t += NHALF) {
-            const int kk = (t - t_begin) / NHALF;       // this half's k-th tile
-            const int st = half * SH + (kk % SH);
+        int kk = 0, slot = 0, nv_prev = 0;
+        unsigned par = 0;
+        for (int t = t_begin + half; t < t_end; t += NHALF, ++kk) {
+            const int st = half * SH + slot;
             if (hw == HW - 1) issue(half, kk + SH - 1);
-            mbar_wait(full_b + st, (unsigned)((kk / SH) & 1));
+            mbar_wait(full_b + st, par);
+            if (++slot == SH) { slot = 0; par ^= 1u; }
             tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
             unsigned char *sb = stage_ptr(st);
             const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
@@ -543,14 +566,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     if (sn != sg) H.kend[kvl * 32 + j] = x + 1;
                 }
                 // Value-outlier sums of this half's previous tile (fixed point) -> osp
-                {
-                    const float inv = 1.f / H.vscale[0];
+                if (nv_prev) {
+                    const float inv = H.vscale[0];
                     for (int x = htid; x < HG * kHeadDim; x += HT) {
                         const int v = H.vfix[x];
                         if (v) { H.osp[x] += (float)v * inv; H.vfix[x] = 0; }
                     }
-                    if (htid == 0) H.vmax[0] = 0;
                 }
+                if (htid == 0) H.vmax[0] = 0;
+                nv_prev = hdr[1] | hdr[3];
                 if (hdr[2]) {
                     // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
                     for (int j = 0; j < ntok; ++j) {
@@ -593,13 +617,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 float acc_c[HG], acc_s[HG];
 #pragma unroll
                 for (int g = 0; g < HG; ++g) { acc_c[g] = 0.f; acc_s[g] = 0.f; }
-                unsigned long long win[HKV];
+                uint32_t wl[HKV], wh[HKV];
 #pragma unroll
                 for (int h = 0; h < HKV; ++h) {
                     unsigned long long w64 = kw_s[(h * 4 * BITS + kq0) * 32 + lane];
                     if (kshift + 2 * BITS * KPW > 32)
                         w64 |= (unsigned long long)kw_s[(h * 4 * BITS + kq0 + 1) * 32 + lane] << 32;
-                    win[h] = w64 >> kshift;
+                    w64 >>= kshift;
+                    wl[h] = (uint32_t)w64;
+                    wh[h] = (uint32_t)(w64 >> 32);
                 }
 #pragma unroll
                 for (int k = 0; k < KPW; ++k) {
@@ -608,13 +634,19 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     const float cc = an.x * t1c[k] - an.y * t1s[k];
                     const float ss = an.x * t1s[k] + an.y * t1c[k];
                     const uint32_t cs = pack_half2(cc, ss);
+                    const int b = 2 * BITS * k - 2;   // bit of (pair code << 2) in the window
 #pragma unroll
                     for (int h = 0; h < HKV; ++h) {
-                        const int pc = (int)((win[h] >> (2 * BITS * k)) & (NE - 1));
+                        uint32_t off;
+                        if (b < 0) off = wl[h] << 2;
+                        else if (b + 2 * BITS + 2 <= 32) off = wl[h] >> b;
+                        else if (b >= 32) off = wh[h] >> (b - 32);
+                        else off = __funnelshift_r(wl[h], wh[h], b);
+                        const uint32_t a = klut_w | (off & ((NE - 1) << 2));
 #pragma unroll
                         for (int gg = 0; gg < G; ++gg) {
                             const int g = h * G + gg;
-                            const uint32_t ab = klut[(g * 64 + i) * NE + pc];
+                            const uint32_t ab = lds_u32(a + (uint32_t)((g * 64 + k) * NE * 4));
                             fma2_f16_f32(ab, cs, acc_c[g], acc_s[g]);
                         }
                     }
@@ -630,7 +662,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 float smax = lane < ntok ? vsz_s[lane].x : 0.f;
                 smax = warp_max_redux(smax);
                 int E_new = E_cur;
-                if (smax > 0.f) E_new = max(E_cur, ilogbf(smax) + 1);
+                if (smax > 0.f) E_new = max(E_cur, ilog2f(smax) + 1);
+                const float pe = pow2i(-E_new);
                 if (hw < HG) {
                     const int g = hw, j = lane;
                     const bool valid = j < ntok;
@@ -654,12 +687,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     z_lane = z_lane * alpha + p * sz.y;
                     m_run = m_new;
                     H.p_s[g * 32 + j] = p;
-                    H.w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * ldexpf(sz.x, -E_new)));
+                    H.w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * (sz.x * pe)));
                     if (alpha != 1.f) {
 #pragma unroll
                         for (int x = 0; x < kHeadDim / 32; ++x) H.osp[g * kHeadDim + x * 32 + lane] *= alpha;
                     }
-                    if (lane == 0) H.beta_s[g] = alpha * ldexpf(1.f, E_cur - E_new);
+                    if (lane == 0) H.beta_s[g] = alpha * pow2i(E_cur - E_new);
                 } else {
                     // meanwhile the other warps compute the Value-outlier deltas
                     // x - (Chat_V[code] s_n + z_n) of the tile's items and their max |delta|
@@ -720,10 +753,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                         for (int r = 0; r < 4; ++r) {
                             const int bit = ((ml * 2 + s2) * 4 + r) * FB;
                             const int wi = bit >> 5, sh = bit & 31;
-                            uint32_t pc;
-                            if (sh + FB <= 32) pc = (vr[wi] >> sh) & (NE - 1);
-                            else pc = __funnelshift_r(vr[wi], vr[wi + 1], sh) & (NE - 1);
-                            a[r] = vlut[pc * 32 + lane];
+                            // (field & (NE-1)) << 7 with one shift (funnel when it straddles)
+                            uint32_t off;
+                            if (sh + FB <= 32) off = sh >= 7 ? (vr[wi] >> (sh - 7)) : (vr[wi] << (7 - sh));
+                            else off = __funnelshift_r(vr[wi], vr[wi + 1], sh - 7);
+                            a[r] = lds_u32(vlut_base + (vlane4 | (off & ((NE - 1) << 7))));
                         }
                         mma_f16_f32(dacc[ml], a, bw[s2]);
                     }
@@ -753,8 +787,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     // sum_n p_n delta_{n,c} in fixed point: |p delta| 2^(24-e) < 2^25 with
                     // 2^e <= max|delta| < 2^(e+1); <= 32 items per (head, channel) and tile
                     const float mx = __int_as_float(H.vmax[0]);
-                    const float S = mx > 0.f ? ldexpf(1.f, 24 - ilogbf(mx)) : 1.f;
-                    if (htid == 0) H.vscale[0] = S;
+                    const int emx = mx > 0.f ? ilog2f(mx) : 0;
+                    const float S = pow2i(24 - emx);
+                    if (htid == 0) H.vscale[0] = pow2i(emx - 24);   // 1/S
                     for (int x = htid; x < nvi; x += HT) {
                         const uint32_t itm = vit[x];
                         const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
@@ -788,8 +823,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             half_sync(half);
             tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
         }
-        {
-            const float inv = 1.f / H.vscale[0];
+        if (nv_prev) {
+            const float inv = H.vscale[0];
             for (int x = htid; x < HG * kHeadDim; x += HT) {
                 const int v = H.vfix[x];
                 if (v) H.osp[x] += (float)v * inv;
@@ -802,7 +837,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         }
         {
             // dense P.V accumulators (units of 2^-E_cur): row g / g+8 = channel, column = head
-            const float sc = ldexpf(1.f, E_cur);
+            const float sc = pow2i(E_cur);
 #pragma unroll
             for (int ml = 0; ml < MTW; ++ml) {
                 const int ch = (mt0 + ml) * 16 + vg;
