@@ -117,6 +117,17 @@ __device__ __forceinline__ float warp_sum(float v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Score terms summed with shared integer atomics (no native float atomics in shared memory):
+// fixed point with 2^-16 resolution in log2-score units, |term| clamped to 2^15.
+constexpr float kKfixScale = 65536.f;
+__device__ __forceinline__ int kfix_of(float v) {
+    return __float2int_rn(fminf(fmaxf(v, -32768.f), 32767.f) * kKfixScale);
+}
 // 2^k as a float for k in [-126, 127] (clamped); exact, no libm call
 __device__ __forceinline__ float pow2i(int k) {
     k = max(-126, min(127, k));
@@ -161,7 +172,7 @@ struct Cfg {
         + 64 * 4                       /* theta32 */
         + HG * 4 * 8                   /* per-head scalars */
         + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
-        + HG * 16 * 4                  /* heavy pair list + counts */
+        + HG * 24 * 4                  /* heavy pair list, counts, flat list */
         + HG * kHeadDim * 4 * 2 + 64 * 4 /* staged s_c, z_c of the group, codebooks */
         + 256;
     static constexpr size_t fixed = klut + vlut + hlut + t1 + small;
@@ -179,7 +190,7 @@ struct Params {
     // stage ring layout (bytes), computed on the host
     int stages;
     int krec_cap;        // u32 records per stage buffer (multiple of 4)
-    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit, so_hdr, so_kcon, so_vdel;
+    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit, so_hdr, so_vdel;
     unsigned long long *timers;   // optional [8] phase cycle sums (diagnostics), may be null
 };
 
@@ -201,8 +212,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     // per compute half h (alternate tiles): scratch of its own tile, at sp + h*half_bytes
     struct Half {
-        float *red, *p_s, *kcorr, *hcorr, *osp, *beta_s, *m_fin, *l_fin, *z_fin;
-        int *kbeg, *kend;       // [HKV][32] Key-item segment of (local KV head, token)
+        float *red, *p_s, *osp, *beta_s, *m_fin, *l_fin, *z_fin;
+        int *kfix;              // [HG][32] Key-outlier + heavy-pair score terms, fixed point
         int *vfix;              // [HG][128] Value-outlier sums of the tile, fixed point
         int *vmax;              // [0] max |delta| of the tile's Value items (float bits)
         float *vscale;          // [0] fixed-point scale of the tile's V items
@@ -210,7 +221,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         uint16_t *w16;
         double2 *anc64;
         float2 *anc32;
-        float *kcon;
     };
     unsigned char *const half_base = sp;
     auto half_at = [&](int h) -> Half {
@@ -218,10 +228,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         unsigned char *q = half_base + h * C::half_bytes;
         H.red = reinterpret_cast<float *>(q); q += HW * HG * 32 * 4;
         H.p_s = reinterpret_cast<float *>(q); q += HG * 32 * 4;
-        H.kcorr = reinterpret_cast<float *>(q); q += HG * 32 * 4;   // overflow fallback only
-        H.hcorr = reinterpret_cast<float *>(q); q += HG * 32 * 4;
-        H.kbeg = reinterpret_cast<int *>(q); q += HG * 32 * 4;
-        H.kend = reinterpret_cast<int *>(q); q += HG * 32 * 4;
+        H.kfix = reinterpret_cast<int *>(q); q += HG * 32 * 4;
+        q += HG * 32 * 4;
+        q += HG * 64 * 4;
         H.w16 = reinterpret_cast<uint16_t *>(q); q += HG * 32 * 2;
         H.osp = reinterpret_cast<float *>(q); q += HG * kHeadDim * 4;
         H.vfix = reinterpret_cast<int *>(q); q += HG * kHeadDim * 4;
@@ -234,7 +243,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         H.z_fin = reinterpret_cast<float *>(q); q += HG * 4;
         H.vmax = reinterpret_cast<int *>(q); q += 4;
         H.vscale = reinterpret_cast<float *>(q); q += 4;
-        H.kcon = reinterpret_cast<float *>(smem_raw + P.so_kcon) + h * c.kcap_g * G;
         H.vdel = reinterpret_cast<float *>(smem_raw + P.so_vdel) + h * c.vcap_g;
         return H;
     };
@@ -248,6 +256,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     uint8_t *heavy_s = reinterpret_cast<uint8_t *>(sp); sp += HG * 64;
     int *hv_pair = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
     int *hv_n = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
+    int *hv_combo = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;   // flat (head, slot) list
     float *ks_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;   // s_c of the group
     float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
@@ -257,6 +266,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     uint64_t *full_b = bars;
 
     const long long t_kernel0 = clock64();
+    const unsigned long long ns_kernel0 = P.timers ? gtimer_ns() : 0ull;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
     const int hg = blockIdx.x % n_hg;
@@ -316,11 +326,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         kz_s[x] = kz[c_lo + x];
     }
     if (tid < 64) cb_s[tid] = c.cb[tid];
-    for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) half_at(x / (HG * 32)).kcorr[x % (HG * 32)] = 0.f;
-    for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) {
-        half_at(x / (HG * 32)).kbeg[x % (HG * 32)] = 0;
-        half_at(x / (HG * 32)).kend[x % (HG * 32)] = 0;
-    }
+    for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) half_at(x / (HG * 32)).kfix[x % (HG * 32)] = 0;
     if (tid < 16) flag_s[tid] = 0;
     __syncthreads();
     // a1: q~ = RoPE(q, pos) * log2(e)/sqrt(d)
@@ -374,6 +380,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         }
     }
     __syncthreads();
+    if (tid == 0) {   // flat (head, heavy slot) list for the K phase
+        int nc = 0;
+        for (int g = 0; g < HG; ++g)
+            for (int h = 0; h < hv_n[g]; ++h) hv_combo[nc++] = g * 8 + h;
+        flag_s[2] = nc;
+    }
     // K table entries: one (head, pair, second code) row of 2^b entries per work item
     for (int x = tid; x < HG * 64 * (CM + 1); x += ATT_THREADS) {
         const int bb = x % (CM + 1), gi = x / (CM + 1);
@@ -457,6 +469,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // softmax state and named barrier; they share the read-only tables and hide each
     // other's latency.  Their partials are merged at the end.
     const int half = warp / HW, hw = warp % HW, htid = tid % HT;
+    const int n_combo = flag_s[2];
     const Half H = half_at(half < NHALF ? half : 0);
     // V-phase task mapping inside a half (tensor cores, mma.m16n8k16): warp -> (local KV
     // head vkv, m-tiles [mt0, mt0 + MTW) of 16 channels); A = V codes (rows = channels,
@@ -549,21 +562,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             // ------------------------------------------ a3: K outliers, heavy pairs
             {
                 const int nk = hdr[0];
-                // items are in (token, channel) order, so each (token, local KV head) is one
-                // segment: contributions go to kcon[item][gg], segment bounds to kbeg/kend;
-                // the softmax lane (g, j) gathers its segment
-                auto seg = [](uint32_t it) { return (int)((it >> 11) & 31u) * 16 + (int)((it & 0x7ffu) >> 7); };
+                // Key-outlier corrections straight into the (head, token) score term, in fixed
+                // point (native shared integer atomics; see kfix_of)
                 for (int x = htid; x < nk; x += HT) {
                     const uint32_t itm = kit[x];
-                    int j = 0, g = 0;
 #pragma unroll
-                    for (int gg = 0; gg < G; ++gg) H.kcon[x * G + gg] = k_corr(itm, gg, j, g);
-                    const int sg = seg(itm);
-                    const int sp = x > 0 ? seg(kit[x - 1]) : -1;
-                    const int sn = x + 1 < nk ? seg(kit[x + 1]) : -1;
-                    const int kvl = (int)((itm & 0x7ffu) >> 7);
-                    if (sp != sg) H.kbeg[kvl * 32 + j] = x;
-                    if (sn != sg) H.kend[kvl * 32 + j] = x + 1;
+                    for (int gg = 0; gg < G; ++gg) {
+                        int j, g;
+                        const float v = k_corr(itm, gg, j, g);
+                        atomicAdd(&H.kfix[g * 32 + j], kfix_of(v));
+                    }
                 }
                 // Value-outlier sums of this half's previous tile (fixed point) -> osp
                 if (nv_prev) {
@@ -588,28 +596,25 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                             for (int gg = 0; gg < G; ++gg) {
                                 int jj, g;
                                 const float v = k_corr(itm, gg, jj, g);
-                                atomicAdd(&H.kcorr[g * 32 + jj], v);
+                                atomicAdd(&H.kfix[g * 32 + jj], kfix_of(v));
                             }
                         }
                     }
                 }
-                if (htid < HG * 32) {
-                    // heavy RoPE pairs of head g in fp32 (tables hlut), one thread per (g, j)
-                    const int g = htid >> 5, j = htid & 31;
-                    float hc = 0.f;
-                    const int nh = hv_n[g];
-                    for (int hsl = 0; hsl < nh; ++hsl) {
-                        const int i = hv_pair[g * 8 + hsl];
-                        const int bit = 2 * BITS * i;
-                        const int wq = (g / G) * 4 * BITS + (bit >> 5);
-                        unsigned long long w64 = kw_s[wq * 32 + j];
-                        if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                        const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                        const float2 ab = hlut[(g * HMAX + hsl) * NE + pc];
-                        const float2 an = anc32[i], tt = t1tab[i * 32 + j];
-                        hc += (an.x * tt.x - an.y * tt.y) * ab.x + (an.x * tt.y + an.y * tt.x) * ab.y;
-                    }
-                    H.hcorr[g * 32 + j] = hc;
+                // heavy RoPE pairs in fp32 (tables hlut): the (head, pair) list spread over the
+                // half's warps, lane = token
+                for (int cb = hw; cb < n_combo; cb += HW) {
+                    const int g = hv_combo[cb] >> 3, hsl = hv_combo[cb] & 7;
+                    const int i = hv_pair[g * 8 + hsl];
+                    const int bit = 2 * BITS * i;
+                    const int wq = (g / G) * 4 * BITS + (bit >> 5);
+                    unsigned long long w64 = kw_s[wq * 32 + lane];
+                    if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + lane] << 32;
+                    const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                    const float2 ab = hlut[(g * HMAX + hsl) * NE + pc];
+                    const float2 an = anc32[i], tt = t1tab[i * 32 + lane];
+                    const float hc = (an.x * tt.x - an.y * tt.y) * ab.x + (an.x * tt.y + an.y * tt.x) * ab.y;
+                    atomicAdd(&H.kfix[g * 32 + lane], kfix_of(hc));
                 }
             }
             // ------------------------------------------------------------ a2: K dense
@@ -670,14 +675,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     float s = 0.f;
 #pragma unroll
                     for (int w = 0; w < HW; ++w) s += H.red[(w * HG + g) * 32 + j];
-                    s = s * lut_inv[g] + H.kcorr[g * 32 + j] + H.hcorr[g * 32 + j];
-                    H.kcorr[g * 32 + j] = 0.f;
-                    {
-                        // gather this (head, token)'s Key-outlier corrections
-                        const int kvl = g / G;
-                        const int xb = H.kbeg[kvl * 32 + j], xe = H.kend[kvl * 32 + j];
-                        for (int x = xb; x < xe; ++x) s += H.kcon[x * G + (g % G)];
-                    }
+                    s = s * lut_inv[g] + (float)H.kfix[g * 32 + j] * (1.f / kKfixScale);
+                    H.kfix[g * 32 + j] = 0;
                     s = valid ? s : -CUDART_INF_F;
                     const float m_new = fmaxf(m_run, warp_max_redux(s));
                     const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
@@ -819,7 +818,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 H.anc64[htid] = b;
                 H.anc32[htid] = make_float2((float)b.x, (float)b.y);
             }
-            for (int x = htid; x < HKV * 32; x += HT) { H.kbeg[x] = 0; H.kend[x] = 0; }
             half_sync(half);
             tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
         }
@@ -857,6 +855,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
             for (int x = 0; x < 5; ++x) atomicAdd(P.timers + x, tm[x]);
             atomicAdd(P.timers + 5, (unsigned long long)ntl);
+            // wall-clock spread across CTAs: first start, last loop end, longest CTA loop
+            atomicMax(P.timers + 6, ~ns_kernel0);
+            const unsigned long long ns1 = gtimer_ns();
+            atomicMax(P.timers + 7, ns1);
+            atomicMax(P.timers + 8, ns1 - ns_kernel0);
         }
     }
     __syncthreads();
@@ -949,10 +952,8 @@ size_t layout(const DevCache &c, Params &P) {
     P.so_vit = (unsigned)off; off = align128(off + (size_t)c.vcap_g * 4);
     const size_t stb = off;
     // per-item Key-outlier contributions (one tile at a time), then the stage ring
-    const size_t kcon = align128((size_t)NHALF * c.kcap_g * c.G * 4);
     const size_t vdel = align128((size_t)NHALF * c.vcap_g * 4);
-    P.so_kcon = (unsigned)align128(C::fixed);
-    P.so_vdel = (unsigned)(P.so_kcon + kcon);
+    P.so_vdel = (unsigned)align128(C::fixed);
     const size_t base = align128(P.so_vdel + vdel + 128);
     P.st_base = (unsigned)base;
     const size_t limit = 227 * 1024;

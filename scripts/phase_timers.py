@@ -43,3 +43,10 @@ print(f"{wname} T={T} attend {e0.elapsed_time(e1) / 5 * 1e3:.1f} us, info {c.inf
 print("compute cycles per tile per CTA:", {n: round(tm[i] / tiles, 1) for i, n in enumerate(names)},
       "total", round(sum(tm[1:5]) / tiles, 1))
 print(f"prologue cycles per CTA: {tm[0] / (5 * ctas):.0f}  loop cycles per CTA: {sum(tm[1:5]) / (5 * ctas):.0f}")
+# one more launch alone for the wall-clock spread across CTAs
+c.attend(q, T, o)
+torch.cuda.synchronize()
+tm = c.phase_timers()
+first_start = (~tm[6]) & 0xFFFFFFFFFFFFFFFF
+print(f"last launch: first CTA start -> last CTA loop end {(tm[7] - first_start) / 1e3:.1f} us; "
+      f"longest CTA start->loop end {tm[8] / 1e3:.1f} us")
