@@ -1,21 +1,22 @@
 // kvq_attend.cu -- ATT: fused single-token decode attention over the compressed cache.
 //
 // One launch per attend.  grid = n_head_groups x splits (head group
-// fastest), one CTA per SM, warp specialized:
-//   warp 16 (producer)  TMA bulk copies (cp.async.bulk + mbarrier complete_tx) of every
-//                       32-token tile of the CTA's head group -- K code words, V code words,
-//                       per-token (s,z), CSC pointers, Value and Key outlier records -- into a
-//                       STAGES-deep shared-memory ring; then compacts the tile's Key-outlier
-//                       records of this head group into a self-contained item list.
-//   warp 17 (producer)  compacts the tile's Value-outlier records of this head group.
-//   warps 0..15         compute, synchronized among themselves with a named barrier:
-//     a2+a3  K phase: RoPE-pair table lookups (lane = token, warp = 4 RoPE pairs, all
-//            heads of the group; fp16 x fp16 -> fp32 FMAs), Key-outlier and heavy-pair
-//            corrections in fp32 (flat over the item list, shared atomics);
-//     a4     online softmax in base 2 (warp g = head g; per-lane deferred sums);
-//     a5+a6  P.V: lane = CPL channels, sum_n (p_n s_n) Chat_V[code] + sum_n p_n z_n
-//            (affine fold), Value-outlier corrections flat over the item list;
-//     a7     the last CTA of each head group merges the split partials (log-sum-exp).
+// fastest), one CTA per SM, each CTA a contiguous range of 32-token tiles of one group of
+// HG query heads.  Two warp groups form a pipeline over the tiles:
+//   K group (8 warps)   waits for the tile's TMA bulk copies (K/V code words, per-token (s,z),
+//                       outlier items of this head group; issued 2 tiles ahead by its last
+//                       warp), then computes the tile's scores: a2 RoPE-pair table lookups
+//                       (lane = token, warp = 8 RoPE pairs of every head; fp16 x fp16 -> fp32),
+//                       a3 Key-outlier and heavy-pair terms in fp32 summed in fixed point with
+//                       shared integer atomics.  Scores go to one of two buffers.
+//   SV group (8 warps)  a4 online softmax in base 2 (warp g = head g; the other warps
+//                       compute the tile's Value-outlier deltas meanwhile), then a5 P.V on the
+//                       tensor cores (mma.m16n8k16: A = Value codes through a pair table,
+//                       B = fp16 weights p s 2^-E) and a6 the Value-outlier terms.
+//   Named barriers hand the score buffers over (FULL: K -> SV, EMPTY: SV -> K) and an
+//   mbarrier per ring slot returns the stage to the TMA issuer, so neither group waits for
+//   the other except on a full/empty buffer.  a7: the last CTA of each head group merges the
+//   split partials (log-sum-exp, ticket counter).
 //   Tables (built per CTA, a1): q~ = RoPE(q, pos) with exact fp64 angles (R11, R12) times
 //   log2(e)/sqrt(d); per (query head g, RoPE pair i) a 2^{2b}-entry table of fp16 pairs
 //   (A, B), A = q~_i K^_i(a) + q~_i' K^_i'(b), B = q~_i' K^_i(a) - q~_i K^_i'(b) with
@@ -23,7 +24,7 @@
 //   and the affine folded in, so one lookup + 2 FMAs give cos(n' th_i) A + sin(n' th_i) B,
 //   exactly the pair's share of q~ . RoPE(K^_n, n') (RoPE after dequantization, P:379,
 //   P:730).  Pairs carrying a heavy Key channel use fp32 tables.  V: the
-//   shared codebook as a pair table, one private copy per lane (conflict free).
+//   shared codebook as a table of (Chat[a], Chat[b]) fp16 pairs, one copy per lane.
 #include "kvq_internal.cuh"
 
 #include <math_constants.h>
@@ -31,13 +32,17 @@
 namespace kvq {
 namespace {
 
-constexpr int NHALF = 2;                      // independent compute halves (alternate tiles)
-constexpr int HW = 8;                         // warps per half
-constexpr int HT = HW * 32;                   // threads per half
-constexpr int NCW = NHALF * HW;               // compute warps
-constexpr int NCT = NCW * 32;                 // compute threads
-constexpr int ATT_THREADS = NCT;              // 16 warps: 4 per SM sub-partition
-constexpr int KPW = kPairs / HW;              // RoPE pairs per warp in the K phase
+constexpr int KW = 8;                         // K-group warps (scores)
+constexpr int SW = 8;                         // SV-group warps (softmax, P.V)
+constexpr int KT = KW * 32, ST = SW * 32;
+constexpr int ATT_THREADS = KT + ST;          // 16 warps: 4 per SM sub-partition
+constexpr int KPW = kPairs / KW;              // RoPE pairs per warp in the K phase
+constexpr int PF = 2;                         // TMA prefetch distance (tiles)
+// named barrier ids (0 = __syncthreads)
+constexpr int BAR_FULL = 1;                   // + buffer: scores ready (K arrives, SV syncs)
+constexpr int BAR_EMPTY = 3;                  // + buffer: scores consumed (SV arrives, K syncs)
+constexpr int BAR_SV = 5;                     // SV group internal
+constexpr int BAR_K = 6;                      // K group internal
 
 // ------------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -77,9 +82,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-// named barrier among the warps of one compute half (ids 1, 2; the producer never joins)
-__device__ __forceinline__ void half_sync(int half) {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "n"(HT) : "memory");
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // acc += lo(x)*lo(y) ; acc2 += hi(x)*hi(y)   (fp16 products, fp32 accumulation)
@@ -161,20 +168,22 @@ struct Cfg {
     static constexpr size_t vlut = (size_t)NE * 32 * 4;
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
     static constexpr size_t t1 = (size_t)kPairs * 32 * 8;
-    // per compute half: red, p, kcorr, hcorr, kbeg/kend, w16, osp, anchors, scalars
-    static constexpr size_t half_bytes =
-        HW * HG * 32 * 4 + HG * 32 * 4 * 3 + HG * 64 * 4 + HG * 32 * 2 + HG * kHeadDim * 4 * 2
-        + 64 * 16 + 64 * 8 + HG * 4 * 4 + 16 + 64;
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
-        + NHALF * half_bytes
-        + 64 * 16 * 2                  /* rot64, qcis */
+        + 2 * KW * HG * 32 * 4         /* red[2] */
+        + 2 * HG * 32 * 4              /* kfix[2] */
+        + HG * 32 * 4 + HG * 32 * 2    /* p_s, w16 */
+        + 2 * HG * kHeadDim * 4        /* vfix[2] */
+        + HG * kHeadDim * 4            /* osp */
+        + 2 * 64 * 16 + 2 * 64 * 8     /* anc64[2], anc32[2] */
+        + HG * 4 * 8 + 64              /* beta, m/l/z, vmax[2], vinv[2] */
+        + 64 * 16 * 2                  /* rot32, qcis */
         + 64 * 4                       /* theta32 */
         + HG * 4 * 8                   /* per-head scalars */
         + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
         + HG * 24 * 4                  /* heavy pair list, counts, flat list */
         + HG * kHeadDim * 4 * 2 + 64 * 4 /* staged s_c, z_c of the group, codebooks */
-        + 256;
+        + 512;
     static constexpr size_t fixed = klut + vlut + hlut + t1 + small;
 };
 
@@ -189,9 +198,8 @@ struct Params {
     int write_partial;
     // stage ring layout (bytes), computed on the host
     int stages;
-    int krec_cap;        // u32 records per stage buffer (multiple of 4)
     unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit, so_hdr, so_vdel;
-    unsigned long long *timers;   // optional [8] phase cycle sums (diagnostics), may be null
+    unsigned long long *timers;   // optional [16] diagnostics, may be null
 };
 
 template <int BITS, int HG, int G>
@@ -209,46 +217,23 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
     float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
     float2 *t1tab = reinterpret_cast<float2 *>(sp); sp += C::t1;   // cis(j theta_i) [i][j]
-    float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
-    // per compute half h (alternate tiles): scratch of its own tile, at sp + h*half_bytes
-    struct Half {
-        float *red, *p_s, *osp, *beta_s, *m_fin, *l_fin, *z_fin;
-        int *kfix;              // [HG][32] Key-outlier + heavy-pair score terms, fixed point
-        int *vfix;              // [HG][128] Value-outlier sums of the tile, fixed point
-        int *vmax;              // [0] max |delta| of the tile's Value items (float bits)
-        float *vscale;          // [0] fixed-point scale of the tile's V items
-        float *vdel;            // [vcap_g] delta of each Value item of the tile
-        uint16_t *w16;
-        double2 *anc64;
-        float2 *anc32;
-    };
-    unsigned char *const half_base = sp;
-    auto half_at = [&](int h) -> Half {
-        Half H;
-        unsigned char *q = half_base + h * C::half_bytes;
-        H.red = reinterpret_cast<float *>(q); q += HW * HG * 32 * 4;
-        H.p_s = reinterpret_cast<float *>(q); q += HG * 32 * 4;
-        H.kfix = reinterpret_cast<int *>(q); q += HG * 32 * 4;
-        q += HG * 32 * 4;
-        q += HG * 64 * 4;
-        H.w16 = reinterpret_cast<uint16_t *>(q); q += HG * 32 * 2;
-        H.osp = reinterpret_cast<float *>(q); q += HG * kHeadDim * 4;
-        H.vfix = reinterpret_cast<int *>(q); q += HG * kHeadDim * 4;
-        q += (16 - ((HG * 32 * 2) % 16)) % 16;
-        H.anc64 = reinterpret_cast<double2 *>(q); q += 64 * 16;
-        H.anc32 = reinterpret_cast<float2 *>(q); q += 64 * 8;
-        H.beta_s = reinterpret_cast<float *>(q); q += HG * 4;
-        H.m_fin = reinterpret_cast<float *>(q); q += HG * 4;
-        H.l_fin = reinterpret_cast<float *>(q); q += HG * 4;
-        H.z_fin = reinterpret_cast<float *>(q); q += HG * 4;
-        H.vmax = reinterpret_cast<int *>(q); q += 4;
-        H.vscale = reinterpret_cast<float *>(q); q += 4;
-        H.vdel = reinterpret_cast<float *>(smem_raw + P.so_vdel) + h * c.vcap_g;
-        return H;
-    };
-    sp += NHALF * C::half_bytes;
-    double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;   // rotation by 64 theta
+    double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += 2 * 64 * 16;   // tile anchors [2][64]
+    double2 *rot32 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;       // rotation by 32 theta
     double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    float2 *anc32 = reinterpret_cast<float2 *>(sp); sp += 2 * 64 * 8;
+    float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
+    float *red = reinterpret_cast<float *>(sp); sp += 2 * KW * HG * 32 * 4;   // [2][KW][HG][32]
+    int *kfix = reinterpret_cast<int *>(sp); sp += 2 * HG * 32 * 4;          // [2][HG][32]
+    float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
+    int *vfix = reinterpret_cast<int *>(sp); sp += 2 * HG * kHeadDim * 4;    // [2][HG][128]
+    float *osp = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
+    uint16_t *w16 = reinterpret_cast<uint16_t *>(sp); sp += ((HG * 32 * 2 + 15) / 16) * 16;
+    float *beta_s = reinterpret_cast<float *>(sp); sp += HG * 4;
+    float *m_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
+    float *l_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
+    float *z_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
+    int *vmax = reinterpret_cast<int *>(sp); sp += 2 * 4;        // [2] max |V delta| (float bits)
+    float *vinv = reinterpret_cast<float *>(sp); sp += 2 * 4;    // [2] 1 / fixed-point scale
     float *theta32 = reinterpret_cast<float *>(sp); sp += 64 * 4;
     float *lut_inv = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *lut_sc = reinterpret_cast<float *>(sp); sp += HG * 4;
@@ -261,9 +246,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
     int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
+    float *vdel = reinterpret_cast<float *>(smem_raw + P.so_vdel);          // [vcap_g]
     // barriers just below the stage ring: full[S], empty[S]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
-    uint64_t *full_b = bars;
+    uint64_t *full_b = bars, *empty_b = bars + 8;
 
     const long long t_kernel0 = clock64();
     const unsigned long long ns_kernel0 = P.timers ? gtimer_ns() : 0ull;
@@ -281,12 +267,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     const float *ks = c.kpar, *kz = c.kpar + D;
     const float *cbK = c.cb + 16, *cbV = c.cb + 48;   // decode codebooks
     const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
+    const int SN = P.stages;
 
     auto stage_ptr = [&](int st) -> unsigned char * { return smem_raw + P.st_base + (size_t)st * P.st_bytes; };
 
     if (tid == 0) {
-        for (int s = 0; s < P.stages; ++s) {
+        for (int s = 0; s < SN; ++s) {
             mbar_init(full_b + s, 1);
+            mbar_init(empty_b + s, 1);
         }
         mbar_fence_init();
     }
@@ -299,14 +287,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         double s, co;
         sincos((double)P.pos * th, &s, &co);
         qcis[i] = make_double2(co, s);
-        for (int h = 0; h < NHALF; ++h) {   // half h starts at tile t_begin + h
-            const double a0 = (double)(c.pos_base + (int64_t)(t_begin + h) * kTileTokens) * th;
-            sincos(a0, &s, &co);
-            half_at(h).anc64[i] = make_double2(co, s);
-            half_at(h).anc32[i] = make_float2((float)co, (float)s);
-        }
-        sincos((double)(NHALF * kTileTokens) * th, &s, &co);
-        rot64[i] = make_double2(co, s);
+        const double a0 = (double)(c.pos_base + (int64_t)t_begin * kTileTokens) * th;
+        sincos(a0, &s, &co);
+        anc64[i] = make_double2(co, s);
+        anc32[i] = make_float2((float)co, (float)s);
+        sincos((double)kTileTokens * th, &s, &co);
+        rot32[i] = make_double2(co, s);
     }
     for (int x = tid; x < kPairs * 32; x += ATT_THREADS) {
         const int i = x >> 5, j = x & 31;
@@ -315,18 +301,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         sincos((double)j * th, &s, &co);
         t1tab[x] = make_float2((float)co, (float)s);
     }
-    for (int x = tid; x < NHALF * HG * kHeadDim; x += ATT_THREADS) {
-        const Half Hx = half_at(x / (HG * kHeadDim));
-        Hx.osp[x % (HG * kHeadDim)] = 0.f;
-        Hx.vfix[x % (HG * kHeadDim)] = 0;
-    }
-    if (tid < NHALF) { half_at(tid).vmax[0] = 0; half_at(tid).vscale[0] = 1.f; }
+    for (int x = tid; x < 2 * HG * kHeadDim; x += ATT_THREADS) vfix[x] = 0;
+    for (int x = tid; x < 2 * HG * 32; x += ATT_THREADS) kfix[x] = 0;
     for (int x = tid; x < HKV * kHeadDim; x += ATT_THREADS) {
         ks_s[x] = ks[c_lo + x];
         kz_s[x] = kz[c_lo + x];
     }
     if (tid < 64) cb_s[tid] = c.cb[tid];
-    for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) half_at(x / (HG * 32)).kfix[x % (HG * 32)] = 0;
+    if (tid < 2) { vmax[tid] = 0; vinv[tid] = 1.f; }
     if (tid < 16) flag_s[tid] = 0;
     __syncthreads();
     // a1: q~ = RoPE(q, pos) * log2(e)/sqrt(d)
@@ -418,124 +400,100 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         vlut[x] = pack_half2(cbV[e & CM], cbV[e >> BITS]);
     }
     __syncthreads();
-
-    // ====================================================== TMA issue (per half)
-    // Each half owns SH = stages/2 ring slots and issues its own tiles: tiles of half h are
-    // t_k = t_begin + h + 2k, slot k % SH.  The last warp of the half issues tile t_{k+SH-1}
-    // at the top of iteration k, into the slot its half released at the end of k-1.
-    auto issue = [&](int hh, int k) {   // called by one full warp
-        const int SH = P.stages / NHALF;
-        const int ti = t_begin + hh + NHALF * k;
-        if (ti >= t_end) return;
-        const int si = hh * SH + (k % SH);
-        unsigned char *sb = stage_ptr(si);
-        uint64_t *bar = full_b + si;
-        uint32_t nk = 0, nv = 0;
-        if (lane == 0) {
-            const uint32_t *gc = c.gcnt + ((int64_t)ti * c.NG + hg) * 2;
-            nk = __ldg(gc);
-            nv = __ldg(gc + 1);
-        }
-        nk = __shfl_sync(0xffffffffu, nk, 0);
-        nv = __shfl_sync(0xffffffffu, nv, 0);
-        const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
-        const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
-        const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
-        const unsigned b_kw = 32u * QWC * 4u;
-        const unsigned total = 2u * b_kw + 256u + bk + bv;
-        if (lane == 0) {
-            int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
-            hdr[0] = kov ? 0 : (int)nk;
-            hdr[1] = vov ? 0 : (int)nv;
-            hdr[2] = kov;
-            hdr[3] = vov;
-            fence_proxy_async();
-            mbar_expect_tx(bar, total);
-        }
-        __syncwarp();
-        const int64_t n0 = (int64_t)ti * 32;
-        const int64_t bucket = (int64_t)ti * c.NG + hg;
-        if (lane == 0)
-            bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
-        if (lane == 1)
-            bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
-        if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
-        if (lane == 3 && bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
-        if (lane == 4 && bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
-    };
-
-    // =========================================================== compute warps
-    // Two independent halves of 8 warps process alternate tiles with their own scratch,
-    // softmax state and named barrier; they share the read-only tables and hide each
-    // other's latency.  Their partials are merged at the end.
-    const int half = warp / HW, hw = warp % HW, htid = tid % HT;
     const int n_combo = flag_s[2];
-    const Half H = half_at(half < NHALF ? half : 0);
-    // V-phase task mapping inside a half (tensor cores, mma.m16n8k16): warp -> (local KV
-    // head vkv, m-tiles [mt0, mt0 + MTW) of 16 channels); A = V codes (rows = channels,
-    // k = tokens) through the pair table, B = fp16 weights (columns = the G query heads of
-    // vkv), D = fp32 P.V accumulators (columns >= G unused).
-    constexpr int WPK = HW / HKV;               // warps per KV head
-    constexpr int MTW = 8 / WPK;                // m-tiles per warp
-    constexpr int FB = 2 * BITS;                // bits per A field (2 tokens x 1 channel)
-    constexpr int NWV = (MTW * 16 * BITS + 31) / 32;   // code words per lane per tile
-    static_assert(HKV <= HW && HW % HKV == 0 && G <= 8, "V task mapping");
-    const int vkv = hw / WPK;                                // local KV head
-    const int mt0 = (hw % WPK) * MTW;
-    const int vbit0 = mt0 * 16 * BITS;
-    const int vw0 = vbit0 >> 5, voff = vbit0 & 31;           // voff = 16 only for b=3, MTW=1
-    const int vg = lane >> 2, vt = lane & 3;
-    const int vq_lo = vkv * G + min(2 * vt, G - 1), vq_hi = vkv * G + min(2 * vt + 1, G - 1);
-    float dacc[MTW][4];
-#pragma unroll
-    for (int x = 0; x < MTW; ++x) dacc[x][0] = dacc[x][1] = dacc[x][2] = dacc[x][3] = 0.f;
-    // lookup address = vlut + ((code << 7) | (lane << 2)): the OR is exact, the base add
-    // folds into the load (uniform base register)
-    const uint32_t vlut_base = smem_u32(vlut), vlane4 = 4u * lane;
-    float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;
-    int E_cur = -126;     // dense V accumulator units: 2^E_cur (uniform in a half)
-    unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
+    const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
+    unsigned long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
-    if (warp < NCW) {
-        // per-lane constants for the K phase: cis(j * theta_i) for this warp's KPW pairs
+    if (warp < KW) {
+        // ================================================================ K group
+        const int kw = warp, ktid = tid;
+        // TMA issue of the it-th tile into ring slot it % SN (one full warp)
+        auto issue = [&](int it) {
+            if (it >= ntl) return;
+            const int ti = t_begin + it;
+            const int si = it % SN;
+            if (it >= SN) mbar_wait(empty_b + si, (unsigned)((it / SN - 1) & 1));
+            unsigned char *sb = stage_ptr(si);
+            uint64_t *bar = full_b + si;
+            uint32_t nk = 0, nv = 0;
+            if (lane == 0) {
+                const uint32_t *gc = c.gcnt + ((int64_t)ti * c.NG + hg) * 2;
+                nk = __ldg(gc);
+                nv = __ldg(gc + 1);
+            }
+            nk = __shfl_sync(0xffffffffu, nk, 0);
+            nv = __shfl_sync(0xffffffffu, nv, 0);
+            const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
+            const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
+            const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
+            const unsigned b_kw = 32u * QWC * 4u;
+            const unsigned total = 2u * b_kw + 256u + bk + bv;
+            if (lane == 0) {
+                int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
+                hdr[0] = kov ? 0 : (int)nk;
+                hdr[1] = vov ? 0 : (int)nv;
+                hdr[2] = kov;
+                hdr[3] = vov;
+                fence_proxy_async();
+                mbar_expect_tx(bar, total);
+            }
+            __syncwarp();
+            const int64_t n0 = (int64_t)ti * 32;
+            const int64_t bucket = (int64_t)ti * c.NG + hg;
+            if (lane == 0)
+                bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
+            if (lane == 1)
+                bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
+            if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
+            if (lane == 3 && bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
+            if (lane == 4 && bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
+        };
+
+        // per-lane constants: cis(j * theta_i) for this warp's KPW pairs
         float t1c[KPW], t1s[KPW];
 #pragma unroll
         for (int k = 0; k < KPW; ++k) {
-            const float2 v = t1tab[(hw * KPW + k) * 32 + lane];
+            const float2 v = t1tab[(kw * KPW + k) * 32 + lane];
             t1c[k] = v.x;
             t1s[k] = v.y;
         }
+        const int kbit0 = 2 * BITS * KPW * kw;
+        const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
         // this warp's K tables: base | (pair code << 2), + a constant per (head, pair); the
         // base is a multiple of NE*4 bytes (dynamic shared memory is 1 KB aligned)
-        const uint32_t klut_w = smem_u32(klut) + (uint32_t)(hw * KPW * NE * 4);
+        const uint32_t klut_w = smem_u32(klut) + (uint32_t)(kw * KPW * NE * 4);
         if (klut_w & (NE * 4u - 1u)) __trap();
-        const int kbit0 = 2 * BITS * KPW * hw;
-        const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
-        const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
+
+        const int pf = min(PF, SN - 1);   // the slot of tile it + pf must be free of it + pf - SN
+        if (kw == KW - 1)
+            for (int k = 0; k < pf; ++k) issue(k);
         long long tc0 = clock64(), tc1;
         tm[0] = tc0 - t_kernel0;   // prologue
-
-        const int SH = P.stages / NHALF;
-        if (hw == HW - 1)
-            for (int k = 0; k < SH - 1; ++k) issue(half, k);
-        int kk = 0, slot = 0, nv_prev = 0;
-        unsigned par = 0;
-        for (int t = t_begin + half; t < t_end; t += NHALF, ++kk) {
-            const int st = half * SH + slot;
-            if (hw == HW - 1) issue(half, kk + SH - 1);
-            mbar_wait(full_b + st, par);
-            if (++slot == SH) { slot = 0; par ^= 1u; }
+        for (int it = 0; it < ntl; ++it) {
+            const int b = it & 1;
+            if (kw == KW - 1) issue(it + pf);
+            // scores buffer b was consumed by SV (tile it-2); doubles as the K-group sync
+            if (it >= 2) bar_sync(BAR_EMPTY + b, KT + ST);
+            else bar_sync(BAR_K, KT);
+            // anchors of tile it+1 (buffers alternate; all K warps are past tile it-1)
+            if (ktid < 64) {
+                const double2 a = anc64[b * 64 + ktid], r = rot32[ktid];
+                const double2 n = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
+                anc64[(b ^ 1) * 64 + ktid] = n;
+                anc32[(b ^ 1) * 64 + ktid] = make_float2((float)n.x, (float)n.y);
+            }
+            tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
+            const int st = it % SN;
+            mbar_wait(full_b + st, (unsigned)((it / SN) & 1));
             tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
             unsigned char *sb = stage_ptr(st);
             const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
-            const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
-            const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
             const uint32_t *kit = reinterpret_cast<const uint32_t *>(sb + P.so_kit);
-            const uint32_t *vit = reinterpret_cast<const uint32_t *>(sb + P.so_vit);
             const int *hdr = reinterpret_cast<const int *>(sb + P.so_hdr);
-            const int64_t n0 = (int64_t)t * 32;
+            const int64_t n0 = (int64_t)(t_begin + it) * 32;
             const int ntok = (int)min((int64_t)32, P.T - n0);
-            const float2 *anc32 = H.anc32;
+            const float2 *an32 = anc32 + b * 64;
+            int *kf = kfix + b * HG * 32;
 
             // K-outlier correction of one item: (x - K^(code)) * dscore/dK for query head
             // kvl*G + gg, in fp32
@@ -550,7 +508,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const int code = (pc >> (up * BITS)) & CM;
                 const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
                 const float delta = xval - (cbKs[code] * ks_s[chl] + kz_s[chl]);
-                const float2 an = anc32[i], tt = t1tab[i * 32 + j];
+                const float2 an = an32[i], tt = t1tab[i * 32 + j];
                 const float co = an.x * tt.x - an.y * tt.y, si = an.x * tt.y + an.y * tt.x;
                 const int g = kvl * G + gg;
                 const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
@@ -564,30 +522,20 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const int nk = hdr[0];
                 // Key-outlier corrections straight into the (head, token) score term, in fixed
                 // point (native shared integer atomics; see kfix_of)
-                for (int x = htid; x < nk; x += HT) {
+                for (int x = ktid; x < nk; x += KT) {
                     const uint32_t itm = kit[x];
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
                         int j, g;
                         const float v = k_corr(itm, gg, j, g);
-                        atomicAdd(&H.kfix[g * 32 + j], kfix_of(v));
+                        atomicAdd(&kf[g * 32 + j], kfix_of(v));
                     }
                 }
-                // Value-outlier sums of this half's previous tile (fixed point) -> osp
-                if (nv_prev) {
-                    const float inv = H.vscale[0];
-                    for (int x = htid; x < HG * kHeadDim; x += HT) {
-                        const int v = H.vfix[x];
-                        if (v) { H.osp[x] += (float)v * inv; H.vfix[x] = 0; }
-                    }
-                }
-                if (htid == 0) H.vmax[0] = 0;
-                nv_prev = hdr[1] | hdr[3];
                 if (hdr[2]) {
                     // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
                     for (int j = 0; j < ntok; ++j) {
                         const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
-                        for (uint32_t r = r0 + htid; r < r1; r += HT) {
+                        for (uint32_t r = r0 + ktid; r < r1; r += KT) {
                             const uint32_t rec = __ldcg(c.kout + r);
                             const int ch = (int)(rec & 0xffffu);
                             if (ch < c_lo || ch >= c_hi) continue;
@@ -596,14 +544,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                             for (int gg = 0; gg < G; ++gg) {
                                 int jj, g;
                                 const float v = k_corr(itm, gg, jj, g);
-                                atomicAdd(&H.kfix[g * 32 + jj], kfix_of(v));
+                                atomicAdd(&kf[g * 32 + jj], kfix_of(v));
                             }
                         }
                     }
                 }
                 // heavy RoPE pairs in fp32 (tables hlut): the (head, pair) list spread over the
-                // half's warps, lane = token
-                for (int cb = hw; cb < n_combo; cb += HW) {
+                // K warps, lane = token
+                for (int cb = kw; cb < n_combo; cb += KW) {
                     const int g = hv_combo[cb] >> 3, hsl = hv_combo[cb] & 7;
                     const int i = hv_pair[g * 8 + hsl];
                     const int bit = 2 * BITS * i;
@@ -612,9 +560,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + lane] << 32;
                     const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
                     const float2 ab = hlut[(g * HMAX + hsl) * NE + pc];
-                    const float2 an = anc32[i], tt = t1tab[i * 32 + lane];
+                    const float2 an = an32[i], tt = t1tab[i * 32 + lane];
                     const float hc = (an.x * tt.x - an.y * tt.y) * ab.x + (an.x * tt.y + an.y * tt.x) * ab.y;
-                    atomicAdd(&H.kfix[g * 32 + lane], kfix_of(hc));
+                    atomicAdd(&kf[g * 32 + lane], kfix_of(hc));
                 }
             }
             // ------------------------------------------------------------ a2: K dense
@@ -634,19 +582,19 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 }
 #pragma unroll
                 for (int k = 0; k < KPW; ++k) {
-                    const int i = hw * KPW + k;
-                    const float2 an = anc32[i];
+                    const int i = kw * KPW + k;
+                    const float2 an = an32[i];
                     const float cc = an.x * t1c[k] - an.y * t1s[k];
                     const float ss = an.x * t1s[k] + an.y * t1c[k];
                     const uint32_t cs = pack_half2(cc, ss);
-                    const int b = 2 * BITS * k - 2;   // bit of (pair code << 2) in the window
+                    const int bsh = 2 * BITS * k - 2;   // bit of (pair code << 2) in the window
 #pragma unroll
                     for (int h = 0; h < HKV; ++h) {
                         uint32_t off;
-                        if (b < 0) off = wl[h] << 2;
-                        else if (b + 2 * BITS + 2 <= 32) off = wl[h] >> b;
-                        else if (b >= 32) off = wh[h] >> (b - 32);
-                        else off = __funnelshift_r(wl[h], wh[h], b);
+                        if (bsh < 0) off = wl[h] << 2;
+                        else if (bsh + 2 * BITS + 2 <= 32) off = wl[h] >> bsh;
+                        else if (bsh >= 32) off = wh[h] >> (bsh - 32);
+                        else off = __funnelshift_r(wl[h], wh[h], bsh);
                         const uint32_t a = klut_w | (off & ((NE - 1) << 2));
 #pragma unroll
                         for (int gg = 0; gg < G; ++gg) {
@@ -656,11 +604,88 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                         }
                     }
                 }
+                float *rd = red + (b * KW + kw) * HG * 32;
 #pragma unroll
-                for (int g = 0; g < HG; ++g) H.red[(hw * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
+                for (int g = 0; g < HG; ++g) rd[g * 32 + lane] = acc_c[g] + acc_s[g];
             }
-            half_sync(half);
-            tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
+            bar_arrive(BAR_FULL + b, KT + ST);   // scores of tile it -> SV group
+            tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
+        }
+        if (P.timers && ktid == 0) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x) atomicAdd(P.timers + x, tm[x]);
+            atomicAdd(P.timers + 5, (unsigned long long)ntl);
+        }
+    } else {
+        // =============================================================== SV group
+        const int sw = warp - KW, stid = tid - KT;
+        // V-phase task mapping (tensor cores, mma.m16n8k16): warp -> (local KV head vkv,
+        // m-tiles [mt0, mt0 + MTW) of 16 channels); A = V codes (rows = channels, k = tokens)
+        // through the pair table, B = fp16 weights (columns = the G query heads of vkv),
+        // D = fp32 P.V accumulators (columns >= G unused).
+        constexpr int WPK = SW / HKV;               // warps per KV head
+        constexpr int MTW = 8 / WPK;                // m-tiles per warp
+        constexpr int FB = 2 * BITS;                // bits per A field (2 tokens x 1 channel)
+        constexpr int NWV = (MTW * 16 * BITS + 31) / 32;   // code words per lane per tile
+        static_assert(HKV <= SW && SW % HKV == 0 && G <= 8, "V task mapping");
+        const int vkv = sw / WPK;                                // local KV head
+        const int mt0 = (sw % WPK) * MTW;
+        const int vbit0 = mt0 * 16 * BITS;
+        const int vw0 = vbit0 >> 5, voff = vbit0 & 31;           // voff = 16 only for b=3, MTW=1
+        const int vg = lane >> 2, vt = lane & 3;
+        const int vq_lo = vkv * G + min(2 * vt, G - 1), vq_hi = vkv * G + min(2 * vt + 1, G - 1);
+        float dacc[MTW][4];
+#pragma unroll
+        for (int x = 0; x < MTW; ++x) dacc[x][0] = dacc[x][1] = dacc[x][2] = dacc[x][3] = 0.f;
+        // lookup address = vlut + ((code << 7) | (lane << 2))
+        const uint32_t vlut_base = smem_u32(vlut), vlane4 = 4u * lane;
+        // Value-outlier sums of a finished tile (fixed point, buffer bb) into the owners'
+        // accumulators, in units of 2^-E; zeroes the buffer
+        auto fold_vfix = [&](int bb, float unit) {
+            const int *vf = vfix + bb * HG * kHeadDim;
+#pragma unroll
+            for (int ml = 0; ml < MTW; ++ml) {
+                const int ch = (mt0 + ml) * 16 + vg;
+#pragma unroll
+                for (int cl = 0; cl < 2; ++cl) {
+                    if (2 * vt + cl < G) {
+                        int *p = const_cast<int *>(vf) + (vkv * G + 2 * vt + cl) * kHeadDim + ch;
+                        dacc[ml][cl] += (float)p[0] * unit;
+                        dacc[ml][2 + cl] += (float)p[8] * unit;
+                        p[0] = 0;
+                        p[8] = 0;
+                    }
+                }
+            }
+        };
+        float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;   // warp g <-> head g
+        int E_cur = -126, E_prev = -126;   // dense V accumulator units: 2^E (uniform)
+        long long tc0 = clock64(), tc1;
+        for (int it = 0; it < ntl; ++it) {
+            const int b = it & 1;
+            const int st = it % SN;
+            bar_sync(BAR_FULL + b, KT + ST);   // scores of tile it are in buffer b
+            mbar_wait(full_b + st, (unsigned)((it / SN) & 1));   // (already complete)
+            tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
+            unsigned char *sb = stage_ptr(st);
+            const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
+            const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
+            const uint32_t *vit = reinterpret_cast<const uint32_t *>(sb + P.so_vit);
+            const int *hdr = reinterpret_cast<const int *>(sb + P.so_hdr);
+            const int64_t n0 = (int64_t)(t_begin + it) * 32;
+            const int ntok = (int)min((int64_t)32, P.T - n0);
+
+            // Value-outlier delta x - (Chat_V[code] s_n + z_n) of item (token j, channel)
+            auto v_delta = [&](int j, int chl, uint16_t xbits) -> float {
+                const int kvl = chl >> 7, cc = chl & 127;
+                const int bit = vf_bit(j, cc, BITS);
+                const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
+                unsigned long long w64 = vwp[0];
+                if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vwp[32] << 32;
+                const int code = (int)((w64 >> (bit & 31)) & CM);
+                const float2 sz = vsz_s[j];
+                return __half2float(__ushort_as_half(xbits)) - (cbVs[code] * sz.x + sz.y);
+            };
 
             // ------------------------------------------------------- a4: online softmax
             {
@@ -669,14 +694,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 int E_new = E_cur;
                 if (smax > 0.f) E_new = max(E_cur, ilog2f(smax) + 1);
                 const float pe = pow2i(-E_new);
-                if (hw < HG) {
-                    const int g = hw, j = lane;
+                if (sw < HG) {
+                    const int g = sw, j = lane;
                     const bool valid = j < ntok;
+                    const float *rd = red + b * KW * HG * 32;
                     float s = 0.f;
 #pragma unroll
-                    for (int w = 0; w < HW; ++w) s += H.red[(w * HG + g) * 32 + j];
-                    s = s * lut_inv[g] + (float)H.kfix[g * 32 + j] * (1.f / kKfixScale);
-                    H.kfix[g * 32 + j] = 0;
+                    for (int w = 0; w < KW; ++w) s += rd[(w * HG + g) * 32 + j];
+                    int *kf = kfix + (b * HG + g) * 32 + j;
+                    s = s * lut_inv[g] + (float)(*kf) * (1.f / kKfixScale);
+                    *kf = 0;
                     s = valid ? s : -CUDART_INF_F;
                     const float m_new = fmaxf(m_run, warp_max_redux(s));
                     const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
@@ -685,44 +712,44 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     l_lane = l_lane * alpha + p;
                     z_lane = z_lane * alpha + p * sz.y;
                     m_run = m_new;
-                    H.p_s[g * 32 + j] = p;
-                    H.w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * (sz.x * pe)));
-                    if (alpha != 1.f) {
-#pragma unroll
-                        for (int x = 0; x < kHeadDim / 32; ++x) H.osp[g * kHeadDim + x * 32 + lane] *= alpha;
-                    }
-                    if (lane == 0) H.beta_s[g] = alpha * pow2i(E_cur - E_new);
+                    p_s[g * 32 + j] = p;
+                    w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * (sz.x * pe)));
+                    if (lane == 0) beta_s[g] = alpha * pow2i(E_cur - E_new);
                 } else {
-                    // meanwhile the other warps compute the Value-outlier deltas
-                    // x - (Chat_V[code] s_n + z_n) of the tile's items and their max |delta|
+                    // meanwhile: the tile's Value-outlier deltas and their max |delta|
                     const int nvi = hdr[1];
                     float mx = 0.f;
-                    for (int x = htid - HG * 32; x < nvi; x += HT - HG * 32) {
+                    for (int x = stid - HG * 32; x < nvi; x += ST - HG * 32) {
                         const uint32_t itm = vit[x];
-                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
-                        const int kvl = chl >> 7, cc = chl & 127;
-                        const int bit = vf_bit(j, cc, BITS);
-                        const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
-                        unsigned long long w64 = vwp[0];
-                        if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vwp[32] << 32;
-                        const int code = (int)((w64 >> (bit & 31)) & CM);
-                        const float2 sz = vsz_s[j];
-                        const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
-                        const float delta = xval - (cbVs[code] * sz.x + sz.y);
-                        H.vdel[x] = delta;
+                        const float delta = v_delta((int)((itm >> 11) & 31u), (int)(itm & 0x7ffu), (uint16_t)(itm >> 16));
+                        vdel[x] = delta;
                         mx = fmaxf(mx, fabsf(delta));
                     }
+                    if (hdr[3]) {
+                        // overflowed bucket: bound over this tile's CSR rows (rare)
+                        for (int r = stid - HG * 32; r < ntok * kv; r += ST - HG * 32) {
+                            const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
+                            const int ch = (int)(rec & 0xffffu);
+                            if (ch < c_lo || ch >= c_hi) continue;
+                            mx = fmaxf(mx, fabsf(v_delta(r / kv, ch - c_lo, (uint16_t)(rec >> 16))));
+                        }
+                    }
                     mx = warp_max_redux(mx);
-                    if (lane == 0 && mx > 0.f) atomicMax(H.vmax, __float_as_int(mx));
+                    if (lane == 0 && mx > 0.f) atomicMax(vmax + b, __float_as_int(mx));
                 }
+                E_prev = E_cur;
                 E_cur = E_new;
             }
-            half_sync(half);
-            tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
+            if (it + 2 < ntl) bar_arrive(BAR_EMPTY + b, KT + ST);   // K may refill buffer b
+            bar_sync(BAR_SV, ST);
+            tc1 = clock64(); tm[5] += tc1 - tc0; tc0 = tc1;
 
             // -------------------------------------------------------- a5: P.V dense
             {
-                const float b_lo = H.beta_s[vq_lo], b_hi = H.beta_s[vq_hi];
+                // previous tile's Value-outlier sums (units 2^-E_prev), then the rescale
+                if (it > 0) fold_vfix(b ^ 1, vinv[b ^ 1] * pow2i(-E_prev));
+                if (stid == 0) vmax[b ^ 1] = 0;
+                const float b_lo = beta_s[vq_lo], b_hi = beta_s[vq_hi];
                 if (b_lo != 1.f || b_hi != 1.f) {
 #pragma unroll
                     for (int x = 0; x < MTW; ++x) {
@@ -739,7 +766,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 uint32_t bw[2][2];
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) {
-                    const uint32_t *w32 = reinterpret_cast<const uint32_t *>(H.w16 + (vkv * G + (vg < G ? vg : 0)) * 32 + 16 * s2 + 2 * vt);
+                    const uint32_t *w32 = reinterpret_cast<const uint32_t *>(w16 + (vkv * G + (vg < G ? vg : 0)) * 32 + 16 * s2 + 2 * vt);
                     bw[s2][0] = vg < G ? w32[0] : 0u;
                     bw[s2][1] = vg < G ? w32[4] : 0u;
                 }
@@ -764,97 +791,70 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             }
             // ---------------------------------------------------- a6: V outliers
             {
-                auto v_item = [&](uint32_t itm) {
+                // sum_n p_n delta_{n,c} in fixed point: |p delta| 2^(24-e) < 2^25 with
+                // 2^e <= max|delta| < 2^(e+1); <= 32 items per (head, channel) and tile
+                const int nvi = hdr[1];
+                const float mx = __int_as_float(vmax[b]);
+                const int emx = mx > 0.f ? ilog2f(mx) : 0;
+                const float S = pow2i(24 - emx);
+                if (stid == 0) vinv[b] = pow2i(emx - 24);
+                int *vf = vfix + b * HG * kHeadDim;
+                for (int x = stid; x < nvi; x += ST) {
+                    const uint32_t itm = vit[x];
                     const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
                     const int kvl = chl >> 7, cc = chl & 127;
-                    const int bit = vf_bit(j, cc, BITS);
-                    const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
-                    unsigned long long w64 = vwp[0];
-                    if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vwp[32] << 32;
-                    const int code = (int)((w64 >> (bit & 31)) & CM);
-                    const float2 sz = vsz_s[j];
-                    const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
-                    const float delta = xval - (cbVs[code] * sz.x + sz.y);
+                    const float dS = vdel[x] * S;
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
                         const int g = kvl * G + gg;
-                        atomicAdd(&H.osp[g * kHeadDim + cc], H.p_s[g * 32 + j] * delta);
-                    }
-                };
-                const int nvi = hdr[1];
-                if (nvi) {
-                    // sum_n p_n delta_{n,c} in fixed point: |p delta| 2^(24-e) < 2^25 with
-                    // 2^e <= max|delta| < 2^(e+1); <= 32 items per (head, channel) and tile
-                    const float mx = __int_as_float(H.vmax[0]);
-                    const int emx = mx > 0.f ? ilog2f(mx) : 0;
-                    const float S = pow2i(24 - emx);
-                    if (htid == 0) H.vscale[0] = pow2i(emx - 24);   // 1/S
-                    for (int x = htid; x < nvi; x += HT) {
-                        const uint32_t itm = vit[x];
-                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
-                        const int kvl = chl >> 7, cc = chl & 127;
-                        const float dS = H.vdel[x] * S;
-#pragma unroll
-                        for (int gg = 0; gg < G; ++gg) {
-                            const int g = kvl * G + gg;
-                            atomicAdd(&H.vfix[g * kHeadDim + cc], __float2int_rn(H.p_s[g * 32 + j] * dS));
-                        }
+                        atomicAdd(&vf[g * kHeadDim + cc], __float2int_rn(p_s[g * 32 + j] * dS));
                     }
                 }
                 if (hdr[3]) {
-                    // overflowed bucket: this tile's Value outliers from the CSR rows (rare)
-                    for (int r = htid; r < ntok * kv; r += HT) {
+                    for (int r = stid; r < ntok * kv; r += ST) {
                         const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
                         const int ch = (int)(rec & 0xffffu);
                         if (ch < c_lo || ch >= c_hi) continue;
-                        v_item((rec & 0xffff0000u) | ((uint32_t)(r / kv) << 11) | (uint32_t)(ch - c_lo));
+                        const int j = r / kv, chl = ch - c_lo;
+                        const int kvl = chl >> 7, cc = chl & 127;
+                        const float dS = v_delta(j, chl, (uint16_t)(rec >> 16)) * S;
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) {
+                            const int g = kvl * G + gg;
+                            atomicAdd(&vf[g * kHeadDim + cc], __float2int_rn(p_s[g * 32 + j] * dS));
+                        }
                     }
                 }
             }
-            // advance this half's anchors by two tiles (fp64 complex rotation by 64 theta_i)
-            if (htid < 64) {
-                const double2 a = H.anc64[htid], r = rot64[htid];
-                const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
-                H.anc64[htid] = b;
-                H.anc32[htid] = make_float2((float)b.x, (float)b.y);
-            }
-            half_sync(half);
-            tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
+            bar_sync(BAR_SV, ST);   // tile it done: vfix[b] complete, p_s / w16 free
+            if (stid == 0) mbar_arrive(empty_b + st);   // ring slot back to the TMA issuer
+            tc1 = clock64(); tm[6] += tc1 - tc0; tc0 = tc1;
         }
-        if (nv_prev) {
-            const float inv = H.vscale[0];
-            for (int x = htid; x < HG * kHeadDim; x += HT) {
-                const int v = H.vfix[x];
-                if (v) H.osp[x] += (float)v * inv;
-            }
-        }
-        half_sync(half);   // osp entries are updated by other threads below
-        if (hw < HG) {
-            const float l = warp_sum(l_lane), z = warp_sum(z_lane);
-            if (lane == 0) { H.m_fin[hw] = m_run; H.l_fin[hw] = l; H.z_fin[hw] = z; }
-        }
+        // last tile's Value-outlier sums, then the accumulators to shared memory
+        if (ntl > 0) fold_vfix((ntl - 1) & 1, vinv[(ntl - 1) & 1] * pow2i(-E_cur));
         {
-            // dense P.V accumulators (units of 2^-E_cur): row g / g+8 = channel, column = head
             const float sc = pow2i(E_cur);
 #pragma unroll
             for (int ml = 0; ml < MTW; ++ml) {
                 const int ch = (mt0 + ml) * 16 + vg;
-                if (2 * vt < G) {
-                    float *o = H.osp + (vkv * G + 2 * vt) * kHeadDim + ch;
-                    o[0] += dacc[ml][0] * sc;
-                    o[8] += dacc[ml][2] * sc;
-                }
-                if (2 * vt + 1 < G) {
-                    float *o = H.osp + (vkv * G + 2 * vt + 1) * kHeadDim + ch;
-                    o[0] += dacc[ml][1] * sc;
-                    o[8] += dacc[ml][3] * sc;
+#pragma unroll
+                for (int cl = 0; cl < 2; ++cl) {
+                    if (2 * vt + cl < G) {
+                        float *o = osp + (vkv * G + 2 * vt + cl) * kHeadDim + ch;
+                        o[0] = dacc[ml][cl] * sc;
+                        o[8] = dacc[ml][2 + cl] * sc;
+                    }
                 }
             }
         }
-        if (P.timers && tid == 0) {
-#pragma unroll
-            for (int x = 0; x < 5; ++x) atomicAdd(P.timers + x, tm[x]);
-            atomicAdd(P.timers + 5, (unsigned long long)ntl);
+        if (sw < HG) {
+            const float l = warp_sum(l_lane), z = warp_sum(z_lane);
+            if (lane == 0) { m_fin[sw] = m_run; l_fin[sw] = l; z_fin[sw] = z; }
+        }
+        if (P.timers && stid == 0) {
+            atomicAdd(P.timers + 4, tm[4]);
+            atomicAdd(P.timers + 9, tm[5]);
+            atomicAdd(P.timers + 10, tm[6]);
             // wall-clock spread across CTAs: first start, last loop end, longest CTA loop
             atomicMax(P.timers + 6, ~ns_kernel0);
             const unsigned long long ns1 = gtimer_ns();
@@ -864,24 +864,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     }
     __syncthreads();
 
-    // ------------------------------------------------ write partial (merge halves)
+    // ----------------------------------------------------------------- write partial
     float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
-    {
-        const Half H0 = half_at(0), H1 = half_at(1);
-        for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
-            const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
-            const bool u0 = ntl > 0 && H0.l_fin[g] != 0.f, u1 = ntl > 1 && H1.l_fin[g] != 0.f;
-            const float m0 = u0 ? H0.m_fin[g] : -CUDART_INF_F, m1 = u1 ? H1.m_fin[g] : -CUDART_INF_F;
-            const float m = fmaxf(m0, m1);
-            const float w0 = u0 ? exp2f(m0 - m) : 0.f, w1 = u1 ? exp2f(m1 - m) : 0.f;
-            const float l = w0 * (u0 ? H0.l_fin[g] : 0.f) + w1 * (u1 ? H1.l_fin[g] : 0.f);
-            float o = 0.f;
-            if (ch < kHeadDim) {
-                if (u0) o += w0 * (H0.osp[g * kHeadDim + ch] + H0.z_fin[g]);
-                if (u1) o += w1 * (H1.osp[g * kHeadDim + ch] + H1.z_fin[g]);
-            }
-            part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
-        }
+    for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
+        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+        const bool used = ntl > 0 && l_fin[g] != 0.f;
+        const float m = used ? m_fin[g] : -CUDART_INF_F;
+        const float l = used ? l_fin[g] : 0.f;
+        const float o = (used && ch < kHeadDim) ? osp[g * kHeadDim + ch] + z_fin[g] : 0.f;
+        part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
     }
     // ------------------------------------------------------- a7: split merge
     __threadfence();
@@ -951,13 +942,13 @@ size_t layout(const DevCache &c, Params &P) {
     P.so_kit = (unsigned)off; off = align128(off + (size_t)c.kcap_g * 4);
     P.so_vit = (unsigned)off; off = align128(off + (size_t)c.vcap_g * 4);
     const size_t stb = off;
-    // per-item Key-outlier contributions (one tile at a time), then the stage ring
-    const size_t vdel = align128((size_t)NHALF * c.vcap_g * 4);
+    // Value-outlier deltas of the tile in flight, then the mbarriers and the stage ring
+    const size_t vdel = align128((size_t)c.vcap_g * 4);
     P.so_vdel = (unsigned)align128(C::fixed);
     const size_t base = align128(P.so_vdel + vdel + 128);
     P.st_base = (unsigned)base;
     const size_t limit = 227 * 1024;
-    for (int stages = 4; stages >= 2; stages -= 2) {
+    for (int stages = 6; stages >= 2; --stages) {
         const size_t total = base + stages * stb;
         if (total <= limit) {
             P.stages = stages;

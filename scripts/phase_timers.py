@@ -37,12 +37,12 @@ e1.record()
 torch.cuda.synchronize()
 tm = c.phase_timers()
 tiles = tm[5]
-names = ["prologue", "tma_wait", "K_phase", "softmax", "V_phase"]
-ctas = info_splits = c.info()["splits"] * (w.H_q // c.info()["heads_per_cta"])
+ctas = c.info()["splits"] * (w.H_q // c.info()["heads_per_cta"])
 print(f"{wname} T={T} attend {e0.elapsed_time(e1) / 5 * 1e3:.1f} us, info {c.info()}")
-print("compute cycles per tile per CTA:", {n: round(tm[i] / tiles, 1) for i, n in enumerate(names)},
-      "total", round(sum(tm[1:5]) / tiles, 1))
-print(f"prologue cycles per CTA: {tm[0] / (5 * ctas):.0f}  loop cycles per CTA: {sum(tm[1:5]) / (5 * ctas):.0f}")
+per = lambda i: round(tm[i] / tiles, 1)
+print(f"cycles per tile  K group: tma_wait {per(1)} empty_wait {per(2)} work {per(3)}   "
+      f"SV group: full_wait {per(4)} softmax {per(9)} PV {per(10)}")
+print(f"prologue cycles per CTA: {tm[0] / (5 * ctas):.0f}")
 # one more launch alone for the wall-clock spread across CTAs
 c.attend(q, T, o)
 torch.cuda.synchronize()
