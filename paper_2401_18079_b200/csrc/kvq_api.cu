@@ -206,7 +206,7 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     c->max_splits = 4 * 148;
     A(&c->parts, (size_t)c->max_splits * d.H_q * (kHeadDim + 2) * 4);
     A(&c->tickets, 64 * 4);
-    if (getenv("KVQ_PHASE_TIMERS")) A(&c->timers, 16 * 8);
+    if (getenv("KVQ_PHASE_TIMERS")) A(&c->timers, (16 + 4096) * 8);   // + trace of CTA 0
     if (st != KVQ_OK) { kvq_cache_destroy(c); return st; }
     {
         cudaError_t e = cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped);
@@ -265,13 +265,22 @@ kvq_status kvq_get_info(const kvq_cache *c, kvq_info *info) {
     return KVQ_OK;
 }
 
+// Diagnostics only (not in kvq.h): per-tile event clocks of CTA 0 of the last attend,
+// [tile][4] = K scores done, SV past FULL, SV softmax done, SV P.V done (clock64).
+extern "C" kvq_status kvq_debug_trace(kvq_cache *c, uint64_t *out, int n) {
+    if (!c || !c->timers) return fail(KVQ_EINVAL, "phase timers disabled");
+    if (n > 4096) n = 4096;
+    CK(cudaMemcpy(out, c->timers + 16, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    return KVQ_OK;
+}
+
 kvq_status kvq_phase_timers(kvq_cache *c, uint64_t *out) {
     if (!c || !out) return fail(KVQ_EINVAL, "null argument");
     if (!c->timers) return fail(KVQ_EINVAL, "phase timers disabled (set KVQ_PHASE_TIMERS=1)");
     CK(cudaSetDevice(c->cfg.device));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out, c->timers, 16 * 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemset(c->timers, 0, 16 * 8));
+    CK(cudaMemset(c->timers, 0, (16 + 4096) * 8));
     return KVQ_OK;
 }
 

@@ -28,6 +28,8 @@
 #include "kvq_internal.cuh"
 
 #include <math_constants.h>
+#include <cstdio>
+#include <cstdlib>
 
 namespace kvq {
 namespace {
@@ -37,12 +39,9 @@ constexpr int SW = 8;                         // SV-group warps (softmax, P.V)
 constexpr int KT = KW * 32, ST = SW * 32;
 constexpr int ATT_THREADS = KT + ST;          // 16 warps: 4 per SM sub-partition
 constexpr int KPW = kPairs / KW;              // RoPE pairs per warp in the K phase
-constexpr int PF = 2;                         // TMA prefetch distance (tiles)
 // named barrier ids (0 = __syncthreads)
-constexpr int BAR_FULL = 1;                   // + buffer: scores ready (K arrives, SV syncs)
-constexpr int BAR_EMPTY = 3;                  // + buffer: scores consumed (SV arrives, K syncs)
 constexpr int BAR_SV = 5;                     // SV group internal
-constexpr int BAR_K = 6;                      // K group internal
+constexpr int NANC = 4;                       // ring of per-tile RoPE anchors (SV writes 2 ahead)
 
 // ------------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -175,7 +174,7 @@ struct Cfg {
         + HG * 32 * 4 + HG * 32 * 2    /* p_s, w16 */
         + 2 * HG * kHeadDim * 4        /* vfix[2] */
         + HG * kHeadDim * 4            /* osp */
-        + 2 * 64 * 16 + 2 * 64 * 8     /* anc64[2], anc32[2] */
+        + NANC * 64 * 16 + NANC * 64 * 8   /* anc64[NANC], anc32[NANC] */
         + HG * 4 * 8 + 64              /* beta, m/l/z, vmax[2], vinv[2] */
         + 64 * 16 * 2                  /* rot32, qcis */
         + 64 * 4                       /* theta32 */
@@ -183,6 +182,7 @@ struct Cfg {
         + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
         + HG * 24 * 4                  /* heavy pair list, counts, flat list */
         + HG * kHeadDim * 4 * 2 + 64 * 4 /* staged s_c, z_c of the group, codebooks */
+        + 8 * 16                       /* slot headers */
         + 512;
     static constexpr size_t fixed = klut + vlut + hlut + t1 + small;
 };
@@ -217,10 +217,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
     float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
     float2 *t1tab = reinterpret_cast<float2 *>(sp); sp += C::t1;   // cis(j theta_i) [i][j]
-    double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += 2 * 64 * 16;   // tile anchors [2][64]
+    double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += NANC * 64 * 16;   // tile anchors [NANC][64]
     double2 *rot32 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;       // rotation by 32 theta
     double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
-    float2 *anc32 = reinterpret_cast<float2 *>(sp); sp += 2 * 64 * 8;
+    float2 *anc32 = reinterpret_cast<float2 *>(sp); sp += NANC * 64 * 8;
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *red = reinterpret_cast<float *>(sp); sp += 2 * KW * HG * 32 * 4;   // [2][KW][HG][32]
     int *kfix = reinterpret_cast<int *>(sp); sp += 2 * HG * 32 * 4;          // [2][HG][32]
@@ -246,10 +246,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
     int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
+    int *hdr_s = reinterpret_cast<int *>(sp); sp += 8 * 4 * 4;             // per ring slot
     float *vdel = reinterpret_cast<float *>(smem_raw + P.so_vdel);          // [vcap_g]
     // barriers just below the stage ring: full[S], empty[S]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
-    uint64_t *full_b = bars, *empty_b = bars + 8;
+    uint64_t *full_b = bars, *empty_b = bars + 6;
+    uint64_t *sfull = bars + 12, *sempty = bars + 14;   // score buffers: K -> SV, SV -> K
 
     const long long t_kernel0 = clock64();
     const unsigned long long ns_kernel0 = P.timers ? gtimer_ns() : 0ull;
@@ -276,6 +278,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             mbar_init(full_b + s, 1);
             mbar_init(empty_b + s, 1);
         }
+        for (int b2 = 0; b2 < 2; ++b2) {
+            mbar_init(sfull + b2, KW);    // one arrival per K warp
+            mbar_init(sempty + b2, 1);
+        }
         mbar_fence_init();
     }
 
@@ -287,10 +293,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         double s, co;
         sincos((double)P.pos * th, &s, &co);
         qcis[i] = make_double2(co, s);
-        const double a0 = (double)(c.pos_base + (int64_t)t_begin * kTileTokens) * th;
-        sincos(a0, &s, &co);
-        anc64[i] = make_double2(co, s);
-        anc32[i] = make_float2((float)co, (float)s);
+        for (int a = 0; a < 2; ++a) {   // anchors of the first two tiles
+            const double a0 = (double)(c.pos_base + (int64_t)(t_begin + a) * kTileTokens) * th;
+            sincos(a0, &s, &co);
+            anc64[a * 64 + i] = make_double2(co, s);
+            anc32[a * 64 + i] = make_float2((float)co, (float)s);
+        }
         sincos((double)kTileTokens * th, &s, &co);
         rot32[i] = make_double2(co, s);
     }
@@ -401,54 +409,71 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     }
     __syncthreads();
     const int n_combo = flag_s[2];
+    // ---------------------------------------------------------------- TMA issue
+    // A bulk copy instruction holds its warp for roughly bytes / 16 cycles, so the copies of
+    // a tile are spread over the four SV warps 4..7 (idle while the softmax warps work):
+    //   part 0: slot header + expect_tx + K code words, part 1: V code words,
+    //   part 2: per-token (s, z) + Key-outlier items, part 3: Value-outlier items.
+    // Tile it + TD is issued at the top of SV iteration it, into the slot the SV group
+    // released at the end of iteration it - 1 (TD = SN - 1); tiles 0..TD-1 in the prologue.
+    uint32_t cnt_k = 0, cnt_v = 0;   // outlier counts, lane i: tile it0 + i (blocks of 4)
+    auto load_counts = [&](int it0) {
+        const int it = it0 + lane;
+        if (lane < 4 && it < ntl) {
+            const uint32_t *gc = c.gcnt + ((int64_t)(t_begin + it) * c.NG + hg) * 2;
+            cnt_k = __ldg(gc);
+            cnt_v = __ldg(gc + 1);
+        }
+    };
+    auto issue = [&](int it, int part) {   // one full warp
+        if (it >= ntl) return;
+        const int ti = t_begin + it;
+        const int si = it % SN;
+        if (it >= SN) mbar_wait(empty_b + si, (unsigned)((it / SN - 1) & 1));
+        unsigned char *sb = stage_ptr(si);
+        uint64_t *bar = full_b + si;
+        const uint32_t nk = __shfl_sync(0xffffffffu, cnt_k, it & 3);
+        const uint32_t nv = __shfl_sync(0xffffffffu, cnt_v, it & 3);
+        if ((it & 3) == 3) load_counts(it + 1);
+        const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
+        const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
+        const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
+        const unsigned b_kw = 32u * QWC * 4u;
+        if (lane != 0) return;
+        const int64_t n0 = (int64_t)ti * 32;
+        const int64_t bucket = (int64_t)ti * c.NG + hg;
+        if (part == 0) {
+            // header in a generic-only array (no proxy fence needed); published by the
+            // expect_tx arrival, read after the full-barrier wait.  (complete_tx of the other
+            // parts may land first: the phase cannot complete before this arrival.)
+            int *hdr = hdr_s + si * 4;
+            hdr[0] = kov ? 0 : (int)nk;
+            hdr[1] = vov ? 0 : (int)nv;
+            hdr[2] = kov;
+            hdr[3] = vov;
+            mbar_expect_tx(bar, 2u * b_kw + 256u + bk + bv);
+            bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
+        } else if (part == 1) {
+            bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
+        } else if (part == 2) {
+            bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
+            if (bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
+        } else {
+            if (bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
+        }
+    };
+    const int TD = SN - 1;
+    const int ipart = warp - (KW + SW - 4);   // SV warps 4..7 -> parts 0..3
+    if (ipart >= 0) {
+        load_counts(0);
+        for (int k = 0; k < TD; ++k) issue(k, ipart);
+    }
     const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
     unsigned long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
     if (warp < KW) {
         // ================================================================ K group
         const int kw = warp, ktid = tid;
-        // TMA issue of the it-th tile into ring slot it % SN (one full warp)
-        auto issue = [&](int it) {
-            if (it >= ntl) return;
-            const int ti = t_begin + it;
-            const int si = it % SN;
-            if (it >= SN) mbar_wait(empty_b + si, (unsigned)((it / SN - 1) & 1));
-            unsigned char *sb = stage_ptr(si);
-            uint64_t *bar = full_b + si;
-            uint32_t nk = 0, nv = 0;
-            if (lane == 0) {
-                const uint32_t *gc = c.gcnt + ((int64_t)ti * c.NG + hg) * 2;
-                nk = __ldg(gc);
-                nv = __ldg(gc + 1);
-            }
-            nk = __shfl_sync(0xffffffffu, nk, 0);
-            nv = __shfl_sync(0xffffffffu, nv, 0);
-            const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
-            const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
-            const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
-            const unsigned b_kw = 32u * QWC * 4u;
-            const unsigned total = 2u * b_kw + 256u + bk + bv;
-            if (lane == 0) {
-                int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
-                hdr[0] = kov ? 0 : (int)nk;
-                hdr[1] = vov ? 0 : (int)nv;
-                hdr[2] = kov;
-                hdr[3] = vov;
-                fence_proxy_async();
-                mbar_expect_tx(bar, total);
-            }
-            __syncwarp();
-            const int64_t n0 = (int64_t)ti * 32;
-            const int64_t bucket = (int64_t)ti * c.NG + hg;
-            if (lane == 0)
-                bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
-            if (lane == 1)
-                bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
-            if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
-            if (lane == 3 && bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
-            if (lane == 4 && bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
-        };
-
         // per-lane constants: cis(j * theta_i) for this warp's KPW pairs
         float t1c[KPW], t1s[KPW];
 #pragma unroll
@@ -464,35 +489,28 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const uint32_t klut_w = smem_u32(klut) + (uint32_t)(kw * KPW * NE * 4);
         if (klut_w & (NE * 4u - 1u)) __trap();
 
-        const int pf = min(PF, SN - 1);   // the slot of tile it + pf must be free of it + pf - SN
-        if (kw == KW - 1)
-            for (int k = 0; k < pf; ++k) issue(k);
         long long tc0 = clock64(), tc1;
         tm[0] = tc0 - t_kernel0;   // prologue
+        int slot = 0;
+        unsigned par = 0;
         for (int it = 0; it < ntl; ++it) {
             const int b = it & 1;
-            if (kw == KW - 1) issue(it + pf);
-            // scores buffer b was consumed by SV (tile it-2); doubles as the K-group sync
-            if (it >= 2) bar_sync(BAR_EMPTY + b, KT + ST);
-            else bar_sync(BAR_K, KT);
-            // anchors of tile it+1 (buffers alternate; all K warps are past tile it-1)
-            if (ktid < 64) {
-                const double2 a = anc64[b * 64 + ktid], r = rot32[ktid];
-                const double2 n = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
-                anc64[(b ^ 1) * 64 + ktid] = n;
-                anc32[(b ^ 1) * 64 + ktid] = make_float2((float)n.x, (float)n.y);
-            }
+            // scores buffer b consumed by SV (tile it-2), which also wrote this tile's
+            // anchors; every K warp waits on its own (no K-group barrier)
+            if (it >= 2) mbar_wait(sempty + b, (unsigned)(((it >> 1) - 1) & 1));
             tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
-            const int st = it % SN;
-            mbar_wait(full_b + st, (unsigned)((it / SN) & 1));
+            const int st = slot;
+            mbar_wait(full_b + st, par);
+            if (++slot == SN) { slot = 0; par ^= 1u; }
             tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
+            if (P.timers && blockIdx.x == 0 && lane == 0 && it < 100) P.timers[16 + it * 32 + kw] = tc1;
             unsigned char *sb = stage_ptr(st);
             const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
             const uint32_t *kit = reinterpret_cast<const uint32_t *>(sb + P.so_kit);
-            const int *hdr = reinterpret_cast<const int *>(sb + P.so_hdr);
+            const int *hdr = hdr_s + st * 4;
             const int64_t n0 = (int64_t)(t_begin + it) * 32;
             const int ntok = (int)min((int64_t)32, P.T - n0);
-            const float2 *an32 = anc32 + b * 64;
+            const float2 *an32 = anc32 + (it % NANC) * 64;
             int *kf = kfix + b * HG * 32;
 
             // K-outlier correction of one item: (x - K^(code)) * dscore/dK for query head
@@ -608,13 +626,20 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
                 for (int g = 0; g < HG; ++g) rd[g * 32 + lane] = acc_c[g] + acc_s[g];
             }
-            bar_arrive(BAR_FULL + b, KT + ST);   // scores of tile it -> SV group
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sfull + b);   // this warp's scores of tile it -> SV group
+            if (P.timers && blockIdx.x == 0 && lane == 0 && it < 100) P.timers[16 + it * 32 + 8 + kw] = clock64();
             tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
         }
         if (P.timers && ktid == 0) {
 #pragma unroll
             for (int x = 0; x < 4; ++x) atomicAdd(P.timers + x, tm[x]);
             atomicAdd(P.timers + 5, (unsigned long long)ntl);
+        }
+        // per-warp work of K warps 3, 5, 7 (imbalance diagnostics)
+        if (P.timers && lane == 0) {
+            atomicAdd(P.timers + 16 + 4000 + kw, tm[3]);         // work
+            atomicAdd(P.timers + 16 + 4010 + kw, tm[1] + tm[2]); // waits
         }
     } else {
         // =============================================================== SV group
@@ -661,17 +686,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;   // warp g <-> head g
         int E_cur = -126, E_prev = -126;   // dense V accumulator units: 2^E (uniform)
         long long tc0 = clock64(), tc1;
+        int slot = 0;
+        unsigned par = 0;
         for (int it = 0; it < ntl; ++it) {
             const int b = it & 1;
-            const int st = it % SN;
-            bar_sync(BAR_FULL + b, KT + ST);   // scores of tile it are in buffer b
-            mbar_wait(full_b + st, (unsigned)((it / SN) & 1));   // (already complete)
+            const int st = slot;
+            if (ipart >= 0) issue(it + TD, ipart);
+            mbar_wait(sfull + b, (unsigned)((it >> 1) & 1));   // scores of tile it in buffer b
+            mbar_wait(full_b + st, par);       // (already complete)
+            if (++slot == SN) { slot = 0; par ^= 1u; }
+            if (P.timers && blockIdx.x == 0 && stid == 0 && it < 100) P.timers[16 + it * 32 + 16] = clock64();
             tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
             unsigned char *sb = stage_ptr(st);
             const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
             const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
             const uint32_t *vit = reinterpret_cast<const uint32_t *>(sb + P.so_vit);
-            const int *hdr = reinterpret_cast<const int *>(sb + P.so_hdr);
+            const int *hdr = hdr_s + st * 4;
             const int64_t n0 = (int64_t)(t_begin + it) * 32;
             const int ntok = (int)min((int64_t)32, P.T - n0);
 
@@ -740,9 +770,23 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 E_prev = E_cur;
                 E_cur = E_new;
             }
-            if (it + 2 < ntl) bar_arrive(BAR_EMPTY + b, KT + ST);   // K may refill buffer b
+            // anchors of tile it+2 (ring slot free: K warps are at tiles it+1 / it+2 at most
+            // once they see this tile's release below)
+            if (stid < 64 && it + 2 < ntl) {
+                const int i = stid;
+                const double2 a = anc64[((it + 1) % NANC) * 64 + i], r = rot32[i];
+                const double2 n = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
+                anc64[((it + 2) % NANC) * 64 + i] = n;
+                anc32[((it + 2) % NANC) * 64 + i] = make_float2((float)n.x, (float)n.y);
+            }
+            if (P.timers && blockIdx.x == 0 && lane == 0 && it < 100 && (sw == 0 || sw == 4 || sw == SW - 1))
+                P.timers[16 + it * 32 + 24 + (sw == 0 ? 0 : sw == 4 ? 1 : 2)] = clock64();
+            if (P.timers && blockIdx.x == 0 && lane == 0 && it < 100 && sw == SW - 1)
+                P.timers[16 + it * 32 + 27] = tc1;   // (sfull passed)
             bar_sync(BAR_SV, ST);
+            if (stid == 0) mbar_arrive(sempty + b);   // K may refill buffer b (tile it+2)
             tc1 = clock64(); tm[5] += tc1 - tc0; tc0 = tc1;
+            if (P.timers && blockIdx.x == 0 && stid == 0 && it < 100) P.timers[16 + it * 32 + 17] = tc1;
 
             // -------------------------------------------------------- a5: P.V dense
             {
@@ -829,6 +873,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             bar_sync(BAR_SV, ST);   // tile it done: vfix[b] complete, p_s / w16 free
             if (stid == 0) mbar_arrive(empty_b + st);   // ring slot back to the TMA issuer
             tc1 = clock64(); tm[6] += tc1 - tc0; tc0 = tc1;
+            if (P.timers && blockIdx.x == 0 && stid == 0 && it < 100) P.timers[16 + it * 32 + 18] = tc1;
         }
         // last tile's Value-outlier sums, then the accumulators to shared memory
         if (ntl > 0) fold_vfix((ntl - 1) & 1, vinv[(ntl - 1) & 1] * pow2i(-E_cur));
@@ -963,6 +1008,9 @@ template <int BITS, int HG, int G>
 cudaError_t launch_t(const DevCache &c, Params &P, int grid, cudaStream_t s) {
     const size_t smem = layout<BITS, HG>(c, P);
     if (smem == 0) return cudaErrorInvalidConfiguration;
+    static bool dbg = getenv("KVQ_DEBUG_LAYOUT") != nullptr;
+    if (dbg) fprintf(stderr, "att_kernel<%d,%d,%d>: smem %zu fixed %zu stages %d stage %u kcap_g %d vcap_g %d\n",
+                     BITS, HG, G, smem, Cfg<BITS, HG>::fixed, P.stages, P.st_bytes, c.kcap_g, c.vcap_g);
     cudaError_t e = cudaFuncSetAttribute(att_kernel<BITS, HG, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
