@@ -2,21 +2,21 @@
 //
 // One launch per attend.  grid = n_head_groups x splits (head group
 // fastest), one CTA per SM, each CTA a contiguous range of 32-token tiles of one group of
-// HG query heads.  Two warp groups form a pipeline over the tiles:
-//   K group (8 warps)   waits for the tile's TMA bulk copies (K/V code words, per-token (s,z),
-//                       outlier items of this head group; issued 2 tiles ahead by its last
-//                       warp), then computes the tile's scores: a2 RoPE-pair table lookups
-//                       (lane = token, warp = 8 RoPE pairs of every head; fp16 x fp16 -> fp32),
-//                       a3 Key-outlier and heavy-pair terms in fp32 summed in fixed point with
-//                       shared integer atomics.  Scores go to one of two buffers.
-//   SV group (8 warps)  a4 online softmax in base 2 (warp g = head g; the other warps
-//                       compute the tile's Value-outlier deltas meanwhile), then a5 P.V on the
-//                       tensor cores (mma.m16n8k16: A = Value codes through a pair table,
-//                       B = fp16 weights p s 2^-E) and a6 the Value-outlier terms.
-//   Named barriers hand the score buffers over (FULL: K -> SV, EMPTY: SV -> K) and an
-//   mbarrier per ring slot returns the stage to the TMA issuer, so neither group waits for
-//   the other except on a full/empty buffer.  a7: the last CTA of each head group merges the
-//   split partials (log-sum-exp, ticket counter).
+// HG query heads.  The CTA's 16 warps form four independent quads; quad q takes the tiles
+// q, q+4, q+8, ... of the range, so four tiles are in flight and a quad only ever waits for
+// its own four warps (one named barrier per tile):
+//   load   at the top of a tile the quad's 128 threads cp.async (16 B each) its next tile --
+//          K/V code words, per-token (s,z), outlier items of this head group -- into a
+//          shared ring slot; completion arrives on the slot's mbarrier.
+//   a2+a3  K: warp w of the quad takes RoPE pairs 16w..16w+15 of every head (lane = token):
+//          pair-table lookups (fp16 x fp16 -> fp32), Key-outlier and heavy-pair terms in fp32
+//          summed in fixed point with shared integer atomics.  -> quad barrier
+//   a4     online softmax in base 2, warp w = head w (4 partial sums per token);
+//   a5+a6  P.V on the tensor cores (mma.m16n8k16: A = Value codes through a pair table,
+//          B = fp16 weights p s 2^-E, warp w = KV head w for MHA), Value-outlier terms in
+//          fixed point folded into the accumulators.
+//   a7     the quads' partials are merged, then the last CTA of each head group merges the
+//          split partials (log-sum-exp, ticket counter).
 //   Tables (built per CTA, a1): q~ = RoPE(q, pos) with exact fp64 angles (R11, R12) times
 //   log2(e)/sqrt(d); per (query head g, RoPE pair i) a 2^{2b}-entry table of fp16 pairs
 //   (A, B), A = q~_i K^_i(a) + q~_i' K^_i'(b), B = q~_i' K^_i(a) - q~_i K^_i'(b) with
@@ -28,20 +28,19 @@
 #include "kvq_internal.cuh"
 
 #include <math_constants.h>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
 namespace kvq {
 namespace {
 
-constexpr int KW = 8;                         // K-group warps (scores)
-constexpr int SW = 8;                         // SV-group warps (softmax, P.V)
-constexpr int KT = KW * 32, ST = SW * 32;
-constexpr int ATT_THREADS = KT + ST;          // 16 warps: 4 per SM sub-partition
-constexpr int KPW = kPairs / KW;              // RoPE pairs per warp in the K phase
-// named barrier ids (0 = __syncthreads)
-constexpr int BAR_SV = 5;                     // SV group internal
-constexpr int NANC = 4;                       // ring of per-tile RoPE anchors (SV writes 2 ahead)
+constexpr int NQ = 4;                         // quads: independent 4-warp pipelines
+constexpr int QWARPS = 4;                     // warps per quad
+constexpr int QT = QWARPS * 32;               // threads per quad
+constexpr int ATT_THREADS = NQ * QT;          // 16 warps: 4 per SM sub-partition
+constexpr int KPW = kPairs / QWARPS;          // RoPE pairs per warp in the K phase (16)
+constexpr int NANC = 3;                       // per-quad ring of tile anchors (written 2 ahead)
 
 // ------------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -80,6 +79,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+// 16-byte cp.async (LDGSTS, L2 only) and the mbarrier arrival fired by its completion
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void bar_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -162,29 +168,26 @@ __device__ __forceinline__ float warp_max_redux(float v) {
 template <int BITS, int HG>
 struct Cfg {
     static constexpr int NE = 1 << (2 * BITS);
-    static constexpr int HMAX = BITS == 4 ? 4 : 8;   // fp32 "heavy" pairs per head
+    static constexpr int HMAX = 4;                   // fp32 "heavy" pairs per head
     static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
     static constexpr size_t vlut = (size_t)NE * 32 * 4;
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
-    static constexpr size_t t1 = (size_t)kPairs * 32 * 8;
+    static constexpr size_t t1 = (size_t)kPairs * 32 * 8;       // prologue only (in the ring)
+    // per quad: red[2], kfix[2], p, w16, vfix, anchors[NANC], beta/m/l/z
+    static constexpr size_t quad =
+        2 * QWARPS * HG * 32 * 4 + 2 * HG * 32 * 4 + HG * 32 * 4 + HG * 32 * 2 + HG * kHeadDim * 4
+        + NANC * 64 * 8 + HG * 4 * 4 + 64;
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
-        + 2 * KW * HG * 32 * 4         /* red[2] */
-        + 2 * HG * 32 * 4              /* kfix[2] */
-        + HG * 32 * 4 + HG * 32 * 2    /* p_s, w16 */
-        + 2 * HG * kHeadDim * 4        /* vfix[2] */
-        + HG * kHeadDim * 4            /* osp */
-        + NANC * 64 * 16 + NANC * 64 * 8   /* anc64[NANC], anc32[NANC] */
-        + HG * 4 * 8 + 64              /* beta, m/l/z, vmax[2], vinv[2] */
-        + 64 * 16 * 2                  /* rot32, qcis */
-        + 64 * 4                       /* theta32 */
-        + HG * 4 * 8                   /* per-head scalars */
-        + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
+        + NQ * quad
+        + 64 * 16                      /* rot128 */
+        + 64 * 5 * 8                   /* cis(2^k theta_i) */
+        + HG * 4 * 2                   /* lut scale / inverse */
         + HG * 24 * 4                  /* heavy pair list, counts, flat list */
         + HG * kHeadDim * 4 * 2 + 64 * 4 /* staged s_c, z_c of the group, codebooks */
-        + 8 * 16                       /* slot headers */
+        + 16 * 4 + 16 * 16             /* flags, slot headers */
         + 512;
-    static constexpr size_t fixed = klut + vlut + hlut + t1 + small;
+    static constexpr size_t fixed = klut + vlut + hlut + small;
 };
 
 struct Params {
@@ -196,10 +199,10 @@ struct Params {
     float *parts;
     unsigned *tickets;
     int write_partial;
-    // stage ring layout (bytes), computed on the host
-    int stages;
-    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit, so_hdr, so_vdel;
-    unsigned long long *timers;   // optional [16] diagnostics, may be null
+    // ring layout (bytes), computed on the host
+    int spq, scap_k, scap_v;      // ring slots per quad; outlier items a slot holds (mult. of 4)
+    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit;
+    unsigned long long *timers;   // optional diagnostics, may be null
 };
 
 template <int BITS, int HG, int G>
@@ -210,51 +213,37 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     constexpr int HKV = HG / G;
     constexpr int QWC = HKV * 4 * BITS;             // K (and V) words per token in the CTA
     constexpr int HMAX = C::HMAX;
+    constexpr int KWW = 2 * BITS * KPW / 32;        // K code words of a warp's pairs (per head)
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sp = smem_raw;
     uint32_t *klut = reinterpret_cast<uint32_t *>(sp); sp += C::klut;
     uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
     float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
-    float2 *t1tab = reinterpret_cast<float2 *>(sp); sp += C::t1;   // cis(j theta_i) [i][j]
-    double2 *anc64 = reinterpret_cast<double2 *>(sp); sp += NANC * 64 * 16;   // tile anchors [NANC][64]
-    double2 *rot32 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;       // rotation by 32 theta
-    double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
-    float2 *anc32 = reinterpret_cast<float2 *>(sp); sp += NANC * 64 * 8;
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
-    float *red = reinterpret_cast<float *>(sp); sp += 2 * KW * HG * 32 * 4;   // [2][KW][HG][32]
-    int *kfix = reinterpret_cast<int *>(sp); sp += 2 * HG * 32 * 4;          // [2][HG][32]
-    float *p_s = reinterpret_cast<float *>(sp); sp += HG * 32 * 4;
-    int *vfix = reinterpret_cast<int *>(sp); sp += 2 * HG * kHeadDim * 4;    // [2][HG][128]
-    float *osp = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
-    uint16_t *w16 = reinterpret_cast<uint16_t *>(sp); sp += ((HG * 32 * 2 + 15) / 16) * 16;
-    float *beta_s = reinterpret_cast<float *>(sp); sp += HG * 4;
-    float *m_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
-    float *l_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
-    float *z_fin = reinterpret_cast<float *>(sp); sp += HG * 4;
-    int *vmax = reinterpret_cast<int *>(sp); sp += 2 * 4;        // [2] max |V delta| (float bits)
-    float *vinv = reinterpret_cast<float *>(sp); sp += 2 * 4;    // [2] 1 / fixed-point scale
-    float *theta32 = reinterpret_cast<float *>(sp); sp += 64 * 4;
+    unsigned char *quad_base = sp; sp += NQ * C::quad;
+    double2 *rot128 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;   // rotation by 128 theta
+    float2 *cisp = reinterpret_cast<float2 *>(sp); sp += 64 * 5 * 8;   // cis(2^k theta_i) [i][k]
     float *lut_inv = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *lut_sc = reinterpret_cast<float *>(sp); sp += HG * 4;
-    float *bound_s = reinterpret_cast<float *>(sp); sp += HG * 64 * 4;
-    uint8_t *heavy_s = reinterpret_cast<uint8_t *>(sp); sp += HG * 64;
     int *hv_pair = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
     int *hv_n = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
     int *hv_combo = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;   // flat (head, slot) list
     float *ks_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;   // s_c of the group
     float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
-    int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
-    int *hdr_s = reinterpret_cast<int *>(sp); sp += 8 * 4 * 4;             // per ring slot
-    float *vdel = reinterpret_cast<float *>(smem_raw + P.so_vdel);          // [vcap_g]
-    // barriers just below the stage ring: full[S], empty[S]
+    int *flag_s = reinterpret_cast<int *>(sp); sp += 16 * 4;
+    int *hdr_s = reinterpret_cast<int *>(sp); sp += 16 * 16;               // per ring slot
+    // mbarriers just below the ring: full[slot] (the cp.async of a tile have landed)
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
-    uint64_t *full_b = bars, *empty_b = bars + 6;
-    uint64_t *sfull = bars + 12, *sempty = bars + 14;   // score buffers: K -> SV, SV -> K
+    uint64_t *full_b = bars;   // [NQ * SPQ]
+    // prologue-only scratch in the (not yet used) ring
+    float2 *t1tab = reinterpret_cast<float2 *>(smem_raw + P.st_base);
+    double2 *qcis = reinterpret_cast<double2 *>(smem_raw + P.st_base + C::t1);
+    float *bound_s = reinterpret_cast<float *>(smem_raw + P.st_base + C::t1 + 64 * 16);
+    uint8_t *heavy_s = reinterpret_cast<uint8_t *>(smem_raw + P.st_base + C::t1 + 64 * 16 + HG * 64 * 4);
 
     const long long t_kernel0 = clock64();
-    const unsigned long long ns_kernel0 = P.timers ? gtimer_ns() : 0ull;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
     const int hg = blockIdx.x % n_hg;
@@ -269,19 +258,39 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     const float *ks = c.kpar, *kz = c.kpar + D;
     const float *cbK = c.cb + 16, *cbV = c.cb + 48;   // decode codebooks
     const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
-    const int SN = P.stages;
+    const int SPQ = P.spq;     // private ring slots per quad
 
+    // quad scratch
+    const int q = warp / QWARPS, w = warp % QWARPS, qtid = tid % QT;
+    struct Quad {
+        float *red;       // [2][QWARPS][HG][32] partial scores
+        int *kfix;        // [2][HG][32] Key-outlier + heavy-pair terms, fixed point
+        float *p_s;       // [HG][32]
+        uint16_t *w16;    // [HG][32] fp16 weights p s 2^-E
+        int *vfix;        // [HG][128] Value-outlier sums of the tile, fixed point
+        float2 *anc;      // [NANC][64] tile anchors cis(n0 theta_i)
+        float *beta, *m_fin, *l_fin, *z_fin;   // [HG]
+    };
+    auto quad_at = [&](int qq) -> Quad {
+        Quad Q;
+        unsigned char *p = quad_base + qq * C::quad;
+        Q.red = reinterpret_cast<float *>(p); p += 2 * QWARPS * HG * 32 * 4;
+        Q.kfix = reinterpret_cast<int *>(p); p += 2 * HG * 32 * 4;
+        Q.p_s = reinterpret_cast<float *>(p); p += HG * 32 * 4;
+        Q.vfix = reinterpret_cast<int *>(p); p += HG * kHeadDim * 4;
+        Q.anc = reinterpret_cast<float2 *>(p); p += NANC * 64 * 8;
+        Q.beta = reinterpret_cast<float *>(p); p += HG * 4;
+        Q.m_fin = reinterpret_cast<float *>(p); p += HG * 4;
+        Q.l_fin = reinterpret_cast<float *>(p); p += HG * 4;
+        Q.z_fin = reinterpret_cast<float *>(p); p += HG * 4;
+        Q.w16 = reinterpret_cast<uint16_t *>(p);
+        return Q;
+    };
+    const Quad Q = quad_at(q);
     auto stage_ptr = [&](int st) -> unsigned char * { return smem_raw + P.st_base + (size_t)st * P.st_bytes; };
 
     if (tid == 0) {
-        for (int s = 0; s < SN; ++s) {
-            mbar_init(full_b + s, 1);
-            mbar_init(empty_b + s, 1);
-        }
-        for (int b2 = 0; b2 < 2; ++b2) {
-            mbar_init(sfull + b2, KW);    // one arrival per K warp
-            mbar_init(sempty + b2, 1);
-        }
+        for (int s = 0; s < NQ * SPQ; ++s) mbar_init(full_b + s, 1);   // the expect_tx arrival
         mbar_fence_init();
     }
 
@@ -289,18 +298,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     if (tid < 64) {
         const int i = tid;
         const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
-        theta32[i] = (float)th;
         double s, co;
         sincos((double)P.pos * th, &s, &co);
         qcis[i] = make_double2(co, s);
-        for (int a = 0; a < 2; ++a) {   // anchors of the first two tiles
-            const double a0 = (double)(c.pos_base + (int64_t)(t_begin + a) * kTileTokens) * th;
-            sincos(a0, &s, &co);
-            anc64[a * 64 + i] = make_double2(co, s);
-            anc32[a * 64 + i] = make_float2((float)co, (float)s);
-        }
-        sincos((double)kTileTokens * th, &s, &co);
-        rot32[i] = make_double2(co, s);
+        sincos((double)(NQ * kTileTokens) * th, &s, &co);
+        rot128[i] = make_double2(co, s);
+    }
+    for (int x = tid; x < kPairs * 5; x += ATT_THREADS) {
+        const int i = x / 5, k = x % 5;
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)(1 << k) * th, &s, &co);
+        cisp[x] = make_float2((float)co, (float)s);
     }
     for (int x = tid; x < kPairs * 32; x += ATT_THREADS) {
         const int i = x >> 5, j = x & 31;
@@ -309,14 +318,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         sincos((double)j * th, &s, &co);
         t1tab[x] = make_float2((float)co, (float)s);
     }
-    for (int x = tid; x < 2 * HG * kHeadDim; x += ATT_THREADS) vfix[x] = 0;
-    for (int x = tid; x < 2 * HG * 32; x += ATT_THREADS) kfix[x] = 0;
+    for (int x = tid; x < NQ * HG * kHeadDim; x += ATT_THREADS) quad_at(x / (HG * kHeadDim)).vfix[x % (HG * kHeadDim)] = 0;
+    for (int x = tid; x < NQ * 2 * HG * 32; x += ATT_THREADS) quad_at(x / (2 * HG * 32)).kfix[x % (2 * HG * 32)] = 0;
     for (int x = tid; x < HKV * kHeadDim; x += ATT_THREADS) {
         ks_s[x] = ks[c_lo + x];
         kz_s[x] = kz[c_lo + x];
     }
     if (tid < 64) cb_s[tid] = c.cb[tid];
-    if (tid < 2) { vmax[tid] = 0; vinv[tid] = 1.f; }
     if (tid < 16) flag_s[tid] = 0;
     __syncthreads();
     // a1: q~ = RoPE(q, pos) * log2(e)/sqrt(d)
@@ -407,45 +415,69 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const int e = x >> 5;
         vlut[x] = pack_half2(cbV[e & CM], cbV[e >> BITS]);
     }
-    __syncthreads();
+    // per-lane constants of the K phase: cis(j theta_i) for this warp's KPW pairs
+    float t1c[KPW], t1s[KPW];
+#pragma unroll
+    for (int k = 0; k < KPW; ++k) {
+        const float2 v = t1tab[(w * KPW + k) * 32 + lane];
+        t1c[k] = v.x;
+        t1s[k] = v.y;
+    }
+    // anchors of each quad's first two tiles; the fp64 running anchor of the next one stays in
+    // registers of the quad's warp 0 (pairs lane, lane + 32)
+    double2 amaster[2];
+    if (w == 0) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+            const int i = lane + 32 * h2;
+            const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+            double s, co;
+            for (int a = 0; a < 2; ++a) {
+                const double a0 = (double)(c.pos_base + (int64_t)(t_begin + q + NQ * a) * kTileTokens) * th;
+                sincos(a0, &s, &co);
+                Q.anc[a * 64 + i] = make_float2((float)co, (float)s);
+            }
+            amaster[h2] = make_double2(co, s);
+        }
+    }
+    __syncthreads();   // tables ready; the ring (t1tab) is free from here on
     const int n_combo = flag_s[2];
-    // ---------------------------------------------------------------- TMA issue
-    // A bulk copy instruction holds its warp for roughly bytes / 16 cycles, so the copies of
-    // a tile are spread over the four SV warps 4..7 (idle while the softmax warps work):
-    //   part 0: slot header + expect_tx + K code words, part 1: V code words,
-    //   part 2: per-token (s, z) + Key-outlier items, part 3: Value-outlier items.
-    // Tile it + TD is issued at the top of SV iteration it, into the slot the SV group
-    // released at the end of iteration it - 1 (TD = SN - 1); tiles 0..TD-1 in the prologue.
-    uint32_t cnt_k = 0, cnt_v = 0;   // outlier counts, lane i: tile it0 + i (blocks of 4)
-    auto load_counts = [&](int it0) {
-        const int it = it0 + lane;
-        if (lane < 4 && it < ntl) {
+    const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
+    unsigned long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+    // ------------------------------------------------------- tile loads (cp.async)
+    // Quad q handles the CTA's tiles it = q + 4i and owns SPQ private ring slots: tile i goes
+    // to slot q*SPQ + i % SPQ, loaded with TMA bulk copies issued by the quad's warps,
+    // completion counted on the slot's mbarrier (complete_tx).  (16-byte cp.async from 128
+    // threads measured ~2000 cycles of issue per tile under the LDS load of the K phase.)  The
+    // slot's previous tile (i - SPQ) is free once every warp of the quad is past the quad
+    // barrier of tile i - SPQ + 1: tile i + 1 is loaded at the top of tile i when SPQ >= 3,
+    // right after the barrier of tile i when SPQ == 2.  Outlier counts are read one load
+    // ahead (registers).
+    const int nqt = ntl > q ? (ntl - q + NQ - 1) / NQ : 0;   // tiles of this quad
+    uint32_t nk_nx = 0, nv_nx = 0;     // counts of the quad's next tile to load
+    auto read_counts = [&](int it, uint32_t &nk, uint32_t &nv) {
+        nk = nv = 0;
+        if (it < ntl) {
             const uint32_t *gc = c.gcnt + ((int64_t)(t_begin + it) * c.NG + hg) * 2;
-            cnt_k = __ldg(gc);
-            cnt_v = __ldg(gc + 1);
+            nk = __ldg(gc);
+            nv = __ldg(gc + 1);
         }
     };
-    auto issue = [&](int it, int part) {   // one full warp
-        if (it >= ntl) return;
-        const int ti = t_begin + it;
-        const int si = it % SN;
-        if (it >= SN) mbar_wait(empty_b + si, (unsigned)((it / SN - 1) & 1));
-        unsigned char *sb = stage_ptr(si);
-        uint64_t *bar = full_b + si;
-        const uint32_t nk = __shfl_sync(0xffffffffu, cnt_k, it & 3);
-        const uint32_t nv = __shfl_sync(0xffffffffu, cnt_v, it & 3);
-        if ((it & 3) == 3) load_counts(it + 1);
-        const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
+    auto load_tile = [&](int ii, uint32_t nk, uint32_t nv) {   // quad iteration ii
+        if (ii >= nqt || lane != 0) return;
+        const int si = q * SPQ + ii % SPQ;
+        const int ti = t_begin + q + NQ * ii;
+        const bool kov = nk > (uint32_t)P.scap_k, vov = nv > (uint32_t)P.scap_v;
         const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
         const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
-        const unsigned b_kw = 32u * QWC * 4u;
-        if (lane != 0) return;
-        const int64_t n0 = (int64_t)ti * 32;
+        const unsigned b_kw = QWC * 32u * 4u;
+        unsigned char *sb = stage_ptr(si);
+        uint64_t *bar = full_b + si;
         const int64_t bucket = (int64_t)ti * c.NG + hg;
-        if (part == 0) {
-            // header in a generic-only array (no proxy fence needed); published by the
-            // expect_tx arrival, read after the full-barrier wait.  (complete_tx of the other
-            // parts may land first: the phase cannot complete before this arrival.)
+        // TMA bulk copies, one or two per warp of the quad (an issue holds its warp for
+        // ~150 cycles); the expect_tx arrival (warp 0) publishes the header written before it
+        if (w == 0) {
             int *hdr = hdr_s + si * 4;
             hdr[0] = kov ? 0 : (int)nk;
             hdr[1] = vov ? 0 : (int)nv;
@@ -453,259 +485,283 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             hdr[3] = vov;
             mbar_expect_tx(bar, 2u * b_kw + 256u + bk + bv);
             bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
-        } else if (part == 1) {
+        } else if (w == 1) {
             bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
-        } else if (part == 2) {
-            bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
+        } else if (w == 2) {
+            bulk_g2s(sb + P.so_vsz, c.vsz + (int64_t)ti * 32, 256u, bar);
             if (bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
         } else {
             if (bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
         }
     };
-    const int TD = SN - 1;
-    const int ipart = warp - (KW + SW - 4);   // SV warps 4..7 -> parts 0..3
-    if (ipart >= 0) {
-        load_counts(0);
-        for (int k = 0; k < TD; ++k) issue(k, ipart);
+    if (nqt > 0) {
+        uint32_t nk0, nv0;
+        read_counts(q, nk0, nv0);
+        read_counts(q + NQ, nk_nx, nv_nx);
+        load_tile(0, nk0, nv0);
     }
-    const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
-    unsigned long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto load_next = [&](int i) {   // tile i + 1 of the quad
+        const uint32_t nk = nk_nx, nv = nv_nx;
+        read_counts(q + NQ * (i + 2), nk_nx, nv_nx);
+        load_tile(i + 1, nk, nv);
+    };
 
-    if (warp < KW) {
-        // ================================================================ K group
-        const int kw = warp, ktid = tid;
-        // per-lane constants: cis(j * theta_i) for this warp's KPW pairs
-        float t1c[KPW], t1s[KPW];
+    // V-phase mapping inside the quad (tensor cores, mma.m16n8k16): warp -> (local KV head
+    // vkv, m-tiles [mt0, mt0 + MTW) of 16 channels); A = V codes (rows = channels, k = tokens)
+    // through the pair table, B = fp16 weights (columns = the G query heads of vkv),
+    // D = fp32 P.V accumulators (columns >= G unused).
+    constexpr int WPK = QWARPS / HKV;           // warps per KV head
+    constexpr int MTW = 8 / WPK;                // m-tiles per warp
+    constexpr int FB = 2 * BITS;                // bits per A field (2 tokens x 1 channel)
+    constexpr int NWV = (MTW * 16 * BITS + 31) / 32;   // code words per lane per tile
+    constexpr bool SELF = (WPK == 1 && G == 1);        // warp w: softmax head w == V head w
+    static_assert(HKV <= QWARPS && QWARPS % HKV == 0 && G <= 8, "V task mapping");
+    const int vkv = w / WPK;
+    const int mt0 = (w % WPK) * MTW;
+    const int vbit0 = mt0 * 16 * BITS;
+    const int vw0 = vbit0 >> 5, voff = vbit0 & 31;           // voff = 16 only for b=3, MTW=1
+    const int vg = lane >> 2, vt = lane & 3;
+    const int vq_lo = vkv * G + min(2 * vt, G - 1), vq_hi = vkv * G + min(2 * vt + 1, G - 1);
+    const uint32_t vlut_base = smem_u32(vlut), vlane4 = 4u * lane;
+    // this warp's K tables: base | (pair code << 2), + a constant per (head, pair)
+    const uint32_t klut_w = smem_u32(klut) + (uint32_t)(w * KPW * NE * 4);
+    if (klut_w & (NE * 4u - 1u)) __trap();
+    float dacc[MTW][4];
 #pragma unroll
-        for (int k = 0; k < KPW; ++k) {
-            const float2 v = t1tab[(kw * KPW + k) * 32 + lane];
-            t1c[k] = v.x;
-            t1s[k] = v.y;
-        }
-        const int kbit0 = 2 * BITS * KPW * kw;
-        const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
-        // this warp's K tables: base | (pair code << 2), + a constant per (head, pair); the
-        // base is a multiple of NE*4 bytes (dynamic shared memory is 1 KB aligned)
-        const uint32_t klut_w = smem_u32(klut) + (uint32_t)(kw * KPW * NE * 4);
-        if (klut_w & (NE * 4u - 1u)) __trap();
+    for (int x = 0; x < MTW; ++x) dacc[x][0] = dacc[x][1] = dacc[x][2] = dacc[x][3] = 0.f;
+    float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;   // softmax head w (w < HG)
+    int E_cur = -126;      // dense V accumulator units: 2^E (uniform in the quad)
+    long long tc0 = clock64(), tc1;
+    tm[0] = tc0 - t_kernel0;
 
-        long long tc0 = clock64(), tc1;
-        tm[0] = tc0 - t_kernel0;   // prologue
-        int slot = 0;
-        unsigned par = 0;
-        for (int it = 0; it < ntl; ++it) {
-            const int b = it & 1;
-            // scores buffer b consumed by SV (tile it-2), which also wrote this tile's
-            // anchors; every K warp waits on its own (no K-group barrier)
-            if (it >= 2) mbar_wait(sempty + b, (unsigned)(((it >> 1) - 1) & 1));
-            tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
-            const int st = slot;
-            mbar_wait(full_b + st, par);
-            if (++slot == SN) { slot = 0; par ^= 1u; }
-            tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
-            if (P.timers && blockIdx.x == 0 && lane == 0 && it < 100) P.timers[16 + it * 32 + kw] = tc1;
-            unsigned char *sb = stage_ptr(st);
-            const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
-            const uint32_t *kit = reinterpret_cast<const uint32_t *>(sb + P.so_kit);
-            const int *hdr = hdr_s + st * 4;
-            const int64_t n0 = (int64_t)(t_begin + it) * 32;
-            const int ntok = (int)min((int64_t)32, P.T - n0);
-            const float2 *an32 = anc32 + (it % NANC) * 64;
-            int *kf = kfix + b * HG * 32;
+    for (int i = 0; i < nqt; ++i) {
+        const int it = q + NQ * i;
+        const int b = i & 1;
+        const int st = q * SPQ + i % SPQ;
+        if (SPQ >= 3) load_next(i);
+        tc1 = clock64(); tm[5] += tc1 - tc0; tc0 = tc1;
+        mbar_wait(full_b + st, (unsigned)((i / SPQ) & 1));
+        tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
+        unsigned char *sb = stage_ptr(st);
+        const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
+        const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
+        const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
+        const uint32_t *kit = reinterpret_cast<const uint32_t *>(sb + P.so_kit);
+        const uint32_t *vit = reinterpret_cast<const uint32_t *>(sb + P.so_vit);
+        const int *hdr = hdr_s + st * 4;
+        const int64_t n0 = (int64_t)(t_begin + it) * 32;
+        const int ntok = (int)min((int64_t)32, P.T - n0);
+        const float2 *an32 = Q.anc + (i % NANC) * 64;
+        int *kf = Q.kfix + b * HG * 32;
 
-            // K-outlier correction of one item: (x - K^(code)) * dscore/dK for query head
-            // kvl*G + gg, in fp32
-            auto k_corr = [&](uint32_t itm, int gg, int &j_out, int &g_out) -> float {
-                const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
-                const int kvl = chl >> 7, cc = chl & 127, i = cc & 63, up = cc >> 6;
-                const int bit = 2 * BITS * i;
-                const int wq = kvl * 4 * BITS + (bit >> 5);
-                unsigned long long w64 = kw_s[wq * 32 + j];
-                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                const int code = (pc >> (up * BITS)) & CM;
-                const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
-                const float delta = xval - (cbKs[code] * ks_s[chl] + kz_s[chl]);
-                const float2 an = an32[i], tt = t1tab[i * 32 + j];
-                const float co = an.x * tt.x - an.y * tt.y, si = an.x * tt.y + an.y * tt.x;
-                const int g = kvl * G + gg;
-                const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
-                j_out = j;
-                g_out = g;
-                return delta * (up ? (qb * co - qa * si) : (qa * co + qb * si));
-            };
-
-            // ------------------------------------------ a3: K outliers, heavy pairs
-            {
-                const int nk = hdr[0];
-                // Key-outlier corrections straight into the (head, token) score term, in fixed
-                // point (native shared integer atomics; see kfix_of)
-                for (int x = ktid; x < nk; x += KT) {
-                    const uint32_t itm = kit[x];
+        // cis((n0 + j) theta_i) = anchor_i * cis(j theta_i), the second factor as a product of
+        // the binary powers cis(2^k theta_i) (fp32 table) -- for items and heavy pairs
+        auto cis_tok = [&](int ii, int j) -> float2 {
+            float2 r = an32[ii];
 #pragma unroll
-                    for (int gg = 0; gg < G; ++gg) {
-                        int j, g;
-                        const float v = k_corr(itm, gg, j, g);
-                        atomicAdd(&kf[g * 32 + j], kfix_of(v));
-                    }
+            for (int k = 0; k < 5; ++k)
+                if ((j >> k) & 1) {
+                    const float2 p = cisp[ii * 5 + k];
+                    r = make_float2(r.x * p.x - r.y * p.y, r.x * p.y + r.y * p.x);
                 }
-                if (hdr[2]) {
-                    // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
-                    for (int j = 0; j < ntok; ++j) {
-                        const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
-                        for (uint32_t r = r0 + ktid; r < r1; r += KT) {
-                            const uint32_t rec = __ldcg(c.kout + r);
-                            const int ch = (int)(rec & 0xffffu);
-                            if (ch < c_lo || ch >= c_hi) continue;
-                            const uint32_t itm = (rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - c_lo);
+            return r;
+        };
+        // K-outlier correction of one item: (x - K^(code)) * dscore/dK for query head
+        // kvl*G + gg, in fp32
+        auto k_corr = [&](uint32_t itm, int gg, int &j_out, int &g_out) -> float {
+            const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+            const int kvl = chl >> 7, cc = chl & 127, ii = cc & 63, up = cc >> 6;
+            const int bit = 2 * BITS * ii;
+            const int wq = kvl * 4 * BITS + (bit >> 5);
+            unsigned long long w64 = kw_s[wq * 32 + j];
+            if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+            const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+            const int code = (pc >> (up * BITS)) & CM;
+            const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+            const float delta = xval - (cbKs[code] * ks_s[chl] + kz_s[chl]);
+            const float2 cs = cis_tok(ii, j);
+            const int g = kvl * G + gg;
+            const float qa = qs[g * kHeadDim + ii], qb = qs[g * kHeadDim + ii + 64];
+            j_out = j;
+            g_out = g;
+            return delta * (up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y));
+        };
+
+        // ------------------------------------------ a3: K outliers, heavy pairs
+        {
+            const int nk = hdr[0];
+            for (int x = qtid; x < nk; x += QT) {
+                const uint32_t itm = kit[x];
 #pragma unroll
-                            for (int gg = 0; gg < G; ++gg) {
-                                int jj, g;
-                                const float v = k_corr(itm, gg, jj, g);
-                                atomicAdd(&kf[g * 32 + jj], kfix_of(v));
-                            }
+                for (int gg = 0; gg < G; ++gg) {
+                    int j, g;
+                    const float v = k_corr(itm, gg, j, g);
+                    atomicAdd(&kf[g * 32 + j], kfix_of(v));
+                }
+            }
+            if (hdr[2]) {
+                // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
+                for (int j = 0; j < ntok; ++j) {
+                    const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
+                    for (uint32_t r = r0 + qtid; r < r1; r += QT) {
+                        const uint32_t rec = __ldcg(c.kout + r);
+                        const int ch = (int)(rec & 0xffffu);
+                        if (ch < c_lo || ch >= c_hi) continue;
+                        const uint32_t itm = (rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - c_lo);
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) {
+                            int jj, g;
+                            const float v = k_corr(itm, gg, jj, g);
+                            atomicAdd(&kf[g * 32 + jj], kfix_of(v));
                         }
                     }
                 }
-                // heavy RoPE pairs in fp32 (tables hlut): the (head, pair) list spread over the
-                // K warps, lane = token
-                for (int cb = kw; cb < n_combo; cb += KW) {
-                    const int g = hv_combo[cb] >> 3, hsl = hv_combo[cb] & 7;
-                    const int i = hv_pair[g * 8 + hsl];
-                    const int bit = 2 * BITS * i;
-                    const int wq = (g / G) * 4 * BITS + (bit >> 5);
-                    unsigned long long w64 = kw_s[wq * 32 + lane];
-                    if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + lane] << 32;
-                    const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                    const float2 ab = hlut[(g * HMAX + hsl) * NE + pc];
-                    const float2 an = an32[i], tt = t1tab[i * 32 + lane];
-                    const float hc = (an.x * tt.x - an.y * tt.y) * ab.x + (an.x * tt.y + an.y * tt.x) * ab.y;
-                    atomicAdd(&kf[g * 32 + lane], kfix_of(hc));
-                }
             }
-            // ------------------------------------------------------------ a2: K dense
-            {
-                float acc_c[HG], acc_s[HG];
+            // heavy RoPE pairs in fp32 (tables hlut): the (head, pair) list spread over the
+            // quad's warps, lane = token
+            for (int cb = w; cb < n_combo; cb += QWARPS) {
+                const int g = hv_combo[cb] >> 3, hsl = hv_combo[cb] & 7;
+                const int ii = hv_pair[g * 8 + hsl];
+                const int bit = 2 * BITS * ii;
+                const int wq = (g / G) * 4 * BITS + (bit >> 5);
+                unsigned long long w64 = kw_s[wq * 32 + lane];
+                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + lane] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                const float2 ab = hlut[(g * HMAX + hsl) * NE + pc];
+                const float2 cs = cis_tok(ii, lane);
+                atomicAdd(&kf[g * 32 + lane], kfix_of(cs.x * ab.x + cs.y * ab.y));
+            }
+        }
+        // ------------------------------------------------------------ a2: K dense
+        {
+            float acc_c[HG], acc_s[HG];
 #pragma unroll
-                for (int g = 0; g < HG; ++g) { acc_c[g] = 0.f; acc_s[g] = 0.f; }
-                uint32_t wl[HKV], wh[HKV];
+            for (int g = 0; g < HG; ++g) { acc_c[g] = 0.f; acc_s[g] = 0.f; }
 #pragma unroll
-                for (int h = 0; h < HKV; ++h) {
-                    unsigned long long w64 = kw_s[(h * 4 * BITS + kq0) * 32 + lane];
-                    if (kshift + 2 * BITS * KPW > 32)
-                        w64 |= (unsigned long long)kw_s[(h * 4 * BITS + kq0 + 1) * 32 + lane] << 32;
-                    w64 >>= kshift;
-                    wl[h] = (uint32_t)w64;
-                    wh[h] = (uint32_t)(w64 >> 32);
-                }
+            for (int h = 0; h < HKV; ++h) {
+                uint32_t wd[KWW];
+#pragma unroll
+                for (int x = 0; x < KWW; ++x) wd[x] = kw_s[(h * 4 * BITS + w * KWW + x) * 32 + lane];
 #pragma unroll
                 for (int k = 0; k < KPW; ++k) {
-                    const int i = kw * KPW + k;
-                    const float2 an = an32[i];
+                    const float2 an = an32[w * KPW + k];
                     const float cc = an.x * t1c[k] - an.y * t1s[k];
                     const float ss = an.x * t1s[k] + an.y * t1c[k];
                     const uint32_t cs = pack_half2(cc, ss);
-                    const int bsh = 2 * BITS * k - 2;   // bit of (pair code << 2) in the window
+                    const int bsh = 2 * BITS * k - 2;   // bit of (pair code << 2) in the words
+                    uint32_t off;
+                    if (bsh < 0) off = wd[0] << 2;
+                    else if ((bsh & 31) + 2 * BITS + 2 <= 32) off = wd[bsh >> 5] >> (bsh & 31);
+                    else off = __funnelshift_r(wd[bsh >> 5], wd[(bsh >> 5) + 1], bsh & 31);
+                    const uint32_t a = klut_w | (off & ((NE - 1) << 2));
 #pragma unroll
-                    for (int h = 0; h < HKV; ++h) {
-                        uint32_t off;
-                        if (bsh < 0) off = wl[h] << 2;
-                        else if (bsh + 2 * BITS + 2 <= 32) off = wl[h] >> bsh;
-                        else if (bsh >= 32) off = wh[h] >> (bsh - 32);
-                        else off = __funnelshift_r(wl[h], wh[h], bsh);
-                        const uint32_t a = klut_w | (off & ((NE - 1) << 2));
-#pragma unroll
-                        for (int gg = 0; gg < G; ++gg) {
-                            const int g = h * G + gg;
-                            const uint32_t ab = lds_u32(a + (uint32_t)((g * 64 + k) * NE * 4));
-                            fma2_f16_f32(ab, cs, acc_c[g], acc_s[g]);
-                        }
+                    for (int gg = 0; gg < G; ++gg) {
+                        const int g = h * G + gg;
+                        const uint32_t ab = lds_u32(a + (uint32_t)((g * 64 + k) * NE * 4));
+                        fma2_f16_f32(ab, cs, acc_c[g], acc_s[g]);
                     }
                 }
-                float *rd = red + (b * KW + kw) * HG * 32;
-#pragma unroll
-                for (int g = 0; g < HG; ++g) rd[g * 32 + lane] = acc_c[g] + acc_s[g];
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(sfull + b);   // this warp's scores of tile it -> SV group
-            if (P.timers && blockIdx.x == 0 && lane == 0 && it < 100) P.timers[16 + it * 32 + 8 + kw] = clock64();
-            tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
-        }
-        if (P.timers && ktid == 0) {
+            float *rd = Q.red + (b * QWARPS + w) * HG * 32;
 #pragma unroll
-            for (int x = 0; x < 4; ++x) atomicAdd(P.timers + x, tm[x]);
-            atomicAdd(P.timers + 5, (unsigned long long)ntl);
+            for (int g = 0; g < HG; ++g) rd[g * 32 + lane] = acc_c[g] + acc_s[g];
         }
-        // per-warp work of K warps 3, 5, 7 (imbalance diagnostics)
-        if (P.timers && lane == 0) {
-            atomicAdd(P.timers + 16 + 4000 + kw, tm[3]);         // work
-            atomicAdd(P.timers + 16 + 4010 + kw, tm[1] + tm[2]); // waits
-        }
-    } else {
-        // =============================================================== SV group
-        const int sw = warp - KW, stid = tid - KT;
-        // V-phase task mapping (tensor cores, mma.m16n8k16): warp -> (local KV head vkv,
-        // m-tiles [mt0, mt0 + MTW) of 16 channels); A = V codes (rows = channels, k = tokens)
-        // through the pair table, B = fp16 weights (columns = the G query heads of vkv),
-        // D = fp32 P.V accumulators (columns >= G unused).
-        constexpr int WPK = SW / HKV;               // warps per KV head
-        constexpr int MTW = 8 / WPK;                // m-tiles per warp
-        constexpr int FB = 2 * BITS;                // bits per A field (2 tokens x 1 channel)
-        constexpr int NWV = (MTW * 16 * BITS + 31) / 32;   // code words per lane per tile
-        static_assert(HKV <= SW && SW % HKV == 0 && G <= 8, "V task mapping");
-        const int vkv = sw / WPK;                                // local KV head
-        const int mt0 = (sw % WPK) * MTW;
-        const int vbit0 = mt0 * 16 * BITS;
-        const int vw0 = vbit0 >> 5, voff = vbit0 & 31;           // voff = 16 only for b=3, MTW=1
-        const int vg = lane >> 2, vt = lane & 3;
-        const int vq_lo = vkv * G + min(2 * vt, G - 1), vq_hi = vkv * G + min(2 * vt + 1, G - 1);
-        float dacc[MTW][4];
+        tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
+        bar_sync(1 + q, QT);   // the quad's scores of tile it are complete
+        tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
+        if (SPQ == 2) load_next(i);
+        // anchors of the quad's tile two ahead (slot free: every warp is past K(i))
+        if (w == 0 && i + 2 < nqt) {
 #pragma unroll
-        for (int x = 0; x < MTW; ++x) dacc[x][0] = dacc[x][1] = dacc[x][2] = dacc[x][3] = 0.f;
-        // lookup address = vlut + ((code << 7) | (lane << 2))
-        const uint32_t vlut_base = smem_u32(vlut), vlane4 = 4u * lane;
-        // Value-outlier sums of a finished tile (fixed point, buffer bb) into the owners'
-        // accumulators, in units of 2^-E; zeroes the buffer
-        auto fold_vfix = [&](int bb, float unit) {
-            const int *vf = vfix + bb * HG * kHeadDim;
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const int ii = lane + 32 * h2;
+                const double2 a = amaster[h2], r = rot128[ii];
+                amaster[h2] = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
+                Q.anc[((i + 2) % NANC) * 64 + ii] = make_float2((float)amaster[h2].x, (float)amaster[h2].y);
+            }
+        }
+
+        // ------------------------------------------------------- a4: online softmax
+        float smax = lane < ntok ? vsz_s[lane].x : 0.f;
+        smax = warp_max_redux(smax);
+        int E_new = E_cur;
+        if (smax > 0.f) E_new = max(E_cur, ilog2f(smax) + 1);
+        const float pe = pow2i(-E_new);
+        float beta_w = 1.f;
+        if (w < HG) {
+            const int g = w, j = lane;
+            const bool valid = j < ntok;
+            const float *rd = Q.red + b * QWARPS * HG * 32;
+            float s = 0.f;
+#pragma unroll
+            for (int x = 0; x < QWARPS; ++x) s += rd[(x * HG + g) * 32 + j];
+            s = s * lut_inv[g] + (float)kf[g * 32 + j] * (1.f / kKfixScale);
+            kf[g * 32 + j] = 0;
+            s = valid ? s : -CUDART_INF_F;
+            const float m_new = fmaxf(m_run, warp_max_redux(s));
+            const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
+            const float p = valid ? exp2f(s - m_new) : 0.f;
+            const float2 sz = valid ? vsz_s[j] : make_float2(0.f, 0.f);
+            l_lane = l_lane * alpha + p;
+            z_lane = z_lane * alpha + p * sz.y;
+            m_run = m_new;
+            Q.p_s[g * 32 + j] = p;
+            Q.w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * (sz.x * pe)));
+            beta_w = alpha * pow2i(E_cur - E_new);
+            if (!SELF && lane == 0) Q.beta[g] = beta_w;
+        }
+        const int E_prev = E_cur;
+        E_cur = E_new;
+        if (SELF) __syncwarp();
+        else bar_sync(1 + q, QT);   // weights of other warps' heads
+
+        // -------------------------------------------------------- a5: P.V dense
+        {
+            const float b_lo = SELF ? beta_w : Q.beta[vq_lo], b_hi = SELF ? beta_w : Q.beta[vq_hi];
+            if (b_lo != 1.f || b_hi != 1.f) {
+#pragma unroll
+                for (int x = 0; x < MTW; ++x) {
+                    dacc[x][0] *= b_lo; dacc[x][1] *= b_hi;
+                    dacc[x][2] *= b_lo; dacc[x][3] *= b_hi;
+                }
+            }
+            uint32_t vr[NWV + 1];
+#pragma unroll
+            for (int x = 0; x < NWV; ++x) vr[x] = vw_s[(vkv * 4 * BITS + vw0 + x) * 32 + lane];
+            vr[NWV] = 0u;
+            if (BITS == 3 && MTW == 1 && voff) { vr[0] = __funnelshift_r(vr[0], vr[1], 16); vr[1] >>= 16; }
+            // B fragments (weights of query head vkv*G + g for tokens 16s + 2t.. / +8..)
+            uint32_t bw[2][2];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const uint32_t *w32 = reinterpret_cast<const uint32_t *>(Q.w16 + (vkv * G + (vg < G ? vg : 0)) * 32 + 16 * s2 + 2 * vt);
+                bw[s2][0] = vg < G ? w32[0] : 0u;
+                bw[s2][1] = vg < G ? w32[4] : 0u;
+            }
 #pragma unroll
             for (int ml = 0; ml < MTW; ++ml) {
-                const int ch = (mt0 + ml) * 16 + vg;
 #pragma unroll
-                for (int cl = 0; cl < 2; ++cl) {
-                    if (2 * vt + cl < G) {
-                        int *p = const_cast<int *>(vf) + (vkv * G + 2 * vt + cl) * kHeadDim + ch;
-                        dacc[ml][cl] += (float)p[0] * unit;
-                        dacc[ml][2 + cl] += (float)p[8] * unit;
-                        p[0] = 0;
-                        p[8] = 0;
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    uint32_t a[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int bit = ((ml * 2 + s2) * 4 + r) * FB;
+                        const int wi = bit >> 5, sh = bit & 31;
+                        uint32_t off;
+                        if (sh + FB <= 32) off = sh >= 7 ? (vr[wi] >> (sh - 7)) : (vr[wi] << (7 - sh));
+                        else off = __funnelshift_r(vr[wi], vr[wi + 1], sh - 7);
+                        a[r] = lds_u32(vlut_base + (vlane4 | (off & ((NE - 1) << 7))));
                     }
+                    mma_f16_f32(dacc[ml], a, bw[s2]);
                 }
             }
-        };
-        float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;   // warp g <-> head g
-        int E_cur = -126, E_prev = -126;   // dense V accumulator units: 2^E (uniform)
-        long long tc0 = clock64(), tc1;
-        int slot = 0;
-        unsigned par = 0;
-        for (int it = 0; it < ntl; ++it) {
-            const int b = it & 1;
-            const int st = slot;
-            if (ipart >= 0) issue(it + TD, ipart);
-            mbar_wait(sfull + b, (unsigned)((it >> 1) & 1));   // scores of tile it in buffer b
-            mbar_wait(full_b + st, par);       // (already complete)
-            if (++slot == SN) { slot = 0; par ^= 1u; }
-            if (P.timers && blockIdx.x == 0 && stid == 0 && it < 100) P.timers[16 + it * 32 + 16] = clock64();
-            tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
-            unsigned char *sb = stage_ptr(st);
-            const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
-            const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
-            const uint32_t *vit = reinterpret_cast<const uint32_t *>(sb + P.so_vit);
-            const int *hdr = hdr_s + st * 4;
-            const int64_t n0 = (int64_t)(t_begin + it) * 32;
-            const int ntok = (int)min((int64_t)32, P.T - n0);
-
-            // Value-outlier delta x - (Chat_V[code] s_n + z_n) of item (token j, channel)
+        }
+        // ---------------------------------------------------- a6: V outliers
+        {
+            // this warp's items (its KV head, its m-tiles): sum_n p_n delta_{n,c} in fixed
+            // point with |p delta| 2^(24-e) < 2^25, 2^e <= max|delta| < 2^(e+1), then folded
+            // into the accumulators (units 2^-E)
+            const int nvi = hdr[1];
             auto v_delta = [&](int j, int chl, uint16_t xbits) -> float {
                 const int kvl = chl >> 7, cc = chl & 127;
                 const int bit = vf_bit(j, cc, BITS);
@@ -716,207 +772,124 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const float2 sz = vsz_s[j];
                 return __half2float(__ushort_as_half(xbits)) - (cbVs[code] * sz.x + sz.y);
             };
-
-            // ------------------------------------------------------- a4: online softmax
-            {
-                float smax = lane < ntok ? vsz_s[lane].x : 0.f;
-                smax = warp_max_redux(smax);
-                int E_new = E_cur;
-                if (smax > 0.f) E_new = max(E_cur, ilog2f(smax) + 1);
-                const float pe = pow2i(-E_new);
-                if (sw < HG) {
-                    const int g = sw, j = lane;
-                    const bool valid = j < ntok;
-                    const float *rd = red + b * KW * HG * 32;
-                    float s = 0.f;
-#pragma unroll
-                    for (int w = 0; w < KW; ++w) s += rd[(w * HG + g) * 32 + j];
-                    int *kf = kfix + (b * HG + g) * 32 + j;
-                    s = s * lut_inv[g] + (float)(*kf) * (1.f / kKfixScale);
-                    *kf = 0;
-                    s = valid ? s : -CUDART_INF_F;
-                    const float m_new = fmaxf(m_run, warp_max_redux(s));
-                    const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
-                    const float p = valid ? exp2f(s - m_new) : 0.f;
-                    const float2 sz = valid ? vsz_s[j] : make_float2(0.f, 0.f);
-                    l_lane = l_lane * alpha + p;
-                    z_lane = z_lane * alpha + p * sz.y;
-                    m_run = m_new;
-                    p_s[g * 32 + j] = p;
-                    w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * (sz.x * pe)));
-                    if (lane == 0) beta_s[g] = alpha * pow2i(E_cur - E_new);
-                } else {
-                    // meanwhile: the tile's Value-outlier deltas and their max |delta|
-                    const int nvi = hdr[1];
-                    float mx = 0.f;
-                    for (int x = stid - HG * 32; x < nvi; x += ST - HG * 32) {
-                        const uint32_t itm = vit[x];
-                        const float delta = v_delta((int)((itm >> 11) & 31u), (int)(itm & 0x7ffu), (uint16_t)(itm >> 16));
-                        vdel[x] = delta;
-                        mx = fmaxf(mx, fabsf(delta));
-                    }
-                    if (hdr[3]) {
-                        // overflowed bucket: bound over this tile's CSR rows (rare)
-                        for (int r = stid - HG * 32; r < ntok * kv; r += ST - HG * 32) {
-                            const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
-                            const int ch = (int)(rec & 0xffffu);
-                            if (ch < c_lo || ch >= c_hi) continue;
-                            mx = fmaxf(mx, fabsf(v_delta(r / kv, ch - c_lo, (uint16_t)(rec >> 16))));
-                        }
-                    }
-                    mx = warp_max_redux(mx);
-                    if (lane == 0 && mx > 0.f) atomicMax(vmax + b, __float_as_int(mx));
-                }
-                E_prev = E_cur;
-                E_cur = E_new;
+            auto mine = [&](int chl) { return (chl >> 7) == vkv && (((chl & 127) >> 4) - mt0) >= 0 && (((chl & 127) >> 4) - mt0) < MTW; };
+            float mx = 0.f;
+            for (int x = lane; x < nvi; x += 32) {
+                const uint32_t itm = vit[x];
+                const int chl = (int)(itm & 0x7ffu);
+                if (mine(chl)) mx = fmaxf(mx, fabsf(v_delta((int)((itm >> 11) & 31u), chl, (uint16_t)(itm >> 16))));
             }
-            // anchors of tile it+2 (ring slot free: K warps are at tiles it+1 / it+2 at most
-            // once they see this tile's release below)
-            if (stid < 64 && it + 2 < ntl) {
-                const int i = stid;
-                const double2 a = anc64[((it + 1) % NANC) * 64 + i], r = rot32[i];
-                const double2 n = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
-                anc64[((it + 2) % NANC) * 64 + i] = n;
-                anc32[((it + 2) % NANC) * 64 + i] = make_float2((float)n.x, (float)n.y);
-            }
-            if (P.timers && blockIdx.x == 0 && lane == 0 && it < 100 && (sw == 0 || sw == 4 || sw == SW - 1))
-                P.timers[16 + it * 32 + 24 + (sw == 0 ? 0 : sw == 4 ? 1 : 2)] = clock64();
-            if (P.timers && blockIdx.x == 0 && lane == 0 && it < 100 && sw == SW - 1)
-                P.timers[16 + it * 32 + 27] = tc1;   // (sfull passed)
-            bar_sync(BAR_SV, ST);
-            if (stid == 0) mbar_arrive(sempty + b);   // K may refill buffer b (tile it+2)
-            tc1 = clock64(); tm[5] += tc1 - tc0; tc0 = tc1;
-            if (P.timers && blockIdx.x == 0 && stid == 0 && it < 100) P.timers[16 + it * 32 + 17] = tc1;
-
-            // -------------------------------------------------------- a5: P.V dense
-            {
-                // previous tile's Value-outlier sums (units 2^-E_prev), then the rescale
-                if (it > 0) fold_vfix(b ^ 1, vinv[b ^ 1] * pow2i(-E_prev));
-                if (stid == 0) vmax[b ^ 1] = 0;
-                const float b_lo = beta_s[vq_lo], b_hi = beta_s[vq_hi];
-                if (b_lo != 1.f || b_hi != 1.f) {
-#pragma unroll
-                    for (int x = 0; x < MTW; ++x) {
-                        dacc[x][0] *= b_lo; dacc[x][1] *= b_hi;
-                        dacc[x][2] *= b_lo; dacc[x][3] *= b_hi;
-                    }
-                }
-                uint32_t vr[NWV + 1];
-#pragma unroll
-                for (int x = 0; x < NWV; ++x) vr[x] = vw_s[(vkv * 4 * BITS + vw0 + x) * 32 + lane];
-                vr[NWV] = 0u;
-                if (BITS == 3 && MTW == 1 && voff) { vr[0] = __funnelshift_r(vr[0], vr[1], 16); vr[1] >>= 16; }
-                // B fragments (weights of query head vkv*G + g for tokens 16s + 2t.. / +8..)
-                uint32_t bw[2][2];
-#pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) {
-                    const uint32_t *w32 = reinterpret_cast<const uint32_t *>(w16 + (vkv * G + (vg < G ? vg : 0)) * 32 + 16 * s2 + 2 * vt);
-                    bw[s2][0] = vg < G ? w32[0] : 0u;
-                    bw[s2][1] = vg < G ? w32[4] : 0u;
-                }
-#pragma unroll
-                for (int ml = 0; ml < MTW; ++ml) {
-#pragma unroll
-                    for (int s2 = 0; s2 < 2; ++s2) {
-                        uint32_t a[4];
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const int bit = ((ml * 2 + s2) * 4 + r) * FB;
-                            const int wi = bit >> 5, sh = bit & 31;
-                            // (field & (NE-1)) << 7 with one shift (funnel when it straddles)
-                            uint32_t off;
-                            if (sh + FB <= 32) off = sh >= 7 ? (vr[wi] >> (sh - 7)) : (vr[wi] << (7 - sh));
-                            else off = __funnelshift_r(vr[wi], vr[wi + 1], sh - 7);
-                            a[r] = lds_u32(vlut_base + (vlane4 | (off & ((NE - 1) << 7))));
-                        }
-                        mma_f16_f32(dacc[ml], a, bw[s2]);
-                    }
+            if (hdr[3]) {
+                for (int r = lane; r < ntok * kv; r += 32) {
+                    const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
+                    const int ch = (int)(rec & 0xffffu);
+                    if (ch < c_lo || ch >= c_hi || !mine(ch - c_lo)) continue;
+                    mx = fmaxf(mx, fabsf(v_delta(r / kv, ch - c_lo, (uint16_t)(rec >> 16))));
                 }
             }
-            // ---------------------------------------------------- a6: V outliers
-            {
-                // sum_n p_n delta_{n,c} in fixed point: |p delta| 2^(24-e) < 2^25 with
-                // 2^e <= max|delta| < 2^(e+1); <= 32 items per (head, channel) and tile
-                const int nvi = hdr[1];
-                const float mx = __int_as_float(vmax[b]);
-                const int emx = mx > 0.f ? ilog2f(mx) : 0;
+            mx = warp_max_redux(mx);
+            if (mx > 0.f) {
+                const int emx = ilog2f(mx);
                 const float S = pow2i(24 - emx);
-                if (stid == 0) vinv[b] = pow2i(emx - 24);
-                int *vf = vfix + b * HG * kHeadDim;
-                for (int x = stid; x < nvi; x += ST) {
+                int *vf = Q.vfix;
+                for (int x = lane; x < nvi; x += 32) {
                     const uint32_t itm = vit[x];
-                    const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
-                    const int kvl = chl >> 7, cc = chl & 127;
-                    const float dS = vdel[x] * S;
+                    const int chl = (int)(itm & 0x7ffu);
+                    if (!mine(chl)) continue;
+                    const int j = (int)((itm >> 11) & 31u), cc = chl & 127;
+                    const float dS = v_delta(j, chl, (uint16_t)(itm >> 16)) * S;
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
-                        const int g = kvl * G + gg;
-                        atomicAdd(&vf[g * kHeadDim + cc], __float2int_rn(p_s[g * 32 + j] * dS));
+                        const int g = vkv * G + gg;
+                        atomicAdd(&vf[g * kHeadDim + cc], __float2int_rn(Q.p_s[g * 32 + j] * dS));
                     }
                 }
                 if (hdr[3]) {
-                    for (int r = stid; r < ntok * kv; r += ST) {
+                    for (int r = lane; r < ntok * kv; r += 32) {
                         const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
                         const int ch = (int)(rec & 0xffffu);
-                        if (ch < c_lo || ch >= c_hi) continue;
-                        const int j = r / kv, chl = ch - c_lo;
-                        const int kvl = chl >> 7, cc = chl & 127;
+                        if (ch < c_lo || ch >= c_hi || !mine(ch - c_lo)) continue;
+                        const int j = r / kv, chl = ch - c_lo, cc = chl & 127;
                         const float dS = v_delta(j, chl, (uint16_t)(rec >> 16)) * S;
 #pragma unroll
                         for (int gg = 0; gg < G; ++gg) {
-                            const int g = kvl * G + gg;
-                            atomicAdd(&vf[g * kHeadDim + cc], __float2int_rn(p_s[g * 32 + j] * dS));
+                            const int g = vkv * G + gg;
+                            atomicAdd(&vf[g * kHeadDim + cc], __float2int_rn(Q.p_s[g * 32 + j] * dS));
+                        }
+                    }
+                }
+                __syncwarp();
+                // fold into the accumulators of the owner lanes (units 2^-E_cur) and clear
+                const float unit = pow2i(emx - 24) * pow2i(-E_cur);
+#pragma unroll
+                for (int ml = 0; ml < MTW; ++ml) {
+                    const int ch = (mt0 + ml) * 16 + vg;
+#pragma unroll
+                    for (int cl = 0; cl < 2; ++cl) {
+                        if (2 * vt + cl < G) {
+                            int *pv = vf + (vkv * G + 2 * vt + cl) * kHeadDim + ch;
+                            dacc[ml][cl] += (float)pv[0] * unit;
+                            dacc[ml][2 + cl] += (float)pv[8] * unit;
+                            pv[0] = 0;
+                            pv[8] = 0;
                         }
                     }
                 }
             }
-            bar_sync(BAR_SV, ST);   // tile it done: vfix[b] complete, p_s / w16 free
-            if (stid == 0) mbar_arrive(empty_b + st);   // ring slot back to the TMA issuer
-            tc1 = clock64(); tm[6] += tc1 - tc0; tc0 = tc1;
-            if (P.timers && blockIdx.x == 0 && stid == 0 && it < 100) P.timers[16 + it * 32 + 18] = tc1;
+            (void)E_prev;
         }
-        // last tile's Value-outlier sums, then the accumulators to shared memory
-        if (ntl > 0) fold_vfix((ntl - 1) & 1, vinv[(ntl - 1) & 1] * pow2i(-E_cur));
-        {
-            const float sc = pow2i(E_cur);
+        tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
+    }
+    // accumulators -> per-quad results (the ring is free once every quad is done)
+    __syncthreads();
+    float *osp = reinterpret_cast<float *>(smem_raw + P.st_base) + q * HG * kHeadDim;   // [NQ][HG][128]
+    {
+        const float sc = pow2i(E_cur);
 #pragma unroll
-            for (int ml = 0; ml < MTW; ++ml) {
-                const int ch = (mt0 + ml) * 16 + vg;
+        for (int ml = 0; ml < MTW; ++ml) {
+            const int ch = (mt0 + ml) * 16 + vg;
 #pragma unroll
-                for (int cl = 0; cl < 2; ++cl) {
-                    if (2 * vt + cl < G) {
-                        float *o = osp + (vkv * G + 2 * vt + cl) * kHeadDim + ch;
-                        o[0] = dacc[ml][cl] * sc;
-                        o[8] = dacc[ml][2 + cl] * sc;
-                    }
+            for (int cl = 0; cl < 2; ++cl) {
+                if (2 * vt + cl < G) {
+                    float *o = osp + (vkv * G + 2 * vt + cl) * kHeadDim + ch;
+                    o[0] = dacc[ml][cl] * sc;
+                    o[8] = dacc[ml][2 + cl] * sc;
                 }
             }
         }
-        if (sw < HG) {
-            const float l = warp_sum(l_lane), z = warp_sum(z_lane);
-            if (lane == 0) { m_fin[sw] = m_run; l_fin[sw] = l; z_fin[sw] = z; }
-        }
-        if (P.timers && stid == 0) {
-            atomicAdd(P.timers + 4, tm[4]);
-            atomicAdd(P.timers + 9, tm[5]);
-            atomicAdd(P.timers + 10, tm[6]);
-            // wall-clock spread across CTAs: first start, last loop end, longest CTA loop
-            atomicMax(P.timers + 6, ~ns_kernel0);
-            const unsigned long long ns1 = gtimer_ns();
-            atomicMax(P.timers + 7, ns1);
-            atomicMax(P.timers + 8, ns1 - ns_kernel0);
-        }
+    }
+    if (w < HG) {
+        const float l = warp_sum(l_lane), z = warp_sum(z_lane);
+        if (lane == 0) { Q.m_fin[w] = m_run; Q.l_fin[w] = l; Q.z_fin[w] = z; }
+    }
+    if (P.timers && qtid == 0) {
+#pragma unroll
+        for (int x = 0; x < 5; ++x) atomicAdd(P.timers + x, tm[x]);
+        atomicAdd(P.timers + 5, (unsigned long long)nqt);
+        atomicAdd(P.timers + 6, tm[5]);
     }
     __syncthreads();
 
-    // ----------------------------------------------------------------- write partial
+    // ------------------------------------------------------ write partial (merge quads)
     float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
     for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
         const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
-        const bool used = ntl > 0 && l_fin[g] != 0.f;
-        const float m = used ? m_fin[g] : -CUDART_INF_F;
-        const float l = used ? l_fin[g] : 0.f;
-        const float o = (used && ch < kHeadDim) ? osp[g * kHeadDim + ch] + z_fin[g] : 0.f;
+        float m = -CUDART_INF_F;
+        for (int qq = 0; qq < NQ; ++qq) {
+            const Quad Qq = quad_at(qq);
+            if (ntl > qq && Qq.l_fin[g] != 0.f) m = fmaxf(m, Qq.m_fin[g]);
+        }
+        float l = 0.f, o = 0.f;
+        for (int qq = 0; qq < NQ; ++qq) {
+            const Quad Qq = quad_at(qq);
+            if (ntl <= qq || Qq.l_fin[g] == 0.f) continue;
+            const float wq = exp2f(Qq.m_fin[g] - m);
+            l += wq * Qq.l_fin[g];
+            if (ch < kHeadDim) {
+                const float *oq = reinterpret_cast<const float *>(smem_raw + P.st_base) + qq * HG * kHeadDim;
+                o += wq * (oq[g * kHeadDim + ch] + Qq.z_fin[g]);
+            }
+        }
         part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
     }
     // ------------------------------------------------------- a7: split merge
@@ -955,6 +928,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     if (tid == 0) P.tickets[hg] = 0;
 }
 
+
+
 __global__ void merge_kernel(const float *__restrict__ parts, int Pn, int H, int d, float *o) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= H * d) return;
@@ -979,26 +954,29 @@ size_t layout(const DevCache &c, Params &P) {
     using C = Cfg<BITS, HG>;
     const int HKV = HG / c.G;
     const size_t qwc = (size_t)HKV * 4 * BITS;
+    // outlier items a ring slot holds: ~2x the expected count (the bucket capacity is ~3x);
+    // a tile with more uses the CSC / CSR fallback
+    P.scap_k = (int)std::min<int64_t>(c.kcap_g, std::max<int64_t>(128, ((int64_t)c.kcap_g * 2 / 3 + 3) & ~3LL));
+    P.scap_v = (int)std::min<int64_t>(c.vcap_g, std::max<int64_t>(128, ((int64_t)c.vcap_g * 2 / 3 + 3) & ~3LL));
     size_t off = 0;
-    P.so_kw = (unsigned)off; off = align128(off + 32 * qwc * 4);
-    P.so_vw = (unsigned)off; off = align128(off + 32 * qwc * 4);
-    P.so_vsz = (unsigned)off; off = align128(off + 256);
-    P.so_hdr = (unsigned)off; off = align128(off + 16);
-    P.so_kit = (unsigned)off; off = align128(off + (size_t)c.kcap_g * 4);
-    P.so_vit = (unsigned)off; off = align128(off + (size_t)c.vcap_g * 4);
-    const size_t stb = off;
-    // Value-outlier deltas of the tile in flight, then the mbarriers and the stage ring
-    const size_t vdel = align128((size_t)c.vcap_g * 4);
-    P.so_vdel = (unsigned)align128(C::fixed);
-    const size_t base = align128(P.so_vdel + vdel + 128);
+    P.so_kw = (unsigned)off; off += 32 * qwc * 4;
+    P.so_vw = (unsigned)off; off += 32 * qwc * 4;
+    P.so_vsz = (unsigned)off; off += 256;
+    P.so_kit = (unsigned)off; off += (size_t)P.scap_k * 4;
+    P.so_vit = (unsigned)off; off += (size_t)P.scap_v * 4;
+    const size_t stb = align128(off);
+    const size_t base = align128(align128(C::fixed) + 128);   // + mbarriers
     P.st_base = (unsigned)base;
     const size_t limit = 227 * 1024;
-    for (int stages = 6; stages >= 2; --stages) {
-        const size_t total = base + stages * stb;
-        if (total <= limit) {
-            P.stages = stages;
+    // 2..3 private slots per quad; the ring also holds the prologue's scratch and the final
+    // per-quad results
+    const size_t need = std::max<size_t>(C::t1 + 64 * 16 + HG * 64 * 5, (size_t)NQ * HG * kHeadDim * 4);
+    for (int spq = 3; spq >= 2; --spq) {
+        const size_t ring = std::max(NQ * spq * stb, need);
+        if (base + ring <= limit) {
+            P.spq = spq;
             P.st_bytes = (unsigned)stb;
-            return total;
+            return base + ring;
         }
     }
     return 0;
@@ -1009,8 +987,8 @@ cudaError_t launch_t(const DevCache &c, Params &P, int grid, cudaStream_t s) {
     const size_t smem = layout<BITS, HG>(c, P);
     if (smem == 0) return cudaErrorInvalidConfiguration;
     static bool dbg = getenv("KVQ_DEBUG_LAYOUT") != nullptr;
-    if (dbg) fprintf(stderr, "att_kernel<%d,%d,%d>: smem %zu fixed %zu stages %d stage %u kcap_g %d vcap_g %d\n",
-                     BITS, HG, G, smem, Cfg<BITS, HG>::fixed, P.stages, P.st_bytes, c.kcap_g, c.vcap_g);
+    if (dbg) fprintf(stderr, "att_kernel<%d,%d,%d>: smem %zu fixed %zu slots/quad %d slot %u scap %d/%d\n",
+                     BITS, HG, G, smem, Cfg<BITS, HG>::fixed, P.spq, P.st_bytes, P.scap_k, P.scap_v);
     cudaError_t e = cudaFuncSetAttribute(att_kernel<BITS, HG, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1041,7 +1019,8 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
 }  // namespace
 
 int attend_heads_per_cta(int bits, int H_q, int G) {
-    const int cap = bits == 4 ? 1 : 4;   // K tables: HG * 64 * 4^b * 4 bytes of shared memory
+    // shared memory: K tables HG * 64 * 4^b * 4 bytes + 4 quads x 2-3 private ring slots
+    const int cap = bits == 4 ? 1 : (G >= 4 ? 4 : 2);
     for (int hg = cap; hg >= 1; hg >>= 1)
         if (H_q % hg == 0 && hg % G == 0) return hg;
     return 0;

@@ -39,28 +39,7 @@ tm = c.phase_timers()
 tiles = tm[5]
 ctas = c.info()["splits"] * (w.H_q // c.info()["heads_per_cta"])
 print(f"{wname} T={T} attend {e0.elapsed_time(e1) / 5 * 1e3:.1f} us, info {c.info()}")
-per = lambda i: round(tm[i] / tiles, 1)
-print(f"cycles per tile  K group: tma_wait {per(1)} empty_wait {per(2)} work {per(3)}   "
-      f"SV group: full_wait {per(4)} softmax {per(9)} PV {per(10)}")
-print(f"prologue cycles per CTA: {tm[0] / (5 * ctas):.0f}")
-# one more launch alone for the wall-clock spread across CTAs
-c.attend(q, T, o)
-torch.cuda.synchronize()
-import ctypes
-buf = (ctypes.c_uint64 * 4096)()
-kvq._lib.kvq_debug_trace(c._h, buf, 4096)
-tm = c.phase_timers()
-first_start = (~tm[6]) & 0xFFFFFFFFFFFFFFFF
-print(f"last launch: first CTA start -> last CTA loop end {(tm[7] - first_start) / 1e3:.1f} us; "
-      f"longest CTA start->loop end {tm[8] / 1e3:.1f} us")
-# per-tile event trace of CTA 0 (last launch)
-if True:
-    raw = np.array(buf, dtype=np.uint64).astype(np.int64)
-    tr = raw[:3200].reshape(100, 32)
-    t0 = tr[0, 0]
-    print("tile: K warp starts | K warp ends | SV full softmax pv   (cycles since K start[0])")
-    for i in range(0, 10):
-        r = tr[i] - t0
-        print(i, "K start", r[0:8].tolist(), "end", r[8:16].tolist(), "SV", r[16:19].tolist(), "issue(entry,empty,expect,copies,sync)", r[19:24].tolist(), "SV warps 0/4/7 pre-bar", r[24:27].tolist())
-    print("per K warp work / wait per tile (last launch):", [round(int(raw[4000 + k]) / (tm[5] or 1)) for k in range(8)],
-          [round(int(raw[4010 + k]) / (tm[5] or 1)) for k in range(8)])
+per = lambda i: round(tm[i] / max(tiles, 1), 1)
+print(f"cycles per quad-tile (quad warp 0): load_issue {per(6)} load_wait {per(1)} K {per(2)} barrier {per(3)} softmax+PV {per(4)}"
+      f"  -> per CTA tile {round(sum(tm[1:5]) / max(tiles, 1) / 4, 1)}")
+print(f"prologue cycles per CTA: {tm[0] / (5 * ctas * 4):.0f}")
