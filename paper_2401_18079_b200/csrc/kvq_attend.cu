@@ -1,22 +1,21 @@
 // kvq_attend.cu -- ATT: fused single-token decode attention over the compressed cache.
 //
 // One launch per attend.  grid = n_head_groups x splits (head group
-// fastest), one CTA per SM, each CTA a contiguous range of 32-token tiles of one group of
-// HG query heads.  The CTA's 16 warps form four independent quads; quad q takes the tiles
-// q, q+4, q+8, ... of the range, so four tiles are in flight and a quad only ever waits for
-// its own four warps (one named barrier per tile):
-//   load   at the top of a tile the quad's 128 threads cp.async (16 B each) its next tile --
-//          K/V code words, per-token (s,z), outlier items of this head group -- into a
-//          shared ring slot; completion arrives on the slot's mbarrier.
-//   a2+a3  K: warp w of the quad takes RoPE pairs 16w..16w+15 of every head (lane = token):
-//          pair-table lookups (fp16 x fp16 -> fp32), Key-outlier and heavy-pair terms in fp32
-//          summed in fixed point with shared integer atomics.  -> quad barrier
-//   a4     online softmax in base 2, warp w = head w (4 partial sums per token);
-//   a5+a6  P.V on the tensor cores (mma.m16n8k16: A = Value codes through a pair table,
-//          B = fp16 weights p s 2^-E, warp w = KV head w for MHA), Value-outlier terms in
-//          fixed point folded into the accumulators.
-//   a7     the quads' partials are merged, then the last CTA of each head group merges the
-//          split partials (log-sum-exp, ticket counter).
+// fastest), one CTA per SM, warp specialized:
+//   warp 16 (producer)  TMA bulk copies (cp.async.bulk + mbarrier complete_tx) of every
+//                       32-token tile of the CTA's head group -- K code words, V code words,
+//                       per-token (s,z), CSC pointers, Value and Key outlier records -- into a
+//                       STAGES-deep shared-memory ring; then compacts the tile's Key-outlier
+//                       records of this head group into a self-contained item list.
+//   warp 17 (producer)  compacts the tile's Value-outlier records of this head group.
+//   warps 0..15         compute, synchronized among themselves with a named barrier:
+//     a2+a3  K phase: RoPE-pair table lookups (lane = token, warp = 4 RoPE pairs, all
+//            heads of the group; fp16 x fp16 -> fp32 FMAs), Key-outlier and heavy-pair
+//            corrections in fp32 (flat over the item list, shared atomics);
+//     a4     online softmax in base 2 (warp g = head g; per-lane deferred sums);
+//     a5+a6  P.V: lane = CPL channels, sum_n (p_n s_n) Chat_V[code] + sum_n p_n z_n
+//            (affine fold), Value-outlier corrections flat over the item list;
+//     a7     the last CTA of each head group merges the split partials (log-sum-exp).
 //   Tables (built per CTA, a1): q~ = RoPE(q, pos) with exact fp64 angles (R11, R12) times
 //   log2(e)/sqrt(d); per (query head g, RoPE pair i) a 2^{2b}-entry table of fp16 pairs
 //   (A, B), A = q~_i K^_i(a) + q~_i' K^_i'(b), B = q~_i' K^_i(a) - q~_i K^_i'(b) with
@@ -24,23 +23,21 @@
 //   and the affine folded in, so one lookup + 2 FMAs give cos(n' th_i) A + sin(n' th_i) B,
 //   exactly the pair's share of q~ . RoPE(K^_n, n') (RoPE after dequantization, P:379,
 //   P:730).  Pairs carrying a heavy Key channel use fp32 tables.  V: the
-//   shared codebook as a table of (Chat[a], Chat[b]) fp16 pairs, one copy per lane.
+//   shared codebook as a pair table, one private copy per lane (conflict free).
 #include "kvq_internal.cuh"
 
 #include <math_constants.h>
-#include <algorithm>
-#include <cstdio>
-#include <cstdlib>
 
 namespace kvq {
 namespace {
 
-constexpr int NQ = 4;                         // quads: independent 4-warp pipelines
-constexpr int QWARPS = 4;                     // warps per quad
-constexpr int QT = QWARPS * 32;               // threads per quad
-constexpr int ATT_THREADS = NQ * QT;          // 16 warps: 4 per SM sub-partition
-constexpr int KPW = kPairs / QWARPS;          // RoPE pairs per warp in the K phase (16)
-constexpr int NANC = 3;                       // per-quad ring of tile anchors (written 2 ahead)
+constexpr int NHALF = 2;                      // independent compute halves (alternate tiles)
+constexpr int HW = 8;                         // warps per half
+constexpr int HT = HW * 32;                   // threads per half
+constexpr int NCW = NHALF * HW;               // compute warps
+constexpr int NCT = NCW * 32;                 // compute threads
+constexpr int ATT_THREADS = NCT;              // 16 warps: 4 per SM sub-partition
+constexpr int KPW = kPairs / HW;              // RoPE pairs per warp in the K phase
 
 // ------------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -80,18 +77,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-// 16-byte cp.async (LDGSTS, L2 only) and the mbarrier arrival fired by its completion
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void bar_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+// named barrier among the warps of one compute half (ids 1, 2; the producer never joins)
+__device__ __forceinline__ void half_sync(int half) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "n"(HT) : "memory");
 }
 
 // acc += lo(x)*lo(y) ; acc2 += hi(x)*hi(y)   (fp16 products, fp32 accumulation)
@@ -168,26 +156,26 @@ __device__ __forceinline__ float warp_max_redux(float v) {
 template <int BITS, int HG>
 struct Cfg {
     static constexpr int NE = 1 << (2 * BITS);
-    static constexpr int HMAX = 4;                   // fp32 "heavy" pairs per head
+    static constexpr int HMAX = BITS == 4 ? 4 : 8;   // fp32 "heavy" pairs per head
     static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
     static constexpr size_t vlut = (size_t)NE * 32 * 4;
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
-    static constexpr size_t t1 = (size_t)kPairs * 32 * 8;       // prologue only (in the ring)
-    // per quad: red[2], kfix[2], p, w16, vfix, anchors[NANC], beta/m/l/z
-    static constexpr size_t quad =
-        2 * QWARPS * HG * 32 * 4 + 2 * HG * 32 * 4 + HG * 32 * 4 + HG * 32 * 2 + HG * kHeadDim * 4
-        + NANC * 64 * 8 + HG * 4 * 4 + 64;
+    static constexpr size_t t1 = (size_t)kPairs * 32 * 8;
+    // per compute half: red, p, kcorr, hcorr, kbeg/kend, w16, osp, anchors, scalars
+    static constexpr size_t half_bytes =
+        HW * HG * 32 * 4 + HG * 32 * 4 * 3 + HG * 64 * 4 + HG * 32 * 2 + HG * kHeadDim * 4 * 2
+        + 64 * 16 + 64 * 8 + HG * 4 * 4 + 16 + 64;
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
-        + NQ * quad
-        + 64 * 16                      /* rot128 */
-        + 64 * 5 * 8                   /* cis(2^k theta_i) */
-        + HG * 4 * 2                   /* lut scale / inverse */
+        + NHALF * half_bytes
+        + 64 * 16 * 2                  /* rot64, qcis */
+        + 64 * 4                       /* theta32 */
+        + HG * 4 * 8                   /* per-head scalars */
+        + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
         + HG * 24 * 4                  /* heavy pair list, counts, flat list */
         + HG * kHeadDim * 4 * 2 + 64 * 4 /* staged s_c, z_c of the group, codebooks */
-        + 16 * 4 + 16 * 16             /* flags, slot headers */
-        + 512;
-    static constexpr size_t fixed = klut + vlut + hlut + small;
+        + 256;
+    static constexpr size_t fixed = klut + vlut + hlut + t1 + small;
 };
 
 struct Params {
@@ -199,10 +187,11 @@ struct Params {
     float *parts;
     unsigned *tickets;
     int write_partial;
-    // ring layout (bytes), computed on the host
-    int spq, scap_k, scap_v;      // ring slots per quad; outlier items a slot holds (mult. of 4)
-    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit;
-    unsigned long long *timers;   // optional diagnostics, may be null
+    // stage ring layout (bytes), computed on the host
+    int stages;
+    int krec_cap;        // u32 records per stage buffer (multiple of 4)
+    unsigned st_base, st_bytes, so_kw, so_vw, so_vsz, so_kit, so_vit, so_hdr, so_vdel;
+    unsigned long long *timers;   // optional [8] phase cycle sums (diagnostics), may be null
 };
 
 template <int BITS, int HG, int G>
@@ -213,37 +202,71 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     constexpr int HKV = HG / G;
     constexpr int QWC = HKV * 4 * BITS;             // K (and V) words per token in the CTA
     constexpr int HMAX = C::HMAX;
-    constexpr int KWW = 2 * BITS * KPW / 32;        // K code words of a warp's pairs (per head)
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *sp = smem_raw;
     uint32_t *klut = reinterpret_cast<uint32_t *>(sp); sp += C::klut;
     uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
     float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
+    float2 *t1tab = reinterpret_cast<float2 *>(sp); sp += C::t1;   // cis(j theta_i) [i][j]
     float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
-    unsigned char *quad_base = sp; sp += NQ * C::quad;
-    double2 *rot128 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;   // rotation by 128 theta
-    float2 *cisp = reinterpret_cast<float2 *>(sp); sp += 64 * 5 * 8;   // cis(2^k theta_i) [i][k]
+    // per compute half h (alternate tiles): scratch of its own tile, at sp + h*half_bytes
+    struct Half {
+        float *red, *p_s, *osp, *beta_s, *m_fin, *l_fin, *z_fin;
+        int *kfix;              // [HG][32] Key-outlier + heavy-pair score terms, fixed point
+        int *vfix;              // [HG][128] Value-outlier sums of the tile, fixed point
+        int *vmax;              // [0] max |delta| of the tile's Value items (float bits)
+        float *vscale;          // [0] fixed-point scale of the tile's V items
+        float *vdel;            // [vcap_g] delta of each Value item of the tile
+        uint16_t *w16;
+        double2 *anc64;
+        float2 *anc32;
+    };
+    unsigned char *const half_base = sp;
+    auto half_at = [&](int h) -> Half {
+        Half H;
+        unsigned char *q = half_base + h * C::half_bytes;
+        H.red = reinterpret_cast<float *>(q); q += HW * HG * 32 * 4;
+        H.p_s = reinterpret_cast<float *>(q); q += HG * 32 * 4;
+        H.kfix = reinterpret_cast<int *>(q); q += HG * 32 * 4;
+        q += HG * 32 * 4;
+        q += HG * 64 * 4;
+        H.w16 = reinterpret_cast<uint16_t *>(q); q += HG * 32 * 2;
+        H.osp = reinterpret_cast<float *>(q); q += HG * kHeadDim * 4;
+        H.vfix = reinterpret_cast<int *>(q); q += HG * kHeadDim * 4;
+        q += (16 - ((HG * 32 * 2) % 16)) % 16;
+        H.anc64 = reinterpret_cast<double2 *>(q); q += 64 * 16;
+        H.anc32 = reinterpret_cast<float2 *>(q); q += 64 * 8;
+        H.beta_s = reinterpret_cast<float *>(q); q += HG * 4;
+        H.m_fin = reinterpret_cast<float *>(q); q += HG * 4;
+        H.l_fin = reinterpret_cast<float *>(q); q += HG * 4;
+        H.z_fin = reinterpret_cast<float *>(q); q += HG * 4;
+        H.vmax = reinterpret_cast<int *>(q); q += 4;
+        H.vscale = reinterpret_cast<float *>(q); q += 4;
+        H.vdel = reinterpret_cast<float *>(smem_raw + P.so_vdel) + h * c.vcap_g;
+        return H;
+    };
+    sp += NHALF * C::half_bytes;
+    double2 *rot64 = reinterpret_cast<double2 *>(sp); sp += 64 * 16;   // rotation by 64 theta
+    double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    float *theta32 = reinterpret_cast<float *>(sp); sp += 64 * 4;
     float *lut_inv = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *lut_sc = reinterpret_cast<float *>(sp); sp += HG * 4;
+    float *bound_s = reinterpret_cast<float *>(sp); sp += HG * 64 * 4;
+    uint8_t *heavy_s = reinterpret_cast<uint8_t *>(sp); sp += HG * 64;
     int *hv_pair = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
     int *hv_n = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
     int *hv_combo = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;   // flat (head, slot) list
     float *ks_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;   // s_c of the group
     float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
-    int *flag_s = reinterpret_cast<int *>(sp); sp += 16 * 4;
-    int *hdr_s = reinterpret_cast<int *>(sp); sp += 16 * 16;               // per ring slot
-    // mbarriers just below the ring: full[slot] (the cp.async of a tile have landed)
+    int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
+    // barriers just below the stage ring: full[S], empty[S]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
-    uint64_t *full_b = bars;   // [NQ * SPQ]
-    // prologue-only scratch in the (not yet used) ring
-    float2 *t1tab = reinterpret_cast<float2 *>(smem_raw + P.st_base);
-    double2 *qcis = reinterpret_cast<double2 *>(smem_raw + P.st_base + C::t1);
-    float *bound_s = reinterpret_cast<float *>(smem_raw + P.st_base + C::t1 + 64 * 16);
-    uint8_t *heavy_s = reinterpret_cast<uint8_t *>(smem_raw + P.st_base + C::t1 + 64 * 16 + HG * 64 * 4);
+    uint64_t *full_b = bars;
 
     const long long t_kernel0 = clock64();
+    const unsigned long long ns_kernel0 = P.timers ? gtimer_ns() : 0ull;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
     const int hg = blockIdx.x % n_hg;
@@ -258,39 +281,13 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     const float *ks = c.kpar, *kz = c.kpar + D;
     const float *cbK = c.cb + 16, *cbV = c.cb + 48;   // decode codebooks
     const int c_lo = h0 * kHeadDim, c_hi = (h0 + HKV) * kHeadDim;
-    const int SPQ = P.spq;     // private ring slots per quad
 
-    // quad scratch
-    const int q = warp / QWARPS, w = warp % QWARPS, qtid = tid % QT;
-    struct Quad {
-        float *red;       // [2][QWARPS][HG][32] partial scores
-        int *kfix;        // [2][HG][32] Key-outlier + heavy-pair terms, fixed point
-        float *p_s;       // [HG][32]
-        uint16_t *w16;    // [HG][32] fp16 weights p s 2^-E
-        int *vfix;        // [HG][128] Value-outlier sums of the tile, fixed point
-        float2 *anc;      // [NANC][64] tile anchors cis(n0 theta_i)
-        float *beta, *m_fin, *l_fin, *z_fin;   // [HG]
-    };
-    auto quad_at = [&](int qq) -> Quad {
-        Quad Q;
-        unsigned char *p = quad_base + qq * C::quad;
-        Q.red = reinterpret_cast<float *>(p); p += 2 * QWARPS * HG * 32 * 4;
-        Q.kfix = reinterpret_cast<int *>(p); p += 2 * HG * 32 * 4;
-        Q.p_s = reinterpret_cast<float *>(p); p += HG * 32 * 4;
-        Q.vfix = reinterpret_cast<int *>(p); p += HG * kHeadDim * 4;
-        Q.anc = reinterpret_cast<float2 *>(p); p += NANC * 64 * 8;
-        Q.beta = reinterpret_cast<float *>(p); p += HG * 4;
-        Q.m_fin = reinterpret_cast<float *>(p); p += HG * 4;
-        Q.l_fin = reinterpret_cast<float *>(p); p += HG * 4;
-        Q.z_fin = reinterpret_cast<float *>(p); p += HG * 4;
-        Q.w16 = reinterpret_cast<uint16_t *>(p);
-        return Q;
-    };
-    const Quad Q = quad_at(q);
     auto stage_ptr = [&](int st) -> unsigned char * { return smem_raw + P.st_base + (size_t)st * P.st_bytes; };
 
     if (tid == 0) {
-        for (int s = 0; s < NQ * SPQ; ++s) mbar_init(full_b + s, 1);   // the expect_tx arrival
+        for (int s = 0; s < P.stages; ++s) {
+            mbar_init(full_b + s, 1);
+        }
         mbar_fence_init();
     }
 
@@ -298,18 +295,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     if (tid < 64) {
         const int i = tid;
         const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        theta32[i] = (float)th;
         double s, co;
         sincos((double)P.pos * th, &s, &co);
         qcis[i] = make_double2(co, s);
-        sincos((double)(NQ * kTileTokens) * th, &s, &co);
-        rot128[i] = make_double2(co, s);
-    }
-    for (int x = tid; x < kPairs * 5; x += ATT_THREADS) {
-        const int i = x / 5, k = x % 5;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
-        double s, co;
-        sincos((double)(1 << k) * th, &s, &co);
-        cisp[x] = make_float2((float)co, (float)s);
+        for (int h = 0; h < NHALF; ++h) {   // half h starts at tile t_begin + h
+            const double a0 = (double)(c.pos_base + (int64_t)(t_begin + h) * kTileTokens) * th;
+            sincos(a0, &s, &co);
+            half_at(h).anc64[i] = make_double2(co, s);
+            half_at(h).anc32[i] = make_float2((float)co, (float)s);
+        }
+        sincos((double)(NHALF * kTileTokens) * th, &s, &co);
+        rot64[i] = make_double2(co, s);
     }
     for (int x = tid; x < kPairs * 32; x += ATT_THREADS) {
         const int i = x >> 5, j = x & 31;
@@ -318,13 +315,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         sincos((double)j * th, &s, &co);
         t1tab[x] = make_float2((float)co, (float)s);
     }
-    for (int x = tid; x < NQ * HG * kHeadDim; x += ATT_THREADS) quad_at(x / (HG * kHeadDim)).vfix[x % (HG * kHeadDim)] = 0;
-    for (int x = tid; x < NQ * 2 * HG * 32; x += ATT_THREADS) quad_at(x / (2 * HG * 32)).kfix[x % (2 * HG * 32)] = 0;
+    for (int x = tid; x < NHALF * HG * kHeadDim; x += ATT_THREADS) {
+        const Half Hx = half_at(x / (HG * kHeadDim));
+        Hx.osp[x % (HG * kHeadDim)] = 0.f;
+        Hx.vfix[x % (HG * kHeadDim)] = 0;
+    }
+    if (tid < NHALF) { half_at(tid).vmax[0] = 0; half_at(tid).vscale[0] = 1.f; }
     for (int x = tid; x < HKV * kHeadDim; x += ATT_THREADS) {
         ks_s[x] = ks[c_lo + x];
         kz_s[x] = kz[c_lo + x];
     }
     if (tid < 64) cb_s[tid] = c.cb[tid];
+    for (int x = tid; x < NHALF * HG * 32; x += ATT_THREADS) half_at(x / (HG * 32)).kfix[x % (HG * 32)] = 0;
     if (tid < 16) flag_s[tid] = 0;
     __syncthreads();
     // a1: q~ = RoPE(q, pos) * log2(e)/sqrt(d)
@@ -415,482 +417,471 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const int e = x >> 5;
         vlut[x] = pack_half2(cbV[e & CM], cbV[e >> BITS]);
     }
-    // per-lane constants of the K phase: cis(j theta_i) for this warp's KPW pairs
-    float t1c[KPW], t1s[KPW];
-#pragma unroll
-    for (int k = 0; k < KPW; ++k) {
-        const float2 v = t1tab[(w * KPW + k) * 32 + lane];
-        t1c[k] = v.x;
-        t1s[k] = v.y;
-    }
-    // anchors of each quad's first two tiles; the fp64 running anchor of the next one stays in
-    // registers of the quad's warp 0 (pairs lane, lane + 32)
-    double2 amaster[2];
-    if (w == 0) {
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-            const int i = lane + 32 * h2;
-            const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
-            double s, co;
-            for (int a = 0; a < 2; ++a) {
-                const double a0 = (double)(c.pos_base + (int64_t)(t_begin + q + NQ * a) * kTileTokens) * th;
-                sincos(a0, &s, &co);
-                Q.anc[a * 64 + i] = make_float2((float)co, (float)s);
-            }
-            amaster[h2] = make_double2(co, s);
-        }
-    }
-    __syncthreads();   // tables ready; the ring (t1tab) is free from here on
-    const int n_combo = flag_s[2];
-    const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
-    unsigned long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    __syncthreads();
 
-    // ------------------------------------------------------- tile loads (cp.async)
-    // Quad q handles the CTA's tiles it = q + 4i and owns SPQ private ring slots: tile i goes
-    // to slot q*SPQ + i % SPQ, loaded with TMA bulk copies issued by the quad's warps,
-    // completion counted on the slot's mbarrier (complete_tx).  (16-byte cp.async from 128
-    // threads measured ~2000 cycles of issue per tile under the LDS load of the K phase.)  The
-    // slot's previous tile (i - SPQ) is free once every warp of the quad is past the quad
-    // barrier of tile i - SPQ + 1: tile i + 1 is loaded at the top of tile i when SPQ >= 3,
-    // right after the barrier of tile i when SPQ == 2.  Outlier counts are read one load
-    // ahead (registers).
-    const int nqt = ntl > q ? (ntl - q + NQ - 1) / NQ : 0;   // tiles of this quad
-    uint32_t nk_nx = 0, nv_nx = 0;     // counts of the quad's next tile to load
-    auto read_counts = [&](int it, uint32_t &nk, uint32_t &nv) {
-        nk = nv = 0;
-        if (it < ntl) {
-            const uint32_t *gc = c.gcnt + ((int64_t)(t_begin + it) * c.NG + hg) * 2;
+    // ====================================================== TMA issue (per half)
+    // Each half owns SH = stages/2 ring slots and issues its own tiles: tiles of half h are
+    // t_k = t_begin + h + 2k, slot k % SH.  The last warp of the half issues tile t_{k+SH-1}
+    // at the top of iteration k, into the slot its half released at the end of k-1.
+    auto issue = [&](int hh, int k) {   // called by one full warp
+        const int SH = P.stages / NHALF;
+        const int ti = t_begin + hh + NHALF * k;
+        if (ti >= t_end) return;
+        const int si = hh * SH + (k % SH);
+        unsigned char *sb = stage_ptr(si);
+        uint64_t *bar = full_b + si;
+        uint32_t nk = 0, nv = 0;
+        if (lane == 0) {
+            const uint32_t *gc = c.gcnt + ((int64_t)ti * c.NG + hg) * 2;
             nk = __ldg(gc);
             nv = __ldg(gc + 1);
         }
-    };
-    auto load_tile = [&](int ii, uint32_t nk, uint32_t nv) {   // quad iteration ii
-        if (ii >= nqt || lane != 0) return;
-        const int si = q * SPQ + ii % SPQ;
-        const int ti = t_begin + q + NQ * ii;
-        const bool kov = nk > (uint32_t)P.scap_k, vov = nv > (uint32_t)P.scap_v;
+        nk = __shfl_sync(0xffffffffu, nk, 0);
+        nv = __shfl_sync(0xffffffffu, nv, 0);
+        const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
         const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
         const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
-        const unsigned b_kw = QWC * 32u * 4u;
-        unsigned char *sb = stage_ptr(si);
-        uint64_t *bar = full_b + si;
-        const int64_t bucket = (int64_t)ti * c.NG + hg;
-        // TMA bulk copies, one or two per warp of the quad (an issue holds its warp for
-        // ~150 cycles); the expect_tx arrival (warp 0) publishes the header written before it
-        if (w == 0) {
-            int *hdr = hdr_s + si * 4;
+        const unsigned b_kw = 32u * QWC * 4u;
+        const unsigned total = 2u * b_kw + 256u + bk + bv;
+        if (lane == 0) {
+            int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
             hdr[0] = kov ? 0 : (int)nk;
             hdr[1] = vov ? 0 : (int)nv;
             hdr[2] = kov;
             hdr[3] = vov;
-            mbar_expect_tx(bar, 2u * b_kw + 256u + bk + bv);
-            bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
-        } else if (w == 1) {
-            bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
-        } else if (w == 2) {
-            bulk_g2s(sb + P.so_vsz, c.vsz + (int64_t)ti * 32, 256u, bar);
-            if (bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
-        } else {
-            if (bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
+            fence_proxy_async();
+            mbar_expect_tx(bar, total);
         }
-    };
-    if (nqt > 0) {
-        uint32_t nk0, nv0;
-        read_counts(q, nk0, nv0);
-        read_counts(q + NQ, nk_nx, nv_nx);
-        load_tile(0, nk0, nv0);
-    }
-    auto load_next = [&](int i) {   // tile i + 1 of the quad
-        const uint32_t nk = nk_nx, nv = nv_nx;
-        read_counts(q + NQ * (i + 2), nk_nx, nv_nx);
-        load_tile(i + 1, nk, nv);
+        __syncwarp();
+        const int64_t n0 = (int64_t)ti * 32;
+        const int64_t bucket = (int64_t)ti * c.NG + hg;
+        if (lane == 0)
+            bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
+        if (lane == 1)
+            bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
+        if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
+        if (lane == 3 && bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
+        if (lane == 4 && bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
     };
 
-    // V-phase mapping inside the quad (tensor cores, mma.m16n8k16): warp -> (local KV head
-    // vkv, m-tiles [mt0, mt0 + MTW) of 16 channels); A = V codes (rows = channels, k = tokens)
-    // through the pair table, B = fp16 weights (columns = the G query heads of vkv),
-    // D = fp32 P.V accumulators (columns >= G unused).
-    constexpr int WPK = QWARPS / HKV;           // warps per KV head
+    // =========================================================== compute warps
+    // Two independent halves of 8 warps process alternate tiles with their own scratch,
+    // softmax state and named barrier; they share the read-only tables and hide each
+    // other's latency.  Their partials are merged at the end.
+    const int half = warp / HW, hw = warp % HW, htid = tid % HT;
+    const int n_combo = flag_s[2];
+    const Half H = half_at(half < NHALF ? half : 0);
+    // V-phase task mapping inside a half (tensor cores, mma.m16n8k16): warp -> (local KV
+    // head vkv, m-tiles [mt0, mt0 + MTW) of 16 channels); A = V codes (rows = channels,
+    // k = tokens) through the pair table, B = fp16 weights (columns = the G query heads of
+    // vkv), D = fp32 P.V accumulators (columns >= G unused).
+    constexpr int WPK = HW / HKV;               // warps per KV head
     constexpr int MTW = 8 / WPK;                // m-tiles per warp
     constexpr int FB = 2 * BITS;                // bits per A field (2 tokens x 1 channel)
     constexpr int NWV = (MTW * 16 * BITS + 31) / 32;   // code words per lane per tile
-    constexpr bool SELF = (WPK == 1 && G == 1);        // warp w: softmax head w == V head w
-    static_assert(HKV <= QWARPS && QWARPS % HKV == 0 && G <= 8, "V task mapping");
-    const int vkv = w / WPK;
-    const int mt0 = (w % WPK) * MTW;
+    static_assert(HKV <= HW && HW % HKV == 0 && G <= 8, "V task mapping");
+    const int vkv = hw / WPK;                                // local KV head
+    const int mt0 = (hw % WPK) * MTW;
     const int vbit0 = mt0 * 16 * BITS;
     const int vw0 = vbit0 >> 5, voff = vbit0 & 31;           // voff = 16 only for b=3, MTW=1
     const int vg = lane >> 2, vt = lane & 3;
     const int vq_lo = vkv * G + min(2 * vt, G - 1), vq_hi = vkv * G + min(2 * vt + 1, G - 1);
-    const uint32_t vlut_base = smem_u32(vlut), vlane4 = 4u * lane;
-    // this warp's K tables: base | (pair code << 2), + a constant per (head, pair)
-    const uint32_t klut_w = smem_u32(klut) + (uint32_t)(w * KPW * NE * 4);
-    if (klut_w & (NE * 4u - 1u)) __trap();
     float dacc[MTW][4];
 #pragma unroll
     for (int x = 0; x < MTW; ++x) dacc[x][0] = dacc[x][1] = dacc[x][2] = dacc[x][3] = 0.f;
-    float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;   // softmax head w (w < HG)
-    int E_cur = -126;      // dense V accumulator units: 2^E (uniform in the quad)
-    long long tc0 = clock64(), tc1;
-    tm[0] = tc0 - t_kernel0;
+    // lookup address = vlut + ((code << 7) | (lane << 2)): the OR is exact, the base add
+    // folds into the load (uniform base register)
+    const uint32_t vlut_base = smem_u32(vlut), vlane4 = 4u * lane;
+    float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;
+    int E_cur = -126;     // dense V accumulator units: 2^E_cur (uniform in a half)
+    unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
 
-    for (int i = 0; i < nqt; ++i) {
-        const int it = q + NQ * i;
-        const int b = i & 1;
-        const int st = q * SPQ + i % SPQ;
-        if (SPQ >= 3) load_next(i);
-        tc1 = clock64(); tm[5] += tc1 - tc0; tc0 = tc1;
-        mbar_wait(full_b + st, (unsigned)((i / SPQ) & 1));
-        tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
-        unsigned char *sb = stage_ptr(st);
-        const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
-        const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
-        const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
-        const uint32_t *kit = reinterpret_cast<const uint32_t *>(sb + P.so_kit);
-        const uint32_t *vit = reinterpret_cast<const uint32_t *>(sb + P.so_vit);
-        const int *hdr = hdr_s + st * 4;
-        const int64_t n0 = (int64_t)(t_begin + it) * 32;
-        const int ntok = (int)min((int64_t)32, P.T - n0);
-        const float2 *an32 = Q.anc + (i % NANC) * 64;
-        int *kf = Q.kfix + b * HG * 32;
-
-        // cis((n0 + j) theta_i) = anchor_i * cis(j theta_i), the second factor as a product of
-        // the binary powers cis(2^k theta_i) (fp32 table) -- for items and heavy pairs
-        auto cis_tok = [&](int ii, int j) -> float2 {
-            float2 r = an32[ii];
+    if (warp < NCW) {
+        // per-lane constants for the K phase: cis(j * theta_i) for this warp's KPW pairs
+        float t1c[KPW], t1s[KPW];
 #pragma unroll
-            for (int k = 0; k < 5; ++k)
-                if ((j >> k) & 1) {
-                    const float2 p = cisp[ii * 5 + k];
-                    r = make_float2(r.x * p.x - r.y * p.y, r.x * p.y + r.y * p.x);
+        for (int k = 0; k < KPW; ++k) {
+            const float2 v = t1tab[(hw * KPW + k) * 32 + lane];
+            t1c[k] = v.x;
+            t1s[k] = v.y;
+        }
+        // this warp's K tables: base | (pair code << 2), + a constant per (head, pair); the
+        // base is a multiple of NE*4 bytes (dynamic shared memory is 1 KB aligned)
+        const uint32_t klut_w = smem_u32(klut) + (uint32_t)(hw * KPW * NE * 4);
+        if (klut_w & (NE * 4u - 1u)) __trap();
+        const int kbit0 = 2 * BITS * KPW * hw;
+        const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
+        const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
+        long long tc0 = clock64(), tc1;
+        tm[0] = tc0 - t_kernel0;   // prologue
+
+        const int SH = P.stages / NHALF;
+        if (hw == HW - 1)
+            for (int k = 0; k < SH - 1; ++k) issue(half, k);
+        int kk = 0, slot = 0, nv_prev = 0;
+        unsigned par = 0;
+        for (int t = t_begin + half; t < t_end; t += NHALF, ++kk) {
+            const int st = half * SH + slot;
+            if (hw == HW - 1) issue(half, kk + SH - 1);
+            mbar_wait(full_b + st, par);
+            if (++slot == SH) { slot = 0; par ^= 1u; }
+            tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
+            unsigned char *sb = stage_ptr(st);
+            const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
+            const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
+            const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
+            const uint32_t *kit = reinterpret_cast<const uint32_t *>(sb + P.so_kit);
+            const uint32_t *vit = reinterpret_cast<const uint32_t *>(sb + P.so_vit);
+            const int *hdr = reinterpret_cast<const int *>(sb + P.so_hdr);
+            const int64_t n0 = (int64_t)t * 32;
+            const int ntok = (int)min((int64_t)32, P.T - n0);
+            const float2 *anc32 = H.anc32;
+
+            // K-outlier correction of one item: (x - K^(code)) * dscore/dK for query head
+            // kvl*G + gg, in fp32
+            auto k_corr = [&](uint32_t itm, int gg, int &j_out, int &g_out) -> float {
+                const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                const int kvl = chl >> 7, cc = chl & 127, i = cc & 63, up = cc >> 6;
+                const int bit = 2 * BITS * i;
+                const int wq = kvl * 4 * BITS + (bit >> 5);
+                unsigned long long w64 = kw_s[wq * 32 + j];
+                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                const int code = (pc >> (up * BITS)) & CM;
+                const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+                const float delta = xval - (cbKs[code] * ks_s[chl] + kz_s[chl]);
+                const float2 an = anc32[i], tt = t1tab[i * 32 + j];
+                const float co = an.x * tt.x - an.y * tt.y, si = an.x * tt.y + an.y * tt.x;
+                const int g = kvl * G + gg;
+                const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
+                j_out = j;
+                g_out = g;
+                return delta * (up ? (qb * co - qa * si) : (qa * co + qb * si));
+            };
+
+            // ------------------------------------------ a3: K outliers, heavy pairs
+            {
+                const int nk = hdr[0];
+                // Key-outlier corrections straight into the (head, token) score term, in fixed
+                // point (native shared integer atomics; see kfix_of)
+                for (int x = htid; x < nk; x += HT) {
+                    const uint32_t itm = kit[x];
+#pragma unroll
+                    for (int gg = 0; gg < G; ++gg) {
+                        int j, g;
+                        const float v = k_corr(itm, gg, j, g);
+                        atomicAdd(&H.kfix[g * 32 + j], kfix_of(v));
+                    }
                 }
-            return r;
-        };
-        // K-outlier correction of one item: (x - K^(code)) * dscore/dK for query head
-        // kvl*G + gg, in fp32
-        auto k_corr = [&](uint32_t itm, int gg, int &j_out, int &g_out) -> float {
-            const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
-            const int kvl = chl >> 7, cc = chl & 127, ii = cc & 63, up = cc >> 6;
-            const int bit = 2 * BITS * ii;
-            const int wq = kvl * 4 * BITS + (bit >> 5);
-            unsigned long long w64 = kw_s[wq * 32 + j];
-            if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + j] << 32;
-            const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-            const int code = (pc >> (up * BITS)) & CM;
-            const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
-            const float delta = xval - (cbKs[code] * ks_s[chl] + kz_s[chl]);
-            const float2 cs = cis_tok(ii, j);
-            const int g = kvl * G + gg;
-            const float qa = qs[g * kHeadDim + ii], qb = qs[g * kHeadDim + ii + 64];
-            j_out = j;
-            g_out = g;
-            return delta * (up ? (qb * cs.x - qa * cs.y) : (qa * cs.x + qb * cs.y));
-        };
-
-        // ------------------------------------------ a3: K outliers, heavy pairs
-        {
-            const int nk = hdr[0];
-            for (int x = qtid; x < nk; x += QT) {
-                const uint32_t itm = kit[x];
-#pragma unroll
-                for (int gg = 0; gg < G; ++gg) {
-                    int j, g;
-                    const float v = k_corr(itm, gg, j, g);
-                    atomicAdd(&kf[g * 32 + j], kfix_of(v));
+                // Value-outlier sums of this half's previous tile (fixed point) -> osp
+                if (nv_prev) {
+                    const float inv = H.vscale[0];
+                    for (int x = htid; x < HG * kHeadDim; x += HT) {
+                        const int v = H.vfix[x];
+                        if (v) { H.osp[x] += (float)v * inv; H.vfix[x] = 0; }
+                    }
                 }
-            }
-            if (hdr[2]) {
-                // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
-                for (int j = 0; j < ntok; ++j) {
-                    const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
-                    for (uint32_t r = r0 + qtid; r < r1; r += QT) {
-                        const uint32_t rec = __ldcg(c.kout + r);
-                        const int ch = (int)(rec & 0xffffu);
-                        if (ch < c_lo || ch >= c_hi) continue;
-                        const uint32_t itm = (rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - c_lo);
+                if (htid == 0) H.vmax[0] = 0;
+                nv_prev = hdr[1] | hdr[3];
+                if (hdr[2]) {
+                    // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
+                    for (int j = 0; j < ntok; ++j) {
+                        const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
+                        for (uint32_t r = r0 + htid; r < r1; r += HT) {
+                            const uint32_t rec = __ldcg(c.kout + r);
+                            const int ch = (int)(rec & 0xffffu);
+                            if (ch < c_lo || ch >= c_hi) continue;
+                            const uint32_t itm = (rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - c_lo);
 #pragma unroll
-                        for (int gg = 0; gg < G; ++gg) {
-                            int jj, g;
-                            const float v = k_corr(itm, gg, jj, g);
-                            atomicAdd(&kf[g * 32 + jj], kfix_of(v));
+                            for (int gg = 0; gg < G; ++gg) {
+                                int jj, g;
+                                const float v = k_corr(itm, gg, jj, g);
+                                atomicAdd(&H.kfix[g * 32 + jj], kfix_of(v));
+                            }
                         }
                     }
                 }
+                // heavy RoPE pairs in fp32 (tables hlut): the (head, pair) list spread over the
+                // half's warps, lane = token
+                for (int cb = hw; cb < n_combo; cb += HW) {
+                    const int g = hv_combo[cb] >> 3, hsl = hv_combo[cb] & 7;
+                    const int i = hv_pair[g * 8 + hsl];
+                    const int bit = 2 * BITS * i;
+                    const int wq = (g / G) * 4 * BITS + (bit >> 5);
+                    unsigned long long w64 = kw_s[wq * 32 + lane];
+                    if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + lane] << 32;
+                    const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                    const float2 ab = hlut[(g * HMAX + hsl) * NE + pc];
+                    const float2 an = anc32[i], tt = t1tab[i * 32 + lane];
+                    const float hc = (an.x * tt.x - an.y * tt.y) * ab.x + (an.x * tt.y + an.y * tt.x) * ab.y;
+                    atomicAdd(&H.kfix[g * 32 + lane], kfix_of(hc));
+                }
             }
-            // heavy RoPE pairs in fp32 (tables hlut): the (head, pair) list spread over the
-            // quad's warps, lane = token
-            for (int cb = w; cb < n_combo; cb += QWARPS) {
-                const int g = hv_combo[cb] >> 3, hsl = hv_combo[cb] & 7;
-                const int ii = hv_pair[g * 8 + hsl];
-                const int bit = 2 * BITS * ii;
-                const int wq = (g / G) * 4 * BITS + (bit >> 5);
-                unsigned long long w64 = kw_s[wq * 32 + lane];
-                if ((bit & 31) + 2 * BITS > 32) w64 |= (unsigned long long)kw_s[(wq + 1) * 32 + lane] << 32;
-                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
-                const float2 ab = hlut[(g * HMAX + hsl) * NE + pc];
-                const float2 cs = cis_tok(ii, lane);
-                atomicAdd(&kf[g * 32 + lane], kfix_of(cs.x * ab.x + cs.y * ab.y));
-            }
-        }
-        // ------------------------------------------------------------ a2: K dense
-        {
-            float acc_c[HG], acc_s[HG];
+            // ------------------------------------------------------------ a2: K dense
+            {
+                float acc_c[HG], acc_s[HG];
 #pragma unroll
-            for (int g = 0; g < HG; ++g) { acc_c[g] = 0.f; acc_s[g] = 0.f; }
+                for (int g = 0; g < HG; ++g) { acc_c[g] = 0.f; acc_s[g] = 0.f; }
+                uint32_t wl[HKV], wh[HKV];
 #pragma unroll
-            for (int h = 0; h < HKV; ++h) {
-                uint32_t wd[KWW];
-#pragma unroll
-                for (int x = 0; x < KWW; ++x) wd[x] = kw_s[(h * 4 * BITS + w * KWW + x) * 32 + lane];
+                for (int h = 0; h < HKV; ++h) {
+                    unsigned long long w64 = kw_s[(h * 4 * BITS + kq0) * 32 + lane];
+                    if (kshift + 2 * BITS * KPW > 32)
+                        w64 |= (unsigned long long)kw_s[(h * 4 * BITS + kq0 + 1) * 32 + lane] << 32;
+                    w64 >>= kshift;
+                    wl[h] = (uint32_t)w64;
+                    wh[h] = (uint32_t)(w64 >> 32);
+                }
 #pragma unroll
                 for (int k = 0; k < KPW; ++k) {
-                    const float2 an = an32[w * KPW + k];
+                    const int i = hw * KPW + k;
+                    const float2 an = anc32[i];
                     const float cc = an.x * t1c[k] - an.y * t1s[k];
                     const float ss = an.x * t1s[k] + an.y * t1c[k];
                     const uint32_t cs = pack_half2(cc, ss);
-                    const int bsh = 2 * BITS * k - 2;   // bit of (pair code << 2) in the words
-                    uint32_t off;
-                    if (bsh < 0) off = wd[0] << 2;
-                    else if ((bsh & 31) + 2 * BITS + 2 <= 32) off = wd[bsh >> 5] >> (bsh & 31);
-                    else off = __funnelshift_r(wd[bsh >> 5], wd[(bsh >> 5) + 1], bsh & 31);
-                    const uint32_t a = klut_w | (off & ((NE - 1) << 2));
+                    const int b = 2 * BITS * k - 2;   // bit of (pair code << 2) in the window
 #pragma unroll
-                    for (int gg = 0; gg < G; ++gg) {
-                        const int g = h * G + gg;
-                        const uint32_t ab = lds_u32(a + (uint32_t)((g * 64 + k) * NE * 4));
-                        fma2_f16_f32(ab, cs, acc_c[g], acc_s[g]);
+                    for (int h = 0; h < HKV; ++h) {
+                        uint32_t off;
+                        if (b < 0) off = wl[h] << 2;
+                        else if (b + 2 * BITS + 2 <= 32) off = wl[h] >> b;
+                        else if (b >= 32) off = wh[h] >> (b - 32);
+                        else off = __funnelshift_r(wl[h], wh[h], b);
+                        const uint32_t a = klut_w | (off & ((NE - 1) << 2));
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) {
+                            const int g = h * G + gg;
+                            const uint32_t ab = lds_u32(a + (uint32_t)((g * 64 + k) * NE * 4));
+                            fma2_f16_f32(ab, cs, acc_c[g], acc_s[g]);
+                        }
                     }
                 }
+#pragma unroll
+                for (int g = 0; g < HG; ++g) H.red[(hw * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
             }
-            float *rd = Q.red + (b * QWARPS + w) * HG * 32;
-#pragma unroll
-            for (int g = 0; g < HG; ++g) rd[g * 32 + lane] = acc_c[g] + acc_s[g];
-        }
-        tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
-        bar_sync(1 + q, QT);   // the quad's scores of tile it are complete
-        tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
-        if (SPQ == 2) load_next(i);
-        // anchors of the quad's tile two ahead (slot free: every warp is past K(i))
-        if (w == 0 && i + 2 < nqt) {
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                const int ii = lane + 32 * h2;
-                const double2 a = amaster[h2], r = rot128[ii];
-                amaster[h2] = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
-                Q.anc[((i + 2) % NANC) * 64 + ii] = make_float2((float)amaster[h2].x, (float)amaster[h2].y);
-            }
-        }
+            half_sync(half);
+            tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
 
-        // ------------------------------------------------------- a4: online softmax
-        float smax = lane < ntok ? vsz_s[lane].x : 0.f;
-        smax = warp_max_redux(smax);
-        int E_new = E_cur;
-        if (smax > 0.f) E_new = max(E_cur, ilog2f(smax) + 1);
-        const float pe = pow2i(-E_new);
-        float beta_w = 1.f;
-        if (w < HG) {
-            const int g = w, j = lane;
-            const bool valid = j < ntok;
-            const float *rd = Q.red + b * QWARPS * HG * 32;
-            float s = 0.f;
+            // ------------------------------------------------------- a4: online softmax
+            {
+                float smax = lane < ntok ? vsz_s[lane].x : 0.f;
+                smax = warp_max_redux(smax);
+                int E_new = E_cur;
+                if (smax > 0.f) E_new = max(E_cur, ilog2f(smax) + 1);
+                const float pe = pow2i(-E_new);
+                if (hw < HG) {
+                    const int g = hw, j = lane;
+                    const bool valid = j < ntok;
+                    float s = 0.f;
 #pragma unroll
-            for (int x = 0; x < QWARPS; ++x) s += rd[(x * HG + g) * 32 + j];
-            s = s * lut_inv[g] + (float)kf[g * 32 + j] * (1.f / kKfixScale);
-            kf[g * 32 + j] = 0;
-            s = valid ? s : -CUDART_INF_F;
-            const float m_new = fmaxf(m_run, warp_max_redux(s));
-            const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
-            const float p = valid ? exp2f(s - m_new) : 0.f;
-            const float2 sz = valid ? vsz_s[j] : make_float2(0.f, 0.f);
-            l_lane = l_lane * alpha + p;
-            z_lane = z_lane * alpha + p * sz.y;
-            m_run = m_new;
-            Q.p_s[g * 32 + j] = p;
-            Q.w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * (sz.x * pe)));
-            beta_w = alpha * pow2i(E_cur - E_new);
-            if (!SELF && lane == 0) Q.beta[g] = beta_w;
-        }
-        const int E_prev = E_cur;
-        E_cur = E_new;
-        if (SELF) __syncwarp();
-        else bar_sync(1 + q, QT);   // weights of other warps' heads
-
-        // -------------------------------------------------------- a5: P.V dense
-        {
-            const float b_lo = SELF ? beta_w : Q.beta[vq_lo], b_hi = SELF ? beta_w : Q.beta[vq_hi];
-            if (b_lo != 1.f || b_hi != 1.f) {
+                    for (int w = 0; w < HW; ++w) s += H.red[(w * HG + g) * 32 + j];
+                    s = s * lut_inv[g] + (float)H.kfix[g * 32 + j] * (1.f / kKfixScale);
+                    H.kfix[g * 32 + j] = 0;
+                    s = valid ? s : -CUDART_INF_F;
+                    const float m_new = fmaxf(m_run, warp_max_redux(s));
+                    const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run - m_new);
+                    const float p = valid ? exp2f(s - m_new) : 0.f;
+                    const float2 sz = valid ? vsz_s[j] : make_float2(0.f, 0.f);
+                    l_lane = l_lane * alpha + p;
+                    z_lane = z_lane * alpha + p * sz.y;
+                    m_run = m_new;
+                    H.p_s[g * 32 + j] = p;
+                    H.w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * (sz.x * pe)));
+                    if (alpha != 1.f) {
 #pragma unroll
-                for (int x = 0; x < MTW; ++x) {
-                    dacc[x][0] *= b_lo; dacc[x][1] *= b_hi;
-                    dacc[x][2] *= b_lo; dacc[x][3] *= b_hi;
+                        for (int x = 0; x < kHeadDim / 32; ++x) H.osp[g * kHeadDim + x * 32 + lane] *= alpha;
+                    }
+                    if (lane == 0) H.beta_s[g] = alpha * pow2i(E_cur - E_new);
+                } else {
+                    // meanwhile the other warps compute the Value-outlier deltas
+                    // x - (Chat_V[code] s_n + z_n) of the tile's items and their max |delta|
+                    const int nvi = hdr[1];
+                    float mx = 0.f;
+                    for (int x = htid - HG * 32; x < nvi; x += HT - HG * 32) {
+                        const uint32_t itm = vit[x];
+                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                        const int kvl = chl >> 7, cc = chl & 127;
+                        const int bit = vf_bit(j, cc, BITS);
+                        const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
+                        unsigned long long w64 = vwp[0];
+                        if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vwp[32] << 32;
+                        const int code = (int)((w64 >> (bit & 31)) & CM);
+                        const float2 sz = vsz_s[j];
+                        const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+                        const float delta = xval - (cbVs[code] * sz.x + sz.y);
+                        H.vdel[x] = delta;
+                        mx = fmaxf(mx, fabsf(delta));
+                    }
+                    mx = warp_max_redux(mx);
+                    if (lane == 0 && mx > 0.f) atomicMax(H.vmax, __float_as_int(mx));
                 }
+                E_cur = E_new;
             }
-            uint32_t vr[NWV + 1];
+            half_sync(half);
+            tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
+
+            // -------------------------------------------------------- a5: P.V dense
+            {
+                const float b_lo = H.beta_s[vq_lo], b_hi = H.beta_s[vq_hi];
+                if (b_lo != 1.f || b_hi != 1.f) {
 #pragma unroll
-            for (int x = 0; x < NWV; ++x) vr[x] = vw_s[(vkv * 4 * BITS + vw0 + x) * 32 + lane];
-            vr[NWV] = 0u;
-            if (BITS == 3 && MTW == 1 && voff) { vr[0] = __funnelshift_r(vr[0], vr[1], 16); vr[1] >>= 16; }
-            // B fragments (weights of query head vkv*G + g for tokens 16s + 2t.. / +8..)
-            uint32_t bw[2][2];
+                    for (int x = 0; x < MTW; ++x) {
+                        dacc[x][0] *= b_lo; dacc[x][1] *= b_hi;
+                        dacc[x][2] *= b_lo; dacc[x][3] *= b_hi;
+                    }
+                }
+                uint32_t vr[NWV + 1];
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
-                const uint32_t *w32 = reinterpret_cast<const uint32_t *>(Q.w16 + (vkv * G + (vg < G ? vg : 0)) * 32 + 16 * s2 + 2 * vt);
-                bw[s2][0] = vg < G ? w32[0] : 0u;
-                bw[s2][1] = vg < G ? w32[4] : 0u;
-            }
-#pragma unroll
-            for (int ml = 0; ml < MTW; ++ml) {
+                for (int x = 0; x < NWV; ++x) vr[x] = vw_s[(vkv * 4 * BITS + vw0 + x) * 32 + lane];
+                vr[NWV] = 0u;
+                if (BITS == 3 && MTW == 1 && voff) { vr[0] = __funnelshift_r(vr[0], vr[1], 16); vr[1] >>= 16; }
+                // B fragments (weights of query head vkv*G + g for tokens 16s + 2t.. / +8..)
+                uint32_t bw[2][2];
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) {
-                    uint32_t a[4];
+                    const uint32_t *w32 = reinterpret_cast<const uint32_t *>(H.w16 + (vkv * G + (vg < G ? vg : 0)) * 32 + 16 * s2 + 2 * vt);
+                    bw[s2][0] = vg < G ? w32[0] : 0u;
+                    bw[s2][1] = vg < G ? w32[4] : 0u;
+                }
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const int bit = ((ml * 2 + s2) * 4 + r) * FB;
-                        const int wi = bit >> 5, sh = bit & 31;
-                        uint32_t off;
-                        if (sh + FB <= 32) off = sh >= 7 ? (vr[wi] >> (sh - 7)) : (vr[wi] << (7 - sh));
-                        else off = __funnelshift_r(vr[wi], vr[wi + 1], sh - 7);
-                        a[r] = lds_u32(vlut_base + (vlane4 | (off & ((NE - 1) << 7))));
+                for (int ml = 0; ml < MTW; ++ml) {
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        uint32_t a[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int bit = ((ml * 2 + s2) * 4 + r) * FB;
+                            const int wi = bit >> 5, sh = bit & 31;
+                            // (field & (NE-1)) << 7 with one shift (funnel when it straddles)
+                            uint32_t off;
+                            if (sh + FB <= 32) off = sh >= 7 ? (vr[wi] >> (sh - 7)) : (vr[wi] << (7 - sh));
+                            else off = __funnelshift_r(vr[wi], vr[wi + 1], sh - 7);
+                            a[r] = lds_u32(vlut_base + (vlane4 | (off & ((NE - 1) << 7))));
+                        }
+                        mma_f16_f32(dacc[ml], a, bw[s2]);
                     }
-                    mma_f16_f32(dacc[ml], a, bw[s2]);
                 }
             }
-        }
-        // ---------------------------------------------------- a6: V outliers
-        {
-            // this warp's items (its KV head, its m-tiles): sum_n p_n delta_{n,c} in fixed
-            // point with |p delta| 2^(24-e) < 2^25, 2^e <= max|delta| < 2^(e+1), then folded
-            // into the accumulators (units 2^-E)
-            const int nvi = hdr[1];
-            auto v_delta = [&](int j, int chl, uint16_t xbits) -> float {
-                const int kvl = chl >> 7, cc = chl & 127;
-                const int bit = vf_bit(j, cc, BITS);
-                const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
-                unsigned long long w64 = vwp[0];
-                if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vwp[32] << 32;
-                const int code = (int)((w64 >> (bit & 31)) & CM);
-                const float2 sz = vsz_s[j];
-                return __half2float(__ushort_as_half(xbits)) - (cbVs[code] * sz.x + sz.y);
-            };
-            auto mine = [&](int chl) { return (chl >> 7) == vkv && (((chl & 127) >> 4) - mt0) >= 0 && (((chl & 127) >> 4) - mt0) < MTW; };
-            float mx = 0.f;
-            for (int x = lane; x < nvi; x += 32) {
-                const uint32_t itm = vit[x];
-                const int chl = (int)(itm & 0x7ffu);
-                if (mine(chl)) mx = fmaxf(mx, fabsf(v_delta((int)((itm >> 11) & 31u), chl, (uint16_t)(itm >> 16))));
-            }
-            if (hdr[3]) {
-                for (int r = lane; r < ntok * kv; r += 32) {
-                    const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
-                    const int ch = (int)(rec & 0xffffu);
-                    if (ch < c_lo || ch >= c_hi || !mine(ch - c_lo)) continue;
-                    mx = fmaxf(mx, fabsf(v_delta(r / kv, ch - c_lo, (uint16_t)(rec >> 16))));
-                }
-            }
-            mx = warp_max_redux(mx);
-            if (mx > 0.f) {
-                const int emx = ilog2f(mx);
-                const float S = pow2i(24 - emx);
-                int *vf = Q.vfix;
-                for (int x = lane; x < nvi; x += 32) {
-                    const uint32_t itm = vit[x];
-                    const int chl = (int)(itm & 0x7ffu);
-                    if (!mine(chl)) continue;
-                    const int j = (int)((itm >> 11) & 31u), cc = chl & 127;
-                    const float dS = v_delta(j, chl, (uint16_t)(itm >> 16)) * S;
+            // ---------------------------------------------------- a6: V outliers
+            {
+                auto v_item = [&](uint32_t itm) {
+                    const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                    const int kvl = chl >> 7, cc = chl & 127;
+                    const int bit = vf_bit(j, cc, BITS);
+                    const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
+                    unsigned long long w64 = vwp[0];
+                    if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)vwp[32] << 32;
+                    const int code = (int)((w64 >> (bit & 31)) & CM);
+                    const float2 sz = vsz_s[j];
+                    const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+                    const float delta = xval - (cbVs[code] * sz.x + sz.y);
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
-                        const int g = vkv * G + gg;
-                        atomicAdd(&vf[g * kHeadDim + cc], __float2int_rn(Q.p_s[g * 32 + j] * dS));
+                        const int g = kvl * G + gg;
+                        atomicAdd(&H.osp[g * kHeadDim + cc], H.p_s[g * 32 + j] * delta);
+                    }
+                };
+                const int nvi = hdr[1];
+                if (nvi) {
+                    // sum_n p_n delta_{n,c} in fixed point: |p delta| 2^(24-e) < 2^25 with
+                    // 2^e <= max|delta| < 2^(e+1); <= 32 items per (head, channel) and tile
+                    const float mx = __int_as_float(H.vmax[0]);
+                    const int emx = mx > 0.f ? ilog2f(mx) : 0;
+                    const float S = pow2i(24 - emx);
+                    if (htid == 0) H.vscale[0] = pow2i(emx - 24);   // 1/S
+                    for (int x = htid; x < nvi; x += HT) {
+                        const uint32_t itm = vit[x];
+                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                        const int kvl = chl >> 7, cc = chl & 127;
+                        const float dS = H.vdel[x] * S;
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) {
+                            const int g = kvl * G + gg;
+                            atomicAdd(&H.vfix[g * kHeadDim + cc], __float2int_rn(H.p_s[g * 32 + j] * dS));
+                        }
                     }
                 }
                 if (hdr[3]) {
-                    for (int r = lane; r < ntok * kv; r += 32) {
+                    // overflowed bucket: this tile's Value outliers from the CSR rows (rare)
+                    for (int r = htid; r < ntok * kv; r += HT) {
                         const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
                         const int ch = (int)(rec & 0xffffu);
-                        if (ch < c_lo || ch >= c_hi || !mine(ch - c_lo)) continue;
-                        const int j = r / kv, chl = ch - c_lo, cc = chl & 127;
-                        const float dS = v_delta(j, chl, (uint16_t)(rec >> 16)) * S;
-#pragma unroll
-                        for (int gg = 0; gg < G; ++gg) {
-                            const int g = vkv * G + gg;
-                            atomicAdd(&vf[g * kHeadDim + cc], __float2int_rn(Q.p_s[g * 32 + j] * dS));
-                        }
-                    }
-                }
-                __syncwarp();
-                // fold into the accumulators of the owner lanes (units 2^-E_cur) and clear
-                const float unit = pow2i(emx - 24) * pow2i(-E_cur);
-#pragma unroll
-                for (int ml = 0; ml < MTW; ++ml) {
-                    const int ch = (mt0 + ml) * 16 + vg;
-#pragma unroll
-                    for (int cl = 0; cl < 2; ++cl) {
-                        if (2 * vt + cl < G) {
-                            int *pv = vf + (vkv * G + 2 * vt + cl) * kHeadDim + ch;
-                            dacc[ml][cl] += (float)pv[0] * unit;
-                            dacc[ml][2 + cl] += (float)pv[8] * unit;
-                            pv[0] = 0;
-                            pv[8] = 0;
-                        }
+                        if (ch < c_lo || ch >= c_hi) continue;
+                        v_item((rec & 0xffff0000u) | ((uint32_t)(r / kv) << 11) | (uint32_t)(ch - c_lo));
                     }
                 }
             }
-            (void)E_prev;
+            // advance this half's anchors by two tiles (fp64 complex rotation by 64 theta_i)
+            if (htid < 64) {
+                const double2 a = H.anc64[htid], r = rot64[htid];
+                const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
+                H.anc64[htid] = b;
+                H.anc32[htid] = make_float2((float)b.x, (float)b.y);
+            }
+            half_sync(half);
+            tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
         }
-        tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
-    }
-    // accumulators -> per-quad results (the ring is free once every quad is done)
-    __syncthreads();
-    float *osp = reinterpret_cast<float *>(smem_raw + P.st_base) + q * HG * kHeadDim;   // [NQ][HG][128]
-    {
-        const float sc = pow2i(E_cur);
+        if (nv_prev) {
+            const float inv = H.vscale[0];
+            for (int x = htid; x < HG * kHeadDim; x += HT) {
+                const int v = H.vfix[x];
+                if (v) H.osp[x] += (float)v * inv;
+            }
+        }
+        half_sync(half);   // osp entries are updated by other threads below
+        if (hw < HG) {
+            const float l = warp_sum(l_lane), z = warp_sum(z_lane);
+            if (lane == 0) { H.m_fin[hw] = m_run; H.l_fin[hw] = l; H.z_fin[hw] = z; }
+        }
+        {
+            // dense P.V accumulators (units of 2^-E_cur): row g / g+8 = channel, column = head
+            const float sc = pow2i(E_cur);
 #pragma unroll
-        for (int ml = 0; ml < MTW; ++ml) {
-            const int ch = (mt0 + ml) * 16 + vg;
-#pragma unroll
-            for (int cl = 0; cl < 2; ++cl) {
-                if (2 * vt + cl < G) {
-                    float *o = osp + (vkv * G + 2 * vt + cl) * kHeadDim + ch;
-                    o[0] = dacc[ml][cl] * sc;
-                    o[8] = dacc[ml][2 + cl] * sc;
+            for (int ml = 0; ml < MTW; ++ml) {
+                const int ch = (mt0 + ml) * 16 + vg;
+                if (2 * vt < G) {
+                    float *o = H.osp + (vkv * G + 2 * vt) * kHeadDim + ch;
+                    o[0] += dacc[ml][0] * sc;
+                    o[8] += dacc[ml][2] * sc;
+                }
+                if (2 * vt + 1 < G) {
+                    float *o = H.osp + (vkv * G + 2 * vt + 1) * kHeadDim + ch;
+                    o[0] += dacc[ml][1] * sc;
+                    o[8] += dacc[ml][3] * sc;
                 }
             }
         }
-    }
-    if (w < HG) {
-        const float l = warp_sum(l_lane), z = warp_sum(z_lane);
-        if (lane == 0) { Q.m_fin[w] = m_run; Q.l_fin[w] = l; Q.z_fin[w] = z; }
-    }
-    if (P.timers && qtid == 0) {
+        if (P.timers && tid == 0) {
 #pragma unroll
-        for (int x = 0; x < 5; ++x) atomicAdd(P.timers + x, tm[x]);
-        atomicAdd(P.timers + 5, (unsigned long long)nqt);
-        atomicAdd(P.timers + 6, tm[5]);
+            for (int x = 0; x < 5; ++x) atomicAdd(P.timers + x, tm[x]);
+            atomicAdd(P.timers + 5, (unsigned long long)ntl);
+            // wall-clock spread across CTAs: first start, last loop end, longest CTA loop
+            atomicMax(P.timers + 6, ~ns_kernel0);
+            const unsigned long long ns1 = gtimer_ns();
+            atomicMax(P.timers + 7, ns1);
+            atomicMax(P.timers + 8, ns1 - ns_kernel0);
+        }
     }
     __syncthreads();
 
-    // ------------------------------------------------------ write partial (merge quads)
+    // ------------------------------------------------ write partial (merge halves)
     float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
-    for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
-        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
-        float m = -CUDART_INF_F;
-        for (int qq = 0; qq < NQ; ++qq) {
-            const Quad Qq = quad_at(qq);
-            if (ntl > qq && Qq.l_fin[g] != 0.f) m = fmaxf(m, Qq.m_fin[g]);
-        }
-        float l = 0.f, o = 0.f;
-        for (int qq = 0; qq < NQ; ++qq) {
-            const Quad Qq = quad_at(qq);
-            if (ntl <= qq || Qq.l_fin[g] == 0.f) continue;
-            const float wq = exp2f(Qq.m_fin[g] - m);
-            l += wq * Qq.l_fin[g];
+    {
+        const Half H0 = half_at(0), H1 = half_at(1);
+        for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
+            const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+            const bool u0 = ntl > 0 && H0.l_fin[g] != 0.f, u1 = ntl > 1 && H1.l_fin[g] != 0.f;
+            const float m0 = u0 ? H0.m_fin[g] : -CUDART_INF_F, m1 = u1 ? H1.m_fin[g] : -CUDART_INF_F;
+            const float m = fmaxf(m0, m1);
+            const float w0 = u0 ? exp2f(m0 - m) : 0.f, w1 = u1 ? exp2f(m1 - m) : 0.f;
+            const float l = w0 * (u0 ? H0.l_fin[g] : 0.f) + w1 * (u1 ? H1.l_fin[g] : 0.f);
+            float o = 0.f;
             if (ch < kHeadDim) {
-                const float *oq = reinterpret_cast<const float *>(smem_raw + P.st_base) + qq * HG * kHeadDim;
-                o += wq * (oq[g * kHeadDim + ch] + Qq.z_fin[g]);
+                if (u0) o += w0 * (H0.osp[g * kHeadDim + ch] + H0.z_fin[g]);
+                if (u1) o += w1 * (H1.osp[g * kHeadDim + ch] + H1.z_fin[g]);
             }
+            part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
         }
-        part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
     }
     // ------------------------------------------------------- a7: split merge
     __threadfence();
@@ -928,8 +919,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     if (tid == 0) P.tickets[hg] = 0;
 }
 
-
-
 __global__ void merge_kernel(const float *__restrict__ parts, int Pn, int H, int d, float *o) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= H * d) return;
@@ -954,29 +943,26 @@ size_t layout(const DevCache &c, Params &P) {
     using C = Cfg<BITS, HG>;
     const int HKV = HG / c.G;
     const size_t qwc = (size_t)HKV * 4 * BITS;
-    // outlier items a ring slot holds: ~2x the expected count (the bucket capacity is ~3x);
-    // a tile with more uses the CSC / CSR fallback
-    P.scap_k = (int)std::min<int64_t>(c.kcap_g, std::max<int64_t>(128, ((int64_t)c.kcap_g * 2 / 3 + 3) & ~3LL));
-    P.scap_v = (int)std::min<int64_t>(c.vcap_g, std::max<int64_t>(128, ((int64_t)c.vcap_g * 2 / 3 + 3) & ~3LL));
     size_t off = 0;
-    P.so_kw = (unsigned)off; off += 32 * qwc * 4;
-    P.so_vw = (unsigned)off; off += 32 * qwc * 4;
-    P.so_vsz = (unsigned)off; off += 256;
-    P.so_kit = (unsigned)off; off += (size_t)P.scap_k * 4;
-    P.so_vit = (unsigned)off; off += (size_t)P.scap_v * 4;
-    const size_t stb = align128(off);
-    const size_t base = align128(align128(C::fixed) + 128);   // + mbarriers
+    P.so_kw = (unsigned)off; off = align128(off + 32 * qwc * 4);
+    P.so_vw = (unsigned)off; off = align128(off + 32 * qwc * 4);
+    P.so_vsz = (unsigned)off; off = align128(off + 256);
+    P.so_hdr = (unsigned)off; off = align128(off + 16);
+    P.so_kit = (unsigned)off; off = align128(off + (size_t)c.kcap_g * 4);
+    P.so_vit = (unsigned)off; off = align128(off + (size_t)c.vcap_g * 4);
+    const size_t stb = off;
+    // per-item Key-outlier contributions (one tile at a time), then the stage ring
+    const size_t vdel = align128((size_t)NHALF * c.vcap_g * 4);
+    P.so_vdel = (unsigned)align128(C::fixed);
+    const size_t base = align128(P.so_vdel + vdel + 128);
     P.st_base = (unsigned)base;
     const size_t limit = 227 * 1024;
-    // 2..3 private slots per quad; the ring also holds the prologue's scratch and the final
-    // per-quad results
-    const size_t need = std::max<size_t>(C::t1 + 64 * 16 + HG * 64 * 5, (size_t)NQ * HG * kHeadDim * 4);
-    for (int spq = 3; spq >= 2; --spq) {
-        const size_t ring = std::max(NQ * spq * stb, need);
-        if (base + ring <= limit) {
-            P.spq = spq;
+    for (int stages = 4; stages >= 2; stages -= 2) {
+        const size_t total = base + stages * stb;
+        if (total <= limit) {
+            P.stages = stages;
             P.st_bytes = (unsigned)stb;
-            return base + ring;
+            return total;
         }
     }
     return 0;
@@ -986,9 +972,6 @@ template <int BITS, int HG, int G>
 cudaError_t launch_t(const DevCache &c, Params &P, int grid, cudaStream_t s) {
     const size_t smem = layout<BITS, HG>(c, P);
     if (smem == 0) return cudaErrorInvalidConfiguration;
-    static bool dbg = getenv("KVQ_DEBUG_LAYOUT") != nullptr;
-    if (dbg) fprintf(stderr, "att_kernel<%d,%d,%d>: smem %zu fixed %zu slots/quad %d slot %u scap %d/%d\n",
-                     BITS, HG, G, smem, Cfg<BITS, HG>::fixed, P.spq, P.st_bytes, P.scap_k, P.scap_v);
     cudaError_t e = cudaFuncSetAttribute(att_kernel<BITS, HG, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1019,8 +1002,7 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
 }  // namespace
 
 int attend_heads_per_cta(int bits, int H_q, int G) {
-    // shared memory: K tables HG * 64 * 4^b * 4 bytes + 4 quads x 2-3 private ring slots
-    const int cap = bits == 4 ? 1 : (G >= 4 ? 4 : 2);
+    const int cap = bits == 4 ? 1 : 4;   // K tables: HG * 64 * 4^b * 4 bytes of shared memory
     for (int hg = cap; hg >= 1; hg >>= 1)
         if (H_q % hg == 0 && hg % G == 0) return hg;
     return 0;

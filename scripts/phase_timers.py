@@ -37,9 +37,16 @@ e1.record()
 torch.cuda.synchronize()
 tm = c.phase_timers()
 tiles = tm[5]
-ctas = c.info()["splits"] * (w.H_q // c.info()["heads_per_cta"])
+names = ["prologue", "tma_wait", "K_phase", "softmax", "V_phase"]
+ctas = info_splits = c.info()["splits"] * (w.H_q // c.info()["heads_per_cta"])
 print(f"{wname} T={T} attend {e0.elapsed_time(e1) / 5 * 1e3:.1f} us, info {c.info()}")
-per = lambda i: round(tm[i] / max(tiles, 1), 1)
-print(f"cycles per quad-tile (quad warp 0): load_issue {per(6)} load_wait {per(1)} K {per(2)} barrier {per(3)} softmax+PV {per(4)}"
-      f"  -> per CTA tile {round(sum(tm[1:5]) / max(tiles, 1) / 4, 1)}")
-print(f"prologue cycles per CTA: {tm[0] / (5 * ctas * 4):.0f}")
+print("compute cycles per tile per CTA:", {n: round(tm[i] / tiles, 1) for i, n in enumerate(names)},
+      "total", round(sum(tm[1:5]) / tiles, 1))
+print(f"prologue cycles per CTA: {tm[0] / (5 * ctas):.0f}  loop cycles per CTA: {sum(tm[1:5]) / (5 * ctas):.0f}")
+# one more launch alone for the wall-clock spread across CTAs
+c.attend(q, T, o)
+torch.cuda.synchronize()
+tm = c.phase_timers()
+first_start = (~tm[6]) & 0xFFFFFFFFFFFFFFFF
+print(f"last launch: first CTA start -> last CTA loop end {(tm[7] - first_start) / 1e3:.1f} us; "
+      f"longest CTA start->loop end {tm[8] / 1e3:.1f} us")
