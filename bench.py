@@ -369,7 +369,7 @@ def run_ours(args):
             "attend_us_per_step": att_ms_mean * 1e3 * L,
             "hbm_gbs_step": bytes_att * L / (ms_per_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": ncu_traffic(w.name),
                          "kernel": "att_kernel (kvq_decode_attend: one launch)",
                          "bytes_per_launch": bytes_att, "peak_kind": peak_kind,
                          "splits": info["splits"], "heads_per_cta": info["heads_per_cta"]},
@@ -383,6 +383,19 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def ncu_traffic(workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum per att_kernel launch from the committed
+    ncu --set full capture (profiles/att_traffic.json), or None if none was taken for this
+    workload."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "att_traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f).get(workload)
+        return None if rec is None else rec["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 if __name__ == "__main__":
