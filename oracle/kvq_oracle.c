@@ -125,7 +125,7 @@ int kvo_outlier_count(int D, int ppm) {
     return (int)(((int64_t)ppm * (int64_t)D + 999999) / 1000000);
 }
 
-static const double *g_sort_vals;
+static _Thread_local const double *g_sort_vals;   /* per-thread qsort context */
 static int cmp_desc_val_asc_idx(const void *a, const void *b) {
     int i = *(const int *)a, j = *(const int *)b;
     double x = g_sort_vals[i], y = g_sort_vals[j];
@@ -144,8 +144,8 @@ static int cmp_asc_val_asc_idx(const void *a, const void *b) {
 /* Two-sided per-token outlier split ("upper and lower outlier thresholds";
  * topk P:1028-1031), reading R3: the ceil(k/2) largest values (value desc, index asc),
  * then the floor(k/2) smallest of the remainder (value asc, index asc).  -0 == +0 by
- * construction of fp64 comparison.  Writes a 0/1 mask. (not thread safe: uses qsort
- * with a file-static key; the oracle's quantization is single threaded) */
+ * construction of fp64 comparison.  Writes a 0/1 mask.  (The qsort comparator reads a
+ * thread-local key array, so tokens may be quantized on several threads.) */
 void kvo_select_outliers(const uint16_t *v, int D, int k, uint8_t *mask) {
     double *vals = (double *)malloc(sizeof(double) * (size_t)D);
     int *order = (int *)malloc(sizeof(int) * (size_t)D);
@@ -219,31 +219,41 @@ int64_t kvo_prefill(int64_t T, int D, const uint16_t *K, const uint16_t *V,
                     uint16_t *kcodes, int64_t *kptr, int32_t *kidx, uint16_t *kval,
                     int64_t kcap, uint16_t *vcodes, int32_t *vidx, uint16_t *vval,
                     float *vs, float *vz) {
+    /* Tokens are independent: each is quantized exactly as kvo_quantize_key /
+     * kvo_quantize_value define, possibly on several OpenMP threads; the Key-outlier CSC is
+     * then laid out in token order, so the result equals T successive appends. */
     int k = kvo_outlier_count(D, ppm);
-    int32_t *tmp_idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)D);
-    uint16_t *tmp_val = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)D);
-    int64_t nnz = 0;
-    kptr[0] = 0;
-    for (int64_t n = 0; n < T; ++n) {
-        int cnt = kvo_quantize_key(K + n * D, D, key_lo, key_hi, cbK, nlev,
-                                   kcodes + n * D, tmp_idx, tmp_val);
-        if (nnz + cnt > kcap) {
-            free(tmp_idx);
-            free(tmp_val);
-            return -1;
+    int32_t *cnt = (int32_t *)malloc(sizeof(int32_t) * (size_t)(T > 0 ? T : 1));
+    if (!cnt) return -2;
+#pragma omp parallel
+    {
+        int32_t *tidx = (int32_t *)malloc(sizeof(int32_t) * (size_t)D);
+        uint16_t *tval = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)D);
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t n = 0; n < T; ++n) {
+            cnt[n] = kvo_quantize_key(K + n * D, D, key_lo, key_hi, cbK, nlev, kcodes + n * D,
+                                      tidx, tval);
+            kvo_quantize_value(V + n * D, D, ppm, cbV, nlev, value_identity_affine,
+                               vcodes + n * D, vidx + n * k, vval + n * k, vs + n, vz + n);
         }
-        for (int r = 0; r < cnt; ++r) {
-            kidx[nnz + r] = tmp_idx[r];
-            kval[nnz + r] = tmp_val[r];
-        }
-        nnz += cnt;
-        kptr[n + 1] = nnz;
-        kvo_quantize_value(V + n * D, D, ppm, cbV, nlev, value_identity_affine,
-                           vcodes + n * D, vidx + n * k, vval + n * k, vs + n, vz + n);
+        free(tidx);
+        free(tval);
     }
-    free(tmp_idx);
-    free(tmp_val);
-    return nnz;
+    kptr[0] = 0;
+    for (int64_t n = 0; n < T; ++n) kptr[n + 1] = kptr[n] + cnt[n];
+    free(cnt);
+    if (kptr[T] > kcap) return -1;
+    /* the Key outliers of every token at its CSC column (same quantization, rerun) */
+#pragma omp parallel
+    {
+        uint16_t *tcode = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)D);
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t n = 0; n < T; ++n)
+            kvo_quantize_key(K + n * D, D, key_lo, key_hi, cbK, nlev, tcode, kidx + kptr[n],
+                             kval + kptr[n]);
+        free(tcode);
+    }
+    return kptr[T];
 }
 
 /* ------------------------------------------------------------------ Attend ---- */

@@ -125,6 +125,7 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
 // Score terms summed with shared integer atomics (no native float atomics in shared memory):
 // fixed point with 2^-16 resolution in log2-score units, |term| clamped to 2^15.
 constexpr float kKfixScale = 65536.f;
+constexpr int WEXP = 14;   // fp16 P.V weights scaled into [0, 2^14]
 __device__ __forceinline__ int kfix_of(float v) {
     return __float2int_rn(fminf(fmaxf(v, -32768.f), 32767.f) * kKfixScale);
 }
@@ -158,7 +159,7 @@ struct Cfg {
     static constexpr int NE = 1 << (2 * BITS);
     static constexpr int HMAX = BITS == 4 ? 4 : 8;   // fp32 "heavy" pairs per head
     static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
-    static constexpr size_t vlut = (size_t)NE * 32 * 4;
+    static constexpr size_t vlut = (size_t)2 * NE * 32 * 4;   // hi and lo halves
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
     static constexpr size_t t1 = (size_t)kPairs * 32 * 8;
     // per compute half: red, p, kcorr, hcorr, kbeg/kend, w16, osp, anchors, scalars
@@ -412,10 +413,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             }
         }
     }
-    // V table: lane-private copies (entry e for lane slot l at word e*32 + l)
+    // V table: lane-private copies (entry e for lane slot l at word e*32 + l), the fp16
+    // codebook pair and, NE*32 words further, the fp16 residuals Chat - fp16(Chat): a diffuse
+    // head averages ~10^4 tokens and the per-level fp16 rounding of Chat does not average out
     for (int x = tid; x < NE * 32; x += ATT_THREADS) {
         const int e = x >> 5;
-        vlut[x] = pack_half2(cbV[e & CM], cbV[e >> BITS]);
+        const float ca = cbV[e & CM], cb = cbV[e >> BITS];
+        vlut[x] = pack_half2(ca, cb);
+        vlut[NE * 32 + x] = pack_half2(ca - __half2float(__float2half_rn(ca)), cb - __half2float(__float2half_rn(cb)));
     }
     __syncthreads();
 
@@ -668,7 +673,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 smax = warp_max_redux(smax);
                 int E_new = E_cur;
                 if (smax > 0.f) E_new = max(E_cur, ilog2f(smax) + 1);
-                const float pe = pow2i(-E_new);
+                // weights p s 2^(WEXP - E) <= 2^WEXP: normal fp16 down to p s 2^-E ~ 2^-28, so
+                // the many small weights of a long context keep 11 significant bits
+                const float pe = pow2i(WEXP - E_new);
                 if (hw < HG) {
                     const int g = hw, j = lane;
                     const bool valid = j < ntok;
@@ -747,7 +754,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 for (int ml = 0; ml < MTW; ++ml) {
 #pragma unroll
                     for (int s2 = 0; s2 < 2; ++s2) {
-                        uint32_t a[4];
+                        uint32_t a[4], alo[4];
 #pragma unroll
                         for (int r = 0; r < 4; ++r) {
                             const int bit = ((ml * 2 + s2) * 4 + r) * FB;
@@ -756,9 +763,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                             uint32_t off;
                             if (sh + FB <= 32) off = sh >= 7 ? (vr[wi] >> (sh - 7)) : (vr[wi] << (7 - sh));
                             else off = __funnelshift_r(vr[wi], vr[wi + 1], sh - 7);
-                            a[r] = lds_u32(vlut_base + (vlane4 | (off & ((NE - 1) << 7))));
+                            const uint32_t ad = vlut_base + (vlane4 | (off & ((NE - 1) << 7)));
+                            a[r] = lds_u32(ad);
+                            alo[r] = lds_u32(ad + NE * 32 * 4);
                         }
                         mma_f16_f32(dacc[ml], a, bw[s2]);
+                        mma_f16_f32(dacc[ml], alo, bw[s2]);
                     }
                 }
             }
@@ -835,7 +845,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         }
         {
             // dense P.V accumulators (units of 2^-E_cur): row g / g+8 = channel, column = head
-            const float sc = pow2i(E_cur);
+            const float sc = pow2i(E_cur - WEXP);
 #pragma unroll
             for (int ml = 0; ml < MTW; ++ml) {
                 const int ch = (mt0 + ml) * 16 + vg;

@@ -1,0 +1,59 @@
+"""Parity at the benchmarked size (BASELINE config C3 / bench.py default): one LLaMA-7B layer
+(32 heads x 128), 131072 cached tokens, 3-bit NUQ, 1% outliers, the launch configuration
+bench.py times (automatic head grouping and split count).  The oracle quantizes the same
+seeded input (OpenMP over tokens) and computes attention for every head in fp64; the GPU
+codes of sampled tokens are compared bit-exactly and the attention output within the
+north_star tolerance.  Slow (~1-2 min): inputs 2 x 1 GiB fp16."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from kvq_synth import CONFIGS, calib, gen
+
+from .gpu_common import make_cache, rel_err_per_head
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def kvq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2401_18079_b200 import kvq as K
+    return K
+
+
+def test_c3_full_size_layer(kvq):
+    w = CONFIGS["c3_nuq3"]
+    T, D, H = w.T, w.D, w.H_q
+    assert (T, D, H, w.bits) == (131072, 4096, 32, 3)
+    cal = calib.calibrate_layer(gen.gen_keys(0, 0, 2048, D, stream=gen.STREAM_CAL_K),
+                                gen.gen_values(0, 0, 2048, D, stream=gen.STREAM_CAL_V), w.bits, w.ppm)
+    Kt = gen.gen_layer_torch(7, 0, T, D, "cpu", "K")
+    Vt = gen.gen_layer_torch(8, 0, T, D, "cpu", "V")
+    K = Kt.numpy()
+    V = Vt.numpy()
+
+    c = make_cache(kvq, cal, H, H, w.bits, w.ppm, capacity=T + 32)
+    c.prefill(Kt.cuda(), Vt.cuda())
+    c.sync()
+    ref = O.prefill(K, V, cal["key_lo"], cal["key_hi"], cal["cbK"], cal["cbV"], w.ppm, kcap=64 * T)
+
+    # codes of sampled tokens (start, middle, ragged tail) bit-exact
+    for t0 in (0, 65_531, T - 40):
+        e = c.export(t0, t0 + 40)
+        np.testing.assert_array_equal(e["kcodes"].astype(np.uint16), ref.kcodes[t0:t0 + 40])
+        np.testing.assert_array_equal(e["vcodes"].astype(np.uint16), ref.vcodes[t0:t0 + 40])
+        np.testing.assert_array_equal(e["vidx"].astype(np.int32), ref.vidx[t0:t0 + 40])
+
+    q = gen.gen_queries(9, 0, H, H, 128)[0]
+    o = torch.zeros((H, 128), dtype=torch.float32, device="cuda")
+    c.attend(torch.from_numpy(q).cuda(), T, o)
+    torch.cuda.synchronize()
+    exp = O.attend(ref, q, T, H_q=H, H_kv=H, d=128, key_lo=cal["key_lo"], key_hi=cal["key_hi"],
+                   cbK_dec=cal["cbK_dec"], cbV_dec=cal["cbV_dec"], pos_base=0, nthreads=0)
+    err = rel_err_per_head(o.cpu().numpy(), exp)
+    print("C3 full-size per-head max rel err: max %.3g median %.3g" % (err.max(), np.median(err)))
+    assert err.max() < TOL, err
