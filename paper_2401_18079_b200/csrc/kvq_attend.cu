@@ -175,6 +175,7 @@ struct Cfg {
         + HG * 64 * 4 + HG * 64        /* bound, heavy flags */
         + HG * 24 * 4                  /* heavy pair list, counts, flat list */
         + HG * kHeadDim * 4 * 2 + 64 * 4 /* staged s_c, z_c of the group, codebooks */
+        + 8 * 16                       /* slot headers */
         + 256;
     static constexpr size_t fixed = klut + vlut + hlut + t1 + small;
 };
@@ -262,6 +263,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
     float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;             // 4 codebooks
     int *flag_s = reinterpret_cast<int *>(sp); sp += 16;
+    int *hdr_s = reinterpret_cast<int *>(sp); sp += 8 * 16;                // per ring slot
     // barriers just below the stage ring: full[S], empty[S]
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + P.st_base - 128);
     uint64_t *full_b = bars;
@@ -428,45 +430,52 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // Each half owns SH = stages/2 ring slots and issues its own tiles: tiles of half h are
     // t_k = t_begin + h + 2k, slot k % SH.  The last warp of the half issues tile t_{k+SH-1}
     // at the top of iteration k, into the slot its half released at the end of k-1.
-    auto issue = [&](int hh, int k) {   // called by one full warp
+    // The five copies of a tile are issued by five different warps (HW-5..HW-1; a bulk copy
+    // holds its warp ~150+ cycles), each from lane 0, with the tile's outlier counts read one
+    // issue ahead (a global load on the issue path stalls the warp ~1 us).
+    uint32_t cnt_nk = 0, cnt_nv = 0;
+    auto read_counts = [&](int hh, int k) {
+        const int ti = t_begin + hh + NHALF * k;
+        cnt_nk = cnt_nv = 0;
+        if (ti < t_end) {
+            const uint32_t *gc = c.gcnt + ((int64_t)ti * c.NG + hg) * 2;
+            cnt_nk = __ldg(gc);
+            cnt_nv = __ldg(gc + 1);
+        }
+    };
+    auto issue = [&](int hh, int k, int part) {   // lane 0 of issuing warp `part` (0..4)
         const int SH = P.stages / NHALF;
         const int ti = t_begin + hh + NHALF * k;
         if (ti >= t_end) return;
+        const uint32_t nk = cnt_nk, nv = cnt_nv;
+        read_counts(hh, k + 1);
         const int si = hh * SH + (k % SH);
         unsigned char *sb = stage_ptr(si);
         uint64_t *bar = full_b + si;
-        uint32_t nk = 0, nv = 0;
-        if (lane == 0) {
-            const uint32_t *gc = c.gcnt + ((int64_t)ti * c.NG + hg) * 2;
-            nk = __ldg(gc);
-            nv = __ldg(gc + 1);
-        }
-        nk = __shfl_sync(0xffffffffu, nk, 0);
-        nv = __shfl_sync(0xffffffffu, nv, 0);
         const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
         const uint32_t bk = kov ? 0u : ((nk + 3u) & ~3u) * 4u;
         const uint32_t bv = vov ? 0u : ((nv + 3u) & ~3u) * 4u;
         const unsigned b_kw = 32u * QWC * 4u;
-        const unsigned total = 2u * b_kw + 256u + bk + bv;
-        if (lane == 0) {
-            int *hdr = reinterpret_cast<int *>(sb + P.so_hdr);
-            hdr[0] = kov ? 0 : (int)nk;
-            hdr[1] = vov ? 0 : (int)nv;
-            hdr[2] = kov;
-            hdr[3] = vov;
-            fence_proxy_async();
-            mbar_expect_tx(bar, total);
-        }
-        __syncwarp();
-        const int64_t n0 = (int64_t)ti * 32;
         const int64_t bucket = (int64_t)ti * c.NG + hg;
-        if (lane == 0)
-            bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
-        if (lane == 1)
-            bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar);
-        if (lane == 2) bulk_g2s(sb + P.so_vsz, c.vsz + n0, 256u, bar);
-        if (lane == 3 && bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar);
-        if (lane == 4 && bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar);
+        switch (part) {
+            case 0: {
+                // header in a generic-only array (no proxy fence); published by the
+                // expect_tx arrival, read after the full-barrier wait (complete_tx of the
+                // other parts may land first: the phase needs this arrival)
+                int *hdr = hdr_s + si * 4;
+                hdr[0] = kov ? 0 : (int)nk;
+                hdr[1] = vov ? 0 : (int)nv;
+                hdr[2] = kov;
+                hdr[3] = vov;
+                mbar_expect_tx(bar, 2u * b_kw + 256u + bk + bv);
+                bulk_g2s(sb + P.so_kw, c.kcodes + ((int64_t)ti * c.QW + h0 * 4 * BITS) * 32, b_kw, bar);
+                break;
+            }
+            case 1: bulk_g2s(sb + P.so_vw, c.vcodes + ((int64_t)ti * c.H_kv + h0) * 32 * 4 * BITS, b_kw, bar); break;
+            case 2: bulk_g2s(sb + P.so_vsz, c.vsz + (int64_t)ti * 32, 256u, bar); break;
+            case 3: if (bk) bulk_g2s(sb + P.so_kit, c.kit + bucket * c.kcap_g, bk, bar); break;
+            default: if (bv) bulk_g2s(sb + P.so_vit, c.vit + bucket * c.vcap_g, bv, bar); break;
+        }
     };
 
     // =========================================================== compute warps
@@ -521,13 +530,16 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         tm[0] = tc0 - t_kernel0;   // prologue
 
         const int SH = P.stages / NHALF;
-        if (hw == HW - 1)
-            for (int k = 0; k < SH - 1; ++k) issue(half, k);
+        const int ipart = hw - (HW - 5);   // issuing warps HW-5..HW-1 of the half
+        if (ipart >= 0 && lane == 0) {
+            read_counts(half, 0);
+            for (int k = 0; k < SH - 1; ++k) issue(half, k, ipart);
+        }
         int kk = 0, slot = 0, nv_prev = 0;
         unsigned par = 0;
         for (int t = t_begin + half; t < t_end; t += NHALF, ++kk) {
             const int st = half * SH + slot;
-            if (hw == HW - 1) issue(half, kk + SH - 1);
+            if (ipart >= 0 && lane == 0) issue(half, kk + SH - 1, ipart);
             mbar_wait(full_b + st, par);
             if (++slot == SH) { slot = 0; par ^= 1u; }
             tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
@@ -537,7 +549,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             const float2 *vsz_s = reinterpret_cast<const float2 *>(sb + P.so_vsz);
             const uint32_t *kit = reinterpret_cast<const uint32_t *>(sb + P.so_kit);
             const uint32_t *vit = reinterpret_cast<const uint32_t *>(sb + P.so_vit);
-            const int *hdr = reinterpret_cast<const int *>(sb + P.so_hdr);
+            const int *hdr = hdr_s + st * 4;
             const int64_t n0 = (int64_t)t * 32;
             const int ntok = (int)min((int64_t)32, P.T - n0);
             const float2 *anc32 = H.anc32;
