@@ -196,7 +196,7 @@ struct Params {
     unsigned long long *timers;   // optional [8] phase cycle sums (diagnostics), may be null
 };
 
-template <int BITS, int HG, int G>
+template <int BITS, int HG, int G, bool TIMED>
 __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params P) {
     using C = Cfg<BITS, HG>;
     constexpr int NE = C::NE;
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     uint64_t *full_b = bars;
 
     const long long t_kernel0 = clock64();
-    const unsigned long long ns_kernel0 = P.timers ? gtimer_ns() : 0ull;
+    const unsigned long long ns_kernel0 = TIMED ? gtimer_ns() : 0ull;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
     const int hg = blockIdx.x % n_hg;
@@ -505,7 +505,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     for (int x = 0; x < MTW; ++x) dacc[x][0] = dacc[x][1] = dacc[x][2] = dacc[x][3] = 0.f;
     // lookup address = vlut + ((code << 7) | (lane << 2)): the OR is exact, the base add
     // folds into the load (uniform base register)
-    const uint32_t vlut_base = smem_u32(vlut), vlane4 = 4u * lane;
+    const uint32_t vlane4 = 4u * lane;
+    // lookups as byte offsets from the dynamic shared memory base: the table's offset (C::klut)
+    // is a compile-time constant that folds into the LDS immediate
+    const unsigned char *vlut_b = smem_raw + C::klut;
     float m_run = -CUDART_INF_F, l_lane = 0.f, z_lane = 0.f;
     int E_cur = -126;     // dense V accumulator units: 2^E_cur (uniform in a half)
     unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
@@ -542,7 +545,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             if (ipart >= 0 && lane == 0) issue(half, kk + SH - 1, ipart);
             mbar_wait(full_b + st, par);
             if (++slot == SH) { slot = 0; par ^= 1u; }
-            tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1;
+            if (TIMED) { tc1 = clock64(); tm[1] += tc1 - tc0; tc0 = tc1; }
             unsigned char *sb = stage_ptr(st);
             const uint32_t *kw_s = reinterpret_cast<const uint32_t *>(sb + P.so_kw);
             const uint32_t *vw_s = reinterpret_cast<const uint32_t *>(sb + P.so_vw);
@@ -677,7 +680,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 for (int g = 0; g < HG; ++g) H.red[(hw * HG + g) * 32 + lane] = acc_c[g] + acc_s[g];
             }
             half_sync(half);
-            tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1;
+            if (TIMED) { tc1 = clock64(); tm[2] += tc1 - tc0; tc0 = tc1; }
 
             // ------------------------------------------------------- a4: online softmax
             {
@@ -737,7 +740,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 E_cur = E_new;
             }
             half_sync(half);
-            tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1;
+            if (TIMED) { tc1 = clock64(); tm[3] += tc1 - tc0; tc0 = tc1; }
 
             // -------------------------------------------------------- a5: P.V dense
             {
@@ -775,9 +778,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                             uint32_t off;
                             if (sh + FB <= 32) off = sh >= 7 ? (vr[wi] >> (sh - 7)) : (vr[wi] << (7 - sh));
                             else off = __funnelshift_r(vr[wi], vr[wi + 1], sh - 7);
-                            const uint32_t ad = vlut_base + (vlane4 | (off & ((NE - 1) << 7)));
-                            a[r] = lds_u32(ad);
-                            alo[r] = lds_u32(ad + NE * 32 * 4);
+                            const uint32_t ad = vlane4 | (off & ((NE - 1) << 7));
+                            a[r] = *reinterpret_cast<const uint32_t *>(vlut_b + ad);
+                            alo[r] = *reinterpret_cast<const uint32_t *>(vlut_b + NE * 32 * 4 + ad);
                         }
                         mma_f16_f32(dacc[ml], a, bw[s2]);
                         mma_f16_f32(dacc[ml], alo, bw[s2]);
@@ -841,7 +844,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 H.anc32[htid] = make_float2((float)b.x, (float)b.y);
             }
             half_sync(half);
-            tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1;
+            if (TIMED) { tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1; }
         }
         if (nv_prev) {
             const float inv = H.vscale[0];
@@ -873,7 +876,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 }
             }
         }
-        if (P.timers && tid == 0) {
+        if (TIMED && tid == 0) {
 #pragma unroll
             for (int x = 0; x < 5; ++x) atomicAdd(P.timers + x, tm[x]);
             atomicAdd(P.timers + 5, (unsigned long long)ntl);
@@ -994,10 +997,17 @@ template <int BITS, int HG, int G>
 cudaError_t launch_t(const DevCache &c, Params &P, int grid, cudaStream_t s) {
     const size_t smem = layout<BITS, HG>(c, P);
     if (smem == 0) return cudaErrorInvalidConfiguration;
-    cudaError_t e = cudaFuncSetAttribute(att_kernel<BITS, HG, G>,
+    if (P.timers) {   // diagnostics build of the kernel (phase clocks)
+        cudaError_t e = cudaFuncSetAttribute(att_kernel<BITS, HG, G, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        att_kernel<BITS, HG, G, true><<<grid, ATT_THREADS, smem, s>>>(c, P);
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaFuncSetAttribute(att_kernel<BITS, HG, G, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    att_kernel<BITS, HG, G><<<grid, ATT_THREADS, smem, s>>>(c, P);
+    att_kernel<BITS, HG, G, false><<<grid, ATT_THREADS, smem, s>>>(c, P);
     return cudaGetLastError();
 }
 
