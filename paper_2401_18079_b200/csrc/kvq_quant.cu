@@ -22,8 +22,8 @@
 namespace kvq {
 namespace {
 
-constexpr int QZ_THREADS = 256;
-constexpr int QZ_WARPS = QZ_THREADS / 32;
+constexpr int QZ_THREADS = 256;     // prefill: one CTA per token, many CTAs
+constexpr int QZ_THREADS_1 = 1024;  // single decode append: one CTA does all the work
 
 __device__ __forceinline__ uint16_t f16_order_key(uint16_t h) {
     if (h == 0x8000u) h = 0;                         // -0 == +0 (R3)
@@ -48,7 +48,9 @@ __device__ __forceinline__ int enc_fp64(double y, double s, double z, const doub
 }
 
 // Block-wide exclusive scan of one int per thread; returns exclusive prefix, *total.
-__device__ __forceinline__ int block_excl_scan(int v, int *total, int *sbuf /*[QZ_WARPS+1]*/) {
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int *total, int *sbuf /*[NT/32+1]*/) {
+    constexpr int QZ_WARPS = NT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int x = v;
 #pragma unroll
@@ -109,13 +111,14 @@ __device__ __forceinline__ void select_bin(const int *hist, int need, int *out /
 // #(cand with key' > tau) < need <= #(cand with key' >= tau), where key' = key (desc=1)
 // or 0xffff - key (desc=0, i.e. ascending order).  Also returns #(key' > tau).
 // Loop trip counts are uniform across the CTA (E elements per thread).
+template <int NT>
 __device__ void radix_select16(const uint16_t *keys, const uint8_t *flags, int D, int c_begin,
                                int E, int need, bool desc, int *hist /*[256]*/,
                                int *shared_out /*[4]*/, int *tau_out, int *gt_out) {
     int prefix_hi = -1;   // selected high byte
     int gt = 0;
     for (int pass = 0; pass < 2; ++pass) {
-        for (int b = threadIdx.x; b < 256; b += QZ_THREADS) hist[b] = 0;
+        for (int b = threadIdx.x; b < 256; b += NT) hist[b] = 0;
         __syncthreads();
         for (int e = 0; e < E; ++e) {
             const int c = c_begin + e;
@@ -137,8 +140,8 @@ __device__ void radix_select16(const uint16_t *keys, const uint8_t *flags, int D
     *gt_out = gt;
 }
 
-template <int BITS>
-__global__ void __launch_bounds__(QZ_THREADS)
+template <int BITS, int NT>
+__global__ void __launch_bounds__(NT)
 qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__ Vin, int64_t n0,
           int mode) {
     constexpr int NLEV = 1 << BITS;
@@ -152,9 +155,10 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     uint8_t *vc = kc + D;                                         // [D]
     uint8_t *vflag = vc + D;                                      // [D]
     int *hist = reinterpret_cast<int *>(vflag + ((D + 15) & ~15));// [256]
-    int *sbuf = hist + 256;                                       // [16]
-    int *sout = sbuf + 16;                                        // [8]
-    float *fred = reinterpret_cast<float *>(sout + 8);            // [16]
+    int *sbuf = hist + 256;                                       // [64]
+    int *sout = sbuf + 64;                                        // [64]
+    float *fred = reinterpret_cast<float *>(sout + 64);           // [64]
+    constexpr int QZ_WARPS = NT / 32;
     __shared__ double s_mk[16], s_mv[16];
 
     const int64_t t = blockIdx.x;
@@ -166,7 +170,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     const uint16_t *vr16 = reinterpret_cast<const uint16_t *>(vrow);
 
     if (tid < NM) { s_mk[tid] = c.mids[tid]; s_mv[tid] = c.mids[16 + tid]; }
-    for (int i = tid; i < D; i += QZ_THREADS) {
+    for (int i = tid; i < D; i += NT) {
         xk[i] = kr16[i];
         if (mode != 1) { uint16_t v = vr16[i]; xv[i] = v; vkey[i] = f16_order_key(v); vflag[i] = 0; }
     }
@@ -174,7 +178,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
 
     const float *ks = c.kpar, *kz = c.kpar + D, *klo = c.kpar + 2 * D, *khi = c.kpar + 3 * D;
     // thread-contiguous channel ownership keeps ranks in ascending channel order
-    const int E = (D + QZ_THREADS - 1) / QZ_THREADS;
+    const int E = (D + NT - 1) / NT;
     const int cb0 = min(D, tid * E), cb1 = min(D, cb0 + E);
 
     // ------------------------------------------------------------------ Keys
@@ -190,7 +194,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         }
     }
     int ktotal;
-    int krank = block_excl_scan(kcnt, &ktotal, sbuf);
+    int krank = block_excl_scan<NT>(kcnt, &ktotal, sbuf);
     if (mode == 1) {
         if (tid == 0) c.counts[t] = ktotal;
         return;
@@ -274,7 +278,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         if (need == 0) continue;
         const bool desc = (sel == 0);
         int tau, gt;
-        radix_select16(vkey, vflag, D, tid * E, E, need, desc, hist, sout, &tau, &gt);
+        radix_select16<NT>(vkey, vflag, D, tid * E, E, need, desc, hist, sout, &tau, &gt);
         // ties at tau: lowest channel index first
         int ties = 0;
         for (int ch = cb0; ch < cb1; ++ch) {
@@ -283,7 +287,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
             ties += (kk == tau);
         }
         int tt;
-        int trank = block_excl_scan(ties, &tt, sbuf);
+        int trank = block_excl_scan<NT>(ties, &tt, sbuf);
         const int take = need - gt;
         for (int ch = cb0; ch < cb1; ++ch) {
             if (vflag[ch]) continue;
@@ -307,15 +311,15 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
         vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     }
-    if ((tid & 31) == 0) { fred[tid >> 5] = vmin; fred[8 + (tid >> 5)] = vmax; }
+    if ((tid & 31) == 0) { fred[tid >> 5] = vmin; fred[32 + (tid >> 5)] = vmax; }
     __syncthreads();
     if (tid == 0) {
-        float a = fred[0], b = fred[8];
-        for (int w = 1; w < QZ_WARPS; ++w) { a = fminf(a, fred[w]); b = fmaxf(b, fred[8 + w]); }
-        fred[0] = a; fred[8] = b;
+        float a = fred[0], b = fred[32];
+        for (int w = 1; w < QZ_WARPS; ++w) { a = fminf(a, fred[w]); b = fmaxf(b, fred[32 + w]); }
+        fred[0] = a; fred[32] = b;
     }
     __syncthreads();
-    vmin = fred[0]; vmax = fred[8];
+    vmin = fred[0]; vmax = fred[32];
     int imin = 0x7fffffff, imax = 0x7fffffff;
     for (int ch = cb0; ch < cb1; ++ch) {
         if (vflag[ch]) continue;
@@ -352,7 +356,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
             vcnt += vflag[ch] != 0;
         }
         int vtot;
-        int vr = block_excl_scan(vcnt, &vtot, sbuf);
+        int vr = block_excl_scan<NT>(vcnt, &vtot, sbuf);
         uint32_t *vo = c.vout + n * (int64_t)k;
         // Value outliers bucketed per (tile, group) as for the Keys
         __shared__ int gvc[64], gbv[64], gvf[64];
@@ -379,7 +383,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     // --------------------------------------------------------------- packing
     constexpr int PB = 2 * BITS;                 // bits per Key pair code
     const int tile = (int)(n >> 5), jj = (int)(n & 31);
-    for (int q = tid; q < c.QW; q += QZ_THREADS) {
+    for (int q = tid; q < c.QW; q += NT) {
         const int h = q / (4 * BITS), w = q % (4 * BITS);
         const int bit0 = 32 * w;
         const int p0 = bit0 / PB, off = bit0 - p0 * PB;
@@ -393,7 +397,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     // Value codes into the fragment layout (kvq_internal.cuh): the two channels 16mt+g and
     // 16mt+g+8 of a head share a lane and sit 2b bits apart, so one OR per pair of codes.
     // Words are shared with the tile's other tokens (zeroed at create/reset).
-    for (int x = tid; x < c.H_kv * 64; x += QZ_THREADS) {
+    for (int x = tid; x < c.H_kv * 64; x += NT) {
         const int hh = x >> 6, mt = (x >> 3) & 7, g = x & 7;
         const int cc = mt * 16 + g;
         const int bit = vf_bit(jj, cc, BITS);
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(256) sort_buckets_kernel(DevCache c, int64_t t
 size_t qz_smem(int D) {
     size_t b = (size_t)D * 2 * 3 + (size_t)D * 3;
     b = (b + 15) & ~size_t(15);
-    b += (256 + 16 + 8 + 16) * 4;
+    b += (256 + 64 + 64 + 64) * 4;
     return b;
 }
 
@@ -484,15 +488,17 @@ template <int BITS>
 cudaError_t launch_qz_bits(const DevCache &c, const __half *K, const __half *V, int64_t n0,
                            int64_t T, cudaStream_t s) {
     size_t smem = qz_smem(c.D);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(qz_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(qz_kernel<BITS, QZ_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(qz_kernel<BITS, QZ_THREADS_1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
     if (T == 1) {
-        qz_kernel<BITS><<<1, QZ_THREADS, smem, s>>>(c, K, V, n0, 0);
+        qz_kernel<BITS, QZ_THREADS_1><<<1, QZ_THREADS_1, smem, s>>>(c, K, V, n0, 0);
         return cudaGetLastError();
     }
-    qz_kernel<BITS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 1);
+    qz_kernel<BITS, QZ_THREADS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 1);
     scan_counts_kernel<<<1, 1024, 0, s>>>(c, n0, T);
-    qz_kernel<BITS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 2);
+    qz_kernel<BITS, QZ_THREADS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 2);
     const int64_t tile0 = n0 / 32, tile1 = (n0 + T - 1) / 32;
     const unsigned nl = (unsigned)((tile1 - tile0 + 1) * c.NG);
     int pk = 1, pv = 1;
