@@ -165,7 +165,7 @@ struct Cfg {
     // per compute half: red, p, kcorr, hcorr, kbeg/kend, w16, osp, anchors, scalars
     static constexpr size_t half_bytes =
         HW * HG * 32 * 4 + HG * 32 * 4 * 3 + HG * 64 * 4 + HG * 32 * 2 + HG * kHeadDim * 4 * 2
-        + 64 * 16 + 64 * 8 + HG * 4 * 4 + 16 + 64;
+        + 64 * 16 + 64 * 8 + 64 * 4 + HG * 4 * 4 + 16 + 64;
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
         + NHALF * half_bytes
@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         uint16_t *w16;
         double2 *anc64;
         float2 *anc32;
+        __half2 *anc16;         // fp16 copy of the anchors for the K dense phase
     };
     unsigned char *const half_base = sp;
     auto half_at = [&](int h) -> Half {
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         q += (16 - ((HG * 32 * 2) % 16)) % 16;
         H.anc64 = reinterpret_cast<double2 *>(q); q += 64 * 16;
         H.anc32 = reinterpret_cast<float2 *>(q); q += 64 * 8;
+        H.anc16 = reinterpret_cast<__half2 *>(q); q += 64 * 4;
         H.beta_s = reinterpret_cast<float *>(q); q += HG * 4;
         H.m_fin = reinterpret_cast<float *>(q); q += HG * 4;
         H.l_fin = reinterpret_cast<float *>(q); q += HG * 4;
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             sincos(a0, &s, &co);
             half_at(h).anc64[i] = make_double2(co, s);
             half_at(h).anc32[i] = make_float2((float)co, (float)s);
+            half_at(h).anc16[i] = __floats2half2_rn((float)co, (float)s);
         }
         sincos((double)(NHALF * kTileTokens) * th, &s, &co);
         rot64[i] = make_double2(co, s);
@@ -515,12 +518,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 
     if (warp < NCW) {
         // per-lane constants for the K phase: cis(j * theta_i) for this warp's KPW pairs
-        float t1c[KPW], t1s[KPW];
+        // as fp16 pairs t = (cos, sin) and t' = (-sin, cos): the tile rotation is then one
+        // HMUL2 + one HFMA2 per pair: (a.x t + a.y t') = (a.x cos - a.y sin, a.x sin + a.y cos)
+        __half2 t1h[KPW], t1r[KPW];
 #pragma unroll
         for (int k = 0; k < KPW; ++k) {
             const float2 v = t1tab[(hw * KPW + k) * 32 + lane];
-            t1c[k] = v.x;
-            t1s[k] = v.y;
+            t1h[k] = __floats2half2_rn(v.x, v.y);
+            t1r[k] = __floats2half2_rn(-v.y, v.x);
         }
         // this warp's K tables: base | (pair code << 2), + a constant per (head, pair); the
         // base is a multiple of NE*4 bytes (dynamic shared memory is 1 KB aligned)
@@ -655,10 +660,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
                 for (int k = 0; k < KPW; ++k) {
                     const int i = hw * KPW + k;
-                    const float2 an = anc32[i];
-                    const float cc = an.x * t1c[k] - an.y * t1s[k];
-                    const float ss = an.x * t1s[k] + an.y * t1c[k];
-                    const uint32_t cs = pack_half2(cc, ss);
+                    const __half2 an = H.anc16[i];
+                    const __half2 csh = __hfma2(__high2half2(an), t1r[k], __hmul2(__low2half2(an), t1h[k]));
+                    const uint32_t cs = *reinterpret_cast<const uint32_t *>(&csh);
                     const int b = 2 * BITS * k - 2;   // bit of (pair code << 2) in the window
 #pragma unroll
                     for (int h = 0; h < HKV; ++h) {
@@ -842,6 +846,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
                 H.anc64[htid] = b;
                 H.anc32[htid] = make_float2((float)b.x, (float)b.y);
+                H.anc16[htid] = __floats2half2_rn((float)b.x, (float)b.y);
             }
             half_sync(half);
             if (TIMED) { tc1 = clock64(); tm[4] += tc1 - tc0; tc0 = tc1; }
