@@ -125,7 +125,8 @@ def qnorm_codebook(xn: np.ndarray, cb):
     return apply_qnorm(cb, x.mean(), x.std(), q.mean(), q.std())
 
 
-def calibrate_layer(Kcal, Vcal, bits: int, ppm: int, qnorm: bool = False):
+def calibrate_layer(Kcal, Vcal, bits: int, ppm: int, qnorm: bool = False,
+                    fp16_codebooks: bool = True):
     """Everything kvq_cache_create needs for one layer (offline)."""
     lo, hi = key_thresholds(Kcal, ppm)
     cbK = key_codebook(Kcal, lo, hi, bits)
@@ -139,4 +140,11 @@ def calibrate_layer(Kcal, Vcal, bits: int, ppm: int, qnorm: bool = False):
         xk = ((K - z) / np.where(s > 0, s, 1.0))[kept]
         out["cbK_dec"] = qnorm_codebook(xk, cbK)
         out["cbV_dec"] = qnorm_codebook(value_normalized(Vcal, ppm), cbV)
+    if fp16_codebooks:
+        # codebooks stored in fp16, as the paper's LUTs ("all arithmetic is performed in
+        # fp16"); reading R23.  Strict ascent survives (k-means centroids are well separated).
+        for key in ("cbK", "cbV", "cbK_dec", "cbV_dec"):
+            cb = np.asarray(out[key], np.float32).astype(np.float16).astype(np.float32)
+            assert np.all(np.diff(cb) > 0), key
+            out[key] = cb
     return out

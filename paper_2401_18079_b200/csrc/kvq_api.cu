@@ -228,6 +228,10 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     double mids[32] = {0};
     for (int k = 0; k < 4; ++k)
         for (int j = 0; j < nlev; ++j) cb[16 * k + j] = cbs[k][j];
+    // R23: an fp16-exact Value decode codebook lets the attend kernel skip its residual pass
+    d.vcb_exact16 = 1;
+    for (int j = 0; j < nlev; ++j)
+        if (__half2float(__float2half_rn(cbs[3][j])) != cbs[3][j]) d.vcb_exact16 = 0;
     for (int j = 0; j + 1 < nlev; ++j) {
         mids[j] = (double)cbs[0][j] + (double)cbs[0][j + 1];
         mids[16 + j] = (double)cbs[2][j] + (double)cbs[2][j + 1];

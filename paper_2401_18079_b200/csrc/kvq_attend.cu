@@ -27,6 +27,7 @@
 #include "kvq_internal.cuh"
 
 #include <math_constants.h>
+#include <type_traits>
 
 namespace kvq {
 namespace {
@@ -769,27 +770,33 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     bw[s2][0] = vg < G ? w32[0] : 0u;
                     bw[s2][1] = vg < G ? w32[4] : 0u;
                 }
+                // the residual pass is skipped when the decode codebook is fp16-exact (R23)
+                auto pv = [&](auto with_lo) {
 #pragma unroll
-                for (int ml = 0; ml < MTW; ++ml) {
+                    for (int ml = 0; ml < MTW; ++ml) {
 #pragma unroll
-                    for (int s2 = 0; s2 < 2; ++s2) {
-                        uint32_t a[4], alo[4];
+                        for (int s2 = 0; s2 < 2; ++s2) {
+                            uint32_t a[4], alo[4];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const int bit = ((ml * 2 + s2) * 4 + r) * FB;
-                            const int wi = bit >> 5, sh = bit & 31;
-                            // (field & (NE-1)) << 7 with one shift (funnel when it straddles)
-                            uint32_t off;
-                            if (sh + FB <= 32) off = sh >= 7 ? (vr[wi] >> (sh - 7)) : (vr[wi] << (7 - sh));
-                            else off = __funnelshift_r(vr[wi], vr[wi + 1], sh - 7);
-                            const uint32_t ad = vlane4 | (off & ((NE - 1) << 7));
-                            a[r] = *reinterpret_cast<const uint32_t *>(vlut_b + ad);
-                            alo[r] = *reinterpret_cast<const uint32_t *>(vlut_b + NE * 32 * 4 + ad);
+                            for (int r = 0; r < 4; ++r) {
+                                const int bit = ((ml * 2 + s2) * 4 + r) * FB;
+                                const int wi = bit >> 5, sh = bit & 31;
+                                // (field & (NE-1)) << 7 with one shift (funnel when it straddles)
+                                uint32_t off;
+                                if (sh + FB <= 32) off = sh >= 7 ? (vr[wi] >> (sh - 7)) : (vr[wi] << (7 - sh));
+                                else off = __funnelshift_r(vr[wi], vr[wi + 1], sh - 7);
+                                const uint32_t ad = vlane4 | (off & ((NE - 1) << 7));
+                                a[r] = *reinterpret_cast<const uint32_t *>(vlut_b + ad);
+                                if constexpr (decltype(with_lo)::value)
+                                    alo[r] = *reinterpret_cast<const uint32_t *>(vlut_b + NE * 32 * 4 + ad);
+                            }
+                            mma_f16_f32(dacc[ml], a, bw[s2]);
+                            if constexpr (decltype(with_lo)::value) mma_f16_f32(dacc[ml], alo, bw[s2]);
                         }
-                        mma_f16_f32(dacc[ml], a, bw[s2]);
-                        mma_f16_f32(dacc[ml], alo, bw[s2]);
                     }
-                }
+                };
+                if (c.vcb_exact16) pv(std::false_type{});
+                else pv(std::true_type{});
             }
             // ---------------------------------------------------- a6: V outliers
             {

@@ -54,6 +54,7 @@ struct DevCache {
     // in token order.  Written by the quantizer next to the token-major CSC/CSR arrays
     // (which stay the canonical form for export and the overflow fallback).
     int NG, GW;             // head groups, channels per group
+    int vcb_exact16;        // 1: every Value decode codebook entry is an fp16 value (R23)
     int kcap_g, vcap_g;     // items per (tile, group)
     uint32_t *kit, *vit;    // [ntiles][NG][cap]
     uint32_t *gcnt;         // [ntiles][NG][2] counts; bit 31 = overflowed (use CSC/CSR)

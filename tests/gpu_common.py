@@ -8,11 +8,12 @@ import oracle as O
 from kvq_synth import calib, gen
 
 
-def setup_layer(seed, layer, H_q, H_kv, bits, ppm, T, n_cal=2048, qnorm=False, d=128):
+def setup_layer(seed, layer, H_q, H_kv, bits, ppm, T, n_cal=2048, qnorm=False, d=128,
+                fp16_codebooks=True):
     D = H_kv * d
     cal = calib.calibrate_layer(gen.gen_keys(seed, layer, n_cal, D, stream=gen.STREAM_CAL_K),
                                 gen.gen_values(seed, layer, n_cal, D, stream=gen.STREAM_CAL_V),
-                                bits, ppm, qnorm=qnorm)
+                                bits, ppm, qnorm=qnorm, fp16_codebooks=fp16_codebooks)
     K = gen.gen_keys(seed, layer, T, D)
     V = gen.gen_values(seed, layer, T, D)
     return cal, K, V

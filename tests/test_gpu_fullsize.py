@@ -25,12 +25,16 @@ def kvq():
     return K
 
 
-def test_c3_full_size_layer(kvq):
+@pytest.mark.parametrize("fp16_codebooks", [True, False])
+def test_c3_full_size_layer(kvq, fp16_codebooks):
+    """fp16_codebooks=False keeps the fp32 k-means centroids, which exercises the attend
+    kernel's residual pass for the V codebook (R23)."""
     w = CONFIGS["c3_nuq3"]
     T, D, H = w.T, w.D, w.H_q
     assert (T, D, H, w.bits) == (131072, 4096, 32, 3)
     cal = calib.calibrate_layer(gen.gen_keys(0, 0, 2048, D, stream=gen.STREAM_CAL_K),
-                                gen.gen_values(0, 0, 2048, D, stream=gen.STREAM_CAL_V), w.bits, w.ppm)
+                                gen.gen_values(0, 0, 2048, D, stream=gen.STREAM_CAL_V), w.bits, w.ppm,
+                                fp16_codebooks=fp16_codebooks)
     Kt = gen.gen_layer_torch(7, 0, T, D, "cpu", "K")
     Vt = gen.gen_layer_torch(8, 0, T, D, "cpu", "V")
     K = Kt.numpy()

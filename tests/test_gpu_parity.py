@@ -136,6 +136,24 @@ def test_attend_matches_oracle(kvq, H_q, H_kv, bits, T):
         assert err.max() < TOL, err
 
 
+@pytest.mark.parametrize("H_q,H_kv,bits,T", [(8, 8, 3, 1000), (4, 1, 3, 129), (2, 2, 4, 333),
+                                             (8, 8, 2, 517)])
+def test_attend_fp32_codebook(kvq, H_q, H_kv, bits, T):
+    """Decode codebooks that are not fp16 values take the residual pass (R23)."""
+    ppm = 10_000
+    cal, K, V = setup_layer(14, 0, H_q, H_kv, bits, ppm, T, fp16_codebooks=False)
+    assert np.any(cal["cbV_dec"].astype(np.float16).astype(np.float32) != cal["cbV_dec"])
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H_q, H_kv, bits, ppm, capacity=T + 64)
+    c.prefill(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    q = gen.gen_queries(14, 0, H_q, H_kv, 128)[0]
+    o = torch.zeros((H_q, 128), dtype=torch.float32, device="cuda")
+    c.attend(torch.from_numpy(q).cuda(), T, o)
+    torch.cuda.synchronize()
+    err = rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, T, H_q, H_kv))
+    assert err.max() < TOL, err
+
+
 @pytest.mark.parametrize("splits", [1, 2, 3, 7, 40])
 def test_attend_independent_of_split_count(kvq, splits):
     H, bits, ppm, T = 8, 3, 10_000, 1234
