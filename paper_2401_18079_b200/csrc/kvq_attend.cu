@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     }
     __syncthreads();
     // K tables: per (head, pair) bound of |A|,|B|.  The few pairs carrying a heavy Key
-    // channel (bound > 1/4 of the head max, at most HMAX per head) get fp32 tables and
+    // channel (bound > 1/2 of the head max, at most HMAX per head) get fp32 tables and
     // are accumulated in fp32; the rest use fp16 tables scaled by the largest remaining
     // bound.
     for (int x = tid; x < HG * 64; x += ATT_THREADS) {
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     for (int g = warp; g < HG; g += ATT_THREADS / 32) {
         const float b0 = bound_s[g * 64 + lane], b1 = bound_s[g * 64 + 32 + lane];
         const float M = warp_max(fmaxf(b0, b1));
-        float tau = 0.25f * M;
+        float tau = 0.5f * M;
         unsigned m0 = __ballot_sync(0xffffffffu, b0 > tau), m1 = __ballot_sync(0xffffffffu, b1 > tau);
         while (__popc(m0) + __popc(m1) > HMAX) {
             tau *= 1.25f;
