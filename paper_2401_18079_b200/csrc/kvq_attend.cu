@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         if (ti >= t_end) return;
         const uint32_t nk = cnt_nk, nv = cnt_nv;
         read_counts(hh, k + 1);
-        const int si = hh * SH + (k % SH);
+        const int si = hh * SH + (SH == 2 ? (k & 1) : (k % SH));
         unsigned char *sb = stage_ptr(si);
         uint64_t *bar = full_b + si;
         const bool kov = nk > (uint32_t)c.kcap_g, vov = nv > (uint32_t)c.vcap_g;
