@@ -125,7 +125,7 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     const int G = C.n_q_heads / C.n_kv_heads;
     if (G != 1 && G != 2 && G != 4 && G != 8) return fail(KVQ_ESHAPE, "GQA group must be 1, 2, 4 or 8");
     const int64_t D = (int64_t)C.n_kv_heads * C.head_dim;
-    if (D > 65535) return fail(KVQ_ESHAPE, "D = H_kv*d must fit a 16-bit channel index");
+    if (D > 8192) return fail(KVQ_ESHAPE, "this build supports D = H_kv*d <= 8192 (got %lld)", (long long)D);
     if (C.capacity_tokens < 1) return fail(KVQ_EINVAL, "capacity_tokens must be >= 1");
     if (!(C.rope_theta > 0) || !std::isfinite(C.rope_theta)) return fail(KVQ_EINVAL, "rope_theta must be > 0");
     if (C.pos_base < 0) return fail(KVQ_EINVAL, "pos_base must be >= 0");

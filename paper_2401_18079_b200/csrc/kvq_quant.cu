@@ -33,18 +33,16 @@ __device__ __forceinline__ uint16_t f16_order_key(uint16_t h) {
 __device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 
 // Exact ENC (R8): count of midpoints with 2(y-z) > s*m_j.
+// The predicate 2(y-z) > s*m_j is true exactly for j < code (m ascending, s >= 0), so the
+// count is found in log2(NLEV) steps: code += step when the predicate holds at code+step-1.
 template <int NM>
 __device__ __forceinline__ int enc_fp64(double y, double s, double z, const double *mids) {
     const double lhs = 2.0 * __dsub_rn(y, z);
-    int lo = 0, hi = NM;
+    int code = 0;
 #pragma unroll
-    for (int it = 0; it < 5; ++it) {
-        if (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if (lhs > __dmul_rn(s, mids[mid])) lo = mid + 1; else hi = mid;
-        }
-    }
-    return lo;
+    for (int step = (NM + 1) / 2; step >= 1; step >>= 1)
+        if (lhs > __dmul_rn(s, mids[code + step - 1])) code += step;
+    return code;
 }
 
 // Block-wide exclusive scan of one int per thread; returns exclusive prefix, *total.
@@ -125,8 +123,11 @@ __device__ void radix_select16(const uint16_t *keys, const uint8_t *flags, int D
             bool valid = c < D && !flags[c];
             int kk = 0;
             if (valid) kk = desc ? keys[c] : (0xffff - keys[c]);
-            if (pass == 1) valid = valid && ((kk >> 8) == prefix_hi);
-            hist_add(hist, pass == 0 ? (kk >> 8) : (kk & 0xff), valid);
+            if (pass == 0) {
+                hist_add(hist, kk >> 8, valid);   // top bytes cluster: aggregate per warp
+            } else if (valid && (kk >> 8) == prefix_hi) {
+                atomicAdd(&hist[kk & 0xff], 1);   // few candidates, spread low bytes
+            }
         }
         __syncthreads();
         if (threadIdx.x < 32) select_bin(hist, need - gt, shared_out);
@@ -183,11 +184,13 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
 
     // ------------------------------------------------------------------ Keys
     int kcnt = 0;
+    uint32_t kmask = 0;   // outlier flags of this thread's channels (E <= 32)
     for (int ch = cb0; ch < cb1; ++ch) {
         float x = h2f(xk[ch]);
         float lo = klo[ch], hi = khi[ch];
         bool out = (x < lo) || (x > hi);
         kcnt += out;
+        kmask |= (uint32_t)out << (ch - cb0);
         if (mode != 1) {
             float y = x < lo ? lo : (x > hi ? hi : x);
             kc[ch] = (uint8_t)enc_fp64<NM>((double)y, (double)ks[ch], (double)kz[ch], s_mk);
@@ -222,10 +225,9 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         __syncthreads();
         if (s_ok) {
             uint32_t pos = s_base + (uint32_t)krank;
-            for (int ch = cb0; ch < cb1; ++ch) {
-                float x = h2f(xk[ch]);
-                if ((x < klo[ch]) || (x > khi[ch]))
-                    c.kout[pos++] = (uint32_t)ch | ((uint32_t)xk[ch] << 16);
+            for (uint32_t m = kmask; m; m &= m - 1) {
+                const int ch = cb0 + __ffs(m) - 1;
+                c.kout[pos++] = (uint32_t)ch | ((uint32_t)xk[ch] << 16);
             }
         }
     }
@@ -259,13 +261,11 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
             const int tile0 = (int)(n >> 5), jj0 = (int)(n & 31);
             int pos = gbk[myg] + (krank - gfirst[myg]);
             uint32_t *dst = c.kit + ((int64_t)tile0 * c.NG + myg) * c.kcap_g;
-            for (int ch = cb0; ch < cb1; ++ch) {
-                float x = h2f(xk[ch]);
-                if ((x < klo[ch]) || (x > khi[ch])) {
-                    if (pos < c.kcap_g)
-                        dst[pos] = ((uint32_t)xk[ch] << 16) | ((uint32_t)jj0 << 11) | (uint32_t)(ch - myg * c.GW);
-                    ++pos;
-                }
+            for (uint32_t m = kmask; m; m &= m - 1) {
+                const int ch = cb0 + __ffs(m) - 1;
+                if (pos < c.kcap_g)
+                    dst[pos] = ((uint32_t)xk[ch] << 16) | ((uint32_t)jj0 << 11) | (uint32_t)(ch - myg * c.GW);
+                ++pos;
             }
         }
     }
