@@ -82,7 +82,7 @@ typedef struct {
     const float *key_lo, *key_hi;
 } kvq_params;
 
-/* Create a layer cache.  Validates: bits, ppm, D = H_kv*d, d == 128, H_q % H_kv,
+/* Create a layer cache.  Validates: bits, ppm, D = H_kv*d <= 8192, d == 128, H_q % H_kv,
  * strictly ascending finite codebooks, finite lo <= hi, k < D, capacity > 0.
  * Allocates every device buffer up front.  Returns KVQ_EINVAL / KVQ_ESHAPE /
  * KVQ_ECUDA (allocation) on failure with *out untouched. */
