@@ -144,6 +144,17 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     return v;
 }
 
+// G consecutive 32-bit shared words (G = 2 or 4) in one vector load
+template <int G>
+__device__ __forceinline__ void lds_vec(uint32_t addr, uint32_t (&v)[G]) {
+    if constexpr (G == 2) {
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(addr));
+    } else {
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(addr));
+    }
+}
+
 // warp max of floats with one REDUX via an order-preserving integer map
 __device__ __forceinline__ float warp_max_redux(float v) {
     unsigned u = __float_as_uint(v);
@@ -402,7 +413,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
         const float qa = qa1 * sc, qb = qb1 * sc;
         const float yb = cbK[bb] * ks_s[cj] + kz_s[cj];
-        uint32_t *dst = klut + (size_t)(g * 64 + i) * NE + (bb << BITS);
+        // MHA: [g][i][pc]; GQA: the G query heads of a KV head interleaved per code,
+        // [h][i][pc][G], so one vector load serves all G heads in the K phase
+        uint32_t *dst = G == 1 ? klut + (size_t)(g * 64 + i) * NE + (bb << BITS)
+                               : klut + ((size_t)((g / G) * 64 + i) * NE + (bb << BITS)) * G + (g % G);
         const bool heavy = heavy_s[gi] != 0;
         int hslot = 0;
         if (heavy)
@@ -411,11 +425,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         for (int a = 0; a <= CM; ++a) {
             const float xa = cbK[a] * ks_s[ci] + kz_s[ci];
             if (heavy) {
-                dst[a] = 0u;
+                dst[a * G] = 0u;
                 hlut[(g * HMAX + hslot) * NE + (bb << BITS) + a] =
                     make_float2(qa1 * xa + qb1 * yb, qb1 * xa - qa1 * yb);
             } else {
-                dst[a] = pack_half2(qa * xa + qb * yb, qb * xa - qa * yb);
+                dst[a * G] = pack_half2(qa * xa + qb * yb, qb * xa - qa * yb);
             }
         }
     }
@@ -530,8 +544,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         }
         // this warp's K tables: base | (pair code << 2), + a constant per (head, pair); the
         // base is a multiple of NE*4 bytes (dynamic shared memory is 1 KB aligned)
-        const uint32_t klut_w = smem_u32(klut) + (uint32_t)(hw * KPW * NE * 4);
-        if (klut_w & (NE * 4u - 1u)) __trap();
+        const uint32_t klut_w = smem_u32(klut) + (uint32_t)(hw * KPW * NE * 4 * G);
+        if (klut_w & (NE * 4u * G - 1u)) __trap();
         const int kbit0 = 2 * BITS * KPW * hw;
         const int kq0 = kbit0 >> 5, kshift = kbit0 & 31;
         const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
@@ -672,12 +686,18 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                         else if (b + 2 * BITS + 2 <= 32) off = wl[h] >> b;
                         else if (b >= 32) off = wh[h] >> (b - 32);
                         else off = __funnelshift_r(wl[h], wh[h], b);
-                        const uint32_t a = klut_w | (off & ((NE - 1) << 2));
+                        if constexpr (G == 1) {
+                            const uint32_t a = klut_w | (off & ((NE - 1) << 2));
+                            const uint32_t ab = lds_u32(a + (uint32_t)((h * 64 + k) * NE * 4));
+                            fma2_f16_f32(ab, cs, acc_c[h], acc_s[h]);
+                        } else {
+                            // entries of the G heads are adjacent: (code << 2) << log2(G)
+                            constexpr int LG = G == 2 ? 1 : 2;
+                            const uint32_t a = klut_w | ((off << LG) & ((NE - 1) << (2 + LG)));
+                            uint32_t ab[G];
+                            lds_vec<G>(a + (uint32_t)((h * 64 + k) * NE * 4 * G), ab);
 #pragma unroll
-                        for (int gg = 0; gg < G; ++gg) {
-                            const int g = h * G + gg;
-                            const uint32_t ab = lds_u32(a + (uint32_t)((g * 64 + k) * NE * 4));
-                            fma2_f16_f32(ab, cs, acc_c[g], acc_s[g]);
+                            for (int gg = 0; gg < G; ++gg) fma2_f16_f32(ab[gg], cs, acc_c[h * G + gg], acc_s[h * G + gg]);
                         }
                     }
                 }
