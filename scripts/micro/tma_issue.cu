@@ -1,3 +1,4 @@
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/micro/tma_issue scripts/micro/tma_issue.cu
 // Microbenchmark: cost of issuing 1-D bulk copies (cp.async.bulk) from one thread, and the
 // copy completion time, per SM, with all 148 SMs loading from HBM at once.
 #include <cstdio>
