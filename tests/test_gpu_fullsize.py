@@ -61,3 +61,33 @@ def test_c3_full_size_layer(kvq, fp16_codebooks):
     err = rel_err_per_head(o.cpu().numpy(), exp)
     print("C3 full-size per-head max rel err: max %.3g median %.3g" % (err.max(), np.median(err)))
     assert err.max() < TOL, err
+
+
+@pytest.mark.parametrize("wname,T", [("c4", 65536), ("c5", 65536)])
+def test_large_gqa_and_qnorm_layers(kvq, wname, T):
+    """C4 (Mistral GQA 32/8, 3-bit) and C5 (2-bit, Q-Norm decode codebooks) layer shapes at
+    65536 tokens, the bench launch configuration; every head against the oracle."""
+    w = CONFIGS[wname]
+    D, H, Hk = w.D, w.H_q, w.H_kv
+    cal = calib.calibrate_layer(gen.gen_keys(1, 0, 2048, D, stream=gen.STREAM_CAL_K),
+                                gen.gen_values(1, 0, 2048, D, stream=gen.STREAM_CAL_V), w.bits, w.ppm,
+                                qnorm=w.qnorm)
+    Kt = gen.gen_layer_torch(17, 0, T, D, "cpu", "K", param_seed=1)
+    Vt = gen.gen_layer_torch(18, 0, T, D, "cpu", "V", param_seed=1)
+    c = make_cache(kvq, cal, H, Hk, w.bits, w.ppm, capacity=T + 32)
+    c.prefill(Kt.cuda(), Vt.cuda())
+    c.sync()
+    ref = O.prefill(Kt.numpy(), Vt.numpy(), cal["key_lo"], cal["key_hi"], cal["cbK"], cal["cbV"], w.ppm,
+                    kcap=64 * T)
+    e = c.export(T - 40, T)
+    np.testing.assert_array_equal(e["kcodes"].astype(np.uint16), ref.kcodes[T - 40:])
+    np.testing.assert_array_equal(e["vcodes"].astype(np.uint16), ref.vcodes[T - 40:])
+    q = gen.gen_queries(19, 0, H, Hk, 128)[0]
+    o = torch.zeros((H, 128), dtype=torch.float32, device="cuda")
+    c.attend(torch.from_numpy(q).cuda(), T, o)
+    torch.cuda.synchronize()
+    exp = O.attend(ref, q, T, H_q=H, H_kv=Hk, d=128, key_lo=cal["key_lo"], key_hi=cal["key_hi"],
+                   cbK_dec=cal["cbK_dec"], cbV_dec=cal["cbV_dec"], pos_base=0, nthreads=0)
+    err = rel_err_per_head(o.cpu().numpy(), exp)
+    print("%s T=%d per-head max rel err: max %.3g median %.3g" % (wname, T, err.max(), np.median(err)))
+    assert err.max() < TOL, err
