@@ -604,7 +604,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 const int nk = hdr[0];
                 // Key-outlier corrections straight into the (head, token) score term, in fixed
                 // point (native shared integer atomics; see kfix_of)
-                for (int x = htid; x < nk; x += HT) {
+                // items interleaved over the warps (item x -> warp x % HW) so every warp of the
+                // half carries the same share and reaches the K barrier together
+                const int ix = lane * HW + hw;
+                for (int x = ix; x < nk; x += HT) {
                     const uint32_t itm = kit[x];
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
