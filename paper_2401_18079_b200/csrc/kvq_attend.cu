@@ -27,6 +27,7 @@
 #include "kvq_internal.cuh"
 
 #include <math_constants.h>
+#include <cstdlib>
 #include <type_traits>
 
 namespace kvq {
@@ -580,7 +581,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             // K-outlier correction of one item: (x - K^(code)) * dscore/dK for query head
             // kvl*G + gg, in fp32
             auto k_corr = [&](uint32_t itm, int gg, int &j_out, int &g_out) -> float {
-                const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x1ffu);
                 const int kvl = chl >> 7, cc = chl & 127, i = cc & 63, up = cc >> 6;
                 const int bit = 2 * BITS * i;
                 const int wq = kvl * 4 * BITS + (bit >> 5);
@@ -749,7 +750,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     float mx = 0.f;
                     for (int x = htid - HG * 32; x < nvi; x += HT - HG * 32) {
                         const uint32_t itm = vit[x];
-                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x1ffu);
                         const int kvl = chl >> 7, cc = chl & 127;
                         const int bit = vf_bit(j, cc, BITS);
                         const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
@@ -824,7 +825,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
             // ---------------------------------------------------- a6: V outliers
             {
                 auto v_item = [&](uint32_t itm) {
-                    const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                    const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x1ffu);
                     const int kvl = chl >> 7, cc = chl & 127;
                     const int bit = vf_bit(j, cc, BITS);
                     const uint32_t *vwp = vw_s + (kvl * 4 * BITS + (bit >> 5)) * 32 + vf_lane(j, cc);
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     if (htid == 0) H.vscale[0] = pow2i(emx - 24);   // 1/S
                     for (int x = htid; x < nvi; x += HT) {
                         const uint32_t itm = vit[x];
-                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x7ffu);
+                        const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x1ffu);
                         const int kvl = chl >> 7, cc = chl & 127;
                         const float dS = H.vdel[x] * S;
 #pragma unroll
@@ -1114,6 +1115,12 @@ cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_us
     P.timers = a.timers;
     const int grid = (c.H_q / hg) * S;
     if (splits_used) *splits_used = S;
+    // MHA at 2-3 bits: the warp-autonomous kernel (kvq_attend_wa.cu); KVQ_ATT_LEGACY=1 or the
+    // phase-timer diagnostics select the two-halves kernel below
+    if (!a.timers && attend_wa_supported(c)) {
+        static const bool legacy = getenv("KVQ_ATT_LEGACY") != nullptr;
+        if (!legacy) return launch_attend_wa(c, a, S, s);
+    }
     switch (c.bits) {
         case 2: return launch_b<2>(c, P, hg, grid, s);
         case 3: return launch_b<3>(c, P, hg, grid, s);

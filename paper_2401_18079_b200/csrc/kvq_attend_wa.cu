@@ -1,0 +1,792 @@
+// kvq_attend_wa.cu -- ATT, warp-autonomous variant for multi-head attention (G = 1) at 2 and
+// 3 bits: single-token decode attention over the compressed cache.
+//
+// Why a second kernel: the two-halves kernel (kvq_attend.cu) splits every 32-token tile over
+// 8 warps (RoPE pairs over warps, then a cross-warp score reduction, a softmax phase on 4 of
+// the 8 warps and a P.V phase), i.e. three barriers and ~2,000 bookkeeping instructions per
+// tile; ncu showed it issue- and latency-bound at IPC ~2.1 (profiles/r1_att_kernel.md).  Here
+// each warp owns whole tiles of the CTA's 4 query heads and runs the complete method on them
+// with no block-level synchronisation in the tile loop:
+//   a1   (prologue, per CTA) q~ = RoPE(q, pos) with exact fp64 angles (R11, R12) times
+//        log2(e)/sqrt(d); per (head, RoPE pair i) a 2^{2b}-entry table of fp16 pairs
+//        (A, B) = the paper's per-channel LUT with the query and the affine
+//        folded in, so one lookup + 2 FMAs give cos(n' th_i) A + sin(n' th_i) B, the pair's
+//        share of q~ . RoPE(K^_n, n') (RoPE after dequantization);
+//   a2   lane = token: per pair one rotation cis(t0 th_i) x cis(j th_i) (fp16x2, shared by
+//        the 4 heads) and per head one table lookup + 2 fp16 x fp16 -> fp32 FMAs;
+//   a3   Key outliers (items bucketed per tile and head group by the quantizer) and the
+//        few "heavy" pairs (fp32 tables) in fp32, lane-parallel;
+//   a4   online softmax per head in base 2 with shuffles only;
+//   a5   P.V on the tensor cores: mma.m16n8k16, A = Value codes (stored in A-fragment
+//        order) through the shared codebook pair table, B = fp16 weights p s_n 2^(14-E)
+//        (every column the same head, so each lane ends with rows g, g+8 of the product),
+//        Sum_n p_n z_n as a per-lane scalar (affine fold);
+//   a6   Value outliers p_n (x - V^(code)) lane-parallel into per-warp shared sums;
+//   a7   warp partials -> CTA partial (log-sum-exp) -> split merge by the last CTA.
+// Data reach the warp straight from HBM into registers (K words of the next tile during the
+// current P.V, V words during the current K phase), so there is no shared staging ring and
+// no producer warp.
+#include "kvq_internal.cuh"
+
+#include <math_constants.h>
+
+#include <cstdlib>
+
+namespace kvq {
+namespace {
+
+constexpr int WEXP = 14;   // fp16 P.V weights scaled into [0, 2^14]
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+// acc += lo(x)*lo(y) ; acc2 += hi(x)*hi(y)   (fp16 products, fp32 accumulation)
+__device__ __forceinline__ void fma2_f16_f32(uint32_t x, uint32_t y, float &acc, float &acc2) {
+    asm("{\n\t.reg .b16 x0, x1, y0, y1;\n\t"
+        "mov.b32 {x0, x1}, %2;\n\t"
+        "mov.b32 {y0, y1}, %3;\n\t"
+        "fma.rn.f32.f16 %0, x0, y0, %0;\n\t"
+        "fma.rn.f32.f16 %1, x1, y1, %1;\n\t}"
+        : "+f"(acc), "+f"(acc2)
+        : "r"(x), "r"(y));
+}
+__device__ __forceinline__ void mma_f16_f32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+    __half2 h = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// warp max of floats with one REDUX via an order-preserving integer map
+__device__ __forceinline__ float warp_max_redux(float v) {
+    unsigned u = __float_as_uint(v);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    u = __reduce_max_sync(0xffffffffu, u);
+    u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+    return __uint_as_float(u);
+}
+__device__ __forceinline__ float pow2i(int k) {
+    k = max(-126, min(127, k));
+    return __int_as_float((k + 127) << 23);
+}
+__device__ __forceinline__ int ilog2f(float x) { return ((__float_as_int(x) >> 23) & 255) - 127; }
+
+constexpr int HG = 4;      // query heads per CTA (MHA: 4 KV heads, one outlier bucket group)
+constexpr int NSTREAM = 8; // tile streams per CTA (warps sharing a stream take other heads)
+
+// Key-outlier score terms in fixed point: 2^-16 log2-score units, |term| < 2^15
+constexpr float kKfixScale = 65536.f;
+__device__ __forceinline__ int kfix_of(float v) {
+    return __float2int_rn(fminf(fmaxf(v, -32768.f), 32767.f) * kKfixScale);
+}
+// a value the compiler cannot see through (keeps table bases OR-able instead of re-added)
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(x));
+    return x;
+}
+
+template <int BITS, bool RESID, int WH>
+struct WCfg {
+    static constexpr int NWARP = NSTREAM * (HG / WH);
+    static constexpr int NTHR = NWARP * 32;
+    static constexpr int IPL = 8;                         // bucket items per lane in registers
+    static constexpr int NE = 1 << (2 * BITS);
+    static constexpr int KWH = 4 * BITS;                  // code words per head per token
+    static constexpr int HMAX = 8;                        // fp32 "heavy" pairs per head
+    static constexpr size_t valign = (size_t)NE * 32 * 4;  // V table alignment (OR addressing)
+    static constexpr size_t vlut = (size_t)(RESID ? 2 : 1) * NE * 32 * 4;
+    static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
+    static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
+    static constexpr size_t t1h = (size_t)kPairs * 32 * 4;    // cis(j th_i) fp16x2 [i][j]
+    static constexpr size_t t1f = (size_t)kPairs * 32 * 8;    // cis(j th_i) fp32 [i][j]
+    // per warp: K words of the tile (after the K phase: p and the V-outlier fixed-point
+    // sums), K-outlier fixed-point terms, anchors (fp16 rotation pairs, fp64 state)
+    static constexpr size_t w_kst = (size_t)WH * KWH * 32 * 4;
+    static constexpr size_t w_bytes = w_kst + WH * 32 * 4 + 64 * 8 * 2 + 64 * 16;
+    static_assert(w_kst >= (size_t)WH * (32 + kHeadDim) * 4, "aliases fit in kst");
+    static constexpr size_t small = HG * kHeadDim * 4 /* qs */ + 64 * 16 /* rot */
+        + HG * kHeadDim * 4 * 2 /* ks, kz */ + 64 * 4 /* cb */ + HG * 64 * 4 /* bound */
+        + HG * 64 /* heavy flags */ + HG * 8 * 4 * 2 /* heavy lists */ + HG * 4 * 2 + 64;
+    static constexpr size_t total = valign + vlut + klut + hlut + t1h + t1f + NWARP * w_bytes + small;
+};
+
+struct WParams {
+    const __half *q;
+    int64_t pos, T;
+    int S, ntiles;
+    float *out, *parts;
+    unsigned *tickets;
+    int write_partial;
+};
+
+template <int BITS, bool RESID, int WH>
+__global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(DevCache c, WParams P) {
+    using C = WCfg<BITS, RESID, WH>;
+    constexpr int NWARP = C::NWARP, NTHR = C::NTHR, IPL = C::IPL;
+    constexpr int NE = C::NE;
+    constexpr int CM = (1 << BITS) - 1;
+    constexpr int KWH = C::KWH;
+    constexpr int HMAX = C::HMAX;
+    constexpr int FB = 2 * BITS;   // bits of one pair / A field
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // the V table starts at a multiple of its size in the shared window, so a lookup address
+    // is (base | code << 7 | lane << 2) with one LOP3
+    const uint32_t s0 = smem_u32(smem_raw);
+    unsigned char *sp = smem_raw + ((C::valign - (s0 % C::valign)) % C::valign);
+    uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
+    uint32_t *klut = reinterpret_cast<uint32_t *>(sp); sp += C::klut;
+    float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
+    uint32_t *t1h = reinterpret_cast<uint32_t *>(sp); sp += C::t1h;
+    float2 *t1f = reinterpret_cast<float2 *>(sp); sp += C::t1f;
+    unsigned char *wbase = sp; sp += NWARP * C::w_bytes;
+    float *qs = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
+    double2 *rot = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    float *ks_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
+    float *kz_s = reinterpret_cast<float *>(sp); sp += HG * kHeadDim * 4;
+    float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;
+    float *bound_s = reinterpret_cast<float *>(sp); sp += HG * 64 * 4;
+    uint8_t *heavy_s = reinterpret_cast<uint8_t *>(sp); sp += HG * 64;
+    int *hv_pair = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
+    int *hv_n = reinterpret_cast<int *>(sp); sp += HG * 8 * 4;
+    float *lut_sc = reinterpret_cast<float *>(sp); sp += HG * 4;
+    float *lut_inv = reinterpret_cast<float *>(sp); sp += HG * 4;
+    int *flag_s = reinterpret_cast<int *>(sp); sp += 64;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_hg = c.H_q / HG;
+    const int hg = blockIdx.x % n_hg;
+    const int split = blockIdx.x / n_hg;
+    const int g0 = hg * HG;               // first query head of the CTA = first KV head (G = 1)
+    const int hw0 = (warp % (HG / WH)) * WH;   // this warp's first head within the CTA
+    const int stream = warp / (HG / WH);
+    const int t_begin = (int)((int64_t)split * P.ntiles / P.S);
+    const int t_end = (int)((int64_t)(split + 1) * P.ntiles / P.S);
+    const int D = c.D;
+    const int c_lo = g0 * kHeadDim;
+    const float *cbK = c.cb + 16, *cbV = c.cb + 48;   // decode codebooks
+
+    // per-warp scratch
+    unsigned char *wp = wbase + warp * C::w_bytes;
+    uint32_t *kst = reinterpret_cast<uint32_t *>(wp); wp += C::w_kst;
+    float *ps = reinterpret_cast<float *>(kst);                 // alias after the K phase
+    int *vfix = reinterpret_cast<int *>(kst) + WH * 32;         // alias after the K phase
+    int *kfix = reinterpret_cast<int *>(wp); wp += WH * 32 * 4;
+    uint2 *anc16 = reinterpret_cast<uint2 *>(wp); wp += 64 * 8;
+    float2 *anc32 = reinterpret_cast<float2 *>(wp); wp += 64 * 8;
+    double2 *anc64 = reinterpret_cast<double2 *>(wp);
+
+    // ------------------------------------------------------------- first tile's data
+    // issued before the table build so the HBM latency overlaps the prologue
+    const int t_first = t_begin + stream;
+    uint32_t kw[WH][KWH];
+    uint32_t kitm[IPL], vitm[IPL];
+    uint32_t cnt_k = 0, cnt_v = 0, ncnt_k = 0, ncnt_v = 0;
+    float2 vsz = make_float2(0.f, 0.f);
+    auto load_k = [&](int t) {
+#pragma unroll
+        for (int h = 0; h < WH; ++h)
+#pragma unroll
+            for (int w = 0; w < KWH; ++w)
+                kw[h][w] = __ldg(c.kcodes + ((int64_t)t * c.QW + (g0 + hw0 + h) * KWH + w) * 32 + lane);
+    };
+    auto load_counts = [&](int t, uint32_t &nk, uint32_t &nv) {
+        nk = nv = 0;
+        if (t < t_end) {
+            const uint32_t *gc = c.gcnt + ((int64_t)t * c.NG + hg) * 2;
+            nk = __ldg(gc);
+            nv = __ldg(gc + 1);
+        }
+    };
+    // Items of a (tile, 4-head group) bucket are in (token, channel) order; a warp keeps the
+    // whole bucket (IPL per lane) and skips the other heads' items.
+    auto load_items = [&](int t) {
+        const int64_t bucket = (int64_t)t * c.NG + hg;
+        const uint32_t nk = cnt_k > (uint32_t)c.kcap_g ? 0u : cnt_k;
+        const uint32_t nv = cnt_v > (uint32_t)c.vcap_g ? 0u : cnt_v;
+#pragma unroll
+        for (int k = 0; k < IPL; ++k) {
+            const uint32_t x = lane + 32 * k;
+            kitm[k] = x < nk ? __ldg(c.kit + bucket * c.kcap_g + x) : 0u;
+            vitm[k] = x < nv ? __ldg(c.vit + bucket * c.vcap_g + x) : 0u;
+        }
+        vsz = (int64_t)t * 32 + lane < P.T ? __ldg(c.vsz + (int64_t)t * 32 + lane) : make_float2(0.f, 0.f);
+    };
+    if (t_first < t_end) {
+        load_k(t_first);
+        load_counts(t_first, cnt_k, cnt_v);
+        load_items(t_first);
+        load_counts(t_first + NSTREAM, ncnt_k, ncnt_v);
+    }
+
+    // ---------------------------------------------------------------- prologue (a1)
+    if (tid < 64) {
+        const int i = tid;
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)(NSTREAM * kTileTokens) * th, &s, &co);
+        rot[i] = make_double2(co, s);
+    }
+    for (int x = tid; x < kPairs * 32; x += NTHR) {
+        const int i = x >> 5, j = x & 31;
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)j * th, &s, &co);
+        t1f[x] = make_float2((float)co, (float)s);
+        t1h[x] = pack_half2((float)co, (float)s);
+    }
+    // this warp's anchors cis((pos_base + 32 t_first) th_i), fp64 (advanced per tile)
+    for (int i = lane; i < 64; i += 32) {
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)(c.pos_base + (int64_t)t_first * kTileTokens) * th, &s, &co);
+        anc64[i] = make_double2(co, s);
+        anc32[i] = make_float2((float)co, (float)s);
+        anc16[i] = make_uint2(pack_half2((float)co, (float)s), pack_half2(-(float)s, (float)co));
+    }
+    for (int x = lane; x < WH * 32; x += 32) kfix[x] = 0;
+    for (int x = tid; x < HG * kHeadDim; x += NTHR) {
+        ks_s[x] = c.kpar[c_lo + x];
+        kz_s[x] = c.kpar[D + c_lo + x];
+    }
+    if (tid < 64) cb_s[tid] = c.cb[tid];
+    if (tid < 16) flag_s[tid] = 0;
+    const double qscale = 1.4426950408889634 / sqrt((double)kHeadDim);
+    for (int x = tid; x < HG * 64; x += NTHR) {
+        const int g = x >> 6, i = x & 63;
+        const __half *qg = P.q + (int64_t)(g0 + g) * kHeadDim;
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)P.pos * th, &s, &co);
+        const double a = (double)__half2float(qg[i]), b = (double)__half2float(qg[i + 64]);
+        qs[g * kHeadDim + i] = (float)((a * co - b * s) * qscale);
+        qs[g * kHeadDim + i + 64] = (float)((b * co + a * s) * qscale);
+    }
+    __syncthreads();
+    // per (head, pair) bound of |A|, |B|: pairs above 1/2 of the head maximum (at most HMAX)
+    // get fp32 tables; the rest fp16 tables scaled so the largest entry is <= 2^14
+    for (int x = tid; x < HG * 64; x += NTHR) {
+        const int g = x >> 6, i = x & 63;
+        const int ci = g * kHeadDim + i, cj = ci + 64;
+        const float mx = fmaxf(fabsf(cbK[0] * ks_s[ci] + kz_s[ci]), fabsf(cbK[CM] * ks_s[ci] + kz_s[ci]));
+        const float my = fmaxf(fabsf(cbK[0] * ks_s[cj] + kz_s[cj]), fabsf(cbK[CM] * ks_s[cj] + kz_s[cj]));
+        const float qa = fabsf(qs[g * kHeadDim + i]), qb = fabsf(qs[g * kHeadDim + i + 64]);
+        bound_s[x] = fmaxf(qa * mx + qb * my, qb * mx + qa * my);
+    }
+    __syncthreads();
+    for (int g = warp; g < HG; g += NWARP) {
+        const float b0 = bound_s[g * 64 + lane], b1 = bound_s[g * 64 + 32 + lane];
+        const float M = warp_max(fmaxf(b0, b1));
+        float tau = 0.5f * M;
+        unsigned m0 = __ballot_sync(0xffffffffu, b0 > tau), m1 = __ballot_sync(0xffffffffu, b1 > tau);
+        while (__popc(m0) + __popc(m1) > HMAX) {
+            tau *= 1.25f;
+            m0 = __ballot_sync(0xffffffffu, b0 > tau);
+            m1 = __ballot_sync(0xffffffffu, b1 > tau);
+        }
+        const unsigned lt = (1u << lane) - 1u;
+        const int n0c = __popc(m0);
+        if ((m0 >> lane) & 1u) hv_pair[g * 8 + __popc(m0 & lt)] = lane;
+        if ((m1 >> lane) & 1u) hv_pair[g * 8 + n0c + __popc(m1 & lt)] = lane + 32;
+        heavy_s[g * 64 + lane] = (m0 >> lane) & 1u;
+        heavy_s[g * 64 + 32 + lane] = (m1 >> lane) & 1u;
+        const float rest = warp_max(fmaxf(((m0 >> lane) & 1u) ? 0.f : b0, ((m1 >> lane) & 1u) ? 0.f : b1));
+        if (lane == 0) {
+            hv_n[g] = n0c + __popc(m1);
+            int e = 0;
+            if (rest > 0.f && isfinite(rest)) e = 14 - ilogbf(rest) - 1;
+            e = max(-100, min(100, e));
+            lut_sc[g] = ldexpf(1.f, e);
+            lut_inv[g] = ldexpf(1.f, -e);
+        }
+    }
+    __syncthreads();
+    // K table entries [g][i][pair code], one (head, pair, second code) row per work item
+    for (int x = tid; x < HG * 64 * (CM + 1); x += NTHR) {
+        const int bb = x % (CM + 1), gi = x / (CM + 1);
+        const int g = gi >> 6, i = gi & 63;
+        const int ci = g * kHeadDim + i, cj = ci + 64;
+        const float sc = lut_sc[g];
+        const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
+        const float qa = qa1 * sc, qb = qb1 * sc;
+        const float yb = cbK[bb] * ks_s[cj] + kz_s[cj];
+        uint32_t *dst = klut + (size_t)(g * 64 + i) * NE + (bb << BITS);
+        const bool heavy = heavy_s[gi] != 0;
+        int hslot = 0;
+        if (heavy)
+            for (int u = 0; u < hv_n[g]; ++u) hslot = hv_pair[g * 8 + u] == i ? u : hslot;
+#pragma unroll
+        for (int a = 0; a <= CM; ++a) {
+            const float xa = cbK[a] * ks_s[ci] + kz_s[ci];
+            if (heavy) {
+                dst[a] = 0u;
+                hlut[(g * HMAX + hslot) * NE + (bb << BITS) + a] = make_float2(qa1 * xa + qb1 * yb, qb1 * xa - qa1 * yb);
+            } else {
+                dst[a] = pack_half2(qa * xa + qb * yb, qb * xa - qa * yb);
+            }
+        }
+    }
+    // V table: lane-private copies (entry e of lane l at word e*32 + l): the fp16 codebook
+    // pair and (RESID) its fp16 residual Chat - fp16(Chat) (R23)
+    for (int x = tid; x < NE * 32; x += NTHR) {
+        const int e = x >> 5;
+        const float ca = cbV[e & CM], cb = cbV[e >> BITS];
+        vlut[x] = pack_half2(ca, cb);
+        if constexpr (RESID)
+            vlut[NE * 32 + x] = pack_half2(ca - __half2float(__float2half_rn(ca)), cb - __half2float(__float2half_rn(cb)));
+    }
+    __syncthreads();
+
+    // ================================================================ tile loop (per warp)
+    // table bases, OR-ed with the shifted codes (the compiler must not turn the OR into an add)
+    const uint32_t klut_u = opaque(smem_u32(klut) + (uint32_t)(hw0 * 64 * NE * 4));
+    const uint32_t vlut_u = opaque(smem_u32(vlut) | (4u * lane));
+    const int vg = lane >> 2, vt = lane & 3;
+    const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
+    float m_run[WH], l_lane[WH], z_lane[WH], acc[WH][4];
+#pragma unroll
+    for (int h = 0; h < WH; ++h) {
+        m_run[h] = -CUDART_INF_F; l_lane[h] = 0.f; z_lane[h] = 0.f;
+        acc[h][0] = acc[h][1] = acc[h][2] = acc[h][3] = 0.f;
+    }
+    // fp32 rotation cis(n' th_i) of token j = anchor(i) x cis(j th_i)
+    auto rot32 = [&](int i, int j, float &co, float &si) {
+        const float2 a = anc32[i];
+        const float ax = a.x, ay = a.y;
+        const float2 tt = t1f[i * 32 + j];
+        co = ax * tt.x - ay * tt.y;
+        si = ax * tt.y + ay * tt.x;
+    };
+
+    for (int t = t_first; t < t_end; t += NSTREAM) {
+        const int64_t n0 = (int64_t)t * 32;
+        const int ntok = (int)min((int64_t)32, P.T - n0);
+        const bool valid = lane < ntok;
+        const bool kov = cnt_k > (uint32_t)c.kcap_g, vov = cnt_v > (uint32_t)c.vcap_g;
+        const int nk = kov ? 0 : (int)cnt_k, nv = vov ? 0 : (int)cnt_v;
+
+        // V words of this tile: in flight during the K phase
+        uint32_t vw[WH][KWH];
+#pragma unroll
+        for (int h = 0; h < WH; ++h)
+#pragma unroll
+            for (int w = 0; w < KWH; ++w)
+                vw[h][w] = __ldg(c.vcodes + vf_word(t, c.H_kv, g0 + hw0 + h, w, lane, BITS));
+
+        // K words to shared memory for the data-dependent readers (heavy pairs, outliers)
+#pragma unroll
+        for (int h = 0; h < WH; ++h)
+#pragma unroll
+            for (int w = 0; w < KWH; ++w) kst[(h * KWH + w) * 32 + lane] = kw[h][w];
+
+        // ---------------------------------------------------------- a2: K dense
+        float acc_c[WH], acc_s[WH];
+#pragma unroll
+        for (int h = 0; h < WH; ++h) { acc_c[h] = 0.f; acc_s[h] = 0.f; }
+#pragma unroll
+        for (int i = 0; i < kPairs; ++i) {
+            const uint2 an = anc16[i];
+            const uint32_t tj = t1h[i * 32 + lane];
+            const __half2 th = *reinterpret_cast<const __half2 *>(&tj);
+            const __half2 csh = __hfma2(*reinterpret_cast<const __half2 *>(&an.y), __high2half2(th),
+                                        __hmul2(*reinterpret_cast<const __half2 *>(&an.x), __low2half2(th)));
+            const uint32_t cs = *reinterpret_cast<const uint32_t *>(&csh);
+            const int bit = FB * i, w = bit >> 5, sh = bit & 31;
+#pragma unroll
+            for (int h = 0; h < WH; ++h) {
+                uint32_t off;
+                if (sh + FB <= 32) off = sh >= 2 ? (kw[h][w] >> (sh - 2)) : (kw[h][w] << (2 - sh));
+                else off = __funnelshift_r(kw[h][w], kw[h][w + 1], sh - 2);
+                const uint32_t a = klut_u | (off & ((NE - 1) << 2));
+                const uint32_t ab = lds_u32(a + (uint32_t)((h * 64 + i) * NE * 4));
+                fma2_f16_f32(ab, cs, acc_c[h], acc_s[h]);
+            }
+        }
+        __syncwarp();
+
+        // -------------------------------------------- a3: heavy pairs, Key outliers (fp32)
+        float sco[WH];
+#pragma unroll
+        for (int h = 0; h < WH; ++h) {
+            const int hc = hw0 + h;
+            float hs = 0.f;
+            const int nh = hv_n[hc];
+            for (int u = 0; u < nh; ++u) {
+                const int i = hv_pair[hc * 8 + u];
+                const int bit = FB * i;
+                const int wq = h * KWH + (bit >> 5);
+                unsigned long long w64 = kst[wq * 32 + lane];
+                if ((bit & 31) + FB > 32) w64 |= (unsigned long long)kst[(wq + 1) * 32 + lane] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                const float2 ab = hlut[(hc * HMAX + u) * NE + pc];
+                float co, si;
+                rot32(i, lane, co, si);
+                hs += co * ab.x + si * ab.y;
+            }
+            sco[h] = (acc_c[h] + acc_s[h]) * lut_inv[hc] + hs;
+        }
+        // item of the CTA's 4-head group -> (token, head of this warp or -1, correction)
+        auto k_corr = [&](uint32_t itm, int &j, int &h) -> float {
+            j = (int)((itm >> 11) & 31u);
+            const int chl = (int)(itm & 0x1ffu), flag = (int)((itm >> 9) & 3u);
+            h = (chl >> 7) - hw0;
+            if (h < 0 || h >= WH) { h = -1; return 0.f; }
+            const int cc = chl & 127, i = cc & 63, up = cc >> 6;
+            int code = flag == 1 ? CM : 0;
+            if (flag == 0) {   // code not named by the item: read it from the tile's words
+                const int bit = FB * i;
+                const int wq = h * KWH + (bit >> 5);
+                unsigned long long w64 = kst[wq * 32 + j];
+                if ((bit & 31) + FB > 32) w64 |= (unsigned long long)kst[(wq + 1) * 32 + j] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                code = (pc >> (up * BITS)) & CM;
+            }
+            const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+            const float delta = xval - (cbKs[code] * ks_s[chl] + kz_s[chl]);
+            float co, si;
+            rot32(i, j, co, si);
+            const float qa = qs[(chl >> 7) * kHeadDim + i], qb = qs[(chl >> 7) * kHeadDim + i + 64];
+            return delta * (up ? (qb * co - qa * si) : (qa * co + qb * si));
+        };
+        {
+            const int64_t bucket = (int64_t)t * c.NG + hg;
+#pragma unroll
+            for (int k = 0; k < IPL; ++k) {
+                if (32 * k < nk && lane + 32 * k < nk) {
+                    int j, h;
+                    const float v = k_corr(kitm[k], j, h);
+                    if (h >= 0) atomicAdd(&kfix[h * 32 + j], kfix_of(v));
+                }
+            }
+            for (int x = 32 * IPL + lane; x < nk; x += 32) {
+                int j, h;
+                const float v = k_corr(__ldg(c.kit + bucket * c.kcap_g + x), j, h);
+                if (h >= 0) atomicAdd(&kfix[h * 32 + j], kfix_of(v));
+            }
+            if (kov) {   // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
+                for (int j = 0; j < ntok; ++j) {
+                    const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
+                    for (uint32_t r = r0 + lane; r < r1; r += 32) {
+                        const uint32_t rec = __ldcg(c.kout + r);
+                        const int ch = (int)(rec & 0xffffu);
+                        if (ch < c_lo || ch >= c_lo + HG * kHeadDim) continue;
+                        int jj, h;
+                        const float v = k_corr((rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - c_lo), jj, h);
+                        if (h >= 0) atomicAdd(&kfix[h * 32 + jj], kfix_of(v));
+                    }
+                }
+            }
+        }
+        __syncwarp();
+
+        // ------------------------------------------------------ a4: online softmax
+        // weights p s_n 2^(WEXP - E) with E from the tile's largest s_n (fp16 normal range)
+        const float smax = warp_max_redux(valid ? vsz.x : 0.f);
+        const int E = smax > 0.f ? ilog2f(smax) + 1 : 0;
+        const float pe = pow2i(WEXP - E), sc_out = pow2i(E - WEXP);
+        uint32_t bw[WH][2][2];
+#pragma unroll
+        for (int h = 0; h < WH; ++h) {
+            float s = sco[h] + (float)kfix[h * 32 + lane] * (1.f / kKfixScale);
+            kfix[h * 32 + lane] = 0;
+            s = valid ? s : -CUDART_INF_F;
+            const float m_new = fmaxf(m_run[h], warp_max_redux(s));
+            const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run[h] - m_new);
+            const float p = valid ? exp2f(s - m_new) : 0.f;
+            l_lane[h] = l_lane[h] * alpha + p;
+            z_lane[h] = z_lane[h] * alpha + p * vsz.y;
+            m_run[h] = m_new;
+            if (alpha != 1.f) {   // warp-uniform
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[h][r] *= alpha;
+            }
+            ps[h * 32 + lane] = p;   // kst is free: heavy pairs and Key items are done
+            const uint32_t w16 = __half_as_ushort(__float2half_rn(p * (vsz.x * pe)));
+            const uint32_t w2 = w16 | (__shfl_down_sync(0xffffffffu, w16, 1) << 16);
+            bw[h][0][0] = __shfl_sync(0xffffffffu, w2, 2 * vt);
+            bw[h][0][1] = __shfl_sync(0xffffffffu, w2, 2 * vt + 8);
+            bw[h][1][0] = __shfl_sync(0xffffffffu, w2, 16 + 2 * vt);
+            bw[h][1][1] = __shfl_sync(0xffffffffu, w2, 16 + 2 * vt + 8);
+        }
+        // the next tile's K words: in flight during P.V
+        const int tn = t + NSTREAM;
+        if (tn < t_end) load_k(tn);
+        // --------------------------------------------------------- a5: P.V dense
+#pragma unroll
+        for (int h = 0; h < WH; ++h) {
+#pragma unroll
+            for (int ml = 0; ml < 8; ++ml) {
+                float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    uint32_t a[4], alo[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int bit = ((ml * 2 + s2) * 4 + r) * FB;
+                        const int wi = bit >> 5, sh = bit & 31;
+                        uint32_t off;
+                        if (sh + FB <= 32) off = sh >= 7 ? (vw[h][wi] >> (sh - 7)) : (vw[h][wi] << (7 - sh));
+                        else off = __funnelshift_r(vw[h][wi], vw[h][wi + 1], sh - 7);
+                        const uint32_t ad = vlut_u | (off & ((NE - 1) << 7));
+                        a[r] = lds_u32(ad);
+                        if constexpr (RESID) alo[r] = lds_u32(ad + NE * 32 * 4);
+                    }
+                    mma_f16_f32(d, a, bw[h][s2]);
+                    if constexpr (RESID) mma_f16_f32(d, alo, bw[h][s2]);
+                }
+                // every column holds head h: lane (g, t) keeps rows g, g+8 of m-tiles t, t+4
+                if (vt == (ml & 3)) {
+                    acc[h][(ml >> 2) * 2] += d[0] * sc_out;
+                    acc[h][(ml >> 2) * 2 + 1] += d[2] * sc_out;
+                }
+            }
+        }
+
+        // ------------------------------------------------------ a6: V outliers
+        // p_n (x - V^(code)) of this warp's items, summed in fixed point (native shared integer
+        // atomics; scale from the tile's largest |term|) and folded into the lanes' accumulators
+        if (nv > 0 || vov) {
+#pragma unroll
+            for (int h = 0; h < WH; ++h)
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) vfix[h * kHeadDim + 16 * (vt + 4 * k) + vg + 8 * r] = 0;
+            __syncwarp();
+            auto v_term = [&](uint32_t itm, bool act, int &h, int &cc) -> float {
+                const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x1ffu), flag = (int)((itm >> 9) & 3u);
+                h = (chl >> 7) - hw0;
+                cc = chl & 127;
+                act = act && h >= 0 && h < WH;
+                int code = flag == 1 ? CM : 0;
+                if (act && flag == 0) {   // code not named by the item: read its word(s) (L2)
+                    const int bit = vf_bit(j, cc, BITS);
+                    const uint32_t *wq = c.vcodes + vf_word(t, c.H_kv, g0 + (chl >> 7), bit >> 5, vf_lane(j, cc), BITS);
+                    unsigned long long w64 = __ldg(wq);
+                    if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)__ldg(wq + 32) << 32;
+                    code = (int)((w64 >> (bit & 31)) & CM);
+                }
+                const float s_n = __shfl_sync(0xffffffffu, vsz.x, j), z_n = __shfl_sync(0xffffffffu, vsz.y, j);
+                const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+                return act ? ps[h * 32 + j] * (xval - (cbVs[code] * s_n + z_n)) : 0.f;
+            };
+            float vt_[IPL];
+            int vix[IPL];   // h * 128 + channel
+            float mx = 0.f;
+#pragma unroll
+            for (int k = 0; k < IPL; ++k) {
+                vt_[k] = 0.f; vix[k] = 0;
+                if (32 * k < nv) {
+                    int h, cc;
+                    vt_[k] = v_term(vitm[k], lane + 32 * k < nv, h, cc);
+                    vix[k] = h * kHeadDim + cc;
+                }
+                mx = fmaxf(mx, fabsf(vt_[k]));
+            }
+            const bool slow = nv > 32 * IPL || vov;
+            float ms = 0.f;
+            const int64_t bucket = (int64_t)t * c.NG + hg;
+            auto slow_term = [&](int x0, int &h, int &cc) -> float {   // item x0 + lane
+                uint32_t itm = 0u;
+                bool act = false;
+                if (x0 < nv) {
+                    act = x0 + lane < nv;
+                    itm = act ? __ldg(c.vit + bucket * c.vcap_g + x0 + lane) : 0u;
+                } else {   // CSR rows of the overflowed bucket, as items
+                    const int kv = c.kv, r = x0 - nv + lane;
+                    act = r < ntok * kv;
+                    if (act) {
+                        const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
+                        const int ch = (int)(rec & 0xffffu);
+                        act = ch >= c_lo && ch < c_lo + HG * kHeadDim;
+                        itm = (rec & 0xffff0000u) | ((uint32_t)(r / kv) << 11) | (uint32_t)(act ? ch - c_lo : 0);
+                    }
+                }
+                return v_term(itm, act, h, cc);
+            };
+            const int x_end = (vov ? ntok * c.kv : 0) + nv;
+            if (slow) {
+                for (int x0 = 32 * IPL; x0 < x_end; x0 += 32) {
+                    int h, cc;
+                    ms = fmaxf(ms, fabsf(slow_term(x0, h, cc)));
+                }
+            }
+            mx = warp_max(fmaxf(mx, ms));
+            const int emx = mx > 0.f ? ilog2f(mx) : 0;
+            const float S = pow2i(24 - emx);
+#pragma unroll
+            for (int k = 0; k < IPL; ++k)
+                if (vt_[k] != 0.f) atomicAdd(&vfix[vix[k]], __float2int_rn(vt_[k] * S));
+            if (slow) {
+                for (int x0 = 32 * IPL; x0 < x_end; x0 += 32) {
+                    int h, cc;
+                    const float v = slow_term(x0, h, cc);
+                    if (v != 0.f) atomicAdd(&vfix[h * kHeadDim + cc], __float2int_rn(v * S));
+                }
+            }
+            __syncwarp();
+            const float inv = pow2i(emx - 24);
+#pragma unroll
+            for (int h = 0; h < WH; ++h)
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int r = 0; r < 2; ++r)
+                        acc[h][2 * k + r] += (float)vfix[h * kHeadDim + 16 * (vt + 4 * k) + vg + 8 * r] * inv;
+        }
+        __syncwarp();
+
+        // advance the anchors by NSTREAM tiles (fp64 complex rotation), next tile's items
+        for (int i = lane; i < 64; i += 32) {
+            const double2 a = anc64[i], r = rot[i];
+            const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
+            anc64[i] = b;
+            anc32[i] = make_float2((float)b.x, (float)b.y);
+            anc16[i] = make_uint2(pack_half2((float)b.x, (float)b.y), pack_half2(-(float)b.y, (float)b.x));
+        }
+        cnt_k = ncnt_k;
+        cnt_v = ncnt_v;
+        if (tn < t_end) {
+            load_items(tn);
+            load_counts(tn + NSTREAM, ncnt_k, ncnt_v);
+        }
+        __syncwarp();
+    }
+
+    // ------------------------------------------- warp partials -> CTA partial (a7)
+    __syncwarp();
+    float *wpart = reinterpret_cast<float *>(kst);   // [WH][d + 2]
+#pragma unroll
+    for (int h = 0; h < WH; ++h) {
+        const float l = warp_sum(l_lane[h]), z = warp_sum(z_lane[h]);
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int ch = 16 * (vt + 4 * k) + vg + 8 * r;
+                wpart[h * (kHeadDim + 2) + ch] = acc[h][2 * k + r] + z;
+            }
+        if (lane == 0) {
+            wpart[h * (kHeadDim + 2) + kHeadDim] = m_run[h];
+            wpart[h * (kHeadDim + 2) + kHeadDim + 1] = l;
+        }
+    }
+    __syncthreads();
+    float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
+    for (int x = tid; x < HG * (kHeadDim + 2); x += NTHR) {
+        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+        const int wh = g / WH, hl = g % WH;   // warps with wh = warp % (HG/WH) hold head g
+        float m = -CUDART_INF_F;
+        for (int s = 0; s < NSTREAM; ++s) {
+            const float *pw = reinterpret_cast<const float *>(wbase + (s * (HG / WH) + wh) * C::w_bytes) + hl * (kHeadDim + 2);
+            if (pw[kHeadDim + 1] != 0.f) m = fmaxf(m, pw[kHeadDim]);
+        }
+        float l = 0.f, o = 0.f;
+        for (int s = 0; s < NSTREAM; ++s) {
+            const float *pw = reinterpret_cast<const float *>(wbase + (s * (HG / WH) + wh) * C::w_bytes) + hl * (kHeadDim + 2);
+            const float lw = pw[kHeadDim + 1];
+            if (lw == 0.f) continue;
+            const float wt = exp2f(pw[kHeadDim] - m);
+            l += wt * lw;
+            if (ch < kHeadDim) o += wt * pw[ch];
+        }
+        part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
+    }
+    // ------------------------------------------------------- a7: split merge
+    __threadfence();
+    __syncthreads();
+    int *s_last = flag_s + 1;
+    if (tid == 0) {
+        const unsigned prev = atomicAdd(&P.tickets[hg], 1u);
+        *s_last = (prev == (unsigned)(P.S - 1));
+    }
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    for (int x = tid; x < HG * (kHeadDim + 2); x += NTHR) {
+        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+        const int gq = g0 + g;
+        float m = -CUDART_INF_F;
+        for (int s = 0; s < P.S; ++s) {
+            const float *ps2 = P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2);
+            if (__ldcg(ps2 + kHeadDim + 1) != 0.f) m = fmaxf(m, __ldcg(ps2 + kHeadDim));
+        }
+        float l = 0.f, o = 0.f;
+        for (int s = 0; s < P.S; ++s) {
+            const float *ps2 = P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2);
+            const float ls = __ldcg(ps2 + kHeadDim + 1);
+            if (ls == 0.f) continue;
+            const float wgt = exp2f(__ldcg(ps2 + kHeadDim) - m);
+            l += wgt * ls;
+            if (ch < kHeadDim) o += wgt * __ldcg(ps2 + ch);
+        }
+        if (P.write_partial) {
+            P.out[gq * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
+        } else if (ch < kHeadDim) {
+            P.out[gq * kHeadDim + ch] = o / l;
+        }
+    }
+    if (tid == 0) P.tickets[hg] = 0;
+}
+
+template <int BITS, bool RESID, int WH>
+cudaError_t launch_wa_t(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
+    using C = WCfg<BITS, RESID, WH>;
+    static_assert(C::total <= 227 * 1024, "shared memory");
+    cudaError_t e = cudaFuncSetAttribute(att_wa_kernel<BITS, RESID, WH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::total);
+    if (e != cudaSuccess) return e;
+    att_wa_kernel<BITS, RESID, WH><<<grid, C::NTHR, C::total, s>>>(c, P);
+    return cudaGetLastError();
+}
+
+template <int BITS, bool RESID>
+cudaError_t launch_wa_r(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
+    static const int wh = getenv("KVQ_WA_WH") ? atoi(getenv("KVQ_WA_WH")) : 2;
+    return wh == 4 ? launch_wa_t<BITS, RESID, 4>(c, P, grid, s) : launch_wa_t<BITS, RESID, 2>(c, P, grid, s);
+}
+
+}  // namespace
+
+bool attend_wa_supported(const DevCache &c) {
+    return c.G == 1 && (c.bits == 2 || c.bits == 3) && c.H_q % HG == 0 &&
+           c.GW == HG * kHeadDim;   // outlier buckets per 4-head group
+}
+
+size_t attend_wa_smem_bytes(int bits, bool resid) {
+    if (bits == 2) return resid ? WCfg<2, true, 2>::total : WCfg<2, false, 2>::total;
+    if (bits == 3) return resid ? WCfg<3, true, 2>::total : WCfg<3, false, 2>::total;
+    return 0;
+}
+
+cudaError_t launch_attend_wa(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s) {
+    WParams P{};
+    P.q = a.q; P.pos = a.pos; P.T = a.T; P.S = S; P.ntiles = (int)((a.T + 31) / 32);
+    P.out = a.out; P.parts = a.parts; P.tickets = a.tickets; P.write_partial = a.write_partial;
+    const int grid = (c.H_q / HG) * S;
+    const bool resid = !c.vcb_exact16;
+    if (c.bits == 2) return resid ? launch_wa_r<2, true>(c, P, grid, s) : launch_wa_r<2, false>(c, P, grid, s);
+    if (c.bits == 3) return resid ? launch_wa_r<3, true>(c, P, grid, s) : launch_wa_r<3, false>(c, P, grid, s);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace kvq

@@ -50,8 +50,7 @@ struct DevCache {
     int *err;       // device view of the sticky error word (host mapped)
     int *counts;    // prefill scratch [cap]
     // Outliers bucketed per (32-token tile, attend head group) for the attend kernel:
-    // item = fp16 value << 16 | token-in-tile << 11 | channel - group_start (11 bits),
-    // in token order.  Written by the quantizer next to the token-major CSC/CSR arrays
+    // item (see item_code_flag) in (token, channel) order.  Written by the quantizer next to the token-major CSC/CSR arrays
     // (which stay the canonical form for export and the overflow fallback).
     int NG, GW;             // head groups, channels per group
     int vcb_exact16;        // 1: every Value decode codebook entry is an fp16 value (R23)
@@ -63,6 +62,16 @@ struct DevCache {
 };
 
 enum ErrBits { kErrKeyCapacity = 1 };
+
+// Outlier item of a (tile, head group) bucket:
+//   fp16 value << 16 | token-in-tile << 11 | code flag << 9 | channel - group start (9 bits)
+// The code flag names the dense code the quantizer stored at the outlier position, which the
+// attend kernel needs for the correction x - deq(code): 1 = the top code 2^b - 1, 2 = code 0
+// (the usual case: an outlier is clamped to the range ends), 0 = read it from the code words.
+template <int BITS>
+__host__ __device__ inline uint32_t item_code_flag(int code) {
+    return code == (1 << BITS) - 1 ? (1u << 9) : (code == 0 ? (2u << 9) : 0u);
+}
 
 // Value-code fragment layout.  Token j (0..31) of a tile, channel cc (0..127) of a head:
 // m-tile mt = cc/16, k-step s = j/16, and the mma.m16n8k16 A-fragment coordinates
@@ -100,5 +109,9 @@ cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_us
                           cudaStream_t s);
 cudaError_t launch_merge(const float *parts, int P, int H, int d, float *o, cudaStream_t s);
 size_t attend_smem_bytes(int bits, int hg);
+// warp-autonomous variant (kvq_attend_wa.cu): MHA at 2-3 bits
+bool attend_wa_supported(const DevCache &c);
+size_t attend_wa_smem_bytes(int bits, bool resid);
+cudaError_t launch_attend_wa(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s);
 
 }  // namespace kvq

@@ -264,7 +264,8 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
             for (uint32_t m = kmask; m; m &= m - 1) {
                 const int ch = cb0 + __ffs(m) - 1;
                 if (pos < c.kcap_g)
-                    dst[pos] = ((uint32_t)xk[ch] << 16) | ((uint32_t)jj0 << 11) | (uint32_t)(ch - myg * c.GW);
+                    dst[pos] = ((uint32_t)xk[ch] << 16) | ((uint32_t)jj0 << 11) | item_code_flag<BITS>(kc[ch]) |
+                               (uint32_t)(ch - myg * c.GW);
                 ++pos;
             }
         }
@@ -374,7 +375,8 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
             if (vflag[ch]) {
                 vo[vr++] = (uint32_t)ch | ((uint32_t)xv[ch] << 16);
                 if (vpos < c.vcap_g)
-                    vdst[vpos] = ((uint32_t)xv[ch] << 16) | ((uint32_t)(n & 31) << 11) | (uint32_t)(ch - myg * c.GW);
+                    vdst[vpos] = ((uint32_t)xv[ch] << 16) | ((uint32_t)(n & 31) << 11) | item_code_flag<BITS>(vc[ch]) |
+                                 (uint32_t)(ch - myg * c.GW);
                 ++vpos;
             }
     }
@@ -459,15 +461,16 @@ __global__ void __launch_bounds__(256) sort_buckets_kernel(DevCache c, int64_t t
     while (n2 < (int)cnt) n2 <<= 1;
     for (int i = threadIdx.x; i < n2; i += blockDim.x) sitem[i] = i < (int)cnt ? lst[i] : 0xffffffffu;
     __syncthreads();
-    // bitonic sort on the low 16 bits (token << 11 | channel); keys are unique per list
+    // bitonic sort on (token, channel) (the low 16 bits without the code flag); keys are
+    // unique per list
     for (int k = 2; k <= n2; k <<= 1)
         for (int jv = k >> 1; jv > 0; jv >>= 1) {
             for (int i = threadIdx.x; i < n2; i += blockDim.x) {
                 const int ixj = i ^ jv;
                 if (ixj > i) {
                     const uint32_t a = sitem[i], b = sitem[ixj];
-                    const uint32_t ka = a == 0xffffffffu ? 0xffffffffu : (a & 0xffffu);
-                    const uint32_t kb = b == 0xffffffffu ? 0xffffffffu : (b & 0xffffu);
+                    const uint32_t ka = a == 0xffffffffu ? 0xffffffffu : (a & 0xf9ffu);
+                    const uint32_t kb = b == 0xffffffffu ? 0xffffffffu : (b & 0xf9ffu);
                     const bool up = (i & k) == 0;
                     if ((ka > kb) == up) { sitem[i] = b; sitem[ixj] = a; }
                 }
