@@ -187,7 +187,7 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     A(&d.counts, (size_t)d.cap * 4);
     // outlier buckets per (tile, attend head group); capacity ~3x the expected count
     {
-        const int hkv_g = hg / G;
+        const int hkv_g = attend_bucket_heads(C.bits, C.n_q_heads, G) / G;
         d.GW = hkv_g * kHeadDim;
         d.NG = C.n_kv_heads / hkv_g;
         const double f = C.outlier_ppm / 1e6;

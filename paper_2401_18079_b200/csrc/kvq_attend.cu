@@ -1069,6 +1069,14 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
 
 }  // namespace
 
+// Query heads per outlier bucket group (the quantizer's (tile, group) item lists): the
+// warp-autonomous MHA kernel reads one 2-head group per warp; the two-halves kernel uses
+// CTAs of exactly one group.
+int attend_bucket_heads(int bits, int H_q, int G) {
+    if (G == 1 && (bits == 2 || bits == 3) && H_q % 4 == 0) return 2;
+    return attend_heads_per_cta(bits, H_q, G);
+}
+
 int attend_heads_per_cta(int bits, int H_q, int G) {
     const int cap = bits == 4 ? 1 : 4;   // K tables: HG * 64 * 4^b * 4 bytes of shared memory
     for (int hg = cap; hg >= 1; hg >>= 1)
@@ -1103,7 +1111,10 @@ int attend_auto_splits(const DevCache &c, int64_t T, int hg) {
 }
 
 cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_used, cudaStream_t s) {
-    const int hg = attend_heads_per_cta(c.bits, c.H_q, c.G);
+    static const bool legacy = getenv("KVQ_ATT_LEGACY") != nullptr;
+    const bool wa = !a.timers && !legacy && attend_wa_supported(c);
+    // CTA heads: 4 for the warp-autonomous kernel, else one bucket group
+    const int hg = wa ? 4 : (c.GW / kHeadDim) * c.G;
     if (hg == 0) return cudaErrorInvalidValue;
     const int ntiles = (int)((a.T + 31) / 32);
     int S = a.splits > 0 ? a.splits : attend_auto_splits(c, a.T, hg);
@@ -1117,10 +1128,7 @@ cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_us
     if (splits_used) *splits_used = S;
     // MHA at 2-3 bits: the warp-autonomous kernel (kvq_attend_wa.cu); KVQ_ATT_LEGACY=1 or the
     // phase-timer diagnostics select the two-halves kernel below
-    if (!a.timers && attend_wa_supported(c)) {
-        static const bool legacy = getenv("KVQ_ATT_LEGACY") != nullptr;
-        if (!legacy) return launch_attend_wa(c, a, S, s);
-    }
+    if (wa) return launch_attend_wa(c, a, S, s);
     switch (c.bits) {
         case 2: return launch_b<2>(c, P, hg, grid, s);
         case 3: return launch_b<3>(c, P, hg, grid, s);

@@ -108,7 +108,7 @@ template <int BITS, bool RESID, int WH>
 struct WCfg {
     static constexpr int NWARP = NSTREAM * (HG / WH);
     static constexpr int NTHR = NWARP * 32;
-    static constexpr int IPL = 8;                         // bucket items per lane in registers
+    static constexpr int IPL = 4;                         // bucket items per lane in registers
     static constexpr int NE = 1 << (2 * BITS);
     static constexpr int KWH = 4 * BITS;                  // code words per head per token
     static constexpr int HMAX = 8;                        // fp32 "heavy" pairs per head
@@ -178,11 +178,14 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     const int split = blockIdx.x / n_hg;
     const int g0 = hg * HG;               // first query head of the CTA = first KV head (G = 1)
     const int hw0 = (warp % (HG / WH)) * WH;   // this warp's first head within the CTA
+    const int c_lo = g0 * kHeadDim;
     const int stream = warp / (HG / WH);
+    // this warp's outlier buckets: the quantizer groups items per WH heads (c.GW = WH * 128)
+    const int grp = (g0 + hw0) / WH;
+    const int w_lo = c_lo + hw0 * kHeadDim;   // first channel of the warp's heads
     const int t_begin = (int)((int64_t)split * P.ntiles / P.S);
     const int t_end = (int)((int64_t)(split + 1) * P.ntiles / P.S);
     const int D = c.D;
-    const int c_lo = g0 * kHeadDim;
     const float *cbK = c.cb + 16, *cbV = c.cb + 48;   // decode codebooks
 
     // per-warp scratch
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     auto load_counts = [&](int t, uint32_t &nk, uint32_t &nv) {
         nk = nv = 0;
         if (t < t_end) {
-            const uint32_t *gc = c.gcnt + ((int64_t)t * c.NG + hg) * 2;
+            const uint32_t *gc = c.gcnt + ((int64_t)t * c.NG + grp) * 2;
             nk = __ldg(gc);
             nv = __ldg(gc + 1);
         }
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     // Items of a (tile, 4-head group) bucket are in (token, channel) order; a warp keeps the
     // whole bucket (IPL per lane) and skips the other heads' items.
     auto load_items = [&](int t) {
-        const int64_t bucket = (int64_t)t * c.NG + hg;
+        const int64_t bucket = (int64_t)t * c.NG + grp;
         const uint32_t nk = cnt_k > (uint32_t)c.kcap_g ? 0u : cnt_k;
         const uint32_t nv = cnt_v > (uint32_t)c.vcap_g ? 0u : cnt_v;
 #pragma unroll
@@ -448,9 +451,9 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         auto k_corr = [&](uint32_t itm, int &j, int &h) -> float {
             j = (int)((itm >> 11) & 31u);
             const int chl = (int)(itm & 0x1ffu), flag = (int)((itm >> 9) & 3u);
-            h = (chl >> 7) - hw0;
-            if (h < 0 || h >= WH) { h = -1; return 0.f; }
+            h = chl >> 7;   // head of this warp
             const int cc = chl & 127, i = cc & 63, up = cc >> 6;
+            const int ccta = hw0 * kHeadDim + chl;   // channel within the CTA's 4 heads
             int code = flag == 1 ? CM : 0;
             if (flag == 0) {   // code not named by the item: read it from the tile's words
                 const int bit = FB * i;
@@ -461,26 +464,26 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                 code = (pc >> (up * BITS)) & CM;
             }
             const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
-            const float delta = xval - (cbKs[code] * ks_s[chl] + kz_s[chl]);
+            const float delta = xval - (cbKs[code] * ks_s[ccta] + kz_s[ccta]);
             float co, si;
             rot32(i, j, co, si);
-            const float qa = qs[(chl >> 7) * kHeadDim + i], qb = qs[(chl >> 7) * kHeadDim + i + 64];
+            const float qa = qs[(hw0 + h) * kHeadDim + i], qb = qs[(hw0 + h) * kHeadDim + i + 64];
             return delta * (up ? (qb * co - qa * si) : (qa * co + qb * si));
         };
         {
-            const int64_t bucket = (int64_t)t * c.NG + hg;
+            const int64_t bucket = (int64_t)t * c.NG + grp;
 #pragma unroll
             for (int k = 0; k < IPL; ++k) {
                 if (32 * k < nk && lane + 32 * k < nk) {
                     int j, h;
                     const float v = k_corr(kitm[k], j, h);
-                    if (h >= 0) atomicAdd(&kfix[h * 32 + j], kfix_of(v));
+                    atomicAdd(&kfix[h * 32 + j], kfix_of(v));
                 }
             }
             for (int x = 32 * IPL + lane; x < nk; x += 32) {
                 int j, h;
                 const float v = k_corr(__ldg(c.kit + bucket * c.kcap_g + x), j, h);
-                if (h >= 0) atomicAdd(&kfix[h * 32 + j], kfix_of(v));
+                atomicAdd(&kfix[h * 32 + j], kfix_of(v));
             }
             if (kov) {   // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
                 for (int j = 0; j < ntok; ++j) {
@@ -488,10 +491,10 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                     for (uint32_t r = r0 + lane; r < r1; r += 32) {
                         const uint32_t rec = __ldcg(c.kout + r);
                         const int ch = (int)(rec & 0xffffu);
-                        if (ch < c_lo || ch >= c_lo + HG * kHeadDim) continue;
+                        if (ch < w_lo || ch >= w_lo + WH * kHeadDim) continue;
                         int jj, h;
-                        const float v = k_corr((rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - c_lo), jj, h);
-                        if (h >= 0) atomicAdd(&kfix[h * 32 + jj], kfix_of(v));
+                        const float v = k_corr((rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - w_lo), jj, h);
+                        atomicAdd(&kfix[h * 32 + jj], kfix_of(v));
                     }
                 }
             }
@@ -574,13 +577,12 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             __syncwarp();
             auto v_term = [&](uint32_t itm, bool act, int &h, int &cc) -> float {
                 const int j = (int)((itm >> 11) & 31u), chl = (int)(itm & 0x1ffu), flag = (int)((itm >> 9) & 3u);
-                h = (chl >> 7) - hw0;
+                h = chl >> 7;   // head of this warp
                 cc = chl & 127;
-                act = act && h >= 0 && h < WH;
                 int code = flag == 1 ? CM : 0;
                 if (act && flag == 0) {   // code not named by the item: read its word(s) (L2)
                     const int bit = vf_bit(j, cc, BITS);
-                    const uint32_t *wq = c.vcodes + vf_word(t, c.H_kv, g0 + (chl >> 7), bit >> 5, vf_lane(j, cc), BITS);
+                    const uint32_t *wq = c.vcodes + vf_word(t, c.H_kv, g0 + hw0 + h, bit >> 5, vf_lane(j, cc), BITS);
                     unsigned long long w64 = __ldg(wq);
                     if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)__ldg(wq + 32) << 32;
                     code = (int)((w64 >> (bit & 31)) & CM);
@@ -604,7 +606,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             }
             const bool slow = nv > 32 * IPL || vov;
             float ms = 0.f;
-            const int64_t bucket = (int64_t)t * c.NG + hg;
+            const int64_t bucket = (int64_t)t * c.NG + grp;
             auto slow_term = [&](int x0, int &h, int &cc) -> float {   // item x0 + lane
                 uint32_t itm = 0u;
                 bool act = false;
@@ -617,15 +619,16 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                     if (act) {
                         const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
                         const int ch = (int)(rec & 0xffffu);
-                        act = ch >= c_lo && ch < c_lo + HG * kHeadDim;
-                        itm = (rec & 0xffff0000u) | ((uint32_t)(r / kv) << 11) | (uint32_t)(act ? ch - c_lo : 0);
+                        act = ch >= w_lo && ch < w_lo + WH * kHeadDim;
+                        itm = (rec & 0xffff0000u) | ((uint32_t)(r / kv) << 11) | (uint32_t)(act ? ch - w_lo : 0);
                     }
                 }
                 return v_term(itm, act, h, cc);
             };
             const int x_end = (vov ? ntok * c.kv : 0) + nv;
+            const int x_beg = vov ? 0 : 32 * IPL;   // overflow: every record from the CSR rows
             if (slow) {
-                for (int x0 = 32 * IPL; x0 < x_end; x0 += 32) {
+                for (int x0 = x_beg; x0 < x_end; x0 += 32) {
                     int h, cc;
                     ms = fmaxf(ms, fabsf(slow_term(x0, h, cc)));
                 }
@@ -637,7 +640,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             for (int k = 0; k < IPL; ++k)
                 if (vt_[k] != 0.f) atomicAdd(&vfix[vix[k]], __float2int_rn(vt_[k] * S));
             if (slow) {
-                for (int x0 = 32 * IPL; x0 < x_end; x0 += 32) {
+                for (int x0 = x_beg; x0 < x_end; x0 += 32) {
                     int h, cc;
                     const float v = slow_term(x0, h, cc);
                     if (v != 0.f) atomicAdd(&vfix[h * kHeadDim + cc], __float2int_rn(v * S));
@@ -761,19 +764,18 @@ cudaError_t launch_wa_t(const DevCache &c, const WParams &P, int grid, cudaStrea
 
 template <int BITS, bool RESID>
 cudaError_t launch_wa_r(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
-    static const int wh = getenv("KVQ_WA_WH") ? atoi(getenv("KVQ_WA_WH")) : 2;
-    return wh == 4 ? launch_wa_t<BITS, RESID, 4>(c, P, grid, s) : launch_wa_t<BITS, RESID, 2>(c, P, grid, s);
+    return launch_wa_t<BITS, RESID, 2>(c, P, grid, s);
 }
 
 }  // namespace
 
 bool attend_wa_supported(const DevCache &c) {
     return c.G == 1 && (c.bits == 2 || c.bits == 3) && c.H_q % HG == 0 &&
-           c.GW == HG * kHeadDim;   // outlier buckets per 4-head group
+           c.GW == 2 * kHeadDim;   // outlier buckets per 2-head group (one per warp)
 }
 
 size_t attend_wa_smem_bytes(int bits, bool resid) {
-    if (bits == 2) return resid ? WCfg<2, true, 2>::total : WCfg<2, false, 2>::total;
+    if (bits == 2) return resid ? WCfg<2, true, 2>::total : WCfg<2, false, 2>::total;  // WH = 2
     if (bits == 3) return resid ? WCfg<3, true, 2>::total : WCfg<3, false, 2>::total;
     return 0;
 }
