@@ -116,7 +116,7 @@ struct WCfg {
     static constexpr size_t vlut = (size_t)(RESID ? 2 : 1) * NE * 32 * 4;
     static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
-    static constexpr size_t t1h = (size_t)kPairs * 32 * 4;    // cis(j th_i) fp16x2 [i][j]
+    static constexpr size_t t1h = (size_t)kPairs * 32 * 4;    // cis(j th_i) fp16x2 [i/2][j][i%2]
     static constexpr size_t t1f = (size_t)kPairs * 32 * 8;    // cis(j th_i) fp32 [i][j]
     // per warp: K words of the tile (after the K phase: p and the V-outlier fixed-point
     // sums), K-outlier fixed-point terms, anchors (fp16 rotation pairs, fp64 state)
@@ -205,12 +205,21 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     uint32_t kitm[IPL], vitm[IPL];
     uint32_t cnt_k = 0, cnt_v = 0, ncnt_k = 0, ncnt_v = 0;
     float2 vsz = make_float2(0.f, 0.f);
-    auto load_k = [&](int t) {
+    // K words in two halves (RoPE pairs 0-31 and 32-63 of every head), so the prefetch of
+    // the next tile fits the register budget: the first half is issued during the second
+    // head's P.V, the second half at the end of the tile (consumed from pair 32 on)
+    auto load_k = [&](int t, int part) {
 #pragma unroll
         for (int h = 0; h < WH; ++h)
 #pragma unroll
-            for (int w = 0; w < KWH; ++w)
+            for (int w = part * KWH / 2; w < (part + 1) * KWH / 2; ++w)
                 kw[h][w] = __ldg(c.kcodes + ((int64_t)t * c.QW + (g0 + hw0 + h) * KWH + w) * 32 + lane);
+    };
+    auto store_k = [&](int part) {   // to shared memory for the data-dependent readers
+#pragma unroll
+        for (int h = 0; h < WH; ++h)
+#pragma unroll
+            for (int w = part * KWH / 2; w < (part + 1) * KWH / 2; ++w) kst[(h * KWH + w) * 32 + lane] = kw[h][w];
     };
     auto load_counts = [&](int t, uint32_t &nk, uint32_t &nv) {
         nk = nv = 0;
@@ -235,10 +244,9 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         vsz = (int64_t)t * 32 + lane < P.T ? __ldg(c.vsz + (int64_t)t * 32 + lane) : make_float2(0.f, 0.f);
     };
     if (t_first < t_end) {
-        load_k(t_first);
+        load_k(t_first, 0);
+        load_k(t_first, 1);
         load_counts(t_first, cnt_k, cnt_v);
-        load_items(t_first);
-        load_counts(t_first + NSTREAM, ncnt_k, ncnt_v);
     }
 
     // ---------------------------------------------------------------- prologue (a1)
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         double s, co;
         sincos((double)j * th, &s, &co);
         t1f[x] = make_float2((float)co, (float)s);
-        t1h[x] = pack_half2((float)co, (float)s);
+        t1h[((i >> 1) * 32 + j) * 2 + (i & 1)] = pack_half2((float)co, (float)s);   // pairs i, i+1 adjacent
     }
     // this warp's anchors cis((pos_base + 32 t_first) th_i), fp64 (advanced per tile)
     for (int i = lane; i < 64; i += 32) {
@@ -386,6 +394,9 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         const bool valid = lane < ntok;
         const bool kov = cnt_k > (uint32_t)c.kcap_g, vov = cnt_v > (uint32_t)c.vcap_g;
         const int nk = kov ? 0 : (int)cnt_k, nv = vov ? 0 : (int)cnt_v;
+        // this tile's outlier items and (s, z) (consumed after the K loop), next tile's counts
+        load_items(t);
+        load_counts(t + NSTREAM, ncnt_k, ncnt_v);
 
         // V words of this tile: in flight during the K phase
         uint32_t vw[WH][KWH];
@@ -395,20 +406,23 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             for (int w = 0; w < KWH; ++w)
                 vw[h][w] = __ldg(c.vcodes + vf_word(t, c.H_kv, g0 + hw0 + h, w, lane, BITS));
 
-        // K words to shared memory for the data-dependent readers (heavy pairs, outliers)
-#pragma unroll
-        for (int h = 0; h < WH; ++h)
-#pragma unroll
-            for (int w = 0; w < KWH; ++w) kst[(h * KWH + w) * 32 + lane] = kw[h][w];
+        store_k(0);
 
         // ---------------------------------------------------------- a2: K dense
         float acc_c[WH], acc_s[WH];
 #pragma unroll
         for (int h = 0; h < WH; ++h) { acc_c[h] = 0.f; acc_s[h] = 0.f; }
+        uint4 an2;
+        uint2 tj2;
 #pragma unroll
         for (int i = 0; i < kPairs; ++i) {
-            const uint2 an = anc16[i];
-            const uint32_t tj = t1h[i * 32 + lane];
+            if (i == kPairs / 2) store_k(1);
+            if ((i & 1) == 0) {   // rotation inputs of pairs i, i+1 in one load each
+                an2 = *reinterpret_cast<const uint4 *>(anc16 + i);
+                tj2 = reinterpret_cast<const uint2 *>(t1h)[(i >> 1) * 32 + lane];
+            }
+            const uint2 an = (i & 1) ? make_uint2(an2.z, an2.w) : make_uint2(an2.x, an2.y);
+            const uint32_t tj = (i & 1) ? tj2.y : tj2.x;
             const __half2 th = *reinterpret_cast<const __half2 *>(&tj);
             const __half2 csh = __hfma2(*reinterpret_cast<const __half2 *>(&an.y), __high2half2(th),
                                         __hmul2(*reinterpret_cast<const __half2 *>(&an.x), __low2half2(th)));
@@ -506,7 +520,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         const float smax = warp_max_redux(valid ? vsz.x : 0.f);
         const int E = smax > 0.f ? ilog2f(smax) + 1 : 0;
         const float pe = pow2i(WEXP - E), sc_out = pow2i(E - WEXP);
-        uint32_t bw[WH][2][2];
+        uint32_t w2s[WH];
 #pragma unroll
         for (int h = 0; h < WH; ++h) {
             float s = sco[h] + (float)kfix[h * 32 + lane] * (1.f / kKfixScale);
@@ -524,18 +538,21 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             }
             ps[h * 32 + lane] = p;   // kst is free: heavy pairs and Key items are done
             const uint32_t w16 = __half_as_ushort(__float2half_rn(p * (vsz.x * pe)));
-            const uint32_t w2 = w16 | (__shfl_down_sync(0xffffffffu, w16, 1) << 16);
-            bw[h][0][0] = __shfl_sync(0xffffffffu, w2, 2 * vt);
-            bw[h][0][1] = __shfl_sync(0xffffffffu, w2, 2 * vt + 8);
-            bw[h][1][0] = __shfl_sync(0xffffffffu, w2, 16 + 2 * vt);
-            bw[h][1][1] = __shfl_sync(0xffffffffu, w2, 16 + 2 * vt + 8);
+            w2s[h] = w16 | (__shfl_down_sync(0xffffffffu, w16, 1) << 16);   // tokens lane, lane+1
         }
-        // the next tile's K words: in flight during P.V
         const int tn = t + NSTREAM;
-        if (tn < t_end) load_k(tn);
         // --------------------------------------------------------- a5: P.V dense
 #pragma unroll
         for (int h = 0; h < WH; ++h) {
+            // the next tile's K words, in flight during the rest of the tile (issued once the
+            // first head's V words are consumed, to keep the register peak down)
+            if (h == 1 && tn < t_end) load_k(tn, 0);
+            uint32_t bw[2][2];   // B fragments: weights of tokens 16 s2 + 2t (+1) and + 8
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                bw[s2][0] = __shfl_sync(0xffffffffu, w2s[h], 16 * s2 + 2 * vt);
+                bw[s2][1] = __shfl_sync(0xffffffffu, w2s[h], 16 * s2 + 2 * vt + 8);
+            }
 #pragma unroll
             for (int ml = 0; ml < 8; ++ml) {
                 float d[4] = {0.f, 0.f, 0.f, 0.f};
@@ -553,8 +570,8 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                         a[r] = lds_u32(ad);
                         if constexpr (RESID) alo[r] = lds_u32(ad + NE * 32 * 4);
                     }
-                    mma_f16_f32(d, a, bw[h][s2]);
-                    if constexpr (RESID) mma_f16_f32(d, alo, bw[h][s2]);
+                    mma_f16_f32(d, a, bw[s2]);
+                    if constexpr (RESID) mma_f16_f32(d, alo, bw[s2]);
                 }
                 // every column holds head h: lane (g, t) keeps rows g, g+8 of m-tiles t, t+4
                 if (vt == (ml & 3)) {
@@ -658,7 +675,8 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         }
         __syncwarp();
 
-        // advance the anchors by NSTREAM tiles (fp64 complex rotation), next tile's items
+        if (tn < t_end) load_k(tn, 1);
+        // advance the anchors by NSTREAM tiles (fp64 complex rotation)
         for (int i = lane; i < 64; i += 32) {
             const double2 a = anc64[i], r = rot[i];
             const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
@@ -668,10 +686,6 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         }
         cnt_k = ncnt_k;
         cnt_v = ncnt_v;
-        if (tn < t_end) {
-            load_items(tn);
-            load_counts(tn + NSTREAM, ncnt_k, ncnt_v);
-        }
         __syncwarp();
     }
 
