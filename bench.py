@@ -370,7 +370,8 @@ def run_ours(args):
             "hbm_gbs_step": bytes_att * L / (ms_per_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(w.name),
-                         "kernel": "att_kernel (kvq_decode_attend: one launch)",
+                         "kernel": ("att_wa_kernel" if info.get("attend_kernel") == 1 else "att_kernel")
+                                   + " (kvq_decode_attend: one launch)",
                          "bytes_per_launch": bytes_att, "peak_kind": peak_kind,
                          "splits": info["splits"], "heads_per_cta": info["heads_per_cta"]},
             "cpu_baseline": cpu, "e2e": e2e,
@@ -386,7 +387,7 @@ def run_ours(args):
 
 
 def ncu_traffic(workload):
-    """dram__bytes_read.sum + dram__bytes_write.sum per att_kernel launch from the committed
+    """dram__bytes_read.sum + dram__bytes_write.sum per attend launch from the committed
     ncu --set full capture (profiles/att_traffic.json), or None if none was taken for this
     workload."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "att_traffic.json")

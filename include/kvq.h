@@ -166,6 +166,10 @@ typedef struct {
     int64_t capacity_tokens;
     int64_t k_outlier_capacity;
     int64_t device_bytes;       /* bytes of device memory owned */
+    int32_t attend_kernel;      /* kernel of the last attend: 1 = warp-autonomous (MHA, 2-3 bits,
+                                   csrc/kvq_attend_wa.cu), 0 = two-halves (csrc/kvq_attend.cu),
+                                   -1 = none yet */
+    int32_t bucket_heads;       /* query heads per outlier bucket group */
 } kvq_info;
 kvq_status kvq_get_info(const kvq_cache *cache, kvq_info *info);
 

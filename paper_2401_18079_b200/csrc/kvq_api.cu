@@ -17,7 +17,8 @@ struct kvq_cache {
     kvq_config cfg;
     DevCache dc;
     int64_t T = 0;             // host shadow of the token count
-    int hg = 0;                // query heads per attend CTA
+    int hg = 0;                // query heads per attend CTA (of the last launch)
+    int last_kernel = -1;      // attend kernel of the last launch (kvq_info.attend_kernel)
     int splits_forced = 0;
     int last_splits = 0;
     float *parts = nullptr;    // [max_splits][H_q][d+2]
@@ -266,6 +267,8 @@ kvq_status kvq_get_info(const kvq_cache *c, kvq_info *info) {
     info->capacity_tokens = c->dc.cap;
     info->k_outlier_capacity = c->dc.kcap;
     info->device_bytes = c->device_bytes;
+    info->attend_kernel = c->last_kernel;
+    info->bucket_heads = c->dc.GW / kHeadDim * c->dc.G;
     return KVQ_OK;
 }
 
@@ -389,6 +392,8 @@ static kvq_status attend_impl(kvq_cache *c, const void *q, int64_t pos, float *o
     a.q = qd; a.pos = pos; a.T = c->T; a.out = od; a.write_partial = partial;
     a.parts = c->parts; a.tickets = c->tickets; a.splits = c->splits_forced;
     a.timers = c->timers;
+    a.kernel_out = &c->last_kernel;
+    a.hg_out = &c->hg;
     cudaError_t e = launch_attend(c->dc, a, &c->last_splits, s);
     if (e != cudaSuccess) return cuda_fail(e, "attend launch");
     if (co == 1) {

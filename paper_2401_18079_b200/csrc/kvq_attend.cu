@@ -1116,6 +1116,8 @@ cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_us
     // CTA heads: 4 for the warp-autonomous kernel, else one bucket group
     const int hg = wa ? 4 : (c.GW / kHeadDim) * c.G;
     if (hg == 0) return cudaErrorInvalidValue;
+    if (a.kernel_out) *a.kernel_out = wa ? 1 : 0;
+    if (a.hg_out) *a.hg_out = hg;
     const int ntiles = (int)((a.T + 31) / 32);
     int S = a.splits > 0 ? a.splits : attend_auto_splits(c, a.T, hg);
     if (S > ntiles) S = ntiles;

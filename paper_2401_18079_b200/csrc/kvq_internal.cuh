@@ -102,6 +102,8 @@ struct AttendArgs {
     unsigned *tickets;   // [n_head_groups], zero between launches
     int splits;          // 0 = auto
     unsigned long long *timers;   // diagnostics: phase cycle sums, or null
+    int *kernel_out;     // optional: 1 = warp-autonomous kernel launched, 0 = two-halves
+    int *hg_out;         // optional: query heads per CTA of the launch
 };
 int attend_heads_per_cta(int bits, int H_q, int G);
 int attend_bucket_heads(int bits, int H_q, int G);

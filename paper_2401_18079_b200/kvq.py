@@ -63,7 +63,8 @@ class kvq_info(ctypes.Structure):
     _fields_ = [("heads_per_cta", ctypes.c_int32), ("splits", ctypes.c_int32),
                 ("value_outliers", ctypes.c_int32), ("words_per_token", ctypes.c_int32),
                 ("capacity_tokens", ctypes.c_int64), ("k_outlier_capacity", ctypes.c_int64),
-                ("device_bytes", ctypes.c_int64)]
+                ("device_bytes", ctypes.c_int64), ("attend_kernel", ctypes.c_int32),
+                ("bucket_heads", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
