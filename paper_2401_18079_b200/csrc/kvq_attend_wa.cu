@@ -40,6 +40,13 @@ constexpr int WEXP = 14;   // fp16 P.V weights scaled into [0, 2^14]
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
+// 16-byte global -> shared copy (LDGSTS), completion by cp.async.wait_all
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -118,11 +125,11 @@ struct WCfg {
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
     static constexpr size_t t1h = (size_t)kPairs * 32 * 4;    // cis(j th_i) fp16x2 [i/2][j][i%2]
     static constexpr size_t t1f = (size_t)kPairs * 32 * 8;    // cis(j th_i) fp32 [i][j]
-    // per warp: K words of the tile (after the K phase: p and the V-outlier fixed-point
-    // sums), K-outlier fixed-point terms, anchors (fp16 rotation pairs, fp64 state)
+    // per warp: K words of the tile (cp.async target), K-outlier fixed-point terms (then p),
+    // V-outlier fixed-point sums, anchors (fp16 rotation pairs, fp32)
     static constexpr size_t w_kst = (size_t)WH * KWH * 32 * 4;
-    static constexpr size_t w_bytes = w_kst + WH * 32 * 4 + 64 * 8 * 2 + 64 * 16;
-    static_assert(w_kst >= (size_t)WH * (32 + kHeadDim) * 4, "aliases fit in kst");
+    static constexpr size_t w_bytes = w_kst + WH * 32 * 4 + WH * kHeadDim * 4 + 64 * 8 * 2;
+    static constexpr int KCH = WH * KWH / 4;              // 16-byte K-word chunks per lane
     static constexpr size_t small = HG * kHeadDim * 4 /* qs */ + 64 * 16 /* rot */
         + HG * kHeadDim * 4 * 2 /* ks, kz */ + 64 * 4 /* cb */ + HG * 64 * 4 /* bound */
         + HG * 64 /* heavy flags */ + HG * 8 * 4 * 2 /* heavy lists */ + HG * 4 * 2 + 64;
@@ -191,35 +198,27 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     // per-warp scratch
     unsigned char *wp = wbase + warp * C::w_bytes;
     uint32_t *kst = reinterpret_cast<uint32_t *>(wp); wp += C::w_kst;
-    float *ps = reinterpret_cast<float *>(kst);                 // alias after the K phase
-    int *vfix = reinterpret_cast<int *>(kst) + WH * 32;         // alias after the K phase
     int *kfix = reinterpret_cast<int *>(wp); wp += WH * 32 * 4;
+    float *ps = reinterpret_cast<float *>(kfix);   // p of the tile, once the K terms are read
+    int *vfix = reinterpret_cast<int *>(wp); wp += WH * kHeadDim * 4;
     uint2 *anc16 = reinterpret_cast<uint2 *>(wp); wp += 64 * 8;
-    float2 *anc32 = reinterpret_cast<float2 *>(wp); wp += 64 * 8;
-    double2 *anc64 = reinterpret_cast<double2 *>(wp);
+    float2 *anc32 = reinterpret_cast<float2 *>(wp);
 
     // ------------------------------------------------------------- first tile's data
     // issued before the table build so the HBM latency overlaps the prologue
     const int t_first = t_begin + stream;
-    uint32_t kw[WH][KWH];
     uint32_t kitm[IPL], vitm[IPL];
     uint32_t cnt_k = 0, cnt_v = 0, ncnt_k = 0, ncnt_v = 0;
     float2 vsz = make_float2(0.f, 0.f);
-    // K words in two halves (RoPE pairs 0-31 and 32-63 of every head), so the prefetch of
-    // the next tile fits the register budget: the first half is issued during the second
-    // head's P.V, the second half at the end of the tile (consumed from pair 32 on)
-    auto load_k = [&](int t, int part) {
+    // K words of a tile (the warp's 2 heads: 3 KB contiguous in HBM) copied straight into kst
+    // with cp.async: issued once the previous tile's readers of kst are done, in flight during
+    // softmax, P.V and the V outliers, no registers held
+    auto issue_k = [&](int t) {
+        const unsigned char *src = reinterpret_cast<const unsigned char *>(
+            c.kcodes + ((int64_t)t * c.QW + (g0 + hw0) * KWH) * 32);
+        const uint32_t dst = smem_u32(kst);
 #pragma unroll
-        for (int h = 0; h < WH; ++h)
-#pragma unroll
-            for (int w = part * KWH / 2; w < (part + 1) * KWH / 2; ++w)
-                kw[h][w] = __ldg(c.kcodes + ((int64_t)t * c.QW + (g0 + hw0 + h) * KWH + w) * 32 + lane);
-    };
-    auto store_k = [&](int part) {   // to shared memory for the data-dependent readers
-#pragma unroll
-        for (int h = 0; h < WH; ++h)
-#pragma unroll
-            for (int w = part * KWH / 2; w < (part + 1) * KWH / 2; ++w) kst[(h * KWH + w) * 32 + lane] = kw[h][w];
+        for (int k = 0; k < C::KCH; ++k) cp_async16(dst + (uint32_t)(lane + 32 * k) * 16u, src + (lane + 32 * k) * 16);
     };
     auto load_counts = [&](int t, uint32_t &nk, uint32_t &nv) {
         nk = nv = 0;
@@ -244,8 +243,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         vsz = (int64_t)t * 32 + lane < P.T ? __ldg(c.vsz + (int64_t)t * 32 + lane) : make_float2(0.f, 0.f);
     };
     if (t_first < t_end) {
-        load_k(t_first, 0);
-        load_k(t_first, 1);
+        issue_k(t_first);
         load_counts(t_first, cnt_k, cnt_v);
     }
 
@@ -265,12 +263,16 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         t1f[x] = make_float2((float)co, (float)s);
         t1h[((i >> 1) * 32 + j) * 2 + (i & 1)] = pack_half2((float)co, (float)s);   // pairs i, i+1 adjacent
     }
-    // this warp's anchors cis((pos_base + 32 t_first) th_i), fp64 (advanced per tile)
-    for (int i = lane; i < 64; i += 32) {
+    // this warp's anchors cis((pos_base + 32 t_first) th_i), fp64 state in registers (pairs
+    // lane and lane + 32), advanced per tile
+    double2 anc64[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int i = lane + 32 * k;
         const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
         double s, co;
         sincos((double)(c.pos_base + (int64_t)t_first * kTileTokens) * th, &s, &co);
-        anc64[i] = make_double2(co, s);
+        anc64[k] = make_double2(co, s);
         anc32[i] = make_float2((float)co, (float)s);
         anc16[i] = make_uint2(pack_half2((float)co, (float)s), pack_half2(-(float)s, (float)co));
     }
@@ -406,7 +408,13 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             for (int w = 0; w < KWH; ++w)
                 vw[h][w] = __ldg(c.vcodes + vf_word(t, c.H_kv, g0 + hw0 + h, w, lane, BITS));
 
-        store_k(0);
+        cp_async_wait_all();
+        __syncwarp();
+        uint32_t kw[WH][KWH];
+#pragma unroll
+        for (int h = 0; h < WH; ++h)
+#pragma unroll
+            for (int w = 0; w < KWH; ++w) kw[h][w] = kst[(h * KWH + w) * 32 + lane];
 
         // ---------------------------------------------------------- a2: K dense
         float acc_c[WH], acc_s[WH];
@@ -416,7 +424,6 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         uint2 tj2;
 #pragma unroll
         for (int i = 0; i < kPairs; ++i) {
-            if (i == kPairs / 2) store_k(1);
             if ((i & 1) == 0) {   // rotation inputs of pairs i, i+1 in one load each
                 an2 = *reinterpret_cast<const uint4 *>(anc16 + i);
                 tj2 = reinterpret_cast<const uint2 *>(t1h)[(i >> 1) * 32 + lane];
@@ -515,6 +522,10 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         }
         __syncwarp();
 
+        // kst is free (heavy pairs and Key items done): the next tile's K words
+        const int tn = t + NSTREAM;
+        if (tn < t_end) issue_k(tn);
+
         // ------------------------------------------------------ a4: online softmax
         // weights p s_n 2^(WEXP - E) with E from the tile's largest s_n (fp16 normal range)
         const float smax = warp_max_redux(valid ? vsz.x : 0.f);
@@ -524,7 +535,6 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
 #pragma unroll
         for (int h = 0; h < WH; ++h) {
             float s = sco[h] + (float)kfix[h * 32 + lane] * (1.f / kKfixScale);
-            kfix[h * 32 + lane] = 0;
             s = valid ? s : -CUDART_INF_F;
             const float m_new = fmaxf(m_run[h], warp_max_redux(s));
             const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run[h] - m_new);
@@ -536,17 +546,15 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
 #pragma unroll
                 for (int r = 0; r < 4; ++r) acc[h][r] *= alpha;
             }
-            ps[h * 32 + lane] = p;   // kst is free: heavy pairs and Key items are done
+            ps[h * 32 + lane] = p;   // over this lane's K term, just read
             const uint32_t w16 = __half_as_ushort(__float2half_rn(p * (vsz.x * pe)));
             w2s[h] = w16 | (__shfl_down_sync(0xffffffffu, w16, 1) << 16);   // tokens lane, lane+1
         }
-        const int tn = t + NSTREAM;
         // --------------------------------------------------------- a5: P.V dense
 #pragma unroll
         for (int h = 0; h < WH; ++h) {
             // the next tile's K words, in flight during the rest of the tile (issued once the
             // first head's V words are consumed, to keep the register peak down)
-            if (h == 1 && tn < t_end) load_k(tn, 0);
             uint32_t bw[2][2];   // B fragments: weights of tokens 16 s2 + 2t (+1) and + 8
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
@@ -674,13 +682,16 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                         acc[h][2 * k + r] += (float)vfix[h * kHeadDim + 16 * (vt + 4 * k) + vg + 8 * r] * inv;
         }
         __syncwarp();
+#pragma unroll
+        for (int h = 0; h < WH; ++h) kfix[h * 32 + lane] = 0;   // p read by every lane: done
 
-        if (tn < t_end) load_k(tn, 1);
         // advance the anchors by NSTREAM tiles (fp64 complex rotation)
-        for (int i = lane; i < 64; i += 32) {
-            const double2 a = anc64[i], r = rot[i];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int i = lane + 32 * k;
+            const double2 a = anc64[k], r = rot[i];
             const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
-            anc64[i] = b;
+            anc64[k] = b;
             anc32[i] = make_float2((float)b.x, (float)b.y);
             anc16[i] = make_uint2(pack_half2((float)b.x, (float)b.y), pack_half2(-(float)b.y, (float)b.x));
         }
@@ -690,6 +701,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     }
 
     // ------------------------------------------- warp partials -> CTA partial (a7)
+    cp_async_wait_all();
     __syncwarp();
     float *wpart = reinterpret_cast<float *>(kst);   // [WH][d + 2]
 #pragma unroll

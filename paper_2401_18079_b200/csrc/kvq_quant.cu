@@ -144,7 +144,10 @@ __device__ void radix_select16(const uint16_t *keys, const uint8_t *flags, int D
 template <int BITS, int NT>
 __global__ void __launch_bounds__(NT)
 qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__ Vin, int64_t n0,
-          int mode) {
+          int mode, int part0) {
+    // part: 0 = Keys and Values of the token; 1 = Keys only, 2 = Values only (a single decode
+    // append runs the two halves as two CTAs, so its latency is the longer half, not the sum)
+    const int part = part0 < 0 ? 1 + (int)blockIdx.x : part0;
     constexpr int NLEV = 1 << BITS;
     constexpr int NM = NLEV - 1;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -162,7 +165,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     constexpr int QZ_WARPS = NT / 32;
     __shared__ double s_mk[16], s_mv[16];
 
-    const int64_t t = blockIdx.x;
+    const int64_t t = part0 < 0 ? 0 : blockIdx.x;
     const int64_t n = n0 + t;
     const int tid = threadIdx.x;
     const __half *krow = Kin + t * (int64_t)D;
@@ -172,8 +175,8 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
 
     if (tid < NM) { s_mk[tid] = c.mids[tid]; s_mv[tid] = c.mids[16 + tid]; }
     for (int i = tid; i < D; i += NT) {
-        xk[i] = kr16[i];
-        if (mode != 1) { uint16_t v = vr16[i]; xv[i] = v; vkey[i] = f16_order_key(v); vflag[i] = 0; }
+        if (part != 2) xk[i] = kr16[i];
+        if (mode != 1 && part != 1) { uint16_t v = vr16[i]; xv[i] = v; vkey[i] = f16_order_key(v); vflag[i] = 0; }
     }
     __syncthreads();
 
@@ -182,6 +185,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     const int E = (D + NT - 1) / NT;
     const int cb0 = min(D, tid * E), cb1 = min(D, cb0 + E);
 
+    if (part != 2) {   // Keys (the whole Key half of the token)
     // ------------------------------------------------------------------ Keys
     int kcnt = 0;
     uint32_t kmask = 0;   // outlier flags of this thread's channels (E <= 32)
@@ -271,6 +275,8 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         }
     }
 
+    }
+    if (part != 1) {   // Values
     // ----------------------------------------------------------------- Values
     const int k = c.kv;
     const int ku = (k + 1) / 2, kl = k / 2;
@@ -382,9 +388,11 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     }
     __syncthreads();
 
+    }
     // --------------------------------------------------------------- packing
     constexpr int PB = 2 * BITS;                 // bits per Key pair code
     const int tile = (int)(n >> 5), jj = (int)(n & 31);
+    if (part != 2)
     for (int q = tid; q < c.QW; q += NT) {
         const int h = q / (4 * BITS), w = q % (4 * BITS);
         const int bit0 = 32 * w;
@@ -396,6 +404,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         }
         c.kcodes[((int64_t)tile * c.QW + q) * 32 + jj] = (uint32_t)(acc >> off);
     }
+    if (part != 1)
     // Value codes into the fragment layout (kvq_internal.cuh): the two channels 16mt+g and
     // 16mt+g+8 of a head share a lane and sit 2b bits apart, so one OR per pair of codes.
     // Words are shared with the tile's other tokens (zeroed at create/reset).
@@ -496,12 +505,12 @@ cudaError_t launch_qz_bits(const DevCache &c, const __half *K, const __half *V, 
         cudaFuncSetAttribute(qz_kernel<BITS, QZ_THREADS_1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     if (T == 1) {
-        qz_kernel<BITS, QZ_THREADS_1><<<1, QZ_THREADS_1, smem, s>>>(c, K, V, n0, 0);
+        qz_kernel<BITS, QZ_THREADS_1><<<2, QZ_THREADS_1, smem, s>>>(c, K, V, n0, 0, -1);
         return cudaGetLastError();
     }
-    qz_kernel<BITS, QZ_THREADS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 1);
+    qz_kernel<BITS, QZ_THREADS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 1, 0);
     scan_counts_kernel<<<1, 1024, 0, s>>>(c, n0, T);
-    qz_kernel<BITS, QZ_THREADS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 2);
+    qz_kernel<BITS, QZ_THREADS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 2, 0);
     const int64_t tile0 = n0 / 32, tile1 = (n0 + T - 1) / 32;
     const unsigned nl = (unsigned)((tile1 - tile0 + 1) * c.NG);
     int pk = 1, pv = 1;
