@@ -370,7 +370,7 @@ def run_ours(args):
             "hbm_gbs_step": bytes_att * L / (ms_per_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(w.name),
-                         "kernel": ("att_wa_kernel" if info.get("attend_kernel") == 1 else "att_kernel")
+                         "kernel": {1: "att_wa_kernel", 2: "att_wag_kernel"}.get(info.get("attend_kernel"), "att_kernel")
                                    + " (kvq_decode_attend: one launch)",
                          "bytes_per_launch": bytes_att, "peak_kind": peak_kind,
                          "splits": info["splits"], "heads_per_cta": info["heads_per_cta"]},

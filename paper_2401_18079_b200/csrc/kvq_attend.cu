@@ -1113,10 +1113,11 @@ int attend_auto_splits(const DevCache &c, int64_t T, int hg) {
 cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_used, cudaStream_t s) {
     static const bool legacy = getenv("KVQ_ATT_LEGACY") != nullptr;
     const bool wa = !a.timers && !legacy && attend_wa_supported(c);
-    // CTA heads: 4 for the warp-autonomous kernel, else one bucket group
-    const int hg = wa ? 4 : (c.GW / kHeadDim) * c.G;
+    const bool wag = !a.timers && !legacy && attend_wag_supported(c);
+    // CTA heads: 4 for the warp-autonomous kernels, else one bucket group
+    const int hg = (wa || wag) ? 4 : (c.GW / kHeadDim) * c.G;
     if (hg == 0) return cudaErrorInvalidValue;
-    if (a.kernel_out) *a.kernel_out = wa ? 1 : 0;
+    if (a.kernel_out) *a.kernel_out = wa ? 1 : (wag ? 2 : 0);
     if (a.hg_out) *a.hg_out = hg;
     const int ntiles = (int)((a.T + 31) / 32);
     int S = a.splits > 0 ? a.splits : attend_auto_splits(c, a.T, hg);
@@ -1131,6 +1132,7 @@ cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_us
     // MHA at 2-3 bits: the warp-autonomous kernel (kvq_attend_wa.cu); KVQ_ATT_LEGACY=1 or the
     // phase-timer diagnostics select the two-halves kernel below
     if (wa) return launch_attend_wa(c, a, S, s);
+    if (wag) return launch_attend_wag(c, a, S, s);
     switch (c.bits) {
         case 2: return launch_b<2>(c, P, hg, grid, s);
         case 3: return launch_b<3>(c, P, hg, grid, s);

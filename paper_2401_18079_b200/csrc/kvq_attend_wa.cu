@@ -793,7 +793,650 @@ cudaError_t launch_wa_r(const DevCache &c, const WParams &P, int grid, cudaStrea
     return launch_wa_t<BITS, RESID, 2>(c, P, grid, s);
 }
 
+
+// ===================================================================================
+// Grouped-query attention (G = 4 query heads per KV head): att_wag_kernel.
+// One CTA = one KV head and its G query heads; 16 warps = 16 tile streams, each warp runs
+// whole tiles for all G heads.  Differences from the MHA kernel:
+//   a2  one lookup per (token, pair) returns the G heads' (A, B) entries (vector LDS of the
+//       code-interleaved tables) -> 2G FMAs, so the rotation and the extraction are shared;
+//   a5  the contraction is dense over the G heads: B = the G heads' weights (columns 0..G-1)
+//       and the mma accumulators persist across tiles (rescaled per head column when the
+//       running max or the weight exponent grows);
+//   a3/a6 every outlier item corrects all G heads.
+constexpr int NSG = 16;    // tile streams (= warps) per GQA CTA
+
+template <int BITS, bool RESID, int G>
+struct GCfg {
+    static constexpr int NWARP = NSG;
+    static constexpr int NTHR = NWARP * 32;
+    static constexpr int IPL = 4;
+    static constexpr int NE = 1 << (2 * BITS);
+    static constexpr int KWH = 4 * BITS;
+    static constexpr int HMAX = 8;
+    static constexpr size_t valign = (size_t)NE * 32 * 4;
+    static constexpr size_t vlut = (size_t)(RESID ? 2 : 1) * NE * 32 * 4;
+    static constexpr size_t klut = (size_t)G * kPairs * NE * 4;   // [i][pair code][G]
+    static constexpr size_t hlut = (size_t)G * HMAX * NE * 8;
+    static constexpr size_t t1h = (size_t)kPairs * 32 * 4;
+    static constexpr size_t t1f = (size_t)kPairs * 32 * 8;
+    // per warp: K words (cp.async target), K-outlier terms (then p) [G][32], V-outlier sums
+    // fp32 [G][128], anchors
+    static constexpr size_t w_kst = (size_t)KWH * 32 * 4;
+    static constexpr size_t w_bytes = w_kst + G * 32 * 4 + G * kHeadDim * 4 + 64 * 8 * 2;
+    static constexpr int KCH = KWH / 4;
+    static constexpr size_t small = G * kHeadDim * 4 /* qs */ + 64 * 16 /* rot */
+        + kHeadDim * 4 * 2 /* ks, kz */ + 64 * 4 /* cb */ + G * 64 * 4 /* bound */
+        + G * 64 /* heavy flags */ + G * 8 * 4 * 2 /* heavy lists */ + G * 4 * 2 + 64;
+    static constexpr size_t total = valign + vlut + klut + hlut + t1h + t1f + NWARP * w_bytes + small;
+};
+
+template <int G>
+__device__ __forceinline__ void lds_vecG(uint32_t addr, uint32_t (&v)[G]) {
+    if constexpr (G == 2) {
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(addr));
+    } else {
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(addr));
+    }
+}
+
+template <int BITS, bool RESID, int G>
+__global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(DevCache c, WParams P) {
+    using C = GCfg<BITS, RESID, G>;
+    constexpr int NWARP = C::NWARP, NTHR = C::NTHR, IPL = C::IPL;
+    constexpr int NE = C::NE;
+    constexpr int CM = (1 << BITS) - 1;
+    constexpr int KWH = C::KWH;
+    constexpr int HMAX = C::HMAX;
+    constexpr int FB = 2 * BITS;
+    constexpr int LG = G == 2 ? 1 : 2;
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t s0 = smem_u32(smem_raw);
+    unsigned char *sp = smem_raw + ((C::valign - (s0 % C::valign)) % C::valign);
+    uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
+    uint32_t *klut = reinterpret_cast<uint32_t *>(sp); sp += C::klut;
+    float2 *hlut = reinterpret_cast<float2 *>(sp); sp += C::hlut;
+    uint32_t *t1h = reinterpret_cast<uint32_t *>(sp); sp += C::t1h;
+    float2 *t1f = reinterpret_cast<float2 *>(sp); sp += C::t1f;
+    unsigned char *wbase = sp; sp += NWARP * C::w_bytes;
+    float *qs = reinterpret_cast<float *>(sp); sp += G * kHeadDim * 4;
+    double2 *rot = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    float *ks_s = reinterpret_cast<float *>(sp); sp += kHeadDim * 4;
+    float *kz_s = reinterpret_cast<float *>(sp); sp += kHeadDim * 4;
+    float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;
+    float *bound_s = reinterpret_cast<float *>(sp); sp += G * 64 * 4;
+    uint8_t *heavy_s = reinterpret_cast<uint8_t *>(sp); sp += G * 64;
+    int *hv_pair = reinterpret_cast<int *>(sp); sp += G * 8 * 4;
+    int *hv_n = reinterpret_cast<int *>(sp); sp += G * 8 * 4;
+    float *lut_sc = reinterpret_cast<float *>(sp); sp += G * 4;
+    float *lut_inv = reinterpret_cast<float *>(sp); sp += G * 4;
+    int *flag_s = reinterpret_cast<int *>(sp); sp += 64;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_hg = c.H_kv;   // one CTA per KV head
+    const int hk = blockIdx.x % n_hg;
+    const int split = blockIdx.x / n_hg;
+    const int g0 = hk * G;     // first query head
+    const int c_lo = hk * kHeadDim;
+    const int t_begin = (int)((int64_t)split * P.ntiles / P.S);
+    const int t_end = (int)((int64_t)(split + 1) * P.ntiles / P.S);
+    const int D = c.D;
+    const float *cbK = c.cb + 16, *cbV = c.cb + 48;
+
+    unsigned char *wp = wbase + warp * C::w_bytes;
+    uint32_t *kst = reinterpret_cast<uint32_t *>(wp); wp += C::w_kst;
+    int *kfix = reinterpret_cast<int *>(wp); wp += G * 32 * 4;
+    float *ps = reinterpret_cast<float *>(kfix);
+    float *osp = reinterpret_cast<float *>(wp); wp += G * kHeadDim * 4;
+    uint2 *anc16 = reinterpret_cast<uint2 *>(wp); wp += 64 * 8;
+    float2 *anc32 = reinterpret_cast<float2 *>(wp);
+
+    const int t_first = t_begin + warp;
+    uint32_t kitm[IPL], vitm[IPL];
+    uint32_t cnt_k = 0, cnt_v = 0, ncnt_k = 0, ncnt_v = 0;
+    float2 vsz = make_float2(0.f, 0.f);
+    auto issue_k = [&](int t) {
+        const unsigned char *src = reinterpret_cast<const unsigned char *>(c.kcodes + ((int64_t)t * c.QW + hk * KWH) * 32);
+        const uint32_t dst = smem_u32(kst);
+#pragma unroll
+        for (int k = 0; k < C::KCH; ++k) cp_async16(dst + (uint32_t)(lane + 32 * k) * 16u, src + (lane + 32 * k) * 16);
+    };
+    auto load_counts = [&](int t, uint32_t &nk, uint32_t &nv) {
+        nk = nv = 0;
+        if (t < t_end) {
+            const uint32_t *gc = c.gcnt + ((int64_t)t * c.NG + hk) * 2;
+            nk = __ldg(gc);
+            nv = __ldg(gc + 1);
+        }
+    };
+    auto load_items = [&](int t) {
+        const int64_t bucket = (int64_t)t * c.NG + hk;
+        const uint32_t nk = cnt_k > (uint32_t)c.kcap_g ? 0u : cnt_k;
+        const uint32_t nv = cnt_v > (uint32_t)c.vcap_g ? 0u : cnt_v;
+#pragma unroll
+        for (int k = 0; k < IPL; ++k) {
+            const uint32_t x = lane + 32 * k;
+            kitm[k] = x < nk ? __ldg(c.kit + bucket * c.kcap_g + x) : 0u;
+            vitm[k] = x < nv ? __ldg(c.vit + bucket * c.vcap_g + x) : 0u;
+        }
+        vsz = (int64_t)t * 32 + lane < P.T ? __ldg(c.vsz + (int64_t)t * 32 + lane) : make_float2(0.f, 0.f);
+    };
+    if (t_first < t_end) {
+        issue_k(t_first);
+        load_counts(t_first, cnt_k, cnt_v);
+    }
+
+    // ---------------------------------------------------------------- prologue (a1)
+    if (tid < 64) {
+        const int i = tid;
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)(NSG * kTileTokens) * th, &s, &co);
+        rot[i] = make_double2(co, s);
+    }
+    for (int x = tid; x < kPairs * 32; x += NTHR) {
+        const int i = x >> 5, j = x & 31;
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)j * th, &s, &co);
+        t1f[x] = make_float2((float)co, (float)s);
+        t1h[((i >> 1) * 32 + j) * 2 + (i & 1)] = pack_half2((float)co, (float)s);
+    }
+    double2 anc64[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int i = lane + 32 * k;
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)(c.pos_base + (int64_t)t_first * kTileTokens) * th, &s, &co);
+        anc64[k] = make_double2(co, s);
+        anc32[i] = make_float2((float)co, (float)s);
+        anc16[i] = make_uint2(pack_half2((float)co, (float)s), pack_half2(-(float)s, (float)co));
+    }
+    for (int x = lane; x < G * 32; x += 32) kfix[x] = 0;
+    for (int x = lane; x < G * kHeadDim; x += 32) osp[x] = 0.f;
+    for (int x = tid; x < kHeadDim; x += NTHR) {
+        ks_s[x] = c.kpar[c_lo + x];
+        kz_s[x] = c.kpar[D + c_lo + x];
+    }
+    if (tid < 64) cb_s[tid] = c.cb[tid];
+    if (tid < 16) flag_s[tid] = 0;
+    const double qscale = 1.4426950408889634 / sqrt((double)kHeadDim);
+    for (int x = tid; x < G * 64; x += NTHR) {
+        const int g = x >> 6, i = x & 63;
+        const __half *qg = P.q + (int64_t)(g0 + g) * kHeadDim;
+        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        double s, co;
+        sincos((double)P.pos * th, &s, &co);
+        const double a = (double)__half2float(qg[i]), b = (double)__half2float(qg[i + 64]);
+        qs[g * kHeadDim + i] = (float)((a * co - b * s) * qscale);
+        qs[g * kHeadDim + i + 64] = (float)((b * co + a * s) * qscale);
+    }
+    __syncthreads();
+    for (int x = tid; x < G * 64; x += NTHR) {
+        const int g = x >> 6, i = x & 63;
+        const int ci = i, cj = i + 64;
+        const float mx = fmaxf(fabsf(cbK[0] * ks_s[ci] + kz_s[ci]), fabsf(cbK[CM] * ks_s[ci] + kz_s[ci]));
+        const float my = fmaxf(fabsf(cbK[0] * ks_s[cj] + kz_s[cj]), fabsf(cbK[CM] * ks_s[cj] + kz_s[cj]));
+        const float qa = fabsf(qs[g * kHeadDim + i]), qb = fabsf(qs[g * kHeadDim + i + 64]);
+        bound_s[x] = fmaxf(qa * mx + qb * my, qb * mx + qa * my);
+    }
+    __syncthreads();
+    for (int g = warp; g < G; g += NWARP) {
+        const float b0 = bound_s[g * 64 + lane], b1 = bound_s[g * 64 + 32 + lane];
+        const float M = warp_max(fmaxf(b0, b1));
+        float tau = 0.5f * M;
+        unsigned m0 = __ballot_sync(0xffffffffu, b0 > tau), m1 = __ballot_sync(0xffffffffu, b1 > tau);
+        while (__popc(m0) + __popc(m1) > HMAX) {
+            tau *= 1.25f;
+            m0 = __ballot_sync(0xffffffffu, b0 > tau);
+            m1 = __ballot_sync(0xffffffffu, b1 > tau);
+        }
+        const unsigned lt = (1u << lane) - 1u;
+        const int n0c = __popc(m0);
+        if ((m0 >> lane) & 1u) hv_pair[g * 8 + __popc(m0 & lt)] = lane;
+        if ((m1 >> lane) & 1u) hv_pair[g * 8 + n0c + __popc(m1 & lt)] = lane + 32;
+        heavy_s[g * 64 + lane] = (m0 >> lane) & 1u;
+        heavy_s[g * 64 + 32 + lane] = (m1 >> lane) & 1u;
+        const float rest = warp_max(fmaxf(((m0 >> lane) & 1u) ? 0.f : b0, ((m1 >> lane) & 1u) ? 0.f : b1));
+        if (lane == 0) {
+            hv_n[g] = n0c + __popc(m1);
+            int e = 0;
+            if (rest > 0.f && isfinite(rest)) e = 14 - ilogbf(rest) - 1;
+            e = max(-100, min(100, e));
+            lut_sc[g] = ldexpf(1.f, e);
+            lut_inv[g] = ldexpf(1.f, -e);
+        }
+    }
+    __syncthreads();
+    // K table entries [i][pair code][g]: the G heads of a code adjacent (one vector load)
+    for (int x = tid; x < G * 64 * (CM + 1); x += NTHR) {
+        const int bb = x % (CM + 1), gi = x / (CM + 1);
+        const int g = gi >> 6, i = gi & 63;
+        const int ci = i, cj = i + 64;
+        const float sc = lut_sc[g];
+        const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
+        const float qa = qa1 * sc, qb = qb1 * sc;
+        const float yb = cbK[bb] * ks_s[cj] + kz_s[cj];
+        uint32_t *dst = klut + ((size_t)i * NE + (bb << BITS)) * G + g;
+        const bool heavy = heavy_s[gi] != 0;
+        int hslot = 0;
+        if (heavy)
+            for (int u = 0; u < hv_n[g]; ++u) hslot = hv_pair[g * 8 + u] == i ? u : hslot;
+#pragma unroll
+        for (int a = 0; a <= CM; ++a) {
+            const float xa = cbK[a] * ks_s[ci] + kz_s[ci];
+            if (heavy) {
+                dst[a * G] = 0u;
+                hlut[(g * HMAX + hslot) * NE + (bb << BITS) + a] = make_float2(qa1 * xa + qb1 * yb, qb1 * xa - qa1 * yb);
+            } else {
+                dst[a * G] = pack_half2(qa * xa + qb * yb, qb * xa - qa * yb);
+            }
+        }
+    }
+    for (int x = tid; x < NE * 32; x += NTHR) {
+        const int e = x >> 5;
+        const float ca = cbV[e & CM], cb = cbV[e >> BITS];
+        vlut[x] = pack_half2(ca, cb);
+        if constexpr (RESID)
+            vlut[NE * 32 + x] = pack_half2(ca - __half2float(__float2half_rn(ca)), cb - __half2float(__float2half_rn(cb)));
+    }
+    __syncthreads();
+
+    // ================================================================ tile loop (per warp)
+    const uint32_t klut_u = opaque(smem_u32(klut));
+    const uint32_t vlut_u = opaque(smem_u32(vlut) | (4u * lane));
+    const int vg = lane >> 2, vt = lane & 3;
+    const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
+    // P.V accumulators (mma D fragments): column 2vt + (0|1) = query head, rows vg, vg + 8 of
+    // m-tile ml; units 2^(E - WEXP) relative to the head's running max
+    float dacc[8][4];
+#pragma unroll
+    for (int ml = 0; ml < 8; ++ml) dacc[ml][0] = dacc[ml][1] = dacc[ml][2] = dacc[ml][3] = 0.f;
+    float m_run[G], l_lane[G], z_lane[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) { m_run[g] = -CUDART_INF_F; l_lane[g] = 0.f; z_lane[g] = 0.f; }
+    int E_run = -126;
+    const int hc0 = min(2 * vt, G - 1), hc1 = min(2 * vt + 1, G - 1);   // this lane's D columns
+    auto rot32 = [&](int i, int j, float &co, float &si) {
+        const float2 a = anc32[i];
+        const float2 tt = t1f[i * 32 + j];
+        co = a.x * tt.x - a.y * tt.y;
+        si = a.x * tt.y + a.y * tt.x;
+    };
+
+    for (int t = t_first; t < t_end; t += NSG) {
+        const int64_t n0 = (int64_t)t * 32;
+        const int ntok = (int)min((int64_t)32, P.T - n0);
+        const bool valid = lane < ntok;
+        const bool kov = cnt_k > (uint32_t)c.kcap_g, vov = cnt_v > (uint32_t)c.vcap_g;
+        const int nk = kov ? 0 : (int)cnt_k, nv = vov ? 0 : (int)cnt_v;
+        load_items(t);
+        load_counts(t + NSG, ncnt_k, ncnt_v);
+        uint32_t vw[KWH];
+#pragma unroll
+        for (int w = 0; w < KWH; ++w) vw[w] = __ldg(c.vcodes + vf_word(t, c.H_kv, hk, w, lane, BITS));
+
+        cp_async_wait_all();
+        __syncwarp();
+        uint32_t kw[KWH];
+#pragma unroll
+        for (int w = 0; w < KWH; ++w) kw[w] = kst[w * 32 + lane];
+
+        // ---------------------------------------------------------- a2: K dense
+        float acc_c[G], acc_s[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) { acc_c[g] = 0.f; acc_s[g] = 0.f; }
+        uint4 an2;
+        uint2 tj2;
+#pragma unroll
+        for (int i = 0; i < kPairs; ++i) {
+            if ((i & 1) == 0) {
+                an2 = *reinterpret_cast<const uint4 *>(anc16 + i);
+                tj2 = reinterpret_cast<const uint2 *>(t1h)[(i >> 1) * 32 + lane];
+            }
+            const uint2 an = (i & 1) ? make_uint2(an2.z, an2.w) : make_uint2(an2.x, an2.y);
+            const uint32_t tj = (i & 1) ? tj2.y : tj2.x;
+            const __half2 th = *reinterpret_cast<const __half2 *>(&tj);
+            const __half2 csh = __hfma2(*reinterpret_cast<const __half2 *>(&an.y), __high2half2(th),
+                                        __hmul2(*reinterpret_cast<const __half2 *>(&an.x), __low2half2(th)));
+            const uint32_t cs = *reinterpret_cast<const uint32_t *>(&csh);
+            const int bit = FB * i, w = bit >> 5, sh = bit & 31;
+            // (pair code << 2) << log2(G): the G heads' entries of a code are adjacent
+            uint32_t off;
+            if (sh + FB <= 32) off = sh >= 2 + LG ? (kw[w] >> (sh - 2 - LG)) : (kw[w] << (2 + LG - sh));
+            else off = __funnelshift_r(kw[w], kw[w + 1], sh - 2 - LG);
+            const uint32_t a = klut_u | (off & ((NE - 1) << (2 + LG)));
+            uint32_t ab[G];
+            lds_vecG<G>(a + (uint32_t)(i * NE * 4 * G), ab);
+#pragma unroll
+            for (int g = 0; g < G; ++g) fma2_f16_f32(ab[g], cs, acc_c[g], acc_s[g]);
+        }
+        __syncwarp();
+
+        // -------------------------------------------- a3: heavy pairs, Key outliers (fp32)
+        float sco[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float hs = 0.f;
+            const int nh = hv_n[g];
+            for (int u = 0; u < nh; ++u) {
+                const int i = hv_pair[g * 8 + u];
+                const int bit = FB * i;
+                const int wq = bit >> 5;
+                unsigned long long w64 = kst[wq * 32 + lane];
+                if ((bit & 31) + FB > 32) w64 |= (unsigned long long)kst[(wq + 1) * 32 + lane] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                const float2 ab = hlut[(g * HMAX + u) * NE + pc];
+                float co, si;
+                rot32(i, lane, co, si);
+                hs += co * ab.x + si * ab.y;
+            }
+            sco[g] = (acc_c[g] + acc_s[g]) * lut_inv[g] + hs;
+        }
+        // item -> the G heads' corrections (x - K^(code)) * dscore/dK
+        auto k_item = [&](uint32_t itm) {
+            const int j = (int)((itm >> 11) & 31u);
+            const int cc = (int)(itm & 0x7fu), flag = (int)((itm >> 9) & 3u);
+            const int i = cc & 63, up = cc >> 6;
+            int code = flag == 1 ? CM : 0;
+            if (flag == 0) {
+                const int bit = FB * i;
+                const int wq = bit >> 5;
+                unsigned long long w64 = kst[wq * 32 + j];
+                if ((bit & 31) + FB > 32) w64 |= (unsigned long long)kst[(wq + 1) * 32 + j] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                code = (pc >> (up * BITS)) & CM;
+            }
+            const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+            const float delta = xval - (cbKs[code] * ks_s[cc] + kz_s[cc]);
+            float co, si;
+            rot32(i, j, co, si);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
+                atomicAdd(&kfix[g * 32 + j], kfix_of(delta * (up ? (qb * co - qa * si) : (qa * co + qb * si))));
+            }
+        };
+        {
+            const int64_t bucket = (int64_t)t * c.NG + hk;
+#pragma unroll
+            for (int k = 0; k < IPL; ++k)
+                if (32 * k < nk && lane + 32 * k < nk) k_item(kitm[k]);
+            for (int x = 32 * IPL + lane; x < nk; x += 32) k_item(__ldg(c.kit + bucket * c.kcap_g + x));
+            if (kov) {
+                for (int j = 0; j < ntok; ++j) {
+                    const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
+                    for (uint32_t r = r0 + lane; r < r1; r += 32) {
+                        const uint32_t rec = __ldcg(c.kout + r);
+                        const int ch = (int)(rec & 0xffffu);
+                        if (ch < c_lo || ch >= c_lo + kHeadDim) continue;
+                        k_item((rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - c_lo));
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        const int tn = t + NSG;
+        if (tn < t_end) issue_k(tn);
+
+        // ------------------------------------------------------ a4: online softmax
+        // weights p s_n 2^(WEXP - E), E the running exponent bound of s_n (the accumulators
+        // persist across tiles)
+        const float smax = warp_max_redux(valid ? vsz.x : 0.f);
+        const int E_new = smax > 0.f ? max(E_run, ilog2f(smax) + 1) : E_run;
+        const float pe = pow2i(WEXP - E_new), rE = pow2i(E_run - E_new);
+        E_run = E_new;
+        uint32_t w2s[G];
+        float al[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float s = sco[g] + (float)kfix[g * 32 + lane] * (1.f / kKfixScale);
+            s = valid ? s : -CUDART_INF_F;
+            const float m_new = fmaxf(m_run[g], warp_max_redux(s));
+            const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run[g] - m_new);
+            const float p = valid ? exp2f(s - m_new) : 0.f;
+            l_lane[g] = l_lane[g] * alpha + p;
+            z_lane[g] = z_lane[g] * alpha + p * vsz.y;
+            m_run[g] = m_new;
+            al[g] = alpha;
+            if (alpha != 1.f) {   // warp-uniform
+#pragma unroll
+                for (int x = 0; x < kHeadDim / 32; ++x) osp[g * kHeadDim + x * 32 + lane] *= alpha;
+            }
+            ps[g * 32 + lane] = p;
+            const uint32_t w16 = __half_as_ushort(__float2half_rn(p * (vsz.x * pe)));
+            w2s[g] = w16 | (__shfl_down_sync(0xffffffffu, w16, 1) << 16);
+        }
+        {   // rescale the accumulators: per column (head) alpha, and the weight exponent
+            float a0 = al[0], a1 = al[0];
+#pragma unroll
+            for (int g = 1; g < G; ++g) { a0 = hc0 == g ? al[g] : a0; a1 = hc1 == g ? al[g] : a1; }
+            a0 *= rE; a1 *= rE;
+            if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
+#pragma unroll
+                for (int ml = 0; ml < 8; ++ml) {
+                    dacc[ml][0] *= a0; dacc[ml][2] *= a0;
+                    dacc[ml][1] *= a1; dacc[ml][3] *= a1;
+                }
+            }
+        }
+        // B fragments: column vg = query head vg (vg < G), tokens 16 s2 + 2 vt (+1) and + 8
+        uint32_t bw[2][2];
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                uint32_t v = 0u;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t x = __shfl_sync(0xffffffffu, w2s[g], 16 * s2 + 2 * vt + 8 * r);
+                    v = vg == g ? x : v;
+                }
+                bw[s2][r] = v;
+            }
+
+        // --------------------------------------------------------- a5: P.V dense
+#pragma unroll
+        for (int ml = 0; ml < 8; ++ml) {
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                uint32_t a[4], alo[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int bit = ((ml * 2 + s2) * 4 + r) * FB;
+                    const int wi = bit >> 5, sh = bit & 31;
+                    uint32_t off;
+                    if (sh + FB <= 32) off = sh >= 7 ? (vw[wi] >> (sh - 7)) : (vw[wi] << (7 - sh));
+                    else off = __funnelshift_r(vw[wi], vw[wi + 1], sh - 7);
+                    const uint32_t ad = vlut_u | (off & ((NE - 1) << 7));
+                    a[r] = lds_u32(ad);
+                    if constexpr (RESID) alo[r] = lds_u32(ad + NE * 32 * 4);
+                }
+                mma_f16_f32(dacc[ml], a, bw[s2]);
+                if constexpr (RESID) mma_f16_f32(dacc[ml], alo, bw[s2]);
+            }
+        }
+
+        // ------------------------------------------------------ a6: V outliers
+        __syncwarp();
+        auto v_item = [&](uint32_t itm, bool act) {
+            const int j = (int)((itm >> 11) & 31u), cc = (int)(itm & 0x7fu), flag = (int)((itm >> 9) & 3u);
+            int code = flag == 1 ? CM : 0;
+            if (act && flag == 0) {
+                const int bit = vf_bit(j, cc, BITS);
+                const uint32_t *wq = c.vcodes + vf_word(t, c.H_kv, hk, bit >> 5, vf_lane(j, cc), BITS);
+                unsigned long long w64 = __ldg(wq);
+                if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)__ldg(wq + 32) << 32;
+                code = (int)((w64 >> (bit & 31)) & CM);
+            }
+            const float s_n = __shfl_sync(0xffffffffu, vsz.x, j), z_n = __shfl_sync(0xffffffffu, vsz.y, j);
+            const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+            const float delta = xval - (cbVs[code] * s_n + z_n);
+            if (act) {
+#pragma unroll
+                for (int g = 0; g < G; ++g) atomicAdd(&osp[g * kHeadDim + cc], ps[g * 32 + j] * delta);
+            }
+        };
+#pragma unroll
+        for (int k = 0; k < IPL; ++k)
+            if (32 * k < nv) v_item(vitm[k], lane + 32 * k < nv);
+        if (nv > 32 * IPL || vov) {
+            const int64_t bucket = (int64_t)t * c.NG + hk;
+            for (int x0 = 32 * IPL; x0 < nv; x0 += 32) {
+                const bool act = x0 + lane < nv;
+                v_item(act ? __ldg(c.vit + bucket * c.vcap_g + x0 + lane) : 0u, act);
+            }
+            if (vov) {
+                const int kv = c.kv;
+                for (int r0 = 0; r0 < ntok * kv; r0 += 32) {
+                    const int r = r0 + lane;
+                    bool act = r < ntok * kv;
+                    uint32_t itm = 0u;
+                    if (act) {
+                        const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
+                        const int ch = (int)(rec & 0xffffu);
+                        act = ch >= c_lo && ch < c_lo + kHeadDim;
+                        itm = (rec & 0xffff0000u) | ((uint32_t)(r / kv) << 11) | (uint32_t)(act ? ch - c_lo : 0);
+                    }
+                    v_item(itm, act);
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < G; ++g) kfix[g * 32 + lane] = 0;
+
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int i = lane + 32 * k;
+            const double2 a = anc64[k], r = rot[i];
+            const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
+            anc64[k] = b;
+            anc32[i] = make_float2((float)b.x, (float)b.y);
+            anc16[i] = make_uint2(pack_half2((float)b.x, (float)b.y), pack_half2(-(float)b.y, (float)b.x));
+        }
+        cnt_k = ncnt_k;
+        cnt_v = ncnt_v;
+        __syncwarp();
+    }
+
+    // ------------------------------------------- warp partials -> CTA partial (a7)
+    cp_async_wait_all();
+    __syncwarp();
+    // osp (V-outlier sums, real units) += the dense accumulators of the lane's columns
+    {
+        const float sc = pow2i(E_run - WEXP);
+#pragma unroll
+        for (int ml = 0; ml < 8; ++ml) {
+            const int ch = ml * 16 + vg;
+            if (2 * vt < G) {
+                osp[(2 * vt) * kHeadDim + ch] += dacc[ml][0] * sc;
+                osp[(2 * vt) * kHeadDim + ch + 8] += dacc[ml][2] * sc;
+            }
+            if (2 * vt + 1 < G) {
+                osp[(2 * vt + 1) * kHeadDim + ch] += dacc[ml][1] * sc;
+                osp[(2 * vt + 1) * kHeadDim + ch + 8] += dacc[ml][3] * sc;
+            }
+        }
+    }
+    __syncwarp();
+    float *wpart = reinterpret_cast<float *>(osp);   // in place: [G][d] o, then m, l in kst
+    float *wml = reinterpret_cast<float *>(kst);     // [G][2]
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const float l = warp_sum(l_lane[g]), z = warp_sum(z_lane[g]);
+#pragma unroll
+        for (int x = 0; x < kHeadDim / 32; ++x) wpart[g * kHeadDim + x * 32 + lane] += z;
+        if (lane == 0) { wml[g * 2] = m_run[g]; wml[g * 2 + 1] = l; }
+    }
+    __syncthreads();
+    float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
+    for (int x = tid; x < G * (kHeadDim + 2); x += NTHR) {
+        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+        float m = -CUDART_INF_F;
+        for (int w = 0; w < NWARP; ++w) {
+            const float *ml = reinterpret_cast<const float *>(wbase + w * C::w_bytes) + g * 2;
+            if (ml[1] != 0.f) m = fmaxf(m, ml[0]);
+        }
+        float l = 0.f, o = 0.f;
+        for (int w = 0; w < NWARP; ++w) {
+            const float *ml = reinterpret_cast<const float *>(wbase + w * C::w_bytes) + g * 2;
+            if (ml[1] == 0.f) continue;
+            const float wt = exp2f(ml[0] - m);
+            l += wt * ml[1];
+            if (ch < kHeadDim) {
+                const float *ow = reinterpret_cast<const float *>(wbase + w * C::w_bytes + C::w_kst + G * 32 * 4);
+                o += wt * ow[g * kHeadDim + ch];
+            }
+        }
+        part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
+    }
+    __threadfence();
+    __syncthreads();
+    int *s_last = flag_s + 1;
+    if (tid == 0) {
+        const unsigned prev = atomicAdd(&P.tickets[hk], 1u);
+        *s_last = (prev == (unsigned)(P.S - 1));
+    }
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    for (int x = tid; x < G * (kHeadDim + 2); x += NTHR) {
+        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+        const int gq = g0 + g;
+        float m = -CUDART_INF_F;
+        for (int s = 0; s < P.S; ++s) {
+            const float *ps2 = P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2);
+            if (__ldcg(ps2 + kHeadDim + 1) != 0.f) m = fmaxf(m, __ldcg(ps2 + kHeadDim));
+        }
+        float l = 0.f, o = 0.f;
+        for (int s = 0; s < P.S; ++s) {
+            const float *ps2 = P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2);
+            const float ls = __ldcg(ps2 + kHeadDim + 1);
+            if (ls == 0.f) continue;
+            const float wgt = exp2f(__ldcg(ps2 + kHeadDim) - m);
+            l += wgt * ls;
+            if (ch < kHeadDim) o += wgt * __ldcg(ps2 + ch);
+        }
+        if (P.write_partial) {
+            P.out[gq * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
+        } else if (ch < kHeadDim) {
+            P.out[gq * kHeadDim + ch] = o / l;
+        }
+    }
+    if (tid == 0) P.tickets[hk] = 0;
+}
+
+template <int BITS, bool RESID>
+cudaError_t launch_wag_t(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
+    using C = GCfg<BITS, RESID, 4>;
+    static_assert(C::total <= 227 * 1024, "shared memory");
+    cudaError_t e = cudaFuncSetAttribute(att_wag_kernel<BITS, RESID, 4>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::total);
+    if (e != cudaSuccess) return e;
+    att_wag_kernel<BITS, RESID, 4><<<grid, C::NTHR, C::total, s>>>(c, P);
+    return cudaGetLastError();
+}
+
 }  // namespace
+
+bool attend_wag_supported(const DevCache &c) {
+    return c.G == 4 && (c.bits == 2 || c.bits == 3) && c.GW == kHeadDim;   // bucket per KV head
+}
+
+cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s) {
+    WParams P{};
+    P.q = a.q; P.pos = a.pos; P.T = a.T; P.S = S; P.ntiles = (int)((a.T + 31) / 32);
+    P.out = a.out; P.parts = a.parts; P.tickets = a.tickets; P.write_partial = a.write_partial;
+    const int grid = c.H_kv * S;
+    const bool resid = !c.vcb_exact16;
+    if (c.bits == 2) return resid ? launch_wag_t<2, true>(c, P, grid, s) : launch_wag_t<2, false>(c, P, grid, s);
+    if (c.bits == 3) return resid ? launch_wag_t<3, true>(c, P, grid, s) : launch_wag_t<3, false>(c, P, grid, s);
+    return cudaErrorInvalidValue;
+}
 
 bool attend_wa_supported(const DevCache &c) {
     return c.G == 1 && (c.bits == 2 || c.bits == 3) && c.H_q % HG == 0 &&

@@ -116,5 +116,8 @@ size_t attend_smem_bytes(int bits, int hg);
 bool attend_wa_supported(const DevCache &c);
 size_t attend_wa_smem_bytes(int bits, bool resid);
 cudaError_t launch_attend_wa(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s);
+// warp-autonomous GQA variant (G = 4, 2-3 bits): one CTA per KV head
+bool attend_wag_supported(const DevCache &c);
+cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s);
 
 }  // namespace kvq
