@@ -225,6 +225,7 @@ def run_ours(args):
                                 gen.gen_values(0, 0, 2048, D, stream=gen.STREAM_CAL_V),
                                 w.bits, w.ppm, qnorm=w.qnorm)
     caches = []
+    prefill_ms = 0.0
     t_setup = time.time()
     for l in range(L):
         c = kvq.KVQCache(n_q_heads=H, n_kv_heads=w.H_kv, head_dim=d, bits=w.bits,
@@ -240,7 +241,15 @@ def run_ours(args):
             b = min(n, a + chunk)
             Kl = gen.gen_layer_torch(1000 * l + 31 * rank + a, l, b - a, D, dev, "K")
             Vl = gen.gen_layer_torch(1000 * l + 31 * rank + a + 7, l, b - a, D, dev, "V")
-            c.prefill(Kl, Vl)
+            if l == 0:   # a9: time layer 0's prefill quantization (kvq_prefill_quantize)
+                pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                pe0.record()
+                c.prefill(Kl, Vl)
+                pe1.record()
+                pe1.synchronize()
+                prefill_ms += pe0.elapsed_time(pe1)
+            else:
+                c.prefill(Kl, Vl)
             del Kl, Vl
         caches.append(c)
     for c in caches:
@@ -343,6 +352,15 @@ def run_ours(args):
     achieved = bytes_att / (att_ms_mean * 1e-3) / 1e9
     info = caches[0].info()
 
+    # a9 prefill: HBM bytes per token-layer = K, V in (fp16) + codes, (s, z), CSC pointer and
+    # outlier records (canonical + bucketed) out; the prefill launches of layer 0, CUDA events
+    n_pf = plan.end - plan.start
+    pf_bytes = n_pf * (4 * D + 2 * D * w.bits / 8 + 8 + 4 + 8 * (kv + nnz_mean / max(Tc, 1)))
+    prefill_line = {"ns_per_token_layer": prefill_ms * 1e6 / max(n_pf, 1), "tokens": n_pf,
+                    "gbs": pf_bytes / (prefill_ms * 1e-3) / 1e9 if prefill_ms > 0 else None,
+                    "frac": (pf_bytes / (prefill_ms * 1e-3) / 1e9) / peak if prefill_ms > 0 else None,
+                    "kernels": "qz_kernel (count) + scan_counts_kernel + qz_kernel (write) + sort_buckets_kernel x2"}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -378,6 +396,8 @@ def run_ours(args):
             "gpu_launches": args.steps * L * (2 if world == 1 else 3),
             "clocks": clocks.summary(),
             "key_outliers_per_token": nnz_mean / max(Tc, 1),
+            "append_us_per_layer": (ms_per_step - att_ms_mean * L) * 1e3 / L,
+            "prefill": prefill_line,
             "setup_s": t_setup,
         }
         print(json.dumps(line), flush=True)
