@@ -253,3 +253,45 @@ def test_key_outlier_capacity_is_sticky(kvq):
     with pytest.raises(kvq.KVQError) as e:
         c.sync()
     assert e.value.status == kvq.KVQ_ECAPACITY
+
+
+@pytest.mark.parametrize("H_q,H_kv", [(8, 8), (32, 8)])
+@pytest.mark.parametrize("fill", ["prefill", "append"])
+def test_attend_concentrated_outliers(kvq, H_q, H_kv, fill):
+    """Outliers concentrated in one attend bucket group: tile 0 overflows its (tile, group)
+    buckets (Key and Value items then come from the CSC / CSR arrays), tile 1 holds more
+    items than the attend kernel keeps in registers (the in-bucket slow path), tile 2 is
+    ordinary.  Codes bit-exact and attention within the tolerance, MHA and GQA kernels."""
+    bits, ppm, T = 3, 10_000, 96
+    cal, K, V = setup_layer(21, 0, H_q, H_kv, bits, ppm, T)
+    K = K.astype(np.float32)
+    V = V.astype(np.float32)
+    gqa = H_q != H_kv
+    hi = cal["key_hi"].astype(np.float32)
+    kch = np.arange(1, 20, 2)                      # 10 Key channels of head 0
+    K[0:32, kch] = hi[kch] + 2.0                   # tile 0: > bucket capacity
+    if not gqa:
+        K[32:64, kch[:4]] = hi[kch[:4]] + 2.0      # tile 1: > 128 items, <= capacity
+    kv = -(-ppm * H_kv * 128 // 1_000_000)         # Value outliers per token
+    vch = np.arange(0, 2 * kv, 2)                  # kv channels of head 0
+    sgn = np.where(np.arange(kv) < (kv + 1) // 2, 1.0, -1.0)
+    V[0:32, vch] = 200.0 * sgn                     # tile 0: every outlier in group 0
+    n1 = 5 if gqa else 6
+    V[32:64, vch[:n1]] = 200.0 * np.where(np.arange(n1) % 2 == 0, 1.0, -1.0)
+    K = K.astype(np.float16)
+    V = V.astype(np.float16)
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H_q, H_kv, bits, ppm, capacity=T + 64)
+    if fill == "prefill":
+        c.prefill(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    else:
+        for n in range(T):
+            c.append(np.ascontiguousarray(K[n]), np.ascontiguousarray(V[n]))
+    c.sync()
+    assert_cache_equal(c.export(), ref)
+    q = gen.gen_queries(22, 0, H_q, H_kv, 128)[0]
+    o = torch.zeros((H_q, 128), dtype=torch.float32, device="cuda")
+    c.attend(torch.from_numpy(q).cuda(), T, o)
+    torch.cuda.synchronize()
+    err = rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, T, H_q, H_kv))
+    assert err.max() < TOL, err
