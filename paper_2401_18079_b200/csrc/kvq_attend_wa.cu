@@ -401,12 +401,15 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         load_counts(t + NSTREAM, ncnt_k, ncnt_v);
 
         // V words of this tile: in flight during the K phase
+        // V words: issued halfway through the K loop, once the first half's K words are dead
         uint32_t vw[WH][KWH];
+        auto load_v = [&]() {
 #pragma unroll
-        for (int h = 0; h < WH; ++h)
+            for (int h = 0; h < WH; ++h)
 #pragma unroll
-            for (int w = 0; w < KWH; ++w)
-                vw[h][w] = __ldg(c.vcodes + vf_word(t, c.H_kv, g0 + hw0 + h, w, lane, BITS));
+                for (int w = 0; w < KWH; ++w)
+                    vw[h][w] = __ldg(c.vcodes + vf_word(t, c.H_kv, g0 + hw0 + h, w, lane, BITS));
+        };
 
         cp_async_wait_all();
         __syncwarp();
@@ -424,6 +427,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         uint2 tj2;
 #pragma unroll
         for (int i = 0; i < kPairs; ++i) {
+            if (i == kPairs / 2) load_v();
             if ((i & 1) == 0) {   // rotation inputs of pairs i, i+1 in one load each
                 an2 = *reinterpret_cast<const uint4 *>(anc16 + i);
                 tj2 = reinterpret_cast<const uint2 *>(t1h)[(i >> 1) * 32 + lane];
