@@ -132,7 +132,8 @@ struct WCfg {
     static constexpr int KCH = WH * KWH / 4;              // 16-byte K-word chunks per lane
     static constexpr size_t small = HG * kHeadDim * 4 /* qs */ + 64 * 16 /* rot */
         + HG * kHeadDim * 4 * 2 /* ks, kz */ + 64 * 4 /* cb */ + HG * 64 * 4 /* bound */
-        + HG * 64 /* heavy flags */ + HG * 8 * 4 * 2 /* heavy lists */ + HG * 4 * 2 + 64;
+        + HG * 64 /* heavy flags */ + HG * 8 * 4 * 2 /* heavy lists */ + HG * 4 * 2 + 64
+        + 64 * 40 /* theta, cis(pos theta), cis(first tile) */;
     static constexpr size_t total = valign + vlut + klut + hlut + t1h + t1f + NWARP * w_bytes + small;
 };
 
@@ -178,6 +179,9 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     float *lut_sc = reinterpret_cast<float *>(sp); sp += HG * 4;
     float *lut_inv = reinterpret_cast<float *>(sp); sp += HG * 4;
     int *flag_s = reinterpret_cast<int *>(sp); sp += 64;
+    double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    double2 *cbase = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    double *th64 = reinterpret_cast<double *>(sp); sp += 64 * 8;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
@@ -248,16 +252,24 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     }
 
     // ---------------------------------------------------------------- prologue (a1)
+    // theta_i and the large-argument angles once per CTA (64 threads): cis(pos theta_i) for the
+    // query, cis((pos_base + 32 t_begin) theta_i) for the CTA's first tile (R11, R12)
     if (tid < 64) {
         const int i = tid;
         const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        th64[i] = th;
         double s, co;
         sincos((double)(NSTREAM * kTileTokens) * th, &s, &co);
         rot[i] = make_double2(co, s);
+        sincos((double)P.pos * th, &s, &co);
+        qcis[i] = make_double2(co, s);
+        sincos((double)(c.pos_base + (int64_t)t_begin * kTileTokens) * th, &s, &co);
+        cbase[i] = make_double2(co, s);
     }
+    __syncthreads();
     for (int x = tid; x < kPairs * 32; x += NTHR) {
         const int i = x >> 5, j = x & 31;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        const double th = th64[i];
         double s, co;
         sincos((double)j * th, &s, &co);
         t1f[x] = make_float2((float)co, (float)s);
@@ -269,9 +281,11 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         const int i = lane + 32 * k;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
-        double s, co;
-        sincos((double)(c.pos_base + (int64_t)t_first * kTileTokens) * th, &s, &co);
+        // cis((pos_base + 32 t_first) th_i) = cis(the CTA's first tile) x cis(32 (t_first - t_begin) th_i)
+        double sr, cr;
+        sincos((double)((t_first - t_begin) * kTileTokens) * th64[i], &sr, &cr);
+        const double2 b0 = cbase[i];
+        const double co = b0.x * cr - b0.y * sr, s = b0.x * sr + b0.y * cr;
         anc64[k] = make_double2(co, s);
         anc32[i] = make_float2((float)co, (float)s);
         anc16[i] = make_uint2(pack_half2((float)co, (float)s), pack_half2(-(float)s, (float)co));
@@ -287,9 +301,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     for (int x = tid; x < HG * 64; x += NTHR) {
         const int g = x >> 6, i = x & 63;
         const __half *qg = P.q + (int64_t)(g0 + g) * kHeadDim;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
-        double s, co;
-        sincos((double)P.pos * th, &s, &co);
+        const double co = qcis[i].x, s = qcis[i].y;
         const double a = (double)__half2float(qg[i]), b = (double)__half2float(qg[i + 64]);
         qs[g * kHeadDim + i] = (float)((a * co - b * s) * qscale);
         qs[g * kHeadDim + i + 64] = (float)((b * co + a * s) * qscale);
@@ -831,7 +843,8 @@ struct GCfg {
     static constexpr int KCH = KWH / 4;
     static constexpr size_t small = G * kHeadDim * 4 /* qs */ + 64 * 16 /* rot */
         + kHeadDim * 4 * 2 /* ks, kz */ + 64 * 4 /* cb */ + G * 64 * 4 /* bound */
-        + G * 64 /* heavy flags */ + G * 8 * 4 * 2 /* heavy lists */ + G * 4 * 2 + 64;
+        + G * 64 /* heavy flags */ + G * 8 * 4 * 2 /* heavy lists */ + G * 4 * 2 + 64
+        + 64 * 40 /* theta, cis(pos theta), cis(first tile) */;
     static constexpr size_t total = valign + vlut + klut + hlut + t1h + t1f + NWARP * w_bytes + small;
 };
 
@@ -877,6 +890,9 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
     float *lut_sc = reinterpret_cast<float *>(sp); sp += G * 4;
     float *lut_inv = reinterpret_cast<float *>(sp); sp += G * 4;
     int *flag_s = reinterpret_cast<int *>(sp); sp += 64;
+    double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    double2 *cbase = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    double *th64 = reinterpret_cast<double *>(sp); sp += 64 * 8;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_kv;   // one CTA per KV head
@@ -933,16 +949,24 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
     }
 
     // ---------------------------------------------------------------- prologue (a1)
+    // theta_i and the large-argument angles once per CTA (64 threads): cis(pos theta_i) for the
+    // query, cis((pos_base + 32 t_begin) theta_i) for the CTA's first tile (R11, R12)
     if (tid < 64) {
         const int i = tid;
         const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        th64[i] = th;
         double s, co;
         sincos((double)(NSG * kTileTokens) * th, &s, &co);
         rot[i] = make_double2(co, s);
+        sincos((double)P.pos * th, &s, &co);
+        qcis[i] = make_double2(co, s);
+        sincos((double)(c.pos_base + (int64_t)t_begin * kTileTokens) * th, &s, &co);
+        cbase[i] = make_double2(co, s);
     }
+    __syncthreads();
     for (int x = tid; x < kPairs * 32; x += NTHR) {
         const int i = x >> 5, j = x & 31;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        const double th = th64[i];
         double s, co;
         sincos((double)j * th, &s, &co);
         t1f[x] = make_float2((float)co, (float)s);
@@ -952,9 +976,11 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         const int i = lane + 32 * k;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
-        double s, co;
-        sincos((double)(c.pos_base + (int64_t)t_first * kTileTokens) * th, &s, &co);
+        // cis((pos_base + 32 t_first) th_i) = cis(the CTA's first tile) x cis(32 (t_first - t_begin) th_i)
+        double sr, cr;
+        sincos((double)((t_first - t_begin) * kTileTokens) * th64[i], &sr, &cr);
+        const double2 b0 = cbase[i];
+        const double co = b0.x * cr - b0.y * sr, s = b0.x * sr + b0.y * cr;
         anc64[k] = make_double2(co, s);
         anc32[i] = make_float2((float)co, (float)s);
         anc16[i] = make_uint2(pack_half2((float)co, (float)s), pack_half2(-(float)s, (float)co));
@@ -971,9 +997,7 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
     for (int x = tid; x < G * 64; x += NTHR) {
         const int g = x >> 6, i = x & 63;
         const __half *qg = P.q + (int64_t)(g0 + g) * kHeadDim;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
-        double s, co;
-        sincos((double)P.pos * th, &s, &co);
+        const double co = qcis[i].x, s = qcis[i].y;
         const double a = (double)__half2float(qg[i]), b = (double)__half2float(qg[i + 64]);
         qs[g * kHeadDim + i] = (float)((a * co - b * s) * qscale);
         qs[g * kHeadDim + i + 64] = (float)((b * co + a * s) * qscale);
