@@ -1,11 +1,11 @@
 #!/bin/bash
-# round-1 evidence after the GQA kernel: smoke, GPU tests, default bench (C3 + oracle CPU
+# GPU evidence for the bench lines and profiles (TAG env = output dir): smoke, GPU tests, default bench (C3 + oracle CPU
 # baseline), C2 / C4 / C5-shard / C3-4bit bench lines, ncu launch list + full captures of the
 # MHA and GQA attend kernels.
 set -u
-OUT=gpurun_out/r1c
+OUT=gpurun_out/${TAG:-r1d}
 mkdir -p $OUT
-bash scripts/gpu_round.sh r1c > $OUT/round.txt 2>&1
+bash scripts/gpu_round.sh ${TAG:-r1d} > $OUT/round.txt 2>&1
 timeout 600 python bench.py --workload c2 --no-cpu-baseline > $OUT/bench_c2.json 2>$OUT/bench_c2.err
 timeout 1200 python bench.py --workload c4 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_c4.json 2>$OUT/bench_c4.err
 timeout 900 python bench.py --workload c5 --tokens 1250000 --layers 4 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_c5.json 2>$OUT/bench_c5.err
