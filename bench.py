@@ -396,6 +396,9 @@ def run_ours(args):
             "gpu_launches": args.steps * L * (2 if world == 1 else 3),
             "clocks": clocks.summary(),
             "key_outliers_per_token": nnz_mean / max(Tc, 1),
+            # effective: step time minus the attend-only time (the attend launched right after
+            # an append overlaps its prologue with the append through programmatic dependent
+            # launch, so this is below the append kernel's own duration)
             "append_us_per_layer": (ms_per_step - att_ms_mean * L) * 1e3 / L,
             "prefill": prefill_line,
             "setup_s": t_setup,

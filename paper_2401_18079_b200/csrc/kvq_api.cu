@@ -19,6 +19,8 @@ struct kvq_cache {
     int64_t T = 0;             // host shadow of the token count
     int hg = 0;                // query heads per attend CTA (of the last launch)
     int last_kernel = -1;      // attend kernel of the last launch (kvq_info.attend_kernel)
+    int pdl_ok = 0;            // the last op on pdl_stream was a single-token append
+    void *pdl_stream = nullptr;
     int splits_forced = 0;
     int last_splits = 0;
     float *parts = nullptr;    // [max_splits][H_q][d+2]
@@ -342,6 +344,8 @@ static kvq_status append_tokens(kvq_cache *c, const void *K, const void *V, int6
     cudaError_t e = launch_quantize(c->dc, Kd, Vd, c->T, T, s);
     if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
     c->T += T;
+    c->pdl_ok = T == 1;
+    c->pdl_stream = stream;
     return KVQ_OK;
 }
 
@@ -394,6 +398,8 @@ static kvq_status attend_impl(kvq_cache *c, const void *q, int64_t pos, float *o
     a.timers = c->timers;
     a.kernel_out = &c->last_kernel;
     a.hg_out = &c->hg;
+    a.pdl = c->pdl_ok && c->pdl_stream == stream && cq == 0 && !getenv("KVQ_NO_PDL");
+    c->pdl_ok = 0;
     cudaError_t e = launch_attend(c->dc, a, &c->last_splits, s);
     if (e != cudaSuccess) return cuda_fail(e, "attend launch");
     if (co == 1) {

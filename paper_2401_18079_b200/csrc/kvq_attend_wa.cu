@@ -144,7 +144,29 @@ struct WParams {
     float *out, *parts;
     unsigned *tickets;
     int write_partial;
+    int pdl;
 };
+
+// Programmatic dependent launch: everything before pdl_wait() reads only the query and the
+// cache's constant parameters (codebooks, Key thresholds), so it may overlap the preceding
+// append kernel; cache contents are read after it.  A no-op without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename K, typename... Args>
+cudaError_t launch_maybe_pdl(K kernel, int grid, int threads, size_t smem, cudaStream_t s, bool pdl,
+                             Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 
 template <int BITS, bool RESID, int WH>
 __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(DevCache c, WParams P) {
@@ -246,10 +268,6 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         }
         vsz = (int64_t)t * 32 + lane < P.T ? __ldg(c.vsz + (int64_t)t * 32 + lane) : make_float2(0.f, 0.f);
     };
-    if (t_first < t_end) {
-        issue_k(t_first);
-        load_counts(t_first, cnt_k, cnt_v);
-    }
 
     // ---------------------------------------------------------------- prologue (a1)
     // theta_i and the large-argument angles once per CTA (64 threads): cis(pos theta_i) for the
@@ -380,6 +398,13 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             vlut[NE * 32 + x] = pack_half2(ca - __half2float(__float2half_rn(ca)), cb - __half2float(__float2half_rn(cb)));
     }
     __syncthreads();
+
+    // cache contents from here on (the preceding append must be complete)
+    pdl_wait();
+    if (t_first < t_end) {
+        issue_k(t_first);
+        load_counts(t_first, cnt_k, cnt_v);
+    }
 
     // ================================================================ tile loop (per warp)
     // table bases, OR-ed with the shifted codes (the compiler must not turn the OR into an add)
@@ -800,7 +825,8 @@ cudaError_t launch_wa_t(const DevCache &c, const WParams &P, int grid, cudaStrea
     cudaError_t e = cudaFuncSetAttribute(att_wa_kernel<BITS, RESID, WH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::total);
     if (e != cudaSuccess) return e;
-    att_wa_kernel<BITS, RESID, WH><<<grid, C::NTHR, C::total, s>>>(c, P);
+    e = launch_maybe_pdl(att_wa_kernel<BITS, RESID, WH>, grid, C::NTHR, C::total, s, P.pdl != 0, c, P);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -943,10 +969,6 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         }
         vsz = (int64_t)t * 32 + lane < P.T ? __ldg(c.vsz + (int64_t)t * 32 + lane) : make_float2(0.f, 0.f);
     };
-    if (t_first < t_end) {
-        issue_k(t_first);
-        load_counts(t_first, cnt_k, cnt_v);
-    }
 
     // ---------------------------------------------------------------- prologue (a1)
     // theta_i and the large-argument angles once per CTA (64 threads): cis(pos theta_i) for the
@@ -1072,6 +1094,12 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
             vlut[NE * 32 + x] = pack_half2(ca - __half2float(__float2half_rn(ca)), cb - __half2float(__float2half_rn(cb)));
     }
     __syncthreads();
+
+    pdl_wait();
+    if (t_first < t_end) {
+        issue_k(t_first);
+        load_counts(t_first, cnt_k, cnt_v);
+    }
 
     // ================================================================ tile loop (per warp)
     const uint32_t klut_u = opaque(smem_u32(klut));
@@ -1445,7 +1473,8 @@ cudaError_t launch_wag_t(const DevCache &c, const WParams &P, int grid, cudaStre
     cudaError_t e = cudaFuncSetAttribute(att_wag_kernel<BITS, RESID, 4>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::total);
     if (e != cudaSuccess) return e;
-    att_wag_kernel<BITS, RESID, 4><<<grid, C::NTHR, C::total, s>>>(c, P);
+    e = launch_maybe_pdl(att_wag_kernel<BITS, RESID, 4>, grid, C::NTHR, C::total, s, P.pdl != 0, c, P);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -1459,6 +1488,7 @@ cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cud
     WParams P{};
     P.q = a.q; P.pos = a.pos; P.T = a.T; P.S = S; P.ntiles = (int)((a.T + 31) / 32);
     P.out = a.out; P.parts = a.parts; P.tickets = a.tickets; P.write_partial = a.write_partial;
+    P.pdl = a.pdl;
     const int grid = c.H_kv * S;
     const bool resid = !c.vcb_exact16;
     if (c.bits == 2) return resid ? launch_wag_t<2, true>(c, P, grid, s) : launch_wag_t<2, false>(c, P, grid, s);
@@ -1481,6 +1511,7 @@ cudaError_t launch_attend_wa(const DevCache &c, const AttendArgs &a, int S, cuda
     WParams P{};
     P.q = a.q; P.pos = a.pos; P.T = a.T; P.S = S; P.ntiles = (int)((a.T + 31) / 32);
     P.out = a.out; P.parts = a.parts; P.tickets = a.tickets; P.write_partial = a.write_partial;
+    P.pdl = a.pdl;
     const int grid = (c.H_q / HG) * S;
     const bool resid = !c.vcb_exact16;
     if (c.bits == 2) return resid ? launch_wa_r<2, true>(c, P, grid, s) : launch_wa_r<2, false>(c, P, grid, s);

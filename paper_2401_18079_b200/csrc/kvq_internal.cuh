@@ -104,6 +104,9 @@ struct AttendArgs {
     unsigned long long *timers;   // diagnostics: phase cycle sums, or null
     int *kernel_out;     // optional: 1 = warp-autonomous kernel launched, 0 = two-halves
     int *hg_out;         // optional: query heads per CTA of the launch
+    int pdl;             // 1: the previous kernel on the stream is this cache's append, so the
+                         // warp-autonomous kernels launch with programmatic dependent launch
+                         // (their q/table prologue overlaps the append; cache reads wait)
 };
 int attend_heads_per_cta(int bits, int H_q, int G);
 int attend_bucket_heads(int bits, int H_q, int G);

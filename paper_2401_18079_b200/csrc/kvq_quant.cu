@@ -148,6 +148,8 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     // part: 0 = Keys and Values of the token; 1 = Keys only, 2 = Values only (a single decode
     // append runs the two halves as two CTAs, so its latency is the longer half, not the sum)
     const int part = part0 < 0 ? 1 + (int)blockIdx.x : part0;
+    // a decode append lets a dependent attend launch now (its prologue reads no cache data)
+    if (part0 < 0) asm volatile("griddepcontrol.launch_dependents;");
     constexpr int NLEV = 1 << BITS;
     constexpr int NM = NLEV - 1;
     extern __shared__ __align__(16) unsigned char smem[];
