@@ -269,6 +269,14 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         vsz = (int64_t)t * 32 + lane < P.T ? __ldg(c.vsz + (int64_t)t * 32 + lane) : make_float2(0.f, 0.f);
     };
 
+    // the first tile's K words and counts overlap the prologue unless the tile is the tail tile
+    // (which a concurrent append may still be writing, see pdl_wait)
+    const bool early = t_first < t_end && t_first != P.ntiles - 1;
+    if (early) {
+        issue_k(t_first);
+        load_counts(t_first, cnt_k, cnt_v);
+    }
+
     // ---------------------------------------------------------------- prologue (a1)
     // theta_i and the large-argument angles once per CTA (64 threads): cis(pos theta_i) for the
     // query, cis((pos_base + 32 t_begin) theta_i) for the CTA's first tile (R11, R12)
@@ -399,9 +407,10 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     }
     __syncthreads();
 
-    // cache contents from here on (the preceding append must be complete)
+    // cache contents from here on (the preceding append must be complete); a first tile that is
+    // not the tail tile (the only one an append writes) was issued before the prologue
     pdl_wait();
-    if (t_first < t_end) {
+    if (t_first < t_end && !early) {
         issue_k(t_first);
         load_counts(t_first, cnt_k, cnt_v);
     }
@@ -970,6 +979,14 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         vsz = (int64_t)t * 32 + lane < P.T ? __ldg(c.vsz + (int64_t)t * 32 + lane) : make_float2(0.f, 0.f);
     };
 
+    // the first tile's K words and counts overlap the prologue unless the tile is the tail tile
+    // (which a concurrent append may still be writing, see pdl_wait)
+    const bool early = t_first < t_end && t_first != P.ntiles - 1;
+    if (early) {
+        issue_k(t_first);
+        load_counts(t_first, cnt_k, cnt_v);
+    }
+
     // ---------------------------------------------------------------- prologue (a1)
     // theta_i and the large-argument angles once per CTA (64 threads): cis(pos theta_i) for the
     // query, cis((pos_base + 32 t_begin) theta_i) for the CTA's first tile (R11, R12)
@@ -1096,7 +1113,7 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
     __syncthreads();
 
     pdl_wait();
-    if (t_first < t_end) {
+    if (t_first < t_end && !early) {
         issue_k(t_first);
         load_counts(t_first, cnt_k, cnt_v);
     }
