@@ -111,7 +111,7 @@ __device__ __forceinline__ void select_bin(const int *hist, int need, int *out /
 // Loop trip counts are uniform across the CTA (E elements per thread).
 template <int NT>
 __device__ void radix_select16(const uint16_t *keys, const uint8_t *flags, int D, int c_begin,
-                               int E, int need, bool desc, int *hist /*[256]*/,
+                               int E, int o16, int o8, int need, bool desc, int *hist /*[256]*/,
                                int *shared_out /*[4]*/, int *tau_out, int *gt_out) {
     int prefix_hi = -1;   // selected high byte
     int gt = 0;
@@ -120,9 +120,9 @@ __device__ void radix_select16(const uint16_t *keys, const uint8_t *flags, int D
         __syncthreads();
         for (int e = 0; e < E; ++e) {
             const int c = c_begin + e;
-            bool valid = c < D && !flags[c];
+            bool valid = c < D && !flags[c + o8];
             int kk = 0;
-            if (valid) kk = desc ? keys[c] : (0xffff - keys[c]);
+            if (valid) kk = desc ? keys[c + o16] : (0xffff - keys[c + o16]);
             if (pass == 0) {
                 hist_add(hist, kk >> 8, valid);   // top bytes cluster: aggregate per warp
             } else if (valid && (kk >> 8) == prefix_hi) {
@@ -154,13 +154,21 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     constexpr int NM = NLEV - 1;
     extern __shared__ __align__(16) unsigned char smem[];
     const int D = c.D;
-    uint16_t *xk = reinterpret_cast<uint16_t *>(smem);          // [D]
-    uint16_t *xv = xk + D;                                        // [D]
-    uint16_t *vkey = xv + D;                                      // [D]
-    uint8_t *kc = reinterpret_cast<uint8_t *>(vkey + D);          // [D]
-    uint8_t *vc = kc + D;                                         // [D]
-    uint8_t *vflag = vc + D;                                      // [D]
-    int *hist = reinterpret_cast<int *>(vflag + ((D + 15) & ~15));// [256]
+    // Per-channel arrays, thread-contiguous ownership (E channels per thread).  Each thread's
+    // segment is padded (2 halves / 4 bytes) when its stride in words would be even, so the
+    // threads of a warp reading "their e-th channel" hit distinct banks (unpadded, E = 16 was
+    // 8-way conflicted on the 16-bit arrays and 4-way on the byte arrays).
+    const int E = (D + NT - 1) / NT;
+    const int pad16 = (E % 4 == 0) ? 2 : 0;
+    const int pad8 = (E % 8 == 0) ? 4 : 0;
+    const int L16 = D + NT * pad16, L8 = D + NT * pad8;
+    uint16_t *xk = reinterpret_cast<uint16_t *>(smem);          // [L16]
+    uint16_t *xv = xk + L16;                                      // [L16]
+    uint16_t *vkey = xv + L16;                                    // [L16]
+    uint8_t *kc = reinterpret_cast<uint8_t *>(vkey + L16);        // [L8]
+    uint8_t *vc = kc + L8;                                        // [L8]
+    uint8_t *vflag = vc + L8;                                     // [L8]
+    int *hist = reinterpret_cast<int *>(vflag + ((L8 + 15) & ~15));// [256]
     int *sbuf = hist + 256;                                       // [64]
     int *sout = sbuf + 64;                                        // [64]
     float *fred = reinterpret_cast<float *>(sout + 64);           // [64]
@@ -170,36 +178,41 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     const int64_t t = part0 < 0 ? 0 : blockIdx.x;
     const int64_t n = n0 + t;
     const int tid = threadIdx.x;
+    // padded index of channel ch (any thread) and this thread's offsets for its own channels
+    const unsigned long long einv = ((1ull << 20) + E - 1) / E;   // exact ch / E for ch < 8192
+    auto seg = [&](int ch) -> int { return (int)(((unsigned long long)ch * einv) >> 20); };
+    auto I16 = [&](int ch) -> int { return ch + seg(ch) * pad16; };
+    auto I8 = [&](int ch) -> int { return ch + seg(ch) * pad8; };
+    const int o16 = tid * pad16, o8 = tid * pad8;
     const __half *krow = Kin + t * (int64_t)D;
     const __half *vrow = Vin + t * (int64_t)D;
     const uint16_t *kr16 = reinterpret_cast<const uint16_t *>(krow);
     const uint16_t *vr16 = reinterpret_cast<const uint16_t *>(vrow);
 
     if (tid < NM) { s_mk[tid] = c.mids[tid]; s_mv[tid] = c.mids[16 + tid]; }
-    for (int i = tid; i < D; i += NT) {
-        if (part != 2) xk[i] = kr16[i];
-        if (mode != 1 && part != 1) { uint16_t v = vr16[i]; xv[i] = v; vkey[i] = f16_order_key(v); vflag[i] = 0; }
+    // thread-contiguous channel ownership keeps ranks in ascending channel order
+    const int cb0 = min(D, tid * E), cb1 = min(D, cb0 + E);
+    for (int i = cb0; i < cb1; ++i) {
+        if (part != 2) xk[i + o16] = kr16[i];
+        if (mode != 1 && part != 1) { uint16_t v = vr16[i]; xv[i + o16] = v; vkey[i + o16] = f16_order_key(v); vflag[i + o8] = 0; }
     }
     __syncthreads();
 
     const float *ks = c.kpar, *kz = c.kpar + D, *klo = c.kpar + 2 * D, *khi = c.kpar + 3 * D;
-    // thread-contiguous channel ownership keeps ranks in ascending channel order
-    const int E = (D + NT - 1) / NT;
-    const int cb0 = min(D, tid * E), cb1 = min(D, cb0 + E);
 
     if (part != 2) {   // Keys (the whole Key half of the token)
     // ------------------------------------------------------------------ Keys
     int kcnt = 0;
     uint32_t kmask = 0;   // outlier flags of this thread's channels (E <= 32)
     for (int ch = cb0; ch < cb1; ++ch) {
-        float x = h2f(xk[ch]);
+        float x = h2f(xk[ch + o16]);
         float lo = klo[ch], hi = khi[ch];
         bool out = (x < lo) || (x > hi);
         kcnt += out;
         kmask |= (uint32_t)out << (ch - cb0);
         if (mode != 1) {
             float y = x < lo ? lo : (x > hi ? hi : x);
-            kc[ch] = (uint8_t)enc_fp64<NM>((double)y, (double)ks[ch], (double)kz[ch], s_mk);
+            kc[ch + o8] = (uint8_t)enc_fp64<NM>((double)y, (double)ks[ch], (double)kz[ch], s_mk);
         }
     }
     int ktotal;
@@ -233,7 +246,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
             uint32_t pos = s_base + (uint32_t)krank;
             for (uint32_t m = kmask; m; m &= m - 1) {
                 const int ch = cb0 + __ffs(m) - 1;
-                c.kout[pos++] = (uint32_t)ch | ((uint32_t)xk[ch] << 16);
+                c.kout[pos++] = (uint32_t)ch | ((uint32_t)xk[ch + o16] << 16);
             }
         }
     }
@@ -270,7 +283,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
             for (uint32_t m = kmask; m; m &= m - 1) {
                 const int ch = cb0 + __ffs(m) - 1;
                 if (pos < c.kcap_g)
-                    dst[pos] = ((uint32_t)xk[ch] << 16) | ((uint32_t)jj0 << 11) | item_code_flag<BITS>(kc[ch]) |
+                    dst[pos] = ((uint32_t)xk[ch + o16] << 16) | ((uint32_t)jj0 << 11) | item_code_flag<BITS>(kc[ch + o8]) |
                                (uint32_t)(ch - myg * c.GW);
                 ++pos;
             }
@@ -287,22 +300,22 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         if (need == 0) continue;
         const bool desc = (sel == 0);
         int tau, gt;
-        radix_select16<NT>(vkey, vflag, D, tid * E, E, need, desc, hist, sout, &tau, &gt);
+        radix_select16<NT>(vkey, vflag, D, tid * E, E, o16, o8, need, desc, hist, sout, &tau, &gt);
         // ties at tau: lowest channel index first
         int ties = 0;
         for (int ch = cb0; ch < cb1; ++ch) {
-            if (vflag[ch]) continue;
-            int kk = desc ? vkey[ch] : (0xffff - vkey[ch]);
+            if (vflag[ch + o8]) continue;
+            int kk = desc ? vkey[ch + o16] : (0xffff - vkey[ch + o16]);
             ties += (kk == tau);
         }
         int tt;
         int trank = block_excl_scan<NT>(ties, &tt, sbuf);
         const int take = need - gt;
         for (int ch = cb0; ch < cb1; ++ch) {
-            if (vflag[ch]) continue;
-            int kk = desc ? vkey[ch] : (0xffff - vkey[ch]);
-            if (kk > tau) vflag[ch] = 1 + sel;
-            else if (kk == tau) { if (trank < take) vflag[ch] = 1 + sel; ++trank; }
+            if (vflag[ch + o8]) continue;
+            int kk = desc ? vkey[ch + o16] : (0xffff - vkey[ch + o16]);
+            if (kk > tau) vflag[ch + o8] = 1 + sel;
+            else if (kk == tau) { if (trank < take) vflag[ch + o8] = 1 + sel; ++trank; }
         }
         __syncthreads();
     }
@@ -310,8 +323,8 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     // kept range: value min/max, then the lowest-index element attaining it
     float vmin = INFINITY, vmax = -INFINITY;
     for (int ch = cb0; ch < cb1; ++ch) {
-        if (vflag[ch]) continue;
-        float x = h2f(xv[ch]);
+        if (vflag[ch + o8]) continue;
+        float x = h2f(xv[ch + o16]);
         vmin = fminf(vmin, x);
         vmax = fmaxf(vmax, x);
     }
@@ -331,8 +344,8 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     vmin = fred[0]; vmax = fred[32];
     int imin = 0x7fffffff, imax = 0x7fffffff;
     for (int ch = cb0; ch < cb1; ++ch) {
-        if (vflag[ch]) continue;
-        float x = h2f(xv[ch]);
+        if (vflag[ch + o8]) continue;
+        float x = h2f(xv[ch + o16]);
         if (x == vmin && imin == 0x7fffffff) imin = ch;
         if (x == vmax && imax == 0x7fffffff) imax = ch;
     }
@@ -348,7 +361,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
     if (tid == 0) {
         int a = sbuf[0], b = sout[0];
         for (int w = 1; w < QZ_WARPS; ++w) { a = min(a, sbuf[w]); b = min(b, sout[w]); }
-        double lo = (double)h2f(xv[a]), hi = (double)h2f(xv[b]);
+        double lo = (double)h2f(xv[I16(a)]), hi = (double)h2f(xv[I16(b)]);
         float s = __double2float_rn(__dsub_rn(hi, lo) / 2.0);
         float z = __double2float_rn(__dadd_rn(hi, lo) / 2.0);
         s_lo = lo; s_hi = hi; s_s = (double)s; s_z = (double)z;
@@ -359,10 +372,10 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         const double lo = s_lo, hi = s_hi, s = s_s, z = s_z;
         int vcnt = 0;
         for (int ch = cb0; ch < cb1; ++ch) {
-            double x = (double)h2f(xv[ch]);
+            double x = (double)h2f(xv[ch + o16]);
             double y = x < lo ? lo : (x > hi ? hi : x);
-            vc[ch] = (uint8_t)enc_fp64<NM>(y, s, z, s_mv);
-            vcnt += vflag[ch] != 0;
+            vc[ch + o8] = (uint8_t)enc_fp64<NM>(y, s, z, s_mv);
+            vcnt += vflag[ch + o8] != 0;
         }
         int vtot;
         int vr = block_excl_scan<NT>(vcnt, &vtot, sbuf);
@@ -380,10 +393,10 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         int vpos = vcnt ? gbv[myg] + (vr - gvf[myg]) : 0;
         uint32_t *vdst = c.vit + ((int64_t)(n >> 5) * c.NG + myg) * c.vcap_g;
         for (int ch = cb0; ch < cb1; ++ch)
-            if (vflag[ch]) {
-                vo[vr++] = (uint32_t)ch | ((uint32_t)xv[ch] << 16);
+            if (vflag[ch + o8]) {
+                vo[vr++] = (uint32_t)ch | ((uint32_t)xv[ch + o16] << 16);
                 if (vpos < c.vcap_g)
-                    vdst[vpos] = ((uint32_t)xv[ch] << 16) | ((uint32_t)(n & 31) << 11) | item_code_flag<BITS>(vc[ch]) |
+                    vdst[vpos] = ((uint32_t)xv[ch + o16] << 16) | ((uint32_t)(n & 31) << 11) | item_code_flag<BITS>(vc[ch + o8]) |
                                  (uint32_t)(ch - myg * c.GW);
                 ++vpos;
             }
@@ -401,7 +414,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         const int p0 = bit0 / PB, off = bit0 - p0 * PB;
         unsigned long long acc = 0;
         for (int p = p0, sh = 0; sh < 32 + off && p < kPairs; ++p, sh += PB) {
-            unsigned pc = (unsigned)kc[h * kHeadDim + p] | ((unsigned)kc[h * kHeadDim + p + kPairs] << BITS);
+            unsigned pc = (unsigned)kc[I8(h * kHeadDim + p)] | ((unsigned)kc[I8(h * kHeadDim + p + kPairs)] << BITS);
             acc |= (unsigned long long)pc << sh;
         }
         c.kcodes[((int64_t)tile * c.QW + q) * 32 + jj] = (uint32_t)(acc >> off);
@@ -414,7 +427,7 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         const int hh = x >> 6, mt = (x >> 3) & 7, g = x & 7;
         const int cc = mt * 16 + g;
         const int bit = vf_bit(jj, cc, BITS);
-        const uint32_t v = (uint32_t)vc[hh * kHeadDim + cc] | ((uint32_t)vc[hh * kHeadDim + cc + 8] << (2 * BITS));
+        const uint32_t v = (uint32_t)vc[I8(hh * kHeadDim + cc)] | ((uint32_t)vc[I8(hh * kHeadDim + cc + 8)] << (2 * BITS));
         const int lane = vf_lane(jj, cc), w = bit >> 5, off = bit & 31;
         uint32_t *dst = c.vcodes + vf_word(tile, c.H_kv, hh, w, lane, BITS);
         atomicOr(dst, v << off);
@@ -491,8 +504,11 @@ __global__ void __launch_bounds__(256) sort_buckets_kernel(DevCache c, int64_t t
     for (int i = threadIdx.x; i < (int)cnt; i += blockDim.x) lst[i] = sitem[i];
 }
 
-size_t qz_smem(int D) {
-    size_t b = (size_t)D * 2 * 3 + (size_t)D * 3;
+size_t qz_smem(int D, int NT) {
+    const int E = (D + NT - 1) / NT;
+    const size_t L16 = (size_t)D + (size_t)NT * ((E % 4 == 0) ? 2 : 0);
+    const size_t L8 = (size_t)D + (size_t)NT * ((E % 8 == 0) ? 4 : 0);
+    size_t b = L16 * 2 * 3 + L8 * 2 + ((L8 + 15) & ~size_t(15));
     b = (b + 15) & ~size_t(15);
     b += (256 + 64 + 64 + 64) * 4;
     return b;
@@ -501,13 +517,13 @@ size_t qz_smem(int D) {
 template <int BITS>
 cudaError_t launch_qz_bits(const DevCache &c, const __half *K, const __half *V, int64_t n0,
                            int64_t T, cudaStream_t s) {
-    size_t smem = qz_smem(c.D);
-    if (smem > 48 * 1024) {
+    const size_t smem = qz_smem(c.D, QZ_THREADS), smem1 = qz_smem(c.D, QZ_THREADS_1);
+    if (smem > 48 * 1024)
         cudaFuncSetAttribute(qz_kernel<BITS, QZ_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(qz_kernel<BITS, QZ_THREADS_1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
+    if (smem1 > 48 * 1024)
+        cudaFuncSetAttribute(qz_kernel<BITS, QZ_THREADS_1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
     if (T == 1) {
-        qz_kernel<BITS, QZ_THREADS_1><<<2, QZ_THREADS_1, smem, s>>>(c, K, V, n0, 0, -1);
+        qz_kernel<BITS, QZ_THREADS_1><<<2, QZ_THREADS_1, smem1, s>>>(c, K, V, n0, 0, -1);
         return cudaGetLastError();
     }
     qz_kernel<BITS, QZ_THREADS><<<(unsigned)T, QZ_THREADS, smem, s>>>(c, K, V, n0, 1, 0);
