@@ -398,7 +398,8 @@ static kvq_status attend_impl(kvq_cache *c, const void *q, int64_t pos, float *o
     a.timers = c->timers;
     a.kernel_out = &c->last_kernel;
     a.hg_out = &c->hg;
-    a.pdl = c->pdl_ok && c->pdl_stream == stream && cq == 0 && !getenv("KVQ_NO_PDL");
+    static const bool no_pdl = getenv("KVQ_NO_PDL") != nullptr;   // diagnostics switch
+    a.pdl = c->pdl_ok && c->pdl_stream == stream && cq == 0 && !no_pdl;
     c->pdl_ok = 0;
     cudaError_t e = launch_attend(c->dc, a, &c->last_splits, s);
     if (e != cudaSuccess) return cuda_fail(e, "attend launch");
