@@ -804,19 +804,43 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     for (int x = tid; x < HG * (kHeadDim + 2); x += NTHR) {
         const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
         const int gq = g0 + g;
+        // the S partials in chunks of 8 independent L2 loads (one round trip per chunk, not per
+        // split: the merge runs after every other CTA of the head group has finished)
+        constexpr int MC = 8;
+        const float *pbase = P.parts + (int64_t)gq * (kHeadDim + 2);
+        const int64_t pstride = (int64_t)c.H_q * (kHeadDim + 2);
         float m = -CUDART_INF_F;
-        for (int s = 0; s < P.S; ++s) {
-            const float *ps2 = P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2);
-            if (__ldcg(ps2 + kHeadDim + 1) != 0.f) m = fmaxf(m, __ldcg(ps2 + kHeadDim));
+        for (int s0 = 0; s0 < P.S; s0 += MC) {
+            float mv[MC], lv[MC];
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                const bool in = s0 + k < P.S;
+                const float *ps2 = pbase + (s0 + k) * pstride;
+                mv[k] = in ? __ldcg(ps2 + kHeadDim) : -CUDART_INF_F;
+                lv[k] = in ? __ldcg(ps2 + kHeadDim + 1) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < MC; ++k)
+                if (lv[k] != 0.f) m = fmaxf(m, mv[k]);
         }
         float l = 0.f, o = 0.f;
-        for (int s = 0; s < P.S; ++s) {
-            const float *ps2 = P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2);
-            const float ls = __ldcg(ps2 + kHeadDim + 1);
-            if (ls == 0.f) continue;
-            const float wgt = exp2f(__ldcg(ps2 + kHeadDim) - m);
-            l += wgt * ls;
-            if (ch < kHeadDim) o += wgt * __ldcg(ps2 + ch);
+        for (int s0 = 0; s0 < P.S; s0 += MC) {
+            float mv[MC], lv[MC], ov[MC];
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                const bool in = s0 + k < P.S;
+                const float *ps2 = pbase + (s0 + k) * pstride;
+                mv[k] = in ? __ldcg(ps2 + kHeadDim) : 0.f;
+                lv[k] = in ? __ldcg(ps2 + kHeadDim + 1) : 0.f;
+                ov[k] = (in && ch < kHeadDim) ? __ldcg(ps2 + ch) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {   // fixed split order, as before
+                if (lv[k] == 0.f) continue;
+                const float wgt = exp2f(mv[k] - m);
+                l += wgt * lv[k];
+                if (ch < kHeadDim) o += wgt * ov[k];
+            }
         }
         if (P.write_partial) {
             P.out[gq * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
@@ -1460,19 +1484,43 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
     for (int x = tid; x < G * (kHeadDim + 2); x += NTHR) {
         const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
         const int gq = g0 + g;
+        // the S partials in chunks of 8 independent L2 loads (one round trip per chunk, not per
+        // split: the merge runs after every other CTA of the head group has finished)
+        constexpr int MC = 8;
+        const float *pbase = P.parts + (int64_t)gq * (kHeadDim + 2);
+        const int64_t pstride = (int64_t)c.H_q * (kHeadDim + 2);
         float m = -CUDART_INF_F;
-        for (int s = 0; s < P.S; ++s) {
-            const float *ps2 = P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2);
-            if (__ldcg(ps2 + kHeadDim + 1) != 0.f) m = fmaxf(m, __ldcg(ps2 + kHeadDim));
+        for (int s0 = 0; s0 < P.S; s0 += MC) {
+            float mv[MC], lv[MC];
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                const bool in = s0 + k < P.S;
+                const float *ps2 = pbase + (s0 + k) * pstride;
+                mv[k] = in ? __ldcg(ps2 + kHeadDim) : -CUDART_INF_F;
+                lv[k] = in ? __ldcg(ps2 + kHeadDim + 1) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < MC; ++k)
+                if (lv[k] != 0.f) m = fmaxf(m, mv[k]);
         }
         float l = 0.f, o = 0.f;
-        for (int s = 0; s < P.S; ++s) {
-            const float *ps2 = P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2);
-            const float ls = __ldcg(ps2 + kHeadDim + 1);
-            if (ls == 0.f) continue;
-            const float wgt = exp2f(__ldcg(ps2 + kHeadDim) - m);
-            l += wgt * ls;
-            if (ch < kHeadDim) o += wgt * __ldcg(ps2 + ch);
+        for (int s0 = 0; s0 < P.S; s0 += MC) {
+            float mv[MC], lv[MC], ov[MC];
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                const bool in = s0 + k < P.S;
+                const float *ps2 = pbase + (s0 + k) * pstride;
+                mv[k] = in ? __ldcg(ps2 + kHeadDim) : 0.f;
+                lv[k] = in ? __ldcg(ps2 + kHeadDim + 1) : 0.f;
+                ov[k] = (in && ch < kHeadDim) ? __ldcg(ps2 + ch) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {   // fixed split order, as before
+                if (lv[k] == 0.f) continue;
+                const float wgt = exp2f(mv[k] - m);
+                l += wgt * lv[k];
+                if (ch < kHeadDim) o += wgt * ov[k];
+            }
         }
         if (P.write_partial) {
             P.out[gq * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
