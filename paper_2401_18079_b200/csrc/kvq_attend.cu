@@ -958,17 +958,37 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     for (int x = tid; x < HG * (kHeadDim + 2); x += ATT_THREADS) {
         const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
         const int gq = g0 + g;
+        // partials in chunks of 8 independent L2 loads (one round trip per chunk)
+        constexpr int MC = 8;
+        const float *pbase = P.parts + (int64_t)gq * (kHeadDim + 2);
+        const int64_t pstride = (int64_t)c.H_q * (kHeadDim + 2);
         float m = -CUDART_INF_F;
-        for (int s = 0; s < P.S; ++s)
-            m = fmaxf(m, __ldcg(P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2) + kHeadDim));
+        for (int s0 = 0; s0 < P.S; s0 += MC) {
+            float mv[MC];
+#pragma unroll
+            for (int k = 0; k < MC; ++k)
+                mv[k] = s0 + k < P.S ? __ldcg(pbase + (s0 + k) * pstride + kHeadDim) : -CUDART_INF_F;
+#pragma unroll
+            for (int k = 0; k < MC; ++k) m = fmaxf(m, mv[k]);
+        }
         float l = 0.f, o = 0.f;
-        for (int s = 0; s < P.S; ++s) {
-            const float *ps = P.parts + ((int64_t)s * c.H_q + gq) * (kHeadDim + 2);
-            const float ls = __ldcg(ps + kHeadDim + 1);
-            if (ls == 0.f) continue;
-            const float wgt = exp2f(__ldcg(ps + kHeadDim) - m);
-            l += wgt * ls;
-            if (ch < kHeadDim) o += wgt * __ldcg(ps + ch);
+        for (int s0 = 0; s0 < P.S; s0 += MC) {
+            float mv[MC], lv[MC], ov[MC];
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                const bool in = s0 + k < P.S;
+                const float *ps = pbase + (s0 + k) * pstride;
+                mv[k] = in ? __ldcg(ps + kHeadDim) : 0.f;
+                lv[k] = in ? __ldcg(ps + kHeadDim + 1) : 0.f;
+                ov[k] = (in && ch < kHeadDim) ? __ldcg(ps + ch) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                if (lv[k] == 0.f) continue;
+                const float wgt = exp2f(mv[k] - m);
+                l += wgt * lv[k];
+                if (ch < kHeadDim) o += wgt * ov[k];
+            }
         }
         if (P.write_partial) {
             const float v = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
