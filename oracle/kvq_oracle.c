@@ -17,7 +17,11 @@
  *   enc             pinned  (SPEC worked values, exact-rational brute-force argmin)
  *   outlier select  pinned  (SPEC worked example, brute force over tie patterns)
  *   key/value quant pinned  (round trip on grid, error bound, exact outliers)
- *   attend          pinned  (lossless mode == textbook fp64 attention; selection; mean)
+ *   attend          pinned  (lossless mode == textbook fp64 attention and torch SDPA;
+ *                            hand-computed d=2 score with a non-identity Key affine,
+ *                            S:506; dominant-score selection returns the hand-
+ *                            dequantized V^_t; uniform scores -> mean of
+ *                            hand-dequantized V^ incl. a lower-index tie)
  *   merge           pinned  (any partition == unsplit)
  *   attention values on realistic synthetic data: "parity unpinned" beyond the special
  *   cases above (the oracle is the reference) -- see DESIGN.md.

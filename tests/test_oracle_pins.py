@@ -320,9 +320,84 @@ def test_attention_selection_and_uniform():
         for r, c in enumerate(cache.vidx[n]):
             deqV[n, c] = np.float64(cache.vval[n, r].view(np.float16))
     np.testing.assert_allclose(o0[0], deqV.mean(axis=0), rtol=1e-12, atol=1e-12)
-    # selection: a query aligned with token 2's rotated key at huge scale -> V^_2
+    # q = 0: every score is exactly 0, so m = 0 and l = T (the selection pin with a
+    # dominant score is test_selection_one_dominant_token_returns_its_dequantized_value)
     p = O.attend_partial(cache, np.zeros((1, d), np.float16), 3, **kw)
     assert p[0, d + 1] == T and p[0, d] == 0.0
+
+
+# ------------------------------------------------ hand-computed attention pins ------
+def _cb4():
+    return np.array([-1.0, -0.5, 0.5, 1.0], np.float32)
+
+
+def test_score_d2_one_token_quantized_key_by_hand():
+    """S:506 (qk_scores example): d=2, one token, key quantized with a NON-identity
+    per-channel affine, score computed by hand.
+
+    key_lo = [0, -2], key_hi = [2, 4]  ->  s_c = (hi-lo)/2 = [1, 3], z_c = (hi+lo)/2 = [1, 1]
+    (reading R6).  x = [1.25, 0.25]: normalised (x-z)/s = [0.25, -0.25] -> nearest
+    centroids of [-1,-.5,.5,1] are 0.5 and -0.5 (codes 2, 1), so
+    K^ = [0.5*1 + 1, -0.5*3 + 1] = [1.5, -0.5]   (P:1368-1369: Chat[code]*s + z).
+    q = [2, 1].  With pos == pos_base + n both sides get the same rotation, so
+    q~.k~ = q.K^ = 2*1.5 - 0.5 = 2.5 and s = 2.5/sqrt(2).  With pos - n = 1 (theta_0 = 1
+    for d=2) q~ = R(1) q and q~.K^ = 2.5 (cos 1 - sin 1).  A slip in the Key
+    dequantization (cb*s - z, (cb+z)*s, s and z swapped) changes both numbers.
+    """
+    lo, hi = np.array([0.0, -2.0], np.float32), np.array([2.0, 4.0], np.float32)
+    K = np.array([[1.25, 0.25]], np.float16)
+    V = np.array([[1.0, 3.0]], np.float16)
+    cache = O.prefill(K, V, lo, hi, _cb4(), _cb4(), ppm=0)
+    assert list(cache.kcodes[0]) == [2, 1] and cache.kidx.size == 0
+    kw = dict(H_q=1, H_kv=1, d=2, key_lo=lo, key_hi=hi, cbK_dec=_cb4(), cbV_dec=_cb4())
+    q = np.array([[2.0, 1.0]], np.float16)
+    p = O.attend_partial(cache, q, 7, pos_base=7, **kw)
+    assert abs(p[0, 2] - 2.5 / np.sqrt(2.0)) < 1e-12 and p[0, 3] == 1.0
+    cos1, sin1 = 0.5403023058681398, 0.8414709848078965   # tests/golden/rope.json d=2 n=1
+    p = O.attend_partial(cache, q, 1, pos_base=0, **kw)
+    assert abs(p[0, 2] - 2.5 * (cos1 - sin1) / np.sqrt(2.0)) < 1e-12
+
+
+def test_selection_one_dominant_token_returns_its_dequantized_value():
+    """S:515 (av_matvec example "w one-hot at token t -> out == dequantized V_t") through
+    attend: a query aligned with token 1's key at fp16 scale 6e4 makes its score exceed
+    the others by > 1e6, so o == V^_1 exactly.
+
+    V_1 = [0.5, 3.0, 1.0, 2.5]: lo = 0.5, hi = 3 -> s_n = 1.25, z_n = 1.75; normalised
+    [-1, 1, -0.6, 0.6] -> codes [0, 3, 1, 2] -> V^_1 = [0.5, 3.0, 1.125, 2.375]
+    (Chat*s_n + z_n; per-token affine).
+    Keys: lo = -8, hi = 8 (s = 8, z = 0); token 1 = +8 everywhere, tokens 0, 2 = -8.
+    pos = pos_base + 1, so token 1 sees no relative rotation: score_1 = 4*6e4*8/2 = 9.6e5,
+    while score_0, score_2 = -q.R(+-1)K^_1/2 < 0.
+    """
+    lo, hi = np.full(4, -8.0, np.float32), np.full(4, 8.0, np.float32)
+    K = np.array([[-8.0] * 4, [8.0] * 4, [-8.0] * 4], np.float16)
+    V = np.array([[-3.0, 7.0, 0.5, 2.0], [0.5, 3.0, 1.0, 2.5], [4.0, -1.0, 6.0, 0.0]], np.float16)
+    cache = O.prefill(K, V, lo, hi, _cb4(), _cb4(), ppm=0)
+    assert list(cache.vcodes[1]) == [0, 3, 1, 2]
+    assert cache.vs[1] == 1.25 and cache.vz[1] == 1.75
+    kw = dict(H_q=1, H_kv=1, d=4, key_lo=lo, key_hi=hi, cbK_dec=_cb4(), cbV_dec=_cb4())
+    q = np.full((1, 4), 60000.0, np.float16)
+    p = O.attend_partial(cache, q, 11, pos_base=10, **kw)
+    assert abs(p[0, 4] - 960000.0) < 1e-6 and p[0, 5] == 1.0
+    o = O.attend(cache, q, 11, pos_base=10, **kw)
+    assert list(o[0]) == [0.5, 3.0, 1.125, 2.375]
+
+
+def test_uniform_scores_mean_of_hand_dequantized_values():
+    """q = 0 gives uniform weights (every score 0), so o = mean of V^ (S:516 convexity).
+    V_0 = [0.5, 3, 1, 2.5] -> V^_0 = [0.5, 3, 1.125, 2.375] (see the selection pin).
+    V_1 = [-2, 2, 0, 1]: s = 2, z = 0, normalised [-1, 1, 0, 0.5]; 0 is equidistant from
+    -0.5 and 0.5 and the tie goes to the lower index (R8) -> codes [0, 3, 1, 2] ->
+    V^_1 = [-2, 2, -1, 1].  Mean = [-0.75, 2.5, 0.0625, 1.6875]."""
+    lo, hi = np.full(4, -8.0, np.float32), np.full(4, 8.0, np.float32)
+    K = np.array([[1.0, -2.0, 3.0, 0.5], [-1.0, 2.0, 5.0, 4.0]], np.float16)
+    V = np.array([[0.5, 3.0, 1.0, 2.5], [-2.0, 2.0, 0.0, 1.0]], np.float16)
+    cache = O.prefill(K, V, lo, hi, _cb4(), _cb4(), ppm=0)
+    assert list(cache.vcodes[1]) == [0, 3, 1, 2]
+    kw = dict(H_q=1, H_kv=1, d=4, key_lo=lo, key_hi=hi, cbK_dec=_cb4(), cbV_dec=_cb4())
+    o = O.attend(cache, np.zeros((1, 4), np.float16), 5, **kw)
+    assert list(o[0]) == [-0.75, 2.5, 0.0625, 1.6875]
 
 
 def test_merge_any_partition_equals_unsplit():
