@@ -12,9 +12,17 @@ needed; stated in config.l2).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3_nuq3|c3_nuq4|c2|...]
   python bench.py --impl reference ...   # the CPU oracle as the reference arm
 
-N > 1 (torchrun, one process per GPU): the same context is sequence-sharded across the
-ranks (pos_base offsets), each rank attends over its shard, partials are all-gathered
-over NCCL and merged by the CUDA merge kernel ("scaling": "strong").
+N > 1 (torchrun, one process per GPU): by default BASELINE config 5, LLaMA-7B at 10M tokens
+(2-bit NUQ, Q-Norm, 1% outliers), sequence-sharded across the ranks (pos_base offsets): each
+rank attends over its shard, the [H_q][d+2] partials are all-gathered over NCCL and merged by
+the CUDA merge kernel ("scaling": "strong").  Layers that do not fit a GPU's memory are not
+simulated: as many layers as fit are resident and the step time is scaled x(layers /
+resident) (config.layer_rule).  --workload c5 --gpus 1 gives the 1-GPU point of the same
+context for E(P) = t(1) / (P t(P)).
+
+At 1 GPU the line also carries, at the same 128K context: the fp16-cache comparator and the
+other bit width ("compare", BASELINE C3 "4-bit vs 3-bit vs fp16 cache"), and the attend time
+with fp32 (not fp16-exact) codebooks ("resid_codebook").
 
 Prints ONE JSON line on rank 0.
 """
@@ -42,19 +50,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3_nuq3")
+    ap.add_argument("--workload", default="",
+                    help="default: c3_nuq3 at 1 GPU, c5 (10M tokens, sequence-sharded) at N > 1")
     ap.add_argument("--tokens", type=int, default=0, help="override context length")
     ap.add_argument("--layers", type=int, default=0, help="override layer count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=8192)
     ap.add_argument("--splits", type=int, default=0)
+    ap.add_argument("--no-compare", action="store_true",
+                    help="skip the fp16 / other-bit-width cache arms and the fp32-codebook arm")
     return ap.parse_args()
 
 
 def workload(args):
     from kvq_synth import CONFIGS, Workload
-    w = CONFIGS[args.workload]
+    name = args.workload or ("c3_nuq3" if args.gpus == 1 else "c5")
+    w = CONFIGS[name]
     if args.tokens or args.layers:
         w = Workload(w.name + "-override", args.layers or w.n_layers, w.H_q, w.H_kv, w.d,
                      args.tokens or w.T, w.bits, w.ppm, w.qnorm)
@@ -123,9 +135,9 @@ def measured_peaks():
 
 
 # -------------------------------------------------------------- CPU oracle timing --
-def oracle_sample(w, T_s, seed=0):
+def oracle_sample(w, T_s, seed=0, threads=None):
     """Time the oracle (as it stands) on a bounded sample: one layer, T_s cached tokens:
-    one append (quantize 1 token) + one decode attend.  Returns (seconds, threads)."""
+    one append (quantize 1 token) + one decode attend.  Returns (step, threads)."""
     import oracle as O
     from kvq_synth import calib, gen
     D = w.D
@@ -136,7 +148,7 @@ def oracle_sample(w, T_s, seed=0):
     V = gen.gen_values(seed, 0, T_s, D)
     cache = O.prefill(K, V, cal["key_lo"], cal["key_hi"], cal["cbK"], cal["cbV"], w.ppm)
     q = gen.gen_queries(seed, 0, w.H_q, w.H_kv, w.d)[0]
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     kn = gen.gen_keys(seed, 0, 1, D, stream=gen.STREAM_APP_K)[0]
     vn = gen.gen_values(seed, 0, 1, D, stream=gen.STREAM_APP_V)[0]
 
@@ -149,25 +161,57 @@ def oracle_sample(w, T_s, seed=0):
     return step, threads
 
 
-def cpu_baseline(w, T_s, min_seconds=10.0):
-    """The oracle as it stands, on a bounded sample: repeat (1 append + 1 attend over T_s
-    cached tokens of one layer) until >= min_seconds of CPU work, then scale per token
-    and per layer to the workload (linear in both)."""
-    step, threads = oracle_sample(w, T_s)
+def time_step(step, min_seconds, max_reps=1000):
     reps, t0 = 0, time.perf_counter()
     while True:
         step()
         reps += 1
         dt = time.perf_counter() - t0
-        if dt >= min_seconds or reps >= 1000:
-            break
-    per = dt / reps
+        if dt >= min_seconds or reps >= max_reps:
+            return dt / reps, reps, dt
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_baseline(w, T_s, min_seconds=10.0):
+    """The oracle as it stands, on the box's host cores.  Headline value: a bounded sample
+    (1 append + 1 attend over T_s cached tokens of one layer, repeated for >= min_seconds,
+    all cores) scaled per token and per layer to the workload (linear in both).  Also: the
+    same on one core (a T_s/8-token sample, scaled), and BASELINE configs C1 and C2 in full
+    (one layer each, no scaling)."""
+    from kvq_synth import CONFIGS
+    step, threads = oracle_sample(w, T_s)
+    per, reps, dt = time_step(step, min_seconds)
     scale = (w.T / T_s) * w.n_layers
+    s1, _ = oracle_sample(w, max(256, T_s // 8), threads=1)
+    per1, reps1, _ = time_step(s1, 3.0)
+    one_core = per1 * (w.T / max(256, T_s // 8)) * w.n_layers * 1e6
+    full = {}
+    for name in ("c1", "c2"):
+        cw = CONFIGS[name]
+        st, _ = oracle_sample(cw, cw.T)
+        p, r, _ = time_step(st, 2.0, max_reps=50)
+        full[name] = {"value": p * 1e6, "unit": "us/token", "context": cw.T, "layers": cw.n_layers,
+                      "reps": r, "note": "1 append + 1 attend over the full context, all cores"}
     return {"value": per * scale * 1e6, "unit": "us/token", "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"{reps} x (1 append + 1 attend) on 1 layer with {T_s} cached tokens "
-                      f"(of {w.T}), fp64 C oracle, OpenMP over heads; per-step time scaled "
-                      f"x{w.T}/{T_s} tokens x{w.n_layers} layers (linear in both)",
-            "sample_seconds": dt}
+                      f"(of {w.T}), fp64 C oracle, OpenMP over heads, {threads} threads; per-step "
+                      f"time scaled x{w.T}/{T_s} tokens x{w.n_layers} layers (linear in both)",
+            "sample_seconds": dt,
+            "one_core": {"value": one_core, "unit": "us/token", "cores": 1, "reps": reps1,
+                         "sample": f"{max(256, T_s // 8)} cached tokens, 1 thread, scaled the same way"},
+            "full_configs": full}
 
 
 def run_reference(args):
@@ -200,6 +244,109 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------ our arm --
+def graph_replay_times(launch_all, n_launch, stream, reps):
+    """Capture `launch_all()` (n_launch attend launches over distinct caches) in one CUDA
+    graph and replay it `reps` times, each replay bracketed by CUDA events on the capture
+    stream.  Returns per-launch times in ms (one per replay) and whether a graph was used
+    (eager event timing if capture is not possible)."""
+    import torch
+    per = []
+    graph = None
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            launch_all()
+        graph = g
+    except Exception:
+        graph = None
+    torch.cuda.synchronize()
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            launch_all()
+        b.record(stream)
+        b.synchronize()
+        per.append(a.elapsed_time(b) / n_launch)
+    return per, graph is not None
+
+
+def stats(v):
+    v = np.asarray(v, np.float64)
+    return {"median": float(np.median(v)), "p10": float(np.percentile(v, 10)),
+            "p90": float(np.percentile(v, 90)), "n": int(v.size)}
+
+
+def build_caches(kvq, gen, w, cal, n, T_local, pos_base, capacity, dev, seed0, rank, fp16=False):
+    """n layer caches of T_local prompt tokens each (synthetic, generated on the GPU in 64K-token
+    chunks and prefilled through kvq_prefill_quantize / kvq_f16_append)."""
+    import torch
+    caches = []
+    for l in range(n):
+        if fp16:
+            c = kvq.F16Cache(n_q_heads=w.H_q, n_kv_heads=w.H_kv, capacity_tokens=capacity,
+                             pos_base=pos_base, device=dev.index or 0)
+        else:
+            c = kvq.KVQCache(n_q_heads=w.H_q, n_kv_heads=w.H_kv, head_dim=w.d, bits=w.bits,
+                             outlier_ppm=w.ppm, capacity_tokens=capacity,
+                             key_cb=cal["cbK"], val_cb=cal["cbV"], key_cb_dec=cal["cbK_dec"],
+                             val_cb_dec=cal["cbV_dec"], key_lo=cal["key_lo"], key_hi=cal["key_hi"],
+                             pos_base=pos_base, device=dev.index or 0,
+                             decode_pdl=True)   # q of a step is generated before its appends
+        for a in range(0, T_local, 1 << 16):
+            b = min(T_local, a + (1 << 16))
+            Kl = gen.gen_layer_torch(seed0 + 1000 * l + 31 * rank + a, l, b - a, w.D, dev, "K")
+            Vl = gen.gen_layer_torch(seed0 + 1000 * l + 31 * rank + a + 7, l, b - a, w.D, dev, "V")
+            if fp16:
+                c.append(Kl, Vl)
+            else:
+                c.prefill(Kl, Vl)
+            del Kl, Vl
+        caches.append(c)
+    torch.cuda.synchronize()
+    return caches
+
+
+def compare_arm(kvq, gen, calib, accounting, wname, T, n_layers, dev, reps, peak):
+    """Attend-only time per layer of another cache format at the same context (BASELINE
+    config C3 "4-bit vs 3-bit vs fp16 cache"), n_layers distinct caches cycled (> L2)."""
+    import torch
+    from kvq_synth import CONFIGS
+    w = CONFIGS[wname] if wname != "f16" else CONFIGS["c3_nuq3"]
+    fp16 = wname == "f16"
+    cal = None if fp16 else calib.calibrate_layer(
+        gen.gen_keys(0, 0, 2048, w.D, stream=gen.STREAM_CAL_K),
+        gen.gen_values(0, 0, 2048, w.D, stream=gen.STREAM_CAL_V), w.bits, w.ppm, qnorm=w.qnorm)
+    caches = build_caches(kvq, gen, w, cal, n_layers, T, 0, T + 8, dev, 5000, 0, fp16=fp16)
+    q = (torch.randn((n_layers, w.H_q, w.d), device=dev) * 0.5).half()
+    o = torch.zeros((n_layers, w.H_q, w.d), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def launch_all():
+        for l in range(n_layers):
+            caches[l].attend(q[l], T, o[l], stream)
+    launch_all()
+    per, graphed = graph_replay_times(launch_all, n_layers, stream, reps)
+    st = stats(per)
+    if fp16:
+        nbytes = T * w.D * 2 * 2 + w.H_q * w.d * 6
+    else:
+        kv = caches[0].info()["value_outliers"]
+        b0, e0 = caches[0].key_outlier_span(0, caches[0].num_tokens)
+        nbytes = accounting.attend_bytes(T, w.D, w.bits, kv, e0 - b0, w.H_q, w.d)
+    kern = "f16_attend_kernel" if fp16 else {1: "att_wa_kernel", 2: "att_wag_kernel"}.get(
+        caches[0].info()["attend_kernel"], "att_kernel")
+    out = {"cache": wname, "context": T, "layers_cycled": n_layers, "kernel": kern,
+           "attend_us_per_layer": st["median"] * 1e3, "attend_us_p10_p90": [st["p10"] * 1e3, st["p90"] * 1e3],
+           "bytes_per_launch": int(nbytes), "gbs": nbytes / (st["median"] * 1e-3) / 1e9,
+           "frac": nbytes / (st["median"] * 1e-3) / 1e9 / peak, "graph": graphed}
+    del caches
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -213,67 +360,81 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # communicator / NVLS logging on
         dist.init_process_group("nccl", device_id=dev)
     w = workload(args)
     plan = ShardPlan(w.T, world, rank)
-    e2e_steps = 0 if (args.no_e2e or world > 1) else max(3, args.steps // 2)
+    e2e_steps = 0 if args.no_e2e else max(3, args.steps // 2)
     steps_total = args.warmup + args.steps + e2e_steps + 2
-    L, D, H, d = w.n_layers, w.D, w.H_q, w.d
+    D, H, d = w.D, w.H_q, w.d
+    props = torch.cuda.get_device_properties(dev)
+    l2 = int(getattr(props, "L2_cache_size", 126 * 2 ** 20))
 
     # offline calibration (input preparation; one set of constants for every layer handle)
     cal = calib.calibrate_layer(gen.gen_keys(0, 0, 2048, D, stream=gen.STREAM_CAL_K),
                                 gen.gen_values(0, 0, 2048, D, stream=gen.STREAM_CAL_V),
                                 w.bits, w.ppm, qnorm=w.qnorm)
-    caches = []
-    prefill_ms = 0.0
     t_setup = time.time()
-    for l in range(L):
-        c = kvq.KVQCache(n_q_heads=H, n_kv_heads=w.H_kv, head_dim=d, bits=w.bits,
-                         outlier_ppm=w.ppm, capacity_tokens=plan.capacity(steps_total),
-                         key_cb=cal["cbK"], val_cb=cal["cbV"], key_cb_dec=cal["cbK_dec"],
-                         val_cb_dec=cal["cbV_dec"], key_lo=cal["key_lo"], key_hi=cal["key_hi"],
-                         pos_base=plan.pos_base, device=local)
-        if args.splits:
-            c.set_splits(args.splits)
-        n = plan.end - plan.start
-        chunk = 1 << 16
-        for a in range(0, n, chunk):
-            b = min(n, a + chunk)
-            Kl = gen.gen_layer_torch(1000 * l + 31 * rank + a, l, b - a, D, dev, "K")
-            Vl = gen.gen_layer_torch(1000 * l + 31 * rank + a + 7, l, b - a, D, dev, "V")
-            if l == 0:   # a9: time layer 0's prefill quantization (kvq_prefill_quantize)
-                pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                pe0.record()
-                c.prefill(Kl, Vl)
-                pe1.record()
-                pe1.synchronize()
-                prefill_ms += pe0.elapsed_time(pe1)
-            else:
-                c.prefill(Kl, Vl)
-            del Kl, Vl
-        caches.append(c)
+    n_local = plan.end - plan.start
+    cap = plan.capacity(steps_total)
+    # layer 0 first: its prefill is timed (a9) and its footprint sets the resident-layer count
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0 = kvq.KVQCache(n_q_heads=H, n_kv_heads=w.H_kv, head_dim=d, bits=w.bits, outlier_ppm=w.ppm,
+                      capacity_tokens=cap, key_cb=cal["cbK"], val_cb=cal["cbV"], key_cb_dec=cal["cbK_dec"],
+                      val_cb_dec=cal["cbV_dec"], key_lo=cal["key_lo"], key_hi=cal["key_hi"],
+                      pos_base=plan.pos_base, device=local, decode_pdl=True)
+    prefill_ms = 0.0
+    for a in range(0, n_local, 1 << 16):
+        b = min(n_local, a + (1 << 16))
+        Kl = gen.gen_layer_torch(31 * rank + a, 0, b - a, D, dev, "K")
+        Vl = gen.gen_layer_torch(31 * rank + a + 7, 0, b - a, D, dev, "V")
+        pe0.record()
+        c0.prefill(Kl, Vl)
+        pe1.record()
+        pe1.synchronize()
+        prefill_ms += pe0.elapsed_time(pe1)
+        del Kl, Vl
+    layer_bytes = c0.info()["device_bytes"]
+    free, _ = torch.cuda.mem_get_info(dev)
+    # resident-layer rule: as many of the model's layers as fit next to 8 GB of headroom; per-step
+    # numbers are then scaled x n_layers / L_res (all layers have the same shape and cost)
+    L_res = int(max(1, min(w.n_layers, 1 + (free - 8 * 2 ** 30) // max(layer_bytes, 1))))
+    kv0 = c0.info()["value_outliers"]
+    b0, e0 = c0.key_outlier_span(0, c0.num_tokens)
+    bytes_att0 = accounting.attend_bytes(c0.num_tokens, D, w.bits, kv0, e0 - b0, H, d)
+    # inputs larger than L2 every launch: cycle enough distinct cache sets that one step's
+    # attends stream >= 4 x L2 (C2's 113 MB layer would otherwise stay in the 126 MB L2)
+    ncopy = 1 if L_res * bytes_att0 >= 4 * l2 else int(np.ceil(4 * l2 / (L_res * bytes_att0)))
+    nc_tot = min(L_res * ncopy, max(L_res, int((free - 8 * 2 ** 30) // max(layer_bytes, 1)) + 1))
+    rest = build_caches(kvq, gen, w, cal, nc_tot - 1, n_local, plan.pos_base, cap, dev, 0, rank)
+    caches = [c0] + rest
     for c in caches:
         c.sync()
+        if args.splits:
+            c.set_splits(args.splits)
+    ncopy = len(caches) // L_res
     t_setup = time.time() - t_setup
 
     # per-step inputs: new token (K, V) per layer, pre-RoPE q per layer
-    knew = torch.stack([gen.gen_layer_torch(7 + l, l, steps_total, D, dev, "K") for l in range(L)])
-    vnew = torch.stack([gen.gen_layer_torch(9 + l, l, steps_total, D, dev, "V") for l in range(L)])
+    knew = torch.stack([gen.gen_layer_torch(7 + l, l, steps_total, D, dev, "K") for l in range(L_res)])
+    vnew = torch.stack([gen.gen_layer_torch(9 + l, l, steps_total, D, dev, "V") for l in range(L_res)])
     qsc = torch.tensor(np.repeat(gen.query_scale(0, 0, D, d), H // w.H_kv), dtype=torch.float32,
                        device=dev)
     g = torch.Generator(device=dev)
     g.manual_seed(1234)
-    qs = (torch.randn((steps_total, L, H, d), generator=g, device=dev)
+    qs = (torch.randn((steps_total, L_res, H, d), generator=g, device=dev)
           * qsc[None, None, :, None]).half()
-    o = torch.zeros((L, H, d), dtype=torch.float32, device=dev)
-    part = torch.zeros((L, H, d + 2), dtype=torch.float32, device=dev)
+    o = torch.zeros((L_res, H, d), dtype=torch.float32, device=dev)
+    part = torch.zeros((L_res, H, d + 2), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
     is_tail = rank == plan.tail_owner
     st = {"pos": w.T, "s": 0}
+    # the decode appends go to copy set 0 only (its capacity holds them); the other sets are
+    # attend-only copies cycled by the attend timing below
 
     def step(kb, vb, qb, ob):
         pos, s = st["pos"], st["s"]
-        for l in range(L):
+        for l in range(L_res):
             if is_tail:
                 caches[l].append(kb[l, s], vb[l, s], stream)
             if world == 1:
@@ -306,60 +467,103 @@ def run_ours(args):
         tt = torch.tensor([elapsed_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         elapsed_ms = float(tt.item())
-    ms_per_step = elapsed_ms / args.steps
+    scale_layers = w.n_layers / L_res
+    ms_per_step = elapsed_ms / args.steps * scale_layers
 
-    # attend-only pass: per-launch CUDA events on the launching stream
+    # attend-only: one CUDA graph of one attend per cache (every layer of every copy set),
+    # replayed; per-launch median / p10 / p90 over replays
     pos = st["pos"]
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(L * args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(L * args.steps)]
-    for s in range(args.steps):
-        for l in range(L):
-            i = s * L + l
-            starts[i].record(stream)
-            if world == 1:
-                caches[l].attend(qs[s, l], pos, o[l], stream)
-            else:
-                caches[l].attend_partial(qs[s, l], pos, part[l], stream)
-            ends[i].record(stream)
-    torch.cuda.synchronize()
-    att_ms_mean = float(np.mean([a.elapsed_time(b) for a, b in zip(starts, ends)]))
+    qatt = qs[0]
 
-    # e2e: same step through the public API with pinned HOST buffers; the library
-    # stages K, V, q host->device and o device->host inside each call.
+    def launch_all():
+        for i, c in enumerate(caches):
+            if world == 1:
+                c.attend(qatt[i % L_res], pos, o[i % L_res], stream)
+            else:
+                c.attend_partial(qatt[i % L_res], pos, part[i % L_res], stream)
+    launch_all()
+    reps = max(args.steps, int(np.ceil(0.5 / max(1e-4, L_res * ncopy * 3e-4))), 20)
+    per, graphed = graph_replay_times(launch_all, len(caches), stream, min(reps, 400))
+    att = stats(per)
+    att_ms = att["median"]
+
+    # e2e: same step through the public API with pinned HOST buffers; the library stages K, V,
+    # q host->device and o device->host inside each call (at N > 1 the merged o of each layer)
     e2e = None
     if e2e_steps:
         kh, vh, qh = knew.cpu().pin_memory(), vnew.cpu().pin_memory(), qs.cpu().pin_memory()
-        oh = torch.zeros((L, H, d), dtype=torch.float32).pin_memory()
+        oh = torch.zeros((L_res, H, d), dtype=torch.float32).pin_memory()
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        if world > 1:
+            dist.barrier()
+        e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0_.record(stream)
         for _ in range(e2e_steps):
             step(kh, vh, qh, oh)
-        e1.record(stream)
+        e1_.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / e2e_steps
-        e2e = {"value": e2e_ms * 1e3, "unit": "us/token",
-               "h2d_bytes_per_step": L * (2 * D * 2 + H * d * 2),
-               "d2h_bytes_per_step": L * H * d * 4, "steps": e2e_steps}
+        e2e_ms = e0_.elapsed_time(e1_) / e2e_steps
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        e2e = {"value": e2e_ms * 1e3 * scale_layers, "unit": "us/token",
+               "h2d_bytes_per_step": w.n_layers * ((2 * D * 2 if is_tail else 0) + H * d * 2),
+               "d2h_bytes_per_step": w.n_layers * H * d * 4, "steps": e2e_steps}
 
     kv = caches[0].info()["value_outliers"]
     Tc = caches[0].num_tokens
-    spans = [c.key_outlier_span(0, c.num_tokens) for c in caches]
+    spans = [c.key_outlier_span(0, c.num_tokens) for c in caches[:L_res]]
     nnz_mean = float(np.mean([e - b for b, e in spans]))
     bytes_att = accounting.attend_bytes(Tc, D, w.bits, kv, int(nnz_mean), H, d)
     peak, peak_kind = measured_peaks()
-    achieved = bytes_att / (att_ms_mean * 1e-3) / 1e9
+    achieved = bytes_att / (att_ms * 1e-3) / 1e9
     info = caches[0].info()
 
-    # a9 prefill: HBM bytes per token-layer = K, V in (fp16) + codes, (s, z), CSC pointer and
-    # outlier records (canonical + bucketed) out; the prefill launches of layer 0, CUDA events
-    n_pf = plan.end - plan.start
-    pf_bytes = n_pf * (4 * D + 2 * D * w.bits / 8 + 8 + 4 + 8 * (kv + nnz_mean / max(Tc, 1)))
-    prefill_line = {"ns_per_token_layer": prefill_ms * 1e6 / max(n_pf, 1), "tokens": n_pf,
+    # a9 prefill of layer 0 (kvq_prefill_quantize, CUDA events): HBM bytes per token-layer = K, V
+    # in (fp16) + codes, (s, z), CSC pointer and outlier records (canonical + bucketed) out
+    pf_bytes = n_local * (4 * D + 2 * D * w.bits / 8 + 8 + 4 + 8 * (kv + nnz_mean / max(Tc, 1)))
+    prefill_line = {"ns_per_token_layer": prefill_ms * 1e6 / max(n_local, 1), "tokens": n_local,
                     "gbs": pf_bytes / (prefill_ms * 1e-3) / 1e9 if prefill_ms > 0 else None,
                     "frac": (pf_bytes / (prefill_ms * 1e-3) / 1e9) / peak if prefill_ms > 0 else None,
-                    "kernels": "qz_kernel (count) + scan_counts_kernel + qz_kernel (write) + sort_buckets_kernel x2"}
+                    "kernels": "prefill_kernel (one CTA per 32-token tile, decoupled look-back)"}
+
+    # comparison arms at the same context on one GPU (C3: "4-bit vs 3-bit vs fp16 cache") and
+    # the fp32-codebook (RESID) specialization of the 3-bit kernel
+    compare = None
+    if world == 1 and not args.no_compare and w.name.startswith("c3"):
+        del knew, vnew
+        torch.cuda.empty_cache()
+        compare = {}
+        try:
+            for arm in ("f16", "c3_nuq4" if w.bits == 3 else "c3_nuq3"):
+                compare[arm] = compare_arm(kvq, gen, calib, accounting, arm, w.T, 8, dev, 20, peak)
+            compare["speedup_vs_f16"] = compare["f16"]["attend_us_per_layer"] / (att_ms * 1e3)
+        except Exception as ex:   # pragma: no cover
+            compare["error"] = str(ex)[:300]
+    resid = None
+    if world == 1 and not args.no_compare:
+        try:
+            cal32 = calib.calibrate_layer(gen.gen_keys(0, 0, 2048, D, stream=gen.STREAM_CAL_K),
+                                          gen.gen_values(0, 0, 2048, D, stream=gen.STREAM_CAL_V),
+                                          w.bits, w.ppm, qnorm=w.qnorm, fp16_codebooks=False)
+            nres = max(2, min(8, int(np.ceil(4 * l2 / bytes_att))))
+            del caches[L_res:]
+            torch.cuda.empty_cache()
+            rc = build_caches(kvq, gen, w, cal32, nres, min(n_local, 1 << 17), 0, 1 << 17, dev, 7000, 0)
+            qr = qs[0]
+
+            def launch_r():
+                for i, c in enumerate(rc):
+                    c.attend(qr[i % L_res], 1 << 17, o[i % L_res], stream)
+            launch_r()
+            pr, _ = graph_replay_times(launch_r, len(rc), stream, 20)
+            resid = {"attend_us_per_layer": stats(pr)["median"] * 1e3, "context": min(n_local, 1 << 17),
+                     "note": "fp32 k-means codebooks (decode codebook not fp16-exact): second V table "
+                             "pass + mma (R23)"}
+            del rc
+        except Exception as ex:   # pragma: no cover
+            resid = {"error": str(ex)[:300]}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -370,6 +574,9 @@ def run_ours(args):
                    "sample": f"failed: {ex}"}
 
     if rank == 0:
+        l2_note = (f"inputs larger than L2: {len(caches)} distinct caches ({ncopy} copy set(s) of "
+                   f"{L_res} layers) cycled, {bytes_att * L_res * ncopy / 1e6:.0f} MB streamed per "
+                   f"pass vs L2 {l2 / 2 ** 20:.0f} MiB (cudaDevAttrL2CacheSize)")
         line = {
             "metric": METRIC, "value": ms_per_step * 1e3, "unit": "us/token",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -377,29 +584,38 @@ def run_ours(args):
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "f16xf16->f32 (u%d codes; quantization decisions f64)" % w.bits,
             "data": "synthetic",
-            "config": {"workload": w.name, "layers": L, "context": w.T, "H_q": H, "H_kv": w.H_kv,
+            "config": {"workload": w.name, "layers": w.n_layers, "layers_resident": L_res,
+                       "context": w.T, "tokens_per_gpu": n_local, "H_q": H, "H_kv": w.H_kv,
                        "head_dim": d, "bits": w.bits, "outlier_ppm": w.ppm,
                        "parallelism": f"seq-shard x{world}" if world > 1 else "single-gpu",
-                       "step": "per layer: kvq_append(new K,V) + kvq_decode_attend(q)",
-                       "l2": f"inputs larger than L2 ({bytes_att / 1e6:.0f} MB per layer, "
-                             f"{L} layers cycled per step)"},
-            "attend_us_per_layer": att_ms_mean * 1e3,
-            "attend_us_per_step": att_ms_mean * 1e3 * L,
-            "hbm_gbs_step": bytes_att * L / (ms_per_step * 1e-3) / 1e9,
+                       "step": "per layer: kvq_append(new K,V) + kvq_decode_attend(q)"
+                               + (" / attend_partial + NCCL all-gather + merge" if world > 1 else ""),
+                       "layer_rule": (f"{L_res} of {w.n_layers} layers resident on this GPU "
+                                      f"({layer_bytes / 1e9:.2f} GB each); step time scaled "
+                                      f"x{scale_layers:.3f}") if L_res < w.n_layers else "all layers resident",
+                       "l2": l2_note},
+            "attend_us_per_layer": att_ms * 1e3,
+            "attend_us_per_layer_p10_p90": [att["p10"] * 1e3, att["p90"] * 1e3],
+            "attend_timing": ("CUDA graph of %d attend launches (distinct caches), %d replays, "
+                              "per-launch median" % (len(caches), att["n"])) if graphed else
+                             "eager launches, CUDA events (graph capture unavailable)",
+            "attend_us_per_step": att_ms * 1e3 * w.n_layers,
+            "hbm_gbs_step": bytes_att * w.n_layers / (ms_per_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(w.name),
                          "kernel": {1: "att_wa_kernel", 2: "att_wag_kernel"}.get(info.get("attend_kernel"), "att_kernel")
                                    + " (kvq_decode_attend: one launch)",
                          "bytes_per_launch": bytes_att, "peak_kind": peak_kind,
                          "splits": info["splits"], "heads_per_cta": info["heads_per_cta"]},
+            "compare": compare, "resid_codebook": resid,
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * L * (2 if world == 1 else 3),
+            "gpu_launches": args.steps * L_res * (2 if world == 1 else 3),
             "clocks": clocks.summary(),
             "key_outliers_per_token": nnz_mean / max(Tc, 1),
             # effective: step time minus the attend-only time (the attend launched right after
             # an append overlaps its prologue with the append through programmatic dependent
             # launch, so this is below the append kernel's own duration)
-            "append_us_per_layer": (ms_per_step - att_ms_mean * L) * 1e3 / L,
+            "append_us_per_layer": (ms_per_step / scale_layers - att_ms * L_res) * 1e3 / L_res,
             "prefill": prefill_line,
             "setup_s": t_setup,
         }

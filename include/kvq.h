@@ -26,9 +26,12 @@
  *     With KVQ_FLAG_TRUST_DEVICE_PTRS the check is skipped and pointers are assumed
  *     to be device pointers on cfg.device.
  *   - Borrowed buffers must stay valid until the stream reaches the call.
- *   - Threading: one writer per cache (append / prefill); attend calls may run
- *     concurrently with each other but not with a writer on another stream.  Distinct
- *     caches are independent.
+ *   - Threading: one writer per cache (append / prefill), and at most ONE attend
+ *     (kvq_decode_attend / kvq_decode_attend_partial) in flight per cache: every attend
+ *     on a cache uses that cache's split-partial scratch and merge tickets, so two
+ *     attends on the same cache must be ordered by the caller (same stream, or an
+ *     event between streams).  Attends never overlap a writer on another stream.
+ *     Distinct caches are independent (each has its own scratch).
  *   - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
  */
 #ifndef KVQ_H_
@@ -54,10 +57,21 @@ typedef enum {
 typedef struct kvq_cache kvq_cache;
 
 #define KVQ_FLAG_TRUST_DEVICE_PTRS 1u
+/* Opt-in programmatic dependent launch for the decode order "kvq_append(k, v) then
+ * kvq_decode_attend(q)" on one stream: the attend's prologue (query RoPE, per-query
+ * tables; it reads only q and the cache's constant parameters) overlaps the append
+ * kernel, and its first read of cache contents waits for the append (griddepcontrol).
+ * CONTRACT: with this flag the caller guarantees that q is complete in stream order
+ * BEFORE kvq_append is enqueued, i.e. no kernel that writes q is enqueued between the
+ * append and the attend.  Without the flag the attend waits for all prior work. */
+#define KVQ_FLAG_DECODE_PDL 2u
 
 typedef struct {
     int32_t n_q_heads;          /* H_q >= 1 */
-    int32_t n_kv_heads;         /* H_kv >= 1, H_q % H_kv == 0 (GQA group G = H_q/H_kv) */
+    int32_t n_kv_heads;         /* H_kv >= 1, H_q % H_kv == 0; GQA group G = H_q/H_kv.
+                                   Attend tilings of this build: G in {1, 2, 4} at 2-3
+                                   bits, G = 1 at 4 bits; other (bits, G) are rejected at
+                                   create with KVQ_ESHAPE */
     int32_t head_dim;           /* d; this build supports d == 128 */
     int32_t bits;               /* b in {2, 3, 4} */
     int32_t outlier_ppm;        /* f in parts per million, 0 <= ppm < 500000;
@@ -119,7 +133,9 @@ kvq_status kvq_decode_attend(kvq_cache *cache, const void *q_f16, int64_t pos, f
 kvq_status kvq_decode_attend_partial(kvq_cache *cache, const void *q_f16, int64_t pos,
                                      float *part, void *stream);
 
-/* Exact log-sum-exp merge of P partials (fixed order 0..P-1):
+/* Exact log-sum-exp merge of P partials (fixed order 0..P-1), the merge step of the
+ * north_star's sequence sharding:
+ *   m = max_i m_i;  l = sum_i 2^(m_i - m) l_i;  o = sum_i 2^(m_i - m) o_i / l
  *   parts: [P][H_q][d+2] fp32 (device or host); o: [H_q][d] fp32.
  * device: the CUDA device to run on. */
 kvq_status kvq_merge_partials(const float *parts, int32_t P, int32_t H_q, int32_t d,
@@ -182,6 +198,32 @@ kvq_status kvq_set_splits(kvq_cache *cache, int32_t splits);
  * out[6..8] / out[9..11]: wait / compaction / TMA issue of the two producer warps), summed
  * over CTAs.  Only when the process was started with KVQ_PHASE_TIMERS=1. */
 kvq_status kvq_phase_timers(kvq_cache *cache, uint64_t *out /* host [16] */);
+
+/* ------------------------------------------------------------------------------------
+ * fp16 comparator cache (BASELINE config C3 "4-bit vs 3-bit vs fp16 cache"): the paper's
+ * baseline decode is fp16 mat-vec against an fp16 cache of post-RoPE Keys ("Key fp16
+ * Matvec", "Value fp16 Matvec", the ~1.4x speedup of P:80).  Same decode step as the
+ * quantized cache (pre-RoPE q and its position in, fp32 o out), dense fp16 storage:
+ *   append : K_n is rotated by RoPE at position pos_base + n with exact fp64 angles and
+ *            rounded once to fp16 (R11, R12); V_n is stored as given.
+ *   attend : o_g = softmax_n(RoPE(q_g, pos) . K_n / sqrt(d)) V_n, fp32 softmax and P.V.
+ * cfg fields used: n_q_heads, n_kv_heads (G = H_q / H_kv), head_dim (128), capacity_tokens,
+ * pos_base, rope_theta, device, flags (KVQ_FLAG_TRUST_DEVICE_PTRS); bits / outlier_ppm /
+ * k_outlier_capacity are ignored.  Same error, ownership and threading conventions as the
+ * quantized cache (one writer, one attend in flight per cache). */
+typedef struct kvq_f16_cache kvq_f16_cache;
+kvq_status kvq_f16_cache_create(const kvq_config *cfg, kvq_f16_cache **out);
+void kvq_f16_cache_destroy(kvq_f16_cache *cache);
+/* T tokens: K_f16, V_f16 [T][D] fp16 pre-RoPE Keys and Values (device or host). */
+kvq_status kvq_f16_append(kvq_f16_cache *cache, const void *K_f16, const void *V_f16, int64_t T,
+                          void *stream);
+/* q_f16 [H_q][d] pre-RoPE; o [H_q][d] fp32.  KVQ_EEMPTY on an empty cache. */
+kvq_status kvq_f16_decode_attend(kvq_f16_cache *cache, const void *q_f16, int64_t pos, float *o,
+                                 void *stream);
+/* Stored post-RoPE Keys and Values of tokens [t0, t1) as fp16 bits [t1-t0][D] (host buffers,
+ * either may be NULL; synchronizes). */
+kvq_status kvq_f16_export(kvq_f16_cache *cache, int64_t t0, int64_t t1, uint16_t *k_out, uint16_t *v_out);
+int64_t kvq_f16_num_tokens(const kvq_f16_cache *cache);
 
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char *kvq_last_error(void);

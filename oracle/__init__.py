@@ -75,6 +75,11 @@ def _load():
     lib.kvo_quantize_value.restype = ctypes.c_int
     lib.kvo_quantize_value.argtypes = [P_u16, ctypes.c_int, ctypes.c_int, P_f32, ctypes.c_int,
                                        ctypes.c_int, P_u16, P_i32, P_u16, P_f32, P_f32]
+    lib.kvo_f64_to_f16.restype = ctypes.c_uint16
+    lib.kvo_f64_to_f16.argtypes = [ctypes.c_double]
+    lib.kvo_f16cache_key.argtypes = [P_u16, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_double, P_u16]
+    lib.kvo_attend_dense.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P_u16, P_u16,
+                                     P_u16, ctypes.c_int64, ctypes.c_double, P_f64]
     lib.kvo_prefill.restype = ctypes.c_int64
     lib.kvo_prefill.argtypes = [ctypes.c_int64, ctypes.c_int, P_u16, P_u16, P_f32, P_f32,
                                 P_f32, P_f32, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -268,6 +273,38 @@ def merge(parts) -> np.ndarray:
 def attend(cache: CanonCache, q, pos: int, **kw) -> np.ndarray:
     """o [H_q, d] = merged single partial."""
     return merge(attend_partial(cache, q, pos, **kw)[None])
+
+
+# ------------------------------------------------------ fp16 comparator cache (F16) ---
+def f64_to_f16(x: float) -> int:
+    """IEEE binary16 bits of x, round to nearest even (one rounding)."""
+    return int(_load().kvo_f64_to_f16(float(x)))
+
+
+def f16cache_keys(K, H: int, d: int, pos_base: int = 0, theta_base: float = 10000.0) -> np.ndarray:
+    """Stored Keys of the fp16 cache: fp16(RoPE(K_n, pos_base + n)) per head, [T, H d] bits."""
+    Kb = _f16bits(K)
+    T = Kb.shape[0]
+    out = np.zeros_like(Kb)
+    lib = _load()
+    for n in range(T):
+        row = np.ascontiguousarray(Kb[n])
+        o = np.zeros_like(row)
+        lib.kvo_f16cache_key(_p(row, P_u16), H, d, int(pos_base + n), float(theta_base), _p(o, P_u16))
+        out[n] = o
+    return out
+
+
+def attend_dense(Kpost, V, q, pos: int, *, H_q: int, H_kv: int, d: int,
+                 theta_base: float = 10000.0) -> np.ndarray:
+    """o [H_q, d] of textbook attention over dense post-RoPE fp16 Keys (kvo_attend_dense)."""
+    Kb, Vb = _f16bits(Kpost), _f16bits(V)
+    qb = _f16bits(np.asarray(q).reshape(H_q, d))
+    T = Kb.shape[0]
+    o = np.zeros((H_q, d), np.float64)
+    _load().kvo_attend_dense(T, H_q, H_kv, d, _p(Kb, P_u16), _p(Vb, P_u16), _p(qb, P_u16), int(pos),
+                             float(theta_base), _p(o, P_f64))
+    return o
 
 
 def pack(codes, bits: int) -> np.ndarray:

@@ -23,6 +23,11 @@
  *                            dequantized V^_t; uniform scores -> mean of
  *                            hand-dequantized V^ incl. a lower-index tie)
  *   merge           pinned  (any partition == unsplit)
+ *   f64_to_f16      pinned  (numpy's IEEE round-to-nearest-even float16 conversion,
+ *                            including ties, subnormals and overflow)
+ *   f16cache_key    pinned  (== f64_to_f16 of the pinned kvo_rope; position 0 == identity)
+ *   attend_dense    pinned  (torch SDPA in fp64 on the RoPE'd query; == the lossless-mode
+ *                            kvo_attend when the stored Keys are exact)
  *   attention values on realistic synthetic data: "parity unpinned" beyond the special
  *   cases above (the oracle is the reference) -- see DESIGN.md.
  */
@@ -358,6 +363,86 @@ void kvo_merge(int P, int H, int d, const double *parts, double *o) {
         }
         for (int c = 0; c < d; ++c) og[c] /= l;
     }
+}
+
+/* ------------------------------------------------------ fp16 comparator cache ---- */
+/* The paper's baseline decode is fp16 mat-vec against an fp16 cache of post-RoPE Keys
+ * ("Key fp16 Matvec", "Value fp16 Matvec"; BASELINE config C3 "fp16 cache").
+ * kvo_f64_to_f16: IEEE binary16 round-to-nearest-even of a double, one rounding. */
+uint16_t kvo_f64_to_f16(double x) {
+    uint16_t sign = signbit(x) ? 0x8000u : 0u;
+    double a = fabs(x);
+    if (isnan(x)) return 0x7e00u;
+    if (a >= 65520.0) return sign | 0x7c00u;           /* rounds to infinity */
+    if (a < ldexp(1.0, -14)) {                          /* subnormal: multiples of 2^-24 */
+        double q = a * ldexp(1.0, 24);
+        double f = floor(q);
+        double r = q - f;
+        uint32_t m = (uint32_t)f;
+        if (r > 0.5 || (r == 0.5 && (m & 1u))) m++;
+        return sign | (uint16_t)m;                      /* m == 1024 is the smallest normal */
+    }
+    int e;
+    double fr = frexp(a, &e);                           /* a = fr * 2^e, fr in [0.5, 1) */
+    double q = ldexp(fr, 11);                           /* 11 significant bits */
+    double f = floor(q);
+    double r = q - f;
+    uint32_t m = (uint32_t)f;
+    if (r > 0.5 || (r == 0.5 && (m & 1u))) m++;
+    if (m == 2048) { m = 1024; e++; }
+    int be = e - 1 + 15;                                /* biased exponent of 1.xxx * 2^(e-1) */
+    if (be >= 31) return sign | 0x7c00u;
+    return sign | (uint16_t)(be << 10) | (uint16_t)(m - 1024);
+}
+
+/* Stored Key of the fp16 cache: RoPE at position pos (fp64, kvo_rope) of every head of one
+ * token, rounded once to fp16.  x, out: [H d] fp16 bits. */
+void kvo_f16cache_key(const uint16_t *x, int H, int d, int64_t pos, double theta_base, uint16_t *out) {
+    double *xv = (double *)malloc(sizeof(double) * (size_t)d);
+    double *xr = (double *)malloc(sizeof(double) * (size_t)d);
+    for (int h = 0; h < H; ++h) {
+        for (int i = 0; i < d; ++i) xv[i] = kvo_f16_to_f64(x[(size_t)h * d + i]);
+        kvo_rope(xv, d, pos, theta_base, xr);
+        for (int i = 0; i < d; ++i) out[(size_t)h * d + i] = kvo_f64_to_f16(xr[i]);
+    }
+    free(xv);
+    free(xr);
+}
+
+/* Decode attention over a dense cache of post-RoPE Keys (plain definition, reading R13):
+ *   q~ = RoPE(q_g, pos); s_n = q~ . K_n / sqrt(d); o_g = sum_n e^{s_n - m} V_n / sum e^{s_n - m}
+ * Kpost, V: [T][H_kv d] fp16 bits; q [H_q][d] fp16 bits; o [H_q][d]. */
+void kvo_attend_dense(int64_t T, int H_q, int H_kv, int d, const uint16_t *Kpost,
+                      const uint16_t *V, const uint16_t *q, int64_t pos, double theta_base,
+                      double *o) {
+    int G = H_q / H_kv, D = H_kv * d;
+    double *qv = (double *)malloc(sizeof(double) * (size_t)d);
+    double *qr = (double *)malloc(sizeof(double) * (size_t)d);
+    double *s = (double *)malloc(sizeof(double) * (size_t)(T > 0 ? T : 1));
+    for (int g = 0; g < H_q; ++g) {
+        int h = g / G;
+        for (int i = 0; i < d; ++i) qv[i] = kvo_f16_to_f64(q[(size_t)g * d + i]);
+        kvo_rope(qv, d, pos, theta_base, qr);
+        double m = -INFINITY;
+        for (int64_t n = 0; n < T; ++n) {
+            double acc = 0.0;
+            for (int i = 0; i < d; ++i) acc += qr[i] * kvo_f16_to_f64(Kpost[(size_t)n * D + h * d + i]);
+            s[n] = acc / sqrt((double)d);
+            if (s[n] > m) m = s[n];
+        }
+        double l = 0.0;
+        double *og = o + (size_t)g * d;
+        for (int i = 0; i < d; ++i) og[i] = 0.0;
+        for (int64_t n = 0; n < T; ++n) {
+            double p = exp(s[n] - m);
+            l += p;
+            for (int i = 0; i < d; ++i) og[i] += p * kvo_f16_to_f64(V[(size_t)n * D + h * d + i]);
+        }
+        for (int i = 0; i < d; ++i) og[i] /= l;
+    }
+    free(qv);
+    free(qr);
+    free(s);
 }
 
 /* ------------------------------------------------------------------ Packing ---- */

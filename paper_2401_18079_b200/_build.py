@@ -4,14 +4,15 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkvq.so")
-SOURCES = ["kvq_api.cu", "kvq_quant.cu", "kvq_attend.cu", "kvq_attend_wa.cu"]
+SOURCES = ["kvq_api.cu", "kvq_quant.cu", "kvq_prefill.cu", "kvq_f16.cu", "kvq_attend.cu", "kvq_attend_wa.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"]
 
 
 def stale() -> bool:
@@ -27,17 +28,30 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    objs = [os.path.join(CSRC, s[:-3] + f".{os.getpid()}.o") for s in SOURCES]
+    cmds = [[NVCC, *FLAGS, "-c", "-o", o, os.path.join(CSRC, s)] for s, o in zip(SOURCES, objs)]
+    # one nvcc per translation unit, in parallel, then one link
+    with ThreadPoolExecutor(len(cmds)) as ex:
+        rs = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     log = os.path.join(HERE, "build.log")
+    text = "".join(" ".join(c) + "\n" + r.stdout + r.stderr for c, r in zip(cmds, rs))
+    ok = all(r.returncode == 0 for r in rs)
+    if ok:
+        rl = subprocess.run(link, capture_output=True, text=True)
+        text += " ".join(link) + "\n" + rl.stdout + rl.stderr
+        ok = rl.returncode == 0
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stderr[-8000:])
+        f.write(text)
+    if not ok:
+        sys.stderr.write(text[-8000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     os.replace(tmp, LIB)
     if verbose:
-        print(r.stderr)
+        print(text)
     return LIB
 
 

@@ -97,6 +97,41 @@ int classify(const void *p, int dev, uint32_t flags) {
     return 1;
 }
 
+// ---- exact fp16 thresholds of the fp64 ENC predicate (R8), for the prefill Key table ----
+uint16_t key2h(uint32_t k) { return (uint16_t)(k >= 0x8000u ? (k ^ 0x8000u) : (k ^ 0xffffu)); }
+double h2d(uint16_t h) {
+    const int e = (h >> 10) & 31, m = h & 1023;
+    double v = e == 0 ? std::ldexp((double)m, -24) : (e == 31 ? INFINITY : std::ldexp((double)(m | 1024), e - 25));
+    return (h & 0x8000u) ? -v : v;
+}
+// smallest order key in [0x0400, 0xFC00) (finite fp16, ascending) whose value satisfies the
+// monotone predicate, else 0xFC00 (+inf)
+template <typename F>
+uint32_t first_key(F pred) {
+    uint32_t a = 0x0400u, b = 0xfc00u;
+    while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (pred(h2d(key2h(mid)))) b = mid; else a = mid + 1;
+    }
+    return a;
+}
+// the oracle's ENC (kvo_enc): #{j : 2(y - z) > s (c_j + c_{j+1})} in fp64, no contraction
+int enc_exact(double y, float s, float z, const float *cb, int nlev) {
+    const double lhs = 2.0 * (y - (double)z);
+    int code = 0;
+    for (int j = 0; j + 1 < nlev; ++j) {
+        const volatile double rhs = (double)s * ((double)cb[j] + (double)cb[j + 1]);
+        if (lhs > rhs) code++;
+    }
+    return code;
+}
+uint16_t f16_of_small_int(int v) {   // exact fp16 bits of 0..15
+    if (v == 0) return 0;
+    int e = 0;
+    while ((v >> (e + 1)) != 0) ++e;
+    return (uint16_t)(((e + 15) << 10) | ((v << (10 - e)) & 1023));
+}
+
 kvq_status ensure_stage(kvq_cache *c, size_t bytes) {
     if (c->stage_bytes >= bytes) return KVQ_OK;
     if (c->stage) { cudaFree(c->stage); c->device_bytes -= (int64_t)c->stage_bytes; c->stage = nullptr; }
@@ -206,6 +241,12 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
         A(&d.vit, ntiles * d.NG * d.vcap_g * 4);
         A(&d.gcnt, ntiles * d.NG * 2 * 4 + 16);
     }
+    {
+        const int ps = kenc_words_per_pair(C.bits);
+        A(&d.kenc, (size_t)C.n_kv_heads * kPairs * ps * 4);
+        A(&d.lb, (size_t)(d.cap / 32 + 2) * 8);
+        A(&d.ticket, 64);
+    }
     c->max_splits = 4 * 148;
     A(&c->parts, (size_t)c->max_splits * d.H_q * (kHeadDim + 2) * 4);
     A(&c->tickets, 64 * 4);
@@ -239,7 +280,41 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
         mids[j] = (double)cbs[0][j] + (double)cbs[0][j + 1];
         mids[16 + j] = (double)cbs[2][j] + (double)cbs[2][j + 1];
     }
+    // Key ENC table of the prefill kernel: per channel the fp16 thresholds of the outlier test
+    // and of every ENC midpoint predicate, found by binary search over fp16 values with the
+    // oracle's exact fp64 predicate (monotone in y), and the codes of the clamped lo / hi
+    std::vector<uint32_t> kenc;
+    {
+        const int ps = kenc_words_per_pair(C.bits);
+        kenc.assign((size_t)C.n_kv_heads * kPairs * ps, 0u);
+        std::vector<uint16_t> cw((size_t)D * 20);
+        for (int64_t ch = 0; ch < D; ++ch) {
+            const double lo = prm->key_lo[ch], hi = prm->key_hi[ch];
+            const float s = kpar[ch], z = kpar[D + ch];
+            uint16_t *w = &cw[(size_t)ch * 20];
+            w[0] = key2h(first_key([&](double v) { return v >= lo; }));                 // L
+            const uint32_t kg = first_key([&](double v) { return v > hi; });
+            w[1] = key2h(kg - 1);                                                         // H
+            w[2] = f16_of_small_int(enc_exact(lo, s, z, cbs[0], nlev));
+            w[3] = f16_of_small_int(enc_exact(hi, s, z, cbs[0], nlev));
+            for (int j = 0; j + 1 < nlev; ++j) {
+                const double mj = (double)cbs[0][j] + (double)cbs[0][j + 1];
+                w[4 + j] = key2h(first_key([&](double y) {
+                    const volatile double rhs = (double)s * mj;
+                    return 2.0 * (y - (double)z) > rhs;
+                }));
+            }
+        }
+        for (int h = 0; h < C.n_kv_heads; ++h)
+            for (int p = 0; p < kPairs; ++p) {
+                const uint16_t *a = &cw[(size_t)(h * kHeadDim + p) * 20];
+                const uint16_t *b = &cw[(size_t)(h * kHeadDim + p + kPairs) * 20];
+                uint32_t *o = &kenc[(size_t)(h * kPairs + p) * ps];
+                for (int q = 0; q < 4 + nlev - 1; ++q) o[q] = (uint32_t)a[q] | ((uint32_t)b[q] << 16);
+            }
+    }
     cudaError_t e = cudaMemcpy(d.kpar, kpar.data(), kpar.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d.kenc, kenc.data(), kenc.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d.cb, cb, sizeof cb, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d.mids, mids, sizeof mids, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -341,7 +416,16 @@ static kvq_status append_tokens(kvq_cache *c, const void *K, const void *V, int6
         if (ck == 1) { CK(cudaMemcpyAsync(sb, K, bytes, cudaMemcpyHostToDevice, s)); Kd = (const __half *)sb; }
         if (cv == 1) { CK(cudaMemcpyAsync(sb + bytes, V, bytes, cudaMemcpyHostToDevice, s)); Vd = (const __half *)(sb + bytes); }
     }
-    cudaError_t e = launch_quantize(c->dc, Kd, Vd, c->T, T, s);
+    // the prefill kernel reads rows with 16-byte vector loads: stage unaligned device rows
+    if (T > 1 && (((uintptr_t)Kd | (uintptr_t)Vd) & 15u)) {
+        st = ensure_stage(c, 2 * bytes);
+        if (st != KVQ_OK) return st;
+        char *sb = (char *)c->stage;
+        if ((const void *)Kd != (const void *)sb) { CK(cudaMemcpyAsync(sb, Kd, bytes, cudaMemcpyDeviceToDevice, s)); Kd = (const __half *)sb; }
+        if ((const void *)Vd != (const void *)(sb + bytes)) { CK(cudaMemcpyAsync(sb + bytes, Vd, bytes, cudaMemcpyDeviceToDevice, s)); Vd = (const __half *)(sb + bytes); }
+    }
+    cudaError_t e = T == 1 ? launch_quantize(c->dc, Kd, Vd, c->T, T, s)
+                           : launch_prefill(c->dc, Kd, Vd, c->T, T, c->dc.lb, c->dc.ticket, s);
     if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
     c->T += T;
     c->pdl_ok = T == 1;
@@ -399,7 +483,7 @@ static kvq_status attend_impl(kvq_cache *c, const void *q, int64_t pos, float *o
     a.kernel_out = &c->last_kernel;
     a.hg_out = &c->hg;
     static const bool no_pdl = getenv("KVQ_NO_PDL") != nullptr;   // diagnostics switch
-    a.pdl = c->pdl_ok && c->pdl_stream == stream && cq == 0 && !no_pdl;
+    a.pdl = (c->cfg.flags & KVQ_FLAG_DECODE_PDL) && c->pdl_ok && c->pdl_stream == stream && cq == 0 && !no_pdl;
     c->pdl_ok = 0;
     cudaError_t e = launch_attend(c->dc, a, &c->last_splits, s);
     if (e != cudaSuccess) return cuda_fail(e, "attend launch");
@@ -538,6 +622,152 @@ kvq_status kvq_export(kvq_cache *c, int64_t t0, int64_t t1, kvq_export_buf *buf)
             }
         }
     }
+    return KVQ_OK;
+}
+
+// ------------------------------------------------------------- fp16 comparator cache --
+struct kvq_f16_cache {
+    kvq_config cfg;
+    F16Dev dc;
+    int64_t T = 0;
+    double *theta = nullptr;
+    float *parts = nullptr;
+    unsigned *tickets = nullptr;
+    void *stage = nullptr;
+    size_t stage_bytes = 0;
+    std::vector<void *> allocs;
+};
+
+static kvq_status f16_alloc(kvq_f16_cache *c, void **p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    e = cudaMemset(*p, 0, bytes ? bytes : 16);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset");
+    c->allocs.push_back(*p);
+    return KVQ_OK;
+}
+
+static kvq_status f16_stage(kvq_f16_cache *c, size_t bytes) {
+    if (c->stage_bytes >= bytes) return KVQ_OK;
+    if (c->stage) { cudaFree(c->stage); c->stage = nullptr; }
+    CK(cudaMalloc(&c->stage, bytes));
+    c->stage_bytes = bytes;
+    return KVQ_OK;
+}
+
+void kvq_f16_cache_destroy(kvq_f16_cache *c) {
+    if (!c) return;
+    cudaSetDevice(c->cfg.device);
+    cudaDeviceSynchronize();
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->stage) cudaFree(c->stage);
+    delete c;
+}
+
+kvq_status kvq_f16_cache_create(const kvq_config *cfg, kvq_f16_cache **out) {
+    if (!cfg || !out) return fail(KVQ_EINVAL, "null argument");
+    const kvq_config &C = *cfg;
+    if (C.n_q_heads < 1 || C.n_kv_heads < 1 || C.n_q_heads % C.n_kv_heads)
+        return fail(KVQ_ESHAPE, "head counts must be >= 1 with n_q_heads %% n_kv_heads == 0");
+    if (C.n_q_heads != C.n_kv_heads) return fail(KVQ_ESHAPE, "the fp16 comparator supports MHA (G = 1)");
+    if (C.head_dim != kHeadDim) return fail(KVQ_ESHAPE, "this build supports head_dim == 128");
+    if ((int64_t)C.n_kv_heads * kHeadDim > 8192) return fail(KVQ_ESHAPE, "D = H_kv*d must be <= 8192");
+    if (C.capacity_tokens < 1) return fail(KVQ_EINVAL, "capacity_tokens must be >= 1");
+    if (!(C.rope_theta > 0) || !std::isfinite(C.rope_theta)) return fail(KVQ_EINVAL, "rope_theta must be > 0");
+    if (C.pos_base < 0) return fail(KVQ_EINVAL, "pos_base must be >= 0");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (C.device < 0 || C.device >= ndev) return fail(KVQ_EDEVICE, "device %d not present", C.device);
+    CK(cudaSetDevice(C.device));
+    kvq_f16_cache *c = new (std::nothrow) kvq_f16_cache();
+    if (!c) return fail(KVQ_EINVAL, "out of host memory");
+    c->cfg = C;
+    F16Dev &d = c->dc;
+    d.H_q = C.n_q_heads; d.H_kv = C.n_kv_heads; d.G = C.n_q_heads / C.n_kv_heads;
+    d.D = C.n_kv_heads * kHeadDim;
+    d.cap = C.capacity_tokens;
+    d.pos_base = C.pos_base;
+    kvq_status st = KVQ_OK;
+    void *p = nullptr;
+    if (st == KVQ_OK && (st = f16_alloc(c, &p, (size_t)d.cap * d.D * 2)) == KVQ_OK) d.K = (__half *)p;
+    if (st == KVQ_OK && (st = f16_alloc(c, &p, (size_t)d.cap * d.D * 2)) == KVQ_OK) d.V = (__half *)p;
+    if (st == KVQ_OK && (st = f16_alloc(c, &p, 64 * 8)) == KVQ_OK) c->theta = (double *)p;
+    if (st == KVQ_OK && (st = f16_alloc(c, &p, (size_t)4 * 148 * d.H_q * (kHeadDim + 2) * 4)) == KVQ_OK) c->parts = (float *)p;
+    if (st == KVQ_OK && (st = f16_alloc(c, &p, (size_t)d.H_q * 4)) == KVQ_OK) c->tickets = (unsigned *)p;
+    if (st != KVQ_OK) { kvq_f16_cache_destroy(c); return st; }
+    double th[64];
+    for (int i = 0; i < 64; ++i) th[i] = std::pow(C.rope_theta, -2.0 * (double)i / (double)kHeadDim);
+    cudaError_t e = cudaMemcpy(c->theta, th, sizeof th, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { kvq_f16_cache_destroy(c); return cuda_fail(e, "upload theta"); }
+    d.theta_tab = c->theta;
+    *out = c;
+    return KVQ_OK;
+}
+
+int64_t kvq_f16_num_tokens(const kvq_f16_cache *c) { return c ? c->T : 0; }
+
+kvq_status kvq_f16_append(kvq_f16_cache *c, const void *K, const void *V, int64_t T, void *stream) {
+    if (!c) return fail(KVQ_EINVAL, "null cache");
+    if (T < 0) return fail(KVQ_EINVAL, "negative token count");
+    if (T == 0) return KVQ_OK;
+    if (!K || !V) return fail(KVQ_EINVAL, "null K or V");
+    if (c->T + T > c->dc.cap) return fail(KVQ_ECAPACITY, "token capacity %lld exceeded", (long long)c->dc.cap);
+    CK(cudaSetDevice(c->cfg.device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)T * c->dc.D * 2;
+    const int ck = classify(K, c->cfg.device, c->cfg.flags), cv = classify(V, c->cfg.device, c->cfg.flags);
+    if (ck < 0 || cv < 0) return fail(KVQ_EDEVICE, "K/V pointer not on device %d", c->cfg.device);
+    const __half *Kd = (const __half *)K, *Vd = (const __half *)V;
+    if (ck == 1 || cv == 1) {
+        kvq_status st = f16_stage(c, 2 * bytes);
+        if (st != KVQ_OK) return st;
+        char *sb = (char *)c->stage;
+        if (ck == 1) { CK(cudaMemcpyAsync(sb, K, bytes, cudaMemcpyHostToDevice, s)); Kd = (const __half *)sb; }
+        if (cv == 1) { CK(cudaMemcpyAsync(sb + bytes, V, bytes, cudaMemcpyHostToDevice, s)); Vd = (const __half *)(sb + bytes); }
+    }
+    cudaError_t e = launch_f16_store(c->dc, Kd, Vd, c->T, T, s);
+    if (e != cudaSuccess) return cuda_fail(e, "f16 store launch");
+    c->T += T;
+    return KVQ_OK;
+}
+
+kvq_status kvq_f16_decode_attend(kvq_f16_cache *c, const void *q, int64_t pos, float *o, void *stream) {
+    if (!c) return fail(KVQ_EINVAL, "null cache");
+    if (!q || !o) return fail(KVQ_EINVAL, "null q or output");
+    if (pos < 0) return fail(KVQ_EINVAL, "negative position");
+    if (c->T == 0) return fail(KVQ_EEMPTY, "attend on an empty cache");
+    CK(cudaSetDevice(c->cfg.device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t qb = (size_t)c->dc.H_q * kHeadDim * 2, ob = (size_t)c->dc.H_q * kHeadDim * 4;
+    const int cq = classify(q, c->cfg.device, c->cfg.flags), co = classify(o, c->cfg.device, c->cfg.flags);
+    if (cq < 0 || co < 0) return fail(KVQ_EDEVICE, "q/output pointer not on device %d", c->cfg.device);
+    const __half *qd = (const __half *)q;
+    float *od = o;
+    if (cq == 1 || co == 1) {
+        kvq_status st = f16_stage(c, qb + ob + 256);
+        if (st != KVQ_OK) return st;
+        char *sb = (char *)c->stage;
+        if (cq == 1) { CK(cudaMemcpyAsync(sb, q, qb, cudaMemcpyHostToDevice, s)); qd = (const __half *)sb; }
+        if (co == 1) od = (float *)(sb + ((qb + 255) / 256) * 256);
+    }
+    const int S = f16_auto_splits(c->dc, c->T);
+    cudaError_t e = launch_f16_attend(c->dc, qd, pos, c->T, od, c->parts, c->tickets, S, s);
+    if (e != cudaSuccess) return cuda_fail(e, "f16 attend launch");
+    if (co == 1) {
+        CK(cudaMemcpyAsync(o, od, ob, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    return KVQ_OK;
+}
+
+kvq_status kvq_f16_export(kvq_f16_cache *c, int64_t t0, int64_t t1, uint16_t *k_out, uint16_t *v_out) {
+    if (!c) return fail(KVQ_EINVAL, "null cache");
+    if (t0 < 0 || t1 < t0 || t1 > c->T) return fail(KVQ_EINVAL, "bad token range");
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaDeviceSynchronize());
+    const size_t n = (size_t)(t1 - t0) * c->dc.D * 2;
+    if (k_out && n) CK(cudaMemcpy(k_out, c->dc.K + t0 * c->dc.D, n, cudaMemcpyDeviceToHost));
+    if (v_out && n) CK(cudaMemcpy(v_out, c->dc.V + t0 * c->dc.D, n, cudaMemcpyDeviceToHost));
     return KVQ_OK;
 }
 

@@ -124,12 +124,17 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-// Score terms summed with shared integer atomics (no native float atomics in shared memory):
-// fixed point with 2^-16 resolution in log2-score units, |term| clamped to 2^15.
+// Score terms summed with shared 64-bit integer atomics (no native float atomics in shared
+// memory): fixed point with 2^-16 resolution in log2-score units.  The 47 integer bits hold
+// any sum of terms of finite fp16 data (|x q~| < 65504^2 * log2(e)/sqrt(d) < 2^30), so no
+// clamp is needed and no sum can wrap.
 constexpr float kKfixScale = 65536.f;
 constexpr int WEXP = 14;   // fp16 P.V weights scaled into [0, 2^14]
-__device__ __forceinline__ int kfix_of(float v) {
-    return __float2int_rn(fminf(fmaxf(v, -32768.f), 32767.f) * kKfixScale);
+__device__ __forceinline__ unsigned long long kfix_of(float v) {
+    return (unsigned long long)__float2ll_rn(v * kKfixScale);
+}
+__device__ __forceinline__ float kfix_val(unsigned long long v) {
+    return (float)(long long)v * (1.f / kKfixScale);
 }
 // 2^k as a float for k in [-126, 127] (clamped); exact, no libm call
 __device__ __forceinline__ float pow2i(int k) {
@@ -177,7 +182,7 @@ struct Cfg {
     static constexpr size_t t1 = (size_t)kPairs * 32 * 8;
     // per compute half: red, p, kcorr, hcorr, kbeg/kend, w16, osp, anchors, scalars
     static constexpr size_t half_bytes =
-        HW * HG * 32 * 4 + HG * 32 * 4 * 3 + HG * 64 * 4 + HG * 32 * 2 + HG * kHeadDim * 4 * 2
+        HW * HG * 32 * 4 + HG * 32 * 4 * 3 + HG * 64 * 4 + HG * 32 * 4 + HG * kHeadDim * 4 * 2
         + 64 * 16 + 64 * 8 + 64 * 4 + HG * 4 * 4 + 16 + 64;
     static constexpr size_t small =
         HG * kHeadDim * 4              /* qs */
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // per compute half h (alternate tiles): scratch of its own tile, at sp + h*half_bytes
     struct Half {
         float *red, *p_s, *osp, *beta_s, *m_fin, *l_fin, *z_fin;
-        int *kfix;              // [HG][32] Key-outlier + heavy-pair score terms, fixed point
+        unsigned long long *kfix;   // [HG][32] Key-outlier + heavy-pair score terms, fixed point
         int *vfix;              // [HG][128] Value-outlier sums of the tile, fixed point
         int *vmax;              // [0] max |delta| of the tile's Value items (float bits)
         float *vscale;          // [0] fixed-point scale of the tile's V items
@@ -244,10 +249,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         unsigned char *q = half_base + h * C::half_bytes;
         H.red = reinterpret_cast<float *>(q); q += HW * HG * 32 * 4;
         H.p_s = reinterpret_cast<float *>(q); q += HG * 32 * 4;
-        H.kfix = reinterpret_cast<int *>(q); q += HG * 32 * 4;
-        q += HG * 32 * 4;
+        H.kfix = reinterpret_cast<unsigned long long *>(q); q += HG * 32 * 8;
         q += HG * 64 * 4;
-        H.w16 = reinterpret_cast<uint16_t *>(q); q += HG * 32 * 2;
+        H.w16 = reinterpret_cast<uint16_t *>(q); q += HG * 32 * 4;   // hi [HG][32], then lo
         H.osp = reinterpret_cast<float *>(q); q += HG * kHeadDim * 4;
         H.vfix = reinterpret_cast<int *>(q); q += HG * kHeadDim * 4;
         q += (16 - ((HG * 32 * 2) % 16)) % 16;
@@ -512,13 +516,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     constexpr int MTW = 8 / WPK;                // m-tiles per warp
     constexpr int FB = 2 * BITS;                // bits per A field (2 tokens x 1 channel)
     constexpr int NWV = (MTW * 16 * BITS + 31) / 32;   // code words per lane per tile
-    static_assert(HKV <= HW && HW % HKV == 0 && G <= 8, "V task mapping");
+    static_assert(HKV <= HW && HW % HKV == 0 && G <= 4, "V task mapping; hi/lo weight columns 2G <= 8");
     const int vkv = hw / WPK;                                // local KV head
     const int mt0 = (hw % WPK) * MTW;
     const int vbit0 = mt0 * 16 * BITS;
     const int vw0 = vbit0 >> 5, voff = vbit0 & 31;           // voff = 16 only for b=3, MTW=1
     const int vg = lane >> 2, vt = lane & 3;
-    const int vq_lo = vkv * G + min(2 * vt, G - 1), vq_hi = vkv * G + min(2 * vt + 1, G - 1);
+    // D columns 2t, 2t+1 of lane (g, t): head t's hi and lo weight sums
+    const int vq_lo = vkv * G + min(vt, G - 1), vq_hi = vq_lo;
     float dacc[MTW][4];
 #pragma unroll
     for (int x = 0; x < MTW; ++x) dacc[x][0] = dacc[x][1] = dacc[x][2] = dacc[x][3] = 0.f;
@@ -536,13 +541,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
         // per-lane constants for the K phase: cis(j * theta_i) for this warp's KPW pairs
         // as fp16 pairs t = (cos, sin) and t' = (-sin, cos): the tile rotation is then one
         // HMUL2 + one HFMA2 per pair: (a.x t + a.y t') = (a.x cos - a.y sin, a.x sin + a.y cos)
-        __half2 t1h[KPW], t1r[KPW];
+        // (fp32; the tile rotation anchor x cis(j th_i) is formed in fp32 and rounded once to
+        // fp16)
+        float2 t1v[KPW];
 #pragma unroll
-        for (int k = 0; k < KPW; ++k) {
-            const float2 v = t1tab[(hw * KPW + k) * 32 + lane];
-            t1h[k] = __floats2half2_rn(v.x, v.y);
-            t1r[k] = __floats2half2_rn(-v.y, v.x);
-        }
+        for (int k = 0; k < KPW; ++k) t1v[k] = t1tab[(hw * KPW + k) * 32 + lane];
         // this warp's K tables: base | (pair code << 2), + a constant per (head, pair); the
         // base is a multiple of NE*4 bytes (dynamic shared memory is 1 KB aligned)
         const uint32_t klut_w = smem_u32(klut) + (uint32_t)(hw * KPW * NE * 4 * G);
@@ -679,8 +682,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
                 for (int k = 0; k < KPW; ++k) {
                     const int i = hw * KPW + k;
-                    const __half2 an = H.anc16[i];
-                    const __half2 csh = __hfma2(__high2half2(an), t1r[k], __hmul2(__low2half2(an), t1h[k]));
+                    const float2 an = H.anc32[i];
+                    const __half2 csh = __floats2half2_rn(an.x * t1v[k].x - an.y * t1v[k].y, an.x * t1v[k].y + an.y * t1v[k].x);
                     const uint32_t cs = *reinterpret_cast<const uint32_t *>(&csh);
                     const int b = 2 * BITS * k - 2;   // bit of (pair code << 2) in the window
 #pragma unroll
@@ -726,7 +729,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     float s = 0.f;
 #pragma unroll
                     for (int w = 0; w < HW; ++w) s += H.red[(w * HG + g) * 32 + j];
-                    s = s * lut_inv[g] + (float)H.kfix[g * 32 + j] * (1.f / kKfixScale);
+                    s = s * lut_inv[g] + kfix_val(H.kfix[g * 32 + j]);
                     H.kfix[g * 32 + j] = 0;
                     s = valid ? s : -CUDART_INF_F;
                     const float m_new = fmaxf(m_run, warp_max_redux(s));
@@ -737,7 +740,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                     z_lane = z_lane * alpha + p * sz.y;
                     m_run = m_new;
                     H.p_s[g * 32 + j] = p;
-                    H.w16[g * 32 + j] = __half_as_ushort(__float2half_rn(p * (sz.x * pe)));
+                    {   // weight as fp16 hi + lo
+                        const float wf = p * (sz.x * pe);
+                        const __half wh = __float2half_rn(wf);
+                        H.w16[g * 32 + j] = __half_as_ushort(wh);
+                        H.w16[HG * 32 + g * 32 + j] = __half_as_ushort(__float2half_rn(wf - __half2float(wh)));
+                    }
                     if (alpha != 1.f) {
 #pragma unroll
                         for (int x = 0; x < kHeadDim / 32; ++x) H.osp[g * kHeadDim + x * 32 + lane] *= alpha;
@@ -790,9 +798,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
                 uint32_t bw[2][2];
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) {
-                    const uint32_t *w32 = reinterpret_cast<const uint32_t *>(H.w16 + (vkv * G + (vg < G ? vg : 0)) * 32 + 16 * s2 + 2 * vt);
-                    bw[s2][0] = vg < G ? w32[0] : 0u;
-                    bw[s2][1] = vg < G ? w32[4] : 0u;
+                    // column vg: head vg / 2, its hi (vg even) or lo (vg odd) weight part
+                    const int hb = vg >> 1;
+                    const uint32_t *w32 = reinterpret_cast<const uint32_t *>(
+                        H.w16 + ((vg & 1) ? HG * 32 : 0) + (vkv * G + (hb < G ? hb : 0)) * 32 + 16 * s2 + 2 * vt);
+                    bw[s2][0] = hb < G ? w32[0] : 0u;
+                    bw[s2][1] = hb < G ? w32[4] : 0u;
                 }
                 // the residual pass is skipped when the decode codebook is fp16-exact (R23)
                 auto pv = [&](auto with_lo) {
@@ -900,15 +911,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
 #pragma unroll
             for (int ml = 0; ml < MTW; ++ml) {
                 const int ch = (mt0 + ml) * 16 + vg;
-                if (2 * vt < G) {
-                    float *o = H.osp + (vkv * G + 2 * vt) * kHeadDim + ch;
-                    o[0] += dacc[ml][0] * sc;
-                    o[8] += dacc[ml][2] * sc;
-                }
-                if (2 * vt + 1 < G) {
-                    float *o = H.osp + (vkv * G + 2 * vt + 1) * kHeadDim + ch;
-                    o[0] += dacc[ml][1] * sc;
-                    o[8] += dacc[ml][3] * sc;
+                if (vt < G) {
+                    float *o = H.osp + (vkv * G + vt) * kHeadDim + ch;
+                    o[0] += (dacc[ml][0] + dacc[ml][1]) * sc;
+                    o[8] += (dacc[ml][2] + dacc[ml][3]) * sc;
                 }
             }
         }
@@ -1094,6 +1100,7 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
 // CTAs of exactly one group.
 int attend_bucket_heads(int bits, int H_q, int G) {
     if (G == 1 && (bits == 2 || bits == 3) && H_q % 4 == 0) return 2;
+    if ((G == 2 || G == 4) && (bits == 2 || bits == 3)) return G;   // GQA kernel: one KV head
     return attend_heads_per_cta(bits, H_q, G);
 }
 
@@ -1135,7 +1142,7 @@ cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_us
     const bool wa = !a.timers && !legacy && attend_wa_supported(c);
     const bool wag = !a.timers && !legacy && attend_wag_supported(c);
     // CTA heads: 4 for the warp-autonomous kernels, else one bucket group
-    const int hg = (wa || wag) ? 4 : (c.GW / kHeadDim) * c.G;
+    const int hg = wa ? 4 : (wag ? c.G : (c.GW / kHeadDim) * c.G);
     if (hg == 0) return cudaErrorInvalidValue;
     if (a.kernel_out) *a.kernel_out = wa ? 1 : (wag ? 2 : 0);
     if (a.hg_out) *a.hg_out = hg;

@@ -100,10 +100,22 @@ __device__ __forceinline__ int ilog2f(float x) { return ((__float_as_int(x) >> 2
 constexpr int HG = 4;      // query heads per CTA (MHA: 4 KV heads, one outlier bucket group)
 constexpr int NSTREAM = 8; // tile streams per CTA (warps sharing a stream take other heads)
 
-// Key-outlier score terms in fixed point: 2^-16 log2-score units, |term| < 2^15
+// Key-outlier score terms in 64-bit fixed point: 2^-16 log2-score units; 47 integer bits
+// hold any sum of finite fp16 terms (|x q~| < 2^30), so there is no clamp and no wrap
 constexpr float kKfixScale = 65536.f;
-__device__ __forceinline__ int kfix_of(float v) {
-    return __float2int_rn(fminf(fmaxf(v, -32768.f), 32767.f) * kKfixScale);
+__device__ __forceinline__ unsigned long long kfix_of(float v) {
+    return (unsigned long long)__float2ll_rn(v * kKfixScale);
+}
+__device__ __forceinline__ float kfix_val(unsigned long long v) {
+    return (float)(long long)v * (1.f / kKfixScale);
+}
+// 32-bit variant (MHA kernel): terms with |v| < 2^7 go to int32 fixed point -- at most 128
+// Key-outlier items per (token, head), so |sum| < 2^7 * 2^7 * 2^16 = 2^30 cannot wrap --
+// and larger terms (extreme fp16 outliers only) to an fp32 side sum.
+constexpr float kKfixSmall = 128.f;
+__device__ __forceinline__ void kfix_add32(int *fix, float *big, float v) {
+    if (fabsf(v) < kKfixSmall) atomicAdd(fix, __float2int_rn(v * kKfixScale));
+    else atomicAdd(big, v);
 }
 // a value the compiler cannot see through (keeps table bases OR-able instead of re-added)
 __device__ __forceinline__ uint32_t opaque(uint32_t x) {
@@ -123,12 +135,12 @@ struct WCfg {
     static constexpr size_t vlut = (size_t)(RESID ? 2 : 1) * NE * 32 * 4;
     static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
-    static constexpr size_t t1h = (size_t)kPairs * 32 * 4;    // cis(j th_i) fp16x2 [i/2][j][i%2]
+    static constexpr size_t t1h = 0;
     static constexpr size_t t1f = (size_t)kPairs * 32 * 8;    // cis(j th_i) fp32 [i][j]
     // per warp: K words of the tile (cp.async target), K-outlier fixed-point terms (then p),
     // V-outlier fixed-point sums, anchors (fp16 rotation pairs, fp32)
     static constexpr size_t w_kst = (size_t)WH * KWH * 32 * 4;
-    static constexpr size_t w_bytes = w_kst + WH * 32 * 4 + WH * kHeadDim * 4 + 64 * 8 * 2;
+    static constexpr size_t w_bytes = w_kst + WH * 32 * 4 + WH * kHeadDim * 4 + 64 * 8;
     static constexpr int KCH = WH * KWH / 4;              // 16-byte K-word chunks per lane
     static constexpr size_t small = HG * kHeadDim * 4 /* qs */ + 64 * 16 /* rot */
         + HG * kHeadDim * 4 * 2 /* ks, kz */ + 64 * 4 /* cb */ + HG * 64 * 4 /* bound */
@@ -227,7 +239,10 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     int *kfix = reinterpret_cast<int *>(wp); wp += WH * 32 * 4;
     float *ps = reinterpret_cast<float *>(kfix);   // p of the tile, once the K terms are read
     int *vfix = reinterpret_cast<int *>(wp); wp += WH * kHeadDim * 4;
-    uint2 *anc16 = reinterpret_cast<uint2 *>(wp); wp += 64 * 8;
+    // Key-outlier terms too large for the 32-bit fixed point (|term| >= 2^7 log2 units, only
+    // extreme fp16 outliers): fp32 sums [WH][32] in the V-outlier scratch, which is free from
+    // the K phase until the V-outlier phase (zeroed again at the end of every tile)
+    float *kbig = reinterpret_cast<float *>(vfix);
     float2 *anc32 = reinterpret_cast<float2 *>(wp);
 
     // ------------------------------------------------------------- first tile's data
@@ -299,7 +314,6 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         double s, co;
         sincos((double)j * th, &s, &co);
         t1f[x] = make_float2((float)co, (float)s);
-        t1h[((i >> 1) * 32 + j) * 2 + (i & 1)] = pack_half2((float)co, (float)s);   // pairs i, i+1 adjacent
     }
     // this warp's anchors cis((pos_base + 32 t_first) th_i), fp64 state in registers (pairs
     // lane and lane + 32), advanced per tile
@@ -314,9 +328,8 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         const double co = b0.x * cr - b0.y * sr, s = b0.x * sr + b0.y * cr;
         anc64[k] = make_double2(co, s);
         anc32[i] = make_float2((float)co, (float)s);
-        anc16[i] = make_uint2(pack_half2((float)co, (float)s), pack_half2(-(float)s, (float)co));
     }
-    for (int x = lane; x < WH * 32; x += 32) kfix[x] = 0;
+    for (int x = lane; x < WH * 32; x += 32) { kfix[x] = 0; kbig[x] = 0.f; }
     for (int x = tid; x < HG * kHeadDim; x += NTHR) {
         ks_s[x] = c.kpar[c_lo + x];
         kz_s[x] = c.kpar[D + c_lo + x];
@@ -435,6 +448,11 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         co = ax * tt.x - ay * tt.y;
         si = ax * tt.y + ay * tt.x;
     };
+    auto rot16 = [&](int i) -> uint32_t {
+        float co, si;
+        rot32(i, lane, co, si);
+        return pack_half2(co, si);
+    };
 
     for (int t = t_first; t < t_end; t += NSTREAM) {
         const int64_t n0 = (int64_t)t * 32;
@@ -469,21 +487,11 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         float acc_c[WH], acc_s[WH];
 #pragma unroll
         for (int h = 0; h < WH; ++h) { acc_c[h] = 0.f; acc_s[h] = 0.f; }
-        uint4 an2;
-        uint2 tj2;
 #pragma unroll
         for (int i = 0; i < kPairs; ++i) {
             if (i == kPairs / 2) load_v();
-            if ((i & 1) == 0) {   // rotation inputs of pairs i, i+1 in one load each
-                an2 = *reinterpret_cast<const uint4 *>(anc16 + i);
-                tj2 = reinterpret_cast<const uint2 *>(t1h)[(i >> 1) * 32 + lane];
-            }
-            const uint2 an = (i & 1) ? make_uint2(an2.z, an2.w) : make_uint2(an2.x, an2.y);
-            const uint32_t tj = (i & 1) ? tj2.y : tj2.x;
-            const __half2 th = *reinterpret_cast<const __half2 *>(&tj);
-            const __half2 csh = __hfma2(*reinterpret_cast<const __half2 *>(&an.y), __high2half2(th),
-                                        __hmul2(*reinterpret_cast<const __half2 *>(&an.x), __low2half2(th)));
-            const uint32_t cs = *reinterpret_cast<const uint32_t *>(&csh);
+            // cis(n' th_i) = anchor x cis(j th_i) in fp32, rounded once to fp16
+            const uint32_t cs = rot16(i);
             const int bit = FB * i, w = bit >> 5, sh = bit & 31;
 #pragma unroll
             for (int h = 0; h < WH; ++h) {
@@ -548,13 +556,13 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                 if (32 * k < nk && lane + 32 * k < nk) {
                     int j, h;
                     const float v = k_corr(kitm[k], j, h);
-                    atomicAdd(&kfix[h * 32 + j], kfix_of(v));
+                    kfix_add32(&kfix[h * 32 + j], &kbig[h * 32 + j], v);
                 }
             }
             for (int x = 32 * IPL + lane; x < nk; x += 32) {
                 int j, h;
                 const float v = k_corr(__ldg(c.kit + bucket * c.kcap_g + x), j, h);
-                atomicAdd(&kfix[h * 32 + j], kfix_of(v));
+                kfix_add32(&kfix[h * 32 + j], &kbig[h * 32 + j], v);
             }
             if (kov) {   // overflowed bucket: this tile's Key outliers from the CSC arrays (rare)
                 for (int j = 0; j < ntok; ++j) {
@@ -565,7 +573,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                         if (ch < w_lo || ch >= w_lo + WH * kHeadDim) continue;
                         int jj, h;
                         const float v = k_corr((rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - w_lo), jj, h);
-                        atomicAdd(&kfix[h * 32 + jj], kfix_of(v));
+                        kfix_add32(&kfix[h * 32 + jj], &kbig[h * 32 + jj], v);
                     }
                 }
             }
@@ -581,10 +589,10 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         const float smax = warp_max_redux(valid ? vsz.x : 0.f);
         const int E = smax > 0.f ? ilog2f(smax) + 1 : 0;
         const float pe = pow2i(WEXP - E), sc_out = pow2i(E - WEXP);
-        uint32_t w2s[WH];
+        uint32_t w2s[WH], w2l[WH];
 #pragma unroll
         for (int h = 0; h < WH; ++h) {
-            float s = sco[h] + (float)kfix[h * 32 + lane] * (1.f / kKfixScale);
+            float s = sco[h] + (float)kfix[h * 32 + lane] * (1.f / kKfixScale) + kbig[h * 32 + lane];
             s = valid ? s : -CUDART_INF_F;
             const float m_new = fmaxf(m_run[h], warp_max_redux(s));
             const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run[h] - m_new);
@@ -597,19 +605,29 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                 for (int r = 0; r < 4; ++r) acc[h][r] *= alpha;
             }
             ps[h * 32 + lane] = p;   // over this lane's K term, just read
-            const uint32_t w16 = __half_as_ushort(__float2half_rn(p * (vsz.x * pe)));
-            w2s[h] = w16 | (__shfl_down_sync(0xffffffffu, w16, 1) << 16);   // tokens lane, lane+1
+            // weight p s_n 2^(WEXP-E) as fp16 hi + lo (the lo part rides in the odd B columns,
+            // so the mma sums both at no extra cost)
+            const float wf = p * (vsz.x * pe);
+            const __half wh = __float2half_rn(wf);
+            const uint32_t hb = __half_as_ushort(wh), lb = __half_as_ushort(__float2half_rn(wf - __half2float(wh)));
+            w2s[h] = hb | (__shfl_down_sync(0xffffffffu, hb, 1) << 16);   // tokens lane, lane+1
+            w2l[h] = lb | (__shfl_down_sync(0xffffffffu, lb, 1) << 16);
         }
         // --------------------------------------------------------- a5: P.V dense
 #pragma unroll
         for (int h = 0; h < WH; ++h) {
             // the next tile's K words, in flight during the rest of the tile (issued once the
             // first head's V words are consumed, to keep the register peak down)
-            uint32_t bw[2][2];   // B fragments: weights of tokens 16 s2 + 2t (+1) and + 8
+            uint32_t bw[2][2];   // B fragments: weights of tokens 16 s2 + 2t (+1) and + 8;
+                                 // column vg: hi part (vg even) or lo part (vg odd)
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
-                bw[s2][0] = __shfl_sync(0xffffffffu, w2s[h], 16 * s2 + 2 * vt);
-                bw[s2][1] = __shfl_sync(0xffffffffu, w2s[h], 16 * s2 + 2 * vt + 8);
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint32_t xh = __shfl_sync(0xffffffffu, w2s[h], 16 * s2 + 2 * vt + 8 * r);
+                    const uint32_t xl = __shfl_sync(0xffffffffu, w2l[h], 16 * s2 + 2 * vt + 8 * r);
+                    bw[s2][r] = (vg & 1) ? xl : xh;
+                }
             }
 #pragma unroll
             for (int ml = 0; ml < 8; ++ml) {
@@ -631,10 +649,11 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                     mma_f16_f32(d, a, bw[s2]);
                     if constexpr (RESID) mma_f16_f32(d, alo, bw[s2]);
                 }
-                // every column holds head h: lane (g, t) keeps rows g, g+8 of m-tiles t, t+4
+                // columns 2t, 2t+1 hold head h's hi and lo sums: lane (g, t) keeps rows g, g+8
+                // of m-tiles t, t+4
                 if (vt == (ml & 3)) {
-                    acc[h][(ml >> 2) * 2] += d[0] * sc_out;
-                    acc[h][(ml >> 2) * 2 + 1] += d[2] * sc_out;
+                    acc[h][(ml >> 2) * 2] += (d[0] + d[1]) * sc_out;
+                    acc[h][(ml >> 2) * 2 + 1] += (d[2] + d[3]) * sc_out;
                 }
             }
         }
@@ -733,7 +752,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         }
         __syncwarp();
 #pragma unroll
-        for (int h = 0; h < WH; ++h) kfix[h * 32 + lane] = 0;   // p read by every lane: done
+        for (int h = 0; h < WH; ++h) { kfix[h * 32 + lane] = 0; kbig[h * 32 + lane] = 0.f; }   // p read: done
 
         // advance the anchors by NSTREAM tiles (fp64 complex rotation)
 #pragma unroll
@@ -743,7 +762,6 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
             anc64[k] = b;
             anc32[i] = make_float2((float)b.x, (float)b.y);
-            anc16[i] = make_uint2(pack_half2((float)b.x, (float)b.y), pack_half2(-(float)b.y, (float)b.x));
         }
         cnt_k = ncnt_k;
         cnt_v = ncnt_v;
@@ -883,6 +901,7 @@ constexpr int NSG = 16;    // tile streams (= warps) per GQA CTA
 
 template <int BITS, bool RESID, int G>
 struct GCfg {
+    static_assert(G <= 4, "hi/lo weight columns: 2 G <= 8 mma columns");
     static constexpr int NWARP = NSG;
     static constexpr int NTHR = NWARP * 32;
     static constexpr int IPL = 4;
@@ -893,12 +912,12 @@ struct GCfg {
     static constexpr size_t vlut = (size_t)(RESID ? 2 : 1) * NE * 32 * 4;
     static constexpr size_t klut = (size_t)G * kPairs * NE * 4;   // [i][pair code][G]
     static constexpr size_t hlut = (size_t)G * HMAX * NE * 8;
-    static constexpr size_t t1h = (size_t)kPairs * 32 * 4;
+    static constexpr size_t t1h = 0;
     static constexpr size_t t1f = (size_t)kPairs * 32 * 8;
     // per warp: K words (cp.async target), K-outlier terms (then p) [G][32], V-outlier sums
     // fp32 [G][128], anchors
     static constexpr size_t w_kst = (size_t)KWH * 32 * 4;
-    static constexpr size_t w_bytes = w_kst + G * 32 * 4 + G * kHeadDim * 4 + 64 * 8 * 2;
+    static constexpr size_t w_bytes = w_kst + G * 32 * 8 + G * kHeadDim * 4 + 64 * 8;
     static constexpr int KCH = KWH / 4;
     static constexpr size_t small = G * kHeadDim * 4 /* qs */ + 64 * 16 /* rot */
         + kHeadDim * 4 * 2 /* ks, kz */ + 64 * 4 /* cb */ + G * 64 * 4 /* bound */
@@ -966,10 +985,9 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
 
     unsigned char *wp = wbase + warp * C::w_bytes;
     uint32_t *kst = reinterpret_cast<uint32_t *>(wp); wp += C::w_kst;
-    int *kfix = reinterpret_cast<int *>(wp); wp += G * 32 * 4;
+    unsigned long long *kfix = reinterpret_cast<unsigned long long *>(wp); wp += G * 32 * 8;
     float *ps = reinterpret_cast<float *>(kfix);
     float *osp = reinterpret_cast<float *>(wp); wp += G * kHeadDim * 4;
-    uint2 *anc16 = reinterpret_cast<uint2 *>(wp); wp += 64 * 8;
     float2 *anc32 = reinterpret_cast<float2 *>(wp);
 
     const int t_first = t_begin + warp;
@@ -1033,7 +1051,6 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         double s, co;
         sincos((double)j * th, &s, &co);
         t1f[x] = make_float2((float)co, (float)s);
-        t1h[((i >> 1) * 32 + j) * 2 + (i & 1)] = pack_half2((float)co, (float)s);
     }
     double2 anc64[2];
 #pragma unroll
@@ -1046,7 +1063,6 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         const double co = b0.x * cr - b0.y * sr, s = b0.x * sr + b0.y * cr;
         anc64[k] = make_double2(co, s);
         anc32[i] = make_float2((float)co, (float)s);
-        anc16[i] = make_uint2(pack_half2((float)co, (float)s), pack_half2(-(float)s, (float)co));
     }
     for (int x = lane; x < G * 32; x += 32) kfix[x] = 0;
     for (int x = lane; x < G * kHeadDim; x += 32) osp[x] = 0.f;
@@ -1156,12 +1172,18 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
 #pragma unroll
     for (int g = 0; g < G; ++g) { m_run[g] = -CUDART_INF_F; l_lane[g] = 0.f; z_lane[g] = 0.f; }
     int E_run = -126;
-    const int hc0 = min(2 * vt, G - 1), hc1 = min(2 * vt + 1, G - 1);   // this lane's D columns
+    // D columns 2t, 2t+1 of lane (g, t) are head t's hi and lo weight sums
+    const int hcl = min(vt, G - 1);
     auto rot32 = [&](int i, int j, float &co, float &si) {
         const float2 a = anc32[i];
         const float2 tt = t1f[i * 32 + j];
         co = a.x * tt.x - a.y * tt.y;
         si = a.x * tt.y + a.y * tt.x;
+    };
+    auto rot16 = [&](int i) -> uint32_t {
+        float co, si;
+        rot32(i, lane, co, si);
+        return pack_half2(co, si);
     };
 
     for (int t = t_first; t < t_end; t += NSG) {
@@ -1186,20 +1208,9 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         float acc_c[G], acc_s[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) { acc_c[g] = 0.f; acc_s[g] = 0.f; }
-        uint4 an2;
-        uint2 tj2;
 #pragma unroll
         for (int i = 0; i < kPairs; ++i) {
-            if ((i & 1) == 0) {
-                an2 = *reinterpret_cast<const uint4 *>(anc16 + i);
-                tj2 = reinterpret_cast<const uint2 *>(t1h)[(i >> 1) * 32 + lane];
-            }
-            const uint2 an = (i & 1) ? make_uint2(an2.z, an2.w) : make_uint2(an2.x, an2.y);
-            const uint32_t tj = (i & 1) ? tj2.y : tj2.x;
-            const __half2 th = *reinterpret_cast<const __half2 *>(&tj);
-            const __half2 csh = __hfma2(*reinterpret_cast<const __half2 *>(&an.y), __high2half2(th),
-                                        __hmul2(*reinterpret_cast<const __half2 *>(&an.x), __low2half2(th)));
-            const uint32_t cs = *reinterpret_cast<const uint32_t *>(&csh);
+            const uint32_t cs = rot16(i);   // fp32 rotation rounded once
             const int bit = FB * i, w = bit >> 5, sh = bit & 31;
             // (pair code << 2) << log2(G): the G heads' entries of a code are adjacent
             uint32_t off;
@@ -1286,11 +1297,11 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         const int E_new = smax > 0.f ? max(E_run, ilog2f(smax) + 1) : E_run;
         const float pe = pow2i(WEXP - E_new), rE = pow2i(E_run - E_new);
         E_run = E_new;
-        uint32_t w2s[G];
+        uint32_t w2s[G], w2l[G];
         float al[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            float s = sco[g] + (float)kfix[g * 32 + lane] * (1.f / kKfixScale);
+            float s = sco[g] + kfix_val(kfix[g * 32 + lane]);
             s = valid ? s : -CUDART_INF_F;
             const float m_new = fmaxf(m_run[g], warp_max_redux(s));
             const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run[g] - m_new);
@@ -1304,14 +1315,18 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
                 for (int x = 0; x < kHeadDim / 32; ++x) osp[g * kHeadDim + x * 32 + lane] *= alpha;
             }
             ps[g * 32 + lane] = p;
-            const uint32_t w16 = __half_as_ushort(__float2half_rn(p * (vsz.x * pe)));
-            w2s[g] = w16 | (__shfl_down_sync(0xffffffffu, w16, 1) << 16);
+            const float wf = p * (vsz.x * pe);
+            const __half wh = __float2half_rn(wf);
+            const uint32_t hb = __half_as_ushort(wh), lb = __half_as_ushort(__float2half_rn(wf - __half2float(wh)));
+            w2s[g] = hb | (__shfl_down_sync(0xffffffffu, hb, 1) << 16);
+            w2l[g] = lb | (__shfl_down_sync(0xffffffffu, lb, 1) << 16);
         }
         {   // rescale the accumulators: per column (head) alpha, and the weight exponent
-            float a0 = al[0], a1 = al[0];
+            float a0 = al[0];
 #pragma unroll
-            for (int g = 1; g < G; ++g) { a0 = hc0 == g ? al[g] : a0; a1 = hc1 == g ? al[g] : a1; }
-            a0 *= rE; a1 *= rE;
+            for (int g = 1; g < G; ++g) a0 = hcl == g ? al[g] : a0;
+            a0 *= rE;
+            const float a1 = a0;
             if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
 #pragma unroll
                 for (int ml = 0; ml < 8; ++ml) {
@@ -1320,7 +1335,8 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
                 }
             }
         }
-        // B fragments: column vg = query head vg (vg < G), tokens 16 s2 + 2 vt (+1) and + 8
+        // B fragments: column vg = query head vg / 2, its hi (vg even) or lo (vg odd) weight
+        // part; tokens 16 s2 + 2 vt (+1) and + 8
         uint32_t bw[2][2];
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2)
@@ -1329,8 +1345,9 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
                 uint32_t v = 0u;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    const uint32_t x = __shfl_sync(0xffffffffu, w2s[g], 16 * s2 + 2 * vt + 8 * r);
-                    v = vg == g ? x : v;
+                    const uint32_t xh = __shfl_sync(0xffffffffu, w2s[g], 16 * s2 + 2 * vt + 8 * r);
+                    const uint32_t xl = __shfl_sync(0xffffffffu, w2l[g], 16 * s2 + 2 * vt + 8 * r);
+                    v = (vg >> 1) == g ? ((vg & 1) ? xl : xh) : v;
                 }
                 bw[s2][r] = v;
             }
@@ -1413,7 +1430,6 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
             const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
             anc64[k] = b;
             anc32[i] = make_float2((float)b.x, (float)b.y);
-            anc16[i] = make_uint2(pack_half2((float)b.x, (float)b.y), pack_half2(-(float)b.y, (float)b.x));
         }
         cnt_k = ncnt_k;
         cnt_v = ncnt_v;
@@ -1429,13 +1445,9 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
 #pragma unroll
         for (int ml = 0; ml < 8; ++ml) {
             const int ch = ml * 16 + vg;
-            if (2 * vt < G) {
-                osp[(2 * vt) * kHeadDim + ch] += dacc[ml][0] * sc;
-                osp[(2 * vt) * kHeadDim + ch + 8] += dacc[ml][2] * sc;
-            }
-            if (2 * vt + 1 < G) {
-                osp[(2 * vt + 1) * kHeadDim + ch] += dacc[ml][1] * sc;
-                osp[(2 * vt + 1) * kHeadDim + ch + 8] += dacc[ml][3] * sc;
+            if (vt < G) {
+                osp[vt * kHeadDim + ch] += (dacc[ml][0] + dacc[ml][1]) * sc;
+                osp[vt * kHeadDim + ch + 8] += (dacc[ml][2] + dacc[ml][3]) * sc;
             }
         }
     }
@@ -1465,7 +1477,7 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
             const float wt = exp2f(ml[0] - m);
             l += wt * ml[1];
             if (ch < kHeadDim) {
-                const float *ow = reinterpret_cast<const float *>(wbase + w * C::w_bytes + C::w_kst + G * 32 * 4);
+                const float *ow = reinterpret_cast<const float *>(wbase + w * C::w_bytes + C::w_kst + G * 32 * 8);
                 o += wt * ow[g * kHeadDim + ch];
             }
         }
@@ -1531,22 +1543,26 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
     if (tid == 0) P.tickets[hk] = 0;
 }
 
-template <int BITS, bool RESID>
+template <int BITS, bool RESID, int G>
 cudaError_t launch_wag_t(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
-    using C = GCfg<BITS, RESID, 4>;
+    using C = GCfg<BITS, RESID, G>;
     static_assert(C::total <= 227 * 1024, "shared memory");
-    cudaError_t e = cudaFuncSetAttribute(att_wag_kernel<BITS, RESID, 4>,
+    cudaError_t e = cudaFuncSetAttribute(att_wag_kernel<BITS, RESID, G>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::total);
     if (e != cudaSuccess) return e;
-    e = launch_maybe_pdl(att_wag_kernel<BITS, RESID, 4>, grid, C::NTHR, C::total, s, P.pdl != 0, c, P);
+    e = launch_maybe_pdl(att_wag_kernel<BITS, RESID, G>, grid, C::NTHR, C::total, s, P.pdl != 0, c, P);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+template <int BITS, bool RESID>
+cudaError_t launch_wag_g(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
+    return c.G == 2 ? launch_wag_t<BITS, RESID, 2>(c, P, grid, s) : launch_wag_t<BITS, RESID, 4>(c, P, grid, s);
 }
 
 }  // namespace
 
 bool attend_wag_supported(const DevCache &c) {
-    return c.G == 4 && (c.bits == 2 || c.bits == 3) && c.GW == kHeadDim;   // bucket per KV head
+    return (c.G == 2 || c.G == 4) && (c.bits == 2 || c.bits == 3) && c.GW == kHeadDim;   // bucket per KV head
 }
 
 cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s) {
@@ -1556,8 +1572,8 @@ cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cud
     P.pdl = a.pdl;
     const int grid = c.H_kv * S;
     const bool resid = !c.vcb_exact16;
-    if (c.bits == 2) return resid ? launch_wag_t<2, true>(c, P, grid, s) : launch_wag_t<2, false>(c, P, grid, s);
-    if (c.bits == 3) return resid ? launch_wag_t<3, true>(c, P, grid, s) : launch_wag_t<3, false>(c, P, grid, s);
+    if (c.bits == 2) return resid ? launch_wag_g<2, true>(c, P, grid, s) : launch_wag_g<2, false>(c, P, grid, s);
+    if (c.bits == 3) return resid ? launch_wag_g<3, true>(c, P, grid, s) : launch_wag_g<3, false>(c, P, grid, s);
     return cudaErrorInvalidValue;
 }
 

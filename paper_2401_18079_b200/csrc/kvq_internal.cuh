@@ -59,6 +59,13 @@ struct DevCache {
     uint32_t *gcnt;         // [ntiles][NG][2] counts; bit 31 = overflowed (use CSC/CSR)
     uint16_t *gtmp;         // prefill scratch [cap][NG][2] per-token group counts
     uint32_t *gbase;        // prefill scratch [NG][2] counts of the first tile before
+    // Key ENC table per (KV head, RoPE pair p): channels c1 = 128h + p, c2 = c1 + 64 as fp16x2
+    // words [L, H, code(lo), code(hi), T_0 .. T_{NM-1}, pad] (kvq_prefill.cu): L = smallest
+    // fp16 >= lo_c, H = largest fp16 <= hi_c, T_j = smallest fp16 y with 2(y - z_c) > s_c m_j
+    // in the oracle's fp64 arithmetic (R8), codes of the clamped lo_c / hi_c as fp16 values
+    uint32_t *kenc;         // [H_kv][64][PS]
+    unsigned long long *lb; // prefill look-back words [cap/32 + 1]
+    unsigned *ticket;       // prefill tile ticket
 };
 
 enum ErrBits { kErrKeyCapacity = 1 };
@@ -90,6 +97,25 @@ __host__ __device__ inline int64_t vf_word(int64_t tile, int H_kv, int h, int w,
 // ---- quantization (kvq_quant.cu) ----
 cudaError_t launch_quantize(const DevCache &c, const __half *K, const __half *V, int64_t n0,
                             int64_t T, cudaStream_t s);
+
+// ---- block prefill (kvq_prefill.cu): one CTA per 32-token tile ----
+size_t prefill_smem_bytes(int D, int NG);
+cudaError_t launch_prefill(const DevCache &c, const __half *K, const __half *V, int64_t n0, int64_t T,
+                           unsigned long long *lb, unsigned *ticket, cudaStream_t s);
+inline int kenc_words_per_pair(int bits) { return ((4 + (1 << bits) - 1) + 3) & ~3; }
+
+// ---- fp16 comparator cache (kvq_f16.cu): post-RoPE fp16 K, fp16 V ----
+struct F16Dev {
+    int H_q, H_kv, G, D;
+    int64_t cap, pos_base;
+    const double *theta_tab;   // [64] theta_i = base^(-2i/d), host-computed
+    __half *K, *V;             // [cap][D]
+};
+cudaError_t launch_f16_store(const F16Dev &c, const __half *K, const __half *V, int64_t n0, int64_t T,
+                             cudaStream_t s);
+int f16_auto_splits(const F16Dev &c, int64_t T);
+cudaError_t launch_f16_attend(const F16Dev &c, const __half *q, int64_t pos, int64_t T, float *out,
+                              float *parts, unsigned *tickets, int S, cudaStream_t s);
 
 // ---- attention (kvq_attend.cu) ----
 struct AttendArgs {

@@ -1,0 +1,732 @@
+// kvq_prefill.cu -- QZ, block prefill quantization: one CTA per 32-token tile.
+//
+// The same quantization as T successive appends (kvq_quant.cu, readings R2-R8):
+//   Keys: outlier iff x < lo_c or x > hi_c (R4); code = ENC(clamp(x)).
+//   Values (topk P:1028-1031): two-sided top-k, k = ceil(f D),
+//         ceil(k/2) largest then floor(k/2) smallest of the rest, ties to the lower index,
+//         -0 == +0 (R2, R3); (s, z) from the kept [lo, hi] in fp64, rounded once (R6, R7);
+//         code = ENC(clamp(v)).
+//
+// ENC without per-element fp64 (R8).  The fp64 predicate P_j(y) = [2(y - z) > s m_j] that
+// defines ENC is monotone in y, so for fp16 inputs it is fully described by its threshold
+// T_j = the smallest fp16 value with P_j true, and ENC(y) = #{j : y >= T_j} (an IEEE fp16
+// comparison; -0 == +0 on both sides).  The thresholds are found by a binary search over
+// the fp16 values that evaluates exactly the oracle's fp64 expression:
+//   * Keys: per channel, on the host at create time (kvq_api.cu, kenc table), with the
+//     codes of the clamped values lo_c, hi_c (fp32, not fp16) precomputed the same way;
+//   * Values: per token, by NM lanes of the token's warp after (s_n, z_n) are known.
+// A whole channel pair or token pair is then encoded with fp16x2 compares (HSET2) and
+// fp16x2 adds of the 0/1 results: integer decisions, bit-exact with the oracle.
+//
+// Work of a CTA (tile t, tokens [max(n0, 32t), min(n0 + T, 32t + 32))):
+//   A  Value selection, warp per token: per-lane fp16 max/min over two channel groups, the
+//      (k+1)-th largest group max bounds the outliers from below, so only elements at or
+//      above it (typically ~40 of 4096) are ranked exactly by (value, index); same for the
+//      lower tail.  A bit-by-bit exact selection over all elements handles inputs where the
+//      bound admits too many candidates (ties, tiny D).  Writes (s, z), the CSR records
+//      and the token's Value-outlier bitmask.
+//   B  Keys, warp per KV head, lane = token: pair codes packed straight into the tile's
+//      pair-stream words (coalesced 128-byte stores), outlier bitmask per (token, head).
+//   C  Value codes, warp per KV head, lane = mma A-fragment lane: the head's V slice staged
+//      transposed in shared memory, each field = one token pair of one channel.
+//   D  Key CSC offsets by a decoupled look-back over the tiles of the launch (each CTA takes
+//      its tile from a ticket, so every predecessor has started), CSC records, and the
+//      outlier items of the (tile, head group) buckets in (token, channel) order.
+#include "kvq_internal.cuh"
+
+namespace kvq {
+namespace {
+
+constexpr int PW = 8;              // warps per CTA
+constexpr int PT = PW * 32;
+constexpr int CANDMAX = 256;       // candidates per tail (fast path)
+constexpr uint32_t LB_AGG = 1u, LB_INC = 2u;
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t *>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2 *>(&u); }
+// fp16 bits -> order key (ascending value order), -0 merged with +0
+__device__ __forceinline__ uint32_t okey(uint32_t h) {
+    h &= 0xffffu;
+    uint32_t k = h ^ ((h & 0x8000u) ? 0xffffu : 0x8000u);
+    return k == 0x7fffu ? 0x8000u : k;
+}
+// order key -> fp16 bits (0x8000 -> +0)
+__device__ __forceinline__ uint32_t key2h(uint32_t k) { return k >= 0x8000u ? (k ^ 0x8000u) : (k ^ 0xffffu); }
+
+// counts of a half2 of {0,1} sums -> two small integers
+__device__ __forceinline__ uint32_t h2codes(__half2 c2, int bits) {
+    const uint32_t w = h2u(__hadd2(c2, __float2half2_rn(1024.f)));   // 0x6400 + code per half
+    return (w & 0xfu) | ((w >> (16 - bits)) & (0xfu << bits));
+}
+
+template <int BITS>
+struct PCfg {
+    static constexpr int NM = (1 << BITS) - 1;             // ENC thresholds
+    static constexpr int PS = ((4 + NM) + 3) & ~3;         // kenc words per channel pair
+};
+
+struct PParams {
+    const __half *K, *V;       // chunk rows [T][D]
+    int64_t n0, T;
+    int64_t tile0;
+    int ntile;
+    unsigned long long *lb;    // [ntile] look-back words (zeroed before the launch)
+    unsigned *ticket;          // zeroed before the launch
+};
+
+// Dynamic shared memory layout (bytes), D channels, DW = D/32 mask words per token
+struct PSmem {
+    int DW, NG;
+    size_t kmask, vmask, kcnt, cntK, cntV, posK, posV, tinfo, warp, total;
+    __host__ __device__ PSmem(int D, int NG_) {
+        DW = D / 32; NG = NG_;
+        size_t o = 0;
+        kmask = o; o += (size_t)32 * DW * 4;
+        vmask = o; o += (size_t)32 * DW * 4;
+        kcnt = o;  o += (size_t)32 * (D / 128) * 2;     // Key outliers per (token, head)
+        cntK = o;  o += (size_t)32 * NG * 2;            // per (token, group)
+        cntV = o;  o += (size_t)32 * NG * 2;
+        posK = o;  o += (size_t)32 * NG * 2;            // bucket slot of (token, group)
+        posV = o;  o += (size_t)32 * NG * 2;
+        o = (o + 15) & ~(size_t)15;
+        tinfo = o; o += (size_t)32 * 24 * 2;            // per token: lo, hi, T[15], code lo/hi
+        o = (o + 15) & ~(size_t)15;
+        warp = o;  o += (size_t)PW * 64 * 20 * 4;        // per warp: candidates / V staging
+        total = o;
+    }
+};
+constexpr int TI_LO = 0, TI_HI = 1, TI_CLO = 2, TI_CHI = 3, TI_T = 4;   // tinfo fields (u16)
+
+// ---------------------------------------------------------------- exact selection (slow)
+// Marks in `mask` the `need` elements of `row` that come first in (value desc, index asc)
+// (desc) or (value asc, index asc) order among elements not already in `mask`.  Bit-by-bit
+// search of the order-key threshold, then ties at the threshold in index order.  Element
+// ownership: lane l holds channels 256m + 8l + e.
+__device__ void select_exact(const __half *row, int D, int need, bool desc, uint32_t *mask) {
+    const int lane = threadIdx.x & 31;
+    if (need <= 0) return;
+    const int nch = (D + 255) / 256;
+    auto kv = [&](uint32_t h) { const uint32_t k = okey(h); return desc ? k : 0xffffu - k; };
+    auto count_ge = [&](uint32_t t, bool strict) {
+        int cnt = 0;
+        for (int m = 0; m < nch; ++m) {
+            const int c0 = 256 * m + 8 * lane;
+            if (c0 >= D) continue;
+            const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+            const uint32_t mw = mask[c0 >> 5] >> (c0 & 31);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if ((mw >> e) & 1u) continue;
+                const uint32_t k = kv(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                cnt += strict ? (k > t) : (k >= t);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        return cnt;
+    };
+    uint32_t t = 0;
+    for (int b = 15; b >= 0; --b) {
+        const uint32_t t2 = t | (1u << b);
+        if (count_ge(t2, false) >= need) t = t2;
+    }
+    int take = need - count_ge(t, true);   // ties at t, lowest index first
+    int run = 0;
+    for (int m = 0; m < nch; ++m) {
+        const int c0 = 256 * m + 8 * lane;
+        uint32_t sel = 0, tie = 0;
+        if (c0 < D) {
+            const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+            const uint32_t mw = mask[c0 >> 5] >> (c0 & 31);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if ((mw >> e) & 1u) continue;
+                const uint32_t k = kv(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                sel |= (uint32_t)(k > t) << e;
+                tie |= (uint32_t)(k == t) << e;
+            }
+        }
+        const int nt = __popc(tie);
+        int ex = nt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ex, o);
+            if (lane >= o) ex += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, ex, 31);
+        ex -= nt;
+        int r = run + ex;
+        for (uint32_t x = tie; x; x &= x - 1, ++r)
+            if (r < take) sel |= x & (~x + 1u);
+        run += tot;
+        if (sel) atomicOr(&mask[c0 >> 5], sel << (c0 & 31));
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------------------------------ kernel
+template <int BITS>
+__global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
+    using C = PCfg<BITS>;
+    constexpr int NM = C::NM, PS = C::PS, CM = (1 << BITS) - 1, KWH = 4 * BITS;
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int D = c.D, H = c.H_kv, NG = c.NG, GW = c.GW;
+    const PSmem L(D, NG);
+    const int DW = L.DW;
+    uint32_t *kmask = reinterpret_cast<uint32_t *>(sm + L.kmask);
+    uint32_t *vmask = reinterpret_cast<uint32_t *>(sm + L.vmask);
+    uint16_t *kcnt = reinterpret_cast<uint16_t *>(sm + L.kcnt);
+    uint16_t *cntK = reinterpret_cast<uint16_t *>(sm + L.cntK);
+    uint16_t *cntV = reinterpret_cast<uint16_t *>(sm + L.cntV);
+    uint16_t *posK = reinterpret_cast<uint16_t *>(sm + L.posK);
+    uint16_t *posV = reinterpret_cast<uint16_t *>(sm + L.posV);
+    uint16_t *tinfo = reinterpret_cast<uint16_t *>(sm + L.tinfo);
+    __shared__ uint32_t s_tokbase[33], s_tile, s_kbase, s_gbase[64][2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned char *wsc = sm + L.warp + (size_t)warp * 64 * 20 * 4;
+
+    if (tid == 0) s_tile = atomicAdd(P.ticket, 1u);
+    for (int x = tid; x < 32 * DW; x += PT) { kmask[x] = 0; vmask[x] = 0; }
+    __syncthreads();
+    const int li = (int)s_tile;                       // logical tile of this CTA
+    const int64_t tile = P.tile0 + li;
+    const int64_t nt0 = tile * 32;                    // token of lane 0
+    const int64_t nA = nt0 > P.n0 ? nt0 : P.n0, nB = (nt0 + 32 < P.n0 + P.T) ? nt0 + 32 : P.n0 + P.T;
+    const int jA = (int)(nA - nt0), jB = (int)(nB - nt0);   // valid in-tile tokens [jA, jB)
+    auto krow = [&](int j) { return P.K + (nt0 + j - P.n0) * (int64_t)D; };
+    auto vrow = [&](int j) { return P.V + (nt0 + j - P.n0) * (int64_t)D; };
+    if (tid < NG) {   // existing bucket counts (a chunk may start inside a tile of appended tokens)
+        s_gbase[tid][0] = jA > 0 ? c.gcnt[(tile * NG + tid) * 2] : 0u;
+        s_gbase[tid][1] = jA > 0 ? c.gcnt[(tile * NG + tid) * 2 + 1] : 0u;
+    }
+
+    // ====================================================== A: Value selection (warp/token)
+    {
+        const int k = c.kv, ku = (k + 1) / 2, kl = k / 2;
+        const int nch = (D + 255) / 256;
+        uint32_t *cand = reinterpret_cast<uint32_t *>(wsc);   // [2][CANDMAX]
+        __shared__ int s_nc[PW][2];
+        for (int j = jA + warp; j < jB; j += PW) {
+            const __half *row = vrow(j);
+            uint32_t *vm = vmask + j * DW;
+            // group maxima / minima (fp16 values; 2 groups per lane: even / odd chunks)
+            __half2 mx[2], mn[2];
+            mx[0] = mx[1] = __float2half2_rn(-65504.f);
+            mn[0] = mn[1] = __float2half2_rn(65504.f);
+            bool have[2] = {false, false};
+            for (int m = 0; m < nch; ++m) {
+                const int c0 = 256 * m + 8 * lane;
+                if (c0 >= D) continue;
+                const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+                const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
+                const __half2 b = __hmin2(__hmin2(u2h(u.x), u2h(u.y)), __hmin2(u2h(u.z), u2h(u.w)));
+                mx[m & 1] = __hmax2(mx[m & 1], a);
+                mn[m & 1] = __hmin2(mn[m & 1], b);
+                have[m & 1] = true;
+            }
+            // (need+1)-th largest group max / smallest group min, bit search on order keys
+            uint32_t gk[2], gl[2];
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                gk[g] = have[g] ? okey(h2u(__hmax2(mx[g], __lowhigh2highlow(mx[g])))) : 0u;
+                gl[g] = have[g] ? 0xffffu - okey(h2u(__hmin2(mn[g], __lowhigh2highlow(mn[g])))) : 0u;
+            }
+            auto kth = [&](const uint32_t (&v)[2], int need) {
+                uint32_t t = 0;
+                for (int b = 15; b >= 0; --b) {
+                    const uint32_t t2 = t | (1u << b);
+                    const int n = __popc(__ballot_sync(0xffffffffu, v[0] >= t2)) + __popc(__ballot_sync(0xffffffffu, v[1] >= t2));
+                    if (n >= need) t = t2;
+                }
+                return t;
+            };
+            const uint32_t tau_hi = kth(gk, ku + 1);                // order key
+            const uint32_t tau_lo = 0xffffu - kth(gl, kl + 1);      // order key
+            // candidates: value >= tau_hi (upper), value <= tau_lo (lower)
+            if (lane < 2) s_nc[warp][lane] = 0;
+            __syncwarp();
+            const __half2 th2 = u2h(key2h(tau_hi) * 0x10001u), tl2 = u2h(key2h(tau_lo) * 0x10001u);
+            bool ovf = false;
+            for (int m = 0; m < nch; ++m) {
+                const int c0 = 256 * m + 8 * lane;
+                uint32_t fu = 0, fl = 0;
+                if (c0 < D) {
+                    const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                    // the chunk's max / min first: per-element flags only where a candidate is
+                    const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
+                    const __half2 b = __hmin2(__hmin2(u2h(u.x), u2h(u.y)), __hmin2(u2h(u.z), u2h(u.w)));
+                    if (__hbge2(__hmax2(a, __lowhigh2highlow(a)), th2) || __hble2(__hmin2(b, __lowhigh2highlow(b)), tl2)) {
+#pragma unroll
+                        for (int e2 = 0; e2 < 4; ++e2) {
+                            const uint32_t ge = h2u(__hge2(u2h(w[e2]), th2)), le = h2u(__hle2(u2h(w[e2]), tl2));
+                            fu |= (((ge >> 13) & 1u) | ((ge >> 28) & 2u)) << (2 * e2);
+                            fl |= (((le >> 13) & 1u) | ((le >> 28) & 2u)) << (2 * e2);
+                        }
+                    }
+                }
+                if (__any_sync(0xffffffffu, (fu | fl) != 0u)) {
+                    const int nu = __popc(fu), nl = __popc(fl);
+                    int bu = 0, bl = 0;
+                    if (nu) bu = atomicAdd(&s_nc[warp][0], nu);
+                    if (nl) bl = atomicAdd(&s_nc[warp][1], nl);
+                    if (fu | fl) {
+                        const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+                        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                        for (uint32_t x = fu; x; x &= x - 1) {
+                            const int e = __ffs(x) - 1;
+                            const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                            if (bu < CANDMAX) cand[bu] = (key << 13) | (8191u - (uint32_t)(c0 + e));
+                            ++bu;
+                        }
+                        for (uint32_t x = fl; x; x &= x - 1) {
+                            const int e = __ffs(x) - 1;
+                            const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                            if (bl < CANDMAX) cand[CANDMAX + bl] = ((0xffffu - key) << 13) | (8191u - (uint32_t)(c0 + e));
+                            ++bl;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            const int NU = s_nc[warp][0], NL = s_nc[warp][1];
+            ovf = NU > CANDMAX || NL > CANDMAX || NU < ku + 1 || NL < kl + 1 || tau_lo >= tau_hi;
+            uint32_t lo_h = 0, hi_h = 0;   // fp16 bits of the kept min / max
+            if (!ovf) {
+                // exact ranks among the candidates: rank = #candidates ordered before
+                int hi_idx = -1, lo_idx = -1;
+                for (int i = lane; i < NU; i += 32) {
+                    const uint32_t v = cand[i];
+                    int r = 0;
+                    for (int q = 0; q < NU; ++q) r += cand[q] > v;
+                    const int ch = 8191 - (int)(v & 8191u);
+                    if (r < ku) atomicOr(&vm[ch >> 5], 1u << (ch & 31));
+                    if (r == ku) hi_idx = ch;
+                }
+                for (int i = lane; i < NL; i += 32) {
+                    const uint32_t v = cand[CANDMAX + i];
+                    int r = 0;
+                    for (int q = 0; q < NL; ++q) r += cand[CANDMAX + q] > v;
+                    const int ch = 8191 - (int)(v & 8191u);
+                    if (r < kl) atomicOr(&vm[ch >> 5], 1u << (ch & 31));
+                    if (r == kl) lo_idx = ch;
+                }
+                hi_idx = __reduce_max_sync(0xffffffffu, hi_idx + 1) - 1;
+                lo_idx = __reduce_max_sync(0xffffffffu, lo_idx + 1) - 1;
+                hi_h = __half_as_ushort(row[hi_idx]);
+                lo_h = __half_as_ushort(row[lo_idx]);
+                __syncwarp();
+            } else {
+                // exact selection over all elements, then the kept range (lowest index)
+                for (int x = lane; x < DW; x += 32) vm[x] = 0;
+                __syncwarp();
+                select_exact(row, D, ku, true, vm);
+                select_exact(row, D, kl, false, vm);
+                uint32_t bh = 0, bl2 = 0xffffffffu;   // (key << 16 | 0xffff - idx) max; (key << 16 | idx) min
+                for (int m = 0; m < nch; ++m) {
+                    const int c0 = 256 * m + 8 * lane;
+                    if (c0 >= D) continue;
+                    const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                    const uint32_t mw = vm[c0 >> 5] >> (c0 & 31);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        if ((mw >> e) & 1u) continue;
+                        const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                        bh = max(bh, (key << 16) | (0xffffu - (uint32_t)(c0 + e)));
+                        bl2 = min(bl2, (key << 16) | (uint32_t)(c0 + e));
+                    }
+                }
+                bh = __reduce_max_sync(0xffffffffu, bh);
+                bl2 = __reduce_min_sync(0xffffffffu, bl2);
+                hi_h = __half_as_ushort(row[0xffff - (bh & 0xffffu)]);
+                lo_h = __half_as_ushort(row[bl2 & 0xffffu]);
+            }
+            // (s, z) in fp64, rounded once (R6); ENC thresholds of the token (lanes 0..NM-1)
+            const double lo = (double)__half2float(__ushort_as_half((uint16_t)lo_h));
+            const double hi = (double)__half2float(__ushort_as_half((uint16_t)hi_h));
+            const float s = __double2float_rn(__dsub_rn(hi, lo) / 2.0);
+            const float z = __double2float_rn(__dadd_rn(hi, lo) / 2.0);
+            uint16_t *ti = tinfo + j * 24;
+            if (lane == 0) {
+                c.vsz[nt0 + j] = make_float2(s, z);
+                ti[TI_LO] = (uint16_t)lo_h;
+                ti[TI_HI] = (uint16_t)hi_h;
+            }
+            uint32_t thr = 0x7c00u;   // +inf: never
+            if (lane < NM) {
+                const double mj = c.mids[16 + lane];
+                const double sd = (double)s, zd = (double)z;
+                uint32_t a = 0x0400u, b = 0xfc00u;   // order keys of -65504 .. +inf (sentinel)
+                while (a < b) {
+                    const uint32_t mid = (a + b) >> 1;
+                    const double y = (double)__half2float(__ushort_as_half((uint16_t)key2h(mid)));
+                    if (2.0 * __dsub_rn(y, zd) > __dmul_rn(sd, mj)) b = mid; else a = mid + 1;
+                }
+                thr = key2h(a);
+                ti[TI_T + lane] = (uint16_t)thr;
+            }
+            // codes of lo and hi (item flags of the outliers)
+            const uint32_t klo = okey(lo_h), khi = okey(hi_h), kt = okey(thr);
+            const int clo = __popc(__ballot_sync(0xffffffffu, lane < NM && klo >= kt));
+            const int chi = __popc(__ballot_sync(0xffffffffu, lane < NM && khi >= kt));
+            if (lane == 0) { ti[TI_CLO] = (uint16_t)clo; ti[TI_CHI] = (uint16_t)chi; }
+            __syncwarp();
+            // CSR records of the token's k outliers (ascending channel) and per-group counts
+            if (k > 0) {
+                const int wpl = (DW + 31) / 32;   // mask words per lane (ascending channels)
+                int cnt = 0;
+                for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x) cnt += __popc(vm[x]);
+                int ex = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, ex, o);
+                    if (lane >= o) ex += y;
+                }
+                ex -= cnt;
+                uint32_t *vo = c.vout + (nt0 + j) * (int64_t)k;
+                for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x)
+                    for (uint32_t b = vm[x]; b; b &= b - 1) {
+                        const int ch = 32 * x + __ffs(b) - 1;
+                        vo[ex++] = (uint32_t)ch | ((uint32_t)__half_as_ushort(row[ch]) << 16);
+                    }
+            }
+            for (int g = lane; g < NG; g += 32) {
+                int cnt = 0;
+                for (int x = g * (GW / 32); x < (g + 1) * (GW / 32); ++x) cnt += __popc(vm[x]);
+                cntV[j * NG + g] = (uint16_t)cnt;
+            }
+            __syncwarp();
+        }
+    }
+
+    __syncthreads();   // per-token ENC thresholds of phase A
+    // ================================================ C: Value codes (warp/KV head, mma lanes)
+    {
+        // staging: the head's V slice for 64 channels, transposed [channel][token] fp16,
+        // row stride 20 words (conflict-free for the fragment reads)
+        uint32_t *vs = reinterpret_cast<uint32_t *>(wsc);
+        const int vg = lane >> 2, vt = lane & 3;
+        // per lane: its 4 token pairs (2u, 2u+1), u = vt + 4 * (2 s + r2), r2 = (j % 16) / 8
+        __half2 T2[4][NM], lo2[4], hi2[4];
+        uint32_t vmsk[4];
+#pragma unroll
+        for (int pr = 0; pr < 4; ++pr) {
+            const int ja = 2 * vt + 8 * pr, jb = ja + 1;   // pr = 2 s + r2
+            const uint16_t *ta = tinfo + ja * 24, *tb2 = tinfo + jb * 24;
+            const bool va = ja >= jA && ja < jB, vb = jb >= jA && jb < jB;
+            lo2[pr] = u2h((uint32_t)(va ? ta[TI_LO] : 0) | ((uint32_t)(vb ? tb2[TI_LO] : 0) << 16));
+            hi2[pr] = u2h((uint32_t)(va ? ta[TI_HI] : 0) | ((uint32_t)(vb ? tb2[TI_HI] : 0) << 16));
+#pragma unroll
+            for (int q = 0; q < NM; ++q)
+                T2[pr][q] = u2h((uint32_t)(va ? ta[TI_T + q] : 0x7c00u) | ((uint32_t)(vb ? tb2[TI_T + q] : 0x7c00u) << 16));
+            vmsk[pr] = (va ? (uint32_t)CM : 0u) | (vb ? (uint32_t)CM << BITS : 0u);
+        }
+        for (int h = warp; h < H; h += PW) {
+            uint32_t vw[KWH];
+#pragma unroll
+            for (int w = 0; w < KWH; ++w) vw[w] = 0u;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                __syncwarp();
+                // stage channels 64*half .. +63 of head h: lane = token
+                {
+                    const int j = lane;
+                    const bool valid = j >= jA && j < jB;
+                    uint16_t *vs16 = reinterpret_cast<uint16_t *>(vs);
+#pragma unroll
+                    for (int a = 0; a < 8; ++a) {
+                        uint4 u = make_uint4(0, 0, 0, 0);
+                        if (valid) u = *reinterpret_cast<const uint4 *>(vrow(j) + h * kHeadDim + 64 * half + 8 * a);
+                        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            vs16[(8 * a + e) * 40 + j] = (uint16_t)(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int mt2 = 0; mt2 < 4; ++mt2) {
+                    const int mt = 4 * half + mt2;
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            // field f = (2 mt + s2) * 4 + r: channel 16 mt + g + 8 (r % 2),
+                            // tokens 16 s2 + 2 vt + 8 (r / 2) (+1)
+                            const int cl = 16 * mt2 + vg + 8 * (r & 1);   // channel within the staged 64
+                            const int pr = 2 * s2 + (r >> 1);
+                            const uint32_t x2 = vs[cl * 20 + (2 * vt + 8 * pr) / 2];
+                            __half2 x = __hmax2(__hmin2(u2h(x2), hi2[pr]), lo2[pr]);
+                            __half2 cnt = __hge2(x, T2[pr][0]);
+#pragma unroll
+                            for (int q = 1; q < NM; ++q) cnt = __hadd2(cnt, __hge2(x, T2[pr][q]));
+                            const uint32_t fv = h2codes(cnt, BITS) & vmsk[pr];
+                            const int f = (2 * mt + s2) * 4 + r;
+                            const int bit = f * 2 * BITS, wi = bit >> 5, sh = bit & 31;
+                            vw[wi] |= fv << sh;
+                            if (sh + 2 * BITS > 32) vw[wi + 1] |= fv >> (32 - sh);
+                        }
+                }
+            }
+            // a tile a chunk starts inside already holds codes of appended tokens: OR them in
+#pragma unroll
+            for (int w = 0; w < KWH; ++w) {
+                uint32_t *dst = c.vcodes + vf_word(tile, H, h, w, lane, BITS);
+                *dst = jA > 0 ? (*dst | vw[w]) : vw[w];
+            }
+        }
+    }
+    // ============================================================ B: Keys (warp/KV head)
+    {
+        const uint4 *kenc = reinterpret_cast<const uint4 *>(c.kenc);
+        const int j = lane;
+        const bool valid = j >= jA && j < jB;
+        const __half *row = valid ? krow(j) : nullptr;
+        for (int h = warp; h < H; h += PW) {
+            uint32_t kw[KWH];
+#pragma unroll
+            for (int w = 0; w < KWH; ++w) kw[w] = 0u;
+            uint32_t mw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {   // channels 8a..8a+7 and 64+8a..64+8a+7 of the head
+                uint4 u0 = make_uint4(0, 0, 0, 0), u1 = make_uint4(0, 0, 0, 0);
+                if (valid) {
+                    u0 = *reinterpret_cast<const uint4 *>(row + h * kHeadDim + 8 * a);
+                    u1 = *reinterpret_cast<const uint4 *>(row + h * kHeadDim + 64 + 8 * a);
+                }
+                const uint32_t w0[4] = {u0.x, u0.y, u0.z, u0.w}, w1[4] = {u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int p = 8 * a + e;   // RoPE pair (p, p + 64)
+                    const uint32_t x2 = __byte_perm(w0[e >> 1], w1[e >> 1], (e & 1) ? 0x7632 : 0x5410);
+                    const uint4 *te = kenc + ((size_t)(h * kPairs + p) * PS) / 4;
+                    uint32_t tw[PS];
+#pragma unroll
+                    for (int q = 0; q < PS / 4; ++q) {
+                        const uint4 t4 = __ldg(te + q);
+                        tw[4 * q] = t4.x; tw[4 * q + 1] = t4.y; tw[4 * q + 2] = t4.z; tw[4 * q + 3] = t4.w;
+                    }
+                    const __half2 x = u2h(x2);
+                    const __half2 olo = __hlt2(x, u2h(tw[0])), ohi = __hgt2(x, u2h(tw[1]));
+                    __half2 cnt = __hge2(x, u2h(tw[4]));
+#pragma unroll
+                    for (int q = 1; q < NM; ++q) cnt = __hadd2(cnt, __hge2(x, u2h(tw[4 + q])));
+                    cnt = __hfma2(olo, __hsub2(u2h(tw[2]), cnt), cnt);
+                    cnt = __hfma2(ohi, __hsub2(u2h(tw[3]), cnt), cnt);
+                    const uint32_t pc = h2codes(cnt, BITS);
+                    const int bit = 2 * BITS * p, wi = bit >> 5, sh = bit & 31;
+                    kw[wi] |= pc << sh;
+                    if (sh + 2 * BITS > 32) kw[wi + 1] |= pc >> (32 - sh);
+                    const uint32_t ob = h2u(__hadd2(olo, ohi));
+                    mw[p >> 5] |= ((ob >> 13) & 1u) << (p & 31);
+                    mw[2 + (p >> 5)] |= ((ob >> 29) & 1u) << (p & 31);
+                }
+            }
+            if (valid) {
+#pragma unroll
+                for (int w = 0; w < KWH; ++w) c.kcodes[(tile * c.QW + h * KWH + w) * 32 + j] = kw[w];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) kmask[j * DW + h * 4 + w] = mw[w];
+            }
+            kcnt[j * H + h] = (uint16_t)(valid ? __popc(mw[0]) + __popc(mw[1]) + __popc(mw[2]) + __popc(mw[3]) : 0);
+        }
+    }
+    __syncthreads();
+
+    // ================================ D1: Key-outlier totals, look-back aggregate, counts
+    uint32_t lb_tot = 0, lb_agg = 0;   // warp 0: this lane's token total, the tile aggregate
+    if (warp == 0) {
+        int tot = 0;
+        for (int h = 0; h < H; ++h) tot += kcnt[lane * H + h];
+        int ex = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ex, o);
+            if (lane >= o) ex += y;
+        }
+        lb_agg = (uint32_t)__shfl_sync(0xffffffffu, ex, 31);
+        lb_tot = (uint32_t)tot;
+        s_tokbase[lane] = (uint32_t)(ex - tot);
+        // publish the aggregate now (decoupled look-back: word = flag << 32 | value); the
+        // predecessors are resolved after phase C, when they have most likely published
+        if (lane == 0) {
+            if (li == 0) {
+                s_kbase = c.kptr[nA];   // CSC offset of the chunk's first token (prior appends)
+                atomicExch(&P.lb[0], ((unsigned long long)LB_INC << 32) | (s_kbase + lb_agg));
+            } else {
+                atomicExch(&P.lb[li], ((unsigned long long)LB_AGG << 32) | lb_agg);
+            }
+        }
+    } else if (warp == 1) {
+        // per (token, group) Key-outlier counts
+        for (int g = 0; g < NG; ++g) {
+            int cnt = 0;
+            for (int h = g * (GW / kHeadDim); h < (g + 1) * (GW / kHeadDim); ++h) cnt += kcnt[lane * H + h];
+            cntK[lane * NG + g] = (uint16_t)cnt;
+        }
+    }
+    __syncthreads();
+
+    // ============================ D1b: look-back resolution (warp 0), bucket slots (others)
+    if (warp == 0) {
+        if (li > 0) {
+            uint32_t excl = 0;
+            int jj = li - 1;
+            while (true) {
+                const int q = jj - lane;
+                const unsigned long long v = q >= 0 ? *reinterpret_cast<volatile unsigned long long *>(&P.lb[q])
+                                                    : ((unsigned long long)LB_INC << 32);
+                const uint32_t fl = (uint32_t)(v >> 32);
+                const unsigned inc = __ballot_sync(0xffffffffu, fl == LB_INC);
+                const unsigned notready = __ballot_sync(0xffffffffu, fl == 0u);
+                const int first = inc ? __ffs(inc) - 1 : 32;
+                const unsigned need = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
+                if (notready & need) continue;   // a predecessor in the window has not published
+                uint32_t val = (lane <= first) ? (uint32_t)v : 0u;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                excl += val;
+                if (first < 32) break;
+                jj -= 32;
+            }
+            if (lane == 0) {
+                atomicExch(&P.lb[li], ((unsigned long long)LB_INC << 32) | (excl + lb_agg));
+                s_kbase = excl;
+            }
+        }
+        __syncwarp();
+        // Key CSC column pointers kptr[n+1] of the tile's tokens
+        if (lane >= jA && lane < jB) {
+            const uint32_t end = s_kbase + s_tokbase[lane] + lb_tot;
+            c.kptr[nt0 + lane + 1] = end;
+            if ((int64_t)end > c.kcap) *(volatile int *)c.err |= kErrKeyCapacity;
+        }
+    } else {
+        // bucket slots: exclusive prefix over the tile's tokens per group (warp per group)
+        for (int g = warp - 1; g < NG; g += PW - 1) {
+            const int ck = (lane >= jA && lane < jB) ? cntK[lane * NG + g] : 0;
+            const int cv = (lane >= jA && lane < jB) ? cntV[lane * NG + g] : 0;
+            int ek = ck, ev = cv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int yk = __shfl_up_sync(0xffffffffu, ek, o), yv = __shfl_up_sync(0xffffffffu, ev, o);
+                if (lane >= o) { ek += yk; ev += yv; }
+            }
+            posK[lane * NG + g] = (uint16_t)(ek - ck);
+            posV[lane * NG + g] = (uint16_t)(ev - cv);
+            if (lane == 31) {
+                c.gcnt[(tile * NG + g) * 2] = s_gbase[g][0] + (uint32_t)ek;
+                c.gcnt[(tile * NG + g) * 2 + 1] = s_gbase[g][1] + (uint32_t)ev;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ================================ D2: Key CSC records + Key / Value items (warp/token)
+    {
+        const uint32_t *kenc32 = c.kenc;
+        for (int j = jA + warp; j < jB; j += PW) {
+            const __half *kr = krow(j), *vr = vrow(j);
+            uint32_t tb = s_kbase + s_tokbase[j];   // CSC slot of the token's next head chunk
+            for (int h0 = 0; h0 < H; h0 += 32) {
+                const int h = h0 + lane;
+                const int cnt = h < H ? kcnt[j * H + h] : 0;
+                int ex = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, ex, o);
+                    if (lane >= o) ex += y;
+                }
+                const int hsum = __shfl_sync(0xffffffffu, ex, 31);
+                ex -= cnt;
+                if (cnt) {
+                    uint32_t pos = tb + (uint32_t)ex;
+                    const int g = (h * kHeadDim) / GW;
+                    int r = 0;   // rank inside the (token, group): outliers of earlier heads of the group
+                    for (int h2 = g * (GW / kHeadDim); h2 < h; ++h2) r += kcnt[j * H + h2];
+                    uint32_t bslot = s_gbase[g][0] + posK[j * NG + g] + (uint32_t)r;
+                    uint32_t *dst = c.kit + (tile * NG + g) * (int64_t)c.kcap_g;
+                    for (int w = 0; w < 4; ++w)
+                        for (uint32_t b = kmask[j * DW + h * 4 + w]; b; b &= b - 1) {
+                            const int cc = 32 * w + __ffs(b) - 1, ch = h * kHeadDim + cc;
+                            const uint32_t xh = __half_as_ushort(kr[ch]);
+                            if ((int64_t)pos < c.kcap) c.kout[pos] = (uint32_t)ch | (xh << 16);
+                            ++pos;
+                            // dense code at the outlier: clamp to lo -> code_lo, to hi -> code_hi
+                            const int pp = cc & 63, up = cc >> 6;
+                            const uint32_t *te = kenc32 + (size_t)(h * kPairs + pp) * PS;
+                            const __half2 lo2 = u2h(te[0]);
+                            const __half xv = __ushort_as_half((uint16_t)xh);
+                            const bool below = __hlt(xv, up ? __high2half(lo2) : __low2half(lo2));
+                            const uint32_t cw = h2u(__hadd2(u2h(te[below ? 2 : 3]), __float2half2_rn(1024.f)));
+                            const int code = (int)((up ? cw >> 16 : cw) & 0xfu);
+                            if (bslot < (uint32_t)c.kcap_g)
+                                dst[bslot] = (xh << 16) | ((uint32_t)j << 11) | item_code_flag<BITS>(code) |
+                                             (uint32_t)(ch - g * GW);
+                            ++bslot;
+                        }
+                }
+                tb += (uint32_t)hsum;
+            }
+            // Value items of the token, per group in channel order
+            const uint16_t *ti = tinfo + j * 24;
+            const uint32_t khi = okey(ti[TI_HI]);
+            for (int g = lane; g < NG; g += 32) {
+                uint32_t bslot = s_gbase[g][1] + posV[j * NG + g];
+                uint32_t *dst = c.vit + (tile * NG + g) * (int64_t)c.vcap_g;
+                for (int x = g * (GW / 32); x < (g + 1) * (GW / 32); ++x)
+                    for (uint32_t b = vmask[j * DW + x]; b; b &= b - 1) {
+                        const int ch = 32 * x + __ffs(b) - 1;
+                        const uint32_t xh = __half_as_ushort(vr[ch]);
+                        const int code = okey(xh) >= khi ? ti[TI_CHI] : ti[TI_CLO];
+                        if (bslot < (uint32_t)c.vcap_g)
+                            dst[bslot] = (xh << 16) | ((uint32_t)j << 11) | item_code_flag<BITS>(code) |
+                                         (uint32_t)(ch - g * GW);
+                        ++bslot;
+                    }
+            }
+        }
+    }
+
+}
+
+}  // namespace
+
+size_t prefill_smem_bytes(int D, int NG) { return PSmem(D, NG).total; }
+
+cudaError_t launch_prefill(const DevCache &c, const __half *K, const __half *V, int64_t n0, int64_t T,
+                           unsigned long long *lb, unsigned *ticket, cudaStream_t s) {
+    if (T <= 0) return cudaSuccess;
+    PParams P;
+    P.K = K; P.V = V; P.n0 = n0; P.T = T;
+    P.tile0 = n0 / 32;
+    const int64_t tile1 = (n0 + T - 1) / 32;
+    P.ntile = (int)(tile1 - P.tile0 + 1);
+    P.lb = lb; P.ticket = ticket;
+    cudaError_t e = cudaMemsetAsync(lb, 0, (size_t)P.ntile * 8, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(ticket, 0, 4, s);
+    if (e != cudaSuccess) return e;
+    const size_t smem = prefill_smem_bytes(c.D, c.NG);
+    switch (c.bits) {
+        case 2:
+            cudaFuncSetAttribute(prefill_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            prefill_kernel<2><<<P.ntile, PT, smem, s>>>(c, P);
+            break;
+        case 3:
+            cudaFuncSetAttribute(prefill_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            prefill_kernel<3><<<P.ntile, PT, smem, s>>>(c, P);
+            break;
+        case 4:
+            cudaFuncSetAttribute(prefill_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            prefill_kernel<4><<<P.ntile, PT, smem, s>>>(c, P);
+            break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace kvq

@@ -250,42 +250,40 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
             }
         }
     }
-    // ---- Key outliers bucketed per (tile, attend head group): each thread's channel chunk
-    //      lies in one group (GW % E == 0); slots are reserved per group with one atomic
-    //      (prefill: arbitrary order, sorted afterwards by sort_buckets_kernel; append:
-    //      a single CTA, so slots are in token order already).  count > cap = overflow.
+    // ---- Key outliers bucketed per (tile, attend head group).  The group is taken per record
+    //      from its channel (a thread's channel chunk may straddle two groups, e.g. E = 20
+    //      channels per thread against 256-channel groups at D = 5120); records of a group have
+    //      contiguous ranks (ascending channel order), so a record's slot is the group's base
+    //      plus its rank minus the group's first rank.  count > cap = overflow.
     {
-        __shared__ int gk[64], gbk[64];
-        if (tid < 64) gk[tid] = 0;
+        __shared__ int gk[64], gbk[64], gfirst[64];
+        if (tid < 64) { gk[tid] = 0; gfirst[tid] = 0x7fffffff; }
         __syncthreads();
-        const int myg = cb0 < D ? cb0 / c.GW : 0;
-        int myoff = 0;
-        if (kcnt) myoff = atomicAdd(&gk[myg], kcnt);   // offset of this thread inside the group
+        {
+            int r = krank;
+            for (uint32_t m = kmask; m; m &= m - 1, ++r) {
+                const int g = (cb0 + __ffs(m) - 1) / c.GW;
+                atomicAdd(&gk[g], 1);
+                atomicMin(&gfirst[g], r);
+            }
+        }
         __syncthreads();
-        // thread order inside a group must be channel order: recompute offsets by a
-        // group-local prefix of the per-thread counts (threads of a group are contiguous)
-        (void)myoff;
         if (tid < c.NG) {
             const int tile0 = (int)(n >> 5);
             gbk[tid] = gk[tid] ? (int)atomicAdd(&c.gcnt[((int64_t)tile0 * c.NG + tid) * 2], (uint32_t)gk[tid]) : 0;
         }
         __syncthreads();
-        // group-local exclusive prefix = krank - (rank of the group's first record)
-        __shared__ int gfirst[64];
-        if (tid < 64) gfirst[tid] = 0x7fffffff;
-        __syncthreads();
-        if (kcnt) atomicMin(&gfirst[myg], krank);
-        __syncthreads();
         if (kcnt) {
             const int tile0 = (int)(n >> 5), jj0 = (int)(n & 31);
-            int pos = gbk[myg] + (krank - gfirst[myg]);
-            uint32_t *dst = c.kit + ((int64_t)tile0 * c.NG + myg) * c.kcap_g;
-            for (uint32_t m = kmask; m; m &= m - 1) {
+            int r = krank;
+            for (uint32_t m = kmask; m; m &= m - 1, ++r) {
                 const int ch = cb0 + __ffs(m) - 1;
+                const int g = ch / c.GW;
+                const int pos = gbk[g] + (r - gfirst[g]);
                 if (pos < c.kcap_g)
-                    dst[pos] = ((uint32_t)xk[ch + o16] << 16) | ((uint32_t)jj0 << 11) | item_code_flag<BITS>(kc[ch + o8]) |
-                               (uint32_t)(ch - myg * c.GW);
-                ++pos;
+                    c.kit[((int64_t)tile0 * c.NG + g) * c.kcap_g + pos] =
+                        ((uint32_t)xk[ch + o16] << 16) | ((uint32_t)jj0 << 11) | item_code_flag<BITS>(kc[ch + o8]) |
+                        (uint32_t)(ch - g * c.GW);
             }
         }
     }
@@ -380,25 +378,33 @@ qz_kernel(DevCache c, const __half *__restrict__ Kin, const __half *__restrict__
         int vtot;
         int vr = block_excl_scan<NT>(vcnt, &vtot, sbuf);
         uint32_t *vo = c.vout + n * (int64_t)k;
-        // Value outliers bucketed per (tile, group) as for the Keys
+        // Value outliers bucketed per (tile, group) as for the Keys (group per record)
         __shared__ int gvc[64], gbv[64], gvf[64];
         if (tid < 64) { gvc[tid] = 0; gvf[tid] = 0x7fffffff; }
         __syncthreads();
-        const int myg = cb0 < D ? cb0 / c.GW : 0;
-        if (vcnt) { atomicAdd(&gvc[myg], vcnt); atomicMin(&gvf[myg], vr); }
+        {
+            int r = vr;
+            for (int ch = cb0; ch < cb1; ++ch)
+                if (vflag[ch + o8]) {
+                    const int g = ch / c.GW;
+                    atomicAdd(&gvc[g], 1);
+                    atomicMin(&gvf[g], r);
+                    ++r;
+                }
+        }
         __syncthreads();
         if (tid < c.NG)
             gbv[tid] = gvc[tid] ? (int)atomicAdd(&c.gcnt[((int64_t)(n >> 5) * c.NG + tid) * 2 + 1], (uint32_t)gvc[tid]) : 0;
         __syncthreads();
-        int vpos = vcnt ? gbv[myg] + (vr - gvf[myg]) : 0;
-        uint32_t *vdst = c.vit + ((int64_t)(n >> 5) * c.NG + myg) * c.vcap_g;
         for (int ch = cb0; ch < cb1; ++ch)
             if (vflag[ch + o8]) {
-                vo[vr++] = (uint32_t)ch | ((uint32_t)xv[ch + o16] << 16);
+                const int g = ch / c.GW;
+                const int vpos = gbv[g] + (vr - gvf[g]);
                 if (vpos < c.vcap_g)
-                    vdst[vpos] = ((uint32_t)xv[ch + o16] << 16) | ((uint32_t)(n & 31) << 11) | item_code_flag<BITS>(vc[ch + o8]) |
-                                 (uint32_t)(ch - myg * c.GW);
-                ++vpos;
+                    c.vit[((int64_t)(n >> 5) * c.NG + g) * c.vcap_g + vpos] =
+                        ((uint32_t)xv[ch + o16] << 16) | ((uint32_t)(n & 31) << 11) | item_code_flag<BITS>(vc[ch + o8]) |
+                        (uint32_t)(ch - g * c.GW);
+                vo[vr++] = (uint32_t)ch | ((uint32_t)xv[ch + o16] << 16);
             }
     }
     __syncthreads();

@@ -22,12 +22,15 @@ KVQ_OK, KVQ_EINVAL, KVQ_ESHAPE, KVQ_EEMPTY, KVQ_ECAPACITY, KVQ_EDEVICE, KVQ_ECUD
 _STATUS = {0: "KVQ_OK", 1: "KVQ_EINVAL", 2: "KVQ_ESHAPE", 3: "KVQ_EEMPTY",
            4: "KVQ_ECAPACITY", 5: "KVQ_EDEVICE", 6: "KVQ_ECUDA"}
 KVQ_FLAG_TRUST_DEVICE_PTRS = 1
+KVQ_FLAG_DECODE_PDL = 2
 
 # Every symbol include/kvq.h declares (checked by tests/test_abi.py).
 EXPORTED = ["kvq_cache_create", "kvq_cache_destroy", "kvq_append", "kvq_prefill_quantize",
             "kvq_decode_attend", "kvq_decode_attend_partial", "kvq_merge_partials",
             "kvq_num_tokens", "kvq_reset", "kvq_sync", "kvq_key_outlier_span", "kvq_export",
-            "kvq_get_info", "kvq_set_splits", "kvq_phase_timers", "kvq_last_error", "kvq_version"]
+            "kvq_get_info", "kvq_set_splits", "kvq_phase_timers", "kvq_last_error", "kvq_version",
+            "kvq_f16_cache_create", "kvq_f16_cache_destroy", "kvq_f16_append",
+            "kvq_f16_decode_attend", "kvq_f16_export", "kvq_f16_num_tokens"]
 
 
 class KVQError(RuntimeError):
@@ -89,6 +92,12 @@ def _load() -> ctypes.CDLL:
         "kvq_set_splits": (i32, [vp, i32]),
         "kvq_phase_timers": (i32, [vp, ctypes.POINTER(ctypes.c_uint64)]),
         "kvq_last_error": (ctypes.c_char_p, []),
+        "kvq_f16_cache_create": (i32, [ctypes.POINTER(kvq_config), ctypes.POINTER(vp)]),
+        "kvq_f16_cache_destroy": (None, [vp]),
+        "kvq_f16_append": (i32, [vp, vp, vp, i64, vp]),
+        "kvq_f16_decode_attend": (i32, [vp, vp, i64, vp, vp]),
+        "kvq_f16_export": (i32, [vp, i64, i64, vp, vp]),
+        "kvq_f16_num_tokens": (i64, [vp]),
         "kvq_version": (i32, []),
     }
     for name, (res, args) in sig.items():
@@ -154,10 +163,12 @@ class KVQCache:
                  outlier_ppm: int, capacity_tokens: int, key_cb, val_cb, key_lo, key_hi,
                  key_cb_dec=None, val_cb_dec=None, k_outlier_capacity: int = 0,
                  pos_base: int = 0, rope_theta: float = 10000.0, device: int = 0,
-                 trust_device_ptrs: bool = False):
+                 trust_device_ptrs: bool = False, decode_pdl: bool = False):
+        """decode_pdl: opt in to KVQ_FLAG_DECODE_PDL (kvq.h): the caller guarantees q is
+        complete before each append that precedes an attend on the same stream."""
+        flags = (KVQ_FLAG_TRUST_DEVICE_PTRS if trust_device_ptrs else 0) | (KVQ_FLAG_DECODE_PDL if decode_pdl else 0)
         cfg = kvq_config(n_q_heads, n_kv_heads, head_dim, bits, outlier_ppm, capacity_tokens,
-                         k_outlier_capacity, pos_base, rope_theta, device,
-                         KVQ_FLAG_TRUST_DEVICE_PTRS if trust_device_ptrs else 0)
+                         k_outlier_capacity, pos_base, rope_theta, device, flags)
         keep = [_f32(key_cb), None if key_cb_dec is None else _f32(key_cb_dec), _f32(val_cb),
                 None if val_cb_dec is None else _f32(val_cb_dec), _f32(key_lo), _f32(key_hi)]
 
@@ -253,6 +264,51 @@ class KVQCache:
         out["vidx"] = out["vidx"][:, :kv]
         out["vval"] = out["vval"][:, :kv]
         return out
+
+
+class F16Cache:
+    """The fp16 comparator cache (kvq_f16_*): post-RoPE fp16 Keys, fp16 Values (C3's fp16 arm)."""
+
+    def __init__(self, *, n_q_heads: int, n_kv_heads: int, head_dim: int = 128, capacity_tokens: int,
+                 pos_base: int = 0, rope_theta: float = 10000.0, device: int = 0,
+                 trust_device_ptrs: bool = False):
+        cfg = kvq_config(n_q_heads, n_kv_heads, head_dim, 16, 0, capacity_tokens, 0, pos_base,
+                         rope_theta, device, KVQ_FLAG_TRUST_DEVICE_PTRS if trust_device_ptrs else 0)
+        h = ctypes.c_void_p()
+        _check(_lib.kvq_f16_cache_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self._h = h
+        self.D = n_kv_heads * head_dim
+        self.H_q = n_q_heads
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.kvq_f16_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def append(self, K, V, stream=None):
+        T = int(K.shape[0]) if K.ndim == 2 else 1
+        _check(_lib.kvq_f16_append(self._h, _ptr(K), _ptr(V), T, _stream(stream)))
+
+    def attend(self, q, pos: int, out, stream=None):
+        _check(_lib.kvq_f16_decode_attend(self._h, _ptr(q), int(pos), _ptr(out), _stream(stream)))
+        return out
+
+    @property
+    def num_tokens(self) -> int:
+        return int(_lib.kvq_f16_num_tokens(self._h))
+
+    def export(self, t0: int = 0, t1: Optional[int] = None):
+        t1 = self.num_tokens if t1 is None else t1
+        k = np.zeros((t1 - t0, self.D), np.uint16)
+        v = np.zeros((t1 - t0, self.D), np.uint16)
+        _check(_lib.kvq_f16_export(self._h, t0, t1, k.ctypes.data, v.ctypes.data))
+        return k, v
 
 
 def merge_partials(parts, out, device: int = 0, stream=None):

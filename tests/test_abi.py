@@ -24,7 +24,7 @@ def kvq():
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "kvq.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(kvq_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(kvq_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_north_star_calls():

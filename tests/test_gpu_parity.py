@@ -3,8 +3,8 @@
 Bars (north_star; DESIGN.md "Tolerances"):
   * packed codes, outlier indices / values, CSC pointers, per-token (s, z): bit-exact
     (the integer decisions are taken in fp64 on both sides, reading R8);
-  * attention output: per query head ||o_gpu - o_ref||_inf / ||o_ref||_inf <= 2e-3
-    (fp16 products with fp32 accumulation, derived in DESIGN.md).
+  * attention output: per query head ||o_gpu - o_ref||_inf / ||o_ref||_inf <= 2e-3, median
+    over heads <= 5e-4 (north_star's bar for fp16 products, reading R24, gpu_common).
 """
 import numpy as np
 import pytest
@@ -12,13 +12,13 @@ import pytest
 import oracle as O
 from kvq_synth import gen
 
-from .gpu_common import (assert_cache_equal, make_cache, merged_partial_to_natural,
-                         rel_err_per_head, setup_layer)
+from .gpu_common import (TOL_ATTEND, TOL_ATTEND_MEDIAN, assert_cache_equal, make_cache,
+                         merged_partial_to_natural, rel_err_per_head, setup_layer)
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-TOL = 2e-3
+TOL = TOL_ATTEND
 
 
 @pytest.fixture(scope="module")
@@ -42,7 +42,8 @@ def oracle_attend(cal, cache, q, pos, H_q, H_kv, pos_base=0):
 # -------------------------------------------------------------- quantization (T1) --
 @pytest.mark.parametrize("H,bits,ppm,T", [(1, 4, 10_000, 77), (2, 3, 10_000, 100),
                                           (2, 2, 10_000, 65), (8, 3, 10_000, 96),
-                                          (4, 4, 1_000, 33), (1, 3, 0, 40)])
+                                          (4, 4, 1_000, 33), (1, 3, 0, 40),
+                                          (40, 3, 10_000, 70), (5, 2, 10_000, 45)])
 def test_prefill_quantization_bit_exact(kvq, H, bits, ppm, T):
     cal, K, V = setup_layer(1, 0, H, H, bits, ppm, T)
     ref = oracle_cache(cal, K, V, ppm)
@@ -70,8 +71,10 @@ def test_append_then_prefill_mixed(kvq, bits):
     assert_cache_equal(c.export(31, 66), ref, 31, 66)
 
 
-def test_adversarial_quantization_inputs(kvq):
-    """ties, -0/+0, all-equal tokens, values on midpoints and on thresholds."""
+@pytest.mark.parametrize("fill", ["mixed", "prefill"])
+def test_adversarial_quantization_inputs(kvq, fill):
+    """ties, -0/+0, all-equal tokens, values on midpoints and on thresholds (the prefill
+    kernel's exact-selection fallback and its ENC thresholds at midpoints)."""
     H, bits, ppm = 1, 3, 20_000
     D = 128
     cb = np.array([-1.0, -0.5, -0.25, 0.0, 0.25, 0.5, 0.75, 1.0], np.float32)
@@ -94,9 +97,12 @@ def test_adversarial_quantization_inputs(kvq):
     ref = oracle_cache(cal, K, V, ppm)
     c = make_cache(kvq, cal, H, H, bits, ppm, capacity=16)
     Kt, Vt = torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda()
-    c.prefill(Kt[:3], Vt[:3])
-    for n in range(3, K.shape[0]):
-        c.append(Kt[n], Vt[n])
+    if fill == "prefill":
+        c.prefill(Kt, Vt)
+    else:
+        c.prefill(Kt[:3], Vt[:3])
+        for n in range(3, K.shape[0]):
+            c.append(Kt[n], Vt[n])
     c.sync()
     assert_cache_equal(c.export(), ref)
 
@@ -120,7 +126,9 @@ def test_host_buffers_are_staged(kvq):
 # ----------------------------------------------------------------- attention (T2) --
 @pytest.mark.parametrize("H_q,H_kv,bits,T", [(1, 1, 4, 4096), (8, 8, 3, 1000), (2, 2, 4, 333),
                                              (8, 8, 2, 517), (8, 2, 3, 300), (4, 1, 3, 129),
-                                             (16, 16, 3, 700), (32, 8, 3, 257)])
+                                             (16, 16, 3, 700), (32, 8, 3, 257),
+                                             (8, 4, 3, 301), (16, 8, 2, 400), (32, 16, 3, 96),
+                                             (40, 40, 3, 130), (32, 8, 2, 333)])
 def test_attend_matches_oracle(kvq, H_q, H_kv, bits, T):
     ppm = 10_000
     cal, K, V = setup_layer(4, 0, H_q, H_kv, bits, ppm, T)
@@ -134,6 +142,7 @@ def test_attend_matches_oracle(kvq, H_q, H_kv, bits, T):
         torch.cuda.synchronize()
         err = rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, pos, H_q, H_kv))
         assert err.max() < TOL, err
+        assert np.median(err) < TOL_ATTEND_MEDIAN, err
 
 
 @pytest.mark.parametrize("H_q,H_kv,bits,T", [(8, 8, 3, 1000), (4, 1, 3, 129), (2, 2, 4, 333),
@@ -169,20 +178,26 @@ def test_attend_independent_of_split_count(kvq, splits):
     assert rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, T, H, H)).max() < TOL
 
 
-def test_long_positions_exact_angles(kvq):
-    """pos_base near 10M: RoPE angles must be reduced exactly (reading R12)."""
-    H, bits, ppm, T = 2, 3, 10_000, 200
-    base = 9_999_000
-    cal, K, V = setup_layer(6, 0, H, H, bits, ppm, T)
+@pytest.mark.parametrize("H_q,H_kv,bits,base", [(2, 2, 3, 9_999_000), (8, 8, 3, 9_990_017),
+                                                (32, 8, 3, 9_990_000), (8, 4, 3, 9_999_500),
+                                                (8, 8, 2, 8_750_000), (32, 8, 2, 8_750_000)])
+def test_long_positions_exact_angles(kvq, H_q, H_kv, bits, base):
+    """pos_base near 10M (C5 shards start at 8.75M for P = 8): RoPE angles must be reduced
+    exactly (reading R12) in every attend kernel -- the two-halves kernel (H = 2), the MHA
+    warp-autonomous kernel (H = 8; its per-CTA fp64 anchors and the per-warp fp64 rotation
+    recurrence over tiles), the GQA kernel (32/8) and G = 2."""
+    ppm, T = 10_000, 600
+    cal, K, V = setup_layer(6, 0, H_q, H_kv, bits, ppm, T)
     ref = oracle_cache(cal, K, V, ppm)
-    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=T, pos_base=base)
+    c = make_cache(kvq, cal, H_q, H_kv, bits, ppm, capacity=T, pos_base=base)
     c.prefill(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
-    q = gen.gen_queries(6, 0, H, H, 128)[0]
-    o = torch.zeros((H, 128), dtype=torch.float32, device="cuda")
-    c.attend(torch.from_numpy(q).cuda(), base + T, o)
-    torch.cuda.synchronize()
-    err = rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, base + T, H, H, pos_base=base))
-    assert err.max() < TOL, err
+    for k, pos in enumerate((base + T - 1, base + T + 123_457)):
+        q = gen.gen_queries(6 + k, 0, H_q, H_kv, 128)[0]
+        o = torch.zeros((H_q, 128), dtype=torch.float32, device="cuda")
+        c.attend(torch.from_numpy(q).cuda(), pos, o)
+        torch.cuda.synchronize()
+        err = rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, pos, H_q, H_kv, pos_base=base))
+        assert err.max() < TOL, err
 
 
 def test_sharded_partials_merge_to_unsharded(kvq):
@@ -295,3 +310,97 @@ def test_attend_concentrated_outliers(kvq, H_q, H_kv, fill):
     torch.cuda.synchronize()
     err = rel_err_per_head(o.cpu().numpy(), oracle_attend(cal, ref, q, T, H_q, H_kv))
     assert err.max() < TOL, err
+
+
+# --------------------------------------------------- degenerate / extreme inputs (T2) --
+def _extreme_layer(seed, H_q, H_kv, bits, ppm, T, kind):
+    cal, K, V = setup_layer(seed, 0, H_q, H_kv, bits, ppm, T)
+    K = K.astype(np.float32)
+    V = V.astype(np.float32)
+    D = H_kv * 128
+    rng = np.random.default_rng(seed)
+    if kind == "flat_values":
+        # tokens whose Value vector is constant: kept range lo == hi, s_n = 0, every code 0
+        # (reading R7); with ppm = 0 there are no Value outliers at all
+        for n in rng.choice(T, size=T // 3, replace=False):
+            V[n, :] = np.float32(rng.normal())
+        V[5, :] = 0.0
+    elif kind == "huge_value_outliers":
+        for n in range(0, T, 3):
+            ch = rng.choice(D, size=3, replace=False)
+            V[n, ch] = np.array([65504.0, -65504.0, 60000.0])[: len(ch)]
+    elif kind == "huge_key_outliers":
+        # fp16 Key outliers near +-65504 in many tokens; the score terms they produce exceed
+        # 2^15 log2 units (the attend kernels' fixed-point Key-outlier sums must not wrap)
+        for n in range(0, T, 4):
+            ch = rng.choice(D, size=4, replace=False)
+            K[n, ch] = np.array([65504.0, -65504.0, 65000.0, -60000.0])
+    return cal, K.astype(np.float16), V.astype(np.float16)
+
+
+@pytest.mark.parametrize("H_q,H_kv,bits", [(8, 8, 3), (32, 8, 3), (2, 2, 4), (8, 8, 2)])
+@pytest.mark.parametrize("kind,ppm", [("flat_values", 0), ("flat_values", 10_000),
+                                      ("huge_value_outliers", 10_000),
+                                      ("huge_key_outliers", 10_000)])
+def test_attend_extreme_inputs(kvq, H_q, H_kv, bits, kind, ppm):
+    """Attention (not only codes) on the method's degenerate and extreme cases: s_n = 0
+    tokens, ppm = 0, fp16 Key and Value outliers at +-65504.
+
+    The flat-value construction (a third of the tokens carry a constant random Value vector,
+    so |o| is an average of many O(1) constants and small against the inputs) is the hardest
+    case for the fp16 products' error budget; the CPU emulation of that
+    arithmetic (scripts/prec_emul.py) reproduces the GPU's error on these inputs."""
+    T = 161
+    cal, K, V = _extreme_layer(31, H_q, H_kv, bits, ppm, T, kind)
+    ref = oracle_cache(cal, K, V, ppm)
+    c = make_cache(kvq, cal, H_q, H_kv, bits, ppm, capacity=T + 8)
+    c.prefill(torch.from_numpy(K[:100]).cuda(), torch.from_numpy(V[:100]).cuda())
+    for n in range(100, T):
+        c.append(torch.from_numpy(K[n]).cuda(), torch.from_numpy(V[n]).cuda())
+    c.sync()
+    assert_cache_equal(c.export(), ref)
+    for k, pos in enumerate((T - 1, T + 77)):
+        q = gen.gen_queries(32 + k, 0, H_q, H_kv, 128)[0]
+        o = torch.zeros((H_q, 128), dtype=torch.float32, device="cuda")
+        c.attend(torch.from_numpy(q).cuda(), pos, o)
+        torch.cuda.synchronize()
+        exp = oracle_attend(cal, ref, q, pos, H_q, H_kv)
+        assert np.all(np.isfinite(o.cpu().numpy()))
+        err = rel_err_per_head(o.cpu().numpy(), exp)
+        assert err.max() < TOL, err
+
+
+@pytest.mark.parametrize("H_q,H_kv,bits", [(8, 8, 3), (32, 8, 3), (8, 8, 2), (2, 2, 4)])
+def test_append_then_attend_sees_new_token_pdl(kvq, H_q, H_kv, bits):
+    """Decode order with programmatic dependent launch (KVQ_FLAG_DECODE_PDL): each attend is
+    enqueued right after the append of the token it must see, with no host sync, across the
+    tile boundaries T = 64 and 96 (T = 0 and 31 mod 32).  The appended token is made the
+    dominant score (a Key outlier aligned with q at the same position, where q~.k~ = q.k),
+    so an attend that missed it would be off by O(1)."""
+    ppm, T0, T1 = 10_000, 62, 98
+    cal, K, V = setup_layer(41, 0, H_q, H_kv, bits, ppm, T1)
+    G = H_q // H_kv
+    qs = gen.gen_queries(42, 0, H_q, H_kv, 128, n=T1 - T0)
+    K = K.astype(np.float32)
+    for n in range(T0, T1):
+        q = qs[n - T0].astype(np.float32)
+        for h in range(H_kv):
+            qh = q[h * G:(h + 1) * G].sum(axis=0)
+            c0 = int(np.argmax(np.abs(qh)))
+            K[n, h * 128 + c0] = 3000.0 * np.sign(qh[c0])
+    K = K.astype(np.float16)
+    c = make_cache(kvq, cal, H_q, H_kv, bits, ppm, capacity=T1 + 8, decode_pdl=True)
+    Kt, Vt = torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda()
+    c.prefill(Kt[:T0], Vt[:T0])
+    qt = torch.from_numpy(qs).cuda()
+    outs = torch.zeros((T1 - T0, H_q, 128), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    for n in range(T0, T1):
+        c.append(Kt[n], Vt[n])
+        c.attend(qt[n - T0], n, outs[n - T0])
+    torch.cuda.synchronize()
+    for n in range(T0, T1):
+        pref = O.prefill(K[:n + 1], V[:n + 1], cal["key_lo"], cal["key_hi"], cal["cbK"], cal["cbV"], ppm)
+        exp = oracle_attend(cal, pref, qs[n - T0], n, H_q, H_kv)
+        err = rel_err_per_head(outs[n - T0].cpu().numpy(), exp)
+        assert err.max() < TOL, (n, err)
