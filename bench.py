@@ -245,29 +245,36 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------ our arm --
 def graph_replay_times(launch_all, n_launch, stream, reps):
-    """Capture `launch_all()` (n_launch attend launches over distinct caches) in one CUDA
-    graph and replay it `reps` times, each replay bracketed by CUDA events on the capture
-    stream.  Returns per-launch times in ms (one per replay) and whether a graph was used
-    (eager event timing if capture is not possible)."""
+    """Capture `launch_all(s)` (n_launch attend launches over distinct caches, issued on stream
+    s) in one CUDA graph on a side stream and replay it `reps` times, each replay bracketed by
+    CUDA events on the replay stream.  Returns per-launch times in ms (one per replay) and
+    whether a graph was used (eager event timing on `stream` if capture is not possible)."""
     import torch
     per = []
     graph = None
+    side = torch.cuda.Stream()
     try:
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            launch_all()
+        # relaxed: the library's host-side checks (pointer attributes, function attributes) are
+        # not stream work
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=side, capture_error_mode="relaxed"):
+            launch_all(side)
         graph = g
-    except Exception:
+    except Exception as ex:
         graph = None
+        graph_replay_times.error = str(ex)[:200]
     torch.cuda.synchronize()
+    rs = side if graph is not None else stream
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        if graph is not None:
-            graph.replay()
-        else:
-            launch_all()
-        b.record(stream)
+        with torch.cuda.stream(rs):
+            a.record(rs)
+            if graph is not None:
+                graph.replay()
+            else:
+                launch_all(rs)
+            b.record(rs)
         b.synchronize()
         per.append(a.elapsed_time(b) / n_launch)
     return per, graph is not None
@@ -320,14 +327,16 @@ def compare_arm(kvq, gen, calib, accounting, wname, T, n_layers, dev, reps, peak
         gen.gen_keys(0, 0, 2048, w.D, stream=gen.STREAM_CAL_K),
         gen.gen_values(0, 0, 2048, w.D, stream=gen.STREAM_CAL_V), w.bits, w.ppm, qnorm=w.qnorm)
     caches = build_caches(kvq, gen, w, cal, n_layers, T, 0, T + 8, dev, 5000, 0, fp16=fp16)
-    q = (torch.randn((n_layers, w.H_q, w.d), device=dev) * 0.5).half()
+    gq = torch.Generator(device=dev)
+    gq.manual_seed(4321)
+    q = (torch.randn((n_layers, w.H_q, w.d), generator=gq, device=dev) * 0.5).half()
     o = torch.zeros((n_layers, w.H_q, w.d), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def launch_all():
+    def launch_all(st):
         for l in range(n_layers):
-            caches[l].attend(q[l], T, o[l], stream)
-    launch_all()
+            caches[l].attend(q[l], T, o[l], st)
+    launch_all(stream)
     per, graphed = graph_replay_times(launch_all, n_layers, stream, reps)
     st = stats(per)
     if fp16:
@@ -475,13 +484,13 @@ def run_ours(args):
     pos = st["pos"]
     qatt = qs[0]
 
-    def launch_all():
+    def launch_all(st):
         for i, c in enumerate(caches):
             if world == 1:
-                c.attend(qatt[i % L_res], pos, o[i % L_res], stream)
+                c.attend(qatt[i % L_res], pos, o[i % L_res], st)
             else:
-                c.attend_partial(qatt[i % L_res], pos, part[i % L_res], stream)
-    launch_all()
+                c.attend_partial(qatt[i % L_res], pos, part[i % L_res], st)
+    launch_all(stream)
     reps = max(args.steps, int(np.ceil(0.5 / max(1e-4, L_res * ncopy * 3e-4))), 20)
     per, graphed = graph_replay_times(launch_all, len(caches), stream, min(reps, 400))
     att = stats(per)
@@ -553,10 +562,10 @@ def run_ours(args):
             rc = build_caches(kvq, gen, w, cal32, nres, min(n_local, 1 << 17), 0, 1 << 17, dev, 7000, 0)
             qr = qs[0]
 
-            def launch_r():
+            def launch_r(st):
                 for i, c in enumerate(rc):
-                    c.attend(qr[i % L_res], 1 << 17, o[i % L_res], stream)
-            launch_r()
+                    c.attend(qr[i % L_res], 1 << 17, o[i % L_res], st)
+            launch_r(stream)
             pr, _ = graph_replay_times(launch_r, len(rc), stream, 20)
             resid = {"attend_us_per_layer": stats(pr)["median"] * 1e3, "context": min(n_local, 1 << 17),
                      "note": "fp32 k-means codebooks (decode codebook not fp16-exact): second V table "
@@ -598,7 +607,8 @@ def run_ours(args):
             "attend_us_per_layer_p10_p90": [att["p10"] * 1e3, att["p90"] * 1e3],
             "attend_timing": ("CUDA graph of %d attend launches (distinct caches), %d replays, "
                               "per-launch median" % (len(caches), att["n"])) if graphed else
-                             "eager launches, CUDA events (graph capture unavailable)",
+                             ("eager launches, CUDA events (graph capture unavailable: %s)"
+                              % getattr(graph_replay_times, "error", "?")),
             "attend_us_per_step": att_ms * 1e3 * w.n_layers,
             "hbm_gbs_step": bytes_att * w.n_layers / (ms_per_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

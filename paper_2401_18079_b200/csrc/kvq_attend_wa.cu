@@ -91,6 +91,12 @@ __device__ __forceinline__ float warp_max_redux(float v) {
     u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
     return __uint_as_float(u);
 }
+// x mod 2 pi into [-pi, pi] in fp64 (x up to ~1e8: the fp64 product and the 2 pi constant err
+// by < 1e-8 rad there)
+__device__ __forceinline__ double red2pi(double x) {
+    constexpr double kTwoPi = 6.283185307179586476925, kInv2Pi = 0.15915494309189533577;
+    return fma(-kTwoPi, rint(x * kInv2Pi), x);
+}
 __device__ __forceinline__ float pow2i(int k) {
     k = max(-126, min(127, k));
     return __int_as_float((k + 127) << 23);
@@ -136,7 +142,7 @@ struct WCfg {
     static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
     static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
     static constexpr size_t t1h = 0;
-    static constexpr size_t t1f = (size_t)kPairs * 32 * 8;    // cis(j th_i) fp32 [i][j]
+    static constexpr size_t t1f = 0;   // (round 2: token angles from MUFU sin/cos, no table)
     // per warp: K words of the tile (cp.async target), K-outlier fixed-point terms (then p),
     // V-outlier fixed-point sums, anchors (fp16 rotation pairs, fp32)
     static constexpr size_t w_kst = (size_t)WH * KWH * 32 * 4;
@@ -293,41 +299,30 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     }
 
     // ---------------------------------------------------------------- prologue (a1)
-    // theta_i and the large-argument angles once per CTA (64 threads): cis(pos theta_i) for the
-    // query, cis((pos_base + 32 t_begin) theta_i) for the CTA's first tile (R11, R12)
+    // theta_i and cis(pos theta_i) for the query once per CTA (64 threads, exact fp64 angles,
+    // R11, R12)
     if (tid < 64) {
         const int i = tid;
         const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
         th64[i] = th;
         double s, co;
-        sincos((double)(NSTREAM * kTileTokens) * th, &s, &co);
-        rot[i] = make_double2(co, s);
         sincos((double)P.pos * th, &s, &co);
         qcis[i] = make_double2(co, s);
-        sincos((double)(c.pos_base + (int64_t)t_begin * kTileTokens) * th, &s, &co);
-        cbase[i] = make_double2(co, s);
     }
     __syncthreads();
-    for (int x = tid; x < kPairs * 32; x += NTHR) {
-        const int i = x >> 5, j = x & 31;
-        const double th = th64[i];
-        double s, co;
-        sincos((double)j * th, &s, &co);
-        t1f[x] = make_float2((float)co, (float)s);
-    }
-    // this warp's anchors cis((pos_base + 32 t_first) th_i), fp64 state in registers (pairs
-    // lane and lane + 32), advanced per tile
-    double2 anc64[2];
+    // Token angles.  Per warp and tile the anchor angle a_i = (pos_base + 32 t + 16) th_i,
+    // reduced mod 2 pi in fp64 (register state, pairs lane and lane + 32, advanced per tile by
+    // the stream stride), is published as (a_i, th_i) fp32; token j's angle is then
+    // a_i + (j - 16) th_i (|.| < pi + 16) in fp32 and cis of it comes from the MUFU sin/cos
+    // (abs error ~1e-6, far below the fp16 rounding of the factors).
+    double ang64[2], step64[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         const int i = lane + 32 * k;
-        // cis((pos_base + 32 t_first) th_i) = cis(the CTA's first tile) x cis(32 (t_first - t_begin) th_i)
-        double sr, cr;
-        sincos((double)((t_first - t_begin) * kTileTokens) * th64[i], &sr, &cr);
-        const double2 b0 = cbase[i];
-        const double co = b0.x * cr - b0.y * sr, s = b0.x * sr + b0.y * cr;
-        anc64[k] = make_double2(co, s);
-        anc32[i] = make_float2((float)co, (float)s);
+        const double th = th64[i];
+        ang64[k] = red2pi((double)(c.pos_base + (int64_t)t_first * kTileTokens + 16) * th);
+        step64[k] = red2pi((double)(NSTREAM * kTileTokens) * th);
+        anc32[i] = make_float2((float)ang64[k], (float)th);
     }
     for (int x = lane; x < WH * 32; x += 32) { kfix[x] = 0; kbig[x] = 0.f; }
     for (int x = tid; x < HG * kHeadDim; x += NTHR) {
@@ -440,13 +435,10 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         m_run[h] = -CUDART_INF_F; l_lane[h] = 0.f; z_lane[h] = 0.f;
         acc[h][0] = acc[h][1] = acc[h][2] = acc[h][3] = 0.f;
     }
-    // fp32 rotation cis(n' th_i) of token j = anchor(i) x cis(j th_i)
+    // fp32 rotation cis(n' th_i) of token j of the tile: anchor angle + (j - 16) th_i
     auto rot32 = [&](int i, int j, float &co, float &si) {
         const float2 a = anc32[i];
-        const float ax = a.x, ay = a.y;
-        const float2 tt = t1f[i * 32 + j];
-        co = ax * tt.x - ay * tt.y;
-        si = ax * tt.y + ay * tt.x;
+        __sincosf(fmaf((float)(j - 16), a.y, a.x), &si, &co);
     };
     auto rot16 = [&](int i) -> uint32_t {
         float co, si;
@@ -754,14 +746,12 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
 #pragma unroll
         for (int h = 0; h < WH; ++h) { kfix[h * 32 + lane] = 0; kbig[h * 32 + lane] = 0.f; }   // p read: done
 
-        // advance the anchors by NSTREAM tiles (fp64 complex rotation)
+        // advance the anchor angles by NSTREAM tiles (fp64, reduced mod 2 pi)
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const int i = lane + 32 * k;
-            const double2 a = anc64[k], r = rot[i];
-            const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
-            anc64[k] = b;
-            anc32[i] = make_float2((float)b.x, (float)b.y);
+            ang64[k] = red2pi(ang64[k] + step64[k]);
+            anc32[i].x = (float)ang64[k];
         }
         cnt_k = ncnt_k;
         cnt_v = ncnt_v;
@@ -897,12 +887,13 @@ cudaError_t launch_wa_r(const DevCache &c, const WParams &P, int grid, cudaStrea
 //       and the mma accumulators persist across tiles (rescaled per head column when the
 //       running max or the weight exponent grows);
 //   a3/a6 every outlier item corrects all G heads.
-constexpr int NSG = 16;    // tile streams (= warps) per GQA CTA
+constexpr int NSG = 16;    // tile streams (= warps) per GQA CTA (14 with the fp32-codebook
+                           // second V table, which needs the shared memory of two warps)
 
 template <int BITS, bool RESID, int G>
 struct GCfg {
     static_assert(G <= 4, "hi/lo weight columns: 2 G <= 8 mma columns");
-    static constexpr int NWARP = NSG;
+    static constexpr int NWARP = (RESID && BITS == 3 && G == 4) ? 14 : NSG;
     static constexpr int NTHR = NWARP * 32;
     static constexpr int IPL = 4;
     static constexpr int NE = 1 << (2 * BITS);
@@ -913,11 +904,11 @@ struct GCfg {
     static constexpr size_t klut = (size_t)G * kPairs * NE * 4;   // [i][pair code][G]
     static constexpr size_t hlut = (size_t)G * HMAX * NE * 8;
     static constexpr size_t t1h = 0;
-    static constexpr size_t t1f = (size_t)kPairs * 32 * 8;
+    static constexpr size_t t1f = 0;   // token angles from MUFU sin/cos (as the MHA kernel)
     // per warp: K words (cp.async target), K-outlier terms (then p) [G][32], V-outlier sums
     // fp32 [G][128], anchors
     static constexpr size_t w_kst = (size_t)KWH * 32 * 4;
-    static constexpr size_t w_bytes = w_kst + G * 32 * 8 + G * kHeadDim * 4 + 64 * 8;
+    static constexpr size_t w_bytes = w_kst + G * 32 * 4 + G * kHeadDim * 4 * 2 + 64 * 8;
     static constexpr int KCH = KWH / 4;
     static constexpr size_t small = G * kHeadDim * 4 /* qs */ + 64 * 16 /* rot */
         + kHeadDim * 4 * 2 /* ks, kz */ + 64 * 4 /* cb */ + G * 64 * 4 /* bound */
@@ -985,9 +976,15 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
 
     unsigned char *wp = wbase + warp * C::w_bytes;
     uint32_t *kst = reinterpret_cast<uint32_t *>(wp); wp += C::w_kst;
-    unsigned long long *kfix = reinterpret_cast<unsigned long long *>(wp); wp += G * 32 * 8;
+    int *kfix = reinterpret_cast<int *>(wp); wp += G * 32 * 4;
     float *ps = reinterpret_cast<float *>(kfix);
     float *osp = reinterpret_cast<float *>(wp); wp += G * kHeadDim * 4;
+    // Value-outlier sums of the tile in fixed point (native shared integer atomics; sm_100a
+    // has no native shared fp32 add), folded into osp at the end of the tile; during the K
+    // phase the same words hold the fp32 side sums of the Key-outlier terms too large for
+    // the 32-bit fixed point (kfix_add32)
+    int *vfix = reinterpret_cast<int *>(wp); wp += G * kHeadDim * 4;
+    float *kbig = reinterpret_cast<float *>(vfix);
     float2 *anc32 = reinterpret_cast<float2 *>(wp);
 
     const int t_first = t_begin + warp;
@@ -1037,35 +1034,23 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
         th64[i] = th;
         double s, co;
-        sincos((double)(NSG * kTileTokens) * th, &s, &co);
-        rot[i] = make_double2(co, s);
         sincos((double)P.pos * th, &s, &co);
         qcis[i] = make_double2(co, s);
-        sincos((double)(c.pos_base + (int64_t)t_begin * kTileTokens) * th, &s, &co);
-        cbase[i] = make_double2(co, s);
     }
     __syncthreads();
-    for (int x = tid; x < kPairs * 32; x += NTHR) {
-        const int i = x >> 5, j = x & 31;
-        const double th = th64[i];
-        double s, co;
-        sincos((double)j * th, &s, &co);
-        t1f[x] = make_float2((float)co, (float)s);
-    }
-    double2 anc64[2];
+    // token angles as in the MHA kernel: per warp and tile (anchor angle a_i mod 2 pi, th_i) fp32,
+    // token j's cis from the MUFU at a_i + (j - 16) th_i
+    double ang64[2], step64[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         const int i = lane + 32 * k;
-        // cis((pos_base + 32 t_first) th_i) = cis(the CTA's first tile) x cis(32 (t_first - t_begin) th_i)
-        double sr, cr;
-        sincos((double)((t_first - t_begin) * kTileTokens) * th64[i], &sr, &cr);
-        const double2 b0 = cbase[i];
-        const double co = b0.x * cr - b0.y * sr, s = b0.x * sr + b0.y * cr;
-        anc64[k] = make_double2(co, s);
-        anc32[i] = make_float2((float)co, (float)s);
+        const double th = th64[i];
+        ang64[k] = red2pi((double)(c.pos_base + (int64_t)t_first * kTileTokens + 16) * th);
+        step64[k] = red2pi((double)(C::NWARP * kTileTokens) * th);
+        anc32[i] = make_float2((float)ang64[k], (float)th);
     }
     for (int x = lane; x < G * 32; x += 32) kfix[x] = 0;
-    for (int x = lane; x < G * kHeadDim; x += 32) osp[x] = 0.f;
+    for (int x = lane; x < G * kHeadDim; x += 32) { osp[x] = 0.f; vfix[x] = 0; }
     for (int x = tid; x < kHeadDim; x += NTHR) {
         ks_s[x] = c.kpar[c_lo + x];
         kz_s[x] = c.kpar[D + c_lo + x];
@@ -1176,9 +1161,7 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
     const int hcl = min(vt, G - 1);
     auto rot32 = [&](int i, int j, float &co, float &si) {
         const float2 a = anc32[i];
-        const float2 tt = t1f[i * 32 + j];
-        co = a.x * tt.x - a.y * tt.y;
-        si = a.x * tt.y + a.y * tt.x;
+        __sincosf(fmaf((float)(j - 16), a.y, a.x), &si, &co);
     };
     auto rot16 = [&](int i) -> uint32_t {
         float co, si;
@@ -1186,14 +1169,14 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         return pack_half2(co, si);
     };
 
-    for (int t = t_first; t < t_end; t += NSG) {
+    for (int t = t_first; t < t_end; t += C::NWARP) {
         const int64_t n0 = (int64_t)t * 32;
         const int ntok = (int)min((int64_t)32, P.T - n0);
         const bool valid = lane < ntok;
         const bool kov = cnt_k > (uint32_t)c.kcap_g, vov = cnt_v > (uint32_t)c.vcap_g;
         const int nk = kov ? 0 : (int)cnt_k, nv = vov ? 0 : (int)cnt_v;
         load_items(t);
-        load_counts(t + NSG, ncnt_k, ncnt_v);
+        load_counts(t + C::NWARP, ncnt_k, ncnt_v);
         uint32_t vw[KWH];
 #pragma unroll
         for (int w = 0; w < KWH; ++w) vw[w] = __ldg(c.vcodes + vf_word(t, c.H_kv, hk, w, lane, BITS));
@@ -1265,7 +1248,7 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
-                atomicAdd(&kfix[g * 32 + j], kfix_of(delta * (up ? (qb * co - qa * si) : (qa * co + qb * si))));
+                kfix_add32(&kfix[g * 32 + j], &kbig[g * 32 + j], delta * (up ? (qb * co - qa * si) : (qa * co + qb * si)));
             }
         };
         {
@@ -1287,7 +1270,7 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
             }
         }
         __syncwarp();
-        const int tn = t + NSG;
+        const int tn = t + C::NWARP;
         if (tn < t_end) issue_k(tn);
 
         // ------------------------------------------------------ a4: online softmax
@@ -1301,7 +1284,8 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         float al[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            float s = sco[g] + kfix_val(kfix[g * 32 + lane]);
+            float s = sco[g] + (float)kfix[g * 32 + lane] * (1.f / kKfixScale) + kbig[g * 32 + lane];
+            kbig[g * 32 + lane] = 0.f;   // the words are the V-outlier sums from here on
             s = valid ? s : -CUDART_INF_F;
             const float m_new = fmaxf(m_run[g], warp_max_redux(s));
             const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run[g] - m_new);
@@ -1375,48 +1359,97 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         }
 
         // ------------------------------------------------------ a6: V outliers
+        // p_g (x - V^(code)) of every item for the G heads, summed in fixed point (scale from
+        // the tile's largest |term|) with native shared integer atomics, folded into osp
         __syncwarp();
-        auto v_item = [&](uint32_t itm, bool act) {
-            const int j = (int)((itm >> 11) & 31u), cc = (int)(itm & 0x7fu), flag = (int)((itm >> 9) & 3u);
-            int code = flag == 1 ? CM : 0;
-            if (act && flag == 0) {
-                const int bit = vf_bit(j, cc, BITS);
-                const uint32_t *wq = c.vcodes + vf_word(t, c.H_kv, hk, bit >> 5, vf_lane(j, cc), BITS);
-                unsigned long long w64 = __ldg(wq);
-                if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)__ldg(wq + 32) << 32;
-                code = (int)((w64 >> (bit & 31)) & CM);
-            }
-            const float s_n = __shfl_sync(0xffffffffu, vsz.x, j), z_n = __shfl_sync(0xffffffffu, vsz.y, j);
-            const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
-            const float delta = xval - (cbVs[code] * s_n + z_n);
-            if (act) {
-#pragma unroll
-                for (int g = 0; g < G; ++g) atomicAdd(&osp[g * kHeadDim + cc], ps[g * 32 + j] * delta);
-            }
-        };
-#pragma unroll
-        for (int k = 0; k < IPL; ++k)
-            if (32 * k < nv) v_item(vitm[k], lane + 32 * k < nv);
-        if (nv > 32 * IPL || vov) {
+        if (nv > 0 || vov) {
+            // item -> (channel, delta); the G terms are ps[g][j] * delta
+            auto v_delta = [&](uint32_t itm, bool act, int &j, int &cc) -> float {
+                j = (int)((itm >> 11) & 31u);
+                cc = (int)(itm & 0x7fu);
+                const int flag = (int)((itm >> 9) & 3u);
+                int code = flag == 1 ? CM : 0;
+                if (act && flag == 0) {
+                    const int bit = vf_bit(j, cc, BITS);
+                    const uint32_t *wq = c.vcodes + vf_word(t, c.H_kv, hk, bit >> 5, vf_lane(j, cc), BITS);
+                    unsigned long long w64 = __ldg(wq);
+                    if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)__ldg(wq + 32) << 32;
+                    code = (int)((w64 >> (bit & 31)) & CM);
+                }
+                const float s_n = __shfl_sync(0xffffffffu, vsz.x, j), z_n = __shfl_sync(0xffffffffu, vsz.y, j);
+                const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+                return act ? xval - (cbVs[code] * s_n + z_n) : 0.f;
+            };
             const int64_t bucket = (int64_t)t * c.NG + hk;
-            for (int x0 = 32 * IPL; x0 < nv; x0 += 32) {
-                const bool act = x0 + lane < nv;
-                v_item(act ? __ldg(c.vit + bucket * c.vcap_g + x0 + lane) : 0u, act);
-            }
-            if (vov) {
-                const int kv = c.kv;
-                for (int r0 = 0; r0 < ntok * kv; r0 += 32) {
-                    const int r = r0 + lane;
-                    bool act = r < ntok * kv;
-                    uint32_t itm = 0u;
+            // the items beyond the registers (rare): x0 + lane for x0 >= 32 IPL, then (overflowed
+            // bucket) every CSR record of the tile's tokens in this KV head
+            const int kvn = c.kv;
+            const int x_beg = vov ? 0 : 32 * IPL;
+            const int x_end = (vov ? ntok * kvn : 0) + nv;
+            auto slow_item = [&](int x0, int &j, int &cc) -> float {
+                uint32_t itm = 0u;
+                bool act = false;
+                if (x0 < nv) {
+                    act = x0 + lane < nv;
+                    itm = act ? __ldg(c.vit + bucket * c.vcap_g + x0 + lane) : 0u;
+                } else {
+                    const int r = x0 - nv + lane;
+                    act = r < ntok * kvn;
                     if (act) {
-                        const uint32_t rec = __ldcg(c.vout + n0 * kv + r);
+                        const uint32_t rec = __ldcg(c.vout + n0 * kvn + r);
                         const int ch = (int)(rec & 0xffffu);
                         act = ch >= c_lo && ch < c_lo + kHeadDim;
-                        itm = (rec & 0xffff0000u) | ((uint32_t)(r / kv) << 11) | (uint32_t)(act ? ch - c_lo : 0);
+                        itm = (rec & 0xffff0000u) | ((uint32_t)(r / kvn) << 11) | (uint32_t)(act ? ch - c_lo : 0);
                     }
-                    v_item(itm, act);
                 }
+                return v_delta(itm, act, j, cc);
+            };
+            const bool slow = nv > 32 * IPL || vov;
+            float dl[IPL];
+            int jx[IPL], cx[IPL];
+            float pmax = 0.f;
+#pragma unroll
+            for (int g = 0; g < G; ++g) pmax = fmaxf(pmax, ps[g * 32 + lane]);
+            pmax = warp_max(pmax);   // every term is <= pmax |delta|
+            float mx = 0.f;
+#pragma unroll
+            for (int k = 0; k < IPL; ++k) {
+                dl[k] = 0.f; jx[k] = 0; cx[k] = 0;
+                if (32 * k < nv && !vov) dl[k] = v_delta(vitm[k], lane + 32 * k < nv, jx[k], cx[k]);
+                mx = fmaxf(mx, fabsf(dl[k]));
+            }
+            if (slow)
+                for (int x0 = x_beg; x0 < x_end; x0 += 32) {
+                    int j, cc;
+                    mx = fmaxf(mx, fabsf(slow_item(x0, j, cc)));
+                }
+            mx = warp_max(mx) * pmax;
+            const int emx = mx > 0.f ? ilog2f(mx) : 0;
+            const float S = pow2i(24 - emx);
+            auto add = [&](float d, int j, int cc) {
+                if (d == 0.f) return;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float v = ps[g * 32 + j] * d;
+                    if (v != 0.f) atomicAdd(&vfix[g * kHeadDim + cc], __float2int_rn(v * S));
+                }
+            };
+            if (!vov) {
+#pragma unroll
+                for (int k = 0; k < IPL; ++k) add(dl[k], jx[k], cx[k]);
+            }
+            if (slow)
+                for (int x0 = x_beg; x0 < x_end; x0 += 32) {
+                    int j, cc;
+                    const float d = slow_item(x0, j, cc);
+                    add(d, j, cc);
+                }
+            __syncwarp();
+            const float inv = pow2i(emx - 24);
+#pragma unroll
+            for (int x = 0; x < G * kHeadDim / 32; ++x) {
+                const int v = vfix[x * 32 + lane];
+                if (v) { osp[x * 32 + lane] += (float)v * inv; vfix[x * 32 + lane] = 0; }
             }
         }
         __syncwarp();
@@ -1426,10 +1459,8 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const int i = lane + 32 * k;
-            const double2 a = anc64[k], r = rot[i];
-            const double2 b = make_double2(a.x * r.x - a.y * r.y, a.x * r.y + a.y * r.x);
-            anc64[k] = b;
-            anc32[i] = make_float2((float)b.x, (float)b.y);
+            ang64[k] = red2pi(ang64[k] + step64[k]);
+            anc32[i].x = (float)ang64[k];
         }
         cnt_k = ncnt_k;
         cnt_v = ncnt_v;
@@ -1477,7 +1508,7 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
             const float wt = exp2f(ml[0] - m);
             l += wt * ml[1];
             if (ch < kHeadDim) {
-                const float *ow = reinterpret_cast<const float *>(wbase + w * C::w_bytes + C::w_kst + G * 32 * 8);
+                const float *ow = reinterpret_cast<const float *>(wbase + w * C::w_bytes + C::w_kst + G * 32 * 4);
                 o += wt * ow[g * kHeadDim + ch];
             }
         }
