@@ -1208,6 +1208,7 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         __syncwarp();
 
         // -------------------------------------------- a3: heavy pairs, Key outliers (fp32)
+        // heavy pairs of each head (fp32 tables, fp32 rotation)
         float sco[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -1445,12 +1446,28 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
                     add(d, j, cc);
                 }
             __syncwarp();
+            // fold only the entries this tile touched: the lanes re-walk their items and the
+            // first to exchange an entry adds it (the others get 0)
             const float inv = pow2i(emx - 24);
+            auto fold = [&](float d, int cc) {
+                if (d == 0.f) return;
 #pragma unroll
-            for (int x = 0; x < G * kHeadDim / 32; ++x) {
-                const int v = vfix[x * 32 + lane];
-                if (v) { osp[x * 32 + lane] += (float)v * inv; vfix[x * 32 + lane] = 0; }
+                for (int g = 0; g < G; ++g) {
+                    const int v = atomicExch(&vfix[g * kHeadDim + cc], 0);
+                    if (v) osp[g * kHeadDim + cc] += (float)v * inv;
+                }
+            };
+            if (!vov) {
+#pragma unroll
+                for (int k = 0; k < IPL; ++k) fold(dl[k], cx[k]);
             }
+            if (slow)
+                for (int x0 = x_beg; x0 < x_end; x0 += 32) {
+                    int j, cc;
+                    const float d = slow_item(x0, j, cc);
+                    fold(d, cc);
+                }
+            __syncwarp();
         }
         __syncwarp();
 #pragma unroll
