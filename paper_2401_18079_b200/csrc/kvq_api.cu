@@ -416,15 +416,15 @@ static kvq_status append_tokens(kvq_cache *c, const void *K, const void *V, int6
         if (ck == 1) { CK(cudaMemcpyAsync(sb, K, bytes, cudaMemcpyHostToDevice, s)); Kd = (const __half *)sb; }
         if (cv == 1) { CK(cudaMemcpyAsync(sb + bytes, V, bytes, cudaMemcpyHostToDevice, s)); Vd = (const __half *)(sb + bytes); }
     }
-    // the prefill kernel reads rows with 16-byte vector loads: stage unaligned device rows
-    if (T > 1 && (((uintptr_t)Kd | (uintptr_t)Vd) & 15u)) {
+    // the quantize kernels read rows with 16-byte vector loads: stage unaligned device rows
+    if (((uintptr_t)Kd | (uintptr_t)Vd) & 15u) {
         st = ensure_stage(c, 2 * bytes);
         if (st != KVQ_OK) return st;
         char *sb = (char *)c->stage;
         if ((const void *)Kd != (const void *)sb) { CK(cudaMemcpyAsync(sb, Kd, bytes, cudaMemcpyDeviceToDevice, s)); Kd = (const __half *)sb; }
         if ((const void *)Vd != (const void *)(sb + bytes)) { CK(cudaMemcpyAsync(sb + bytes, Vd, bytes, cudaMemcpyDeviceToDevice, s)); Vd = (const __half *)(sb + bytes); }
     }
-    cudaError_t e = T == 1 ? launch_quantize(c->dc, Kd, Vd, c->T, T, s)
+    cudaError_t e = T == 1 ? launch_append(c->dc, Kd, Vd, c->T, s)
                            : launch_prefill(c->dc, Kd, Vd, c->T, T, c->dc.lb, c->dc.ticket, s);
     if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
     c->T += T;

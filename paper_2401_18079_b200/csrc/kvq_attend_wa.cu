@@ -476,13 +476,14 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             for (int w = 0; w < KWH; ++w) kw[h][w] = kst[(h * KWH + w) * 32 + lane];
 
         // ---------------------------------------------------------- a2: K dense
-        float acc_c[WH], acc_s[WH];
+        // two accumulator pairs per head (even / odd pairs): shorter FMA dependency chains
+        float acc_c[WH][2], acc_s[WH][2];
 #pragma unroll
-        for (int h = 0; h < WH; ++h) { acc_c[h] = 0.f; acc_s[h] = 0.f; }
+        for (int h = 0; h < WH; ++h) acc_c[h][0] = acc_s[h][0] = acc_c[h][1] = acc_s[h][1] = 0.f;
 #pragma unroll
         for (int i = 0; i < kPairs; ++i) {
             if (i == kPairs / 2) load_v();
-            // cis(n' th_i) = anchor x cis(j th_i) in fp32, rounded once to fp16
+            // cis(n' th_i) from the MUFU, rounded once to fp16
             const uint32_t cs = rot16(i);
             const int bit = FB * i, w = bit >> 5, sh = bit & 31;
 #pragma unroll
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                 else off = __funnelshift_r(kw[h][w], kw[h][w + 1], sh - 2);
                 const uint32_t a = klut_u | (off & ((NE - 1) << 2));
                 const uint32_t ab = lds_u32(a + (uint32_t)((h * 64 + i) * NE * 4));
-                fma2_f16_f32(ab, cs, acc_c[h], acc_s[h]);
+                fma2_f16_f32(ab, cs, acc_c[h][i & 1], acc_s[h][i & 1]);
             }
         }
         __syncwarp();
@@ -508,15 +509,15 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                 const int i = hv_pair[hc * 8 + u];
                 const int bit = FB * i;
                 const int wq = h * KWH + (bit >> 5);
-                unsigned long long w64 = kst[wq * 32 + lane];
-                if ((bit & 31) + FB > 32) w64 |= (unsigned long long)kst[(wq + 1) * 32 + lane] << 32;
-                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                // the word after may be past the head's last (then unused): kst is followed by
+                // the warp's other scratch, so the read stays in bounds
+                const int pc = (int)(__funnelshift_r(kst[wq * 32 + lane], kst[(wq + 1) * 32 + lane], bit & 31) & (NE - 1));
                 const float2 ab = hlut[(hc * HMAX + u) * NE + pc];
                 float co, si;
                 rot32(i, lane, co, si);
                 hs += co * ab.x + si * ab.y;
             }
-            sco[h] = (acc_c[h] + acc_s[h]) * lut_inv[hc] + hs;
+            sco[h] = ((acc_c[h][0] + acc_s[h][0]) + (acc_c[h][1] + acc_s[h][1])) * lut_inv[hc] + hs;
         }
         // item of the CTA's 4-head group -> (token, head of this warp or -1, correction)
         auto k_corr = [&](uint32_t itm, int &j, int &h) -> float {

@@ -1,6 +1,7 @@
-// kvq_prefill.cu -- QZ, block prefill quantization: one CTA per 32-token tile.
+// kvq_prefill.cu -- QZ: block prefill quantization (one CTA per 32-token tile)
+// and quantize-on-append of one decode token (a8, append_kernel at the end of the file).
 //
-// The same quantization as T successive appends (kvq_quant.cu, readings R2-R8):
+// Both compute exactly what T successive appends define (readings R2-R8):
 //   Keys: outlier iff x < lo_c or x > hi_c (R4); code = ENC(clamp(x)).
 //   Values (topk P:1028-1031): two-sided top-k, k = ceil(f D),
 //         ceil(k/2) largest then floor(k/2) smallest of the rest, ties to the lower index,
@@ -166,6 +167,201 @@ __device__ void select_exact(const __half *row, int D, int need, bool desc, uint
     __syncwarp();
 }
 
+// One token's Value quantization by one warp (reads R2, R3, R6, R7, R8): the two-sided top-k
+// outliers (bitmask vm, [D/32] words, zeroed by the caller), kept range, (s, z) -> c.vsz[n],
+// ENC thresholds and the codes of lo / hi -> tinfo_row, CSR records -> c.vout row n.
+// cand: per-warp scratch [2][CANDMAX]; nc2: per-warp [2] counters.
+template <int NM>
+__device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_t *vm, uint32_t *cand,
+                            int *nc2, uint16_t *tinfo_row, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    const int DW = D / 32;
+    const int k = c.kv, ku = (k + 1) / 2, kl = k / 2;
+    const int nch = (D + 255) / 256;
+        // group maxima / minima (fp16 values; 2 groups per lane: even / odd chunks)
+        __half2 mx[2], mn[2];
+        mx[0] = mx[1] = __float2half2_rn(-65504.f);
+        mn[0] = mn[1] = __float2half2_rn(65504.f);
+        bool have[2] = {false, false};
+        for (int m = 0; m < nch; ++m) {
+            const int c0 = 256 * m + 8 * lane;
+            if (c0 >= D) continue;
+            const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+            const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
+            const __half2 b = __hmin2(__hmin2(u2h(u.x), u2h(u.y)), __hmin2(u2h(u.z), u2h(u.w)));
+            mx[m & 1] = __hmax2(mx[m & 1], a);
+            mn[m & 1] = __hmin2(mn[m & 1], b);
+            have[m & 1] = true;
+        }
+        // (need+1)-th largest group max / smallest group min, bit search on order keys
+        uint32_t gk[2], gl[2];
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            gk[g] = have[g] ? okey(h2u(__hmax2(mx[g], __lowhigh2highlow(mx[g])))) : 0u;
+            gl[g] = have[g] ? 0xffffu - okey(h2u(__hmin2(mn[g], __lowhigh2highlow(mn[g])))) : 0u;
+        }
+        auto kth = [&](const uint32_t (&v)[2], int need) {
+            uint32_t t = 0;
+            for (int b = 15; b >= 0; --b) {
+                const uint32_t t2 = t | (1u << b);
+                const int n = __popc(__ballot_sync(0xffffffffu, v[0] >= t2)) + __popc(__ballot_sync(0xffffffffu, v[1] >= t2));
+                if (n >= need) t = t2;
+            }
+            return t;
+        };
+        const uint32_t tau_hi = kth(gk, ku + 1);                // order key
+        const uint32_t tau_lo = 0xffffu - kth(gl, kl + 1);      // order key
+        // candidates: value >= tau_hi (upper), value <= tau_lo (lower)
+        if (lane < 2) nc2[lane] = 0;
+        __syncwarp();
+        const __half2 th2 = u2h(key2h(tau_hi) * 0x10001u), tl2 = u2h(key2h(tau_lo) * 0x10001u);
+        bool ovf = false;
+        for (int m = 0; m < nch; ++m) {
+            const int c0 = 256 * m + 8 * lane;
+            uint32_t fu = 0, fl = 0;
+            if (c0 < D) {
+                const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                // the chunk's max / min first: per-element flags only where a candidate is
+                const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
+                const __half2 b = __hmin2(__hmin2(u2h(u.x), u2h(u.y)), __hmin2(u2h(u.z), u2h(u.w)));
+                if (__hbge2(__hmax2(a, __lowhigh2highlow(a)), th2) || __hble2(__hmin2(b, __lowhigh2highlow(b)), tl2)) {
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const uint32_t ge = h2u(__hge2(u2h(w[e2]), th2)), le = h2u(__hle2(u2h(w[e2]), tl2));
+                        fu |= (((ge >> 13) & 1u) | ((ge >> 28) & 2u)) << (2 * e2);
+                        fl |= (((le >> 13) & 1u) | ((le >> 28) & 2u)) << (2 * e2);
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, (fu | fl) != 0u)) {
+                const int nu = __popc(fu), nl = __popc(fl);
+                int bu = 0, bl = 0;
+                if (nu) bu = atomicAdd(&nc2[0], nu);
+                if (nl) bl = atomicAdd(&nc2[1], nl);
+                if (fu | fl) {
+                    const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                    for (uint32_t x = fu; x; x &= x - 1) {
+                        const int e = __ffs(x) - 1;
+                        const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                        if (bu < CANDMAX) cand[bu] = (key << 13) | (8191u - (uint32_t)(c0 + e));
+                        ++bu;
+                    }
+                    for (uint32_t x = fl; x; x &= x - 1) {
+                        const int e = __ffs(x) - 1;
+                        const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                        if (bl < CANDMAX) cand[CANDMAX + bl] = ((0xffffu - key) << 13) | (8191u - (uint32_t)(c0 + e));
+                        ++bl;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        const int NU = nc2[0], NL = nc2[1];
+        ovf = NU > CANDMAX || NL > CANDMAX || NU < ku + 1 || NL < kl + 1 || tau_lo >= tau_hi;
+        uint32_t lo_h = 0, hi_h = 0;   // fp16 bits of the kept min / max
+        if (!ovf) {
+            // exact ranks among the candidates: rank = #candidates ordered before
+            int hi_idx = -1, lo_idx = -1;
+            for (int i = lane; i < NU; i += 32) {
+                const uint32_t v = cand[i];
+                int r = 0;
+                for (int q = 0; q < NU; ++q) r += cand[q] > v;
+                const int ch = 8191 - (int)(v & 8191u);
+                if (r < ku) atomicOr(&vm[ch >> 5], 1u << (ch & 31));
+                if (r == ku) hi_idx = ch;
+            }
+            for (int i = lane; i < NL; i += 32) {
+                const uint32_t v = cand[CANDMAX + i];
+                int r = 0;
+                for (int q = 0; q < NL; ++q) r += cand[CANDMAX + q] > v;
+                const int ch = 8191 - (int)(v & 8191u);
+                if (r < kl) atomicOr(&vm[ch >> 5], 1u << (ch & 31));
+                if (r == kl) lo_idx = ch;
+            }
+            hi_idx = __reduce_max_sync(0xffffffffu, hi_idx + 1) - 1;
+            lo_idx = __reduce_max_sync(0xffffffffu, lo_idx + 1) - 1;
+            hi_h = __half_as_ushort(row[hi_idx]);
+            lo_h = __half_as_ushort(row[lo_idx]);
+            __syncwarp();
+        } else {
+            // exact selection over all elements, then the kept range (lowest index)
+            for (int x = lane; x < DW; x += 32) vm[x] = 0;
+            __syncwarp();
+            select_exact(row, D, ku, true, vm);
+            select_exact(row, D, kl, false, vm);
+            uint32_t bh = 0, bl2 = 0xffffffffu;   // (key << 16 | 0xffff - idx) max; (key << 16 | idx) min
+            for (int m = 0; m < nch; ++m) {
+                const int c0 = 256 * m + 8 * lane;
+                if (c0 >= D) continue;
+                const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                const uint32_t mw = vm[c0 >> 5] >> (c0 & 31);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    if ((mw >> e) & 1u) continue;
+                    const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                    bh = max(bh, (key << 16) | (0xffffu - (uint32_t)(c0 + e)));
+                    bl2 = min(bl2, (key << 16) | (uint32_t)(c0 + e));
+                }
+            }
+            bh = __reduce_max_sync(0xffffffffu, bh);
+            bl2 = __reduce_min_sync(0xffffffffu, bl2);
+            hi_h = __half_as_ushort(row[0xffff - (bh & 0xffffu)]);
+            lo_h = __half_as_ushort(row[bl2 & 0xffffu]);
+        }
+        // (s, z) in fp64, rounded once (R6); ENC thresholds of the token (lanes 0..NM-1)
+        const double lo = (double)__half2float(__ushort_as_half((uint16_t)lo_h));
+        const double hi = (double)__half2float(__ushort_as_half((uint16_t)hi_h));
+        const float s = __double2float_rn(__dsub_rn(hi, lo) / 2.0);
+        const float z = __double2float_rn(__dadd_rn(hi, lo) / 2.0);
+        uint16_t *ti = tinfo_row;
+        if (lane == 0) {
+            c.vsz[n] = make_float2(s, z);
+            ti[TI_LO] = (uint16_t)lo_h;
+            ti[TI_HI] = (uint16_t)hi_h;
+        }
+        uint32_t thr = 0x7c00u;   // +inf: never
+        if (lane < NM) {
+            const double mj = c.mids[16 + lane];
+            const double sd = (double)s, zd = (double)z;
+            uint32_t a = 0x0400u, b = 0xfc00u;   // order keys of -65504 .. +inf (sentinel)
+            while (a < b) {
+                const uint32_t mid = (a + b) >> 1;
+                const double y = (double)__half2float(__ushort_as_half((uint16_t)key2h(mid)));
+                if (2.0 * __dsub_rn(y, zd) > __dmul_rn(sd, mj)) b = mid; else a = mid + 1;
+            }
+            thr = key2h(a);
+            ti[TI_T + lane] = (uint16_t)thr;
+        }
+        // codes of lo and hi (item flags of the outliers)
+        const uint32_t klo = okey(lo_h), khi = okey(hi_h), kt = okey(thr);
+        const int clo = __popc(__ballot_sync(0xffffffffu, lane < NM && klo >= kt));
+        const int chi = __popc(__ballot_sync(0xffffffffu, lane < NM && khi >= kt));
+        if (lane == 0) { ti[TI_CLO] = (uint16_t)clo; ti[TI_CHI] = (uint16_t)chi; }
+        __syncwarp();
+        // CSR records of the token's k outliers (ascending channel) and per-group counts
+        if (k > 0) {
+            const int wpl = (DW + 31) / 32;   // mask words per lane (ascending channels)
+            int cnt = 0;
+            for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x) cnt += __popc(vm[x]);
+            int ex = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, ex, o);
+                if (lane >= o) ex += y;
+            }
+            ex -= cnt;
+            uint32_t *vo = c.vout + n * (int64_t)k;
+            for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x)
+                for (uint32_t b = vm[x]; b; b &= b - 1) {
+                    const int ch = 32 * x + __ffs(b) - 1;
+                    vo[ex++] = (uint32_t)ch | ((uint32_t)__half_as_ushort(row[ch]) << 16);
+                }
+        }
+}
+
 // ------------------------------------------------------------------------------ kernel
 template <int BITS>
 __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
@@ -204,195 +400,12 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
 
     // ====================================================== A: Value selection (warp/token)
     {
-        const int k = c.kv, ku = (k + 1) / 2, kl = k / 2;
-        const int nch = (D + 255) / 256;
         uint32_t *cand = reinterpret_cast<uint32_t *>(wsc);   // [2][CANDMAX]
         __shared__ int s_nc[PW][2];
         for (int j = jA + warp; j < jB; j += PW) {
             const __half *row = vrow(j);
             uint32_t *vm = vmask + j * DW;
-            // group maxima / minima (fp16 values; 2 groups per lane: even / odd chunks)
-            __half2 mx[2], mn[2];
-            mx[0] = mx[1] = __float2half2_rn(-65504.f);
-            mn[0] = mn[1] = __float2half2_rn(65504.f);
-            bool have[2] = {false, false};
-            for (int m = 0; m < nch; ++m) {
-                const int c0 = 256 * m + 8 * lane;
-                if (c0 >= D) continue;
-                const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
-                const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
-                const __half2 b = __hmin2(__hmin2(u2h(u.x), u2h(u.y)), __hmin2(u2h(u.z), u2h(u.w)));
-                mx[m & 1] = __hmax2(mx[m & 1], a);
-                mn[m & 1] = __hmin2(mn[m & 1], b);
-                have[m & 1] = true;
-            }
-            // (need+1)-th largest group max / smallest group min, bit search on order keys
-            uint32_t gk[2], gl[2];
-#pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                gk[g] = have[g] ? okey(h2u(__hmax2(mx[g], __lowhigh2highlow(mx[g])))) : 0u;
-                gl[g] = have[g] ? 0xffffu - okey(h2u(__hmin2(mn[g], __lowhigh2highlow(mn[g])))) : 0u;
-            }
-            auto kth = [&](const uint32_t (&v)[2], int need) {
-                uint32_t t = 0;
-                for (int b = 15; b >= 0; --b) {
-                    const uint32_t t2 = t | (1u << b);
-                    const int n = __popc(__ballot_sync(0xffffffffu, v[0] >= t2)) + __popc(__ballot_sync(0xffffffffu, v[1] >= t2));
-                    if (n >= need) t = t2;
-                }
-                return t;
-            };
-            const uint32_t tau_hi = kth(gk, ku + 1);                // order key
-            const uint32_t tau_lo = 0xffffu - kth(gl, kl + 1);      // order key
-            // candidates: value >= tau_hi (upper), value <= tau_lo (lower)
-            if (lane < 2) s_nc[warp][lane] = 0;
-            __syncwarp();
-            const __half2 th2 = u2h(key2h(tau_hi) * 0x10001u), tl2 = u2h(key2h(tau_lo) * 0x10001u);
-            bool ovf = false;
-            for (int m = 0; m < nch; ++m) {
-                const int c0 = 256 * m + 8 * lane;
-                uint32_t fu = 0, fl = 0;
-                if (c0 < D) {
-                    const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
-                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-                    // the chunk's max / min first: per-element flags only where a candidate is
-                    const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
-                    const __half2 b = __hmin2(__hmin2(u2h(u.x), u2h(u.y)), __hmin2(u2h(u.z), u2h(u.w)));
-                    if (__hbge2(__hmax2(a, __lowhigh2highlow(a)), th2) || __hble2(__hmin2(b, __lowhigh2highlow(b)), tl2)) {
-#pragma unroll
-                        for (int e2 = 0; e2 < 4; ++e2) {
-                            const uint32_t ge = h2u(__hge2(u2h(w[e2]), th2)), le = h2u(__hle2(u2h(w[e2]), tl2));
-                            fu |= (((ge >> 13) & 1u) | ((ge >> 28) & 2u)) << (2 * e2);
-                            fl |= (((le >> 13) & 1u) | ((le >> 28) & 2u)) << (2 * e2);
-                        }
-                    }
-                }
-                if (__any_sync(0xffffffffu, (fu | fl) != 0u)) {
-                    const int nu = __popc(fu), nl = __popc(fl);
-                    int bu = 0, bl = 0;
-                    if (nu) bu = atomicAdd(&s_nc[warp][0], nu);
-                    if (nl) bl = atomicAdd(&s_nc[warp][1], nl);
-                    if (fu | fl) {
-                        const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
-                        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-                        for (uint32_t x = fu; x; x &= x - 1) {
-                            const int e = __ffs(x) - 1;
-                            const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
-                            if (bu < CANDMAX) cand[bu] = (key << 13) | (8191u - (uint32_t)(c0 + e));
-                            ++bu;
-                        }
-                        for (uint32_t x = fl; x; x &= x - 1) {
-                            const int e = __ffs(x) - 1;
-                            const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
-                            if (bl < CANDMAX) cand[CANDMAX + bl] = ((0xffffu - key) << 13) | (8191u - (uint32_t)(c0 + e));
-                            ++bl;
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            const int NU = s_nc[warp][0], NL = s_nc[warp][1];
-            ovf = NU > CANDMAX || NL > CANDMAX || NU < ku + 1 || NL < kl + 1 || tau_lo >= tau_hi;
-            uint32_t lo_h = 0, hi_h = 0;   // fp16 bits of the kept min / max
-            if (!ovf) {
-                // exact ranks among the candidates: rank = #candidates ordered before
-                int hi_idx = -1, lo_idx = -1;
-                for (int i = lane; i < NU; i += 32) {
-                    const uint32_t v = cand[i];
-                    int r = 0;
-                    for (int q = 0; q < NU; ++q) r += cand[q] > v;
-                    const int ch = 8191 - (int)(v & 8191u);
-                    if (r < ku) atomicOr(&vm[ch >> 5], 1u << (ch & 31));
-                    if (r == ku) hi_idx = ch;
-                }
-                for (int i = lane; i < NL; i += 32) {
-                    const uint32_t v = cand[CANDMAX + i];
-                    int r = 0;
-                    for (int q = 0; q < NL; ++q) r += cand[CANDMAX + q] > v;
-                    const int ch = 8191 - (int)(v & 8191u);
-                    if (r < kl) atomicOr(&vm[ch >> 5], 1u << (ch & 31));
-                    if (r == kl) lo_idx = ch;
-                }
-                hi_idx = __reduce_max_sync(0xffffffffu, hi_idx + 1) - 1;
-                lo_idx = __reduce_max_sync(0xffffffffu, lo_idx + 1) - 1;
-                hi_h = __half_as_ushort(row[hi_idx]);
-                lo_h = __half_as_ushort(row[lo_idx]);
-                __syncwarp();
-            } else {
-                // exact selection over all elements, then the kept range (lowest index)
-                for (int x = lane; x < DW; x += 32) vm[x] = 0;
-                __syncwarp();
-                select_exact(row, D, ku, true, vm);
-                select_exact(row, D, kl, false, vm);
-                uint32_t bh = 0, bl2 = 0xffffffffu;   // (key << 16 | 0xffff - idx) max; (key << 16 | idx) min
-                for (int m = 0; m < nch; ++m) {
-                    const int c0 = 256 * m + 8 * lane;
-                    if (c0 >= D) continue;
-                    const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
-                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-                    const uint32_t mw = vm[c0 >> 5] >> (c0 & 31);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        if ((mw >> e) & 1u) continue;
-                        const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
-                        bh = max(bh, (key << 16) | (0xffffu - (uint32_t)(c0 + e)));
-                        bl2 = min(bl2, (key << 16) | (uint32_t)(c0 + e));
-                    }
-                }
-                bh = __reduce_max_sync(0xffffffffu, bh);
-                bl2 = __reduce_min_sync(0xffffffffu, bl2);
-                hi_h = __half_as_ushort(row[0xffff - (bh & 0xffffu)]);
-                lo_h = __half_as_ushort(row[bl2 & 0xffffu]);
-            }
-            // (s, z) in fp64, rounded once (R6); ENC thresholds of the token (lanes 0..NM-1)
-            const double lo = (double)__half2float(__ushort_as_half((uint16_t)lo_h));
-            const double hi = (double)__half2float(__ushort_as_half((uint16_t)hi_h));
-            const float s = __double2float_rn(__dsub_rn(hi, lo) / 2.0);
-            const float z = __double2float_rn(__dadd_rn(hi, lo) / 2.0);
-            uint16_t *ti = tinfo + j * 24;
-            if (lane == 0) {
-                c.vsz[nt0 + j] = make_float2(s, z);
-                ti[TI_LO] = (uint16_t)lo_h;
-                ti[TI_HI] = (uint16_t)hi_h;
-            }
-            uint32_t thr = 0x7c00u;   // +inf: never
-            if (lane < NM) {
-                const double mj = c.mids[16 + lane];
-                const double sd = (double)s, zd = (double)z;
-                uint32_t a = 0x0400u, b = 0xfc00u;   // order keys of -65504 .. +inf (sentinel)
-                while (a < b) {
-                    const uint32_t mid = (a + b) >> 1;
-                    const double y = (double)__half2float(__ushort_as_half((uint16_t)key2h(mid)));
-                    if (2.0 * __dsub_rn(y, zd) > __dmul_rn(sd, mj)) b = mid; else a = mid + 1;
-                }
-                thr = key2h(a);
-                ti[TI_T + lane] = (uint16_t)thr;
-            }
-            // codes of lo and hi (item flags of the outliers)
-            const uint32_t klo = okey(lo_h), khi = okey(hi_h), kt = okey(thr);
-            const int clo = __popc(__ballot_sync(0xffffffffu, lane < NM && klo >= kt));
-            const int chi = __popc(__ballot_sync(0xffffffffu, lane < NM && khi >= kt));
-            if (lane == 0) { ti[TI_CLO] = (uint16_t)clo; ti[TI_CHI] = (uint16_t)chi; }
-            __syncwarp();
-            // CSR records of the token's k outliers (ascending channel) and per-group counts
-            if (k > 0) {
-                const int wpl = (DW + 31) / 32;   // mask words per lane (ascending channels)
-                int cnt = 0;
-                for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x) cnt += __popc(vm[x]);
-                int ex = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, ex, o);
-                    if (lane >= o) ex += y;
-                }
-                ex -= cnt;
-                uint32_t *vo = c.vout + (nt0 + j) * (int64_t)k;
-                for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x)
-                    for (uint32_t b = vm[x]; b; b &= b - 1) {
-                        const int ch = 32 * x + __ffs(b) - 1;
-                        vo[ex++] = (uint32_t)ch | ((uint32_t)__half_as_ushort(row[ch]) << 16);
-                    }
-            }
+            vtoken_warp<NM>(c, row, D, vm, cand, s_nc[warp], tinfo + j * 24, nt0 + j);
             for (int g = lane; g < NG; g += 32) {
                 int cnt = 0;
                 for (int x = g * (GW / 32); x < (g + 1) * (GW / 32); ++x) cnt += __popc(vm[x]);
@@ -693,9 +706,222 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
 
 }
 
+
+// ============================================================================ append
+// Quantize-on-append of ONE decode token, latency-oriented: one CTA of 32
+// warps.  Warp 0 runs the Value selection / thresholds / CSR records of the token (the same
+// vtoken_warp as the prefill); warps 1..31 take a KV head each: lane = RoPE pairs (lane,
+// lane + 32), codes from the exact fp16 ENC thresholds (kenc), pair codes assembled into the
+// head's 12 pair-stream words, outlier bits by ballot.  Then the Key CSC slot (kptr), Key
+// records and bucket items, Value items, and the Value codes OR-ed into the fragment-ordered
+// tile words (one OR per two codes).  The kernel lets a dependent attend launch at once
+// (programmatic dependent launch; its prologue reads no cache data).
+constexpr int AT = 1024, AW = AT / 32;
+
+template <int BITS>
+__global__ void __launch_bounds__(AT, 1) append_kernel(DevCache c, const __half *K, const __half *V, int64_t n) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    using Cf = PCfg<BITS>;
+    constexpr int NM = Cf::NM, PS = Cf::PS, CM = (1 << BITS) - 1, KWH = 4 * BITS;
+    __shared__ uint32_t vm[8192 / 32], cand[2 * CANDMAX], kmh[64 * 4];
+    __shared__ uint8_t pcs[64 * 64];
+    __shared__ int nc2[2], kcnt[64], kbase[64], gslotK[64], gslotV[64];
+    __shared__ uint16_t ti[24];
+    __shared__ uint32_t s_kb0, s_ok;
+    // the token's K and V rows staged in shared memory by all threads first: the single
+    // selection warp then never waits on HBM latency (in a one-token launch nothing hides it)
+    __shared__ __align__(16) __half ks[8192], vs[8192];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = c.D, H = c.H_kv, NG = c.NG, GW = c.GW, DW = D / 32;
+    const int64_t tile = n >> 5;
+    const int jj = (int)(n & 31);
+    for (int x = tid; x < D / 8; x += AT) {
+        reinterpret_cast<uint4 *>(ks)[x] = reinterpret_cast<const uint4 *>(K)[x];
+        reinterpret_cast<uint4 *>(vs)[x] = reinterpret_cast<const uint4 *>(V)[x];
+    }
+    __syncthreads();
+    K = ks;
+    V = vs;
+
+    // ---------------------------------------------------------------- Values (warp 0)
+    if (warp == 0) {
+        for (int x = lane; x < DW; x += 32) vm[x] = 0;
+        __syncwarp();
+        vtoken_warp<NM>(c, V, D, vm, cand, nc2, ti, n);
+    } else {
+        // ------------------------------------------------------------ Keys (warps 1..31)
+        const uint4 *kenc = reinterpret_cast<const uint4 *>(c.kenc);
+        for (int h = warp - 1; h < H; h += AW - 1) {
+            uint32_t ob01[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int p = lane + 32 * q;
+                const uint32_t x2 = (uint32_t)__half_as_ushort(K[h * kHeadDim + p]) |
+                                    ((uint32_t)__half_as_ushort(K[h * kHeadDim + p + kPairs]) << 16);
+                const uint4 *te = kenc + ((size_t)(h * kPairs + p) * PS) / 4;
+                uint32_t tw[PS];
+#pragma unroll
+                for (int r = 0; r < PS / 4; ++r) {
+                    const uint4 t4 = __ldg(te + r);
+                    tw[4 * r] = t4.x; tw[4 * r + 1] = t4.y; tw[4 * r + 2] = t4.z; tw[4 * r + 3] = t4.w;
+                }
+                const __half2 x = u2h(x2);
+                const __half2 olo = __hlt2(x, u2h(tw[0])), ohi = __hgt2(x, u2h(tw[1]));
+                __half2 cnt = __hge2(x, u2h(tw[4]));
+#pragma unroll
+                for (int r = 1; r < NM; ++r) cnt = __hadd2(cnt, __hge2(x, u2h(tw[4 + r])));
+                cnt = __hfma2(olo, __hsub2(u2h(tw[2]), cnt), cnt);
+                cnt = __hfma2(ohi, __hsub2(u2h(tw[3]), cnt), cnt);
+                pcs[h * 64 + p] = (uint8_t)h2codes(cnt, BITS);
+                ob01[q] = h2u(__hadd2(olo, ohi));
+            }
+            // outlier bits of channels lane, lane + 32 (low halves) and lane + 64, + 96 (high)
+            const uint32_t m0 = __ballot_sync(0xffffffffu, (ob01[0] >> 13) & 1u);
+            const uint32_t m1 = __ballot_sync(0xffffffffu, (ob01[1] >> 13) & 1u);
+            const uint32_t m2 = __ballot_sync(0xffffffffu, (ob01[0] >> 29) & 1u);
+            const uint32_t m3 = __ballot_sync(0xffffffffu, (ob01[1] >> 29) & 1u);
+            if (lane == 0) {
+                kmh[h * 4 + 0] = m0; kmh[h * 4 + 1] = m1; kmh[h * 4 + 2] = m2; kmh[h * 4 + 3] = m3;
+                kcnt[h] = __popc(m0) + __popc(m1) + __popc(m2) + __popc(m3);
+            }
+            __syncwarp();
+            // the head's pair-stream words: pair p occupies bits [2b p, 2b p + 2b)
+            if (lane < KWH) {
+                const int w = lane;
+                uint32_t word = 0;
+                const int p0 = (32 * w) / (2 * BITS), p1 = min(kPairs - 1, (32 * w + 31) / (2 * BITS));
+                for (int p = p0; p <= p1; ++p) {
+                    const int sh = 2 * BITS * p - 32 * w;
+                    const uint32_t pc = pcs[h * 64 + p];
+                    word |= sh >= 0 ? (pc << sh) : (pc >> -sh);
+                }
+                c.kcodes[(tile * c.QW + h * KWH + w) * 32 + jj] = word;
+            }
+        }
+    }
+    __syncthreads();
+    // ------------------------------------------- Key CSC slot and bucket slots (warp 0)
+    if (warp == 0) {
+        int e0 = lane < H ? kcnt[lane] : 0, e1 = lane + 32 < H ? kcnt[lane + 32] : 0;
+        int x0 = e0, x1 = e1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+            if (lane >= o) { x0 += y0; x1 += y1; }
+        }
+        const int t0 = __shfl_sync(0xffffffffu, x0, 31);
+        if (lane < H) kbase[lane] = x0 - e0;
+        if (lane + 32 < H) kbase[lane + 32] = t0 + x1 - e1;
+        const int total = t0 + __shfl_sync(0xffffffffu, x1, 31);
+        if (lane == 0) {
+            const uint32_t base = c.kptr[n];
+            const bool ok = (int64_t)base + total <= c.kcap;
+            if (!ok) *(volatile int *)c.err |= kErrKeyCapacity;
+            c.kptr[n + 1] = ok ? base + (uint32_t)total : base;
+            s_kb0 = base;
+            s_ok = ok;
+        }
+        for (int g = lane; g < NG; g += 32) {
+            gslotK[g] = (int)c.gcnt[(tile * NG + g) * 2];
+            gslotV[g] = (int)c.gcnt[(tile * NG + g) * 2 + 1];
+        }
+    }
+    __syncthreads();
+    // ----------------------------- Key records + items (warps 1..31), Value items (warp 0)
+    if (warp > 0) {
+        const uint32_t *kenc32 = c.kenc;
+        for (int h = warp - 1; h < H; h += AW - 1) {
+            if (kcnt[h] == 0) continue;
+            const int g = (h * kHeadDim) / GW;
+            int before = 0;   // the group's records of earlier heads (channel order)
+            for (int h2 = (g * GW) / kHeadDim; h2 < h; ++h2) before += kcnt[h2];
+            int rank = 0;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const uint32_t m = kmh[h * 4 + w];
+                if ((m >> lane) & 1u) {
+                    const int r = rank + __popc(m & ((1u << lane) - 1u));
+                    const int cc = 32 * w + lane, ch = h * kHeadDim + cc;
+                    const uint32_t xh = __half_as_ushort(K[ch]);
+                    if (s_ok) c.kout[s_kb0 + (uint32_t)(kbase[h] + r)] = (uint32_t)ch | (xh << 16);
+                    const int pp = cc & 63, up = cc >> 6;
+                    const uint32_t *te = kenc32 + (size_t)(h * kPairs + pp) * PS;
+                    const __half2 lo2 = u2h(te[0]);
+                    const bool below = __hlt(__ushort_as_half((uint16_t)xh), up ? __high2half(lo2) : __low2half(lo2));
+                    const uint32_t cw = h2u(__hadd2(u2h(te[below ? 2 : 3]), __float2half2_rn(1024.f)));
+                    const int code = (int)((up ? cw >> 16 : cw) & 0xfu);
+                    const int slot = gslotK[g] + before + r;
+                    if (slot < c.kcap_g)
+                        c.kit[(tile * NG + g) * (int64_t)c.kcap_g + slot] =
+                            (xh << 16) | ((uint32_t)jj << 11) | item_code_flag<BITS>(code) | (uint32_t)(ch - g * GW);
+                }
+                rank += __popc(m);
+            }
+        }
+    } else {
+        const uint32_t khi = okey(ti[TI_HI]);
+        for (int g = lane; g < NG; g += 32) {
+            int slot = gslotV[g];
+            for (int x = g * (GW / 32); x < (g + 1) * (GW / 32); ++x)
+                for (uint32_t b = vm[x]; b; b &= b - 1) {
+                    const int ch = 32 * x + __ffs(b) - 1;
+                    const uint32_t xh = __half_as_ushort(V[ch]);
+                    const int code = okey(xh) >= khi ? ti[TI_CHI] : ti[TI_CLO];
+                    if (slot < c.vcap_g)
+                        c.vit[(tile * NG + g) * (int64_t)c.vcap_g + slot] =
+                            (xh << 16) | ((uint32_t)jj << 11) | item_code_flag<BITS>(code) | (uint32_t)(ch - g * GW);
+                    ++slot;
+                }
+            // new counts (>= cap: the attend kernels use the CSC / CSR arrays for the tile)
+            int kc = 0;
+            for (int h2 = (g * GW) / kHeadDim; h2 < ((g + 1) * GW) / kHeadDim; ++h2) kc += kcnt[h2];
+            c.gcnt[(tile * NG + g) * 2] = (uint32_t)(gslotK[g] + kc);
+            c.gcnt[(tile * NG + g) * 2 + 1] = (uint32_t)slot;
+        }
+    }
+    // ------------------------------------------------ Value codes (every thread)
+    // channels cc and cc + 8 of a head share a lane of the fragment layout and sit 2b bits
+    // apart: one OR per two codes (the words are shared with the tile's other tokens)
+    {
+        const __half lo = __ushort_as_half(ti[TI_LO]), hi = __ushort_as_half(ti[TI_HI]);
+        __half T[NM];
+#pragma unroll
+        for (int q = 0; q < NM; ++q) T[q] = __ushort_as_half(ti[TI_T + q]);
+        for (int x = tid; x < H * 64; x += AT) {
+            const int hh = x >> 6, mt = (x >> 3) & 7, g8 = x & 7;
+            const int cc = mt * 16 + g8;
+            uint32_t v = 0;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                __half y = V[hh * kHeadDim + cc + 8 * e];
+                y = __hmax(__hmin(y, hi), lo);
+                int code = 0;
+#pragma unroll
+                for (int q = 0; q < NM; ++q) code += __hge(y, T[q]) ? 1 : 0;
+                v |= (uint32_t)code << (2 * BITS * e);
+            }
+            const int bit = vf_bit(jj, cc, BITS);
+            const int ln = vf_lane(jj, cc), w = bit >> 5, off = bit & 31;
+            uint32_t *dst = c.vcodes + vf_word(tile, H, hh, w, ln, BITS);
+            atomicOr(dst, v << off);
+            if (off + 3 * BITS > 32) atomicOr(dst + 32, v >> (32 - off));
+        }
+    }
+}
+
 }  // namespace
 
 size_t prefill_smem_bytes(int D, int NG) { return PSmem(D, NG).total; }
+
+cudaError_t launch_append(const DevCache &c, const __half *K, const __half *V, int64_t n, cudaStream_t s) {
+    switch (c.bits) {
+        case 2: append_kernel<2><<<1, AT, 0, s>>>(c, K, V, n); break;
+        case 3: append_kernel<3><<<1, AT, 0, s>>>(c, K, V, n); break;
+        case 4: append_kernel<4><<<1, AT, 0, s>>>(c, K, V, n); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_prefill(const DevCache &c, const __half *K, const __half *V, int64_t n0, int64_t T,
                            unsigned long long *lb, unsigned *ticket, cudaStream_t s) {
