@@ -225,7 +225,12 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     A(&d.counts, (size_t)d.cap * 4);
     // outlier buckets per (tile, attend head group); capacity ~3x the expected count
     {
-        const int hkv_g = attend_bucket_heads(C.bits, C.n_q_heads, G) / G;
+        // R23: an fp16-exact Value decode codebook lets the attend kernels skip their residual
+        // pass (and selects the warp-autonomous kernel at 4 bits, which has no residual pass)
+        d.vcb_exact16 = 1;
+        for (int j = 0; j < nlev; ++j)
+            if (__half2float(__float2half_rn(cbs[3][j])) != cbs[3][j]) d.vcb_exact16 = 0;
+        const int hkv_g = attend_bucket_heads(C.bits, C.n_q_heads, G, d.vcb_exact16) / G;
         d.GW = hkv_g * kHeadDim;
         d.NG = C.n_kv_heads / hkv_g;
         const double f = C.outlier_ppm / 1e6;
@@ -272,10 +277,6 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     double mids[32] = {0};
     for (int k = 0; k < 4; ++k)
         for (int j = 0; j < nlev; ++j) cb[16 * k + j] = cbs[k][j];
-    // R23: an fp16-exact Value decode codebook lets the attend kernel skip its residual pass
-    d.vcb_exact16 = 1;
-    for (int j = 0; j < nlev; ++j)
-        if (__half2float(__float2half_rn(cbs[3][j])) != cbs[3][j]) d.vcb_exact16 = 0;
     for (int j = 0; j + 1 < nlev; ++j) {
         mids[j] = (double)cbs[0][j] + (double)cbs[0][j + 1];
         mids[16 + j] = (double)cbs[2][j] + (double)cbs[2][j + 1];

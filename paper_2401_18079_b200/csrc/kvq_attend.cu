@@ -1098,8 +1098,9 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
 // Query heads per outlier bucket group (the quantizer's (tile, group) item lists): the
 // warp-autonomous MHA kernel reads one 2-head group per warp; the two-halves kernel uses
 // CTAs of exactly one group.
-int attend_bucket_heads(int bits, int H_q, int G) {
-    if (G == 1 && (bits == 2 || bits == 3) && H_q % 4 == 0) return 2;
+int attend_bucket_heads(int bits, int H_q, int G, int vcb_exact16) {
+    // MHA warp-autonomous kernel (4 bits only without the fp32-codebook residual pass)
+    if (G == 1 && (bits == 2 || bits == 3 || (bits == 4 && vcb_exact16)) && H_q % 4 == 0) return 2;
     if ((G == 2 || G == 4) && (bits == 2 || bits == 3)) return G;   // GQA kernel: one KV head
     return attend_heads_per_cta(bits, H_q, G);
 }

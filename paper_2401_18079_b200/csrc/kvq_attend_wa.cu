@@ -137,10 +137,14 @@ struct WCfg {
     static constexpr int NE = 1 << (2 * BITS);
     static constexpr int KWH = 4 * BITS;                  // code words per head per token
     static constexpr int HMAX = 8;                        // fp32 "heavy" pairs per head
+    // K table entries per (head, RoPE pair): 2-3 bits, one entry per pair code (the query and
+    // both channels folded in); 4 bits, per channel (16 + 16 entries, their two lookups summed
+    // by the FMAs), since a 256-entry pair table per pair would need 64 KB per head
+    static constexpr int NK = BITS == 4 ? 32 : NE;
     static constexpr size_t valign = (size_t)NE * 32 * 4;  // V table alignment (OR addressing)
     static constexpr size_t vlut = (size_t)(RESID ? 2 : 1) * NE * 32 * 4;
-    static constexpr size_t klut = (size_t)HG * kPairs * NE * 4;
-    static constexpr size_t hlut = (size_t)HG * HMAX * NE * 8;
+    static constexpr size_t klut = (size_t)HG * kPairs * NK * 4;
+    static constexpr size_t hlut = (size_t)HG * HMAX * NK * 8;
     static constexpr size_t t1h = 0;
     static constexpr size_t t1f = 0;   // (round 2: token angles from MUFU sin/cos, no table)
     // per warp: K words of the tile (cp.async target), K-outlier fixed-point terms (then p),
@@ -379,6 +383,28 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         }
     }
     __syncthreads();
+    if constexpr (BITS == 4) {
+        // per (head, pair): T1[a] = (qa x(a), qb x(a)) for channel i, T2[b] = (qb y(b), -qa y(b))
+        // for channel i + 64, so T1[a] + T2[b] is the pair table entry of the 2-3 bit kernels
+        for (int x = tid; x < HG * 64 * 32; x += NTHR) {
+            const int e = x & 31, gi = x >> 5;
+            const int g = gi >> 6, i = gi & 63;
+            const int ch = g * kHeadDim + i + (e < 16 ? 0 : 64);
+            const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
+            const float v = cbK[e & 15] * ks_s[ch] + kz_s[ch];
+            const float2 t = e < 16 ? make_float2(qa1 * v, qb1 * v) : make_float2(qb1 * v, -qa1 * v);
+            const bool heavy = heavy_s[gi] != 0;
+            if (heavy) {
+                int hslot = 0;
+                for (int u = 0; u < hv_n[g]; ++u) hslot = hv_pair[g * 8 + u] == i ? u : hslot;
+                klut[(size_t)gi * 32 + e] = 0u;
+                hlut[(g * HMAX + hslot) * 32 + e] = t;
+            } else {
+                const float sc = lut_sc[g];
+                klut[(size_t)gi * 32 + e] = pack_half2(t.x * sc, t.y * sc);
+            }
+        }
+    } else
     // K table entries [g][i][pair code], one (head, pair, second code) row per work item
     for (int x = tid; x < HG * 64 * (CM + 1); x += NTHR) {
         const int bb = x % (CM + 1), gi = x / (CM + 1);
@@ -425,7 +451,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
 
     // ================================================================ tile loop (per warp)
     // table bases, OR-ed with the shifted codes (the compiler must not turn the OR into an add)
-    const uint32_t klut_u = opaque(smem_u32(klut) + (uint32_t)(hw0 * 64 * NE * 4));
+    const uint32_t klut_u = opaque(smem_u32(klut) + (uint32_t)(hw0 * 64 * C::NK * 4));
     const uint32_t vlut_u = opaque(smem_u32(vlut) | (4u * lane));
     const int vg = lane >> 2, vt = lane & 3;
     const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
@@ -469,11 +495,13 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
 
         cp_async_wait_all();
         __syncwarp();
-        uint32_t kw[WH][KWH];
+        uint32_t kw[WH][BITS == 4 ? 1 : KWH];   // 4 bits: read from kst per word in the loop
+        if constexpr (BITS != 4) {
 #pragma unroll
-        for (int h = 0; h < WH; ++h)
+            for (int h = 0; h < WH; ++h)
 #pragma unroll
-            for (int w = 0; w < KWH; ++w) kw[h][w] = kst[(h * KWH + w) * 32 + lane];
+                for (int w = 0; w < KWH; ++w) kw[h][w] = kst[(h * KWH + w) * 32 + lane];
+        }
 
         // ---------------------------------------------------------- a2: K dense
         // two accumulator pairs per head (even / odd pairs): shorter FMA dependency chains
@@ -485,6 +513,22 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
             if (i == kPairs / 2) load_v();
             // cis(n' th_i) from the MUFU, rounded once to fp16
             const uint32_t cs = rot16(i);
+            if constexpr (BITS == 4) {
+                // pair i = byte i % 4 of word i / 4: code a (low nibble, channel i) and b (high
+                // nibble, channel i + 64), one lookup each in the pair's T1 / T2 halves
+                const int sh = 8 * (i & 3);
+#pragma unroll
+                for (int h = 0; h < WH; ++h) {
+                    if ((i & 3) == 0) kw[h][0] = kst[(h * KWH + (i >> 2)) * 32 + lane];
+                    const uint32_t w = kw[h][0];
+                    const uint32_t oa = (sh >= 2 ? (w >> (sh - 2)) : (w << 2)) & 0x3cu;
+                    const uint32_t ob = (w >> (sh + 2)) & 0x3cu;
+                    const uint32_t base = klut_u + (uint32_t)((h * 64 + i) * 32 * 4);
+                    const uint32_t t1 = lds_u32(base | oa), t2 = lds_u32(base | 64u | ob);
+                    fma2_f16_f32(t1, cs, acc_c[h][i & 1], acc_s[h][i & 1]);
+                    fma2_f16_f32(t2, cs, acc_c[h][i & 1], acc_s[h][i & 1]);
+                }
+            } else {
             const int bit = FB * i, w = bit >> 5, sh = bit & 31;
 #pragma unroll
             for (int h = 0; h < WH; ++h) {
@@ -494,6 +538,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                 const uint32_t a = klut_u | (off & ((NE - 1) << 2));
                 const uint32_t ab = lds_u32(a + (uint32_t)((h * 64 + i) * NE * 4));
                 fma2_f16_f32(ab, cs, acc_c[h][i & 1], acc_s[h][i & 1]);
+            }
             }
         }
         __syncwarp();
@@ -512,7 +557,13 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
                 // the word after may be past the head's last (then unused): kst is followed by
                 // the warp's other scratch, so the read stays in bounds
                 const int pc = (int)(__funnelshift_r(kst[wq * 32 + lane], kst[(wq + 1) * 32 + lane], bit & 31) & (NE - 1));
-                const float2 ab = hlut[(hc * HMAX + u) * NE + pc];
+                float2 ab;
+                if constexpr (BITS == 4) {
+                    const float2 t1 = hlut[(hc * HMAX + u) * 32 + (pc & 15)], t2 = hlut[(hc * HMAX + u) * 32 + 16 + (pc >> 4)];
+                    ab = make_float2(t1.x + t2.x, t1.y + t2.y);
+                } else {
+                    ab = hlut[(hc * HMAX + u) * NE + pc];
+                }
                 float co, si;
                 rot32(i, lane, co, si);
                 hs += co * ab.x + si * ab.y;
@@ -1627,13 +1678,14 @@ cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cud
 }
 
 bool attend_wa_supported(const DevCache &c) {
-    return c.G == 1 && (c.bits == 2 || c.bits == 3) && c.H_q % HG == 0 &&
-           c.GW == 2 * kHeadDim;   // outlier buckets per 2-head group (one per warp)
+    return c.G == 1 && (c.bits == 2 || c.bits == 3 || (c.bits == 4 && c.vcb_exact16)) &&
+           c.H_q % HG == 0 && c.GW == 2 * kHeadDim;   // outlier buckets per 2-head group (one per warp)
 }
 
 size_t attend_wa_smem_bytes(int bits, bool resid) {
     if (bits == 2) return resid ? WCfg<2, true, 2>::total : WCfg<2, false, 2>::total;  // WH = 2
     if (bits == 3) return resid ? WCfg<3, true, 2>::total : WCfg<3, false, 2>::total;
+    if (bits == 4) return WCfg<4, false, 2>::total;
     return 0;
 }
 
@@ -1646,6 +1698,7 @@ cudaError_t launch_attend_wa(const DevCache &c, const AttendArgs &a, int S, cuda
     const bool resid = !c.vcb_exact16;
     if (c.bits == 2) return resid ? launch_wa_r<2, true>(c, P, grid, s) : launch_wa_r<2, false>(c, P, grid, s);
     if (c.bits == 3) return resid ? launch_wa_r<3, true>(c, P, grid, s) : launch_wa_r<3, false>(c, P, grid, s);
+    if (c.bits == 4 && !resid) return launch_wa_r<4, false>(c, P, grid, s);
     return cudaErrorInvalidValue;
 }
 

@@ -133,7 +133,7 @@ struct AttendArgs {
                          // (their q/table prologue overlaps the append; cache reads wait)
 };
 int attend_heads_per_cta(int bits, int H_q, int G);
-int attend_bucket_heads(int bits, int H_q, int G);
+int attend_bucket_heads(int bits, int H_q, int G, int vcb_exact16);
 int attend_auto_splits(const DevCache &c, int64_t T, int hg);
 cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_used,
                           cudaStream_t s);

@@ -128,7 +128,8 @@ def test_host_buffers_are_staged(kvq):
                                              (8, 8, 2, 517), (8, 2, 3, 300), (4, 1, 3, 129),
                                              (16, 16, 3, 700), (32, 8, 3, 257),
                                              (8, 4, 3, 301), (16, 8, 2, 400), (32, 16, 3, 96),
-                                             (40, 40, 3, 130), (32, 8, 2, 333)])
+                                             (40, 40, 3, 130), (32, 8, 2, 333),
+                                             (8, 8, 4, 1000), (32, 32, 4, 300)])
 def test_attend_matches_oracle(kvq, H_q, H_kv, bits, T):
     ppm = 10_000
     cal, K, V = setup_layer(4, 0, H_q, H_kv, bits, ppm, T)
@@ -180,7 +181,8 @@ def test_attend_independent_of_split_count(kvq, splits):
 
 @pytest.mark.parametrize("H_q,H_kv,bits,base", [(2, 2, 3, 9_999_000), (8, 8, 3, 9_990_017),
                                                 (32, 8, 3, 9_990_000), (8, 4, 3, 9_999_500),
-                                                (8, 8, 2, 8_750_000), (32, 8, 2, 8_750_000)])
+                                                (8, 8, 2, 8_750_000), (32, 8, 2, 8_750_000),
+                                                (8, 8, 4, 9_990_001)])
 def test_long_positions_exact_angles(kvq, H_q, H_kv, bits, base):
     """pos_base near 10M (C5 shards start at 8.75M for P = 8): RoPE angles must be reduced
     exactly (reading R12) in every attend kernel -- the two-halves kernel (H = 2), the MHA
@@ -338,7 +340,7 @@ def _extreme_layer(seed, H_q, H_kv, bits, ppm, T, kind):
     return cal, K.astype(np.float16), V.astype(np.float16)
 
 
-@pytest.mark.parametrize("H_q,H_kv,bits", [(8, 8, 3), (32, 8, 3), (2, 2, 4), (8, 8, 2)])
+@pytest.mark.parametrize("H_q,H_kv,bits", [(8, 8, 3), (32, 8, 3), (2, 2, 4), (8, 8, 2), (8, 8, 4)])
 @pytest.mark.parametrize("kind,ppm", [("flat_values", 0), ("flat_values", 10_000),
                                       ("huge_value_outliers", 10_000),
                                       ("huge_key_outliers", 10_000)])
@@ -370,7 +372,7 @@ def test_attend_extreme_inputs(kvq, H_q, H_kv, bits, kind, ppm):
         assert err.max() < TOL, err
 
 
-@pytest.mark.parametrize("H_q,H_kv,bits", [(8, 8, 3), (32, 8, 3), (8, 8, 2), (2, 2, 4)])
+@pytest.mark.parametrize("H_q,H_kv,bits", [(8, 8, 3), (32, 8, 3), (8, 8, 2), (2, 2, 4), (8, 8, 4)])
 def test_append_then_attend_sees_new_token_pdl(kvq, H_q, H_kv, bits):
     """Decode order with programmatic dependent launch (KVQ_FLAG_DECODE_PDL): each attend is
     enqueued right after the append of the token it must see, with no host sync, across the
