@@ -441,10 +441,15 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
     }
     __syncthreads();
 
-    // cache contents from here on (the preceding append must be complete); a first tile that is
-    // not the tail tile (the only one an append writes) was issued before the prologue
-    pdl_wait();
+    // The preceding append (programmatic dependent launch) writes only the tail tile (its
+    // token's code words, (s, z), outlier records, bucket items and counts), so a warp waits
+    // for it only before its first read of tail-tile data; every other tile streams while the
+    // append is still running.  (Without the launch attribute the wait is a no-op.)
+    auto tail_wait = [&](int tt) {
+        if (tt == P.ntiles - 1) pdl_wait();
+    };
     if (t_first < t_end && !early) {
+        tail_wait(t_first);
         issue_k(t_first);
         load_counts(t_first, cnt_k, cnt_v);
     }
@@ -480,6 +485,7 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         const int nk = kov ? 0 : (int)cnt_k, nv = vov ? 0 : (int)cnt_v;
         // this tile's outlier items and (s, z) (consumed after the K loop), next tile's counts
         load_items(t);
+        tail_wait(t + NSTREAM);
         load_counts(t + NSTREAM, ncnt_k, ncnt_v);
 
         // V words of this tile: in flight during the K phase
@@ -626,7 +632,10 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
 
         // kst is free (heavy pairs and Key items done): the next tile's K words
         const int tn = t + NSTREAM;
-        if (tn < t_end) issue_k(tn);
+        if (tn < t_end) {
+            tail_wait(tn);
+            issue_k(tn);
+        }
 
         // ------------------------------------------------------ a4: online softmax
         // weights p s_n 2^(WEXP - E) with E from the tile's largest s_n (fp16 normal range)
