@@ -75,6 +75,8 @@ def _load():
     lib.kvo_quantize_value.restype = ctypes.c_int
     lib.kvo_quantize_value.argtypes = [P_u16, ctypes.c_int, ctypes.c_int, P_f32, ctypes.c_int,
                                        ctypes.c_int, P_u16, P_i32, P_u16, P_f32, P_f32]
+    lib.kvo_key_thresholds_online.restype = ctypes.c_int
+    lib.kvo_key_thresholds_online.argtypes = [ctypes.c_int64, ctypes.c_int, P_u16, ctypes.c_int, P_f32, P_f32]
     lib.kvo_f64_to_f16.restype = ctypes.c_uint16
     lib.kvo_f64_to_f16.argtypes = [ctypes.c_double]
     lib.kvo_f16cache_key.argtypes = [P_u16, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_double, P_u16]
@@ -273,6 +275,20 @@ def merge(parts) -> np.ndarray:
 def attend(cache: CanonCache, q, pos: int, **kw) -> np.ndarray:
     """o [H_q, d] = merged single partial."""
     return merge(attend_partial(cache, q, pos, **kw)[None])
+
+
+# --------------------------------------------- online per-channel Key thresholds (f2) ---
+def key_thresholds_online(K, ppm: int):
+    """Per-channel (lo, hi) fp32 from the Keys of a prefill block [T, D] ("Online for K",
+    P:1036-1064): order statistics floor(n/2) and T-1-ceil(n/2), n = ceil(ppm T / 1e6)."""
+    Kb = _f16bits(K)
+    T, D = Kb.shape
+    lo = np.zeros(D, np.float32)
+    hi = np.zeros(D, np.float32)
+    rc = _load().kvo_key_thresholds_online(T, D, _p(Kb, P_u16), int(ppm), _p(lo, P_f32), _p(hi, P_f32))
+    if rc != 0:
+        raise ValueError("too many outliers for the block")
+    return lo, hi
 
 
 # ------------------------------------------------------ fp16 comparator cache (F16) ---

@@ -23,6 +23,8 @@
  *                            dequantized V^_t; uniform scores -> mean of
  *                            hand-dequantized V^ incl. a lower-index tie)
  *   merge           pinned  (any partition == unsplit)
+ *   key thresholds  pinned  (online: numpy sort order statistics; brute-force outlier
+ *    (online)               counts per channel; the two-sided kept range of S:328-333)
  *   f64_to_f16      pinned  (numpy's IEEE round-to-nearest-even float16 conversion,
  *                            including ties, subnormals and overflow)
  *   f16cache_key    pinned  (== f64_to_f16 of the pinned kvo_rope; position 0 == identity)
@@ -363,6 +365,33 @@ void kvo_merge(int P, int H, int d, const double *parts, double *o) {
         }
         for (int c = 0; c < d; ++c) og[c] /= l;
     }
+}
+
+/* ------------------------------------------- online per-channel Key thresholds ---- */
+/* "Online for K" (tab:calibration): the per-channel Key outlier
+ * thresholds and scaling factors computed from the Keys being quantized instead of offline
+ * calibration data.  Per channel c over the T tokens of a block: n = ceil(f T) outliers
+ * (integer ceil from ppm, reading R2), the ceil(n/2) largest and floor(n/2) smallest excluded
+ * (two-sided, reading R3), lo_c / hi_c = the smallest / largest kept value -- i.e. the
+ * floor(n/2)-th and (T-1-ceil(n/2))-th order statistics.  -0 is returned as +0 (R3). */
+static int cmp_f64(const void *a, const void *b) {
+    double x = *(const double *)a, y = *(const double *)b;
+    return (x > y) - (x < y);
+}
+int kvo_key_thresholds_online(int64_t T, int D, const uint16_t *K, int ppm, float *lo, float *hi) {
+    int64_t n = (int64_t)(((int64_t)ppm * T + 999999) / 1000000);
+    int64_t ku = (n + 1) / 2, kl = n / 2;
+    if (T < 1 || ku + kl >= T) return -1;
+    double *col = (double *)malloc(sizeof(double) * (size_t)T);
+    for (int c = 0; c < D; ++c) {
+        for (int64_t t = 0; t < T; ++t) col[t] = kvo_f16_to_f64(K[(size_t)t * D + c]);
+        qsort(col, (size_t)T, sizeof(double), cmp_f64);
+        double l = col[kl], h = col[T - 1 - ku];
+        lo[c] = (float)(l == 0.0 ? 0.0 : l);
+        hi[c] = (float)(h == 0.0 ? 0.0 : h);
+    }
+    free(col);
+    return 0;
 }
 
 /* ------------------------------------------------------ fp16 comparator cache ---- */

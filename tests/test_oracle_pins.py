@@ -434,3 +434,28 @@ def test_prefill_equals_successive_appends():
         c2, i2, v2, s, z = O.quantize_value(V[n], 125_000, cb)
         assert np.array_equal(full.vcodes[n], c2) and np.array_equal(full.vidx[n], i2)
         assert full.vs[n] == s and full.vz[n] == z
+
+
+# ------------------------------------------------ online Key thresholds (f2) pins --
+@pytest.mark.parametrize("T,D,ppm", [(97, 8, 10_000), (2048, 16, 10_000), (300, 4, 50_000), (50, 3, 0)])
+def test_online_key_thresholds_order_statistics(T, D, ppm):
+    """lo / hi = the floor(n/2)-th smallest and ceil(n/2)-th largest excluded -> numpy's sort
+    (a library routine), and brute force: exactly ceil(n/2) values of the channel lie strictly
+    above hi or tie into the excluded set, floor(n/2) below lo likewise."""
+    rng = np.random.default_rng(T + D)
+    K = (rng.standard_t(3, size=(T, D)) * 2.0).astype(np.float16)
+    K[T // 3, 0] = np.float16(-0.0)
+    lo, hi = O.key_thresholds_online(K, ppm)
+    n = (ppm * T + 999_999) // 1_000_000
+    ku, kl = (n + 1) // 2, n // 2
+    srt = np.sort(K.astype(np.float64), axis=0)
+    np.testing.assert_array_equal(lo, srt[kl].astype(np.float32) + 0.0)
+    np.testing.assert_array_equal(hi, srt[T - 1 - ku].astype(np.float32) + 0.0)
+    for c in range(D):
+        x = K[:, c].astype(np.float64)
+        assert (x > hi[c]).sum() <= ku and (x >= hi[c]).sum() >= ku + 1
+        assert (x < lo[c]).sum() <= kl and (x <= lo[c]).sum() >= kl + 1
+    # the worked example of S:328-333 read per channel: {2, 4} excluded, kept range [-0.2, 0.3]
+    v = np.array([0.1, -0.2, 5.0, 0.3, -4.0, 0.0], np.float16)[:, None]
+    lo1, hi1 = O.key_thresholds_online(v, 333_333)   # ceil(6 f) = 2
+    assert float(lo1[0]) == float(np.float16(-0.2)) and float(hi1[0]) == float(np.float16(0.3))
