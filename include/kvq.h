@@ -133,6 +133,16 @@ kvq_status kvq_decode_attend(kvq_cache *cache, const void *q_f16, int64_t pos, f
 kvq_status kvq_decode_attend_partial(kvq_cache *cache, const void *q_f16, int64_t pos,
                                      float *part, void *stream);
 
+/* Batched decode (the paper's BS = 4 rows): one decode step for B
+ * independent sequences, each with its own cache, query q[i] ([H_q][d] fp16, device), position
+ * pos[i] and output o[i] ([H_q][d] fp32, device).  When every cache is attended by the
+ * warp-autonomous MHA kernel with the same bits / codebook kind / head shape and B <= 64, the
+ * B attends are ONE launch whose CTAs are split over the sequences in proportion to their
+ * lengths (one wave for many short contexts instead of B latency-bound launches); otherwise
+ * (other shapes) it is B ordinary attends.  Same errors per sequence as kvq_decode_attend. */
+kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const void *const *q,
+                                   const int64_t *pos, float *const *o, void *stream);
+
 /* Exact log-sum-exp merge of P partials (fixed order 0..P-1), the merge step of the
  * north_star's sequence sharding:
  *   m = max_i m_i;  l = sum_i 2^(m_i - m) l_i;  o = sum_i 2^(m_i - m) o_i / l
@@ -198,6 +208,17 @@ kvq_status kvq_set_splits(kvq_cache *cache, int32_t splits);
  * out[6..8] / out[9..11]: wait / compaction / TMA issue of the two producer warps), summed
  * over CTAs.  Only when the process was started with KVQ_PHASE_TIMERS=1. */
 kvq_status kvq_phase_timers(kvq_cache *cache, uint64_t *out /* host [16] */);
+
+/* Online per-channel Key thresholds ("Online for K", tab:calibration
+ * P:1036-1064): lo_c / hi_c computed on the GPU from the Keys of a prefill block rather
+ * than offline calibration data.  Per channel over the T tokens: n = ceil(ppm T / 1e6)
+ * outliers, the ceil(n/2) largest and floor(n/2) smallest excluded (R2, R3); lo_c / hi_c =
+ * the smallest / largest kept value (the floor(n/2)-th and (T-1-ceil(n/2))-th order statistics;
+ * -0 returned as +0).  K_f16 [T][D] fp16 pre-RoPE Keys (device or host); key_lo, key_hi [D]
+ * fp32 (device or host; host outputs make the call synchronous).  The result is meant for
+ * kvq_cache_create's kvq_params.key_lo / key_hi.  KVQ_EINVAL when 2 ceil(n/2) >= T. */
+kvq_status kvq_key_thresholds_online(const void *K_f16, int64_t T, int32_t D, int32_t outlier_ppm,
+                                     float *key_lo, float *key_hi, int32_t device, void *stream);
 
 /* ------------------------------------------------------------------------------------
  * fp16 comparator cache (BASELINE config C3 "4-bit vs 3-bit vs fp16 cache"): the paper's

@@ -9,7 +9,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkvq.so")
-SOURCES = ["kvq_api.cu", "kvq_prefill.cu", "kvq_f16.cu", "kvq_attend.cu", "kvq_attend_wa.cu"]
+SOURCES = ["kvq_api.cu", "kvq_prefill.cu", "kvq_f16.cu", "kvq_calib.cu", "kvq_attend.cu", "kvq_attend_wa.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"]

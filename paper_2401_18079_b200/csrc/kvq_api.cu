@@ -503,6 +503,57 @@ kvq_status kvq_decode_attend_partial(kvq_cache *c, const void *q, int64_t pos, f
     return attend_impl(c, q, pos, part, 1, stream);
 }
 
+kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const void *const *q, const int64_t *pos,
+                                   float *const *o, void *stream) {
+    if (!caches || !q || !pos || !o) return fail(KVQ_EINVAL, "null argument");
+    if (B < 1) return fail(KVQ_EINVAL, "B must be >= 1");
+    for (int i = 0; i < B; ++i) {
+        if (!caches[i] || !q[i] || !o[i]) return fail(KVQ_EINVAL, "null cache, q or o at %d", i);
+        if (pos[i] < 0) return fail(KVQ_EINVAL, "negative position at %d", i);
+        if (caches[i]->T == 0) return fail(KVQ_EEMPTY, "attend on an empty cache (sequence %d)", i);
+        if (caches[i]->cfg.device != caches[0]->cfg.device) return fail(KVQ_EDEVICE, "caches on different devices");
+        kvq_status st = check_sticky(caches[i]);
+        if (st != KVQ_OK) return st;
+    }
+    bool one_launch = B <= attend_batch_max();
+    const DevCache &d0 = caches[0]->dc;
+    for (int i = 0; i < B && one_launch; ++i) {
+        const DevCache &d = caches[i]->dc;
+        one_launch = attend_wa_supported(d) && d.bits == d0.bits && d.vcb_exact16 == d0.vcb_exact16 &&
+                     d.H_q == d0.H_q && d.H_kv == d0.H_kv;
+    }
+    if (!one_launch) {   // shapes the batched kernel does not cover: one attend per cache
+        for (int i = 0; i < B; ++i) {
+            kvq_status st = attend_impl(caches[i], q[i], pos[i], o[i], 0, stream);
+            if (st != KVQ_OK) return st;
+        }
+        return KVQ_OK;
+    }
+    const int dev = caches[0]->cfg.device;
+    CK(cudaSetDevice(dev));
+    std::vector<const DevCache *> cs((size_t)B);
+    std::vector<AttendArgs> as((size_t)B);
+    std::vector<int> splits((size_t)B);
+    for (int i = 0; i < B; ++i) {
+        kvq_cache *c = caches[i];
+        if (classify(q[i], dev, c->cfg.flags) != 0 || classify(o[i], dev, c->cfg.flags) != 0)
+            return fail(KVQ_EDEVICE, "batched attend takes device q / o on device %d (sequence %d)", dev, i);
+        cs[(size_t)i] = &c->dc;
+        AttendArgs &a = as[(size_t)i];
+        a = AttendArgs{};
+        a.q = (const __half *)q[i]; a.pos = pos[i]; a.T = c->T; a.out = o[i]; a.write_partial = 0;
+        a.parts = c->parts; a.tickets = c->tickets; a.splits = c->splits_forced;
+    }
+    cudaError_t e = launch_attend_wa_batch(cs.data(), as.data(), B, (cudaStream_t)stream, splits.data());
+    if (e != cudaSuccess) return cuda_fail(e, "batched attend launch");
+    for (int i = 0; i < B; ++i) {
+        caches[i]->last_splits = splits[(size_t)i];
+        caches[i]->last_kernel = 1;
+        caches[i]->pdl_ok = 0;
+    }
+    return KVQ_OK;
+}
+
 kvq_status kvq_merge_partials(const float *parts, int32_t P, int32_t H, int32_t d, float *o,
                               int32_t device, void *stream) {
     if (!parts || !o) return fail(KVQ_EINVAL, "null argument");
@@ -623,6 +674,39 @@ kvq_status kvq_export(kvq_cache *c, int64_t t0, int64_t t1, kvq_export_buf *buf)
             }
         }
     }
+    return KVQ_OK;
+}
+
+// ------------------------------------------------ online per-channel Key thresholds --
+kvq_status kvq_key_thresholds_online(const void *K, int64_t T, int32_t D, int32_t ppm, float *key_lo,
+                                     float *key_hi, int32_t device, void *stream) {
+    if (!K || !key_lo || !key_hi) return fail(KVQ_EINVAL, "null argument");
+    if (T < 1 || D < 1) return fail(KVQ_EINVAL, "T and D must be >= 1");
+    if (ppm < 0 || ppm >= 500000) return fail(KVQ_EINVAL, "outlier_ppm must be in [0, 500000)");
+    const int64_t n = ((int64_t)ppm * T + 999999) / 1000000;
+    if ((n + 1) / 2 + n / 2 >= T) return fail(KVQ_EINVAL, "too many outliers (%lld) for %lld tokens", (long long)n, (long long)T);
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(KVQ_EDEVICE, "device %d not present", device);
+    CK(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int ck = classify(K, device, 0), cl = classify(key_lo, device, 0), ch = classify(key_hi, device, 0);
+    if (ck < 0 || cl < 0 || ch < 0) return fail(KVQ_EDEVICE, "pointer not on device %d", device);
+    const size_t kb = (size_t)T * D * 2, ob = (size_t)D * 4;
+    void *tmp = nullptr;
+    const size_t need = (ck == 1 ? kb : 0) + 2 * ob + 256;
+    CK(cudaMallocAsync(&tmp, need, s));
+    char *tp = (char *)tmp;
+    const __half *Kd = (const __half *)K;
+    if (ck == 1) { CK(cudaMemcpyAsync(tp, K, kb, cudaMemcpyHostToDevice, s)); Kd = (const __half *)tp; tp += (kb + 255) / 256 * 256; }
+    float *lo = cl == 1 ? (float *)tp : key_lo;
+    float *hi = ch == 1 ? (float *)(tp + ob) : key_hi;
+    cudaError_t e = launch_online_key_thresholds(Kd, T, D, ppm, lo, hi, s);
+    if (e != cudaSuccess) { cudaFreeAsync(tmp, s); return cuda_fail(e, "online thresholds launch"); }
+    if (cl == 1) CK(cudaMemcpyAsync(key_lo, lo, ob, cudaMemcpyDeviceToHost, s));
+    if (ch == 1) CK(cudaMemcpyAsync(key_hi, hi, ob, cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(tmp, s));
+    if (cl == 1 || ch == 1) CK(cudaStreamSynchronize(s));
     return KVQ_OK;
 }
 

@@ -190,8 +190,9 @@ cudaError_t launch_maybe_pdl(K kernel, int grid, int threads, size_t smem, cudaS
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// the kernel body; blk is the CTA's index within its own attend (one cache)
 template <int BITS, bool RESID, int WH>
-__global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(DevCache c, WParams P) {
+__device__ __forceinline__ void att_wa_body(const DevCache &c, const WParams &P, const int blk) {
     using C = WCfg<BITS, RESID, WH>;
     constexpr int NWARP = C::NWARP, NTHR = C::NTHR, IPL = C::IPL;
     constexpr int NE = C::NE;
@@ -229,8 +230,8 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_hg = c.H_q / HG;
-    const int hg = blockIdx.x % n_hg;
-    const int split = blockIdx.x / n_hg;
+    const int hg = blk % n_hg;
+    const int split = blk / n_hg;
     const int g0 = hg * HG;               // first query head of the CTA = first KV head (G = 1)
     const int hw0 = (warp % (HG / WH)) * WH;   // this warp's first head within the CTA
     const int c_lo = g0 * kHeadDim;
@@ -918,6 +919,31 @@ __global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(
         }
     }
     if (tid == 0) P.tickets[hg] = 0;
+}
+
+template <int BITS, bool RESID, int WH>
+__global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_kernel(DevCache c, WParams P) {
+    att_wa_body<BITS, RESID, WH>(c, P, (int)blockIdx.x);
+}
+
+// Batched decode: one launch attends B independent caches of the same
+// configuration (each its own context length, scratch and output).  The per-sequence
+// descriptors travel in the kernel parameter space (constant bank, indexed by the CTA's
+// sequence); CTA ranges are consecutive per sequence.
+constexpr int kMaxBatch = 64;
+struct WBatch {
+    int n;
+    int cta0[kMaxBatch + 1];
+    DevCache c[kMaxBatch];
+    WParams p[kMaxBatch];
+};
+
+template <int BITS, bool RESID, int WH>
+__global__ void __launch_bounds__(WCfg<BITS, RESID, WH>::NTHR, 1) att_wa_batch_kernel(const __grid_constant__ WBatch b) {
+    const int blk = (int)blockIdx.x;
+    int s = 0;
+    while (s + 1 < b.n && blk >= b.cta0[s + 1]) ++s;
+    att_wa_body<BITS, RESID, WH>(b.c[s], b.p[s], blk - b.cta0[s]);
 }
 
 template <int BITS, bool RESID, int WH>
@@ -1683,6 +1709,57 @@ cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cud
     const bool resid = !c.vcb_exact16;
     if (c.bits == 2) return resid ? launch_wag_g<2, true>(c, P, grid, s) : launch_wag_g<2, false>(c, P, grid, s);
     if (c.bits == 3) return resid ? launch_wag_g<3, true>(c, P, grid, s) : launch_wag_g<3, false>(c, P, grid, s);
+    return cudaErrorInvalidValue;
+}
+
+template <int BITS, bool RESID>
+cudaError_t launch_wa_batch_t(const WBatch &b, int grid, cudaStream_t s) {
+    using C = WCfg<BITS, RESID, 2>;
+    cudaError_t e = cudaFuncSetAttribute(att_wa_batch_kernel<BITS, RESID, 2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::total);
+    if (e != cudaSuccess) return e;
+    att_wa_batch_kernel<BITS, RESID, 2><<<grid, C::NTHR, C::total, s>>>(b);
+    return cudaGetLastError();
+}
+
+int attend_batch_max() { return kMaxBatch; }
+
+cudaError_t launch_attend_wa_batch(const DevCache *const *cs, const AttendArgs *as, int B, cudaStream_t s,
+                                   int *splits_out) {
+    if (B < 1 || B > kMaxBatch) return cudaErrorInvalidValue;
+    static WBatch b;   // large: build on the host once per call (not thread-safe across host threads)
+    WBatch &bb = b;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t tiles_all = 0;
+    for (int i = 0; i < B; ++i) tiles_all += (as[i].T + 31) / 32;
+    bb.n = B;
+    int cta = 0;
+    for (int i = 0; i < B; ++i) {
+        const DevCache &c = *cs[i];
+        const int n_hg = c.H_q / HG;
+        const int ntiles = (int)((as[i].T + 31) / 32);
+        // splits in proportion to the sequence's share of all tiles, so the launch fills one
+        // wave of one CTA per SM (at least one split per head group)
+        int S = (int)((int64_t)sms * ntiles / (tiles_all * n_hg));
+        if (as[i].splits > 0) S = as[i].splits;
+        S = S < 1 ? 1 : (S > ntiles ? ntiles : S);
+        WParams &P = bb.p[i];
+        P = WParams{};
+        P.q = as[i].q; P.pos = as[i].pos; P.T = as[i].T; P.S = S; P.ntiles = ntiles;
+        P.out = as[i].out; P.parts = as[i].parts; P.tickets = as[i].tickets; P.write_partial = as[i].write_partial;
+        P.pdl = 0;
+        bb.c[i] = c;
+        bb.cta0[i] = cta;
+        cta += n_hg * S;
+        if (splits_out) splits_out[i] = S;
+    }
+    bb.cta0[B] = cta;
+    const DevCache &c0 = *cs[0];
+    const bool resid = !c0.vcb_exact16;
+    if (c0.bits == 2) return resid ? launch_wa_batch_t<2, true>(bb, cta, s) : launch_wa_batch_t<2, false>(bb, cta, s);
+    if (c0.bits == 3) return resid ? launch_wa_batch_t<3, true>(bb, cta, s) : launch_wa_batch_t<3, false>(bb, cta, s);
+    if (c0.bits == 4 && !resid) return launch_wa_batch_t<4, false>(bb, cta, s);
     return cudaErrorInvalidValue;
 }
 

@@ -115,6 +115,10 @@ int f16_auto_splits(const F16Dev &c, int64_t T);
 cudaError_t launch_f16_attend(const F16Dev &c, const __half *q, int64_t pos, int64_t T, float *out,
                               float *parts, unsigned *tickets, int S, cudaStream_t s);
 
+// ---- online per-channel Key thresholds (kvq_calib.cu) ----
+cudaError_t launch_online_key_thresholds(const __half *K, int64_t T, int D, int ppm, float *lo, float *hi,
+                                         cudaStream_t s);
+
 // ---- attention (kvq_attend.cu) ----
 struct AttendArgs {
     const __half *q;
@@ -143,6 +147,11 @@ size_t attend_smem_bytes(int bits, int hg);
 bool attend_wa_supported(const DevCache &c);
 size_t attend_wa_smem_bytes(int bits, bool resid);
 cudaError_t launch_attend_wa(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s);
+// batched decode over B caches of one configuration (all attend_wa_supported, same bits and
+// codebook kind): one launch
+int attend_batch_max();
+cudaError_t launch_attend_wa_batch(const DevCache *const *cs, const AttendArgs *as, int B, cudaStream_t s,
+                                   int *splits_out);
 // warp-autonomous GQA variant (G = 4, 2-3 bits): one CTA per KV head
 bool attend_wag_supported(const DevCache &c);
 cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s);

@@ -30,7 +30,8 @@ EXPORTED = ["kvq_cache_create", "kvq_cache_destroy", "kvq_append", "kvq_prefill_
             "kvq_num_tokens", "kvq_reset", "kvq_sync", "kvq_key_outlier_span", "kvq_export",
             "kvq_get_info", "kvq_set_splits", "kvq_phase_timers", "kvq_last_error", "kvq_version",
             "kvq_f16_cache_create", "kvq_f16_cache_destroy", "kvq_f16_append",
-            "kvq_f16_decode_attend", "kvq_f16_export", "kvq_f16_num_tokens"]
+            "kvq_f16_decode_attend", "kvq_f16_export", "kvq_f16_num_tokens",
+            "kvq_key_thresholds_online", "kvq_decode_attend_batch"]
 
 
 class KVQError(RuntimeError):
@@ -98,6 +99,8 @@ def _load() -> ctypes.CDLL:
         "kvq_f16_decode_attend": (i32, [vp, vp, i64, vp, vp]),
         "kvq_f16_export": (i32, [vp, i64, i64, vp, vp]),
         "kvq_f16_num_tokens": (i64, [vp]),
+        "kvq_key_thresholds_online": (i32, [vp, i64, i32, i32, vp, vp, i32, vp]),
+        "kvq_decode_attend_batch": (i32, [vp, i32, vp, vp, vp, vp]),
         "kvq_version": (i32, []),
     }
     for name, (res, args) in sig.items():
@@ -264,6 +267,33 @@ class KVQCache:
         out["vidx"] = out["vidx"][:, :kv]
         out["vval"] = out["vval"][:, :kv]
         return out
+
+
+def attend_batch(caches, qs, positions, outs, stream=None):
+    """Batched decode (kvq_decode_attend_batch): caches[i] attends qs[i] at positions[i] into
+    outs[i] (device tensors), one launch when the caches share a configuration."""
+    B = len(caches)
+    hs = (ctypes.c_void_p * B)(*[c.handle.value for c in caches])
+    qp = (ctypes.c_void_p * B)(*[_ptr(q).value for q in qs])
+    op = (ctypes.c_void_p * B)(*[_ptr(o).value for o in outs])
+    pp = (ctypes.c_int64 * B)(*[int(p) for p in positions])
+    _check(_lib.kvq_decode_attend_batch(ctypes.cast(hs, ctypes.c_void_p), B, ctypes.cast(qp, ctypes.c_void_p),
+                                        ctypes.cast(pp, ctypes.c_void_p), ctypes.cast(op, ctypes.c_void_p),
+                                        _stream(stream)))
+    return outs
+
+
+def key_thresholds_online(K, outlier_ppm: int, lo=None, hi=None, device: int = 0, stream=None):
+    """Per-channel Key (lo, hi) from a prefill block K [T, D] fp16 on the GPU.
+    Outputs default to host numpy arrays (the call then synchronizes)."""
+    T, D = (int(x) for x in K.shape)
+    if lo is None:
+        lo = np.zeros(D, np.float32)
+    if hi is None:
+        hi = np.zeros(D, np.float32)
+    _check(_lib.kvq_key_thresholds_online(_ptr(K), T, D, int(outlier_ppm), _ptr(lo), _ptr(hi), int(device),
+                                          _stream(stream)))
+    return lo, hi
 
 
 class F16Cache:
