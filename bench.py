@@ -550,6 +550,63 @@ def run_ours(args):
             compare["speedup_vs_f16"] = compare["f16"]["attend_us_per_layer"] / (att_ms * 1e3)
         except Exception as ex:   # pragma: no cover
             compare["error"] = str(ex)[:300]
+    # batched decode of 32 LLaMA-7B-layer sequences x 4096 tokens, one launch
+    # (kvq_decode_attend_batch) vs 32 separate attends; f2: online Key thresholds of the
+    # layer-0 prefill block
+    batch = None
+    online = None
+    if world == 1 and not args.no_compare and w.name.startswith("c3"):
+        try:
+            nb, tb = 32, 4096
+            bc = build_caches(kvq, gen, w, cal, nb, tb, 0, tb + 8, dev, 9000, 0)
+            gq2 = torch.Generator(device=dev)
+            gq2.manual_seed(99)
+            qb = [(torch.randn((H, d), generator=gq2, device=dev) * 0.5).half() for _ in range(nb)]
+            ob = [torch.zeros((H, d), dtype=torch.float32, device=dev) for _ in range(nb)]
+            pb = [tb] * nb
+
+            def launch_batched(st):
+                kvq.attend_batch(bc, qb, pb, ob, st)
+
+            def launch_each(st):
+                for i in range(nb):
+                    bc[i].attend(qb[i], tb, ob[i], st)
+            launch_batched(stream)
+            launch_each(stream)
+            pb1, g1 = graph_replay_times(launch_batched, 1, stream, 50)
+            pe1, g2 = graph_replay_times(launch_each, 1, stream, 50)
+            tb_us, te_us = stats(pb1)["median"] * 1e3, stats(pe1)["median"] * 1e3
+            kv_b = bc[0].info()["value_outliers"]
+            nbytes = sum(accounting.attend_bytes(tb, D, w.bits, kv_b, e - b0_, H, d)
+                         for b0_, e in (c.key_outlier_span(0, c.num_tokens) for c in bc))
+            batch = {"sequences": nb, "tokens_each": tb, "batched_us_per_step": tb_us,
+                     "separate_us_per_step": te_us, "speedup": te_us / tb_us,
+                     "batched_frac": nbytes / (tb_us * 1e-6) / 1e9 / peak, "graph": g1 and g2,
+                     "note": "one kvq_decode_attend_batch launch vs 32 kvq_decode_attend launches, "
+                             "both CUDA-graph replayed; per-step time for all 32 sequences of one layer"}
+            del bc
+            torch.cuda.empty_cache()
+        except Exception as ex:   # pragma: no cover
+            batch = {"error": str(ex)[:300]}
+        try:
+            Kl = gen.gen_layer_torch(31 * rank, 0, min(n_local, 1 << 17), D, dev, "K")
+            lo_d = torch.zeros(D, dtype=torch.float32, device=dev)
+            hi_d = torch.zeros(D, dtype=torch.float32, device=dev)
+            kvq.key_thresholds_online(Kl, w.ppm, lo_d, hi_d, device=local, stream=stream)
+            o0, o1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            o0.record(stream)
+            for _ in range(5):
+                kvq.key_thresholds_online(Kl, w.ppm, lo_d, hi_d, device=local, stream=stream)
+            o1.record(stream)
+            o1.synchronize()
+            ms = o0.elapsed_time(o1) / 5
+            online = {"tokens": int(Kl.shape[0]), "ms": ms, "ns_per_token_layer": ms * 1e6 / Kl.shape[0],
+                      "gbs": 2 * Kl.numel() * 2 / (ms * 1e-3) / 1e9,
+                      "kernels": "online_hist_kernel x2 + online_select_kernel x2 (two radix passes over K)"}
+            del Kl
+        except Exception as ex:   # pragma: no cover
+            online = {"error": str(ex)[:300]}
+
     resid = None
     if world == 1 and not args.no_compare:
         try:
@@ -617,7 +674,8 @@ def run_ours(args):
                                    + " (kvq_decode_attend: one launch)",
                          "bytes_per_launch": bytes_att, "peak_kind": peak_kind,
                          "splits": info["splits"], "heads_per_cta": info["heads_per_cta"]},
-            "compare": compare, "resid_codebook": resid,
+            "compare": compare, "resid_codebook": resid, "batched_decode": batch,
+            "online_key_thresholds": online,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps * L_res * (2 if world == 1 else 3),
             "clocks": clocks.summary(),
