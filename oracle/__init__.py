@@ -338,3 +338,215 @@ def unpack(words, n: int, bits: int) -> np.ndarray:
     codes = np.zeros(max(n, 1), dtype=np.uint16)
     _load().kvo_unpack(_p(words, P_u32), int(n), int(bits), _p(codes, P_u16))
     return codes[:n]
+
+
+# ------------------------------------------ mixed-precision sensitivity (f4) -----------
+def dequantize(cache: CanonCache, key_lo, key_hi, cbK_dec, cbV_dec):
+    """K^, V^ [T, D] fp64 of a canonical cache, the plain definition the attend uses
+    (readings R5, R6): an outlier entry is its stored fp16 value, every other
+    entry Chat_dec[code] * s + z with s_c, z_c = fp32((hi-lo)/2), fp32((hi+lo)/2) for the
+    Keys (per channel) and the stored fp32 (s_n, z_n) for the Values (per token)."""
+    T, D = cache.kcodes.shape
+    lo = np.asarray(key_lo, np.float32).astype(np.float64)
+    hi = np.asarray(key_hi, np.float32).astype(np.float64)
+    s = ((hi - lo) / 2.0).astype(np.float32).astype(np.float64)
+    z = ((hi + lo) / 2.0).astype(np.float32).astype(np.float64)
+    cK = np.asarray(cbK_dec, np.float32).astype(np.float64)
+    cV = np.asarray(cbV_dec, np.float32).astype(np.float64)
+    Kh = cK[cache.kcodes.astype(np.int64)] * s[None, :] + z[None, :]
+    Vh = (cV[cache.vcodes.astype(np.int64)] * cache.vs.astype(np.float64)[:, None]
+          + cache.vz.astype(np.float64)[:, None])
+    for n in range(T):
+        a, b = int(cache.kptr[n]), int(cache.kptr[n + 1])
+        Kh[n, cache.kidx[a:b]] = cache.kval[a:b].view(np.float16).astype(np.float64)
+        if cache.vidx.shape[1]:
+            Vh[n, cache.vidx[n]] = cache.vval[n].view(np.float16).astype(np.float64)
+    return Kh, Vh
+
+
+def fisher_diag(grads) -> np.ndarray:
+    """Diagonal Fisher information F^D = diag(g (.) g) summed over samples (SPEC
+    fisher_diag: sum, not mean), fp64."""
+    gs = [np.asarray(g, np.float64) for g in grads]
+    if not gs:
+        raise ValueError("no gradient samples")
+    F = np.zeros_like(gs[0])
+    for g in gs:
+        if g.shape != F.shape:
+            raise ValueError("gradient shapes differ")
+        F = F + g * g
+    return F
+
+
+def layer_sensitivity(a, qa, f=None) -> float:
+    """Omega = (A - Q(A))^T F^D (A - Q(A)) = sum F (A - Q(A))^2 (eq:opt2, P:1336-1339), fp64;
+    f = None means F = 1 (the plain quantization error)."""
+    a = np.asarray(a, np.float64)
+    qa = np.asarray(qa, np.float64)
+    if a.shape != qa.shape:
+        raise ValueError("shape mismatch")
+    e = a - qa
+    if f is None:
+        return float(np.sum(e * e))
+    f = np.asarray(f, np.float64)
+    if f.shape != a.shape:
+        raise ValueError("shape mismatch")
+    return float(np.sum(f * e * e))
+
+
+def layer_omega(K, V, key_lo, key_hi, cbK, cbV, ppm: int, FK=None, FV=None, cbK_dec=None, cbV_dec=None):
+    """(Omega_K, Omega_V) of one layer quantized with the given (lower-precision) codebooks and
+    thresholds ("quantization error computed at the lower precision"; reading R26):
+    prefill -> dequantize -> layer_sensitivity on the Keys and on the Values."""
+    cbK_dec = cbK if cbK_dec is None else cbK_dec
+    cbV_dec = cbV if cbV_dec is None else cbV_dec
+    cache = prefill(K, V, key_lo, key_hi, cbK, cbV, ppm)
+    Kh, Vh = dequantize(cache, key_lo, key_hi, cbK_dec, cbV_dec)
+    Kf = _f16bits(K).view(np.float16).astype(np.float64)
+    Vf = _f16bits(V).view(np.float16).astype(np.float64)
+    return layer_sensitivity(Kf, Kh, FK), layer_sensitivity(Vf, Vh, FV)
+
+
+def assign_mixed_precision(omegas, demote_count: int) -> list:
+    """The demote_count layer ids with the smallest Omega, which get the lower bit width
+    (one-shot assignment); ties to the lower layer id (SPEC
+    assign_mixed_precision).  Plain selection: repeatedly take the smallest remaining."""
+    om = [float(x) for x in omegas]
+    if not 0 <= demote_count <= len(om):
+        raise ValueError("demote_count out of range")
+    left = list(range(len(om)))
+    out = []
+    for _ in range(demote_count):
+        best = left[0]
+        for i in left:
+            if om[i] < om[best]:
+                best = i
+        out.append(best)
+        left.remove(best)
+    return sorted(out)
+
+
+# --------------------------------------------- offline calibration on the GPU (f3) ------
+# The readings these follow (DESIGN.md R27, R28): normalized points of the kept values only
+# (P:340 "the remaining numbers in the vector are normalized to the range [-1,1]"), Lloyd
+# k-means for eq:fisher_kmeans (P:316-322) with per-element Fisher weights on the normalized
+# residual, centroids initialised at the k equal-width bin centres of [-1, 1], nearest
+# centroid with ties to the lower index, empty clusters keep their centroid, stop when the
+# largest move < tol or after max_iter updates; Q-Norm (eq:qnorm P:355-358) statistics over the
+# same normalized points (unweighted, population std), post-quantization values from the
+# encode codebook the cache will use.
+def calib_key_points(Kcal, key_lo, key_hi, FK=None):
+    """Normalized kept Key values and their weights, token-major order.  A value is kept when
+    lo_c <= x <= hi_c (R4) and hi_c > lo_c; x' = (x - z_c) / s_c with s_c = (hi_c - lo_c)/2,
+    z_c = (hi_c + lo_c)/2 in fp64 (P:321, P:340)."""
+    K = _f16bits(Kcal).view(np.float16).astype(np.float64)
+    lo = np.asarray(key_lo, np.float32).astype(np.float64)[None, :]
+    hi = np.asarray(key_hi, np.float32).astype(np.float64)[None, :]
+    s = (hi - lo) / 2.0
+    z = (hi + lo) / 2.0
+    kept = (K >= lo) & (K <= hi) & (hi > lo)
+    xn = (K - z) / np.where(hi > lo, s, 1.0)
+    w = np.ones_like(K) if FK is None else np.asarray(FK, np.float32).astype(np.float64)
+    return xn[kept], w[kept]
+
+
+def calib_value_points(Vcal, ppm: int, FV=None):
+    """Normalized kept Value values per token: the k = ceil(f D) outliers of the two-sided
+    split (R2, R3; the pinned select_outliers) removed, [lo_n, hi_n] the kept range, x' =
+    (v - z_n) / s_n in fp64; tokens with hi_n == lo_n contribute nothing."""
+    Vb = _f16bits(Vcal)
+    N, D = Vb.shape
+    k = outlier_count(D, ppm)
+    V = Vb.view(np.float16).astype(np.float64)
+    W = np.ones_like(V) if FV is None else np.asarray(FV, np.float32).astype(np.float64)
+    xs, ws = [], []
+    for n in range(N):
+        kept = ~select_outliers(Vb[n], k)
+        lo, hi = V[n, kept].min(), V[n, kept].max()
+        if hi > lo:
+            s, z = (hi - lo) / 2.0, (hi + lo) / 2.0
+            xs.append((V[n, kept] - z) / s)
+            ws.append(W[n, kept])
+    if not xs:
+        return np.zeros(0), np.zeros(0)
+    return np.concatenate(xs), np.concatenate(ws)
+
+
+def nearest_label(x, cb) -> np.ndarray:
+    """Index of the nearest centroid, ties to the lower index: #{j : 2x > c_j + c_{j+1}}."""
+    x = np.asarray(x, np.float64)
+    c = np.asarray(cb, np.float64)
+    lab = np.zeros(x.shape, np.int64)
+    for j in range(c.size - 1):
+        lab += (2.0 * x > c[j] + c[j + 1])
+    return lab
+
+
+def fisher_kmeans(x, w, k: int, max_iter: int = 100, tol: float = 1e-6):
+    """Weighted Lloyd k-means in 1-D for eq:fisher_kmeans: returns (centroids
+    ascending fp64, number of updates run)."""
+    x = np.asarray(x, np.float64)
+    w = np.asarray(w, np.float64)
+    c = -1.0 + (2.0 * np.arange(k) + 1.0) / k
+    it = 0
+    for it in range(1, max_iter + 1):
+        lab = nearest_label(x, c)
+        sw = np.array([w[lab == j].sum() for j in range(k)])
+        sx = np.array([(w[lab == j] * x[lab == j]).sum() for j in range(k)])
+        new = np.where(sw > 0, sx / np.where(sw > 0, sw, 1.0), c)
+        new = np.sort(new)
+        move = np.max(np.abs(new - c))
+        c = new
+        if move < tol:
+            break
+    return c, it
+
+
+def qnorm_stats(x, cb):
+    """(mu1, sigma1, mu2, sigma2): mean / population std of the points and of their nearest
+    codebook values (eq:qnorm P:355-358)."""
+    x = np.asarray(x, np.float64)
+    q = np.asarray(cb, np.float64)[nearest_label(x, cb)]
+    return x.mean(), x.std(), q.mean(), q.std()
+
+
+def apply_qnorm(cb, mu1, sigma1, mu2, sigma2) -> np.ndarray:
+    """eq:qnorm: C^_i = (C_i - mu2) sigma1 / sigma2 + mu1."""
+    c = np.asarray(cb, np.float64)
+    return (c - mu2) * sigma1 / sigma2 + mu1
+
+
+def _codebook_store(c, fp16: bool) -> np.ndarray:
+    """fp32 (or fp16-valued, R23) storage of an ascending codebook, one rounding per entry;
+    an entry that would not exceed its predecessor is bumped to the next representable value."""
+    out = np.zeros(len(c), np.float32)
+    for i, v in enumerate(np.asarray(c, np.float64)):
+        r = np.float32(np.array([f64_to_f16(v)], np.uint16).view(np.float16)[0]) if fp16 else np.float32(v)
+        if i and r <= out[i - 1]:
+            if fp16:
+                r = np.float32(np.nextafter(np.float16(out[i - 1]), np.float16(np.inf)))
+            else:
+                r = np.nextafter(out[i - 1], np.float32(np.inf))
+        out[i] = r
+    return out
+
+
+def calibrate_layer(Kcal, Vcal, bits: int, ppm: int, FK=None, FV=None, max_iter: int = 100,
+                    tol: float = 1e-6, qnorm: bool = False, fp16_codebooks: bool = True) -> dict:
+    """Offline calibration of one layer: per-channel Key
+    thresholds over the calibration tokens (the order statistics of key_thresholds_online),
+    Key / Value codebooks by Fisher-weighted k-means on the normalized kept values, optional
+    Q-Norm'd decode codebooks."""
+    lo, hi = key_thresholds_online(Kcal, ppm)
+    k = 1 << bits
+    xk, wk = calib_key_points(Kcal, lo, hi, FK)
+    xv, wv = calib_value_points(Vcal, ppm, FV)
+    ck, itk = fisher_kmeans(xk, wk, k, max_iter, tol)
+    cv, itv = fisher_kmeans(xv, wv, k, max_iter, tol)
+    cbK, cbV = _codebook_store(ck, fp16_codebooks), _codebook_store(cv, fp16_codebooks)
+    out = dict(key_lo=lo, key_hi=hi, cbK=cbK, cbV=cbV, cbK_dec=cbK.copy(), cbV_dec=cbV.copy(),
+               iters=(itk, itv), centroids=(ck, cv))
+    if qnorm:
+        out["cbK_dec"] = _codebook_store(apply_qnorm(cbK, *qnorm_stats(xk, cbK)), fp16_codebooks)
+        out["cbV_dec"] = _codebook_store(apply_qnorm(cbV, *qnorm_stats(xv, cbV)), fp16_codebooks)
+    return out
