@@ -220,6 +220,33 @@ kvq_status kvq_phase_timers(kvq_cache *cache, uint64_t *out /* host [16] */);
 kvq_status kvq_key_thresholds_online(const void *K_f16, int64_t T, int32_t D, int32_t outlier_ppm,
                                      float *key_lo, float *key_hi, int32_t device, void *stream);
 
+/* Mixed-precision sensitivity (sec:appendix-mp, eq:opt2 P:1336-1339):
+ *   Omega = (A - Q(A))^T F^D (A - Q(A)) = sum_{n,c} F[n][c] (A[n][c] - A^[n][c])^2
+ * for the tokens [t0, t0 + T) of `cache`, which the caller has quantized into it (the cache is
+ * created at the candidate LOWER precision with that layer's codebooks and thresholds
+ * "quantization error computed at the lower precision").  A^ is the dequantized cache entry
+ * (outliers exact; else Chat_dec[code] s + z, fp64 from the stored fp32 values, R5 / R6).
+ *   K_f16, V_f16 : [T][D] fp16, the same pre-RoPE Keys / Values that were appended (device or host)
+ *   FK, FV       : [T][D] fp32 diagonal Fisher weights (>= 0; device or host), NULL = all ones
+ *                  (plain squared quantization error, the "quantization error-based" baseline)
+ *   omega        : double [2] (device or host; host makes the call synchronous) =
+ *                  (Omega over the Keys, Omega over the Values); Omega_i = sum of the two (R26).
+ * Accumulated in fp64 with atomics: the summation order is not fixed (results agree to ~1e-15
+ * relative).  KVQ_EINVAL when the token range is not cached. */
+kvq_status kvq_layer_sensitivity(kvq_cache *cache, const void *K_f16, const void *V_f16, const float *FK,
+                                 const float *FV, int64_t t0, int64_t T, double *omega, void *stream);
+
+/* Diagonal Fisher information (F^D = diag(g (.) g), the F^D of eq:opt2): F[i] += g[i]^2 for n elements,
+ * fp32 with one rounding per step (fmaf).  F, g: device pointers on `device`. */
+kvq_status kvq_fisher_accumulate(float *F, const float *g, int64_t n, int32_t device, void *stream);
+
+/* One-shot mixed-precision assignment: the demote_count layers with
+ * the smallest omega (ties to the lower layer index) get bits_low, the rest bits_high.
+ * Host only.  omega [L] >= 0, bits_out [L].  KVQ_EINVAL when demote_count is outside [0, L] or
+ * an omega is negative / NaN. */
+kvq_status kvq_assign_bits(const double *omega, int32_t L, int32_t demote_count, int32_t bits_high,
+                           int32_t bits_low, int32_t *bits_out);
+
 /* ------------------------------------------------------------------------------------
  * fp16 comparator cache (BASELINE config C3 "4-bit vs 3-bit vs fp16 cache"): the paper's
  * baseline decode is fp16 mat-vec against an fp16 cache of post-RoPE Keys ("Key fp16

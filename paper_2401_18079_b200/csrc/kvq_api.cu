@@ -1,4 +1,5 @@
 // kvq_api.cu -- C ABI of libkvq: validation, the cache object, staging, export.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -707,6 +708,81 @@ kvq_status kvq_key_thresholds_online(const void *K, int64_t T, int32_t D, int32_
     if (ch == 1) CK(cudaMemcpyAsync(key_hi, hi, ob, cudaMemcpyDeviceToHost, s));
     CK(cudaFreeAsync(tmp, s));
     if (cl == 1 || ch == 1) CK(cudaStreamSynchronize(s));
+    return KVQ_OK;
+}
+
+// ------------------------------------------- mixed-precision sensitivity (f4) ----------
+kvq_status kvq_layer_sensitivity(kvq_cache *c, const void *K, const void *V, const float *FK, const float *FV,
+                                 int64_t t0, int64_t T, double *omega, void *stream) {
+    if (!c || !K || !V || !omega) return fail(KVQ_EINVAL, "null argument");
+    if (t0 < 0 || T < 0 || t0 + T > c->T) return fail(KVQ_EINVAL, "tokens [%lld, %lld) not cached (%lld)",
+                                                     (long long)t0, (long long)(t0 + T), (long long)c->T);
+    kvq_status st = check_sticky(c);
+    if (st != KVQ_OK) return st;
+    const int dev = c->cfg.device;
+    CK(cudaSetDevice(dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    const void *ins[4] = {K, V, FK, FV};
+    int cls[4];
+    for (int i = 0; i < 4; ++i) {
+        cls[i] = ins[i] ? classify(ins[i], dev, 0) : 0;
+        if (cls[i] < 0) return fail(KVQ_EDEVICE, "input pointer not on device %d", dev);
+    }
+    const int co = classify(omega, dev, 0);
+    if (co < 0) return fail(KVQ_EDEVICE, "omega pointer not on device %d", dev);
+    const size_t eb[4] = {(size_t)T * c->dc.D * 2, (size_t)T * c->dc.D * 2, (size_t)T * c->dc.D * 4,
+                          (size_t)T * c->dc.D * 4};
+    size_t need = 256;
+    for (int i = 0; i < 4; ++i) if (cls[i] == 1) need += (eb[i] + 255) / 256 * 256;
+    void *tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, need, s));
+    char *tp = (char *)tmp;
+    const void *dv[4];
+    for (int i = 0; i < 4; ++i) {
+        dv[i] = ins[i];
+        if (cls[i] == 1 && eb[i]) {
+            CK(cudaMemcpyAsync(tp, ins[i], eb[i], cudaMemcpyHostToDevice, s));
+            dv[i] = tp;
+            tp += (eb[i] + 255) / 256 * 256;
+        }
+    }
+    double *od = co == 1 ? (double *)tp : omega;
+    cudaError_t e = launch_layer_sensitivity(c->dc, (const __half *)dv[0], (const __half *)dv[1],
+                                             (const float *)dv[2], (const float *)dv[3], t0, T, od, s);
+    if (e != cudaSuccess) { cudaFreeAsync(tmp, s); return cuda_fail(e, "sensitivity launch"); }
+    if (co == 1) CK(cudaMemcpyAsync(omega, od, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(tmp, s));
+    if (co == 1) CK(cudaStreamSynchronize(s));
+    return KVQ_OK;
+}
+
+kvq_status kvq_fisher_accumulate(float *F, const float *g, int64_t n, int32_t device, void *stream) {
+    if (!F || !g) return fail(KVQ_EINVAL, "null argument");
+    if (n < 0) return fail(KVQ_EINVAL, "negative element count");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(KVQ_EDEVICE, "device %d not present", device);
+    CK(cudaSetDevice(device));
+    if (classify(F, device, 0) != 0 || classify(g, device, 0) != 0)
+        return fail(KVQ_EDEVICE, "F and g must be device pointers on device %d", device);
+    cudaError_t e = launch_fisher_accumulate(F, g, n, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "fisher launch");
+    return KVQ_OK;
+}
+
+kvq_status kvq_assign_bits(const double *omega, int32_t L, int32_t demote_count, int32_t bits_high,
+                           int32_t bits_low, int32_t *bits_out) {
+    if (!omega || !bits_out) return fail(KVQ_EINVAL, "null argument");
+    if (L < 0 || demote_count < 0 || demote_count > L)
+        return fail(KVQ_EINVAL, "demote_count %d out of [0, %d]", demote_count, L);
+    for (int i = 0; i < L; ++i)
+        if (!(omega[i] >= 0.0)) return fail(KVQ_EINVAL, "omega[%d] is negative or NaN", i);
+    std::vector<int> idx((size_t)L);
+    for (int i = 0; i < L; ++i) idx[(size_t)i] = i;
+    // smallest omega first, ties to the lower layer index (a stable order)
+    std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return omega[x] < omega[y]; });
+    for (int i = 0; i < L; ++i) bits_out[i] = bits_high;
+    for (int r = 0; r < demote_count; ++r) bits_out[idx[(size_t)r]] = bits_low;
     return KVQ_OK;
 }
 

@@ -131,7 +131,133 @@ __global__ void __launch_bounds__(256) online_select_kernel(OnlineArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// SURVEY 8(f) f4, mixed-precision sensitivity (sec:appendix-mp, eq:opt2 P:1336-1339):
+//   Omega = (A - Q(A))^T F^D (A - Q(A)) = sum_{n,c} F[n][c] (A[n][c] - A^[n][c])^2
+// over the tokens [n0, n0 + T) of a cache that holds them (quantized at the candidate, lower,
+// precision), A^ the dequantized cache entry (R5, R6: outliers exact, else
+// Chat_dec[code] s + z in fp64 from the stored fp32 s, z and codebook), separately for the
+// Keys (pre-RoPE, as cached) and the Values.  One CTA per 32-token tile: the tile's outlier
+// positions become a shared bitmap, then every (token, channel) element is visited once,
+// channel-fastest, so K/V/F reads are coalesced rows and the tile's code words stay in L1.
+struct SensArgs {
+    DevCache c;
+    const uint16_t *K, *V;     // [T][D] fp16 bits, row n - n0
+    const float *FK, *FV;      // [T][D] or null (F = 1)
+    int64_t n0, T;
+    double *omega;             // [2] accumulated (zeroed by the caller)
+};
+
+__device__ __forceinline__ double h2d_dev(uint16_t h) { return (double)__half2float(__ushort_as_half(h)); }
+
+__global__ void __launch_bounds__(256) sens_kernel(SensArgs a) {
+    extern __shared__ uint32_t bm[];   // [2][32][D/32] outlier bitmaps (Key, Value)
+    const DevCache &c = a.c;
+    const int D = c.D, DW = D / 32, b = c.bits;
+    const int64_t tile = a.n0 / 32 + blockIdx.x;
+    const int64_t t0 = tile * 32;
+    const int64_t lo = t0 > a.n0 ? t0 : a.n0;
+    const int64_t hi = (t0 + 32 < a.n0 + a.T) ? t0 + 32 : a.n0 + a.T;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t *kbm = bm, *vbm = bm + 32 * DW;
+    for (int x = tid; x < 64 * DW; x += 256) bm[x] = 0;
+    __syncthreads();
+    for (int64_t n = lo + warp; n < hi; n += 8) {
+        const int j = (int)(n - t0);
+        const uint32_t r0 = c.kptr[n], r1 = c.kptr[n + 1];
+        for (uint32_t r = r0 + lane; r < r1; r += 32) {
+            const uint32_t ch = c.kout[r] & 0xffffu;
+            atomicOr(&kbm[j * DW + (ch >> 5)], 1u << (ch & 31));
+        }
+        for (int r = lane; r < c.kv; r += 32) {
+            const uint32_t ch = c.vout[n * c.kv + r] & 0xffffu;
+            atomicOr(&vbm[j * DW + (ch >> 5)], 1u << (ch & 31));
+        }
+    }
+    __syncthreads();
+    const float *cbK = c.cb + 16, *cbV = c.cb + 48;
+    const uint32_t m1 = (1u << b) - 1, m2 = (1u << (2 * b)) - 1;
+    double ak = 0.0, av = 0.0;
+    const int64_t ne = (hi - lo) * D;
+    for (int64_t x = tid; x < ne; x += 256) {
+        const int64_t n = lo + x / D;
+        const int ch = (int)(x % D), j = (int)(n - t0);
+        const int h = ch / kHeadDim, cc = ch % kHeadDim;
+        const int64_t row = (n - a.n0) * D + ch;
+        if (!((kbm[j * DW + (ch >> 5)] >> (ch & 31)) & 1u)) {
+            const int p = cc & (kPairs - 1), bit = 2 * b * p, q = h * 4 * b + bit / 32;
+            const uint32_t *wp = c.kcodes + ((size_t)tile * c.QW + q) * 32 + j;
+            uint64_t w = __ldg(wp);
+            if (bit % 32 + 2 * b > 32) w |= (uint64_t)__ldg(wp + 32) << 32;
+            const uint32_t pc = (uint32_t)(w >> (bit % 32)) & m2;
+            const uint32_t code = cc >= kPairs ? pc >> b : pc & m1;
+            const double xh = (double)cbK[code] * (double)c.kpar[ch] + (double)c.kpar[D + ch];
+            const double e = h2d_dev(a.K[row]) - xh;
+            ak += (a.FK ? (double)a.FK[row] : 1.0) * e * e;
+        }
+        if (!((vbm[j * DW + (ch >> 5)] >> (ch & 31)) & 1u)) {
+            const int bit = vf_bit(j, cc, b);
+            const uint32_t *wp = c.vcodes + vf_word(tile, c.H_kv, h, bit / 32, vf_lane(j, cc), b);
+            uint64_t w = __ldg(wp);
+            if (bit % 32 + b > 32) w |= (uint64_t)__ldg(wp + 32) << 32;
+            const uint32_t code = (uint32_t)(w >> (bit % 32)) & m1;
+            const float2 sz = c.vsz[n];
+            const double vh = (double)cbV[code] * (double)sz.x + (double)sz.y;
+            const double e = h2d_dev(a.V[row]) - vh;
+            av += (a.FV ? (double)a.FV[row] : 1.0) * e * e;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ak += __shfl_xor_sync(0xffffffffu, ak, o);
+        av += __shfl_xor_sync(0xffffffffu, av, o);
+    }
+    __shared__ double red[8][2];
+    if (lane == 0) { red[warp][0] = ak; red[warp][1] = av; }
+    __syncthreads();
+    if (tid == 0) {
+        double sk = 0.0, sv = 0.0;
+        for (int w = 0; w < 8; ++w) { sk += red[w][0]; sv += red[w][1]; }
+        atomicAdd(a.omega, sk);
+        atomicAdd(a.omega + 1, sv);
+    }
+}
+
+// Diagonal Fisher information (F^D = diag(g (.) g); SPEC fisher_diag): F += g (.) g, one rounding (fmaf).
+__global__ void fisher_kernel(float *F, const float *g, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = g[i];
+        F[i] = fmaf(x, x, F[i]);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_layer_sensitivity(const DevCache &c, const __half *K, const __half *V, const float *FK,
+                                     const float *FV, int64_t n0, int64_t T, double *omega, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(omega, 0, 2 * sizeof(double), s);
+    if (e != cudaSuccess || T == 0) return e;
+    SensArgs a;
+    a.c = c;
+    a.K = reinterpret_cast<const uint16_t *>(K);
+    a.V = reinterpret_cast<const uint16_t *>(V);
+    a.FK = FK; a.FV = FV; a.n0 = n0; a.T = T; a.omega = omega;
+    const int64_t tiles = (n0 + T + 31) / 32 - n0 / 32;
+    const size_t smem = (size_t)2 * 32 * (c.D / 32) * 4;
+    cudaFuncSetAttribute(sens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sens_kernel<<<(unsigned)tiles, 256, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fisher_accumulate(float *F, const float *g, int64_t n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (n + 255) / 256;
+    const unsigned grid = (unsigned)(want < 8 * sms ? want : 8 * sms);
+    fisher_kernel<<<grid, 256, 0, s>>>(F, g, n);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_online_key_thresholds(const __half *K, int64_t T, int D, int ppm, float *lo, float *hi,
                                          cudaStream_t s) {

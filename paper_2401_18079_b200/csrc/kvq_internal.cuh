@@ -118,6 +118,10 @@ cudaError_t launch_f16_attend(const F16Dev &c, const __half *q, int64_t pos, int
 // ---- online per-channel Key thresholds (kvq_calib.cu) ----
 cudaError_t launch_online_key_thresholds(const __half *K, int64_t T, int D, int ppm, float *lo, float *hi,
                                          cudaStream_t s);
+// ---- mixed-precision sensitivity (kvq_calib.cu) ----
+cudaError_t launch_layer_sensitivity(const DevCache &c, const __half *K, const __half *V, const float *FK,
+                                     const float *FV, int64_t n0, int64_t T, double *omega, cudaStream_t s);
+cudaError_t launch_fisher_accumulate(float *F, const float *g, int64_t n, cudaStream_t s);
 
 // ---- attention (kvq_attend.cu) ----
 struct AttendArgs {

@@ -31,7 +31,8 @@ EXPORTED = ["kvq_cache_create", "kvq_cache_destroy", "kvq_append", "kvq_prefill_
             "kvq_get_info", "kvq_set_splits", "kvq_phase_timers", "kvq_last_error", "kvq_version",
             "kvq_f16_cache_create", "kvq_f16_cache_destroy", "kvq_f16_append",
             "kvq_f16_decode_attend", "kvq_f16_export", "kvq_f16_num_tokens",
-            "kvq_key_thresholds_online", "kvq_decode_attend_batch"]
+            "kvq_key_thresholds_online", "kvq_decode_attend_batch", "kvq_layer_sensitivity",
+            "kvq_fisher_accumulate", "kvq_assign_bits"]
 
 
 class KVQError(RuntimeError):
@@ -101,6 +102,9 @@ def _load() -> ctypes.CDLL:
         "kvq_f16_num_tokens": (i64, [vp]),
         "kvq_key_thresholds_online": (i32, [vp, i64, i32, i32, vp, vp, i32, vp]),
         "kvq_decode_attend_batch": (i32, [vp, i32, vp, vp, vp, vp]),
+        "kvq_layer_sensitivity": (i32, [vp, vp, vp, vp, vp, i64, i64, vp, vp]),
+        "kvq_fisher_accumulate": (i32, [vp, vp, i64, i32, vp]),
+        "kvq_assign_bits": (i32, [vp, i32, i32, i32, i32, vp]),
         "kvq_version": (i32, []),
     }
     for name, (res, args) in sig.items():
@@ -294,6 +298,35 @@ def key_thresholds_online(K, outlier_ppm: int, lo=None, hi=None, device: int = 0
     _check(_lib.kvq_key_thresholds_online(_ptr(K), T, D, int(outlier_ppm), _ptr(lo), _ptr(hi), int(device),
                                           _stream(stream)))
     return lo, hi
+
+
+def layer_sensitivity(cache, K, V, FK=None, FV=None, t0: int = 0, omega=None, stream=None):
+    """(Omega_K, Omega_V) of eq:opt2 over the cache's tokens [t0, t0 + len(K)).
+    K, V: the [T, D] fp16 tensors that were quantized into `cache`; FK, FV: fp32 Fisher
+    diagonals of the same shape or None (ones).  Returns a host numpy float64 [2] unless a
+    device `omega` tensor is given (then asynchronous)."""
+    T = int(K.shape[0])
+    out = np.zeros(2, np.float64) if omega is None else omega
+    _check(_lib.kvq_layer_sensitivity(cache.handle, _ptr(K), _ptr(V), _ptr(FK), _ptr(FV), int(t0), T, _ptr(out),
+                                      _stream(stream)))
+    return out
+
+
+def fisher_accumulate(F, g, device: int = 0, stream=None):
+    """F += g * g elementwise on the GPU (fp32 device tensors of equal size)."""
+    if F.numel() != g.numel():
+        raise ValueError("F and g differ in size")
+    _check(_lib.kvq_fisher_accumulate(_ptr(F), _ptr(g), int(F.numel()), int(device), _stream(stream)))
+    return F
+
+
+def assign_bits(omega, demote_count: int, bits_high: int, bits_low: int) -> np.ndarray:
+    """Per-layer bit widths: the demote_count least sensitive layers get bits_low (host)."""
+    om = np.ascontiguousarray(np.asarray(omega, dtype=np.float64))
+    out = np.zeros(om.shape[0], np.int32)
+    _check(_lib.kvq_assign_bits(_ptr(om), int(om.shape[0]), int(demote_count), int(bits_high), int(bits_low),
+                                _ptr(out)))
+    return out
 
 
 class F16Cache:
