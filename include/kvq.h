@@ -247,6 +247,40 @@ kvq_status kvq_fisher_accumulate(float *F, const float *g, int64_t n, int32_t de
 kvq_status kvq_assign_bits(const double *omega, int32_t L, int32_t demote_count, int32_t bits_high,
                            int32_t bits_low, int32_t *bits_out);
 
+/* Offline calibration of one layer on the GPU: everything kvq_params needs,
+ * from N calibration tokens (P:316-322 eq:fisher_kmeans, P:340, P:355-358 eq:qnorm):
+ *   key_lo, key_hi  per-channel order statistics over the N tokens, exactly as
+ *                   kvq_key_thresholds_online (R2, R3)
+ *   key_cb, val_cb  2^bits centroids of Fisher-weighted Lloyd k-means on the normalized kept
+ *                   values (Keys: lo_c <= x <= hi_c, x' = (x - z_c)/s_c; Values: per token the
+ *                   two-sided top-k outliers removed, x' = (v - z_n)/s_n; fp64), initialised at
+ *                   the bin centres -1 + (2j+1)/k, ties to the lower centroid, empty clusters
+ *                   keep their centroid, stop when the largest move < tol or after max_iter
+ *                   updates (readings R27, R28)
+ *   *_cb_dec        Q-Norm'd decode codebooks (eq:qnorm; moments of the normalized points and of
+ *                   their encode-codebook values) when cfg.qnorm, else copies of the encode ones
+ * Codebooks are stored as fp32, or as fp16 values when cfg.fp16_codebooks (R23); an entry that
+ * would not exceed its predecessor after rounding is bumped to the next representable value.
+ *   K_cal, V_cal : [N][D] fp16 (device or host);  FK, FV : [N][D] fp32 Fisher diagonals (device or
+ *   host) or NULL (ones);  outputs: key_lo, key_hi [D], codebooks [2^bits] fp32, iters [2] int32
+ *   (Lloyd updates run for the Keys / Values; may be NULL) -- device or host, host makes the
+ *   call synchronous.  D % 128 == 0, D <= 8192.  Deterministic for a given input (fixed grid,
+ *   fixed reduction order).  KVQ_EINVAL on bad bits / ppm / max_iter / tol or too many outliers
+ *   for N tokens. */
+typedef struct {
+    int32_t bits;            /* 2, 3 or 4 */
+    int32_t outlier_ppm;     /* as kvq_config.outlier_ppm */
+    int32_t max_iter;        /* >= 1 */
+    int32_t qnorm;           /* 1: Q-Norm'd decode codebooks */
+    int32_t fp16_codebooks;  /* 1: store fp16 values (R23) */
+    int32_t reserved;
+    double tol;              /* >= 0; 0 runs max_iter updates */
+} kvq_calib_config;
+kvq_status kvq_calibrate_layer(const void *K_cal, const void *V_cal, const float *FK, const float *FV, int64_t N,
+                               int32_t D, const kvq_calib_config *cfg, float *key_lo, float *key_hi,
+                               float *key_cb, float *key_cb_dec, float *val_cb, float *val_cb_dec,
+                               int32_t *iters, int32_t device, void *stream);
+
 /* ------------------------------------------------------------------------------------
  * fp16 comparator cache (BASELINE config C3 "4-bit vs 3-bit vs fp16 cache"): the paper's
  * baseline decode is fp16 mat-vec against an fp16 cache of post-RoPE Keys ("Key fp16

@@ -491,8 +491,8 @@ def fisher_kmeans(x, w, k: int, max_iter: int = 100, tol: float = 1e-6):
     it = 0
     for it in range(1, max_iter + 1):
         lab = nearest_label(x, c)
-        sw = np.array([w[lab == j].sum() for j in range(k)])
-        sx = np.array([(w[lab == j] * x[lab == j]).sum() for j in range(k)])
+        sw = np.bincount(lab, weights=w, minlength=k)          # sum of w per cluster
+        sx = np.bincount(lab, weights=w * x, minlength=k)      # sum of w x per cluster
         new = np.where(sw > 0, sx / np.where(sw > 0, sw, 1.0), c)
         new = np.sort(new)
         move = np.max(np.abs(new - c))
@@ -547,6 +547,10 @@ def calibrate_layer(Kcal, Vcal, bits: int, ppm: int, FK=None, FV=None, max_iter:
     out = dict(key_lo=lo, key_hi=hi, cbK=cbK, cbV=cbV, cbK_dec=cbK.copy(), cbV_dec=cbV.copy(),
                iters=(itk, itv), centroids=(ck, cv))
     if qnorm:
-        out["cbK_dec"] = _codebook_store(apply_qnorm(cbK, *qnorm_stats(xk, cbK)), fp16_codebooks)
-        out["cbV_dec"] = _codebook_store(apply_qnorm(cbV, *qnorm_stats(xv, cbV)), fp16_codebooks)
+        for key, x, cb in (("cbK_dec", xk, cbK), ("cbV_dec", xv, cbV)):
+            if x.size == 0:
+                continue                       # no points: decode = encode
+            st = qnorm_stats(x, cb)
+            if st[3] > 0:                      # sigma2 = 0 (one level used): decode = encode
+                out[key] = _codebook_store(apply_qnorm(cb, *st), fp16_codebooks)
     return out

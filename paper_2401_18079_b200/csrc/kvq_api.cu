@@ -786,6 +786,75 @@ kvq_status kvq_assign_bits(const double *omega, int32_t L, int32_t demote_count,
     return KVQ_OK;
 }
 
+kvq_status kvq_calibrate_layer(const void *K, const void *V, const float *FK, const float *FV, int64_t N, int32_t D,
+                               const kvq_calib_config *cfg, float *key_lo, float *key_hi, float *key_cb,
+                               float *key_cb_dec, float *val_cb, float *val_cb_dec, int32_t *iters,
+                               int32_t device, void *stream) {
+    if (!K || !V || !cfg || !key_lo || !key_hi || !key_cb || !key_cb_dec || !val_cb || !val_cb_dec)
+        return fail(KVQ_EINVAL, "null argument");
+    const kvq_calib_config &C = *cfg;
+    if (C.bits < 2 || C.bits > 4) return fail(KVQ_EINVAL, "bits must be 2, 3 or 4");
+    if (C.outlier_ppm < 0 || C.outlier_ppm >= 500000) return fail(KVQ_EINVAL, "outlier_ppm must be in [0, 500000)");
+    if (C.max_iter < 1) return fail(KVQ_EINVAL, "max_iter must be >= 1");
+    if (!(C.tol >= 0.0)) return fail(KVQ_EINVAL, "tol must be >= 0");
+    if (N < 1 || D < 128 || D % 128 || D > 8192) return fail(KVQ_EINVAL, "need N >= 1 and D a multiple of 128 <= 8192");
+    const int64_t n = ((int64_t)C.outlier_ppm * N + 999999) / 1000000;
+    if ((n + 1) / 2 + n / 2 >= N) return fail(KVQ_EINVAL, "too many Key outliers (%lld) for %lld tokens", (long long)n, (long long)N);
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(KVQ_EDEVICE, "device %d not present", device);
+    CK(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const void *ins[4] = {K, V, FK, FV};
+    const size_t ib[4] = {(size_t)N * D * 2, (size_t)N * D * 2, (size_t)N * D * 4, (size_t)N * D * 4};
+    void *outs[7] = {key_lo, key_hi, key_cb, key_cb_dec, val_cb, val_cb_dec, iters};
+    const int nlev = 1 << C.bits;
+    const size_t ob[7] = {(size_t)D * 4, (size_t)D * 4, (size_t)nlev * 4, (size_t)nlev * 4, (size_t)nlev * 4,
+                          (size_t)nlev * 4, 2 * 4};
+    int ci[4], co[7];
+    for (int i = 0; i < 4; ++i) {
+        ci[i] = ins[i] ? classify(ins[i], device, 0) : 0;
+        if (ci[i] < 0) return fail(KVQ_EDEVICE, "input pointer not on device %d", device);
+    }
+    bool host_out = false;
+    for (int i = 0; i < 7; ++i) {
+        co[i] = outs[i] ? classify(outs[i], device, 0) : 0;
+        if (co[i] < 0) return fail(KVQ_EDEVICE, "output pointer not on device %d", device);
+        host_out |= outs[i] && co[i] == 1;
+    }
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    size_t need = al((size_t)D * 4) * 2 + al(64 * 4) + al(4 * 4);
+    for (int i = 0; i < 4; ++i) if (ci[i] == 1) need += al(ib[i]);
+    void *tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, need, s));
+    char *tp = (char *)tmp;
+    float *lo_d = (float *)tp; tp += al((size_t)D * 4);
+    float *hi_d = (float *)tp; tp += al((size_t)D * 4);
+    float *cb_d = (float *)tp; tp += al(64 * 4);
+    int *it_d = (int *)tp; tp += al(4 * 4);
+    const void *dv[4];
+    for (int i = 0; i < 4; ++i) {
+        dv[i] = ins[i];
+        if (ins[i] && ci[i] == 1) {
+            CK(cudaMemcpyAsync(tp, ins[i], ib[i], cudaMemcpyHostToDevice, s));
+            dv[i] = tp;
+            tp += al(ib[i]);
+        }
+    }
+    cudaError_t e = launch_calibrate((const __half *)dv[0], (const __half *)dv[1], (const float *)dv[2],
+                                     (const float *)dv[3], N, D, C.bits, C.outlier_ppm, C.max_iter, C.tol, C.qnorm,
+                                     C.fp16_codebooks, lo_d, hi_d, cb_d, it_d, s);
+    if (e != cudaSuccess) { cudaFreeAsync(tmp, s); return cuda_fail(e, "calibration launch"); }
+    const void *srcs[7] = {lo_d, hi_d, cb_d, cb_d + 16, cb_d + 32, cb_d + 48, it_d};
+    for (int i = 0; i < 7; ++i) {
+        if (!outs[i]) continue;
+        CK(cudaMemcpyAsync(outs[i], srcs[i], ob[i], co[i] == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    }
+    CK(cudaFreeAsync(tmp, s));
+    if (host_out) CK(cudaStreamSynchronize(s));
+    return KVQ_OK;
+}
+
 // ------------------------------------------------------------- fp16 comparator cache --
 struct kvq_f16_cache {
     kvq_config cfg;

@@ -231,6 +231,338 @@ __global__ void fisher_kernel(float *F, const float *g, int64_t n) {
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// SURVEY 8(f) f3, offline calibration on the GPU (P:316-322 eq:fisher_kmeans, P:340, P:355-358
+// eq:qnorm): the per-layer nuqX codebooks from calibration Keys / Values (readings R27,
+// R28 in DESIGN.md):
+//   points   Keys: x' = (x - z_c) / s_c for lo_c <= x <= hi_c (thresholds from the order-
+//            statistics kernels above); Values: per token the two-sided top-k outliers removed
+//            (R2, R3, ties to the lower index), x' = (v - z_n) / s_n over the kept range; fp64;
+//            zero-width vectors contribute nothing
+//   k-means  Lloyd, centroids initialised at the bin centres -1 + (2j+1)/k, nearest centroid with
+//            ties to the lower index (2x' > c_j + c_{j+1}), per-element Fisher weights, empty
+//            clusters keep their centroid, stop when the largest move < tol or after max_iter
+//   Q-Norm   mean / population std of the points and of their encode-codebook values.
+// Deterministic: a fixed grid (kCalG CTAs), per-CTA partials reduced in a fixed order.
+constexpr int kCalG = 296;
+constexpr int kCalT = 256;
+
+struct CalArgs {
+    const uint16_t *X[2];      // Keys, Values [N][D] fp16 bits
+    const float *F[2];         // Fisher weights [N][D] or null
+    int64_t N;
+    int D, kv, k;
+    const float *klo, *khi;    // [D] Key thresholds
+    float *vlo, *vhi;          // [N] Value kept ranges (fp16 values)
+    uint32_t *vmask;           // [N][D/32] Value outlier bits
+    double *cent;              // [2][16] current centroids
+    double *part;              // [2][kCalG][32] per-CTA sums
+    int *done, *iters;         // [2]
+    double tol;
+    float *cb;                 // [4][16] outputs: Key enc, Key dec, Value enc, Value dec
+    int fp16;
+};
+
+__device__ __forceinline__ uint16_t cal_d2h(double x) {
+    unsigned short r;
+    asm("cvt.rn.f16.f64 %0, %1;" : "=h"(r) : "d"(x));
+    return r;
+}
+__device__ __forceinline__ float cal_h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+
+// one warp per token: the two-sided split of the token's Values, its kept range and outlier bits
+__global__ void __launch_bounds__(128) cal_vrange_kernel(CalArgs a) {
+    extern __shared__ uint4 rows[];   // [4][D/8]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n = (int64_t)blockIdx.x * 4 + warp;
+    if (n >= a.N) return;
+    const int D = a.D, NC = D / 8, DW = D / 32;
+    uint4 *r = rows + (size_t)warp * NC;
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.X[1] + n * D);
+    for (int i = lane; i < NC; i += 32) r[i] = src[i];
+    __syncwarp();
+    const int ku = (a.kv + 1) / 2, kl = a.kv / 2;
+    auto keys8 = [&](int i, uint32_t (&k8)[8]) {
+        const uint4 u = r[i];
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) k8[e] = okey16((uint16_t)(w[e >> 1] >> (16 * (e & 1))));
+    };
+    // count of elements with pred(key, idx), whole warp
+    auto count = [&](auto pred) {
+        int c = 0;
+        for (int i = lane; i < NC; i += 32) {
+            uint32_t k8[8];
+            keys8(i, k8);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c += pred(k8[e], 8 * i + e) ? 1 : 0;
+        }
+        return (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+    };
+    // index (+1) of the need-th element (index order) with pred, 0 if need == 0
+    auto cut_at = [&](auto pred, int need) {
+        if (need <= 0) return 0;
+        int run = 0;
+        for (int m = 0; m * 32 < NC; ++m) {
+            const int i = lane + 32 * m;
+            uint32_t k8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            bool ok = i < NC;
+            if (ok) keys8(i, k8);
+            int c = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c += (ok && pred(k8[e], 8 * i + e)) ? 1 : 0;
+            int inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const int tot = __shfl_sync(0xffffffffu, inc, 31);
+            if (run + tot >= need) {
+                const int exc = inc - c;
+                int idx = 0;
+                const bool mine = run + exc < need && need <= run + inc;
+                if (mine) {
+                    int rr = need - run - exc;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (pred(k8[e], 8 * i + e) && --rr == 0 && idx == 0) idx = 8 * i + e + 1;
+                }
+                const int src_l = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+                return __shfl_sync(0xffffffffu, idx, src_l);
+            }
+            run += tot;
+        }
+        return 0;
+    };
+    // upper outliers: the ku largest (value desc, index asc)
+    uint32_t thi = 0;
+    int cut_hi = 0;
+    if (ku > 0) {
+        for (int b = 15; b >= 0; --b) {
+            const uint32_t t2 = thi | (1u << b);
+            if (count([&](uint32_t k, int) { return k >= t2; }) >= ku) thi = t2;
+        }
+        const int above = count([&](uint32_t k, int) { return k > thi; });
+        cut_hi = cut_at([&](uint32_t k, int) { return k == thi; }, ku - above);
+    }
+    auto upper = [&](uint32_t k, int idx) { return ku > 0 && (k > thi || (k == thi && idx < cut_hi)); };
+    // lower outliers: the kl smallest of the rest (value asc, index asc)
+    uint32_t tlo = 0;
+    int cut_lo = 0;
+    if (kl > 0) {
+        for (int b = 15; b >= 0; --b) {
+            const uint32_t t2 = tlo | (1u << b);
+            if (count([&](uint32_t k, int idx) { return !upper(k, idx) && k < t2; }) < kl) tlo = t2;
+        }
+        const int below = count([&](uint32_t k, int idx) { return !upper(k, idx) && k < tlo; });
+        cut_lo = cut_at([&](uint32_t k, int idx) { return !upper(k, idx) && k == tlo; }, kl - below);
+    }
+    auto lower = [&](uint32_t k, int idx) {
+        return kl > 0 && !upper(k, idx) && (k < tlo || (k == tlo && idx < cut_lo));
+    };
+    uint32_t kmin = 0xffffffffu, kmax = 0;
+    for (int m = 0; m * 32 < NC; ++m) {
+        const int i = lane + 32 * m;
+        uint32_t bits = 0;
+        if (i < NC) {
+            uint32_t k8[8];
+            keys8(i, k8);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const bool out = upper(k8[e], 8 * i + e) || lower(k8[e], 8 * i + e);
+                bits |= (out ? 1u : 0u) << e;
+                if (!out) { kmin = min(kmin, k8[e]); kmax = max(kmax, k8[e]); }
+            }
+        }
+        bits <<= 8 * (lane & 3);
+        bits |= __shfl_xor_sync(0xffffffffu, bits, 1);
+        bits |= __shfl_xor_sync(0xffffffffu, bits, 2);
+        if (i < NC && (lane & 3) == 0) a.vmask[n * DW + i / 4] = bits;
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (lane == 0) {
+        a.vlo[n] = cal_h2f(key2h16(kmin));
+        a.vhi[n] = cal_h2f(key2h16(kmax));
+    }
+}
+
+// MODE 0: per-cluster (sum w, sum w x') of a Lloyd step; MODE 1: Q-Norm moments (n, sum x',
+// sum x'^2, sum q, sum q^2) with q the encode-codebook value.  blockIdx.y = 0 Keys, 1 Values.
+template <int KC, int MODE>
+__global__ void __launch_bounds__(kCalT) cal_km_kernel(CalArgs a) {
+    extern __shared__ double acc[];   // MODE 0: [2 KC][kCalT]
+    __shared__ double mid[16], cv[16];
+    const int y = blockIdx.y, tid = threadIdx.x;
+    if (MODE == 0 && a.done[y]) return;
+    if (tid < KC) {
+        if (MODE == 0) {
+            cv[tid] = a.cent[y * 16 + tid];
+        } else {
+            cv[tid] = (double)a.cb[(2 * y) * 16 + tid];
+        }
+    }
+    __syncthreads();
+    if (tid + 1 < KC) mid[tid] = cv[tid] + cv[tid + 1];
+    if (MODE == 0)
+        for (int j = 0; j < 2 * KC; ++j) acc[j * kCalT + tid] = 0.0;
+    __syncthreads();
+    double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
+    const int D = a.D, DW = D / 32;
+    const uint16_t *X = a.X[y];
+    const float *F = a.F[y];
+    const int64_t nchunks = a.N * D / 8;
+    for (int64_t ch = (int64_t)blockIdx.x * kCalT + tid; ch < nchunks; ch += (int64_t)gridDim.x * kCalT) {
+        const int64_t e0 = ch * 8;
+        const int64_t n = e0 / D;
+        const int c0 = (int)(e0 - n * D);
+        const uint4 u = *reinterpret_cast<const uint4 *>(X + e0);
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+        float wt[8];
+        if (F) {
+            const float4 f0 = *reinterpret_cast<const float4 *>(F + e0), f1 = *reinterpret_cast<const float4 *>(F + e0 + 4);
+            wt[0] = f0.x; wt[1] = f0.y; wt[2] = f0.z; wt[3] = f0.w; wt[4] = f1.x; wt[5] = f1.y; wt[6] = f1.z; wt[7] = f1.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) wt[e] = 1.f;
+        }
+        uint32_t vbits = 0;
+        double vl = 0, vh = 0;
+        if (y == 1) {
+            vbits = (a.vmask[n * DW + c0 / 32] >> (c0 & 31)) & 0xffu;
+            vl = (double)a.vlo[n];
+            vh = (double)a.vhi[n];
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const double x = (double)cal_h2f((uint16_t)(w4[e >> 1] >> (16 * (e & 1))));
+            double lo, hi;
+            bool kept;
+            if (y == 0) {
+                lo = (double)a.klo[c0 + e];
+                hi = (double)a.khi[c0 + e];
+                kept = lo <= x && x <= hi && hi > lo;
+            } else {
+                lo = vl; hi = vh;
+                kept = !((vbits >> e) & 1u) && hi > lo;
+            }
+            if (!kept) continue;
+            const double xn = (x - (hi + lo) / 2.0) / ((hi - lo) / 2.0);
+            int lab = 0;
+#pragma unroll
+            for (int j = 0; j + 1 < KC; ++j) lab += (2.0 * xn > mid[j]) ? 1 : 0;
+            if (MODE == 0) {
+                const double w = (double)wt[e];
+                acc[lab * kCalT + tid] += w;
+                acc[(KC + lab) * kCalT + tid] += w * xn;
+            } else {
+                const double q = cv[lab];
+                m0 += 1.0; m1 += xn; m2 += xn * xn; m3 += q; m4 += q * q;
+            }
+        }
+    }
+    if (MODE == 1) {
+        acc[0 * kCalT + tid] = m0; acc[1 * kCalT + tid] = m1; acc[2 * kCalT + tid] = m2;
+        acc[3 * kCalT + tid] = m3; acc[4 * kCalT + tid] = m4;
+    }
+    __syncthreads();
+    const int NA = MODE == 0 ? 2 * KC : 5;
+    if (tid < NA) {
+        double s = 0.0;
+        for (int t = 0; t < kCalT; ++t) s += acc[tid * kCalT + t];
+        a.part[((size_t)y * kCalG + blockIdx.x) * 32 + tid] = s;
+    }
+}
+
+__device__ float cal_store(double v, float prev, bool first, int fp16) {
+    float r;
+    if (fp16) {
+        const uint16_t h = cal_d2h(v);
+        r = cal_h2f(h);
+        if (!first && !(r > prev)) {
+            const uint16_t p = __half_as_ushort(__float2half_rn(prev));   // prev is an fp16 value
+            const uint16_t nx = (p & 0x8000u) ? (p == 0x8000u ? (uint16_t)1 : (uint16_t)(p - 1)) : (uint16_t)(p + 1);
+            r = cal_h2f(nx);
+        }
+    } else {
+        r = (float)v;
+        if (!first && !(r > prev)) r = nextafterf(prev, INFINITY);
+    }
+    return r;
+}
+
+// one Lloyd update per matrix: thread (y, j) reduces the partials, thread 0 of each half sorts
+__global__ void cal_update_kernel(CalArgs a, int KC) {
+    __shared__ double sums[2][32];
+    const int y = threadIdx.x >> 5, t = threadIdx.x & 31;
+    if (a.done[y]) return;
+    if (t < 2 * KC) {
+        double s = 0.0;
+        for (int g = 0; g < kCalG; ++g) s += a.part[((size_t)y * kCalG + g) * 32 + t];
+        sums[y][t] = s;
+    }
+    __syncwarp();
+    if (t == 0) {
+        double c[16];
+        for (int j = 0; j < KC; ++j) {
+            const double old = a.cent[y * 16 + j], sw = sums[y][j];
+            c[j] = sw > 0.0 ? sums[y][KC + j] / sw : old;
+        }
+        for (int i = 1; i < KC; ++i)
+            for (int j = i; j > 0 && c[j] < c[j - 1]; --j) { const double x = c[j]; c[j] = c[j - 1]; c[j - 1] = x; }
+        double move = 0.0;
+        for (int j = 0; j < KC; ++j) { move = fmax(move, fabs(c[j] - a.cent[y * 16 + j])); a.cent[y * 16 + j] = c[j]; }
+        a.iters[y] += 1;
+        if (move < a.tol) a.done[y] = 1;
+    }
+}
+
+// MODE 0: store the encode codebooks (and copy them to the decode slots); MODE 1: Q-Norm'd
+// decode codebooks from the moments
+template <int MODE>
+__global__ void cal_store_kernel(CalArgs a) {
+    const int y = threadIdx.x;
+    if (y >= 2) return;
+    float *enc = a.cb + (2 * y) * 16, *dec = a.cb + (2 * y + 1) * 16;
+    if (MODE == 0) {
+        float prev = 0.f;
+        for (int j = 0; j < a.k; ++j) { prev = cal_store(a.cent[y * 16 + j], prev, j == 0, a.fp16); enc[j] = prev; dec[j] = prev; }
+    } else {
+        double s[5];
+        for (int t = 0; t < 5; ++t) {
+            s[t] = 0.0;
+            for (int g = 0; g < kCalG; ++g) s[t] += a.part[((size_t)y * kCalG + g) * 32 + t];
+        }
+        if (!(s[0] > 0.0)) return;
+        const double mu1 = s[1] / s[0], mu2 = s[3] / s[0];
+        const double sg1 = sqrt(fmax(s[2] / s[0] - mu1 * mu1, 0.0)), sg2 = sqrt(fmax(s[4] / s[0] - mu2 * mu2, 0.0));
+        if (!(sg2 > 0.0)) return;
+        float prev = 0.f;
+        for (int j = 0; j < a.k; ++j) {
+            prev = cal_store(((double)enc[j] - mu2) * sg1 / sg2 + mu1, prev, j == 0, a.fp16);
+            dec[j] = prev;
+        }
+    }
+}
+
+template <int KC>
+cudaError_t cal_run(CalArgs &a, int max_iter, int qnorm, cudaStream_t s) {
+    const size_t sm0 = (size_t)2 * KC * kCalT * 8, sm1 = (size_t)5 * kCalT * 8;
+    cudaFuncSetAttribute(cal_km_kernel<KC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0);
+    const dim3 grid(kCalG, 2);
+    for (int it = 0; it < max_iter; ++it) {
+        cal_km_kernel<KC, 0><<<grid, kCalT, sm0, s>>>(a);
+        cal_update_kernel<<<1, 64, 0, s>>>(a, KC);
+    }
+    cal_store_kernel<0><<<1, 32, 0, s>>>(a);
+    if (qnorm) {
+        cal_km_kernel<KC, 1><<<grid, kCalT, sm1, s>>>(a);
+        cal_store_kernel<1><<<1, 32, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_layer_sensitivity(const DevCache &c, const __half *K, const __half *V, const float *FK,
@@ -247,6 +579,54 @@ cudaError_t launch_layer_sensitivity(const DevCache &c, const __half *K, const _
     cudaFuncSetAttribute(sens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sens_kernel<<<(unsigned)tiles, 256, smem, s>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_calibrate(const __half *K, const __half *V, const float *FK, const float *FV, int64_t N, int D,
+                             int bits, int ppm, int max_iter, double tol, int qnorm, int fp16, float *key_lo,
+                             float *key_hi, float *cb, int *iters, cudaStream_t s) {
+    cudaError_t e = launch_online_key_thresholds(K, N, D, ppm, key_lo, key_hi, s);
+    if (e != cudaSuccess) return e;
+    const int k = 1 << bits;
+    const size_t DW = (size_t)D / 32;
+    const size_t b_v = (size_t)N * 4, b_m = (size_t)N * DW * 4, b_c = 32 * 8, b_p = (size_t)2 * kCalG * 32 * 8;
+    void *scratch = nullptr;
+    e = cudaMallocAsync(&scratch, 2 * b_v + b_m + b_c + b_p + 64, s);
+    if (e != cudaSuccess) return e;
+    char *p = reinterpret_cast<char *>(scratch);
+    CalArgs a;
+    a.X[0] = reinterpret_cast<const uint16_t *>(K);
+    a.X[1] = reinterpret_cast<const uint16_t *>(V);
+    a.F[0] = FK; a.F[1] = FV;
+    a.N = N; a.D = D; a.k = k;
+    a.kv = (int)(((int64_t)ppm * D + 999999) / 1000000);
+    a.klo = key_lo; a.khi = key_hi;
+    a.cent = reinterpret_cast<double *>(p); p += b_c;
+    a.part = reinterpret_cast<double *>(p); p += b_p;
+    a.vlo = reinterpret_cast<float *>(p); p += b_v;
+    a.vhi = reinterpret_cast<float *>(p); p += b_v;
+    a.vmask = reinterpret_cast<uint32_t *>(p); p += b_m;
+    a.done = iters + 2;    // iters: [2] counts + [2] done flags (caller's device scratch)
+    a.iters = iters;
+    a.tol = tol;
+    a.cb = cb;
+    a.fp16 = fp16;
+    double c0[32];
+    for (int y = 0; y < 2; ++y)
+        for (int j = 0; j < 16; ++j) c0[y * 16 + j] = j < k ? -1.0 + (2.0 * j + 1.0) / k : 0.0;
+    e = cudaMemcpyAsync(a.cent, c0, sizeof c0, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(iters, 0, 4 * sizeof(int), s);
+    if (e != cudaSuccess) { cudaFreeAsync(scratch, s); return e; }
+    const size_t smv = (size_t)4 * D * 2;
+    cudaFuncSetAttribute(cal_vrange_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smv);
+    cal_vrange_kernel<<<(unsigned)((N + 3) / 4), 128, smv, s>>>(a);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+        if (k == 4) e = cal_run<4>(a, max_iter, qnorm, s);
+        else if (k == 8) e = cal_run<8>(a, max_iter, qnorm, s);
+        else e = cal_run<16>(a, max_iter, qnorm, s);
+    }
+    cudaFreeAsync(scratch, s);
+    return e;
 }
 
 cudaError_t launch_fisher_accumulate(float *F, const float *g, int64_t n, cudaStream_t s) {

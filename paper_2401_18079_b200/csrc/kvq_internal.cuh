@@ -122,6 +122,12 @@ cudaError_t launch_online_key_thresholds(const __half *K, int64_t T, int D, int 
 cudaError_t launch_layer_sensitivity(const DevCache &c, const __half *K, const __half *V, const float *FK,
                                      const float *FV, int64_t n0, int64_t T, double *omega, cudaStream_t s);
 cudaError_t launch_fisher_accumulate(float *F, const float *g, int64_t n, cudaStream_t s);
+// ---- offline calibration (kvq_calib.cu) ----
+// cb: device [4][16] (Key enc, Key dec, Value enc, Value dec); iters: device int [4] scratch
+// (Lloyd updates run for Keys / Values, then two done flags)
+cudaError_t launch_calibrate(const __half *K, const __half *V, const float *FK, const float *FV, int64_t N, int D,
+                             int bits, int ppm, int max_iter, double tol, int qnorm, int fp16, float *key_lo,
+                             float *key_hi, float *cb, int *iters, cudaStream_t s);
 
 // ---- attention (kvq_attend.cu) ----
 struct AttendArgs {

@@ -32,13 +32,19 @@ EXPORTED = ["kvq_cache_create", "kvq_cache_destroy", "kvq_append", "kvq_prefill_
             "kvq_f16_cache_create", "kvq_f16_cache_destroy", "kvq_f16_append",
             "kvq_f16_decode_attend", "kvq_f16_export", "kvq_f16_num_tokens",
             "kvq_key_thresholds_online", "kvq_decode_attend_batch", "kvq_layer_sensitivity",
-            "kvq_fisher_accumulate", "kvq_assign_bits"]
+            "kvq_fisher_accumulate", "kvq_assign_bits", "kvq_calibrate_layer"]
 
 
 class KVQError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{_STATUS.get(status, status)}: {msg}")
         self.status = status
+
+
+class kvq_calib_config(ctypes.Structure):
+    _fields_ = [("bits", ctypes.c_int32), ("outlier_ppm", ctypes.c_int32), ("max_iter", ctypes.c_int32),
+                ("qnorm", ctypes.c_int32), ("fp16_codebooks", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("tol", ctypes.c_double)]
 
 
 class kvq_config(ctypes.Structure):
@@ -105,6 +111,8 @@ def _load() -> ctypes.CDLL:
         "kvq_layer_sensitivity": (i32, [vp, vp, vp, vp, vp, i64, i64, vp, vp]),
         "kvq_fisher_accumulate": (i32, [vp, vp, i64, i32, vp]),
         "kvq_assign_bits": (i32, [vp, i32, i32, i32, i32, vp]),
+        "kvq_calibrate_layer": (i32, [vp, vp, vp, vp, i64, i32, ctypes.POINTER(kvq_calib_config), vp, vp, vp, vp,
+                                      vp, vp, vp, i32, vp]),
         "kvq_version": (i32, []),
     }
     for name, (res, args) in sig.items():
@@ -298,6 +306,25 @@ def key_thresholds_online(K, outlier_ppm: int, lo=None, hi=None, device: int = 0
     _check(_lib.kvq_key_thresholds_online(_ptr(K), T, D, int(outlier_ppm), _ptr(lo), _ptr(hi), int(device),
                                           _stream(stream)))
     return lo, hi
+
+
+def calibrate_layer(K, V, bits: int, outlier_ppm: int, FK=None, FV=None, max_iter: int = 100, tol: float = 1e-6,
+                    qnorm: bool = False, fp16_codebooks: bool = True, device: int = 0, stream=None) -> dict:
+    """Offline calibration of one layer on the GPU (kvq_calibrate_layer): Key
+    thresholds and the four codebooks for KVQCache, from calibration K, V [N, D] fp16 (device or
+    host) and optional fp32 Fisher diagonals.  Returns host numpy arrays (synchronizes)."""
+    N, D = (int(x) for x in K.shape)
+    k = 1 << int(bits)
+    cfg = kvq_calib_config(int(bits), int(outlier_ppm), int(max_iter), int(bool(qnorm)), int(bool(fp16_codebooks)),
+                           0, float(tol))
+    out = dict(key_lo=np.zeros(D, np.float32), key_hi=np.zeros(D, np.float32), cbK=np.zeros(k, np.float32),
+               cbK_dec=np.zeros(k, np.float32), cbV=np.zeros(k, np.float32), cbV_dec=np.zeros(k, np.float32),
+               iters=np.zeros(2, np.int32))
+    _check(_lib.kvq_calibrate_layer(_ptr(K), _ptr(V), _ptr(FK), _ptr(FV), N, D, ctypes.byref(cfg),
+                                    _ptr(out["key_lo"]), _ptr(out["key_hi"]), _ptr(out["cbK"]), _ptr(out["cbK_dec"]),
+                                    _ptr(out["cbV"]), _ptr(out["cbV_dec"]), _ptr(out["iters"]), int(device),
+                                    _stream(stream)))
+    return out
 
 
 def layer_sensitivity(cache, K, V, FK=None, FV=None, t0: int = 0, omega=None, stream=None):
