@@ -555,6 +555,8 @@ def run_ours(args):
     # layer-0 prefill block
     batch = None
     online = None
+    calib_out = None
+    sens = None
     if world == 1 and not args.no_compare and w.name.startswith("c3"):
         try:
             nb, tb = 32, 4096
@@ -606,6 +608,58 @@ def run_ours(args):
             del Kl
         except Exception as ex:   # pragma: no cover
             online = {"error": str(ex)[:300]}
+        # f3: offline calibration of one layer on the GPU at the paper's calibration size (16
+        # samples x 2K tokens, tab:kmeans P:1124-1135); f4: the eq:opt2 sensitivity of that layer at
+        # the lower precision (2 bits) with Fisher weights
+        try:
+            ncal = 16 * 2048
+            Kc = gen.gen_layer_torch(41, 0, ncal, D, dev, "K")
+            Vc = gen.gen_layer_torch(41, 0, ncal, D, dev, "V")
+            gF = torch.Generator(device=dev)
+            gF.manual_seed(5)
+            FK = torch.rand((ncal, D), generator=gF, device=dev) ** 2
+            FV = torch.rand((ncal, D), generator=gF, device=dev) ** 2
+            kvq.calibrate_layer(Kc, Vc, w.bits, w.ppm, FK, FV, max_iter=2, device=local, stream=stream)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            res = kvq.calibrate_layer(Kc, Vc, w.bits, w.ppm, FK, FV, max_iter=100, tol=1e-6, qnorm=w.qnorm,
+                                      device=local, stream=stream)
+            c1.record(stream)
+            c1.synchronize()
+            cms = c0.elapsed_time(c1)
+            calib_out = {"tokens": ncal, "D": D, "bits": w.bits, "ms": cms,
+                         "lloyd_updates": [int(x) for x in res["iters"]],
+                         "ms_per_update": cms / max(1, int(max(res["iters"]))),
+                         "note": "thresholds + Value splits + Fisher-weighted k-means (Keys and Values) + "
+                                 "Q-Norm, one kvq_calibrate_layer call; the paper reports minutes per layer "
+                                 "on a CPU (tab:kmeans)"}
+            cal2 = {"key_lo": res["key_lo"], "key_hi": res["key_hi"]}
+            r2 = kvq.calibrate_layer(Kc[:4096], Vc[:4096], 2, w.ppm, max_iter=30, device=local, stream=stream)
+            cal2.update({k: r2[k] for k in ("cbK", "cbV", "cbK_dec", "cbV_dec")})
+            pc = kvq.KVQCache(n_q_heads=H, n_kv_heads=w.H_kv, head_dim=d, bits=2, outlier_ppm=w.ppm,
+                              capacity_tokens=ncal, key_cb=cal2["cbK"], val_cb=cal2["cbV"],
+                              key_cb_dec=cal2["cbK_dec"], val_cb_dec=cal2["cbV_dec"], key_lo=cal2["key_lo"],
+                              key_hi=cal2["key_hi"], device=local)
+            pc.prefill(Kc, Vc, stream)
+            om = torch.zeros(2, dtype=torch.float64, device=dev)
+            kvq.layer_sensitivity(pc, Kc, Vc, FK, FV, 0, om, stream)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(5):
+                kvq.layer_sensitivity(pc, Kc, Vc, FK, FV, 0, om, stream)
+            s1.record(stream)
+            s1.synchronize()
+            sms_ = s0.elapsed_time(s1) / 5
+            sbytes = ncal * D * (2 + 2 + 4 + 4) + ncal * D * 2 * 2 // 8
+            sens = {"tokens": ncal, "bits": 2, "ms": sms_, "ns_per_token_layer": sms_ * 1e6 / ncal,
+                    "omega": [float(x) for x in om.cpu()], "gbs": sbytes / (sms_ * 1e-3) / 1e9,
+                    "note": "kvq_layer_sensitivity: reads K, V (fp16), F_K, F_V (fp32) and the 2-bit cache"}
+            del pc, Kc, Vc, FK, FV
+            torch.cuda.empty_cache()
+        except Exception as ex:   # pragma: no cover
+            if calib_out is None:
+                calib_out = {"error": str(ex)[:300]}
+            sens = {"error": str(ex)[:300]}
 
     resid = None
     if world == 1 and not args.no_compare:
@@ -675,7 +729,7 @@ def run_ours(args):
                          "bytes_per_launch": bytes_att, "peak_kind": peak_kind,
                          "splits": info["splits"], "heads_per_cta": info["heads_per_cta"]},
             "compare": compare, "resid_codebook": resid, "batched_decode": batch,
-            "online_key_thresholds": online,
+            "online_key_thresholds": online, "offline_calibration": calib_out, "sensitivity": sens,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps * L_res * (2 if world == 1 else 3),
             "clocks": clocks.summary(),

@@ -426,7 +426,7 @@ static kvq_status append_tokens(kvq_cache *c, const void *K, const void *V, int6
         if ((const void *)Kd != (const void *)sb) { CK(cudaMemcpyAsync(sb, Kd, bytes, cudaMemcpyDeviceToDevice, s)); Kd = (const __half *)sb; }
         if ((const void *)Vd != (const void *)(sb + bytes)) { CK(cudaMemcpyAsync(sb + bytes, Vd, bytes, cudaMemcpyDeviceToDevice, s)); Vd = (const __half *)(sb + bytes); }
     }
-    cudaError_t e = T == 1 ? launch_append(c->dc, Kd, Vd, c->T, s)
+    cudaError_t e = T == 1 ? launch_append(c->dc, Kd, Vd, c->T, s, c->timers ? c->timers + 16 : nullptr)
                            : launch_prefill(c->dc, Kd, Vd, c->T, T, c->dc.lb, c->dc.ticket, s);
     if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
     c->T += T;

@@ -51,6 +51,12 @@ __device__ __forceinline__ uint32_t okey(uint32_t h) {
     uint32_t k = h ^ ((h & 0x8000u) ? 0xffffu : 0x8000u);
     return k == 0x7fffu ? 0x8000u : k;
 }
+// fp16 bits of element e (0..7, run-time) of an 8-half vector, without indexing a register
+// array (a dynamic index would put the array on the stack: a local-memory round trip per use)
+__device__ __forceinline__ uint32_t half_at(const uint4 &u, int e) {
+    const uint32_t w = (e & 4) ? ((e & 2) ? u.w : u.z) : ((e & 2) ? u.y : u.x);
+    return (e & 1) ? (w >> 16) : (w & 0xffffu);
+}
 // order key -> fp16 bits (0x8000 -> +0)
 __device__ __forceinline__ uint32_t key2h(uint32_t k) { return k >= 0x8000u ? (k ^ 0x8000u) : (k ^ 0xffffu); }
 
@@ -103,7 +109,7 @@ constexpr int TI_LO = 0, TI_HI = 1, TI_CLO = 2, TI_CHI = 3, TI_T = 4;   // tinfo
 // (desc) or (value asc, index asc) order among elements not already in `mask`.  Bit-by-bit
 // search of the order-key threshold, then ties at the threshold in index order.  Element
 // ownership: lane l holds channels 256m + 8l + e.
-__device__ void select_exact(const __half *row, int D, int need, bool desc, uint32_t *mask) {
+__device__ __noinline__ void select_exact(const __half *row, int D, int need, bool desc, uint32_t *mask) {
     const int lane = threadIdx.x & 31;
     if (need <= 0) return;
     const int nch = (D + 255) / 256;
@@ -167,39 +173,155 @@ __device__ void select_exact(const __half *row, int D, int need, bool desc, uint
     __syncwarp();
 }
 
+// Exact two-sided selection of one token by one warp (the slow path): the ku largest, then the kl
+// smallest of the rest, into `vm` (zeroed here), and the kept min / max (lowest index attaining
+// them, R7) as fp16 bits.
+__device__ __noinline__ void vselect_exact_warp(const __half *row, int D, int ku, int kl, uint32_t *vm, uint32_t &lo_h,
+                                   uint32_t &hi_h) {
+    const int lane = threadIdx.x & 31, DW = D / 32, nch = (D + 255) / 256;
+    for (int x = lane; x < DW; x += 32) vm[x] = 0;
+    __syncwarp();
+    select_exact(row, D, ku, true, vm);
+    select_exact(row, D, kl, false, vm);
+    uint32_t bh = 0, bl2 = 0xffffffffu;   // (key << 16 | 0xffff - idx) max; (key << 16 | idx) min
+    for (int m = 0; m < nch; ++m) {
+        const int c0 = 256 * m + 8 * lane;
+        if (c0 >= D) continue;
+        const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        const uint32_t mw = vm[c0 >> 5] >> (c0 & 31);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if ((mw >> e) & 1u) continue;
+            const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+            bh = max(bh, (key << 16) | (0xffffu - (uint32_t)(c0 + e)));
+            bl2 = min(bl2, (key << 16) | (uint32_t)(c0 + e));
+        }
+    }
+    bh = __reduce_max_sync(0xffffffffu, bh);
+    bl2 = __reduce_min_sync(0xffffffffu, bl2);
+    hi_h = __half_as_ushort(row[0xffff - (bh & 0xffffu)]);
+    lo_h = __half_as_ushort(row[bl2 & 0xffffu]);
+}
+
+// The rest of one token's Value quantization by one warp, after the selection: (s, z) in fp64
+// rounded once (R6), the token's ENC thresholds and the codes of lo / hi (tinfo_row), the CSR
+// records of its k outliers (ascending channel).
+template <int NM>
+__device__ void vfinish_warp(const DevCache &c, const __half *row, int D, const uint32_t *vm, uint32_t lo_h,
+                             uint32_t hi_h, uint16_t *tinfo_row, int64_t n, const double *vmids) {
+    const int lane = threadIdx.x & 31, DW = D / 32, k = c.kv;
+    // (s, z) in fp64, rounded once (R6); ENC thresholds of the token (lanes 0..NM-1)
+    const double lo = (double)__half2float(__ushort_as_half((uint16_t)lo_h));
+    const double hi = (double)__half2float(__ushort_as_half((uint16_t)hi_h));
+    const float s = __double2float_rn(__dsub_rn(hi, lo) / 2.0);
+    const float z = __double2float_rn(__dadd_rn(hi, lo) / 2.0);
+    uint16_t *ti = tinfo_row;
+    if (lane == 0) {
+        c.vsz[n] = make_float2(s, z);
+        ti[TI_LO] = (uint16_t)lo_h;
+        ti[TI_HI] = (uint16_t)hi_h;
+    }
+    uint32_t thr = 0x7c00u;   // +inf: never
+    if (lane < NM) {
+        // T_j = the smallest fp16 (order key in [0x0400, 0xfc00), else the +inf sentinel 0xfc00)
+        // with 2(y - z) > s m_j in fp64 -- a monotone predicate.  Start at the fp16 nearest to
+        // z + s m_j / 2 and walk to the boundary (one or two steps); a binary search if the walk
+        // is long.
+        const double mj = vmids[lane];
+        const double sd = (double)s, zd = (double)z;
+        auto pred = [&](uint32_t key) {
+            const double y = (double)__half2float(__ushort_as_half((uint16_t)key2h(key)));
+            return 2.0 * __dsub_rn(y, zd) > __dmul_rn(sd, mj);
+        };
+        unsigned short h0;
+        asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h0) : "d"(__fma_rn(0.5 * sd, mj, zd)));
+        uint32_t a = min(max(okey(h0), 0x0400u), 0xfbffu);
+        int steps = 0;
+        if (pred(a)) {
+            while (a > 0x0400u && steps < 8 && pred(a - 1)) { --a; ++steps; }
+        } else {
+            while (a < 0xfc00u && steps < 8 && !pred(a)) { ++a; ++steps; }
+        }
+        if (steps == 8) {
+            uint32_t lo = 0x0400u, hi = 0xfc00u;   // order keys of -65504 .. +inf (sentinel)
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (pred(mid)) hi = mid; else lo = mid + 1;
+            }
+            a = lo;
+        }
+        thr = key2h(a);
+        ti[TI_T + lane] = (uint16_t)thr;
+    }
+    // codes of lo and hi (item flags of the outliers)
+    const uint32_t klo = okey(lo_h), khi = okey(hi_h), kt = okey(thr);
+    const int clo = __popc(__ballot_sync(0xffffffffu, lane < NM && klo >= kt));
+    const int chi = __popc(__ballot_sync(0xffffffffu, lane < NM && khi >= kt));
+    if (lane == 0) { ti[TI_CLO] = (uint16_t)clo; ti[TI_CHI] = (uint16_t)chi; }
+    __syncwarp();
+    // CSR records of the token's k outliers (ascending channel) and per-group counts
+    if (k > 0) {
+        const int wpl = (DW + 31) / 32;   // mask words per lane (ascending channels)
+        int cnt = 0;
+        for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x) cnt += __popc(vm[x]);
+        int ex = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ex, o);
+            if (lane >= o) ex += y;
+        }
+        ex -= cnt;
+        uint32_t *vo = c.vout + n * (int64_t)k;
+        for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x)
+            for (uint32_t b = vm[x]; b; b &= b - 1) {
+                const int ch = 32 * x + __ffs(b) - 1;
+                vo[ex++] = (uint32_t)ch | ((uint32_t)__half_as_ushort(row[ch]) << 16);
+            }
+    }
+}
+
 // One token's Value quantization by one warp (reads R2, R3, R6, R7, R8): the two-sided top-k
 // outliers (bitmask vm, [D/32] words, zeroed by the caller), kept range, (s, z) -> c.vsz[n],
 // ENC thresholds and the codes of lo / hi -> tinfo_row, CSR records -> c.vout row n.
 // cand: per-warp scratch [2][CANDMAX]; nc2: per-warp [2] counters.
 template <int NM>
 __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_t *vm, uint32_t *cand,
-                            int *nc2, uint16_t *tinfo_row, int64_t n) {
+                            int *nc2, uint16_t *tinfo_row, int64_t n, unsigned long long *tr = nullptr) {
     const int lane = threadIdx.x & 31;
     const int DW = D / 32;
+    auto vstamp = [&](int i) {   // diagnostics (append trace only)
+        if (tr && lane == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMax(tr + i, t);
+        }
+    };
     const int k = c.kv, ku = (k + 1) / 2, kl = k / 2;
     const int nch = (D + 255) / 256;
         // group maxima / minima (fp16 values; 2 groups per lane: even / odd chunks)
-        __half2 mx[2], mn[2];
-        mx[0] = mx[1] = __float2half2_rn(-65504.f);
-        mn[0] = mn[1] = __float2half2_rn(65504.f);
-        bool have[2] = {false, false};
-        for (int m = 0; m < nch; ++m) {
-            const int c0 = 256 * m + 8 * lane;
-            if (c0 >= D) continue;
-            const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
-            const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
-            const __half2 b = __hmin2(__hmin2(u2h(u.x), u2h(u.y)), __hmin2(u2h(u.z), u2h(u.w)));
-            mx[m & 1] = __hmax2(mx[m & 1], a);
-            mn[m & 1] = __hmin2(mn[m & 1], b);
-            have[m & 1] = true;
+        // (scalars, chunk pairs per iteration: a run-time index into a register array would
+        // live on the stack)
+        __half2 mx0 = __float2half2_rn(-65504.f), mx1 = mx0, mn0 = __float2half2_rn(65504.f), mn1 = mn0;
+        bool have0 = false, have1 = false;
+        for (int m = 0; m < nch; m += 2) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int c0 = 256 * (m + q) + 8 * lane;
+                if (m + q >= nch || c0 >= D) continue;
+                const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
+                const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
+                const __half2 b = __hmin2(__hmin2(u2h(u.x), u2h(u.y)), __hmin2(u2h(u.z), u2h(u.w)));
+                if (q == 0) { mx0 = __hmax2(mx0, a); mn0 = __hmin2(mn0, b); have0 = true; }
+                else        { mx1 = __hmax2(mx1, a); mn1 = __hmin2(mn1, b); have1 = true; }
+            }
         }
         // (need+1)-th largest group max / smallest group min, bit search on order keys
         uint32_t gk[2], gl[2];
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-            gk[g] = have[g] ? okey(h2u(__hmax2(mx[g], __lowhigh2highlow(mx[g])))) : 0u;
-            gl[g] = have[g] ? 0xffffu - okey(h2u(__hmin2(mn[g], __lowhigh2highlow(mn[g])))) : 0u;
-        }
+        gk[0] = have0 ? okey(h2u(__hmax2(mx0, __lowhigh2highlow(mx0)))) : 0u;
+        gk[1] = have1 ? okey(h2u(__hmax2(mx1, __lowhigh2highlow(mx1)))) : 0u;
+        gl[0] = have0 ? 0xffffu - okey(h2u(__hmin2(mn0, __lowhigh2highlow(mn0)))) : 0u;
+        gl[1] = have1 ? 0xffffu - okey(h2u(__hmin2(mn1, __lowhigh2highlow(mn1)))) : 0u;
         auto kth = [&](const uint32_t (&v)[2], int need) {
             uint32_t t = 0;
             for (int b = 15; b >= 0; --b) {
@@ -209,8 +331,10 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
             }
             return t;
         };
+        vstamp(8);
         const uint32_t tau_hi = kth(gk, ku + 1);                // order key
         const uint32_t tau_lo = 0xffffu - kth(gl, kl + 1);      // order key
+        vstamp(9);
         // candidates: value >= tau_hi (upper), value <= tau_lo (lower)
         if (lane < 2) nc2[lane] = 0;
         __syncwarp();
@@ -241,16 +365,15 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
                 if (nl) bl = atomicAdd(&nc2[1], nl);
                 if (fu | fl) {
                     const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
-                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
                     for (uint32_t x = fu; x; x &= x - 1) {
                         const int e = __ffs(x) - 1;
-                        const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                        const uint32_t key = okey(half_at(u, e));
                         if (bu < CANDMAX) cand[bu] = (key << 13) | (8191u - (uint32_t)(c0 + e));
                         ++bu;
                     }
                     for (uint32_t x = fl; x; x &= x - 1) {
                         const int e = __ffs(x) - 1;
-                        const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                        const uint32_t key = okey(half_at(u, e));
                         if (bl < CANDMAX) cand[CANDMAX + bl] = ((0xffffu - key) << 13) | (8191u - (uint32_t)(c0 + e));
                         ++bl;
                     }
@@ -258,6 +381,7 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
             }
         }
         __syncwarp();
+        vstamp(10);
         const int NU = nc2[0], NL = nc2[1];
         ovf = NU > CANDMAX || NL > CANDMAX || NU < ku + 1 || NL < kl + 1 || tau_lo >= tau_hi;
         uint32_t lo_h = 0, hi_h = 0;   // fp16 bits of the kept min / max
@@ -286,80 +410,12 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
             lo_h = __half_as_ushort(row[lo_idx]);
             __syncwarp();
         } else {
-            // exact selection over all elements, then the kept range (lowest index)
-            for (int x = lane; x < DW; x += 32) vm[x] = 0;
-            __syncwarp();
-            select_exact(row, D, ku, true, vm);
-            select_exact(row, D, kl, false, vm);
-            uint32_t bh = 0, bl2 = 0xffffffffu;   // (key << 16 | 0xffff - idx) max; (key << 16 | idx) min
-            for (int m = 0; m < nch; ++m) {
-                const int c0 = 256 * m + 8 * lane;
-                if (c0 >= D) continue;
-                const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
-                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-                const uint32_t mw = vm[c0 >> 5] >> (c0 & 31);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    if ((mw >> e) & 1u) continue;
-                    const uint32_t key = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
-                    bh = max(bh, (key << 16) | (0xffffu - (uint32_t)(c0 + e)));
-                    bl2 = min(bl2, (key << 16) | (uint32_t)(c0 + e));
-                }
-            }
-            bh = __reduce_max_sync(0xffffffffu, bh);
-            bl2 = __reduce_min_sync(0xffffffffu, bl2);
-            hi_h = __half_as_ushort(row[0xffff - (bh & 0xffffu)]);
-            lo_h = __half_as_ushort(row[bl2 & 0xffffu]);
+            vselect_exact_warp(row, D, ku, kl, vm, lo_h, hi_h);
         }
-        // (s, z) in fp64, rounded once (R6); ENC thresholds of the token (lanes 0..NM-1)
-        const double lo = (double)__half2float(__ushort_as_half((uint16_t)lo_h));
-        const double hi = (double)__half2float(__ushort_as_half((uint16_t)hi_h));
-        const float s = __double2float_rn(__dsub_rn(hi, lo) / 2.0);
-        const float z = __double2float_rn(__dadd_rn(hi, lo) / 2.0);
-        uint16_t *ti = tinfo_row;
-        if (lane == 0) {
-            c.vsz[n] = make_float2(s, z);
-            ti[TI_LO] = (uint16_t)lo_h;
-            ti[TI_HI] = (uint16_t)hi_h;
-        }
-        uint32_t thr = 0x7c00u;   // +inf: never
-        if (lane < NM) {
-            const double mj = c.mids[16 + lane];
-            const double sd = (double)s, zd = (double)z;
-            uint32_t a = 0x0400u, b = 0xfc00u;   // order keys of -65504 .. +inf (sentinel)
-            while (a < b) {
-                const uint32_t mid = (a + b) >> 1;
-                const double y = (double)__half2float(__ushort_as_half((uint16_t)key2h(mid)));
-                if (2.0 * __dsub_rn(y, zd) > __dmul_rn(sd, mj)) b = mid; else a = mid + 1;
-            }
-            thr = key2h(a);
-            ti[TI_T + lane] = (uint16_t)thr;
-        }
-        // codes of lo and hi (item flags of the outliers)
-        const uint32_t klo = okey(lo_h), khi = okey(hi_h), kt = okey(thr);
-        const int clo = __popc(__ballot_sync(0xffffffffu, lane < NM && klo >= kt));
-        const int chi = __popc(__ballot_sync(0xffffffffu, lane < NM && khi >= kt));
-        if (lane == 0) { ti[TI_CLO] = (uint16_t)clo; ti[TI_CHI] = (uint16_t)chi; }
-        __syncwarp();
-        // CSR records of the token's k outliers (ascending channel) and per-group counts
-        if (k > 0) {
-            const int wpl = (DW + 31) / 32;   // mask words per lane (ascending channels)
-            int cnt = 0;
-            for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x) cnt += __popc(vm[x]);
-            int ex = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, ex, o);
-                if (lane >= o) ex += y;
-            }
-            ex -= cnt;
-            uint32_t *vo = c.vout + n * (int64_t)k;
-            for (int x = wpl * lane; x < wpl * lane + wpl && x < DW; ++x)
-                for (uint32_t b = vm[x]; b; b &= b - 1) {
-                    const int ch = 32 * x + __ffs(b) - 1;
-                    vo[ex++] = (uint32_t)ch | ((uint32_t)__half_as_ushort(row[ch]) << 16);
-                }
-        }
+        vstamp(11);
+        if (tr && lane == 0) atomicMax(tr + 15, (unsigned long long)(ovf ? 1000000 + NU * 1000 + NL : NU * 1000 + NL));
+        vfinish_warp<NM>(c, row, D, vm, lo_h, hi_h, tinfo_row, n, c.mids + 16);
+
 }
 
 // ------------------------------------------------------------------------------ kernel
@@ -709,47 +765,208 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
 
 // ============================================================================ append
 // Quantize-on-append of ONE decode token, latency-oriented: one CTA of 32
-// warps.  Warp 0 runs the Value selection / thresholds / CSR records of the token (the same
-// vtoken_warp as the prefill); warps 1..31 take a KV head each: lane = RoPE pairs (lane,
-// lane + 32), codes from the exact fp16 ENC thresholds (kenc), pair codes assembled into the
-// head's 12 pair-stream words, outlier bits by ballot.  Then the Key CSC slot (kptr), Key
-// records and bucket items, Value items, and the Value codes OR-ed into the fragment-ordered
-// tile words (one OR per two codes).  The kernel lets a dependent attend launch at once
-// (programmatic dependent launch; its prologue reads no cache data).
+// warps, every phase spread over the CTA (a single warp's serial selection took 14 of the
+// 19 us of the round-2 kernel).
+//   1  rows staged in shared memory; warp 31 fetches the CSC base kptr[n] and the bucket counts
+//      of the tile at the same time (their latency hides under the staging)
+//   2  Value selection by the whole CTA (vselect_block): per-thread groups of 8 elements, the
+//      two candidate bounds by warps 0 / 1, candidates compacted by every warp, one rank per
+//      thread -- the same bound argument and result as vtoken_warp
+//   3  warp 0: (s, z), the token's ENC thresholds, CSR records (vfinish_warp); warps 1..31: Keys,
+//      a KV head each: lane = RoPE pairs (lane, lane + 32), codes from the exact fp16 ENC
+//      thresholds (kenc), pair-stream words, outlier bits by ballot
+//   4  Key CSC slot; Key records + bucket items (warp per head; codes from the pair codes);
+//      Value items (thread per mask word); Value codes OR-ed into the fragment-ordered tile
+//      words (one OR per two codes)
+// The kernel lets a dependent attend launch at once (programmatic dependent launch; its
+// prologue reads no cache data).
 constexpr int AT = 1024, AW = AT / 32;
 
+// Block-wide selection of the token's ku largest and then kl smallest Values (R2, R3), into vm
+// (D/32 words), and the kept min / max fp16 bits (lowest index attaining them, R7).  Groups of 8
+// elements per thread: the (ku+1)-th largest group max tau bounds the ku + 1 largest elements
+// from below for any grouping, so the candidates (elements >= tau) contain them; each candidate
+// is ranked by (value desc, index asc) against the others.  The exact warp path takes over when
+// the bound admits more than CANDMAX candidates (ties, tiny D).  sh: [8] shared ints.
+__device__ void vselect_block(const __half *row, int D, int ku, int kl, uint32_t *vm, uint32_t *cand,
+                              uint32_t *gk, uint32_t *gl, int *sh, uint32_t &lo_h, uint32_t &hi_h) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ng = D / 8, DW = D / 32;
+    for (int x = tid; x < DW; x += AT) vm[x] = 0;
+    if (tid < 8) sh[tid] = 0;
+    const bool act = tid < ng;
+    uint4 u = make_uint4(0, 0, 0, 0);
+    uint32_t kmax = 0, kmin = 0xffffu;
+    if (act) {
+        u = *reinterpret_cast<const uint4 *>(row + 8 * tid);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint32_t k = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+            kmax = max(kmax, k);
+            kmin = min(kmin, k);
+        }
+    }
+    // the bounds: a high-byte histogram of the group maxima (and of the mirrored minima); tau =
+    // the lowest key of the bin holding the (ku+1)-th largest, a valid (slightly lower) bound
+    uint32_t *hist = gk;   // [2][256]
+    if (tid < 512) hist[tid] = 0;
+    __syncthreads();
+    if (act) {
+        atomicAdd(&hist[kmax >> 8], 1u);
+        atomicAdd(&hist[256 + ((0xffffu - kmin) >> 8)], 1u);
+    }
+    __syncthreads();
+    if (warp < 2) {   // warp 0: upper side, warp 1: lower side (mirrored keys)
+        const uint32_t *hh = hist + 256 * warp;
+        const int need = warp == 0 ? ku + 1 : kl + 1;
+        int cb[8], sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { cb[q] = (int)hh[255 - 8 * lane - q]; sum += cb[q]; }   // descending bins
+        int inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const int exc = inc - sum;
+        const bool mine = exc < need && need <= inc;
+        int bin = 0;
+        if (mine) {
+            int run = exc;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (run < need && need <= run + cb[q]) bin = 255 - 8 * lane - q;
+                run += cb[q];
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, mine);
+        bin = bal ? __shfl_sync(0xffffffffu, bin, __ffs(bal) - 1) : 0;   // none: fewer groups than need
+        if (lane == 0) sh[2 + warp] = (int)(warp == 0 ? ((uint32_t)bin << 8) : 0xffffu - ((uint32_t)bin << 8));
+    }
+    __syncthreads();
+    const uint32_t tau_hi = (uint32_t)sh[2], tau_lo = (uint32_t)sh[3];
+    // candidates, compacted per warp
+    uint32_t fu = 0, fl = 0;
+    if (act) {
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint32_t k = okey(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+            fu |= (uint32_t)(k >= tau_hi) << e;
+            fl |= (uint32_t)(k <= tau_lo) << e;
+        }
+    }
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        const uint32_t f = side ? fl : fu;
+        const int cntl = __popc(f);
+        int inc = cntl;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        int base = 0;
+        if (lane == 31 && inc) base = atomicAdd(&sh[side], inc);
+        base = __shfl_sync(0xffffffffu, base, 31) + inc - cntl;
+        for (uint32_t x = f; x; x &= x - 1) {
+            const int e = __ffs(x) - 1, ch = 8 * tid + e;
+            const uint32_t k = okey(half_at(u, e));
+            if (base < CANDMAX)
+                cand[side * CANDMAX + base] = ((side ? 0xffffu - k : k) << 13) | (8191u - (uint32_t)ch);
+            ++base;
+        }
+    }
+    __syncthreads();
+    const int NU = sh[0], NL = sh[1];
+    const bool ovf = NU > CANDMAX || NL > CANDMAX || NU < ku + 1 || NL < kl + 1 || tau_lo >= tau_hi;
+    if (!ovf) {
+        const int side = tid >= AT / 2 ? 1 : 0, i = tid - side * (AT / 2);
+        const int nn = side ? NL : NU, kk = side ? kl : ku;
+        if (i < nn) {
+            const uint32_t *cs = cand + side * CANDMAX;
+            const uint32_t v = cs[i];
+            int r = 0;
+            for (int q = 0; q < nn; ++q) r += cs[q] > v ? 1 : 0;
+            const int ch = 8191 - (int)(v & 8191u);
+            if (r < kk) atomicOr(&vm[ch >> 5], 1u << (ch & 31));
+            if (r == kk) sh[4 + side] = ch;
+        }
+        __syncthreads();
+        hi_h = __half_as_ushort(row[sh[4]]);
+        lo_h = __half_as_ushort(row[sh[5]]);
+    } else {
+        if (warp == 0) {
+            uint32_t l, h;
+            vselect_exact_warp(row, D, ku, kl, vm, l, h);
+            if (lane == 0) { sh[6] = (int)l; sh[7] = (int)h; }
+        }
+        __syncthreads();
+        lo_h = (uint32_t)sh[6];
+        hi_h = (uint32_t)sh[7];
+    }
+}
+
 template <int BITS>
-__global__ void __launch_bounds__(AT, 1) append_kernel(DevCache c, const __half *K, const __half *V, int64_t n) {
+__global__ void __launch_bounds__(AT, 1) append_kernel(DevCache c, const __half *K, const __half *V, int64_t n,
+                                                        unsigned long long *tr) {
     asm volatile("griddepcontrol.launch_dependents;");
+    // diagnostics: %globaltimer at phase ends, max over the threads that reach them
+    auto stamp = [&](int i) {
+        if (tr) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMax(tr + i, t);
+        }
+    };
+    if (threadIdx.x == 0) stamp(0);
     using Cf = PCfg<BITS>;
     constexpr int NM = Cf::NM, PS = Cf::PS, CM = (1 << BITS) - 1, KWH = 4 * BITS;
     __shared__ uint32_t vm[8192 / 32], cand[2 * CANDMAX], kmh[64 * 4];
-    __shared__ uint8_t pcs[64 * 64];
-    __shared__ int nc2[2], kcnt[64], kbase[64], gslotK[64], gslotV[64];
+    // group bounds of the selection, then (dead by then) the pair codes of the Keys
+    __shared__ __align__(16) uint32_t gkl[2 * AT];
+    uint32_t *gk = gkl, *gl = gkl + AT;
+    uint8_t *pcs = reinterpret_cast<uint8_t *>(gkl);   // [64 heads][64 pairs]
+    __shared__ int sh[8], kcnt[64], kbase[64], gslotK[64], gslotV[64];
     __shared__ uint16_t ti[24];
     __shared__ uint32_t s_kb0, s_ok;
-    // the token's K and V rows staged in shared memory by all threads first: the single
-    // selection warp then never waits on HBM latency (in a one-token launch nothing hides it)
+    __shared__ double s_mids[16];
     __shared__ __align__(16) __half ks[8192], vs[8192];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = c.D, H = c.H_kv, NG = c.NG, GW = c.GW, DW = D / 32;
     const int64_t tile = n >> 5;
     const int jj = (int)(n & 31);
+    const int k = c.kv, ku = (k + 1) / 2, kl = k / 2;
+    // 1: rows -> shared; the CSC base and the tile's bucket counts fetched alongside
     for (int x = tid; x < D / 8; x += AT) {
         reinterpret_cast<uint4 *>(ks)[x] = reinterpret_cast<const uint4 *>(K)[x];
         reinterpret_cast<uint4 *>(vs)[x] = reinterpret_cast<const uint4 *>(V)[x];
     }
+    if (warp == AW - 1) {
+        if (lane == 0) s_kb0 = c.kptr[n];
+        if (lane < 16) s_mids[lane] = c.mids[16 + lane];
+        for (int g = lane; g < NG; g += 32) {
+            gslotK[g] = (int)c.gcnt[(tile * NG + g) * 2];
+            gslotV[g] = (int)c.gcnt[(tile * NG + g) * 2 + 1];
+        }
+    }
     __syncthreads();
+    if (threadIdx.x == 0) stamp(1);
     K = ks;
     V = vs;
 
-    // ---------------------------------------------------------------- Values (warp 0)
+    // 2: Value selection, whole CTA
+    uint32_t lo_h, hi_h;
+    vselect_block(V, D, ku, kl, vm, cand, gk, gl, sh, lo_h, hi_h);
+    if (threadIdx.x == 0) stamp(8);
+
     if (warp == 0) {
-        for (int x = lane; x < DW; x += 32) vm[x] = 0;
-        __syncwarp();
-        vtoken_warp<NM>(c, V, D, vm, cand, nc2, ti, n);
+        // 3a: (s, z), thresholds, CSR records
+        vfinish_warp<NM>(c, V, D, vm, lo_h, hi_h, ti, n, s_mids);
+        if (lane == 0) stamp(2);
     } else {
-        // ------------------------------------------------------------ Keys (warps 1..31)
+        // 3b: Keys (warps 1..31)
         const uint4 *kenc = reinterpret_cast<const uint4 *>(c.kenc);
         for (int h = warp - 1; h < H; h += AW - 1) {
             uint32_t ob01[2];
@@ -791,16 +1008,18 @@ __global__ void __launch_bounds__(AT, 1) append_kernel(DevCache c, const __half 
                 uint32_t word = 0;
                 const int p0 = (32 * w) / (2 * BITS), p1 = min(kPairs - 1, (32 * w + 31) / (2 * BITS));
                 for (int p = p0; p <= p1; ++p) {
-                    const int sh = 2 * BITS * p - 32 * w;
+                    const int sh2 = 2 * BITS * p - 32 * w;
                     const uint32_t pc = pcs[h * 64 + p];
-                    word |= sh >= 0 ? (pc << sh) : (pc >> -sh);
+                    word |= sh2 >= 0 ? (pc << sh2) : (pc >> -sh2);
                 }
                 c.kcodes[(tile * c.QW + h * KWH + w) * 32 + jj] = word;
             }
         }
+        if (lane == 0) stamp(3);
     }
     __syncthreads();
-    // ------------------------------------------- Key CSC slot and bucket slots (warp 0)
+    if (threadIdx.x == 0) stamp(4);
+    // 4a: Key CSC slot (warp 0)
     if (warp == 0) {
         int e0 = lane < H ? kcnt[lane] : 0, e1 = lane + 32 < H ? kcnt[lane + 32] : 0;
         int x0 = e0, x1 = e1;
@@ -814,22 +1033,18 @@ __global__ void __launch_bounds__(AT, 1) append_kernel(DevCache c, const __half 
         if (lane + 32 < H) kbase[lane + 32] = t0 + x1 - e1;
         const int total = t0 + __shfl_sync(0xffffffffu, x1, 31);
         if (lane == 0) {
-            const uint32_t base = c.kptr[n];
+            const uint32_t base = s_kb0;
             const bool ok = (int64_t)base + total <= c.kcap;
             if (!ok) *(volatile int *)c.err |= kErrKeyCapacity;
             c.kptr[n + 1] = ok ? base + (uint32_t)total : base;
-            s_kb0 = base;
             s_ok = ok;
-        }
-        for (int g = lane; g < NG; g += 32) {
-            gslotK[g] = (int)c.gcnt[(tile * NG + g) * 2];
-            gslotV[g] = (int)c.gcnt[(tile * NG + g) * 2 + 1];
         }
     }
     __syncthreads();
-    // ----------------------------- Key records + items (warps 1..31), Value items (warp 0)
+    if (threadIdx.x == 0) stamp(5);
+    // 4b: Key records + items (warps 1..31, a head each); Value items (thread per mask word of
+    // warp 0, in channel order within each group)
     if (warp > 0) {
-        const uint32_t *kenc32 = c.kenc;
         for (int h = warp - 1; h < H; h += AW - 1) {
             if (kcnt[h] == 0) continue;
             const int g = (h * kHeadDim) / GW;
@@ -844,12 +1059,8 @@ __global__ void __launch_bounds__(AT, 1) append_kernel(DevCache c, const __half 
                     const int cc = 32 * w + lane, ch = h * kHeadDim + cc;
                     const uint32_t xh = __half_as_ushort(K[ch]);
                     if (s_ok) c.kout[s_kb0 + (uint32_t)(kbase[h] + r)] = (uint32_t)ch | (xh << 16);
-                    const int pp = cc & 63, up = cc >> 6;
-                    const uint32_t *te = kenc32 + (size_t)(h * kPairs + pp) * PS;
-                    const __half2 lo2 = u2h(te[0]);
-                    const bool below = __hlt(__ushort_as_half((uint16_t)xh), up ? __high2half(lo2) : __low2half(lo2));
-                    const uint32_t cw = h2u(__hadd2(u2h(te[below ? 2 : 3]), __float2half2_rn(1024.f)));
-                    const int code = (int)((up ? cw >> 16 : cw) & 0xfu);
+                    const uint32_t pc = pcs[h * 64 + (cc & 63)];
+                    const int code = (int)((cc >> 6) ? (pc >> BITS) : (pc & CM));
                     const int slot = gslotK[g] + before + r;
                     if (slot < c.kcap_g)
                         c.kit[(tile * NG + g) * (int64_t)c.kcap_g + slot] =
@@ -860,28 +1071,34 @@ __global__ void __launch_bounds__(AT, 1) append_kernel(DevCache c, const __half 
         }
     } else {
         const uint32_t khi = okey(ti[TI_HI]);
-        for (int g = lane; g < NG; g += 32) {
+        const int wpg = GW / 32;   // mask words per group
+        for (int x = lane; x < DW; x += 32) {
+            const int g = x / wpg;
             int slot = gslotV[g];
-            for (int x = g * (GW / 32); x < (g + 1) * (GW / 32); ++x)
-                for (uint32_t b = vm[x]; b; b &= b - 1) {
-                    const int ch = 32 * x + __ffs(b) - 1;
-                    const uint32_t xh = __half_as_ushort(V[ch]);
-                    const int code = okey(xh) >= khi ? ti[TI_CHI] : ti[TI_CLO];
-                    if (slot < c.vcap_g)
-                        c.vit[(tile * NG + g) * (int64_t)c.vcap_g + slot] =
-                            (xh << 16) | ((uint32_t)jj << 11) | item_code_flag<BITS>(code) | (uint32_t)(ch - g * GW);
-                    ++slot;
-                }
-            // new counts (>= cap: the attend kernels use the CSC / CSR arrays for the tile)
-            int kc = 0;
+            for (int x2 = g * wpg; x2 < x; ++x2) slot += __popc(vm[x2]);
+            for (uint32_t b = vm[x]; b; b &= b - 1) {
+                const int ch = 32 * x + __ffs(b) - 1;
+                const uint32_t xh = __half_as_ushort(V[ch]);
+                const int code = okey(xh) >= khi ? ti[TI_CHI] : ti[TI_CLO];
+                if (slot < c.vcap_g)
+                    c.vit[(tile * NG + g) * (int64_t)c.vcap_g + slot] =
+                        (xh << 16) | ((uint32_t)jj << 11) | item_code_flag<BITS>(code) | (uint32_t)(ch - g * GW);
+                ++slot;
+            }
+        }
+        // new counts (>= cap: the attend kernels use the CSC / CSR arrays for the tile)
+        for (int g = lane; g < NG; g += 32) {
+            int kc = 0, vc = 0;
             for (int h2 = (g * GW) / kHeadDim; h2 < ((g + 1) * GW) / kHeadDim; ++h2) kc += kcnt[h2];
+            for (int x2 = g * wpg; x2 < (g + 1) * wpg; ++x2) vc += __popc(vm[x2]);
             c.gcnt[(tile * NG + g) * 2] = (uint32_t)(gslotK[g] + kc);
-            c.gcnt[(tile * NG + g) * 2 + 1] = (uint32_t)slot;
+            c.gcnt[(tile * NG + g) * 2 + 1] = (uint32_t)(gslotV[g] + vc);
         }
     }
-    // ------------------------------------------------ Value codes (every thread)
-    // channels cc and cc + 8 of a head share a lane of the fragment layout and sit 2b bits
-    // apart: one OR per two codes (the words are shared with the tile's other tokens)
+    if (lane == 0) stamp(6);
+    // 4c: Value codes (every thread).  Channels cc and cc + 8 of a head share a lane of the
+    // fragment layout and sit 2b bits apart: one OR per two codes (the words are shared with the
+    // tile's other tokens)
     {
         const __half lo = __ushort_as_half(ti[TI_LO]), hi = __ushort_as_half(ti[TI_HI]);
         __half T[NM];
@@ -907,17 +1124,19 @@ __global__ void __launch_bounds__(AT, 1) append_kernel(DevCache c, const __half 
             if (off + 3 * BITS > 32) atomicOr(dst + 32, v >> (32 - off));
         }
     }
+    if (lane == 0) stamp(7);
 }
 
 }  // namespace
 
 size_t prefill_smem_bytes(int D, int NG) { return PSmem(D, NG).total; }
 
-cudaError_t launch_append(const DevCache &c, const __half *K, const __half *V, int64_t n, cudaStream_t s) {
+cudaError_t launch_append(const DevCache &c, const __half *K, const __half *V, int64_t n, cudaStream_t s,
+                          unsigned long long *tr) {
     switch (c.bits) {
-        case 2: append_kernel<2><<<1, AT, 0, s>>>(c, K, V, n); break;
-        case 3: append_kernel<3><<<1, AT, 0, s>>>(c, K, V, n); break;
-        case 4: append_kernel<4><<<1, AT, 0, s>>>(c, K, V, n); break;
+        case 2: append_kernel<2><<<1, AT, 0, s>>>(c, K, V, n, tr); break;
+        case 3: append_kernel<3><<<1, AT, 0, s>>>(c, K, V, n, tr); break;
+        case 4: append_kernel<4><<<1, AT, 0, s>>>(c, K, V, n, tr); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
