@@ -427,7 +427,8 @@ static kvq_status append_tokens(kvq_cache *c, const void *K, const void *V, int6
         if ((const void *)Vd != (const void *)(sb + bytes)) { CK(cudaMemcpyAsync(sb + bytes, Vd, bytes, cudaMemcpyDeviceToDevice, s)); Vd = (const __half *)(sb + bytes); }
     }
     cudaError_t e = T == 1 ? launch_append(c->dc, Kd, Vd, c->T, s, c->timers ? c->timers + 16 : nullptr)
-                           : launch_prefill(c->dc, Kd, Vd, c->T, T, c->dc.lb, c->dc.ticket, s);
+                           : launch_prefill(c->dc, Kd, Vd, c->T, T, c->dc.lb, c->dc.ticket, s,
+                                            c->timers ? c->timers + 16 + 64 : nullptr);
     if (e != cudaSuccess) return cuda_fail(e, "quantize launch");
     c->T += T;
     c->pdl_ok = T == 1;

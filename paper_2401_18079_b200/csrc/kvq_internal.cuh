@@ -98,7 +98,8 @@ __host__ __device__ inline int64_t vf_word(int64_t tile, int H_kv, int h, int w,
 // ---- block prefill (kvq_prefill.cu): one CTA per 32-token tile ----
 size_t prefill_smem_bytes(int D, int NG);
 cudaError_t launch_prefill(const DevCache &c, const __half *K, const __half *V, int64_t n0, int64_t T,
-                           unsigned long long *lb, unsigned *ticket, cudaStream_t s);
+                           unsigned long long *lb, unsigned *ticket, cudaStream_t s,
+                           unsigned long long *tm = nullptr);   // tm: diagnostics (phase clocks) or null
 cudaError_t launch_append(const DevCache &c, const __half *K, const __half *V, int64_t n, cudaStream_t s,
                           unsigned long long *trace = nullptr);   // trace: diagnostics (phase clocks) or null
 inline int kenc_words_per_pair(int bits) { return ((4 + (1 << bits) - 1) + 3) & ~3; }

@@ -79,6 +79,7 @@ struct PParams {
     int ntile;
     unsigned long long *lb;    // [ntile] look-back words (zeroed before the launch)
     unsigned *ticket;          // zeroed before the launch
+    unsigned long long *tm;    // diagnostics: per-phase clock sums [6] (tid 0 of every CTA), or null
 };
 
 // Dynamic shared memory layout (bytes), D channels, DW = D/32 mask words per token
@@ -304,6 +305,7 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
         // live on the stack)
         __half2 mx0 = __float2half2_rn(-65504.f), mx1 = mx0, mn0 = __float2half2_rn(65504.f), mn1 = mn0;
         bool have0 = false, have1 = false;
+#pragma unroll 4
         for (int m = 0; m < nch; m += 2) {
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -340,11 +342,22 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
         __syncwarp();
         const __half2 th2 = u2h(key2h(tau_hi) * 0x10001u), tl2 = u2h(key2h(tau_lo) * 0x10001u);
         bool ovf = false;
-        for (int m = 0; m < nch; ++m) {
+        // (chunks in batches of 4: their loads are in flight together)
+        for (int m0 = 0; m0 < nch; m0 += 4) {
+          uint4 ub[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c0 = 256 * (m0 + q) + 8 * lane;
+            ub[q] = (m0 + q < nch && c0 < D) ? *reinterpret_cast<const uint4 *>(row + c0) : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int m = m0 + q;
+            if (m >= nch) break;
             const int c0 = 256 * m + 8 * lane;
+            const uint4 u = ub[q];
             uint32_t fu = 0, fl = 0;
             if (c0 < D) {
-                const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
                 const uint32_t w[4] = {u.x, u.y, u.z, u.w};
                 // the chunk's max / min first: per-element flags only where a candidate is
                 const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
@@ -364,7 +377,6 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
                 if (nu) bu = atomicAdd(&nc2[0], nu);
                 if (nl) bl = atomicAdd(&nc2[1], nl);
                 if (fu | fl) {
-                    const uint4 u = *reinterpret_cast<const uint4 *>(row + c0);
                     for (uint32_t x = fu; x; x &= x - 1) {
                         const int e = __ffs(x) - 1;
                         const uint32_t key = okey(half_at(u, e));
@@ -379,6 +391,7 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
                     }
                 }
             }
+          }
         }
         __syncwarp();
         vstamp(10);
@@ -438,10 +451,21 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
     __shared__ uint32_t s_tokbase[33], s_tile, s_kbase, s_gbase[64][2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned char *wsc = sm + L.warp + (size_t)warp * 64 * 20 * 4;
+    long long t_prev = clock64();
+    int phase = 0;
+    auto pmark = [&]() {   // diagnostics: CTA time per phase (sync to sync)
+        if (P.tm && tid == 0) {
+            const long long t = clock64();
+            atomicAdd(P.tm + phase, (unsigned long long)(t - t_prev));
+            t_prev = t;
+        }
+        ++phase;
+    };
 
     if (tid == 0) s_tile = atomicAdd(P.ticket, 1u);
     for (int x = tid; x < 32 * DW; x += PT) { kmask[x] = 0; vmask[x] = 0; }
     __syncthreads();
+    pmark();
     const int li = (int)s_tile;                       // logical tile of this CTA
     const int64_t tile = P.tile0 + li;
     const int64_t nt0 = tile * 32;                    // token of lane 0
@@ -472,6 +496,7 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
     }
 
     __syncthreads();   // per-token ENC thresholds of phase A
+    pmark();
     // ================================================ C: Value codes (warp/KV head, mma lanes)
     {
         // staging: the head's V slice for 64 channels, transposed [channel][token] fp16,
@@ -604,6 +629,7 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
         }
     }
     __syncthreads();
+    pmark();
 
     // ================================ D1: Key-outlier totals, look-back aggregate, counts
     uint32_t lb_tot = 0, lb_agg = 0;   // warp 0: this lane's token total, the tile aggregate
@@ -638,6 +664,7 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
         }
     }
     __syncthreads();
+    pmark();
 
     // ============================ D1b: look-back resolution (warp 0), bucket slots (others)
     if (warp == 0) {
@@ -693,6 +720,7 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
         }
     }
     __syncthreads();
+    pmark();
 
     // ================================ D2: Key CSC records + Key / Value items (warp/token)
     {
@@ -721,16 +749,19 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
                     for (int w = 0; w < 4; ++w)
                         for (uint32_t b = kmask[j * DW + h * 4 + w]; b; b &= b - 1) {
                             const int cc = 32 * w + __ffs(b) - 1, ch = h * kHeadDim + cc;
+                            // the value and the pair's (lo, code(lo), code(hi)) table words: four
+                            // independent loads in flight together
+                            const int pp = cc & 63, up = cc >> 6;
+                            const uint32_t *te = kenc32 + (size_t)(h * kPairs + pp) * PS;
                             const uint32_t xh = __half_as_ushort(kr[ch]);
+                            const uint32_t t0 = __ldg(te), t2 = __ldg(te + 2), t3 = __ldg(te + 3);
                             if ((int64_t)pos < c.kcap) c.kout[pos] = (uint32_t)ch | (xh << 16);
                             ++pos;
                             // dense code at the outlier: clamp to lo -> code_lo, to hi -> code_hi
-                            const int pp = cc & 63, up = cc >> 6;
-                            const uint32_t *te = kenc32 + (size_t)(h * kPairs + pp) * PS;
-                            const __half2 lo2 = u2h(te[0]);
+                            const __half2 lo2 = u2h(t0);
                             const __half xv = __ushort_as_half((uint16_t)xh);
                             const bool below = __hlt(xv, up ? __high2half(lo2) : __low2half(lo2));
-                            const uint32_t cw = h2u(__hadd2(u2h(te[below ? 2 : 3]), __float2half2_rn(1024.f)));
+                            const uint32_t cw = h2u(__hadd2(u2h(below ? t2 : t3), __float2half2_rn(1024.f)));
                             const int code = (int)((up ? cw >> 16 : cw) & 0xfu);
                             if (bslot < (uint32_t)c.kcap_g)
                                 dst[bslot] = (xh << 16) | ((uint32_t)j << 11) | item_code_flag<BITS>(code) |
@@ -740,26 +771,32 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
                 }
                 tb += (uint32_t)hsum;
             }
-            // Value items of the token, per group in channel order
+            // Value items of the token, per group in channel order: a lane per mask word (its
+            // slot = the group's base + the outliers of the group's earlier words)
             const uint16_t *ti = tinfo + j * 24;
             const uint32_t khi = okey(ti[TI_HI]);
-            for (int g = lane; g < NG; g += 32) {
+            const int wpg = GW / 32;
+            for (int x = lane; x < DW; x += 32) {
+                const uint32_t bits = vmask[j * DW + x];
+                if (!bits) continue;
+                const int g = x / wpg;
                 uint32_t bslot = s_gbase[g][1] + posV[j * NG + g];
+                for (int x2 = g * wpg; x2 < x; ++x2) bslot += __popc(vmask[j * DW + x2]);
                 uint32_t *dst = c.vit + (tile * NG + g) * (int64_t)c.vcap_g;
-                for (int x = g * (GW / 32); x < (g + 1) * (GW / 32); ++x)
-                    for (uint32_t b = vmask[j * DW + x]; b; b &= b - 1) {
-                        const int ch = 32 * x + __ffs(b) - 1;
-                        const uint32_t xh = __half_as_ushort(vr[ch]);
-                        const int code = okey(xh) >= khi ? ti[TI_CHI] : ti[TI_CLO];
-                        if (bslot < (uint32_t)c.vcap_g)
-                            dst[bslot] = (xh << 16) | ((uint32_t)j << 11) | item_code_flag<BITS>(code) |
-                                         (uint32_t)(ch - g * GW);
-                        ++bslot;
-                    }
+                for (uint32_t b = bits; b; b &= b - 1) {
+                    const int ch = 32 * x + __ffs(b) - 1;
+                    const uint32_t xh = __half_as_ushort(vr[ch]);
+                    const int code = okey(xh) >= khi ? ti[TI_CHI] : ti[TI_CLO];
+                    if (bslot < (uint32_t)c.vcap_g)
+                        dst[bslot] = (xh << 16) | ((uint32_t)j << 11) | item_code_flag<BITS>(code) |
+                                     (uint32_t)(ch - g * GW);
+                    ++bslot;
+                }
             }
         }
     }
 
+    if (P.tm) { __syncthreads(); pmark(); }
 }
 
 
@@ -1143,14 +1180,14 @@ cudaError_t launch_append(const DevCache &c, const __half *K, const __half *V, i
 }
 
 cudaError_t launch_prefill(const DevCache &c, const __half *K, const __half *V, int64_t n0, int64_t T,
-                           unsigned long long *lb, unsigned *ticket, cudaStream_t s) {
+                           unsigned long long *lb, unsigned *ticket, cudaStream_t s, unsigned long long *tm) {
     if (T <= 0) return cudaSuccess;
     PParams P;
     P.K = K; P.V = V; P.n0 = n0; P.T = T;
     P.tile0 = n0 / 32;
     const int64_t tile1 = (n0 + T - 1) / 32;
     P.ntile = (int)(tile1 - P.tile0 + 1);
-    P.lb = lb; P.ticket = ticket;
+    P.lb = lb; P.ticket = ticket; P.tm = tm;
     cudaError_t e = cudaMemsetAsync(lb, 0, (size_t)P.ntile * 8, s);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(ticket, 0, 4, s);

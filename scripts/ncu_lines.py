@@ -48,3 +48,6 @@ for l in sorted(lines, key=lambda x: -x[1])[:40]:
 print("top lines by shared wavefronts:")
 for l in sorted(lines, key=lambda x: -x[4])[:20]:
     print(f"{l[0]:5d} wf {l[4] / units:5.0f}/u (ideal {l[5] / units:4.0f})  {l[3]}")
+print("top lines by stall samples:")
+for l in sorted(lines, key=lambda x: -x[2])[:25]:
+    print(f"{l[0]:5d} stall {100 * l[2] / max(ts, 1):5.1f}%  inst {l[1] / units:6.0f}/u  {l[3]}")
