@@ -13,6 +13,8 @@ SOURCES = ["kvq_api.cu", "kvq_prefill.cu", "kvq_f16.cu", "kvq_calib.cu", "kvq_at
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"]
+# diagnostics builds only (e.g. -DKVQ_TS_DEBUG: phase timestamps of the attend kernel)
+FLAGS += os.environ.get("KVQ_EXTRA_NVCC_FLAGS", "").split()
 
 
 def stale() -> bool:

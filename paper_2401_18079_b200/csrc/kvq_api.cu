@@ -253,6 +253,11 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
         A(&d.lb, (size_t)(d.cap / 32 + 2) * 8);
         A(&d.ticket, 64);
     }
+    {
+        double *tt = nullptr;
+        A(&tt, 64 * 8);
+        d.theta_tab = tt;
+    }
     c->max_splits = 4 * 148;
     A(&c->parts, (size_t)c->max_splits * d.H_q * (kHeadDim + 2) * 4);
     A(&c->tickets, 64 * 4);
@@ -319,6 +324,11 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     if (e == cudaSuccess) e = cudaMemcpy(d.kenc, kenc.data(), kenc.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d.cb, cb, sizeof cb, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d.mids, mids, sizeof mids, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        double th[64];
+        for (int i = 0; i < 64; ++i) th[i] = std::pow(C.rope_theta, -2.0 * (double)i / (double)kHeadDim);
+        e = cudaMemcpy(const_cast<double *>(d.theta_tab), th, sizeof th, cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { kvq_cache_destroy(c); return cuda_fail(e, "upload parameters"); }
     *out = c;

@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     // ---------------------------------------------------------------- prologue
     if (tid < 64) {
         const int i = tid;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        const double th = c.theta_tab[i];
         theta32[i] = (float)th;
         double s, co;
         sincos((double)P.pos * th, &s, &co);
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) att_kernel(DevCache c, Params 
     }
     for (int x = tid; x < kPairs * 32; x += ATT_THREADS) {
         const int i = x >> 5, j = x & 31;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        const double th = c.theta_tab[i];
         double s, co;
         sincos((double)j * th, &s, &co);
         t1tab[x] = make_float2((float)co, (float)s);

@@ -183,10 +183,10 @@ __device__ __forceinline__ void att_wa_body(const DevCache &c, const WParams &P,
     // R11, R12)
     if (tid < 64) {
         const int i = tid;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        const double th = c.theta_tab[i];
         th64[i] = th;
         double s, co;
-        sincos((double)P.pos * th, &s, &co);
+        sincos(red2pi((double)P.pos * th), &s, &co);   // reduced first: fast-path sincos
         qcis[i] = make_double2(co, s);
     }
     __syncthreads();
@@ -281,30 +281,32 @@ __device__ __forceinline__ void att_wa_body(const DevCache &c, const WParams &P,
             }
         }
     } else
-    // K table entries [g][i][pair code], one (head, pair, second code) row per work item
+    // K table entries [g][i][pair code], one (head, pair, second code) row per work item,
+    // written as 16-byte vectors (the 2^b entries of a row are contiguous)
     for (int x = tid; x < HG * 64 * (CM + 1); x += NTHR) {
         const int bb = x % (CM + 1), gi = x / (CM + 1);
         const int g = gi >> 6, i = gi & 63;
         const int ci = g * kHeadDim + i, cj = ci + 64;
+        const float *cbKsh = cb_s + 16;
         const float sc = lut_sc[g];
         const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
         const float qa = qa1 * sc, qb = qb1 * sc;
-        const float yb = cbK[bb] * ks_s[cj] + kz_s[cj];
-        uint32_t *dst = klut + (size_t)(g * 64 + i) * NE + (bb << BITS);
+        const float ksi = ks_s[ci], kzi = kz_s[ci];
+        const float yb = cbKsh[bb] * ks_s[cj] + kz_s[cj];
         const bool heavy = heavy_s[gi] != 0;
         int hslot = 0;
         if (heavy)
             for (int u = 0; u < hv_n[g]; ++u) hslot = hv_pair[g * 8 + u] == i ? u : hslot;
+        uint32_t e[CM + 1];
 #pragma unroll
         for (int a = 0; a <= CM; ++a) {
-            const float xa = cbK[a] * ks_s[ci] + kz_s[ci];
-            if (heavy) {
-                dst[a] = 0u;
-                hlut[(g * HMAX + hslot) * NE + (bb << BITS) + a] = make_float2(qa1 * xa + qb1 * yb, qb1 * xa - qa1 * yb);
-            } else {
-                dst[a] = pack_half2(qa * xa + qb * yb, qb * xa - qa * yb);
-            }
+            const float xa = cbKsh[a] * ksi + kzi;
+            e[a] = heavy ? 0u : pack_half2(qa * xa + qb * yb, qb * xa - qa * yb);
+            if (heavy) hlut[(g * HMAX + hslot) * NE + (bb << BITS) + a] = make_float2(qa1 * xa + qb1 * yb, qb1 * xa - qa1 * yb);
         }
+        uint4 *dst = reinterpret_cast<uint4 *>(klut + (size_t)(g * 64 + i) * NE + (bb << BITS));
+#pragma unroll
+        for (int v = 0; v < (CM + 1) / 4; ++v) dst[v] = make_uint4(e[4 * v], e[4 * v + 1], e[4 * v + 2], e[4 * v + 3]);
     }
     // V table: lane-private copies (entry e of lane l at word e*32 + l): the fp16 codebook
     // pair and (RESID) its fp16 residual Chat - fp16(Chat) (R23)
@@ -993,10 +995,10 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
     // query, cis((pos_base + 32 t_begin) theta_i) for the CTA's first tile (R11, R12)
     if (tid < 64) {
         const int i = tid;
-        const double th = pow(c.theta, -2.0 * (double)i / (double)kHeadDim);
+        const double th = c.theta_tab[i];
         th64[i] = th;
         double s, co;
-        sincos((double)P.pos * th, &s, &co);
+        sincos(red2pi((double)P.pos * th), &s, &co);   // reduced first: fast-path sincos
         qcis[i] = make_double2(co, s);
     }
     __syncthreads();
@@ -1065,29 +1067,29 @@ __global__ void __launch_bounds__(GCfg<BITS, RESID, G>::NTHR, 1) att_wag_kernel(
         }
     }
     __syncthreads();
-    // K table entries [i][pair code][g]: the G heads of a code adjacent (one vector load)
-    for (int x = tid; x < G * 64 * (CM + 1); x += NTHR) {
-        const int bb = x % (CM + 1), gi = x / (CM + 1);
-        const int g = gi >> 6, i = gi & 63;
-        const int ci = i, cj = i + 64;
-        const float sc = lut_sc[g];
-        const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
-        const float qa = qa1 * sc, qb = qb1 * sc;
-        const float yb = cbK[bb] * ks_s[cj] + kz_s[cj];
-        uint32_t *dst = klut + ((size_t)i * NE + (bb << BITS)) * G + g;
-        const bool heavy = heavy_s[gi] != 0;
-        int hslot = 0;
-        if (heavy)
-            for (int u = 0; u < hv_n[g]; ++u) hslot = hv_pair[g * 8 + u] == i ? u : hslot;
-#pragma unroll
-        for (int a = 0; a <= CM; ++a) {
-            const float xa = cbK[a] * ks_s[ci] + kz_s[ci];
-            if (heavy) {
-                dst[a * G] = 0u;
-                hlut[(g * HMAX + hslot) * NE + (bb << BITS) + a] = make_float2(qa1 * xa + qb1 * yb, qb1 * xa - qa1 * yb);
+    // K table entries [i][pair code][g]: the G heads of a code adjacent (one vector load);
+    // one entry per work item, consecutive threads on consecutive words (conflict-free stores)
+    {
+        const float *cbKsh = cb_s + 16;
+        for (int x = tid; x < G * 64 * NE; x += NTHR) {
+            const int g = x % G, rest = x / G;
+            const int code = rest % NE, i = rest / NE;
+            const int a = code & CM, bb = code >> BITS;
+            const int gi = g * 64 + i;
+            const float qa1 = qs[g * kHeadDim + i], qb1 = qs[g * kHeadDim + i + 64];
+            const float xa = cbKsh[a] * ks_s[i] + kz_s[i];
+            const float yb = cbKsh[bb] * ks_s[i + 64] + kz_s[i + 64];
+            const float A = qa1 * xa + qb1 * yb, B = qb1 * xa - qa1 * yb;
+            uint32_t e = 0u;
+            if (heavy_s[gi] != 0) {
+                int hslot = 0;
+                for (int u = 0; u < hv_n[g]; ++u) hslot = hv_pair[g * 8 + u] == i ? u : hslot;
+                hlut[(g * HMAX + hslot) * NE + code] = make_float2(A, B);
             } else {
-                dst[a * G] = pack_half2(qa * xa + qb * yb, qb * xa - qa * yb);
+                const float sc = lut_sc[g];
+                e = pack_half2(A * sc, B * sc);
             }
+            klut[x] = e;
         }
     }
     for (int x = tid; x < NE * 32; x += NTHR) {

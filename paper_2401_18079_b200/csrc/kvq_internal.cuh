@@ -42,6 +42,7 @@ struct DevCache {
     int VW;                                // Value words per token (= D*b/32)
     int64_t cap, kcap, pos_base;
     double theta;
+    const double *theta_tab;   // [64] theta_i = base^(-2i/d) in fp64, host-computed at create
     uint32_t *kcodes, *vcodes, *vout, *kptr, *kout;
     float2 *vsz;
     float *kpar;    // [4][D]
