@@ -41,7 +41,7 @@ struct WCfg {
     static constexpr int IPL = 4;                         // bucket items per lane in registers
     static constexpr int NE = 1 << (2 * BITS);
     static constexpr int KWH = 4 * BITS;                  // code words per head per token
-    static constexpr int HMAX = 8;                        // fp32 "heavy" pairs per head
+    static constexpr int HMAX = 4;                        // fp32 "heavy" pairs per head (R24: 4 keep the error of 8)
     // K table entries per (head, RoPE pair): 2-3 bits, one entry per pair code (the query and
     // both channels folded in); 4 bits, per channel (16 + 16 entries, their two lookups summed
     // by the FMAs), since a 256-entry pair table per pair would need 64 KB per head
