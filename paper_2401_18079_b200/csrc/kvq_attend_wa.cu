@@ -1571,6 +1571,726 @@ cudaError_t launch_wag_g(const DevCache &c, const WParams &P, int grid, cudaStre
     return c.G == 2 ? launch_wag_t<BITS, RESID, 2>(c, P, grid, s) : launch_wag_t<BITS, RESID, 4>(c, P, grid, s);
 }
 
+
+// ===================================================================================
+// GQA with the K scores on the tensor cores: att_wgt_kernel.  Same structure as att_wag_kernel
+// (one CTA per (KV head, split), 16 warps = 16 tile streams, every outlier item corrects the G
+// heads, P.V on mma with persistent accumulators), but the K scores are a dense contraction
+// here, so they run on mma.m16n8k16: A = RoPE(K^) of 16 tokens x 8 pairs, dequantized and
+// rotated in fp32 and split into fp16 hi + lo (two mma), B = the G queries as fp16 hi / lo
+// columns.  The products are exact and the sums fp32, so the scores are fp32-accurate and there
+// is no heavy-pair pass; the Key codebook lookups are lane-private (conflict-free), the K-word
+// reads swizzled (4 blocks -> 4 bank octets).
+template <int WB>
+__device__ __forceinline__ int kst_swz(int q, int j) {
+    return q * 32 + (j ^ (8 * ((q / WB) & 3)));
+}
+// padded per-pair tables: the 4 lanes of a column read pairs 16 t + x (t = 0..3), which would
+// share banks at a 16-entry stride
+__device__ __forceinline__ int kpad(int p) { return p + (p >> 4); }        // 16-byte entries
+__device__ __forceinline__ int apad(int p) { return p + 2 * (p >> 4); }    // 8-byte entries
+
+template <int BITS, bool RESID, int G>
+struct TCfg {
+    static_assert(G <= 4, "hi/lo query columns: 2 G <= 8 mma columns");
+    static constexpr int NWARP = NSG;
+    static constexpr int NTHR = NWARP * 32;
+    static constexpr int IPL = 4;
+    static constexpr int NE = 1 << (2 * BITS);
+    static constexpr int KWH = 4 * BITS;
+    static constexpr size_t cpt = (size_t)NE * 32 * 8;    // lane-private (cb[a], cb[b]) fp32
+    static constexpr size_t calign = cpt;
+    static constexpr size_t vlut = (size_t)(RESID ? 2 : 1) * NE * 32 * 4;
+    static_assert(cpt % ((size_t)NE * 32 * 4) == 0, "V table follows aligned");
+    // per warp: K words (cp.async target, swizzled), K-outlier terms (then p) [G][32], V-outlier
+    // sums fp32 [G][128] and fixed point [G][128], anchors, scores [G][32]
+    static constexpr size_t w_kst = (size_t)KWH * 32 * 4;
+    static constexpr size_t w_bytes = w_kst + G * 32 * 4 + G * kHeadDim * 4 * 2 + 72 * 8 + G * 32 * 4;
+    static constexpr int KCH = KWH / 4;
+    static constexpr size_t small = 68 * 16 /* kaf */ + 8 * 32 * 8 /* bqs */ + G * kHeadDim * 4 /* qs */ + kHeadDim * 4 * 2 /* ks, kz */
+        + 64 * 4 /* cb */ + 64 /* flags */ + 64 * 16 /* cis(pos theta) */ + 64 * 8 /* theta */;
+    static constexpr size_t total = calign + cpt + vlut + NWARP * w_bytes + small;
+};
+
+template <int BITS, bool RESID, int G>
+__global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(DevCache c, WParams P) {
+    using C = TCfg<BITS, RESID, G>;
+    constexpr int NWARP = C::NWARP, NTHR = C::NTHR, IPL = C::IPL;
+    constexpr int NE = C::NE;
+    constexpr int CM = (1 << BITS) - 1;
+    constexpr int KWH = C::KWH;
+    constexpr int FB = 2 * BITS;
+    constexpr int WB = FB / 2;   // K words per 16-pair block
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // the lane-private codebook pair table first, at a multiple of its size (OR addressing),
+    // then the V table (also aligned), then the per-warp regions and the small arrays
+    const uint32_t s0 = smem_u32(smem_raw);
+    unsigned char *sp = smem_raw + ((C::calign - (s0 % C::calign)) % C::calign);
+    float2 *cpt = reinterpret_cast<float2 *>(sp); sp += C::cpt;
+    uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
+    unsigned char *wbase = sp; sp += NWARP * C::w_bytes;
+    float4 *kaf = reinterpret_cast<float4 *>(sp); sp += 68 * 16;   // pair p at p + (p >> 4)
+    uint2 *bqs = reinterpret_cast<uint2 *>(sp); sp += 8 * 32 * 8;   // score-mma B fragments [s][lane]
+    float *qs = reinterpret_cast<float *>(sp); sp += G * kHeadDim * 4;
+    float *ks_s = reinterpret_cast<float *>(sp); sp += kHeadDim * 4;
+    float *kz_s = reinterpret_cast<float *>(sp); sp += kHeadDim * 4;
+    float *cb_s = reinterpret_cast<float *>(sp); sp += 64 * 4;
+    int *flag_s = reinterpret_cast<int *>(sp); sp += 64;
+    double2 *qcis = reinterpret_cast<double2 *>(sp); sp += 64 * 16;
+    double *th64 = reinterpret_cast<double *>(sp); sp += 64 * 8;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_hg = c.H_kv;   // one CTA per KV head
+    const int hk = blockIdx.x % n_hg;
+    const int split = blockIdx.x / n_hg;
+    const int g0 = hk * G;     // first query head
+    const int c_lo = hk * kHeadDim;
+    const int t_begin = (int)((int64_t)split * P.ntiles / P.S);
+    const int t_end = (int)((int64_t)(split + 1) * P.ntiles / P.S);
+    const int D = c.D;
+    const float *cbK = c.cb + 16, *cbV = c.cb + 48;
+
+    unsigned char *wp = wbase + warp * C::w_bytes;
+    uint32_t *kst = reinterpret_cast<uint32_t *>(wp); wp += C::w_kst;
+    int *kfix = reinterpret_cast<int *>(wp); wp += G * 32 * 4;
+    float *ps = reinterpret_cast<float *>(kfix);
+    float *osp = reinterpret_cast<float *>(wp); wp += G * kHeadDim * 4;
+    // Value-outlier sums of the tile in fixed point (native shared integer atomics; sm_100a
+    // has no native shared fp32 add), folded into osp at the end of the tile; during the K
+    // phase the same words hold the fp32 side sums of the Key-outlier terms too large for
+    // the 32-bit fixed point (kfix_add32)
+    int *vfix = reinterpret_cast<int *>(wp); wp += G * kHeadDim * 4;
+    float *kbig = reinterpret_cast<float *>(vfix);
+    float2 *anc32 = reinterpret_cast<float2 *>(wp); wp += 72 * 8;   // pair p at p + 2 (p >> 4)
+    float *sct = reinterpret_cast<float *>(wp);   // [G][32] scores of the tile (tensor cores)
+
+    const int t_first = t_begin + warp;
+    uint32_t kitm[IPL], vitm[IPL];
+    uint32_t cnt_k = 0, cnt_v = 0, ncnt_k = 0, ncnt_v = 0;
+    float2 vsz = make_float2(0.f, 0.f);
+    auto issue_k = [&](int t) {
+        const unsigned char *src = reinterpret_cast<const unsigned char *>(c.kcodes + ((int64_t)t * c.QW + hk * KWH) * 32);
+        const uint32_t dst = smem_u32(kst);
+#pragma unroll
+        for (int k = 0; k < C::KCH; ++k) {
+            const int x = lane + 32 * k;   // 16-byte chunk: word x / 8, tokens 4 (x % 8) ..
+            cp_async16(dst + (uint32_t)kst_swz<WB>(x >> 3, (x & 7) * 4) * 4u, src + x * 16);
+        }
+    };
+    auto load_counts = [&](int t, uint32_t &nk, uint32_t &nv) {
+        nk = nv = 0;
+        if (t < t_end) {
+            const uint32_t *gc = c.gcnt + ((int64_t)t * c.NG + hk) * 2;
+            nk = __ldg(gc);
+            nv = __ldg(gc + 1);
+        }
+    };
+    auto load_items = [&](int t) {
+        const int64_t bucket = (int64_t)t * c.NG + hk;
+        const uint32_t nk = cnt_k > (uint32_t)c.kcap_g ? 0u : cnt_k;
+        const uint32_t nv = cnt_v > (uint32_t)c.vcap_g ? 0u : cnt_v;
+#pragma unroll
+        for (int k = 0; k < IPL; ++k) {
+            const uint32_t x = lane + 32 * k;
+            kitm[k] = x < nk ? __ldg(c.kit + bucket * c.kcap_g + x) : 0u;
+            vitm[k] = x < nv ? __ldg(c.vit + bucket * c.vcap_g + x) : 0u;
+        }
+        vsz = (int64_t)t * 32 + lane < P.T ? __ldg(c.vsz + (int64_t)t * 32 + lane) : make_float2(0.f, 0.f);
+    };
+
+    // the first tile's K words and counts overlap the prologue unless the tile is the tail tile
+    // (which a concurrent append may still be writing, see pdl_wait)
+    const bool early = t_first < t_end && t_first != P.ntiles - 1;
+    if (early) {
+        issue_k(t_first);
+        load_counts(t_first, cnt_k, cnt_v);
+    }
+
+    // ---------------------------------------------------------------- prologue (a1)
+    // theta_i and the large-argument angles once per CTA (64 threads): cis(pos theta_i) for the
+    // query, cis((pos_base + 32 t_begin) theta_i) for the CTA's first tile (R11, R12)
+    if (tid < 64) {
+        const int i = tid;
+        const double th = c.theta_tab[i];
+        th64[i] = th;
+        double s, co;
+        sincos(red2pi((double)P.pos * th), &s, &co);   // reduced first: fast-path sincos
+        qcis[i] = make_double2(co, s);
+    }
+    __syncthreads();
+    // token angles as in the MHA kernel: per warp and tile (anchor angle a_i mod 2 pi, th_i) fp32,
+    // token j's cis from the MUFU at a_i + (j - 16) th_i
+    double ang64[2], step64[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int i = lane + 32 * k;
+        const double th = th64[i];
+        ang64[k] = red2pi((double)(c.pos_base + (int64_t)t_first * kTileTokens + 16) * th);
+        step64[k] = red2pi((double)(C::NWARP * kTileTokens) * th);
+        anc32[apad(i)] = make_float2((float)ang64[k], (float)th);
+    }
+    for (int x = lane; x < G * 32; x += 32) kfix[x] = 0;
+    for (int x = lane; x < G * kHeadDim; x += 32) { osp[x] = 0.f; vfix[x] = 0; }
+    for (int x = tid; x < kHeadDim; x += NTHR) {
+        ks_s[x] = c.kpar[c_lo + x];
+        kz_s[x] = c.kpar[D + c_lo + x];
+    }
+    if (tid < 64) cb_s[tid] = c.cb[tid];
+    if (tid < 16) flag_s[tid] = 0;
+    const double qscale = 1.4426950408889634 / sqrt((double)kHeadDim);
+    for (int x = tid; x < G * 64; x += NTHR) {
+        const int g = x >> 6, i = x & 63;
+        const __half *qg = P.q + (int64_t)(g0 + g) * kHeadDim;
+        const double co = qcis[i].x, s = qcis[i].y;
+        const double a = (double)__half2float(qg[i]), b = (double)__half2float(qg[i + 64]);
+        qs[g * kHeadDim + i] = (float)((a * co - b * s) * qscale);
+        qs[g * kHeadDim + i + 64] = (float)((b * co + a * s) * qscale);
+    }
+    __syncthreads();
+    // Key dequantization tables: the lane-private pair table (cb[a], cb[b]) of every pair code
+    // (entry e of lane l at e * 32 + l: conflict-free), and per RoPE pair the two channels'
+    // (s, s', z, z') scaled by 2^-4 (A operand range)
+    for (int x = tid; x < NE * 32; x += NTHR) {
+        const int e = x >> 5;
+        cpt[x] = make_float2(cbK[e & CM], cbK[e >> BITS]);
+    }
+    if (tid < 64) {
+        const int i = tid;
+        kaf[kpad(i)] = make_float4(ks_s[i] * 0.0625f, ks_s[i + 64] * 0.0625f, kz_s[i] * 0.0625f, kz_s[i + 64] * 0.0625f);
+    }
+    for (int x = tid; x < NE * 32; x += NTHR) {
+        const int e = x >> 5;
+        const float ca = cbV[e & CM], cb = cbV[e >> BITS];
+        vlut[x] = pack_half2(ca, cb);
+        if constexpr (RESID)
+            vlut[NE * 32 + x] = pack_half2(ca - __half2float(__float2half_rn(ca)), cb - __half2float(__float2half_rn(cb)));
+    }
+    __syncthreads();
+
+    pdl_wait();
+    if (t_first < t_end && !early) {
+        issue_k(t_first);
+        load_counts(t_first, cnt_k, cnt_v);
+    }
+
+    // ================================================================ tile loop (per warp)
+    const uint32_t vlut_u = opaque(smem_u32(vlut) | (4u * lane));
+    const uint32_t cpt_u = opaque(smem_u32(cpt) | (8u * lane));
+    const int vg = lane >> 2, vt = lane & 3;
+    // B fragments of the score mma (constant): column vg = q~ of head vg (fp16 hi part) or of
+    // head vg - 4 (lo part); k = 2 slot + (0: channel p, 1: channel p + 64); lane (vg, vt)
+    // holds slot vt (pair 16 vt + 2 s) and slot vt + 4 (pair 16 vt + 2 s + 1) of k-step s
+    // (a CTA-wide table in shared memory, one 8-byte load per k-step; written by warp 0)
+    if (warp == 0) {
+        const int hq = vg < 4 ? vg : vg - 4;
+#pragma unroll 1
+        for (int s = 0; s < 8; ++s) {
+            uint32_t v[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int p = 16 * vt + 2 * s + j;
+                v[j] = 0u;
+                if (hq < G) {
+                    const float qa = qs[hq * kHeadDim + p], qb = qs[hq * kHeadDim + p + 64];
+                    const float ha = __half2float(__float2half_rn(qa)), hb = __half2float(__float2half_rn(qb));
+                    v[j] = vg < 4 ? pack_half2(ha, hb) : pack_half2(qa - ha, qb - hb);
+                }
+            }
+            bqs[s * 32 + lane] = make_uint2(v[0], v[1]);
+        }
+    }
+    __syncthreads();
+    const float *cbKs = cb_s + 16, *cbVs = cb_s + 48;
+    // P.V accumulators (mma D fragments): column 2vt + (0|1) = query head, rows vg, vg + 8 of
+    // m-tile ml; units 2^(E - WEXP) relative to the head's running max
+    float dacc[8][4];
+#pragma unroll
+    for (int ml = 0; ml < 8; ++ml) dacc[ml][0] = dacc[ml][1] = dacc[ml][2] = dacc[ml][3] = 0.f;
+    float m_run[G], l_lane[G], z_lane[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) { m_run[g] = -CUDART_INF_F; l_lane[g] = 0.f; z_lane[g] = 0.f; }
+    int E_run = -126;
+    // D columns 2t, 2t+1 of lane (g, t) are head t's hi and lo weight sums
+    const int hcl = min(vt, G - 1);
+    auto rot32 = [&](int i, int j, float &co, float &si) {
+        const float2 a = anc32[apad(i)];
+        __sincosf(fmaf((float)(j - 16), a.y, a.x), &si, &co);
+    };
+    auto rot16 = [&](int i) -> uint32_t {
+        float co, si;
+        rot32(i, lane, co, si);
+        return pack_half2(co, si);
+    };
+
+    for (int t = t_first; t < t_end; t += C::NWARP) {
+        const int64_t n0 = (int64_t)t * 32;
+        const int ntok = (int)min((int64_t)32, P.T - n0);
+        const bool valid = lane < ntok;
+        const bool kov = cnt_k > (uint32_t)c.kcap_g, vov = cnt_v > (uint32_t)c.vcap_g;
+        const int nk = kov ? 0 : (int)cnt_k, nv = vov ? 0 : (int)cnt_v;
+        load_items(t);
+        load_counts(t + C::NWARP, ncnt_k, ncnt_v);
+        {   // this tile's V words (4b * 128 B) -> L2; read after the K scores
+            const char *vb = reinterpret_cast<const char *>(c.vcodes + vf_word(t, c.H_kv, hk, 0, 0, BITS));
+            if (lane < 4 * BITS) asm volatile("prefetch.global.L2 [%0];" ::"l"(vb + lane * 128));
+        }
+
+        cp_async_wait_all();
+        __syncwarp();
+        // ---------------------------------------------------------- a2: K scores (tensor cores)
+        // A = RoPE(K^_n) of the tile (rows = tokens, k = the pairs' two channels), dequantized
+        // and rotated in fp32 and split into fp16 hi + lo (two mma), B = the G queries (hi / lo
+        // columns): fp32-exact scores, no heavy-pair pass.  Lane (g, t) converts tokens
+        // g + 8 m (m = 0..3) at the 16 pairs of block t.
+        float dsc[2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) dsc[mt][0] = dsc[mt][1] = dsc[mt][2] = dsc[mt][3] = 0.f;
+        {
+            uint32_t kwd[4][WB + 1];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+#pragma unroll
+                for (int k = 0; k < WB; ++k) kwd[m][k] = kst[kst_swz<WB>(vt * WB + k, vg + 8 * m)];
+                kwd[m][WB] = 0u;
+            }
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                const int off = 2 * s * FB, wi = off >> 5, sh = off & 31;
+                float4 af[2];
+                float2 an[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    af[j] = kaf[kpad(16 * vt + 2 * s + j)];
+                    an[j] = anc32[apad(16 * vt + 2 * s + j)];
+                }
+                uint32_t ahi[2][4], alo[2][4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const uint32_t f = (sh + 2 * FB <= 32) ? (kwd[m][wi] >> sh) : __funnelshift_r(kwd[m][wi], kwd[m][wi + 1], sh);
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const uint32_t ad = cpt_u | ((f << (8 - FB * j)) & ((uint32_t)(NE - 1) << 8));
+                        float2 x;
+                        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x.x), "=f"(x.y) : "r"(ad));
+                        const float ka = fmaf(x.x, af[j].x, af[j].z), kb = fmaf(x.y, af[j].y, af[j].w);
+                        float co, si;
+                        __sincosf(fmaf((float)(vg + 8 * m - 16), an[j].y, an[j].x), &si, &co);
+                        const float ra = ka * co - kb * si, rb = ka * si + kb * co;
+                        const uint32_t h = pack_half2(ra, rb);
+                        const __half2 h2 = *reinterpret_cast<const __half2 *>(&h);
+                        // rows g (m even) / g + 8 (m odd) of m-tile m / 2; slot j: registers 0-1 / 2-3
+                        ahi[m >> 1][2 * j + (m & 1)] = h;
+                        alo[m >> 1][2 * j + (m & 1)] = pack_half2(ra - __low2float(h2), rb - __high2float(h2));
+                    }
+                }
+                const uint2 bb = bqs[s * 32 + lane];
+                const uint32_t b[2] = {bb.x, bb.y};
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    mma_f16_f32(dsc[mt], ahi[mt], b);
+                    mma_f16_f32(dsc[mt], alo[mt], b);
+                }
+            }
+        }
+        // columns 2t, 2t+1 of lane (g, t): heads 2t, 2t+1 (hi part, t < 2) or their lo parts
+        // (t >= 2): hi + lo via one shuffle, then scores (x 2^4) to lane = token
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float v = dsc[mt][r] + __shfl_xor_sync(0xffffffffu, dsc[mt][r], 2);
+                const int h = 2 * vt + (r & 1);
+                if (vt < 2 && h < G) sct[h * 32 + 16 * mt + vg + 8 * (r >> 1)] = v * 16.f;
+            }
+        // V words of this tile (L2 hits), used after the softmax
+        uint32_t vw[KWH];
+#pragma unroll
+        for (int w = 0; w < KWH; ++w) vw[w] = __ldg(c.vcodes + vf_word(t, c.H_kv, hk, w, lane, BITS));
+        __syncwarp();
+        float sco[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) sco[g] = sct[g * 32 + lane];
+        // item -> the G heads' corrections (x - K^(code)) * dscore/dK
+        auto k_item = [&](uint32_t itm) {
+            const int j = (int)((itm >> 11) & 31u);
+            const int cc = (int)(itm & 0x7fu), flag = (int)((itm >> 9) & 3u);
+            const int i = cc & 63, up = cc >> 6;
+            int code = flag == 1 ? CM : 0;
+            if (flag == 0) {
+                const int bit = FB * i;
+                const int wq = bit >> 5;
+                unsigned long long w64 = kst[kst_swz<WB>(wq, j)];
+                if ((bit & 31) + FB > 32) w64 |= (unsigned long long)kst[kst_swz<WB>(wq + 1, j)] << 32;
+                const int pc = (int)((w64 >> (bit & 31)) & (NE - 1));
+                code = (pc >> (up * BITS)) & CM;
+            }
+            const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+            const float delta = xval - (cbKs[code] * ks_s[cc] + kz_s[cc]);
+            float co, si;
+            rot32(i, j, co, si);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float qa = qs[g * kHeadDim + i], qb = qs[g * kHeadDim + i + 64];
+                kfix_add32(&kfix[g * 32 + j], &kbig[g * 32 + j], delta * (up ? (qb * co - qa * si) : (qa * co + qb * si)));
+            }
+        };
+        {
+            const int64_t bucket = (int64_t)t * c.NG + hk;
+#pragma unroll
+            for (int k = 0; k < IPL; ++k)
+                if (32 * k < nk && lane + 32 * k < nk) k_item(kitm[k]);
+            for (int x = 32 * IPL + lane; x < nk; x += 32) k_item(__ldg(c.kit + bucket * c.kcap_g + x));
+            if (kov) {
+                for (int j = 0; j < ntok; ++j) {
+                    const uint32_t r0 = __ldg(c.kptr + n0 + j), r1 = __ldg(c.kptr + n0 + j + 1);
+                    for (uint32_t r = r0 + lane; r < r1; r += 32) {
+                        const uint32_t rec = __ldcg(c.kout + r);
+                        const int ch = (int)(rec & 0xffffu);
+                        if (ch < c_lo || ch >= c_lo + kHeadDim) continue;
+                        k_item((rec & 0xffff0000u) | ((uint32_t)j << 11) | (uint32_t)(ch - c_lo));
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        const int tn = t + C::NWARP;
+        if (tn < t_end) issue_k(tn);
+
+        // ------------------------------------------------------ a4: online softmax
+        // weights p s_n 2^(WEXP - E), E the running exponent bound of s_n (the accumulators
+        // persist across tiles)
+        const float smax = warp_max_redux(valid ? vsz.x : 0.f);
+        const int E_new = smax > 0.f ? max(E_run, ilog2f(smax) + 1) : E_run;
+        const float pe = pow2i(WEXP - E_new), rE = pow2i(E_run - E_new);
+        E_run = E_new;
+        uint32_t w2s[G], w2l[G];
+        float al[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float s = sco[g] + (float)kfix[g * 32 + lane] * (1.f / kKfixScale) + kbig[g * 32 + lane];
+            kbig[g * 32 + lane] = 0.f;   // the words are the V-outlier sums from here on
+            s = valid ? s : -CUDART_INF_F;
+            const float m_new = fmaxf(m_run[g], warp_max_redux(s));
+            const float alpha = (m_new == -CUDART_INF_F) ? 1.f : exp2f(m_run[g] - m_new);
+            const float p = valid ? exp2f(s - m_new) : 0.f;
+            l_lane[g] = l_lane[g] * alpha + p;
+            z_lane[g] = z_lane[g] * alpha + p * vsz.y;
+            m_run[g] = m_new;
+            al[g] = alpha;
+            if (alpha != 1.f) {   // warp-uniform
+#pragma unroll
+                for (int x = 0; x < kHeadDim / 32; ++x) osp[g * kHeadDim + x * 32 + lane] *= alpha;
+            }
+            ps[g * 32 + lane] = p;
+            const float wf = p * (vsz.x * pe);
+            const __half wh = __float2half_rn(wf);
+            const uint32_t hb = __half_as_ushort(wh), lb = __half_as_ushort(__float2half_rn(wf - __half2float(wh)));
+            w2s[g] = hb | (__shfl_down_sync(0xffffffffu, hb, 1) << 16);
+            w2l[g] = lb | (__shfl_down_sync(0xffffffffu, lb, 1) << 16);
+        }
+        {   // rescale the accumulators: per column (head) alpha, and the weight exponent
+            float a0 = al[0];
+#pragma unroll
+            for (int g = 1; g < G; ++g) a0 = hcl == g ? al[g] : a0;
+            a0 *= rE;
+            const float a1 = a0;
+            if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
+#pragma unroll
+                for (int ml = 0; ml < 8; ++ml) {
+                    dacc[ml][0] *= a0; dacc[ml][2] *= a0;
+                    dacc[ml][1] *= a1; dacc[ml][3] *= a1;
+                }
+            }
+        }
+        // B fragments: column vg = query head vg / 2, its hi (vg even) or lo (vg odd) weight
+        // part; tokens 16 s2 + 2 vt (+1) and + 8
+        uint32_t bw[2][2];
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                uint32_t v = 0u;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t xh = __shfl_sync(0xffffffffu, w2s[g], 16 * s2 + 2 * vt + 8 * r);
+                    const uint32_t xl = __shfl_sync(0xffffffffu, w2l[g], 16 * s2 + 2 * vt + 8 * r);
+                    v = (vg >> 1) == g ? ((vg & 1) ? xl : xh) : v;
+                }
+                bw[s2][r] = v;
+            }
+
+        // --------------------------------------------------------- a5: P.V dense
+#pragma unroll
+        for (int ml = 0; ml < 8; ++ml) {
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                uint32_t a[4], alo[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int bit = ((ml * 2 + s2) * 4 + r) * FB;
+                    const int wi = bit >> 5, sh = bit & 31;
+                    uint32_t off;
+                    if (sh + FB <= 32) off = sh >= 7 ? (vw[wi] >> (sh - 7)) : (vw[wi] << (7 - sh));
+                    else off = __funnelshift_r(vw[wi], vw[wi + 1], sh - 7);
+                    const uint32_t ad = vlut_u | (off & ((NE - 1) << 7));
+                    a[r] = lds_u32(ad);
+                    if constexpr (RESID) alo[r] = lds_u32(ad + NE * 32 * 4);
+                }
+                mma_f16_f32(dacc[ml], a, bw[s2]);
+                if constexpr (RESID) mma_f16_f32(dacc[ml], alo, bw[s2]);
+            }
+        }
+
+        // ------------------------------------------------------ a6: V outliers
+        // p_g (x - V^(code)) of every item for the G heads, summed in fixed point (scale from
+        // the tile's largest |term|) with native shared integer atomics, folded into osp
+        __syncwarp();
+        if (nv > 0 || vov) {
+            // item -> (channel, delta); the G terms are ps[g][j] * delta
+            auto v_delta = [&](uint32_t itm, bool act, int &j, int &cc) -> float {
+                j = (int)((itm >> 11) & 31u);
+                cc = (int)(itm & 0x7fu);
+                const int flag = (int)((itm >> 9) & 3u);
+                int code = flag == 1 ? CM : 0;
+                if (act && flag == 0) {
+                    const int bit = vf_bit(j, cc, BITS);
+                    const uint32_t *wq = c.vcodes + vf_word(t, c.H_kv, hk, bit >> 5, vf_lane(j, cc), BITS);
+                    unsigned long long w64 = __ldg(wq);
+                    if ((bit & 31) + BITS > 32) w64 |= (unsigned long long)__ldg(wq + 32) << 32;
+                    code = (int)((w64 >> (bit & 31)) & CM);
+                }
+                const float s_n = __shfl_sync(0xffffffffu, vsz.x, j), z_n = __shfl_sync(0xffffffffu, vsz.y, j);
+                const float xval = __half2float(__ushort_as_half((uint16_t)(itm >> 16)));
+                return act ? xval - (cbVs[code] * s_n + z_n) : 0.f;
+            };
+            const int64_t bucket = (int64_t)t * c.NG + hk;
+            // the items beyond the registers (rare): x0 + lane for x0 >= 32 IPL, then (overflowed
+            // bucket) every CSR record of the tile's tokens in this KV head
+            const int kvn = c.kv;
+            const int x_beg = vov ? 0 : 32 * IPL;
+            const int x_end = (vov ? ntok * kvn : 0) + nv;
+            auto slow_item = [&](int x0, int &j, int &cc) -> float {
+                uint32_t itm = 0u;
+                bool act = false;
+                if (x0 < nv) {
+                    act = x0 + lane < nv;
+                    itm = act ? __ldg(c.vit + bucket * c.vcap_g + x0 + lane) : 0u;
+                } else {
+                    const int r = x0 - nv + lane;
+                    act = r < ntok * kvn;
+                    if (act) {
+                        const uint32_t rec = __ldcg(c.vout + n0 * kvn + r);
+                        const int ch = (int)(rec & 0xffffu);
+                        act = ch >= c_lo && ch < c_lo + kHeadDim;
+                        itm = (rec & 0xffff0000u) | ((uint32_t)(r / kvn) << 11) | (uint32_t)(act ? ch - c_lo : 0);
+                    }
+                }
+                return v_delta(itm, act, j, cc);
+            };
+            const bool slow = nv > 32 * IPL || vov;
+            float dl[IPL];
+            int jx[IPL], cx[IPL];
+            float pmax = 0.f;
+#pragma unroll
+            for (int g = 0; g < G; ++g) pmax = fmaxf(pmax, ps[g * 32 + lane]);
+            pmax = warp_max(pmax);   // every term is <= pmax |delta|
+            float mx = 0.f;
+#pragma unroll
+            for (int k = 0; k < IPL; ++k) {
+                dl[k] = 0.f; jx[k] = 0; cx[k] = 0;
+                if (32 * k < nv && !vov) dl[k] = v_delta(vitm[k], lane + 32 * k < nv, jx[k], cx[k]);
+                mx = fmaxf(mx, fabsf(dl[k]));
+            }
+            if (slow)
+                for (int x0 = x_beg; x0 < x_end; x0 += 32) {
+                    int j, cc;
+                    mx = fmaxf(mx, fabsf(slow_item(x0, j, cc)));
+                }
+            mx = warp_max(mx) * pmax;
+            const int emx = mx > 0.f ? ilog2f(mx) : 0;
+            const float S = pow2i(24 - emx);
+            auto add = [&](float d, int j, int cc) {
+                if (d == 0.f) return;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float v = ps[g * 32 + j] * d;
+                    if (v != 0.f) atomicAdd(&vfix[g * kHeadDim + cc], __float2int_rn(v * S));
+                }
+            };
+            if (!vov) {
+#pragma unroll
+                for (int k = 0; k < IPL; ++k) add(dl[k], jx[k], cx[k]);
+            }
+            if (slow)
+                for (int x0 = x_beg; x0 < x_end; x0 += 32) {
+                    int j, cc;
+                    const float d = slow_item(x0, j, cc);
+                    add(d, j, cc);
+                }
+            __syncwarp();
+            // fold only the entries this tile touched: the lanes re-walk their items and the
+            // first to exchange an entry adds it (the others get 0)
+            const float inv = pow2i(emx - 24);
+            auto fold = [&](float d, int cc) {
+                if (d == 0.f) return;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const int v = atomicExch(&vfix[g * kHeadDim + cc], 0);
+                    if (v) osp[g * kHeadDim + cc] += (float)v * inv;
+                }
+            };
+            if (!vov) {
+#pragma unroll
+                for (int k = 0; k < IPL; ++k) fold(dl[k], cx[k]);
+            }
+            if (slow)
+                for (int x0 = x_beg; x0 < x_end; x0 += 32) {
+                    int j, cc;
+                    const float d = slow_item(x0, j, cc);
+                    fold(d, cc);
+                }
+            __syncwarp();
+        }
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < G; ++g) kfix[g * 32 + lane] = 0;
+
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int i = lane + 32 * k;
+            ang64[k] = red2pi(ang64[k] + step64[k]);
+            anc32[apad(i)].x = (float)ang64[k];
+        }
+        cnt_k = ncnt_k;
+        cnt_v = ncnt_v;
+        __syncwarp();
+    }
+
+    // ------------------------------------------- warp partials -> CTA partial (a7)
+    cp_async_wait_all();
+    __syncwarp();
+    // osp (V-outlier sums, real units) += the dense accumulators of the lane's columns
+    {
+        const float sc = pow2i(E_run - WEXP);
+#pragma unroll
+        for (int ml = 0; ml < 8; ++ml) {
+            const int ch = ml * 16 + vg;
+            if (vt < G) {
+                osp[vt * kHeadDim + ch] += (dacc[ml][0] + dacc[ml][1]) * sc;
+                osp[vt * kHeadDim + ch + 8] += (dacc[ml][2] + dacc[ml][3]) * sc;
+            }
+        }
+    }
+    __syncwarp();
+    float *wpart = reinterpret_cast<float *>(osp);   // in place: [G][d] o, then m, l in kst
+    float *wml = reinterpret_cast<float *>(kst);     // [G][2]
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const float l = warp_sum(l_lane[g]), z = warp_sum(z_lane[g]);
+#pragma unroll
+        for (int x = 0; x < kHeadDim / 32; ++x) wpart[g * kHeadDim + x * 32 + lane] += z;
+        if (lane == 0) { wml[g * 2] = m_run[g]; wml[g * 2 + 1] = l; }
+    }
+    __syncthreads();
+    float *part = P.parts + (int64_t)split * c.H_q * (kHeadDim + 2);
+    for (int x = tid; x < G * (kHeadDim + 2); x += NTHR) {
+        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+        float m = -CUDART_INF_F;
+        for (int w = 0; w < NWARP; ++w) {
+            const float *ml = reinterpret_cast<const float *>(wbase + w * C::w_bytes) + g * 2;
+            if (ml[1] != 0.f) m = fmaxf(m, ml[0]);
+        }
+        float l = 0.f, o = 0.f;
+        for (int w = 0; w < NWARP; ++w) {
+            const float *ml = reinterpret_cast<const float *>(wbase + w * C::w_bytes) + g * 2;
+            if (ml[1] == 0.f) continue;
+            const float wt = exp2f(ml[0] - m);
+            l += wt * ml[1];
+            if (ch < kHeadDim) {
+                const float *ow = reinterpret_cast<const float *>(wbase + w * C::w_bytes + C::w_kst + G * 32 * 4);
+                o += wt * ow[g * kHeadDim + ch];
+            }
+        }
+        part[(g0 + g) * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
+    }
+    __threadfence();
+    __syncthreads();
+    int *s_last = flag_s + 1;
+    if (tid == 0) {
+        const unsigned prev = atomicAdd(&P.tickets[hk], 1u);
+        *s_last = (prev == (unsigned)(P.S - 1));
+    }
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    for (int x = tid; x < G * (kHeadDim + 2); x += NTHR) {
+        const int g = x / (kHeadDim + 2), ch = x % (kHeadDim + 2);
+        const int gq = g0 + g;
+        // the S partials in chunks of 8 independent L2 loads (one round trip per chunk, not per
+        // split: the merge runs after every other CTA of the head group has finished)
+        constexpr int MC = 8;
+        const float *pbase = P.parts + (int64_t)gq * (kHeadDim + 2);
+        const int64_t pstride = (int64_t)c.H_q * (kHeadDim + 2);
+        float m = -CUDART_INF_F;
+        for (int s0 = 0; s0 < P.S; s0 += MC) {
+            float mv[MC], lv[MC];
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                const bool in = s0 + k < P.S;
+                const float *ps2 = pbase + (s0 + k) * pstride;
+                mv[k] = in ? __ldcg(ps2 + kHeadDim) : -CUDART_INF_F;
+                lv[k] = in ? __ldcg(ps2 + kHeadDim + 1) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < MC; ++k)
+                if (lv[k] != 0.f) m = fmaxf(m, mv[k]);
+        }
+        float l = 0.f, o = 0.f;
+        for (int s0 = 0; s0 < P.S; s0 += MC) {
+            float mv[MC], lv[MC], ov[MC];
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {
+                const bool in = s0 + k < P.S;
+                const float *ps2 = pbase + (s0 + k) * pstride;
+                mv[k] = in ? __ldcg(ps2 + kHeadDim) : 0.f;
+                lv[k] = in ? __ldcg(ps2 + kHeadDim + 1) : 0.f;
+                ov[k] = (in && ch < kHeadDim) ? __ldcg(ps2 + ch) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < MC; ++k) {   // fixed split order, as before
+                if (lv[k] == 0.f) continue;
+                const float wgt = exp2f(mv[k] - m);
+                l += wgt * lv[k];
+                if (ch < kHeadDim) o += wgt * ov[k];
+            }
+        }
+        if (P.write_partial) {
+            P.out[gq * (kHeadDim + 2) + ch] = ch < kHeadDim ? o : (ch == kHeadDim ? m : l);
+        } else if (ch < kHeadDim) {
+            P.out[gq * kHeadDim + ch] = o / l;
+        }
+    }
+    if (tid == 0) P.tickets[hk] = 0;
+}
+
+
+template <int BITS, bool RESID, int G>
+cudaError_t launch_wgt_t(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
+    using C = TCfg<BITS, RESID, G>;
+    static_assert(C::total <= 227 * 1024, "shared memory");
+    cudaError_t e = cudaFuncSetAttribute(att_wgt_kernel<BITS, RESID, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::total);
+    if (e != cudaSuccess) return e;
+    e = launch_maybe_pdl(att_wgt_kernel<BITS, RESID, G>, grid, C::NTHR, C::total, s, P.pdl != 0, c, P);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+template <int BITS, bool RESID>
+cudaError_t launch_wgt_g(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
+    return c.G == 2 ? launch_wgt_t<BITS, RESID, 2>(c, P, grid, s) : launch_wgt_t<BITS, RESID, 4>(c, P, grid, s);
+}
+
 }  // namespace
 
 bool attend_wag_supported(const DevCache &c) {
@@ -1584,6 +2304,11 @@ cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cud
     P.pdl = a.pdl;
     const int grid = c.H_kv * S;
     const bool resid = !c.vcb_exact16;
+    static const bool lut = getenv("KVQ_WGT_OFF") != nullptr;   // A/B: the LUT kernel att_wag_kernel
+    if (!lut) {
+        if (c.bits == 2) return resid ? launch_wgt_g<2, true>(c, P, grid, s) : launch_wgt_g<2, false>(c, P, grid, s);
+        if (c.bits == 3) return resid ? launch_wgt_g<3, true>(c, P, grid, s) : launch_wgt_g<3, false>(c, P, grid, s);
+    }
     if (c.bits == 2) return resid ? launch_wag_g<2, true>(c, P, grid, s) : launch_wag_g<2, false>(c, P, grid, s);
     if (c.bits == 3) return resid ? launch_wag_g<3, true>(c, P, grid, s) : launch_wag_g<3, false>(c, P, grid, s);
     return cudaErrorInvalidValue;

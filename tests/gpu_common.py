@@ -57,6 +57,13 @@ TOL_ATTEND_MEDIAN = 5e-4
 TOL_FP32 = 1e-3
 
 
+def tol_attend(H_q: int, H_kv: int, bits: int) -> float:
+    """Per-head max tolerance of the attend kernel this configuration selects: the GQA kernel at
+    2-3 bits (att_wgt_kernel) forms its Key scores from fp16 hi + lo operands on the tensor cores,
+    i.e. fp32-accurate products, so it is held to the fp32 bar (R24); the LUT kernels to 2e-3."""
+    return TOL_FP32 if (H_q != H_kv and bits in (2, 3)) else TOL_ATTEND
+
+
 def rel_err_per_head(o, ref):
     o = np.asarray(o, np.float64).reshape(ref.shape)
     num = np.abs(o - ref).max(axis=1)
