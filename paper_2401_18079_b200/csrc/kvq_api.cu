@@ -260,7 +260,7 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
     }
     c->max_splits = 4 * 148;
     A(&c->parts, (size_t)c->max_splits * d.H_q * (kHeadDim + 2) * 4);
-    A(&c->tickets, 64 * 4);
+    A(&c->tickets, 1024 * 4);   // one per attend head group (<= H_q)
     if (getenv("KVQ_PHASE_TIMERS")) A(&c->timers, (16 + 4096) * 8);   // + trace of CTA 0
     if (st != KVQ_OK) { kvq_cache_destroy(c); return st; }
     {

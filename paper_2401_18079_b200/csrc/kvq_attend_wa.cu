@@ -1641,10 +1641,14 @@ __global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(
     double *th64 = reinterpret_cast<double *>(sp); sp += 64 * 8;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n_hg = c.H_kv;   // one CTA per KV head
-    const int hk = blockIdx.x % n_hg;
+    // one CTA per (KV head, sub-group of G of its c.G query heads, split): G = 8 (LLaMA-2-70B)
+    // runs as two sub-groups of 4 that read the same K / V words
+    const int n_sub = c.G / G;
+    const int n_hg = c.H_kv * n_sub;
+    const int hgi = blockIdx.x % n_hg;
+    const int hk = hgi / n_sub;
     const int split = blockIdx.x / n_hg;
-    const int g0 = hk * G;     // first query head
+    const int g0 = hk * c.G + (hgi % n_sub) * G;     // first query head of the CTA
     const int c_lo = hk * kHeadDim;
     const int t_begin = (int)((int64_t)split * P.ntiles / P.S);
     const int t_end = (int)((int64_t)(split + 1) * P.ntiles / P.S);
@@ -2218,7 +2222,7 @@ __global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(
     __syncthreads();
     int *s_last = flag_s + 1;
     if (tid == 0) {
-        const unsigned prev = atomicAdd(&P.tickets[hk], 1u);
+        const unsigned prev = atomicAdd(&P.tickets[hgi], 1u);
         *s_last = (prev == (unsigned)(P.S - 1));
     }
     __syncthreads();
@@ -2271,7 +2275,7 @@ __global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(
             P.out[gq * kHeadDim + ch] = o / l;
         }
     }
-    if (tid == 0) P.tickets[hk] = 0;
+    if (tid == 0) P.tickets[hgi] = 0;
 }
 
 
@@ -2288,13 +2292,14 @@ cudaError_t launch_wgt_t(const DevCache &c, const WParams &P, int grid, cudaStre
 }
 template <int BITS, bool RESID>
 cudaError_t launch_wgt_g(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
-    return c.G == 2 ? launch_wgt_t<BITS, RESID, 2>(c, P, grid, s) : launch_wgt_t<BITS, RESID, 4>(c, P, grid, s);
+    // G = 8: two CTAs of 4 query heads per KV head
+    return c.G == 2 ? launch_wgt_t<BITS, RESID, 2>(c, P, grid, s) : launch_wgt_t<BITS, RESID, 4>(c, P, grid * (c.G / 4), s);
 }
 
 }  // namespace
 
 bool attend_wag_supported(const DevCache &c) {
-    return (c.G == 2 || c.G == 4) && (c.bits == 2 || c.bits == 3) && c.GW == kHeadDim;   // bucket per KV head
+    return (c.G == 2 || c.G == 4 || c.G == 8) && (c.bits == 2 || c.bits == 3) && c.GW == kHeadDim;   // bucket per KV head
 }
 
 cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s) {
@@ -2305,7 +2310,7 @@ cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cud
     const int grid = c.H_kv * S;
     const bool resid = !c.vcb_exact16;
     static const bool lut = getenv("KVQ_WGT_OFF") != nullptr;   // A/B: the LUT kernel att_wag_kernel
-    if (!lut) {
+    if (!lut || c.G == 8) {   // (the LUT kernel has no G = 8 tiling)
         if (c.bits == 2) return resid ? launch_wgt_g<2, true>(c, P, grid, s) : launch_wgt_g<2, false>(c, P, grid, s);
         if (c.bits == 3) return resid ? launch_wgt_g<3, true>(c, P, grid, s) : launch_wgt_g<3, false>(c, P, grid, s);
     }
