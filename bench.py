@@ -41,6 +41,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+GQA_KERNEL = "att_wag_kernel" if os.environ.get("KVQ_WGT_OFF") else "att_wgt_kernel"
 METRIC = "decode-attn µs/token & HBM GB/s vs roofline at 128K–10M ctx, 1/2/4/8 B200"
 
 
@@ -345,7 +346,7 @@ def compare_arm(kvq, gen, calib, accounting, wname, T, n_layers, dev, reps, peak
         kv = caches[0].info()["value_outliers"]
         b0, e0 = caches[0].key_outlier_span(0, caches[0].num_tokens)
         nbytes = accounting.attend_bytes(T, w.D, w.bits, kv, e0 - b0, w.H_q, w.d)
-    kern = "f16_attend_kernel" if fp16 else {1: "att_wa_kernel", 2: "att_wag_kernel"}.get(
+    kern = "f16_attend_kernel" if fp16 else {1: "att_wa_kernel", 2: GQA_KERNEL}.get(
         caches[0].info()["attend_kernel"], "att_kernel")
     out = {"cache": wname, "context": T, "layers_cycled": n_layers, "kernel": kern,
            "attend_us_per_layer": st["median"] * 1e3, "attend_us_p10_p90": [st["p10"] * 1e3, st["p90"] * 1e3],
@@ -724,7 +725,7 @@ def run_ours(args):
             "hbm_gbs_step": bytes_att * w.n_layers / (ms_per_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(w.name),
-                         "kernel": {1: "att_wa_kernel", 2: "att_wag_kernel"}.get(info.get("attend_kernel"), "att_kernel")
+                         "kernel": {1: "att_wa_kernel", 2: GQA_KERNEL}.get(info.get("attend_kernel"), "att_kernel")
                                    + " (kvq_decode_attend: one launch)",
                          "bytes_per_launch": bytes_att, "peak_kind": peak_kind,
                          "splits": info["splits"], "heads_per_cta": info["heads_per_cta"]},

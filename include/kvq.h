@@ -193,7 +193,7 @@ typedef struct {
     int64_t k_outlier_capacity;
     int64_t device_bytes;       /* bytes of device memory owned */
     int32_t attend_kernel;      /* kernel of the last attend: 1 = warp-autonomous (MHA, 2-3 bits,
-                                   csrc/kvq_attend_wa.cu), 2 = its GQA variant (G = 4, 2-3 bits),
+                                   csrc/kvq_attend_wa.cu), 2 = GQA (G = 2, 4, 8, 2-3 bits: att_wgt_kernel, K scores on the tensor cores; KVQ_WGT_OFF=1: the LUT kernel att_wag_kernel),
                                    0 = two-halves (csrc/kvq_attend.cu),
                                    -1 = none yet */
     int32_t bucket_heads;       /* query heads per outlier bucket group */
