@@ -69,9 +69,10 @@ typedef struct kvq_cache kvq_cache;
 typedef struct {
     int32_t n_q_heads;          /* H_q >= 1 */
     int32_t n_kv_heads;         /* H_kv >= 1, H_q % H_kv == 0; GQA group G = H_q/H_kv.
-                                   Attend tilings of this build: G in {1, 2, 4, 8} at 2-3
-                                   bits (G = 8: LLaMA-2-70B), G = 1 at 4 bits; other
-                                   (bits, G) are rejected at create with KVQ_ESHAPE */
+                                   Attend tilings of this build: G in {1, 2, 4, 8} at 2-4
+                                   bits (G = 8: LLaMA-2-70B); 4-bit GQA needs an fp16-exact
+                                   Value decode codebook (R23); other (bits, G) are rejected
+                                   at create with KVQ_ESHAPE */
     int32_t head_dim;           /* d; this build supports d == 128 */
     int32_t bits;               /* b in {2, 3, 4} */
     int32_t outlier_ppm;        /* f in parts per million, 0 <= ppm < 500000;

@@ -231,6 +231,9 @@ kvq_status kvq_cache_create(const kvq_config *cfg, const kvq_params *prm, kvq_ca
         d.vcb_exact16 = 1;
         for (int j = 0; j < nlev; ++j)
             if (__half2float(__float2half_rn(cbs[3][j])) != cbs[3][j]) d.vcb_exact16 = 0;
+        // 4-bit GQA runs on att_wgt_kernel, which has no fp32-codebook residual pass (R23)
+        if (G > 1 && C.bits == 4 && !d.vcb_exact16)
+            st = fail(KVQ_ESHAPE, "4-bit GQA needs an fp16-exact Value decode codebook (R23)");
         const int hkv_g = attend_bucket_heads(C.bits, C.n_q_heads, G, d.vcb_exact16) / G;
         d.GW = hkv_g * kHeadDim;
         d.NG = C.n_kv_heads / hkv_g;

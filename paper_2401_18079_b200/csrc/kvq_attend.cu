@@ -1101,12 +1101,12 @@ cudaError_t launch_b(const DevCache &c, Params &P, int hg, int grid, cudaStream_
 int attend_bucket_heads(int bits, int H_q, int G, int vcb_exact16) {
     // MHA warp-autonomous kernel (4 bits only without the fp32-codebook residual pass)
     if (G == 1 && (bits == 2 || bits == 3 || (bits == 4 && vcb_exact16)) && H_q % 4 == 0) return 2;
-    if ((G == 2 || G == 4 || G == 8) && (bits == 2 || bits == 3)) return G;   // GQA kernels: one KV head
+    if ((G == 2 || G == 4 || G == 8) && bits >= 2 && bits <= 4) return G;   // GQA kernels: one KV head
     return attend_heads_per_cta(bits, H_q, G);
 }
 
 int attend_heads_per_cta(int bits, int H_q, int G) {
-    if (G == 8 && (bits == 2 || bits == 3)) return 4;   // att_wgt_kernel: two 4-head CTAs per KV head
+    if (G > 1 && bits >= 2 && bits <= 4) return G < 4 ? G : 4;   // att_wgt_kernel (G = 8: two 4-head CTAs per KV head)
     const int cap = bits == 4 ? 1 : 4;   // K tables: HG * 64 * 4^b * 4 bytes of shared memory
     for (int hg = cap; hg >= 1; hg >>= 1)
         if (H_q % hg == 0 && hg % G == 0) return hg;

@@ -1599,9 +1599,14 @@ struct TCfg {
     static constexpr int NE = 1 << (2 * BITS);
     static constexpr int KWH = 4 * BITS;
     static constexpr size_t cpt = (size_t)NE * 32 * 8;    // lane-private (cb[a], cb[b]) fp32
-    static constexpr size_t calign = cpt;
     static constexpr size_t vlut = (size_t)(RESID ? 2 : 1) * NE * 32 * 4;
-    static_assert(cpt % ((size_t)NE * 32 * 4) == 0, "V table follows aligned");
+    static constexpr size_t valign = (size_t)NE * 32 * 4;
+    // 2-3 bits: the codebook pair table first, aligned to its size (OR addressing), the V table
+    // after it (aligned too); 4 bits (64 KB pair table, 32 KB V table): byte-aligned codes, PRMT +
+    // add addressing, no alignment
+    static constexpr size_t calign = BITS == 4 ? 16 : cpt;
+    static_assert(BITS == 4 || cpt % valign == 0, "V table follows aligned");
+    static_assert(BITS < 4 || !RESID, "4-bit GQA: fp16-exact Value decode codebook only");
     // per warp: K words (cp.async target, swizzled), K-outlier terms (then p) [G][32], V-outlier
     // sums fp32 [G][128] and fixed point [G][128], anchors, scores [G][32]
     static constexpr size_t w_kst = (size_t)KWH * 32 * 4;
@@ -1627,8 +1632,15 @@ __global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(
     // then the V table (also aligned), then the per-warp regions and the small arrays
     const uint32_t s0 = smem_u32(smem_raw);
     unsigned char *sp = smem_raw + ((C::calign - (s0 % C::calign)) % C::calign);
-    float2 *cpt = reinterpret_cast<float2 *>(sp); sp += C::cpt;
-    uint32_t *vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
+    float2 *cpt;
+    uint32_t *vlut;
+    if constexpr (BITS == 4) {
+        vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
+        cpt = reinterpret_cast<float2 *>(sp); sp += C::cpt;
+    } else {
+        cpt = reinterpret_cast<float2 *>(sp); sp += C::cpt;
+        vlut = reinterpret_cast<uint32_t *>(sp); sp += C::vlut;
+    }
     unsigned char *wbase = sp; sp += NWARP * C::w_bytes;
     float4 *kaf = reinterpret_cast<float4 *>(sp); sp += 68 * 16;   // pair p at p + (p >> 4)
     uint2 *bqs = reinterpret_cast<uint2 *>(sp); sp += 8 * 32 * 8;   // score-mma B fragments [s][lane]
@@ -1779,8 +1791,8 @@ __global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(
     }
 
     // ================================================================ tile loop (per warp)
-    const uint32_t vlut_u = opaque(smem_u32(vlut) | (4u * lane));
-    const uint32_t cpt_u = opaque(smem_u32(cpt) | (8u * lane));
+    const uint32_t vlut_u = BITS == 4 ? smem_u32(vlut) + 4u * lane : opaque(smem_u32(vlut) | (4u * lane));
+    const uint32_t cpt_u = BITS == 4 ? smem_u32(cpt) + 8u * lane : opaque(smem_u32(cpt) | (8u * lane));
     const int vg = lane >> 2, vt = lane & 3;
     // B fragments of the score mma (constant): column vg = q~ of head vg (fp16 hi part) or of
     // head vg - 4 (lo part); k = 2 slot + (0: channel p, 1: channel p + 64); lane (vg, vt)
@@ -1874,7 +1886,14 @@ __global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(
                     const uint32_t f = (sh + 2 * FB <= 32) ? (kwd[m][wi] >> sh) : __funnelshift_r(kwd[m][wi], kwd[m][wi + 1], sh);
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
-                        const uint32_t ad = cpt_u | ((f << (8 - FB * j)) & ((uint32_t)(NE - 1) << 8));
+                        uint32_t ad;
+                        if constexpr (BITS == 4) {   // byte j of the field, times 256, plus the lane base
+                            uint32_t cj;
+                            asm("prmt.b32 %0, %1, 0, %2;" : "=r"(cj) : "r"(f), "r"(0x4440u + (uint32_t)j));
+                            ad = cpt_u + (cj << 8);
+                        } else {
+                            ad = cpt_u | ((f << (8 - FB * j)) & ((uint32_t)(NE - 1) << 8));
+                        }
                         float2 x;
                         asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x.x), "=f"(x.y) : "r"(ad));
                         const float ka = fmaf(x.x, af[j].x, af[j].z), kb = fmaf(x.y, af[j].y, af[j].w);
@@ -2034,10 +2053,17 @@ __global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(
                 for (int r = 0; r < 4; ++r) {
                     const int bit = ((ml * 2 + s2) * 4 + r) * FB;
                     const int wi = bit >> 5, sh = bit & 31;
-                    uint32_t off;
-                    if (sh + FB <= 32) off = sh >= 7 ? (vw[wi] >> (sh - 7)) : (vw[wi] << (7 - sh));
-                    else off = __funnelshift_r(vw[wi], vw[wi + 1], sh - 7);
-                    const uint32_t ad = vlut_u | (off & ((NE - 1) << 7));
+                    uint32_t ad;
+                    if constexpr (BITS == 4) {   // byte-aligned fields: PRMT + add (no table alignment)
+                        uint32_t cf;
+                        asm("prmt.b32 %0, %1, 0, %2;" : "=r"(cf) : "r"(vw[wi]), "r"(0x4440u + (uint32_t)(sh >> 3)));
+                        ad = vlut_u + (cf << 7);
+                    } else {
+                        uint32_t off;
+                        if (sh + FB <= 32) off = sh >= 7 ? (vw[wi] >> (sh - 7)) : (vw[wi] << (7 - sh));
+                        else off = __funnelshift_r(vw[wi], vw[wi + 1], sh - 7);
+                        ad = vlut_u | (off & ((NE - 1) << 7));
+                    }
                     a[r] = lds_u32(ad);
                     if constexpr (RESID) alo[r] = lds_u32(ad + NE * 32 * 4);
                 }
@@ -2299,7 +2325,8 @@ cudaError_t launch_wgt_g(const DevCache &c, const WParams &P, int grid, cudaStre
 }  // namespace
 
 bool attend_wag_supported(const DevCache &c) {
-    return (c.G == 2 || c.G == 4 || c.G == 8) && (c.bits == 2 || c.bits == 3) && c.GW == kHeadDim;   // bucket per KV head
+    return (c.G == 2 || c.G == 4 || c.G == 8) && (c.bits == 2 || c.bits == 3 || (c.bits == 4 && c.vcb_exact16)) &&
+           c.GW == kHeadDim;   // bucket per KV head
 }
 
 cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s) {
@@ -2310,9 +2337,10 @@ cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cud
     const int grid = c.H_kv * S;
     const bool resid = !c.vcb_exact16;
     static const bool lut = getenv("KVQ_WGT_OFF") != nullptr;   // A/B: the LUT kernel att_wag_kernel
-    if (!lut || c.G == 8) {   // (the LUT kernel has no G = 8 tiling)
+    if (!lut || c.G == 8 || c.bits == 4) {   // (the LUT kernel has no G = 8 or 4-bit tiling)
         if (c.bits == 2) return resid ? launch_wgt_g<2, true>(c, P, grid, s) : launch_wgt_g<2, false>(c, P, grid, s);
         if (c.bits == 3) return resid ? launch_wgt_g<3, true>(c, P, grid, s) : launch_wgt_g<3, false>(c, P, grid, s);
+        if (c.bits == 4 && !resid) return launch_wgt_g<4, false>(c, P, grid, s);
     }
     if (c.bits == 2) return resid ? launch_wag_g<2, true>(c, P, grid, s) : launch_wag_g<2, false>(c, P, grid, s);
     if (c.bits == 3) return resid ? launch_wag_g<3, true>(c, P, grid, s) : launch_wag_g<3, false>(c, P, grid, s);

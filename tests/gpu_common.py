@@ -59,9 +59,9 @@ TOL_FP32 = 1e-3
 
 def tol_attend(H_q: int, H_kv: int, bits: int) -> float:
     """Per-head max tolerance of the attend kernel this configuration selects: the GQA kernel at
-    2-3 bits (att_wgt_kernel) forms its Key scores from fp16 hi + lo operands on the tensor cores,
+    2-4 bits (att_wgt_kernel) forms its Key scores from fp16 hi + lo operands on the tensor cores,
     i.e. fp32-accurate products, so it is held to the fp32 bar (R24); the LUT kernels to 2e-3."""
-    return TOL_FP32 if (H_q != H_kv and bits in (2, 3)) else TOL_ATTEND
+    return TOL_FP32 if (H_q != H_kv and bits in (2, 3, 4)) else TOL_ATTEND
 
 
 def rel_err_per_head(o, ref):

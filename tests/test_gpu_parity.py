@@ -131,7 +131,9 @@ def test_host_buffers_are_staged(kvq):
                                              (40, 40, 3, 130), (32, 8, 2, 333),
                                              (8, 8, 4, 1000), (32, 32, 4, 300),
                                              # G = 8 (LLaMA-2-70B 64/8): two 4-head CTAs per KV head
-                                             (16, 2, 3, 300), (64, 8, 3, 257), (16, 2, 2, 200)])
+                                             (16, 2, 3, 300), (64, 8, 3, 257), (16, 2, 2, 200),
+                                             # 4-bit GQA (Mistral-7B nuq4): the tensor-core GQA kernel
+                                             (8, 2, 4, 300), (32, 8, 4, 257), (16, 2, 4, 200), (8, 4, 4, 150)])
 def test_attend_matches_oracle(kvq, H_q, H_kv, bits, T):
     ppm = 10_000
     cal, K, V = setup_layer(4, 0, H_q, H_kv, bits, ppm, T)
