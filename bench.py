@@ -65,9 +65,9 @@ def parse():
 
 
 def workload(args):
-    from kvq_synth import CONFIGS, Workload
+    from kvq_synth import CONFIGS, EXTRA_CONFIGS, Workload
     name = args.workload or ("c3_nuq3" if args.gpus == 1 else "c5")
-    w = CONFIGS[name]
+    w = CONFIGS[name] if name in CONFIGS else EXTRA_CONFIGS[name]
     if args.tokens or args.layers:
         w = Workload(w.name + "-override", args.layers or w.n_layers, w.H_q, w.H_kv, w.d,
                      args.tokens or w.T, w.bits, w.ppm, w.qnorm)

@@ -39,6 +39,13 @@ CONFIGS = {
     "c5": Workload("c5-llama7b-10M-nuq2-1%-qnorm", 32, 32, 32, 128, 10_000_000, 2, qnorm=True),
 }
 
+# Not BASELINE configs: the other paper models the attend kernels tile, for extra
+# measurements only (bench.py --workload NAME).
+EXTRA_CONFIGS = {
+    "c4_nuq4": Workload("x-mistral7b-32L-1M-nuq4-1%", 32, 32, 8, 128, 1 << 20, 4),
+    "l70b": Workload("x-llama2-70b-80L-128K-nuq3-1%", 80, 64, 8, 128, 131072, 3),
+}
+
 
 def calibrate(seed: int, layer: int, D: int, bits: int, ppm: int, n_cal: int = 4096,
               qnorm: bool = False):

@@ -7,11 +7,11 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from kvq_synth import CONFIGS, calib, gen  # noqa: E402
+from kvq_synth import CONFIGS, EXTRA_CONFIGS, calib, gen  # noqa: E402
 from paper_2401_18079_b200 import kvq  # noqa: E402
 
 wname = sys.argv[1] if len(sys.argv) > 1 else "c3_nuq3"
-w = CONFIGS[wname]
+w = CONFIGS[wname] if wname in CONFIGS else EXTRA_CONFIGS[wname]
 dev = torch.device("cuda", 0)
 cal = calib.calibrate_layer(gen.gen_keys(0, 0, 2048, w.D, stream=gen.STREAM_CAL_K),
                             gen.gen_values(0, 0, 2048, w.D, stream=gen.STREAM_CAL_V), w.bits, w.ppm)
