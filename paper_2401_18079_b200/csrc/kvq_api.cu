@@ -532,10 +532,14 @@ kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const vo
     }
     bool one_launch = B <= attend_batch_max();
     const DevCache &d0 = caches[0]->dc;
+    // MHA: att_wa_batch_kernel; GQA: att_wgt_batch_kernel (getenv read once: KVQ_WGT_OFF keeps the
+    // per-sequence LUT kernel for A/B)
+    static const bool wgt_off = getenv("KVQ_WGT_OFF") != nullptr;
+    const bool gqa = attend_wag_supported(d0) && !(wgt_off && d0.G != 8 && d0.bits != 4);
     for (int i = 0; i < B && one_launch; ++i) {
         const DevCache &d = caches[i]->dc;
-        one_launch = attend_wa_supported(d) && d.bits == d0.bits && d.vcb_exact16 == d0.vcb_exact16 &&
-                     d.H_q == d0.H_q && d.H_kv == d0.H_kv;
+        one_launch = (gqa ? attend_wag_supported(d) : attend_wa_supported(d)) && d.bits == d0.bits &&
+                     d.vcb_exact16 == d0.vcb_exact16 && d.H_q == d0.H_q && d.H_kv == d0.H_kv;
     }
     if (!one_launch) {   // shapes the batched kernel does not cover: one attend per cache
         for (int i = 0; i < B; ++i) {
@@ -559,11 +563,12 @@ kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const vo
         a.q = (const __half *)q[i]; a.pos = pos[i]; a.T = c->T; a.out = o[i]; a.write_partial = 0;
         a.parts = c->parts; a.tickets = c->tickets; a.splits = c->splits_forced;
     }
-    cudaError_t e = launch_attend_wa_batch(cs.data(), as.data(), B, (cudaStream_t)stream, splits.data());
+    cudaError_t e = gqa ? launch_attend_wgt_batch(cs.data(), as.data(), B, (cudaStream_t)stream, splits.data())
+                        : launch_attend_wa_batch(cs.data(), as.data(), B, (cudaStream_t)stream, splits.data());
     if (e != cudaSuccess) return cuda_fail(e, "batched attend launch");
     for (int i = 0; i < B; ++i) {
         caches[i]->last_splits = splits[(size_t)i];
-        caches[i]->last_kernel = 1;
+        caches[i]->last_kernel = gqa ? 2 : 1;
         caches[i]->pdl_ok = 0;
     }
     return KVQ_OK;

@@ -1618,7 +1618,7 @@ struct TCfg {
 };
 
 template <int BITS, bool RESID, int G>
-__global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(DevCache c, WParams P) {
+__device__ __forceinline__ void att_wgt_body(const DevCache &c, const WParams &P, const int blk) {
     using C = TCfg<BITS, RESID, G>;
     constexpr int NWARP = C::NWARP, NTHR = C::NTHR, IPL = C::IPL;
     constexpr int NE = C::NE;
@@ -1657,9 +1657,9 @@ __global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(
     // runs as two sub-groups of 4 that read the same K / V words
     const int n_sub = c.G / G;
     const int n_hg = c.H_kv * n_sub;
-    const int hgi = blockIdx.x % n_hg;
+    const int hgi = blk % n_hg;
     const int hk = hgi / n_sub;
-    const int split = blockIdx.x / n_hg;
+    const int split = blk / n_hg;
     const int g0 = hk * c.G + (hgi % n_sub) * G;     // first query head of the CTA
     const int c_lo = hk * kHeadDim;
     const int t_begin = (int)((int64_t)split * P.ntiles / P.S);
@@ -2306,6 +2306,21 @@ __global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(
 
 
 template <int BITS, bool RESID, int G>
+__global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_kernel(DevCache c, WParams P) {
+    att_wgt_body<BITS, RESID, G>(c, P, (int)blockIdx.x);
+}
+
+// Batched GQA decode: B independent caches of one configuration in one launch,
+// per-sequence descriptors in the kernel parameter space (as att_wa_batch_kernel)
+template <int BITS, bool RESID, int G>
+__global__ void __launch_bounds__(TCfg<BITS, RESID, G>::NTHR, 1) att_wgt_batch_kernel(const __grid_constant__ WBatch b) {
+    const int blk = (int)blockIdx.x;
+    int s = 0;
+    while (s + 1 < b.n && blk >= b.cta0[s + 1]) ++s;
+    att_wgt_body<BITS, RESID, G>(b.c[s], b.p[s], blk - b.cta0[s]);
+}
+
+template <int BITS, bool RESID, int G>
 cudaError_t launch_wgt_t(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
     using C = TCfg<BITS, RESID, G>;
     static_assert(C::total <= 227 * 1024, "shared memory");
@@ -2316,6 +2331,20 @@ cudaError_t launch_wgt_t(const DevCache &c, const WParams &P, int grid, cudaStre
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
+template <int BITS, bool RESID, int G>
+cudaError_t launch_wgt_batch_t(const WBatch &b, int grid, cudaStream_t s) {
+    using C = TCfg<BITS, RESID, G>;
+    cudaError_t e = cudaFuncSetAttribute(att_wgt_batch_kernel<BITS, RESID, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::total);
+    if (e != cudaSuccess) return e;
+    att_wgt_batch_kernel<BITS, RESID, G><<<grid, C::NTHR, C::total, s>>>(b);
+    return cudaGetLastError();
+}
+template <int BITS, bool RESID>
+cudaError_t launch_wgt_batch_g(const WBatch &b, int G, int grid, cudaStream_t s) {
+    return G == 2 ? launch_wgt_batch_t<BITS, RESID, 2>(b, grid, s) : launch_wgt_batch_t<BITS, RESID, 4>(b, grid, s);
+}
+
 template <int BITS, bool RESID>
 cudaError_t launch_wgt_g(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
     // G = 8: two CTAs of 4 query heads per KV head
@@ -2395,6 +2424,46 @@ cudaError_t launch_attend_wa_batch(const DevCache *const *cs, const AttendArgs *
     if (c0.bits == 2) return resid ? launch_wa_batch_t<2, true>(bb, cta, s) : launch_wa_batch_t<2, false>(bb, cta, s);
     if (c0.bits == 3) return resid ? launch_wa_batch_t<3, true>(bb, cta, s) : launch_wa_batch_t<3, false>(bb, cta, s);
     if (c0.bits == 4 && !resid) return launch_wa_batch_t<4, false>(bb, cta, s);
+    return cudaErrorInvalidValue;
+}
+
+// Batched GQA decode: one att_wgt_batch_kernel launch over B caches of one configuration (the
+// GQA kernel's tiling: H_kv x G / Gs head groups of Gs = min(G, 4) query heads per sequence)
+cudaError_t launch_attend_wgt_batch(const DevCache *const *cs, const AttendArgs *as, int B, cudaStream_t s,
+                                    int *splits_out) {
+    if (B < 1 || B > kMaxBatch) return cudaErrorInvalidValue;
+    static WBatch b;   // large: built on the host per call (not thread-safe across host threads)
+    WBatch &bb = b;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t tiles_all = 0;
+    for (int i = 0; i < B; ++i) tiles_all += (as[i].T + 31) / 32;
+    const DevCache &c0 = *cs[0];
+    const int Gs = c0.G < 4 ? c0.G : 4;
+    bb.n = B;
+    int cta = 0;
+    for (int i = 0; i < B; ++i) {
+        const DevCache &c = *cs[i];
+        const int n_hg = c.H_kv * (c.G / Gs);
+        const int ntiles = (int)((as[i].T + 31) / 32);
+        int S = (int)((int64_t)sms * ntiles / (tiles_all * n_hg));
+        if (as[i].splits > 0) S = as[i].splits;
+        S = S < 1 ? 1 : (S > ntiles ? ntiles : S);
+        WParams &P = bb.p[i];
+        P = WParams{};
+        P.q = as[i].q; P.pos = as[i].pos; P.T = as[i].T; P.S = S; P.ntiles = ntiles;
+        P.out = as[i].out; P.parts = as[i].parts; P.tickets = as[i].tickets; P.write_partial = as[i].write_partial;
+        P.pdl = 0;
+        bb.c[i] = c;
+        bb.cta0[i] = cta;
+        cta += n_hg * S;
+        if (splits_out) splits_out[i] = S;
+    }
+    bb.cta0[B] = cta;
+    const bool resid = !c0.vcb_exact16;
+    if (c0.bits == 2) return resid ? launch_wgt_batch_g<2, true>(bb, Gs, cta, s) : launch_wgt_batch_g<2, false>(bb, Gs, cta, s);
+    if (c0.bits == 3) return resid ? launch_wgt_batch_g<3, true>(bb, Gs, cta, s) : launch_wgt_batch_g<3, false>(bb, Gs, cta, s);
+    if (c0.bits == 4 && !resid) return launch_wgt_batch_g<4, false>(bb, Gs, cta, s);
     return cudaErrorInvalidValue;
 }
 

@@ -165,6 +165,9 @@ cudaError_t launch_attend_wa(const DevCache &c, const AttendArgs &a, int S, cuda
 int attend_batch_max();
 cudaError_t launch_attend_wa_batch(const DevCache *const *cs, const AttendArgs *as, int B, cudaStream_t s,
                                    int *splits_out);
+// batched GQA decode over B caches of one configuration (all attend_wag_supported): one launch
+cudaError_t launch_attend_wgt_batch(const DevCache *const *cs, const AttendArgs *as, int B, cudaStream_t s,
+                                    int *splits_out);
 // warp-autonomous GQA variant (G = 4, 2-3 bits): one CTA per KV head
 bool attend_wag_supported(const DevCache &c);
 cudaError_t launch_attend_wag(const DevCache &c, const AttendArgs &a, int S, cudaStream_t s);
