@@ -1106,7 +1106,8 @@ int attend_bucket_heads(int bits, int H_q, int G, int vcb_exact16) {
 }
 
 int attend_heads_per_cta(int bits, int H_q, int G) {
-    if (G > 1 && bits >= 2 && bits <= 4) return G < 4 ? G : 4;   // att_wgt_kernel (G = 8: two 4-head CTAs per KV head)
+    if (G == 8 && (bits == 2 || bits == 3)) return 8;             // att_wgt_kernel: one CTA per KV head
+    if (G > 1 && bits >= 2 && bits <= 4) return G < 4 ? G : 4;   // att_wgt_kernel (4-bit G = 8: two 4-head CTAs)
     const int cap = bits == 4 ? 1 : 4;   // K tables: HG * 64 * 4^b * 4 bytes of shared memory
     for (int hg = cap; hg >= 1; hg >>= 1)
         if (H_q % hg == 0 && hg % G == 0) return hg;
@@ -1144,7 +1145,7 @@ cudaError_t launch_attend(const DevCache &c, const AttendArgs &a, int *splits_us
     const bool wa = !a.timers && !legacy && attend_wa_supported(c);
     const bool wag = !a.timers && !legacy && attend_wag_supported(c);
     // CTA heads: 4 for the warp-autonomous kernels, else one bucket group
-    const int hg = wa ? 4 : (wag ? (c.G < 4 ? c.G : 4) : (c.GW / kHeadDim) * c.G);
+    const int hg = wa ? 4 : (wag ? attend_heads_per_cta(c.bits, c.H_q, c.G) : (c.GW / kHeadDim) * c.G);
     if (hg == 0) return cudaErrorInvalidValue;
     if (a.kernel_out) *a.kernel_out = wa ? 1 : (wag ? 2 : 0);
     if (a.hg_out) *a.hg_out = hg;

@@ -1592,8 +1592,8 @@ __device__ __forceinline__ int apad(int p) { return p + 2 * (p >> 4); }    // 8-
 
 template <int BITS, bool RESID, int G>
 struct TCfg {
-    static_assert(G <= 4, "hi/lo query columns: 2 G <= 8 mma columns");
-    static constexpr int NWARP = NSG;
+    static_assert(G <= 4 || G == 8, "G <= 4: hi / lo query columns; G = 8: hi and lo B fragments");
+    static constexpr int NWARP = G == 8 ? 12 : NSG;   // G = 8: [8][128] outlier sums per warp
     static constexpr int NTHR = NWARP * 32;
     static constexpr int IPL = 4;
     static constexpr int NE = 1 << (2 * BITS);
@@ -1612,7 +1612,7 @@ struct TCfg {
     static constexpr size_t w_kst = (size_t)KWH * 32 * 4;
     static constexpr size_t w_bytes = w_kst + G * 32 * 4 + G * kHeadDim * 4 * 2 + 72 * 8 + G * 32 * 4;
     static constexpr int KCH = KWH / 4;
-    static constexpr size_t small = 68 * 16 /* kaf */ + 8 * 32 * 8 /* bqs */ + G * kHeadDim * 4 /* qs */ + kHeadDim * 4 * 2 /* ks, kz */
+    static constexpr size_t small = 68 * 16 /* kaf */ + 8 * 32 * 16 /* bqs */ + G * kHeadDim * 4 /* qs */ + kHeadDim * 4 * 2 /* ks, kz */
         + 64 * 4 /* cb */ + 64 /* flags */ + 64 * 16 /* cis(pos theta) */ + 64 * 8 /* theta */;
     static constexpr size_t total = calign + cpt + vlut + NWARP * w_bytes + small;
 };
@@ -1643,7 +1643,8 @@ __device__ __forceinline__ void att_wgt_body(const DevCache &c, const WParams &P
     }
     unsigned char *wbase = sp; sp += NWARP * C::w_bytes;
     float4 *kaf = reinterpret_cast<float4 *>(sp); sp += 68 * 16;   // pair p at p + (p >> 4)
-    uint2 *bqs = reinterpret_cast<uint2 *>(sp); sp += 8 * 32 * 8;   // score-mma B fragments [s][lane]
+    uint4 *bqs = reinterpret_cast<uint4 *>(sp); sp += 8 * 32 * 16;   // score-mma B fragments [s][lane]
+    constexpr bool G8 = G == 8;   // 8 query heads: columns = heads, hi and lo as two B fragments
     float *qs = reinterpret_cast<float *>(sp); sp += G * kHeadDim * 4;
     float *ks_s = reinterpret_cast<float *>(sp); sp += kHeadDim * 4;
     float *kz_s = reinterpret_cast<float *>(sp); sp += kHeadDim * 4;
@@ -1799,21 +1800,22 @@ __device__ __forceinline__ void att_wgt_body(const DevCache &c, const WParams &P
     // holds slot vt (pair 16 vt + 2 s) and slot vt + 4 (pair 16 vt + 2 s + 1) of k-step s
     // (a CTA-wide table in shared memory, one 8-byte load per k-step; written by warp 0)
     if (warp == 0) {
-        const int hq = vg < 4 ? vg : vg - 4;
+        const int hq = G8 ? vg : (vg < 4 ? vg : vg - 4);
 #pragma unroll 1
         for (int s = 0; s < 8; ++s) {
-            uint32_t v[2];
+            uint32_t v[2], vl[2];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int p = 16 * vt + 2 * s + j;
-                v[j] = 0u;
+                v[j] = vl[j] = 0u;
                 if (hq < G) {
                     const float qa = qs[hq * kHeadDim + p], qb = qs[hq * kHeadDim + p + 64];
                     const float ha = __half2float(__float2half_rn(qa)), hb = __half2float(__float2half_rn(qb));
-                    v[j] = vg < 4 ? pack_half2(ha, hb) : pack_half2(qa - ha, qb - hb);
+                    if (G8) { v[j] = pack_half2(ha, hb); vl[j] = pack_half2(qa - ha, qb - hb); }
+                    else v[j] = vg < 4 ? pack_half2(ha, hb) : pack_half2(qa - ha, qb - hb);
                 }
             }
-            bqs[s * 32 + lane] = make_uint2(v[0], v[1]);
+            bqs[s * 32 + lane] = make_uint4(v[0], v[1], vl[0], vl[1]);
         }
     }
     __syncthreads();
@@ -1907,12 +1909,16 @@ __device__ __forceinline__ void att_wgt_body(const DevCache &c, const WParams &P
                         alo[m >> 1][2 * j + (m & 1)] = pack_half2(ra - __low2float(h2), rb - __high2float(h2));
                     }
                 }
-                const uint2 bb = bqs[s * 32 + lane];
+                const uint4 bb = bqs[s * 32 + lane];
                 const uint32_t b[2] = {bb.x, bb.y};
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt) {
                     mma_f16_f32(dsc[mt], ahi[mt], b);
                     mma_f16_f32(dsc[mt], alo[mt], b);
+                    if constexpr (G8) {   // + A_hi x q~_lo (A_lo x q~_lo is below fp32 rounding)
+                        const uint32_t bl[2] = {bb.z, bb.w};
+                        mma_f16_f32(dsc[mt], ahi[mt], bl);
+                    }
                 }
             }
         }
@@ -1922,9 +1928,13 @@ __device__ __forceinline__ void att_wgt_body(const DevCache &c, const WParams &P
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const float v = dsc[mt][r] + __shfl_xor_sync(0xffffffffu, dsc[mt][r], 2);
                 const int h = 2 * vt + (r & 1);
-                if (vt < 2 && h < G) sct[h * 32 + 16 * mt + vg + 8 * (r >> 1)] = v * 16.f;
+                if constexpr (G8) {   // column = head, hi and lo already summed by the mma
+                    sct[h * 32 + 16 * mt + vg + 8 * (r >> 1)] = dsc[mt][r] * 16.f;
+                } else {
+                    const float v = dsc[mt][r] + __shfl_xor_sync(0xffffffffu, dsc[mt][r], 2);
+                    if (vt < 2 && h < G) sct[h * 32 + 16 * mt + vg + 8 * (r >> 1)] = v * 16.f;
+                }
             }
         // V words of this tile (L2 hits), used after the softmax
         uint32_t vw[KWH];
@@ -2013,11 +2023,15 @@ __device__ __forceinline__ void att_wgt_body(const DevCache &c, const WParams &P
             w2l[g] = lb | (__shfl_down_sync(0xffffffffu, lb, 1) << 16);
         }
         {   // rescale the accumulators: per column (head) alpha, and the weight exponent
-            float a0 = al[0];
+            // (G <= 4: columns 2t, 2t+1 are head t's hi / lo sums; G = 8: heads 2t, 2t+1)
+            float a0 = al[0], a1 = al[0];
 #pragma unroll
-            for (int g = 1; g < G; ++g) a0 = hcl == g ? al[g] : a0;
+            for (int g = 1; g < G; ++g) {
+                if constexpr (G8) { a0 = 2 * vt == g ? al[g] : a0; a1 = 2 * vt + 1 == g ? al[g] : a1; }
+                else a0 = hcl == g ? al[g] : a0;
+            }
             a0 *= rE;
-            const float a1 = a0;
+            if constexpr (G8) a1 *= rE; else a1 = a0;
             if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
 #pragma unroll
                 for (int ml = 0; ml < 8; ++ml) {
@@ -2026,21 +2040,24 @@ __device__ __forceinline__ void att_wgt_body(const DevCache &c, const WParams &P
                 }
             }
         }
-        // B fragments: column vg = query head vg / 2, its hi (vg even) or lo (vg odd) weight
-        // part; tokens 16 s2 + 2 vt (+1) and + 8
-        uint32_t bw[2][2];
+        // B fragments: G <= 4: column vg = query head vg / 2, its hi (vg even) or lo (vg odd)
+        // weight part; G = 8: column vg = head vg, hi (bw) and lo (bwl) as two B fragments;
+        // tokens 16 s2 + 2 vt (+1) and + 8
+        uint32_t bw[2][2], bwl[2][2];
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2)
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                uint32_t v = 0u;
+                uint32_t v = 0u, vl = 0u;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const uint32_t xh = __shfl_sync(0xffffffffu, w2s[g], 16 * s2 + 2 * vt + 8 * r);
                     const uint32_t xl = __shfl_sync(0xffffffffu, w2l[g], 16 * s2 + 2 * vt + 8 * r);
-                    v = (vg >> 1) == g ? ((vg & 1) ? xl : xh) : v;
+                    if constexpr (G8) { v = vg == g ? xh : v; vl = vg == g ? xl : vl; }
+                    else v = (vg >> 1) == g ? ((vg & 1) ? xl : xh) : v;
                 }
                 bw[s2][r] = v;
+                bwl[s2][r] = vl;
             }
 
         // --------------------------------------------------------- a5: P.V dense
@@ -2069,6 +2086,10 @@ __device__ __forceinline__ void att_wgt_body(const DevCache &c, const WParams &P
                 }
                 mma_f16_f32(dacc[ml], a, bw[s2]);
                 if constexpr (RESID) mma_f16_f32(dacc[ml], alo, bw[s2]);
+                if constexpr (G8) {
+                    mma_f16_f32(dacc[ml], a, bwl[s2]);
+                    if constexpr (RESID) mma_f16_f32(dacc[ml], alo, bwl[s2]);
+                }
             }
         }
 
@@ -2206,7 +2227,12 @@ __device__ __forceinline__ void att_wgt_body(const DevCache &c, const WParams &P
 #pragma unroll
         for (int ml = 0; ml < 8; ++ml) {
             const int ch = ml * 16 + vg;
-            if (vt < G) {
+            if constexpr (G8) {   // columns 2t, 2t+1 = heads 2t, 2t+1
+                osp[(2 * vt) * kHeadDim + ch] += dacc[ml][0] * sc;
+                osp[(2 * vt + 1) * kHeadDim + ch] += dacc[ml][1] * sc;
+                osp[(2 * vt) * kHeadDim + ch + 8] += dacc[ml][2] * sc;
+                osp[(2 * vt + 1) * kHeadDim + ch + 8] += dacc[ml][3] * sc;
+            } else if (vt < G) {
                 osp[vt * kHeadDim + ch] += (dacc[ml][0] + dacc[ml][1]) * sc;
                 osp[vt * kHeadDim + ch + 8] += (dacc[ml][2] + dacc[ml][3]) * sc;
             }
@@ -2342,12 +2368,16 @@ cudaError_t launch_wgt_batch_t(const WBatch &b, int grid, cudaStream_t s) {
 }
 template <int BITS, bool RESID>
 cudaError_t launch_wgt_batch_g(const WBatch &b, int G, int grid, cudaStream_t s) {
+    if constexpr (BITS < 4)
+        if (G == 8) return launch_wgt_batch_t<BITS, RESID, 8>(b, grid, s);
     return G == 2 ? launch_wgt_batch_t<BITS, RESID, 2>(b, grid, s) : launch_wgt_batch_t<BITS, RESID, 4>(b, grid, s);
 }
 
 template <int BITS, bool RESID>
 cudaError_t launch_wgt_g(const DevCache &c, const WParams &P, int grid, cudaStream_t s) {
-    // G = 8: two CTAs of 4 query heads per KV head
+    // G = 8: one 8-head CTA per KV head at 2-3 bits; at 4 bits (shared memory) two CTAs of 4
+    if constexpr (BITS < 4)
+        if (c.G == 8) return launch_wgt_t<BITS, RESID, 8>(c, P, grid, s);
     return c.G == 2 ? launch_wgt_t<BITS, RESID, 2>(c, P, grid, s) : launch_wgt_t<BITS, RESID, 4>(c, P, grid * (c.G / 4), s);
 }
 
@@ -2439,7 +2469,7 @@ cudaError_t launch_attend_wgt_batch(const DevCache *const *cs, const AttendArgs 
     int64_t tiles_all = 0;
     for (int i = 0; i < B; ++i) tiles_all += (as[i].T + 31) / 32;
     const DevCache &c0 = *cs[0];
-    const int Gs = c0.G < 4 ? c0.G : 4;
+    const int Gs = (c0.G == 8 && c0.bits < 4) ? 8 : (c0.G < 4 ? c0.G : 4);   // query heads per CTA
     bb.n = B;
     int cta = 0;
     for (int i = 0; i < B; ++i) {

@@ -10,7 +10,7 @@ from paper_2401_18079_b200 import kvq as K_  # noqa: E402
 from tests.gpu_common import make_cache, rel_err_per_head, setup_layer  # noqa: E402
 from tests.test_gpu_parity import oracle_attend, oracle_cache  # noqa: E402
 
-for (H, Hk, bits, T) in [(40, 40, 3, 130), (8, 8, 3, 1000), (16, 16, 3, 700), (8, 8, 2, 517), (32, 8, 3, 257), (8, 4, 3, 301), (16, 8, 2, 400), (32, 16, 3, 96), (32, 8, 2, 333)]:
+for (H, Hk, bits, T) in [(16, 2, 3, 300), (64, 8, 3, 257), (16, 2, 2, 200), (40, 40, 3, 130), (8, 8, 3, 1000), (16, 16, 3, 700), (8, 8, 2, 517), (32, 8, 3, 257), (8, 4, 3, 301), (16, 8, 2, 400), (32, 16, 3, 96), (32, 8, 2, 333)]:
     cal, K, V = setup_layer(4, 0, H, Hk, bits, 10_000, T)
     ref = oracle_cache(cal, K, V, 10_000)
     c = make_cache(K_, cal, H, Hk, bits, 10_000, capacity=T + 64)
