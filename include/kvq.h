@@ -21,7 +21,8 @@
  *     faults) are STICKY: the next call on that cache (or kvq_sync) returns them.
  *   - "device or host" buffers: the library detects host memory (pinned or pageable)
  *     with cudaPointerGetAttributes and stages it through device scratch on the call's
- *     stream (H2D before, D2H after, all stream ordered; pageable host memory makes the
+ *     stream (H2D before, D2H after, all stream ordered: a page-locked host output is
+ *     valid once the stream reaches the end of the call; pageable host memory makes the
  *     call synchronous).  Device buffers must live on cfg.device (else KVQ_EDEVICE).
  *     With KVQ_FLAG_TRUST_DEVICE_PTRS the check is skipped and pointers are assumed
  *     to be device pointers on cfg.device.

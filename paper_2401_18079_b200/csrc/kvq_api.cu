@@ -88,6 +88,14 @@ kvq_status dev_alloc(kvq_cache *c, T **p, size_t bytes) {
 }
 
 // Classify a user pointer: 0 = device on `dev`, 1 = host, -1 = device elsewhere.
+// page-locked (cudaHostAlloc / cudaHostRegister) host memory: device-to-host copies into it
+// stay asynchronous (stream ordered, kvq.h); pageable host outputs make the call synchronous
+bool host_pinned(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeHost;
+}
+
 int classify(const void *p, int dev, uint32_t flags) {
     if (flags & KVQ_FLAG_TRUST_DEVICE_PTRS) return 0;
     cudaPointerAttributes at;
@@ -505,7 +513,7 @@ static kvq_status attend_impl(kvq_cache *c, const void *q, int64_t pos, float *o
     if (e != cudaSuccess) return cuda_fail(e, "attend launch");
     if (co == 1) {
         CK(cudaMemcpyAsync(out, od, obytes, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        if (!host_pinned(out)) CK(cudaStreamSynchronize(s));
     }
     return KVQ_OK;
 }
@@ -595,7 +603,7 @@ kvq_status kvq_merge_partials(const float *parts, int32_t P, int32_t H, int32_t 
     if (e != cudaSuccess) return cuda_fail(e, "merge launch");
     if (co == 1) { CK(cudaMemcpyAsync(o, od, ob, cudaMemcpyDeviceToHost, s)); }
     if (tmp) { CK(cudaFreeAsync(tmp, s)); }
-    if (co == 1) CK(cudaStreamSynchronize(s));
+    if (co == 1 && !host_pinned(o)) CK(cudaStreamSynchronize(s));
     return KVQ_OK;
 }
 
@@ -1004,7 +1012,7 @@ kvq_status kvq_f16_decode_attend(kvq_f16_cache *c, const void *q, int64_t pos, f
     if (e != cudaSuccess) return cuda_fail(e, "f16 attend launch");
     if (co == 1) {
         CK(cudaMemcpyAsync(o, od, ob, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        if (!host_pinned(o)) CK(cudaStreamSynchronize(s));
     }
     return KVQ_OK;
 }

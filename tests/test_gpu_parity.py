@@ -123,6 +123,23 @@ def test_host_buffers_are_staged(kvq):
     assert rel_err_per_head(o, oracle_attend(cal, ref, q, T - 1, H, H)).max() < TOL
 
 
+def test_pinned_host_output_is_stream_ordered(kvq):
+    """Page-locked host q / o: the D2H copy stays on the call's stream (kvq.h), so the output
+    is valid after a stream synchronize, and equals the device-buffer result."""
+    H, bits, ppm, T = 8, 3, 10_000, 300
+    cal, K, V = setup_layer(5, 0, H, H, bits, ppm, T)
+    c = make_cache(kvq, cal, H, H, bits, ppm, capacity=T)
+    c.prefill(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    q = gen.gen_queries(5, 0, H, H, 128)[0]
+    od = torch.zeros((H, 128), dtype=torch.float32, device="cuda")
+    c.attend(torch.from_numpy(q).cuda(), T - 1, od)
+    qh = torch.from_numpy(q).pin_memory()
+    oh = torch.full((H, 128), -1.0, dtype=torch.float32).pin_memory()
+    c.attend(qh, T - 1, oh)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, od.cpu())
+
+
 # ----------------------------------------------------------------- attention (T2) --
 @pytest.mark.parametrize("H_q,H_kv,bits,T", [(1, 1, 4, 4096), (8, 8, 3, 1000), (2, 2, 4, 333),
                                              (8, 8, 2, 517), (8, 2, 3, 300), (4, 1, 3, 129),
