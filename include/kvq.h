@@ -137,13 +137,21 @@ kvq_status kvq_decode_attend_partial(kvq_cache *cache, const void *q_f16, int64_
 
 /* Batched decode (the paper's BS = 4 rows): one decode step for B
  * independent sequences, each with its own cache, query q[i] ([H_q][d] fp16, device), position
- * pos[i] and output o[i] ([H_q][d] fp32, device).  When every cache is attended by the
- * warp-autonomous MHA kernel with the same bits / codebook kind / head shape and B <= 64, the
- * B attends are ONE launch whose CTAs are split over the sequences in proportion to their
- * lengths (one wave for many short contexts instead of B latency-bound launches); otherwise
- * (other shapes) it is B ordinary attends.  Same errors per sequence as kvq_decode_attend. */
+ * pos[i] and output o[i] ([H_q][d] fp32, device).  When every cache is attended by the same
+ * kernel family (the warp-autonomous MHA kernel, or the tensor-core GQA kernel) with the same
+ * bits / codebook kind / head shape and B <= 64, the B attends are ONE launch whose CTAs are
+ * split over the sequences in proportion to their lengths (one wave for many short contexts
+ * instead of B latency-bound launches); otherwise (other shapes) it is B ordinary attends.
+ * Same errors per sequence as kvq_decode_attend. */
 kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const void *const *q,
                                    const int64_t *pos, float *const *o, void *stream);
+
+/* Batched partials: as kvq_decode_attend_batch, but writes each cache's un-normalized partial
+ * part[i] ([H_q][d+2] fp32, device; see kvq_decode_attend_partial).  Every cache must hold at
+ * least one token.  Used for chunk-paged sequences (paper_2401_18079_b200/paged.py: the chunks
+ * of many sequences in one launch, then kvq_merge_partials per sequence). */
+kvq_status kvq_decode_attend_batch_partial(kvq_cache *const *caches, int32_t B, const void *const *q,
+                                           const int64_t *pos, float *const *part, void *stream);
 
 /* Exact log-sum-exp merge of P partials (fixed order 0..P-1), the merge step of the
  * north_star's sequence sharding:
@@ -159,6 +167,11 @@ int64_t kvq_num_tokens(const kvq_cache *cache);
 /* Drop every cached token (capacity kept).  Stream ordered after prior work on
  * `stream`. */
 kvq_status kvq_reset(kvq_cache *cache, void *stream);
+
+/* Move an EMPTY cache to another position range: token t of the cache is position
+ * pos_base + t from now on (cfg.pos_base at create).  KVQ_EINVAL if the cache holds tokens
+ * or pos_base < 0.  Lets a pool reuse fixed-size chunk caches across sequences (paged.py). */
+kvq_status kvq_set_pos_base(kvq_cache *cache, int64_t pos_base);
 
 /* Synchronize the cache's device and surface sticky errors. */
 kvq_status kvq_sync(kvq_cache *cache);

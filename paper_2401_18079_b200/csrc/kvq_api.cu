@@ -405,6 +405,15 @@ kvq_status kvq_sync(kvq_cache *c) {
     return check_sticky(c);
 }
 
+kvq_status kvq_set_pos_base(kvq_cache *c, int64_t pos_base) {
+    if (!c) return fail(KVQ_EINVAL, "null cache");
+    if (c->T != 0) return fail(KVQ_EINVAL, "set_pos_base needs an empty cache (it holds %lld tokens)", (long long)c->T);
+    if (pos_base < 0) return fail(KVQ_EINVAL, "pos_base must be >= 0");
+    c->cfg.pos_base = pos_base;
+    c->dc.pos_base = pos_base;
+    return KVQ_OK;
+}
+
 kvq_status kvq_reset(kvq_cache *c, void *stream) {
     if (!c) return fail(KVQ_EINVAL, "null cache");
     CK(cudaSetDevice(c->cfg.device));
@@ -526,8 +535,8 @@ kvq_status kvq_decode_attend_partial(kvq_cache *c, const void *q, int64_t pos, f
     return attend_impl(c, q, pos, part, 1, stream);
 }
 
-kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const void *const *q, const int64_t *pos,
-                                   float *const *o, void *stream) {
+static kvq_status attend_batch_impl(kvq_cache *const *caches, int32_t B, const void *const *q, const int64_t *pos,
+                                    float *const *o, int partial, void *stream) {
     if (!caches || !q || !pos || !o) return fail(KVQ_EINVAL, "null argument");
     if (B < 1) return fail(KVQ_EINVAL, "B must be >= 1");
     for (int i = 0; i < B; ++i) {
@@ -551,7 +560,7 @@ kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const vo
     }
     if (!one_launch) {   // shapes the batched kernel does not cover: one attend per cache
         for (int i = 0; i < B; ++i) {
-            kvq_status st = attend_impl(caches[i], q[i], pos[i], o[i], 0, stream);
+            kvq_status st = attend_impl(caches[i], q[i], pos[i], o[i], partial, stream);
             if (st != KVQ_OK) return st;
         }
         return KVQ_OK;
@@ -568,7 +577,7 @@ kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const vo
         cs[(size_t)i] = &c->dc;
         AttendArgs &a = as[(size_t)i];
         a = AttendArgs{};
-        a.q = (const __half *)q[i]; a.pos = pos[i]; a.T = c->T; a.out = o[i]; a.write_partial = 0;
+        a.q = (const __half *)q[i]; a.pos = pos[i]; a.T = c->T; a.out = o[i]; a.write_partial = partial;
         a.parts = c->parts; a.tickets = c->tickets; a.splits = c->splits_forced;
     }
     cudaError_t e = gqa ? launch_attend_wgt_batch(cs.data(), as.data(), B, (cudaStream_t)stream, splits.data())
@@ -580,6 +589,16 @@ kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const vo
         caches[i]->pdl_ok = 0;
     }
     return KVQ_OK;
+}
+
+kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const void *const *q, const int64_t *pos,
+                                   float *const *o, void *stream) {
+    return attend_batch_impl(caches, B, q, pos, o, 0, stream);
+}
+
+kvq_status kvq_decode_attend_batch_partial(kvq_cache *const *caches, int32_t B, const void *const *q,
+                                           const int64_t *pos, float *const *part, void *stream) {
+    return attend_batch_impl(caches, B, q, pos, part, 1, stream);
 }
 
 kvq_status kvq_merge_partials(const float *parts, int32_t P, int32_t H, int32_t d, float *o,

@@ -32,7 +32,8 @@ EXPORTED = ["kvq_cache_create", "kvq_cache_destroy", "kvq_append", "kvq_prefill_
             "kvq_f16_cache_create", "kvq_f16_cache_destroy", "kvq_f16_append",
             "kvq_f16_decode_attend", "kvq_f16_export", "kvq_f16_num_tokens",
             "kvq_key_thresholds_online", "kvq_decode_attend_batch", "kvq_layer_sensitivity",
-            "kvq_fisher_accumulate", "kvq_assign_bits", "kvq_calibrate_layer"]
+            "kvq_fisher_accumulate", "kvq_assign_bits", "kvq_calibrate_layer",
+            "kvq_decode_attend_batch_partial", "kvq_set_pos_base"]
 
 
 class KVQError(RuntimeError):
@@ -108,6 +109,8 @@ def _load() -> ctypes.CDLL:
         "kvq_f16_num_tokens": (i64, [vp]),
         "kvq_key_thresholds_online": (i32, [vp, i64, i32, i32, vp, vp, i32, vp]),
         "kvq_decode_attend_batch": (i32, [vp, i32, vp, vp, vp, vp]),
+        "kvq_decode_attend_batch_partial": (i32, [vp, i32, vp, vp, vp, vp]),
+        "kvq_set_pos_base": (i32, [vp, i64]),
         "kvq_layer_sensitivity": (i32, [vp, vp, vp, vp, vp, i64, i64, vp, vp]),
         "kvq_fisher_accumulate": (i32, [vp, vp, i64, i32, vp]),
         "kvq_assign_bits": (i32, [vp, i32, i32, i32, i32, vp]),
@@ -238,6 +241,10 @@ class KVQCache:
     def reset(self, stream=None):
         _check(_lib.kvq_reset(self._h, _stream(stream)))
 
+    def set_pos_base(self, pos_base: int):
+        """Reposition an EMPTY cache (token t -> position pos_base + t), kvq_set_pos_base."""
+        _check(_lib.kvq_set_pos_base(self._h, int(pos_base)))
+
     def sync(self):
         _check(_lib.kvq_sync(self._h))
 
@@ -293,6 +300,21 @@ def attend_batch(caches, qs, positions, outs, stream=None):
                                         ctypes.cast(pp, ctypes.c_void_p), ctypes.cast(op, ctypes.c_void_p),
                                         _stream(stream)))
     return outs
+
+
+def attend_batch_partial(caches, qs, positions, parts, stream=None):
+    """Batched partials (kvq_decode_attend_batch_partial): caches[i] attends qs[i] at
+    positions[i] into parts[i] ([H_q, d+2] fp32 device tensors), one launch when the caches share
+    a configuration."""
+    B = len(caches)
+    hs = (ctypes.c_void_p * B)(*[c.handle.value for c in caches])
+    qp = (ctypes.c_void_p * B)(*[_ptr(q).value for q in qs])
+    op = (ctypes.c_void_p * B)(*[_ptr(o).value for o in parts])
+    pp = (ctypes.c_int64 * B)(*[int(p) for p in positions])
+    _check(_lib.kvq_decode_attend_batch_partial(ctypes.cast(hs, ctypes.c_void_p), B, ctypes.cast(qp, ctypes.c_void_p),
+                                                ctypes.cast(pp, ctypes.c_void_p), ctypes.cast(op, ctypes.c_void_p),
+                                                _stream(stream)))
+    return parts
 
 
 def key_thresholds_online(K, outlier_ppm: int, lo=None, hi=None, device: int = 0, stream=None):
