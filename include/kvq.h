@@ -168,6 +168,19 @@ int64_t kvq_num_tokens(const kvq_cache *cache);
  * `stream`. */
 kvq_status kvq_reset(kvq_cache *cache, void *stream);
 
+/* Snapshot / restore (checkpoint / resume; SPEC S:535-536 cache dump / load).  The snapshot is
+ * the device state of the cached tokens (code words, outlier buckets and counts, Value (s, z),
+ * CSR / CSC records) behind a header with the cache's shape; it restores into any cache created
+ * with the same configuration (heads, bits, D, outlier fraction) and enough capacity, which then
+ * continues exactly as the original would (appends, attends).  Both calls synchronize the device.
+ *   kvq_snapshot_bytes: bytes a snapshot of the current contents needs.
+ *   kvq_snapshot: writes it to host memory `host` of `bytes` bytes (KVQ_EINVAL if too small).
+ *   kvq_restore: replaces the cache's contents (KVQ_ESHAPE: other configuration; KVQ_ECAPACITY:
+ *   more tokens or Key outliers than the cache holds; KVQ_EINVAL: not a snapshot / truncated). */
+kvq_status kvq_snapshot_bytes(kvq_cache *cache, int64_t *bytes);
+kvq_status kvq_snapshot(kvq_cache *cache, void *host, int64_t bytes);
+kvq_status kvq_restore(kvq_cache *cache, const void *host, int64_t bytes);
+
 /* Move an EMPTY cache to another position range: token t of the cache is position
  * pos_base + t from now on (cfg.pos_base at create).  KVQ_EINVAL if the cache holds tokens
  * or pos_base < 0.  Lets a pool reuse fixed-size chunk caches across sequences (paged.py). */

@@ -12,6 +12,17 @@
 #include "../../include/kvq.h"
 #include "kvq_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
+namespace {
+// NVTX range around a public call (SURVEY 5 tracing): visible in Nsight / ncu timelines, a
+// no-op without a tool attached
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 using namespace kvq;
 
 struct kvq_cache {
@@ -405,6 +416,108 @@ kvq_status kvq_sync(kvq_cache *c) {
     return check_sticky(c);
 }
 
+// ---- snapshot / restore (SURVEY 5 checkpoint / resume; SPEC S:535-536 cache dump / load) ----
+// The device state of tokens [0, T): the tile arrays of ceil(T/32) tiles (Key and Value code
+// words, outlier buckets and their counts), the per-token arrays (Value (s, z), CSR records,
+// CSC pointers) and the T_K Key-outlier records; everything else is derived from the create
+// parameters.  Layout: a 16-word header, then the arrays in that order.
+namespace {
+struct SnapHdr {
+    uint32_t magic, version, H_q, H_kv, bits, D, kv, NG, kcap_g, vcap_g, QW, VW;
+    int64_t T, nnzK;
+};
+constexpr uint32_t kSnapMagic = 0x5351564bu;   // "KVQS"
+struct SnapPart { void *dev; size_t bytes; };
+std::vector<SnapPart> snap_parts(kvq_cache *c, int64_t T, int64_t nnzK) {
+    const DevCache &d = c->dc;
+    const size_t nt = (size_t)((T + 31) / 32);
+    return {
+        {d.kcodes, nt * d.QW * 32 * 4},
+        {d.vcodes, nt * 32 * (size_t)d.VW * 4},
+        {d.kit, nt * d.NG * (size_t)d.kcap_g * 4},
+        {d.vit, nt * d.NG * (size_t)d.vcap_g * 4},
+        {d.gcnt, nt * d.NG * 2 * 4},
+        {d.vsz, (size_t)T * sizeof(float2)},
+        {d.vout, (size_t)T * d.kv * 4},
+        {d.kptr, (size_t)(T + 1) * 4},
+        {d.kout, (size_t)nnzK * 4},
+    };
+}
+SnapHdr snap_header(const kvq_cache *c, int64_t T, int64_t nnzK) {
+    const DevCache &d = c->dc;
+    return SnapHdr{kSnapMagic, 1u, (uint32_t)d.H_q, (uint32_t)d.H_kv, (uint32_t)d.bits, (uint32_t)d.D,
+                   (uint32_t)d.kv, (uint32_t)d.NG, (uint32_t)d.kcap_g, (uint32_t)d.vcap_g, (uint32_t)d.QW,
+                   (uint32_t)d.VW, T, nnzK};
+}
+}  // namespace
+
+kvq_status kvq_snapshot_bytes(kvq_cache *c, int64_t *bytes) {
+    if (!c || !bytes) return fail(KVQ_EINVAL, "null argument");
+    kvq_status st = check_sticky(c);
+    if (st != KVQ_OK) return st;
+    CK(cudaSetDevice(c->cfg.device));
+    uint32_t nnz = 0;
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(&nnz, c->dc.kptr + c->T, 4, cudaMemcpyDeviceToHost));
+    size_t b = sizeof(SnapHdr);
+    for (const SnapPart &x : snap_parts(c, c->T, nnz)) b += x.bytes;
+    *bytes = (int64_t)b;
+    return KVQ_OK;
+}
+
+kvq_status kvq_snapshot(kvq_cache *c, void *host, int64_t bytes) {
+    NvtxRange r("kvq_snapshot");
+    if (!c || !host) return fail(KVQ_EINVAL, "null argument");
+    int64_t need = 0;
+    kvq_status st = kvq_snapshot_bytes(c, &need);
+    if (st != KVQ_OK) return st;
+    if (bytes < need) return fail(KVQ_EINVAL, "snapshot needs %lld bytes (got %lld)", (long long)need, (long long)bytes);
+    uint32_t nnz = 0;
+    CK(cudaMemcpy(&nnz, c->dc.kptr + c->T, 4, cudaMemcpyDeviceToHost));
+    const SnapHdr h = snap_header(c, c->T, nnz);
+    char *p = (char *)host;
+    memcpy(p, &h, sizeof h);
+    p += sizeof h;
+    for (const SnapPart &x : snap_parts(c, c->T, nnz)) {
+        if (x.bytes) CK(cudaMemcpy(p, x.dev, x.bytes, cudaMemcpyDeviceToHost));
+        p += x.bytes;
+    }
+    return KVQ_OK;
+}
+
+kvq_status kvq_restore(kvq_cache *c, const void *host, int64_t bytes) {
+    NvtxRange r("kvq_restore");
+    if (!c || !host) return fail(KVQ_EINVAL, "null argument");
+    if (bytes < (int64_t)sizeof(SnapHdr)) return fail(KVQ_EINVAL, "snapshot too short");
+    SnapHdr h;
+    memcpy(&h, host, sizeof h);
+    if (h.magic != kSnapMagic || h.version != 1u) return fail(KVQ_EINVAL, "not a kvq snapshot (magic / version)");
+    const SnapHdr mine = snap_header(c, h.T, h.nnzK);
+    if (memcmp(&h, &mine, offsetof(SnapHdr, T)) != 0)
+        return fail(KVQ_ESHAPE, "snapshot of another cache configuration (heads, bits, D, outliers or buckets differ)");
+    if (h.T < 0 || h.T > c->dc.cap) return fail(KVQ_ECAPACITY, "snapshot holds %lld tokens, capacity %lld",
+                                                (long long)h.T, (long long)c->dc.cap);
+    if (h.nnzK < 0 || h.nnzK > c->dc.kcap) return fail(KVQ_ECAPACITY, "snapshot Key outliers exceed the capacity");
+    size_t need = sizeof h;
+    const std::vector<SnapPart> parts = snap_parts(c, h.T, h.nnzK);
+    for (const SnapPart &x : parts) need += x.bytes;
+    if ((size_t)bytes < need) return fail(KVQ_EINVAL, "snapshot truncated (%lld of %zu bytes)", (long long)bytes, need);
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaDeviceSynchronize());
+    // start from an empty cache (zeroed code words beyond the restored tiles)
+    kvq_status st = kvq_reset(c, nullptr);
+    if (st != KVQ_OK) return st;
+    const char *p = (const char *)host + sizeof h;
+    for (const SnapPart &x : parts) {
+        if (x.bytes) CK(cudaMemcpy(x.dev, p, x.bytes, cudaMemcpyHostToDevice));
+        p += x.bytes;
+    }
+    CK(cudaDeviceSynchronize());
+    c->T = h.T;
+    c->pdl_ok = 0;
+    return KVQ_OK;
+}
+
 kvq_status kvq_set_pos_base(kvq_cache *c, int64_t pos_base) {
     if (!c) return fail(KVQ_EINVAL, "null cache");
     if (c->T != 0) return fail(KVQ_EINVAL, "set_pos_base needs an empty cache (it holds %lld tokens)", (long long)c->T);
@@ -467,10 +580,12 @@ static kvq_status append_tokens(kvq_cache *c, const void *K, const void *V, int6
 }
 
 kvq_status kvq_append(kvq_cache *c, const void *k, const void *v, void *stream) {
+    NvtxRange r("kvq_append");
     return append_tokens(c, k, v, 1, stream);
 }
 
 kvq_status kvq_prefill_quantize(kvq_cache *c, const void *K, const void *V, int64_t T, void *stream) {
+    NvtxRange r("kvq_prefill_quantize");
     return append_tokens(c, K, V, T, stream);
 }
 
@@ -528,10 +643,12 @@ static kvq_status attend_impl(kvq_cache *c, const void *q, int64_t pos, float *o
 }
 
 kvq_status kvq_decode_attend(kvq_cache *c, const void *q, int64_t pos, float *o, void *stream) {
+    NvtxRange r("kvq_decode_attend");
     return attend_impl(c, q, pos, o, 0, stream);
 }
 
 kvq_status kvq_decode_attend_partial(kvq_cache *c, const void *q, int64_t pos, float *part, void *stream) {
+    NvtxRange r("kvq_decode_attend_partial");
     return attend_impl(c, q, pos, part, 1, stream);
 }
 
@@ -593,16 +710,19 @@ static kvq_status attend_batch_impl(kvq_cache *const *caches, int32_t B, const v
 
 kvq_status kvq_decode_attend_batch(kvq_cache *const *caches, int32_t B, const void *const *q, const int64_t *pos,
                                    float *const *o, void *stream) {
+    NvtxRange r("kvq_decode_attend_batch");
     return attend_batch_impl(caches, B, q, pos, o, 0, stream);
 }
 
 kvq_status kvq_decode_attend_batch_partial(kvq_cache *const *caches, int32_t B, const void *const *q,
                                            const int64_t *pos, float *const *part, void *stream) {
+    NvtxRange r("kvq_decode_attend_batch_partial");
     return attend_batch_impl(caches, B, q, pos, part, 1, stream);
 }
 
 kvq_status kvq_merge_partials(const float *parts, int32_t P, int32_t H, int32_t d, float *o,
                               int32_t device, void *stream) {
+    NvtxRange r("kvq_merge_partials");
     if (!parts || !o) return fail(KVQ_EINVAL, "null argument");
     if (P < 1 || H < 1 || d < 1) return fail(KVQ_EINVAL, "P, H_q, d must be >= 1");
     CK(cudaSetDevice(device));

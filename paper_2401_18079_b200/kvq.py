@@ -33,7 +33,8 @@ EXPORTED = ["kvq_cache_create", "kvq_cache_destroy", "kvq_append", "kvq_prefill_
             "kvq_f16_decode_attend", "kvq_f16_export", "kvq_f16_num_tokens",
             "kvq_key_thresholds_online", "kvq_decode_attend_batch", "kvq_layer_sensitivity",
             "kvq_fisher_accumulate", "kvq_assign_bits", "kvq_calibrate_layer",
-            "kvq_decode_attend_batch_partial", "kvq_set_pos_base"]
+            "kvq_decode_attend_batch_partial", "kvq_set_pos_base", "kvq_snapshot_bytes", "kvq_snapshot",
+            "kvq_restore"]
 
 
 class KVQError(RuntimeError):
@@ -111,6 +112,9 @@ def _load() -> ctypes.CDLL:
         "kvq_decode_attend_batch": (i32, [vp, i32, vp, vp, vp, vp]),
         "kvq_decode_attend_batch_partial": (i32, [vp, i32, vp, vp, vp, vp]),
         "kvq_set_pos_base": (i32, [vp, i64]),
+        "kvq_snapshot_bytes": (i32, [vp, ctypes.POINTER(ctypes.c_int64)]),
+        "kvq_snapshot": (i32, [vp, vp, i64]),
+        "kvq_restore": (i32, [vp, vp, i64]),
         "kvq_layer_sensitivity": (i32, [vp, vp, vp, vp, vp, i64, i64, vp, vp]),
         "kvq_fisher_accumulate": (i32, [vp, vp, i64, i32, vp]),
         "kvq_assign_bits": (i32, [vp, i32, i32, i32, i32, vp]),
@@ -240,6 +244,19 @@ class KVQCache:
 
     def reset(self, stream=None):
         _check(_lib.kvq_reset(self._h, _stream(stream)))
+
+    def snapshot(self) -> np.ndarray:
+        """The cache contents as a host byte array (kvq_snapshot; synchronizes)."""
+        n = ctypes.c_int64()
+        _check(_lib.kvq_snapshot_bytes(self._h, ctypes.byref(n)))
+        buf = np.empty(n.value, np.uint8)
+        _check(_lib.kvq_snapshot(self._h, buf.ctypes.data, n.value))
+        return buf
+
+    def restore(self, buf: np.ndarray):
+        """Replace the contents with a snapshot of a cache of the same configuration."""
+        buf = np.ascontiguousarray(buf, np.uint8)
+        _check(_lib.kvq_restore(self._h, buf.ctypes.data, buf.size))
 
     def set_pos_base(self, pos_base: int):
         """Reposition an EMPTY cache (token t -> position pos_base + t), kvq_set_pos_base."""
