@@ -1590,10 +1590,13 @@ __device__ __forceinline__ int kst_swz(int q, int j) {
 __device__ __forceinline__ int kpad(int p) { return p + (p >> 4); }        // 16-byte entries
 __device__ __forceinline__ int apad(int p) { return p + 2 * (p >> 4); }    // 8-byte entries
 
+#ifndef WGT_NW
+#define WGT_NW 16
+#endif
 template <int BITS, bool RESID, int G>
 struct TCfg {
     static_assert(G <= 4 || G == 8, "G <= 4: hi / lo query columns; G = 8: hi and lo B fragments");
-    static constexpr int NWARP = G == 8 ? 12 : NSG;   // G = 8: [8][128] outlier sums per warp
+    static constexpr int NWARP = G == 8 ? 12 : WGT_NW;   // G = 8: [8][128] outlier sums per warp
     static constexpr int NTHR = NWARP * 32;
     static constexpr int IPL = 4;
     static constexpr int NE = 1 << (2 * BITS);
