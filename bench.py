@@ -416,6 +416,13 @@ def run_ours(args):
     # attends stream >= 4 x L2 (C2's 113 MB layer would otherwise stay in the 126 MB L2)
     ncopy = 1 if L_res * bytes_att0 >= 4 * l2 else int(np.ceil(4 * l2 / (L_res * bytes_att0)))
     nc_tot = min(L_res * ncopy, max(L_res, int((free - 8 * 2 ** 30) // max(layer_bytes, 1)) + 1))
+    if world > 1:
+        # every rank must run the same layers per step (one all-gather per layer): the smallest
+        # resident-layer and cache counts over the ranks
+        tt = torch.tensor([L_res, nc_tot], dtype=torch.int64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MIN)
+        L_res, nc_tot = int(tt[0].item()), int(tt[1].item())
+        nc_tot = max(nc_tot, L_res)
     rest = build_caches(kvq, gen, w, cal, nc_tot - 1, n_local, plan.pos_base, cap, dev, 0, rank)
     caches = [c0] + rest
     for c in caches:
