@@ -90,7 +90,7 @@ struct PSmem {
         DW = D / 32; NG = NG_;
         size_t o = 0;
         kmask = o; o += (size_t)32 * DW * 4;
-        vmask = o; o += (size_t)32 * DW * 4;
+        vmask = 0;   // (the Value outlier mask of a token lives in its warp's scratch during A)
         kcnt = o;  o += (size_t)32 * (D / 128) * 2;     // Key outliers per (token, head)
         cntK = o;  o += (size_t)32 * NG * 2;            // per (token, group)
         cntV = o;  o += (size_t)32 * NG * 2;
@@ -99,7 +99,7 @@ struct PSmem {
         o = (o + 15) & ~(size_t)15;
         tinfo = o; o += (size_t)32 * 24 * 2;            // per token: lo, hi, T[15], code lo/hi
         o = (o + 15) & ~(size_t)15;
-        warp = o;  o += (size_t)PW * 64 * 20 * 4;        // per warp: candidates / V staging
+        warp = o;  o += (size_t)PW * 64 * 20 * 4;        // per warp: candidates + mask / V staging
         total = o;
     }
 };
@@ -433,7 +433,7 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
 
 // ------------------------------------------------------------------------------ kernel
 template <int BITS>
-__global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
+__global__ void __launch_bounds__(PT, BITS == 4 ? 2 : 3) prefill_kernel(DevCache c, PParams P) {
     using C = PCfg<BITS>;
     constexpr int NM = C::NM, PS = C::PS, CM = (1 << BITS) - 1, KWH = 4 * BITS;
     extern __shared__ __align__(16) unsigned char sm[];
@@ -441,7 +441,6 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
     const PSmem L(D, NG);
     const int DW = L.DW;
     uint32_t *kmask = reinterpret_cast<uint32_t *>(sm + L.kmask);
-    uint32_t *vmask = reinterpret_cast<uint32_t *>(sm + L.vmask);
     uint16_t *kcnt = reinterpret_cast<uint16_t *>(sm + L.kcnt);
     uint16_t *cntK = reinterpret_cast<uint16_t *>(sm + L.cntK);
     uint16_t *cntV = reinterpret_cast<uint16_t *>(sm + L.cntV);
@@ -463,7 +462,7 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
     };
 
     if (tid == 0) s_tile = atomicAdd(P.ticket, 1u);
-    for (int x = tid; x < 32 * DW; x += PT) { kmask[x] = 0; vmask[x] = 0; }
+    for (int x = tid; x < 32 * DW; x += PT) kmask[x] = 0;
     __syncthreads();
     pmark();
     const int li = (int)s_tile;                       // logical tile of this CTA
@@ -481,10 +480,13 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
     // ====================================================== A: Value selection (warp/token)
     {
         uint32_t *cand = reinterpret_cast<uint32_t *>(wsc);   // [2][CANDMAX]
+        uint32_t *vm = cand + 2 * CANDMAX;                      // [DW] the token's outlier mask
+        static_assert(2 * CANDMAX * 4 + 8192 / 8 <= 64 * 20 * 4, "warp scratch: candidates + mask");
         __shared__ int s_nc[PW][2];
         for (int j = jA + warp; j < jB; j += PW) {
             const __half *row = vrow(j);
-            uint32_t *vm = vmask + j * DW;
+            for (int x = lane; x < DW; x += 32) vm[x] = 0;
+            __syncwarp();
             vtoken_warp<NM>(c, row, D, vm, cand, s_nc[warp], tinfo + j * 24, nt0 + j);
             for (int g = lane; g < NG; g += 32) {
                 int cnt = 0;
@@ -726,7 +728,7 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
     {
         const uint32_t *kenc32 = c.kenc;
         for (int j = jA + warp; j < jB; j += PW) {
-            const __half *kr = krow(j), *vr = vrow(j);
+            const __half *kr = krow(j);
             uint32_t tb = s_kbase + s_tokbase[j];   // CSC slot of the token's next head chunk
             for (int h0 = 0; h0 < H; h0 += 32) {
                 const int h = h0 + lane;
@@ -771,26 +773,35 @@ __global__ void __launch_bounds__(PT, 2) prefill_kernel(DevCache c, PParams P) {
                 }
                 tb += (uint32_t)hsum;
             }
-            // Value items of the token, per group in channel order: a lane per mask word (its
-            // slot = the group's base + the outliers of the group's earlier words)
-            const uint16_t *ti = tinfo + j * 24;
-            const uint32_t khi = okey(ti[TI_HI]);
-            const int wpg = GW / 32;
-            for (int x = lane; x < DW; x += 32) {
-                const uint32_t bits = vmask[j * DW + x];
-                if (!bits) continue;
-                const int g = x / wpg;
-                uint32_t bslot = s_gbase[g][1] + posV[j * NG + g];
-                for (int x2 = g * wpg; x2 < x; ++x2) bslot += __popc(vmask[j * DW + x2]);
-                uint32_t *dst = c.vit + (tile * NG + g) * (int64_t)c.vcap_g;
-                for (uint32_t b = bits; b; b &= b - 1) {
-                    const int ch = 32 * x + __ffs(b) - 1;
-                    const uint32_t xh = __half_as_ushort(vr[ch]);
-                    const int code = okey(xh) >= khi ? ti[TI_CHI] : ti[TI_CLO];
-                    if (bslot < (uint32_t)c.vcap_g)
-                        dst[bslot] = (xh << 16) | ((uint32_t)j << 11) | item_code_flag<BITS>(code) |
-                                     (uint32_t)(ch - g * GW);
-                    ++bslot;
+            // Value items of the token from its CSR row (phase A: k records in ascending channel
+            // order), a lane per record: slot = the group's base + the record's rank in its group
+            // (its index minus the token's outliers in earlier groups: a scan of cntV)
+            const int kv = c.kv;
+            if (kv > 0) {
+                const uint16_t *ti = tinfo + j * 24;
+                const uint32_t khi = okey(ti[TI_HI]);
+                const int c0 = lane < NG ? cntV[j * NG + lane] : 0, c1 = lane + 32 < NG ? cntV[j * NG + 32 + lane] : 0;
+                int s0 = c0, s1 = c1;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y0 = __shfl_up_sync(0xffffffffu, s0, o), y1 = __shfl_up_sync(0xffffffffu, s1, o);
+                    if (lane >= o) { s0 += y0; s1 += y1; }
+                }
+                const int e0 = s0 - c0, e1 = s1 - c1 + __shfl_sync(0xffffffffu, s0, 31);
+                const uint32_t *vo = c.vout + (nt0 + j) * (int64_t)kv;
+                for (int eb = 0; eb < kv; eb += 32) {
+                    const int e = eb + lane;
+                    const uint32_t rec = e < kv ? vo[e] : 0u;
+                    const int ch = (int)(rec & 0xffffu), g = ch / GW;
+                    const int st0 = __shfl_sync(0xffffffffu, e0, g & 31), st1 = __shfl_sync(0xffffffffu, e1, g & 31);
+                    if (e < kv) {
+                        const uint32_t bslot = s_gbase[g][1] + posV[j * NG + g] + (uint32_t)(e - (g < 32 ? st0 : st1));
+                        const uint32_t xh = rec >> 16;
+                        const int code = okey(xh) >= khi ? ti[TI_CHI] : ti[TI_CLO];
+                        if (bslot < (uint32_t)c.vcap_g)
+                            (c.vit + (tile * NG + g) * (int64_t)c.vcap_g)[bslot] =
+                                (xh << 16) | ((uint32_t)j << 11) | item_code_flag<BITS>(code) | (uint32_t)(ch - g * GW);
+                    }
                 }
             }
         }

@@ -9,8 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from kvq_synth import CONFIGS, calib, gen  # noqa: E402
 from paper_2401_18079_b200 import kvq  # noqa: E402
 
-w = CONFIGS["c3_nuq3"]
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+w = CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "c3_nuq3"]
 dev = torch.device("cuda", 0)
 cal = calib.calibrate_layer(gen.gen_keys(0, 0, 2048, w.D, stream=gen.STREAM_CAL_K),
                             gen.gen_values(0, 0, 2048, w.D, stream=gen.STREAM_CAL_V), w.bits, w.ppm)
