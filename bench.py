@@ -773,7 +773,9 @@ def run_ours(args):
             "compare": compare, "resid_codebook": resid, "batched_decode": batch,
             "online_key_thresholds": online, "offline_calibration": calib_out, "sensitivity": sens,
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * L_res * (2 if world == 1 else 3),
+            # all ranks: append (tail rank) + attend per layer at N = 1; at N > 1 every rank's
+            # attend_partial + merge and the tail rank's append (NCCL's all-gather not counted)
+            "gpu_launches": args.steps * L_res * (2 if world == 1 else 2 * world + 1),
             "clocks": clocks.summary(),
             "key_outliers_per_token": nnz_mean / max(Tc, 1),
             # effective: step time minus the attend-only time (the attend launched right after
