@@ -89,7 +89,42 @@ class Clocks:
         self._stop = threading.Event()
         self._thr = None
 
+    def _nvml(self):
+        """NVML handle of the CUDA device (matched by PCI bus id), or None."""
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(self.device)
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                pci = pynvml.nvmlDeviceGetPciInfo(h)
+                if (pci.domain, pci.bus, pci.device) == (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id):
+                    return pynvml, h
+            return None
+        except Exception as e:   # no NVML: the nvidia-smi sampler below
+            print(f"clocks: NVML unavailable ({e!r}), sampling with nvidia-smi", file=sys.stderr)
+            return None
+
     def _run(self):
+        # NVML in-process (a sample every ~10 ms, so even a short timed region is covered),
+        # else nvidia-smi (~0.1-0.2 s per sample)
+        nv = self._nv
+        if nv is not None:
+            pynvml, h = nv
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = [0x8, 0x40, 0x20, 0x4]   # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = get_reasons(h)
+                    self.samples.append([str(sm), str(mx), ""] + ["Active" if r & b else "Not Active" for b in bits])
+                except Exception:
+                    pass
+                self._stop.wait(0.01)
+            return
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -105,6 +140,8 @@ class Clocks:
             self._stop.wait(0.2)
 
     def __enter__(self):
+        if not hasattr(self, "_nv"):
+            self._nv = self._nvml()   # before the timed region: nvmlInit takes ~0.1 s
         self._thr = threading.Thread(target=self._run, daemon=True)
         self._thr.start()
         return self
@@ -123,7 +160,7 @@ class Clocks:
                           if len(s) > 3 + i and s[3 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "sampler": "nvml" if getattr(self, "_nv", None) else "nvidia-smi"}
 
 
 def measured_peaks():
