@@ -324,18 +324,18 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
         gk[1] = have1 ? okey(h2u(__hmax2(mx1, __lowhigh2highlow(mx1)))) : 0u;
         gl[0] = have0 ? 0xffffu - okey(h2u(__hmin2(mn0, __lowhigh2highlow(mn0)))) : 0u;
         gl[1] = have1 ? 0xffffu - okey(h2u(__hmin2(mn1, __lowhigh2highlow(mn1)))) : 0u;
-        auto kth = [&](const uint32_t (&v)[2], int need) {
-            uint32_t t = 0;
-            for (int b = 15; b >= 0; --b) {
-                const uint32_t t2 = t | (1u << b);
-                const int n = __popc(__ballot_sync(0xffffffffu, v[0] >= t2)) + __popc(__ballot_sync(0xffffffffu, v[1] >= t2));
-                if (n >= need) t = t2;
-            }
-            return t;
-        };
         vstamp(8);
-        const uint32_t tau_hi = kth(gk, ku + 1);                // order key
-        const uint32_t tau_lo = 0xffffu - kth(gl, kl + 1);      // order key
+        // both searches in one loop (two independent ballot chains in flight)
+        uint32_t t_hi = 0, t_lo = 0;
+        for (int b = 15; b >= 0; --b) {
+            const uint32_t a2 = t_hi | (1u << b), b2 = t_lo | (1u << b);
+            const int na = __popc(__ballot_sync(0xffffffffu, gk[0] >= a2)) + __popc(__ballot_sync(0xffffffffu, gk[1] >= a2));
+            const int nb = __popc(__ballot_sync(0xffffffffu, gl[0] >= b2)) + __popc(__ballot_sync(0xffffffffu, gl[1] >= b2));
+            if (na >= ku + 1) t_hi = a2;
+            if (nb >= kl + 1) t_lo = b2;
+        }
+        const uint32_t tau_hi = t_hi;              // order key: (ku+1)-th largest group max
+        const uint32_t tau_lo = 0xffffu - t_lo;    // order key: (kl+1)-th smallest group min
         vstamp(9);
         // candidates: value >= tau_hi (upper), value <= tau_lo (lower)
         if (lane < 2) nc2[lane] = 0;
@@ -363,11 +363,13 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
                 const __half2 a = __hmax2(__hmax2(u2h(u.x), u2h(u.y)), __hmax2(u2h(u.z), u2h(u.w)));
                 const __half2 b = __hmin2(__hmin2(u2h(u.x), u2h(u.y)), __hmin2(u2h(u.z), u2h(u.w)));
                 if (__hbge2(__hmax2(a, __lowhigh2highlow(a)), th2) || __hble2(__hmin2(b, __lowhigh2highlow(b)), tl2)) {
+                    // a true half compares to 1.0 (0x3c00: bits 10-13); word e2 keeps bit 10 + e2
+                    // of each half: element 2 e2 -> flag bit 10 + e2, 2 e2 + 1 -> 26 + e2
 #pragma unroll
                     for (int e2 = 0; e2 < 4; ++e2) {
-                        const uint32_t ge = h2u(__hge2(u2h(w[e2]), th2)), le = h2u(__hle2(u2h(w[e2]), tl2));
-                        fu |= (((ge >> 13) & 1u) | ((ge >> 28) & 2u)) << (2 * e2);
-                        fl |= (((le >> 13) & 1u) | ((le >> 28) & 2u)) << (2 * e2);
+                        const uint32_t sel = 0x04000400u << e2;
+                        fu |= h2u(__hge2(u2h(w[e2]), th2)) & sel;
+                        fl |= h2u(__hle2(u2h(w[e2]), tl2)) & sel;
                     }
                 }
             }
@@ -378,13 +380,13 @@ __device__ void vtoken_warp(const DevCache &c, const __half *row, int D, uint32_
                 if (nl) bl = atomicAdd(&nc2[1], nl);
                 if (fu | fl) {
                     for (uint32_t x = fu; x; x &= x - 1) {
-                        const int e = __ffs(x) - 1;
+                        const int b = __ffs(x) - 1, e = b < 16 ? 2 * (b - 10) : 2 * (b - 26) + 1;
                         const uint32_t key = okey(half_at(u, e));
                         if (bu < CANDMAX) cand[bu] = (key << 13) | (8191u - (uint32_t)(c0 + e));
                         ++bu;
                     }
                     for (uint32_t x = fl; x; x &= x - 1) {
-                        const int e = __ffs(x) - 1;
+                        const int b = __ffs(x) - 1, e = b < 16 ? 2 * (b - 10) : 2 * (b - 26) + 1;
                         const uint32_t key = okey(half_at(u, e));
                         if (bl < CANDMAX) cand[CANDMAX + bl] = ((0xffffu - key) << 13) | (8191u - (uint32_t)(c0 + e));
                         ++bl;
