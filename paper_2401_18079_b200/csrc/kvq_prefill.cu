@@ -501,6 +501,96 @@ __global__ void __launch_bounds__(PT, BITS == 4 ? 2 : 3) prefill_kernel(DevCache
 
     __syncthreads();   // per-token ENC thresholds of phase A
     pmark();
+    // ============================================================ B: Keys (warp/KV head)
+    {
+        const uint4 *kenc = reinterpret_cast<const uint4 *>(c.kenc);
+        const int j = lane;
+        const bool valid = j >= jA && j < jB;
+        const __half *row = valid ? krow(j) : nullptr;
+        for (int h = warp; h < H; h += PW) {
+            uint32_t kw[KWH];
+#pragma unroll
+            for (int w = 0; w < KWH; ++w) kw[w] = 0u;
+            uint32_t mw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {   // channels 8a..8a+7 and 64+8a..64+8a+7 of the head
+                uint4 u0 = make_uint4(0, 0, 0, 0), u1 = make_uint4(0, 0, 0, 0);
+                if (valid) {
+                    u0 = *reinterpret_cast<const uint4 *>(row + h * kHeadDim + 8 * a);
+                    u1 = *reinterpret_cast<const uint4 *>(row + h * kHeadDim + 64 + 8 * a);
+                }
+                const uint32_t w0[4] = {u0.x, u0.y, u0.z, u0.w}, w1[4] = {u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int p = 8 * a + e;   // RoPE pair (p, p + 64)
+                    const uint32_t x2 = __byte_perm(w0[e >> 1], w1[e >> 1], (e & 1) ? 0x7632 : 0x5410);
+                    const uint4 *te = kenc + ((size_t)(h * kPairs + p) * PS) / 4;
+                    uint32_t tw[PS];
+#pragma unroll
+                    for (int q = 0; q < PS / 4; ++q) {
+                        const uint4 t4 = __ldg(te + q);
+                        tw[4 * q] = t4.x; tw[4 * q + 1] = t4.y; tw[4 * q + 2] = t4.z; tw[4 * q + 3] = t4.w;
+                    }
+                    const __half2 x = u2h(x2);
+                    const __half2 olo = __hlt2(x, u2h(tw[0])), ohi = __hgt2(x, u2h(tw[1]));
+                    __half2 cnt = __hge2(x, u2h(tw[4]));
+#pragma unroll
+                    for (int q = 1; q < NM; ++q) cnt = __hadd2(cnt, __hge2(x, u2h(tw[4 + q])));
+                    cnt = __hfma2(olo, __hsub2(u2h(tw[2]), cnt), cnt);
+                    cnt = __hfma2(ohi, __hsub2(u2h(tw[3]), cnt), cnt);
+                    const uint32_t pc = h2codes(cnt, BITS);
+                    const int bit = 2 * BITS * p, wi = bit >> 5, sh = bit & 31;
+                    kw[wi] |= pc << sh;
+                    if (sh + 2 * BITS > 32) kw[wi + 1] |= pc >> (32 - sh);
+                    const uint32_t ob = h2u(__hadd2(olo, ohi));
+                    mw[p >> 5] |= ((ob >> 13) & 1u) << (p & 31);
+                    mw[2 + (p >> 5)] |= ((ob >> 29) & 1u) << (p & 31);
+                }
+            }
+            if (valid) {
+#pragma unroll
+                for (int w = 0; w < KWH; ++w) c.kcodes[(tile * c.QW + h * KWH + w) * 32 + j] = kw[w];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) kmask[j * DW + h * 4 + w] = mw[w];
+            }
+            kcnt[j * H + h] = (uint16_t)(valid ? __popc(mw[0]) + __popc(mw[1]) + __popc(mw[2]) + __popc(mw[3]) : 0);
+        }
+    }
+    __syncthreads();
+    pmark();
+
+    // ================================ D1: Key-outlier totals, look-back aggregate, counts
+    uint32_t lb_tot = 0, lb_agg = 0;   // warp 0: this lane's token total, the tile aggregate
+    if (warp == 0) {
+        int tot = 0;
+        for (int h = 0; h < H; ++h) tot += kcnt[lane * H + h];
+        int ex = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, ex, o);
+            if (lane >= o) ex += y;
+        }
+        lb_agg = (uint32_t)__shfl_sync(0xffffffffu, ex, 31);
+        lb_tot = (uint32_t)tot;
+        s_tokbase[lane] = (uint32_t)(ex - tot);
+        // publish the aggregate now (decoupled look-back: word = flag << 32 | value); the
+        // predecessors are resolved after phase C (next), when they have most likely published
+        if (lane == 0) {
+            if (li == 0) {
+                s_kbase = c.kptr[nA];   // CSC offset of the chunk's first token (prior appends)
+                atomicExch(&P.lb[0], ((unsigned long long)LB_INC << 32) | (s_kbase + lb_agg));
+            } else {
+                atomicExch(&P.lb[li], ((unsigned long long)LB_AGG << 32) | lb_agg);
+            }
+        }
+    } else if (warp == 1) {
+        // per (token, group) Key-outlier counts
+        for (int g = 0; g < NG; ++g) {
+            int cnt = 0;
+            for (int h = g * (GW / kHeadDim); h < (g + 1) * (GW / kHeadDim); ++h) cnt += kcnt[lane * H + h];
+            cntK[lane * NG + g] = (uint16_t)cnt;
+        }
+    }
     // ================================================ C: Value codes (warp/KV head, mma lanes)
     {
         // staging: the head's V slice for 64 channels, transposed [channel][token] fp16,
@@ -577,96 +667,6 @@ __global__ void __launch_bounds__(PT, BITS == 4 ? 2 : 3) prefill_kernel(DevCache
             }
         }
     }
-    // ============================================================ B: Keys (warp/KV head)
-    {
-        const uint4 *kenc = reinterpret_cast<const uint4 *>(c.kenc);
-        const int j = lane;
-        const bool valid = j >= jA && j < jB;
-        const __half *row = valid ? krow(j) : nullptr;
-        for (int h = warp; h < H; h += PW) {
-            uint32_t kw[KWH];
-#pragma unroll
-            for (int w = 0; w < KWH; ++w) kw[w] = 0u;
-            uint32_t mw[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-            for (int a = 0; a < 8; ++a) {   // channels 8a..8a+7 and 64+8a..64+8a+7 of the head
-                uint4 u0 = make_uint4(0, 0, 0, 0), u1 = make_uint4(0, 0, 0, 0);
-                if (valid) {
-                    u0 = *reinterpret_cast<const uint4 *>(row + h * kHeadDim + 8 * a);
-                    u1 = *reinterpret_cast<const uint4 *>(row + h * kHeadDim + 64 + 8 * a);
-                }
-                const uint32_t w0[4] = {u0.x, u0.y, u0.z, u0.w}, w1[4] = {u1.x, u1.y, u1.z, u1.w};
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int p = 8 * a + e;   // RoPE pair (p, p + 64)
-                    const uint32_t x2 = __byte_perm(w0[e >> 1], w1[e >> 1], (e & 1) ? 0x7632 : 0x5410);
-                    const uint4 *te = kenc + ((size_t)(h * kPairs + p) * PS) / 4;
-                    uint32_t tw[PS];
-#pragma unroll
-                    for (int q = 0; q < PS / 4; ++q) {
-                        const uint4 t4 = __ldg(te + q);
-                        tw[4 * q] = t4.x; tw[4 * q + 1] = t4.y; tw[4 * q + 2] = t4.z; tw[4 * q + 3] = t4.w;
-                    }
-                    const __half2 x = u2h(x2);
-                    const __half2 olo = __hlt2(x, u2h(tw[0])), ohi = __hgt2(x, u2h(tw[1]));
-                    __half2 cnt = __hge2(x, u2h(tw[4]));
-#pragma unroll
-                    for (int q = 1; q < NM; ++q) cnt = __hadd2(cnt, __hge2(x, u2h(tw[4 + q])));
-                    cnt = __hfma2(olo, __hsub2(u2h(tw[2]), cnt), cnt);
-                    cnt = __hfma2(ohi, __hsub2(u2h(tw[3]), cnt), cnt);
-                    const uint32_t pc = h2codes(cnt, BITS);
-                    const int bit = 2 * BITS * p, wi = bit >> 5, sh = bit & 31;
-                    kw[wi] |= pc << sh;
-                    if (sh + 2 * BITS > 32) kw[wi + 1] |= pc >> (32 - sh);
-                    const uint32_t ob = h2u(__hadd2(olo, ohi));
-                    mw[p >> 5] |= ((ob >> 13) & 1u) << (p & 31);
-                    mw[2 + (p >> 5)] |= ((ob >> 29) & 1u) << (p & 31);
-                }
-            }
-            if (valid) {
-#pragma unroll
-                for (int w = 0; w < KWH; ++w) c.kcodes[(tile * c.QW + h * KWH + w) * 32 + j] = kw[w];
-#pragma unroll
-                for (int w = 0; w < 4; ++w) kmask[j * DW + h * 4 + w] = mw[w];
-            }
-            kcnt[j * H + h] = (uint16_t)(valid ? __popc(mw[0]) + __popc(mw[1]) + __popc(mw[2]) + __popc(mw[3]) : 0);
-        }
-    }
-    __syncthreads();
-    pmark();
-
-    // ================================ D1: Key-outlier totals, look-back aggregate, counts
-    uint32_t lb_tot = 0, lb_agg = 0;   // warp 0: this lane's token total, the tile aggregate
-    if (warp == 0) {
-        int tot = 0;
-        for (int h = 0; h < H; ++h) tot += kcnt[lane * H + h];
-        int ex = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, ex, o);
-            if (lane >= o) ex += y;
-        }
-        lb_agg = (uint32_t)__shfl_sync(0xffffffffu, ex, 31);
-        lb_tot = (uint32_t)tot;
-        s_tokbase[lane] = (uint32_t)(ex - tot);
-        // publish the aggregate now (decoupled look-back: word = flag << 32 | value); the
-        // predecessors are resolved after phase C, when they have most likely published
-        if (lane == 0) {
-            if (li == 0) {
-                s_kbase = c.kptr[nA];   // CSC offset of the chunk's first token (prior appends)
-                atomicExch(&P.lb[0], ((unsigned long long)LB_INC << 32) | (s_kbase + lb_agg));
-            } else {
-                atomicExch(&P.lb[li], ((unsigned long long)LB_AGG << 32) | lb_agg);
-            }
-        }
-    } else if (warp == 1) {
-        // per (token, group) Key-outlier counts
-        for (int g = 0; g < NG; ++g) {
-            int cnt = 0;
-            for (int h = g * (GW / kHeadDim); h < (g + 1) * (GW / kHeadDim); ++h) cnt += kcnt[lane * H + h];
-            cntK[lane * NG + g] = (uint16_t)cnt;
-        }
-    }
     __syncthreads();
     pmark();
 
@@ -684,7 +684,10 @@ __global__ void __launch_bounds__(PT, BITS == 4 ? 2 : 3) prefill_kernel(DevCache
                 const unsigned notready = __ballot_sync(0xffffffffu, fl == 0u);
                 const int first = inc ? __ffs(inc) - 1 : 32;
                 const unsigned need = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
-                if (notready & need) continue;   // a predecessor in the window has not published
+                if (notready & need) {   // a predecessor in the window has not published: back off
+                    __nanosleep(128);      // (frees issue slots for the SM's other CTAs)
+                    continue;
+                }
                 uint32_t val = (lane <= first) ? (uint32_t)v : 0u;
 #pragma unroll
                 for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);

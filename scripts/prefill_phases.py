@@ -29,7 +29,7 @@ lib.kvq_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
 buf = np.zeros(72, np.uint64)
 lib.kvq_debug_trace(c.handle, buf.ctypes.data, 72)
 ph = buf[64:70].astype(np.float64)
-names = ["init", "A: V select", "C+B: V codes, Keys", "D1", "D1b", "D2"]
+names = ["init", "A: V select", "B: Keys", "D1 + C: V codes", "D1b", "D2"]
 tot = ph.sum()
 for n_, v in zip(names, ph):
     print(f"  {n_:22s} {100 * v / tot:5.1f}%   {v / (T / 32) / 1.9e3:8.1f} us per CTA-tile")
