@@ -25,14 +25,17 @@
 //      above it (typically ~40 of 4096) are ranked exactly by (value, index); same for the
 //      lower tail.  A bit-by-bit exact selection over all elements handles inputs where the
 //      bound admits too many candidates (ties, tiny D).  Writes (s, z), the CSR records
-//      and the token's Value-outlier bitmask.
+//      and the token's per-group outlier counts (its bitmask lives in the warp's scratch).
 //   B  Keys, warp per KV head, lane = token: pair codes packed straight into the tile's
 //      pair-stream words (coalesced 128-byte stores), outlier bitmask per (token, head).
 //   C  Value codes, warp per KV head, lane = mma A-fragment lane: the head's V slice staged
 //      transposed in shared memory, each field = one token pair of one channel.
 //   D  Key CSC offsets by a decoupled look-back over the tiles of the launch (each CTA takes
 //      its tile from a ticket, so every predecessor has started), CSC records, and the
-//      outlier items of the (tile, head group) buckets in (token, channel) order.
+//      outlier items of the (tile, head group) buckets in (token, channel) order (Value
+//      items from the tokens' CSR rows).
+// Order in the kernel: A, B, publish the tile's Key-outlier aggregate, C, resolve the
+// look-back (so the wait for the predecessors overlaps C), D.
 #include "kvq_internal.cuh"
 
 namespace kvq {
