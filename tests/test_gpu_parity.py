@@ -150,7 +150,10 @@ def test_pinned_host_output_is_stream_ordered(kvq):
                                              # G = 8 (LLaMA-2-70B 64/8): two 4-head CTAs per KV head
                                              (16, 2, 3, 300), (64, 8, 3, 257), (16, 2, 2, 200),
                                              # 4-bit GQA (Mistral-7B nuq4): the tensor-core GQA kernel
-                                             (8, 2, 4, 300), (32, 8, 4, 257), (16, 2, 4, 200), (8, 4, 4, 150)])
+                                             (8, 2, 4, 300), (32, 8, 4, 257), (16, 2, 4, 200), (8, 4, 4, 150),
+                                             # 40 KV heads of a GQA layer: 40 head groups (> 32: the
+                                             # second half of the prefill's per-group scans)
+                                             (80, 40, 3, 100), (80, 40, 2, 70)])
 def test_attend_matches_oracle(kvq, H_q, H_kv, bits, T):
     ppm = 10_000
     cal, K, V = setup_layer(4, 0, H_q, H_kv, bits, ppm, T)
