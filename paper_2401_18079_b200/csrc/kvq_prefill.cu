@@ -596,9 +596,7 @@ __global__ void __launch_bounds__(PT, BITS == 4 ? 2 : 3) prefill_kernel(DevCache
     }
     // ================================================ C: Value codes (warp/KV head, mma lanes)
     {
-        // staging: the head's V slice for 64 channels, transposed [channel][token] fp16,
-        // row stride 20 words (conflict-free for the fragment reads)
-        uint32_t *vs = reinterpret_cast<uint32_t *>(wsc);
+        // staging (warp scratch): the head's V slice for 64 channels, [token][channel] fp16
         const int vg = lane >> 2, vt = lane & 3;
         // per lane: its 4 token pairs (2u, 2u+1), u = vt + 4 * (2 s + r2), r2 = (j % 16) / 8
         __half2 T2[4][NM], lo2[4], hi2[4];
@@ -622,19 +620,16 @@ __global__ void __launch_bounds__(PT, BITS == 4 ? 2 : 3) prefill_kernel(DevCache
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 __syncwarp();
-                // stage channels 64*half .. +63 of head h: lane = token
+                // stage channels 64*half .. +63 of head h row-major: lane = token, row stride
+                // 144 bytes (16-byte stores and ldmatrix row reads hit 8 distinct bank quads)
                 {
                     const int j = lane;
                     const bool valid = j >= jA && j < jB;
-                    uint16_t *vs16 = reinterpret_cast<uint16_t *>(vs);
 #pragma unroll
                     for (int a = 0; a < 8; ++a) {
                         uint4 u = make_uint4(0, 0, 0, 0);
                         if (valid) u = *reinterpret_cast<const uint4 *>(vrow(j) + h * kHeadDim + 64 * half + 8 * a);
-                        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            vs16[(8 * a + e) * 40 + j] = (uint16_t)(e & 1 ? w[e >> 1] >> 16 : w[e >> 1]);
+                        *reinterpret_cast<uint4 *>(wsc + j * 144 + 16 * a) = u;
                     }
                 }
                 __syncwarp();
@@ -642,14 +637,23 @@ __global__ void __launch_bounds__(PT, BITS == 4 ? 2 : 3) prefill_kernel(DevCache
                 for (int mt2 = 0; mt2 < 4; ++mt2) {
                     const int mt = 4 * half + mt2;
 #pragma unroll
-                    for (int s2 = 0; s2 < 2; ++s2)
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        // the 4 fields r of (mt2, s2) with one ldmatrix.x4.trans: matrix r = tokens
+                        // 8 (2 s2 + r / 2) .. +7 x channels 16 mt2 + 8 (r % 2) .. +7; transposed, lane
+                        // (g, t) receives tokens 2t, 2t+1 of the block at channel g (one half2)
+                        uint32_t xr[4];
+                        {
+                            const int m = lane >> 3, tok = 8 * (2 * s2 + (m >> 1)) + (lane & 7);
+                            const uint32_t ad = (uint32_t)__cvta_generic_to_shared(wsc + tok * 144 + 2 * (16 * mt2 + 8 * (m & 1)));
+                            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(xr[0]), "=r"(xr[1]), "=r"(xr[2]), "=r"(xr[3]) : "r"(ad));
+                        }
 #pragma unroll
                         for (int r = 0; r < 4; ++r) {
                             // field f = (2 mt + s2) * 4 + r: channel 16 mt + g + 8 (r % 2),
                             // tokens 16 s2 + 2 vt + 8 (r / 2) (+1)
-                            const int cl = 16 * mt2 + vg + 8 * (r & 1);   // channel within the staged 64
                             const int pr = 2 * s2 + (r >> 1);
-                            const uint32_t x2 = vs[cl * 20 + (2 * vt + 8 * pr) / 2];
+                            const uint32_t x2 = xr[r];
                             __half2 x = __hmax2(__hmin2(u2h(x2), hi2[pr]), lo2[pr]);
                             __half2 cnt = __hge2(x, T2[pr][0]);
 #pragma unroll
@@ -660,6 +664,7 @@ __global__ void __launch_bounds__(PT, BITS == 4 ? 2 : 3) prefill_kernel(DevCache
                             vw[wi] |= fv << sh;
                             if (sh + 2 * BITS > 32) vw[wi + 1] |= fv >> (32 - sh);
                         }
+                    }
                 }
             }
             // a tile a chunk starts inside already holds codes of appended tokens: OR them in
